@@ -1,0 +1,429 @@
+"""B200-native compressed NMF (FastHALS-RP) -- Python mirror of the reference API.
+
+The product is the C-ABI library ``lib/libcnmf_b200.so`` (include/cnmf_b200.h):
+CUDA kernels for sm_100a plus a C++ host.  This module binds it with ctypes
+and mirrors the reference's interface for this path
+(/root/reference/proj/include/cnmf/solvers.hpp, compression.hpp, metrics.hpp):
+
+  SolverConfig, SketchConfig   <- cnmf::SolverConfig / SketchConfig
+  run(x, config) -> RunResult  <- cnmf::run (solvers.hpp:104)
+  ConfigError / DimensionError / InputError  <- errors.hpp:10-28
+
+plus the step-level entry points (build_projectors, compress, ...) used by the
+parity tests.  There is no CPU fallback: without the CUDA library or a GPU,
+every compute call raises CudaError.
+"""
+from __future__ import annotations
+
+import ctypes as C
+import os
+import subprocess
+from dataclasses import dataclass, field
+from typing import List, Optional
+
+import numpy as np
+
+HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(HERE, "lib", "libcnmf_b200.so")
+HEADER = os.path.join(os.path.dirname(HERE), "include", "cnmf_b200.h")
+
+# cnmf::Algorithm (algorithm.hpp:8-15)
+MU, MU_RP, HALS, HALS_RP, FASTHALS, FASTHALS_RP = range(6)
+ALGORITHM_NAMES = {"mu": MU, "mu-rp": MU_RP, "hals": HALS, "hals-rp": HALS_RP,
+                   "fasthals": FASTHALS, "fasthals-rp": FASTHALS_RP}
+# cnmf::RunStatus (metrics.hpp:62-66)
+CONVERGED, REACHED_MAX_ITERATIONS, ABORTED = range(3)
+STATUS_NAMES = {CONVERGED: "converged", REACHED_MAX_ITERATIONS: "reached_max_iterations",
+                ABORTED: "aborted"}
+
+
+class CnmfError(Exception):
+    pass
+
+
+class ConfigError(CnmfError, ValueError):
+    """cnmf::ConfigError (std::invalid_argument)."""
+
+
+class DimensionError(CnmfError, ValueError):
+    """cnmf::DimensionError (std::invalid_argument)."""
+
+
+class InputError(CnmfError, ValueError):
+    """cnmf::InputError (std::invalid_argument)."""
+
+
+class CudaError(CnmfError, RuntimeError):
+    """Device failure or no usable CUDA device (the product never falls back to the CPU)."""
+
+
+class NcclError(CnmfError, RuntimeError):
+    pass
+
+
+class UnsupportedError(CnmfError, NotImplementedError):
+    """Valid for the reference, outside this build's hot path."""
+
+
+_ERRORS = {1: ConfigError, 2: DimensionError, 3: InputError, 4: CudaError, 5: NcclError,
+           6: UnsupportedError}
+
+
+class _Config(C.Structure):
+    _fields_ = [("algorithm", C.c_int32), ("k", C.c_uint64), ("sketch_q", C.c_uint64),
+                ("sketch_power_iterations", C.c_uint64), ("sketch_seed", C.c_uint64),
+                ("alpha", C.c_double), ("beta", C.c_double), ("max_iterations", C.c_uint64),
+                ("rel_tolerance", C.c_double), ("error_interval", C.c_uint64),
+                ("seed", C.c_uint64), ("normalize_a", C.c_int32)]
+
+
+class _Record(C.Structure):
+    _fields_ = [("iteration", C.c_uint64), ("error", C.c_double),
+                ("elapsed_seconds", C.c_double)]
+
+
+class _Trace(C.Structure):
+    _fields_ = [("records", C.POINTER(_Record)), ("records_capacity", C.c_uint64),
+                ("records_count", C.c_uint64), ("update_seconds", C.c_double),
+                ("compress_seconds", C.c_double), ("error_seconds", C.c_double),
+                ("gini_b", C.c_double), ("status", C.c_int32), ("iterations_run", C.c_uint64),
+                ("power_iterations", C.c_uint64), ("alpha", C.c_double), ("beta", C.c_double),
+                ("seed", C.c_uint64), ("estimate_flops_per_iteration", C.c_double),
+                ("estimate_memory_floats", C.c_double), ("x_norm_sq", C.c_double),
+                ("redraws", C.c_uint64), ("x_passes", C.c_uint64), ("message", C.c_char * 256)]
+
+
+# Every exported symbol of include/cnmf_b200.h (checked by tests/test_abi.py).
+EXPORTS = [
+    "cnmf_abi_version", "cnmf_context_create", "cnmf_context_destroy",
+    "cnmf_context_last_error", "cnmf_context_stream", "cnmf_solver_config_init",
+    "cnmf_solver_config_validate", "cnmf_run", "cnmf_run_device", "cnmf_gaussian_sketch",
+    "cnmf_initialize", "cnmf_powered_range_finder", "cnmf_build_projectors", "cnmf_compress",
+    "cnmf_compress_factors", "cnmf_fasthals_rp_steps", "cnmf_reconstruction_error",
+    "cnmf_thin_qr", "cnmf_xs_nn", "cnmf_xs_tn", "cnmf_synth_x",
+]
+
+
+def build(force: bool = False) -> str:
+    """Compile lib/libcnmf_b200.so for sm_100a (nvcc, no GPU needed)."""
+    cmd = ["make", "-s", "-C", os.path.join(HERE, "csrc")]
+    if force:
+        subprocess.run(cmd + ["clean"], check=True)
+    subprocess.run(cmd + ["-j8"], check=True)
+    return LIB_PATH
+
+
+_lib = None
+
+
+def load_library(path: str = LIB_PATH):
+    """Load the C-ABI library; raises CudaError when it is missing."""
+    global _lib
+    if _lib is not None:
+        return _lib
+    if not os.path.exists(path):
+        raise CudaError(f"{path} is missing: build it with paper_1712_02248_b200.build()")
+    L = C.CDLL(path)
+    u64, vp, dp, fp = C.c_uint64, C.c_void_p, C.POINTER(C.c_double), C.c_void_p
+    L.cnmf_abi_version.restype = C.c_int
+    L.cnmf_context_create.argtypes = [C.c_int, C.POINTER(vp)]
+    L.cnmf_context_destroy.argtypes = [vp]
+    L.cnmf_context_destroy.restype = None
+    L.cnmf_context_last_error.argtypes = [vp]
+    L.cnmf_context_last_error.restype = C.c_char_p
+    L.cnmf_context_stream.argtypes = [vp]
+    L.cnmf_context_stream.restype = vp
+    L.cnmf_solver_config_init.argtypes = [C.POINTER(_Config)]
+    L.cnmf_solver_config_init.restype = None
+    L.cnmf_solver_config_validate.argtypes = [C.POINTER(_Config), u64, u64, C.c_char_p,
+                                              C.c_size_t]
+    L.cnmf_run.argtypes = [vp, fp, u64, u64, u64, C.POINTER(_Config), fp, fp, C.POINTER(_Trace)]
+    L.cnmf_run_device.argtypes = L.cnmf_run.argtypes
+    L.cnmf_gaussian_sketch.argtypes = [vp, u64, u64, u64, fp]
+    L.cnmf_initialize.argtypes = [vp, u64, u64, u64, u64, fp, fp]
+    L.cnmf_powered_range_finder.argtypes = [vp, fp, u64, u64, u64, u64, u64, u64, C.c_int, fp]
+    L.cnmf_build_projectors.argtypes = [vp, fp, u64, u64, u64, u64, u64, u64, fp, fp]
+    L.cnmf_compress.argtypes = [vp, fp, u64, u64, u64, fp, fp, u64, fp, fp]
+    L.cnmf_compress_factors.argtypes = [vp, fp, fp, fp, fp, u64, u64, u64, u64, vp, vp]
+    L.cnmf_fasthals_rp_steps.argtypes = [vp, fp, fp, fp, fp, u64, u64, u64, u64, fp, fp, vp, vp,
+                                         C.c_int, C.c_double, C.c_double, u64, u64,
+                                         C.POINTER(u64)]
+    L.cnmf_reconstruction_error.argtypes = [vp, fp, u64, u64, u64, fp, fp, u64, dp]
+    L.cnmf_thin_qr.argtypes = [vp, fp, u64, u64, fp]
+    L.cnmf_xs_nn.argtypes = [vp, fp, u64, u64, u64, fp, u64, fp]
+    L.cnmf_xs_tn.argtypes = [vp, fp, u64, u64, u64, fp, u64, fp]
+    L.cnmf_synth_x.argtypes = [vp, u64, u64, u64, C.c_int, C.c_int, C.c_double, u64, u64, u64,
+                               u64, fp]
+    if L.cnmf_abi_version() != 1:
+        raise CudaError("libcnmf_b200.so ABI version mismatch")
+    _lib = L
+    return L
+
+
+@dataclass
+class SketchConfig:
+    """cnmf::SketchConfig (compression.hpp:13-17)."""
+    q: int = 0
+    power_iterations: int = 4
+    seed: int = 1
+
+
+@dataclass
+class SolverConfig:
+    """cnmf::SolverConfig (solvers.hpp:13-29); defaults as the reference."""
+    algorithm: int = FASTHALS
+    k: int = 2
+    sketch: SketchConfig = field(default_factory=SketchConfig)
+    alpha: float = 0.0
+    beta: float = 0.0
+    max_iterations: int = 200
+    rel_tolerance: float = 1e-9
+    error_interval: int = 5
+    seed: int = 1
+    normalize_a: bool = True
+
+    def _c(self) -> _Config:
+        algo = ALGORITHM_NAMES[self.algorithm] if isinstance(self.algorithm, str) else self.algorithm
+        return _Config(int(algo), self.k, self.sketch.q, self.sketch.power_iterations,
+                       self.sketch.seed, self.alpha, self.beta, self.max_iterations,
+                       self.rel_tolerance, self.error_interval, self.seed,
+                       int(bool(self.normalize_a)))
+
+    def validate(self, d: int, n: int) -> None:
+        """SolverConfig::validate (solvers.cpp:298-312); pure host logic."""
+        L = load_library()
+        msg = C.create_string_buffer(256)
+        cfg = self._c()
+        st = L.cnmf_solver_config_validate(C.byref(cfg), d, n, msg, 256)
+        if st:
+            raise _ERRORS.get(st, CnmfError)(msg.value.decode())
+
+
+@dataclass
+class RunRecord:
+    iteration: int
+    error: float
+    elapsed_seconds: float
+
+
+@dataclass
+class RunTrace:
+    """cnmf::RunTrace (metrics.hpp:70-84) plus device timing."""
+    records: List[RunRecord]
+    update_seconds: float
+    compress_seconds: float
+    error_seconds: float
+    gini_b: float
+    status: int
+    iterations_run: int
+    power_iterations: int
+    alpha: float
+    beta: float
+    seed: int
+    estimate_flops_per_iteration: float
+    estimate_memory_floats: float
+    x_norm_sq: float
+    redraws: int
+    x_passes: int
+    message: str
+
+    @property
+    def status_name(self) -> str:
+        return STATUS_NAMES[self.status]
+
+
+@dataclass
+class RunResult:
+    """cnmf::RunResult (solvers.hpp:94-97): factors (A d x k, B n x k) + trace."""
+    a: np.ndarray
+    b: np.ndarray
+    trace: RunTrace
+
+
+def _ptr(t) -> int:
+    """Raw pointer of a numpy array or a torch tensor (device pointers for CUDA tensors)."""
+    if isinstance(t, np.ndarray):
+        return t.ctypes.data
+    return t.data_ptr()
+
+
+class Context:
+    """One CUDA device + stream (cnmf_context)."""
+
+    def __init__(self, device: int = 0):
+        self.L = load_library()
+        h = C.c_void_p()
+        st = self.L.cnmf_context_create(device, C.byref(h))
+        if st:
+            raise _ERRORS.get(st, CnmfError)(f"cannot create a context on CUDA device {device}")
+        self.h = h
+
+    def close(self):
+        if getattr(self, "h", None):
+            self.L.cnmf_context_destroy(self.h)
+            self.h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    def _check(self, st: int):
+        if st:
+            raise _ERRORS.get(st, CnmfError)(self.L.cnmf_context_last_error(self.h).decode())
+
+    def stream(self) -> int:
+        return self.L.cnmf_context_stream(self.h)
+
+    # ---- run() -------------------------------------------------------------
+    def _trace(self, cap: int):
+        recs = (_Record * cap)()
+        tr = _Trace()
+        tr.records = C.cast(recs, C.POINTER(_Record))
+        tr.records_capacity = cap
+        return recs, tr
+
+    @staticmethod
+    def _result_trace(recs, tr) -> RunTrace:
+        n = min(tr.records_count, tr.records_capacity)
+        return RunTrace([RunRecord(recs[i].iteration, recs[i].error, recs[i].elapsed_seconds)
+                         for i in range(n)], tr.update_seconds, tr.compress_seconds,
+                        tr.error_seconds, tr.gini_b, tr.status, tr.iterations_run,
+                        tr.power_iterations, tr.alpha, tr.beta, tr.seed,
+                        tr.estimate_flops_per_iteration, tr.estimate_memory_floats,
+                        tr.x_norm_sq, tr.redraws, tr.x_passes, tr.message.decode())
+
+    def run(self, x, config: SolverConfig) -> RunResult:
+        """cnmf::run with X in host memory (numpy, float32, row-major)."""
+        x = np.ascontiguousarray(x, dtype=np.float32)
+        d, n = x.shape
+        cfg = config._c()
+        recs, tr = self._trace(config.max_iterations + 2)
+        a = np.empty((d, config.k), dtype=np.float32)
+        b = np.empty((n, config.k), dtype=np.float32)
+        self._check(self.L.cnmf_run(self.h, _ptr(x), d, n, n, C.byref(cfg), _ptr(a), _ptr(b),
+                                    C.byref(tr)))
+        return RunResult(a, b, self._result_trace(recs, tr))
+
+    def run_device(self, x, config: SolverConfig, a_out=None, b_out=None):
+        """cnmf::run with X already resident on the device (torch CUDA tensor)."""
+        import torch
+        d, n = x.shape
+        ldx = x.stride(0)
+        a = a_out if a_out is not None else torch.empty((d, config.k), device=x.device)
+        b = b_out if b_out is not None else torch.empty((n, config.k), device=x.device)
+        cfg = config._c()
+        recs, tr = self._trace(config.max_iterations + 2)
+        self._check(self.L.cnmf_run_device(self.h, _ptr(x), d, n, ldx, C.byref(cfg), _ptr(a),
+                                           _ptr(b), C.byref(tr)))
+        return a, b, self._result_trace(recs, tr)
+
+    # ---- step level (torch CUDA tensors) -------------------------------------
+    def gaussian_sketch(self, rows, cols, seed, out):
+        self._check(self.L.cnmf_gaussian_sketch(self.h, rows, cols, seed, _ptr(out)))
+        return out
+
+    def initialize(self, d, n, k, seed, a, b):
+        self._check(self.L.cnmf_initialize(self.h, d, n, k, seed, _ptr(a), _ptr(b)))
+        return a, b
+
+    def powered_range_finder(self, x, q, w, seed, transpose, out):
+        d, n = x.shape
+        self._check(self.L.cnmf_powered_range_finder(self.h, _ptr(x), d, n, x.stride(0), q, w,
+                                                     seed, int(transpose), _ptr(out)))
+        return out
+
+    def build_projectors(self, x, q, w, seed, left, right):
+        d, n = x.shape
+        self._check(self.L.cnmf_build_projectors(self.h, _ptr(x), d, n, x.stride(0), q, w, seed,
+                                                 _ptr(left), _ptr(right)))
+        return left, right
+
+    def compress(self, x, left, right, xhat, xcheck):
+        d, n = x.shape
+        q = left.shape[1]
+        self._check(self.L.cnmf_compress(self.h, _ptr(x), d, n, x.stride(0), _ptr(left),
+                                         _ptr(right), q, _ptr(xhat), _ptr(xcheck)))
+        return xhat, xcheck
+
+    def compress_factors(self, a, b, left, right, a_hat, b_check):
+        d, k = a.shape
+        n = b.shape[0]
+        q = left.shape[1]
+        self._check(self.L.cnmf_compress_factors(self.h, _ptr(a), _ptr(b), _ptr(left),
+                                                 _ptr(right), d, n, q, k, _ptr(a_hat),
+                                                 _ptr(b_check)))
+        return a_hat, b_check
+
+    def fasthals_rp_steps(self, xhat, xcheck, left, right, a, b, a_hat, b_check,
+                          normalize_a=True, alpha=0.0, beta=0.0, rng_seed=1, steps=1) -> int:
+        d, k = a.shape
+        n = b.shape[0]
+        q = left.shape[1]
+        red = C.c_uint64()
+        self._check(self.L.cnmf_fasthals_rp_steps(self.h, _ptr(xhat), _ptr(xcheck), _ptr(left),
+                                                  _ptr(right), d, n, q, k, _ptr(a), _ptr(b),
+                                                  _ptr(a_hat), _ptr(b_check), int(normalize_a),
+                                                  alpha, beta, rng_seed, steps, C.byref(red)))
+        return red.value
+
+    def reconstruction_error(self, x, a, b) -> float:
+        d, n = x.shape
+        out = C.c_double()
+        self._check(self.L.cnmf_reconstruction_error(self.h, _ptr(x), d, n, x.stride(0), _ptr(a),
+                                                     _ptr(b), a.shape[1], C.byref(out)))
+        return out.value
+
+    def thin_qr(self, y, out):
+        self._check(self.L.cnmf_thin_qr(self.h, _ptr(y), y.shape[0], y.shape[1], _ptr(out)))
+        return out
+
+    def xs_nn(self, x, s, out):
+        d, n = x.shape
+        self._check(self.L.cnmf_xs_nn(self.h, _ptr(x), d, n, x.stride(0), _ptr(s), s.shape[1],
+                                      _ptr(out)))
+        return out
+
+    def xs_tn(self, x, t, out):
+        d, n = x.shape
+        self._check(self.L.cnmf_xs_tn(self.h, _ptr(x), d, n, x.stride(0), _ptr(t), t.shape[1],
+                                      _ptr(out)))
+        return out
+
+    def synth_x(self, d, n, rank, factor_kind, noise_kind, sigma, seed, out, col_lo=0,
+                col_hi=None):
+        col_hi = n if col_hi is None else col_hi
+        self._check(self.L.cnmf_synth_x(self.h, d, n, rank, factor_kind, noise_kind, sigma, seed,
+                                        col_lo, col_hi, out.stride(0), _ptr(out)))
+        return out
+
+
+_default_ctx: Optional[Context] = None
+
+
+def default_context() -> Context:
+    global _default_ctx
+    if _default_ctx is None:
+        _default_ctx = Context(0)
+    return _default_ctx
+
+
+def run(x, config: SolverConfig) -> RunResult:
+    """cnmf::run(x, config) (solvers.hpp:104) on the default CUDA device."""
+    return default_context().run(x, config)
+
+
+# BASELINE.json configurations (synthetic stand-ins).
+CONFIGS = {
+    "c1": dict(d=1000, n=1000, rank=20, factor_kind=0, noise_kind=1, sigma=0.01, k=20, q=30,
+               w=2, iters=100),
+    "c2": dict(d=10000, n=5000, rank=16, factor_kind=1, noise_kind=1, sigma=0.05, k=16, q=36,
+               w=2, iters=200),
+    "c3": dict(d=100000, n=20000, rank=50, factor_kind=0, noise_kind=1, sigma=0.01, k=50, q=70,
+               w=2, iters=100),
+    "c4": dict(d=50000, n=100000, rank=100, factor_kind=2, noise_kind=2, sigma=0.0, k=100,
+               q=120, w=1, iters=100),
+    "c5": dict(d=200000, n=500000, rank=64, factor_kind=0, noise_kind=1, sigma=0.01, k=64, q=84,
+               w=1, iters=50),
+}

@@ -1,0 +1,866 @@
+// engine.cpp -- host side of the B200 FastHALS-RP path (C++, behind the C ABI
+// in include/cnmf_b200.h).
+//
+// Restates the orchestration of the reference's run_impl
+// (proj/src/solvers.cpp:189-294): validate, scan the data, seed one Rng, fill
+// A then B, build the projectors and compressed views, evaluate the
+// uncompressed objective on the error cadence, stop on the relative-decrease
+// tolerance, report the Gini of B.  All arithmetic runs in the device kernels
+// (csrc/*.cu); the host only sequences launches, reads back scalars, and
+// serves the rare dead-component redraws from the run's host Rng (the
+// reference draws them from the same mt19937_64 stream, solvers.cpp:17-31).
+#include <cuda_runtime.h>
+
+#include <cmath>
+#include <cstdio>
+#include <cstring>
+#include <map>
+#include <mutex>
+#include <random>
+#include <stdexcept>
+#include <string>
+#include <vector>
+
+#include "../../include/cnmf_b200.h"
+#include "kernels.h"
+
+using namespace cnmf;
+
+namespace {
+
+struct Fail : std::runtime_error {
+  cnmf_status status;
+  Fail(cnmf_status s, const std::string& m) : std::runtime_error(m), status(s) {}
+};
+
+void ck(cudaError_t e, const char* what) {
+  if (e != cudaSuccess)
+    throw Fail(CNMF_ERR_CUDA, std::string(what) + ": " + cudaGetErrorString(e));
+}
+#define CK(x) ck((x), #x)
+
+struct DevBuf {
+  void* p = nullptr;
+  size_t bytes = 0;
+};
+
+int64_t pad4(int64_t v) { return (v + 3) & ~int64_t(3); }
+
+}  // namespace
+
+struct cnmf_context {
+  int device = 0;
+  int nsm = 148;
+  cudaStream_t stream = nullptr;
+  cudaEvent_t ev[4] = {nullptr, nullptr, nullptr, nullptr};
+  std::string err;
+  std::mutex mu;
+  std::map<std::string, DevBuf> bufs;
+  HaltInfo* halt_host = nullptr;  // pinned
+
+  template <typename T>
+  T* ws(const std::string& name, size_t count) {
+    DevBuf& b = bufs[name];
+    const size_t bytes = std::max<size_t>(count * sizeof(T), 256);
+    if (b.bytes < bytes) {
+      if (b.p) CK(cudaFree(b.p));
+      b.p = nullptr;
+      b.bytes = 0;
+      CK(cudaMalloc(&b.p, bytes));
+      b.bytes = bytes;
+    }
+    return static_cast<T*>(b.p);
+  }
+  void sync() { CK(cudaStreamSynchronize(stream)); }
+  double elapsed(int a, int b) {
+    float ms = 0.f;
+    CK(cudaEventElapsedTime(&ms, ev[a], ev[b]));
+    return ms * 1e-3;
+  }
+};
+
+namespace {
+
+// ---------------------------------------------------------------- config ----
+void validate(const cnmf_solver_config& c, uint64_t d, uint64_t n) {
+  // SolverConfig::validate, solvers.cpp:298-312 (same messages).
+  const uint64_t mn = std::min(d, n);
+  const bool rp = c.algorithm == CNMF_MU_RP || c.algorithm == CNMF_HALS_RP ||
+                  c.algorithm == CNMF_FASTHALS_RP;
+  if (c.algorithm < CNMF_MU || c.algorithm > CNMF_FASTHALS_RP)
+    throw Fail(CNMF_ERR_CONFIG, "unknown algorithm");
+  if (c.k == 0 || c.k > mn) throw Fail(CNMF_ERR_CONFIG, "k must satisfy 1 <= k <= min(d, n)");
+  if (rp && (c.sketch_q <= c.k || c.sketch_q > mn))
+    throw Fail(CNMF_ERR_CONFIG, "compressed algorithms require k < q <= min(d, n)");
+  if (!(c.alpha >= 0.0) || !std::isfinite(c.alpha) || !(c.beta >= 0.0) || !std::isfinite(c.beta))
+    throw Fail(CNMF_ERR_CONFIG, "alpha and beta must be finite and non-negative");
+  if ((c.alpha != 0.0 || c.beta != 0.0) && c.algorithm != CNMF_HALS_RP &&
+      c.algorithm != CNMF_FASTHALS_RP)
+    throw Fail(CNMF_ERR_CONFIG, "penalties are supported by hals-rp and fasthals-rp only");
+  if (c.error_interval == 0) throw Fail(CNMF_ERR_CONFIG, "error_interval must be positive");
+  if (!(c.rel_tolerance > 0.0) || !std::isfinite(c.rel_tolerance))
+    throw Fail(CNMF_ERR_CONFIG, "rel_tolerance must be positive and finite");
+}
+
+void require_shapes(uint64_t k, uint64_t q) {
+  if (q > 128 || k > 128)
+    throw Fail(CNMF_ERR_UNSUPPORTED, "this build supports q <= 128 and k <= 128");
+}
+
+// ------------------------------------------------------------------ rng -----
+// uniform_positive of cnmf::Rng (rng.hpp:20-29) on std::mt19937_64.
+double uniform_positive(std::mt19937_64& e) {
+  double v = 0.0;
+  while (v == 0.0) v = static_cast<double>(e() >> 11) * 0x1.0p-53;
+  return v;
+}
+
+// gaussian_sketch(rows, cols, seed) into out (ld), on the device.
+void gen_normals(cnmf_context* c, uint64_t seed, int64_t rows, int64_t cols, float* out, int ld,
+                 const std::string& tag) {
+  const uint64_t count = (uint64_t)rows * cols;
+  const uint64_t nwords = 2 * ((count + 1) / 2) + 256;
+  uint64_t* words = c->ws<uint64_t>("words_" + tag, nwords);
+  int* flag = c->ws<int>("nflag_" + tag, 4);
+  CK(cudaMemsetAsync(flag, 0, sizeof(int), c->stream));
+  MtJobs jobs{};
+  jobs.job[0] = MtJob{seed, nwords, words};
+  launch_mt_streams(jobs, 1, c->stream);
+  launch_normal_map(words, count, (int)cols, ld, out, flag, c->nsm, c->stream);
+  launch_normal_exact(words, nwords, count, (int)cols, ld, out, flag, c->stream);
+  CK(cudaGetLastError());
+}
+
+// Two sketches generated concurrently (one MT engine per CTA).
+void gen_normals2(cnmf_context* c, uint64_t seed0, int64_t rows0, int64_t cols, float* out0,
+                  uint64_t seed1, int64_t rows1, float* out1, int ld) {
+  const uint64_t c0 = (uint64_t)rows0 * cols, c1 = (uint64_t)rows1 * cols;
+  const uint64_t n0 = 2 * ((c0 + 1) / 2) + 256, n1 = 2 * ((c1 + 1) / 2) + 256;
+  uint64_t* w0 = c->ws<uint64_t>("words_L", n0);
+  uint64_t* w1 = c->ws<uint64_t>("words_R", n1);
+  int* flag = c->ws<int>("nflag2", 4);
+  CK(cudaMemsetAsync(flag, 0, 2 * sizeof(int), c->stream));
+  MtJobs jobs{};
+  jobs.job[0] = MtJob{seed0, n0, w0};
+  jobs.job[1] = MtJob{seed1, n1, w1};
+  launch_mt_streams(jobs, 2, c->stream);
+  launch_normal_map(w0, c0, (int)cols, ld, out0, flag, c->nsm, c->stream);
+  launch_normal_exact(w0, n0, c0, (int)cols, ld, out0, flag, c->stream);
+  launch_normal_map(w1, c1, (int)cols, ld, out1, flag + 1, c->nsm, c->stream);
+  launch_normal_exact(w1, n1, c1, (int)cols, ld, out1, flag + 1, c->stream);
+  CK(cudaGetLastError());
+}
+
+// initialize(d, n, k, seed) into column-major A_cm / B_cm; returns the
+// device counter of raw draws consumed (for positioning the host Rng).
+uint64_t* gen_init(cnmf_context* c, uint64_t seed, int64_t d, int64_t n, int k, float* a_cm,
+                   float* b_cm) {
+  const uint64_t total = (uint64_t)(d + n) * k;
+  const uint64_t nwords = total + 256;
+  uint64_t* words = c->ws<uint64_t>("words_init", nwords);
+  int* flag = c->ws<int>("iflag", 4);
+  uint64_t* consumed = c->ws<uint64_t>("iconsumed", 1);
+  CK(cudaMemsetAsync(flag, 0, sizeof(int), c->stream));
+  CK(cudaMemcpyAsync(consumed, &total, sizeof(uint64_t), cudaMemcpyHostToDevice, c->stream));
+  MtJobs jobs{};
+  jobs.job[0] = MtJob{seed, nwords, words};
+  launch_mt_streams(jobs, 1, c->stream);
+  launch_uniform_init(words, d, n, k, a_cm, b_cm, flag, c->nsm, c->stream);
+  launch_uniform_init_exact(words, nwords, d, n, k, a_cm, b_cm, flag, consumed, c->stream);
+  CK(cudaGetLastError());
+  return consumed;
+}
+
+// ---------------------------------------------------------- compression -----
+struct XView {
+  const float* x;
+  int64_t ldx, d, n;
+};
+
+// Orthonormal basis (rows x lp) of range(X) (transpose = false) or of
+// range(X^T) (transpose = true); range_finder_impl, compression.cpp:23-42.
+// `omega` holds the sketch (op_cols x lp).  Returns the X passes made.
+int range_finder(cnmf_context* c, const XView& X, int q, int lp, uint64_t w, bool transpose,
+                 const float* omega, float* basis, const std::string& tag) {
+  const int64_t rows = transpose ? X.n : X.d, cols = transpose ? X.d : X.n;
+  float* y = c->ws<float>("rf_y_" + tag, rows * lp);
+  float* z = c->ws<float>("rf_z_" + tag, cols * lp);
+  float* zq = c->ws<float>("rf_zq_" + tag, cols * lp);
+  float* xs = c->ws<float>("xs_ws", xstream_ws_floats(X.d, X.n, lp, c->nsm));
+  void* qws = c->ws<char>("qr_ws", qr_ws_bytes(std::max(X.d, X.n), lp, c->nsm));
+  auto apply = [&](const float* s, float* out, bool tn) {
+    if (tn)
+      launch_xs_tn(X.x, X.ldx, X.d, X.n, s, lp, out, xs, c->nsm, c->stream);
+    else
+      launch_xs_nn(X.x, X.ldx, X.d, X.n, s, lp, out, xs, c->nsm, c->stream);
+  };
+  apply(omega, y, transpose);
+  launch_thin_qr(y, rows, q, lp, basis, qws, c->nsm, c->stream);
+  for (uint64_t it = 0; it < w; ++it) {
+    apply(basis, z, !transpose);
+    launch_thin_qr(z, cols, q, lp, zq, qws, c->nsm, c->stream);
+    apply(zq, y, transpose);
+    launch_thin_qr(y, rows, q, lp, basis, qws, c->nsm, c->stream);
+  }
+  CK(cudaGetLastError());
+  return 1 + 2 * (int)w;
+}
+
+// ------------------------------------------------------------------ HALS ----
+struct HalsRun {
+  HalsState st;
+  int grid;
+};
+
+HalsRun make_hals(cnmf_context* c, int64_t d, int64_t n, int l, int lp, int k) {
+  HalsRun r;
+  HalsState& s = r.st;
+  s.d = d;
+  s.n = n;
+  s.l = l;
+  s.lp = lp;
+  s.k = k;
+  s.a = c->ws<float>("A_cm", (size_t)k * d);
+  s.b = c->ws<float>("B_cm", (size_t)k * n);
+  s.bold = c->ws<float>("B_old", (size_t)k * n);
+  s.h = c->ws<float>("H_cm", (size_t)k * d);
+  s.ahat = c->ws<double>("Ahat", (size_t)lp * k);
+  s.bchk = c->ws<double>("Bchk", (size_t)lp * k);
+  s.g = c->ws<double>("Gk", (size_t)k * k);
+  s.w = c->ws<double>("Wk", (size_t)k * k);
+  r.grid = hals_grid(s, c->nsm);
+  s.part = c->ws<double>("hals_part", hals_part_doubles(r.grid, lp, k));
+  s.npart = c->ws<double>("hals_npart", (size_t)k * r.grid);
+  s.zflag = c->ws<int>("hals_zflag", (size_t)k * r.grid);
+  s.bar = c->ws<unsigned>("hals_bar", 2);
+  s.halt = c->ws<HaltInfo>("hals_halt", 1);
+  CK(cudaMemsetAsync(s.bar, 0, 2 * sizeof(unsigned), c->stream));
+  CK(cudaMemsetAsync(s.ahat, 0, sizeof(double) * lp * k, c->stream));
+  CK(cudaMemsetAsync(s.bchk, 0, sizeof(double) * lp * k, c->stream));
+  return r;
+}
+
+// Draws reinit_column (solvers.cpp:28-31) from the host Rng into a device column.
+void redraw_column(cnmf_context* c, std::mt19937_64& rng, float* col_dev, int64_t rows) {
+  std::vector<float> v((size_t)rows);
+  for (int64_t i = 0; i < rows; ++i) v[(size_t)i] = (float)(uniform_positive(rng) * 1e-3);
+  CK(cudaMemcpyAsync(col_dev, v.data(), sizeof(float) * rows, cudaMemcpyHostToDevice, c->stream));
+  c->sync();  // v goes out of scope
+}
+
+// Runs 0-based iterations [ib, ie) with halt/redraw servicing.  `rng` is
+// produced lazily (positioning the host stream costs a discard).
+template <typename RngFn>
+void run_hals(cnmf_context* c, HalsRun& hr, int normalize_a, double alpha, double beta,
+              int64_t ib, int64_t ie, RngFn&& get_rng, double* update_seconds,
+              uint64_t* redraws) {
+  HalsState& st = hr.st;
+  int half = 0, col = 0, skip = -1;
+  int64_t begin = ib;
+  for (;;) {
+    CK(cudaEventRecord(c->ev[0], c->stream));
+    CK(launch_hals(st, normalize_a, alpha, beta, (int)begin, (int)ie, half, col, skip, hr.grid,
+                   c->stream));
+    CK(cudaEventRecord(c->ev[1], c->stream));
+    CK(cudaMemcpyAsync(c->halt_host, st.halt, sizeof(HaltInfo), cudaMemcpyDeviceToHost,
+                       c->stream));
+    c->sync();
+    *update_seconds += c->elapsed(0, 1);
+    const HaltInfo h = *c->halt_host;
+    if (!h.halted) break;
+    std::mt19937_64& rng = get_rng();
+    const int j = h.column;
+    switch (h.kind) {
+      case kEvDeadB:  // solvers.cpp:424-428
+        redraw_column(c, rng, st.b + (int64_t)j * st.n, st.n);
+        launch_compress_factors(st, 1, j, c->stream);
+        half = 0; col = j; skip = j;
+        break;
+      case kEvZeroA:  // solvers.cpp:435-436
+        redraw_column(c, rng, st.a + (int64_t)j * st.d, st.d);
+        if (normalize_a) launch_normalize_column(st.a, st.d, j, c->stream);
+        half = 0; col = j + 1; skip = -1;
+        break;
+      case kEvDeadA:  // solvers.cpp:445-449
+        redraw_column(c, rng, st.a + (int64_t)j * st.d, st.d);
+        launch_compress_factors(st, 0, j, c->stream);
+        half = 1; col = j; skip = j;
+        break;
+      case kEvZeroB:  // solvers.cpp:452
+        redraw_column(c, rng, st.b + (int64_t)j * st.n, st.n);
+        half = 1; col = j + 1; skip = -1;
+        break;
+      default:
+        throw Fail(CNMF_ERR_CUDA, "corrupt halt record from the HALS kernel");
+    }
+    CK(cudaGetLastError());
+    begin = h.iter - 1;
+    ++*redraws;
+  }
+}
+
+double recon_error(cnmf_context* c, const XView& X, const float* a_cm, const float* b_cm, int k) {
+  double* out = c->ws<double>("err_out", 1);
+  void* ws = c->ws<char>("metrics_ws", metrics_ws_bytes(X.d, X.n, c->nsm));
+  launch_recon_error(X.x, X.ldx, X.d, X.n, a_cm, b_cm, k, out, ws, c->nsm, c->stream);
+  CK(cudaGetLastError());
+  double v = 0.0;
+  CK(cudaMemcpyAsync(&v, out, sizeof(double), cudaMemcpyDeviceToHost, c->stream));
+  c->sync();
+  return v;
+}
+
+// X with ldx % 4 == 0 and 16-byte alignment (the X-stream kernels use
+// 128-bit loads); otherwise a padded device copy.
+XView prepare_x(cnmf_context* c, const float* x, int64_t d, int64_t n, int64_t ldx) {
+  if (ldx < n) throw Fail(CNMF_ERR_DIMENSION, "ldx must be >= n");
+  if (ldx % 4 == 0 && (reinterpret_cast<uintptr_t>(x) & 15) == 0) return XView{x, ldx, d, n};
+  const int64_t lp = pad4(n);
+  float* xp = c->ws<float>("x_padded", (size_t)d * lp);
+  CK(cudaMemset2DAsync(xp, lp * sizeof(float), 0, lp * sizeof(float), d, c->stream));
+  CK(cudaMemcpy2DAsync(xp, lp * sizeof(float), x, ldx * sizeof(float), n * sizeof(float), d,
+                       cudaMemcpyDeviceToDevice, c->stream));
+  return XView{xp, lp, d, n};
+}
+
+// --------------------------------------------------------------- run() ------
+void run_device_impl(cnmf_context* c, const float* x_in, int64_t d, int64_t n, int64_t ldx,
+                     const cnmf_solver_config& cfg, float* a_out, float* b_out,
+                     cnmf_run_trace* tr) {
+  validate(cfg, d, n);
+  if (cfg.algorithm != CNMF_FASTHALS_RP)
+    throw Fail(CNMF_ERR_UNSUPPORTED, "this build implements the fasthals-rp path only");
+  require_shapes(cfg.k, cfg.sketch_q);
+  const int k = (int)cfg.k, q = (int)cfg.sketch_q, lp = pad16(q);
+  const uint64_t w = cfg.sketch_power_iterations;
+
+  cnmf_run_trace t{};
+  t.records = tr->records;
+  t.records_capacity = tr->records_capacity;
+  t.status = CNMF_REACHED_MAX_ITERATIONS;
+  t.power_iterations = w;
+  t.alpha = cfg.alpha;
+  t.beta = cfg.beta;
+  t.seed = cfg.seed;
+  t.estimate_flops_per_iteration = 2.0 * (double)d * k * q;  // metrics.cpp:45
+  t.estimate_memory_floats = (2.0 * q + k) * ((double)d + (double)n);
+  auto push = [&](uint64_t it, double err, double el) {
+    if (t.records_count < t.records_capacity) t.records[t.records_count] = {it, err, el};
+    ++t.records_count;
+  };
+
+  const XView X = prepare_x(c, x_in, d, n, ldx);
+
+  // check_data (solvers.cpp:47-52) + ||X||^2
+  {
+    int* flag = c->ws<int>("cflag", 4);
+    double* nrm = c->ws<double>("xnorm", 1);
+    void* ws = c->ws<char>("metrics_ws", metrics_ws_bytes(d, n, c->nsm));
+    CK(cudaMemsetAsync(flag, 0, sizeof(int), c->stream));
+    launch_check_data(X.x, X.ldx, d, n, flag, nrm, ws, c->nsm, c->stream);
+    CK(cudaGetLastError());
+    int hflag = 0;
+    CK(cudaMemcpyAsync(&hflag, flag, sizeof(int), cudaMemcpyDeviceToHost, c->stream));
+    CK(cudaMemcpyAsync(&t.x_norm_sq, nrm, sizeof(double), cudaMemcpyDeviceToHost, c->stream));
+    c->sync();
+    if (hflag) throw Fail(CNMF_ERR_INPUT, "solver input must be entrywise non-negative and finite");
+  }
+
+  HalsRun hr = make_hals(c, d, n, q, lp, k);
+  HalsState& st = hr.st;
+
+  // Rng rng(seed); A then B uniform_positive (solvers.cpp:206-211).
+  uint64_t* consumed_dev = gen_init(c, cfg.seed, d, n, k, st.a, st.b);
+
+  // ---- compression (build_projectors + compress_left/right) ----
+  float* omega_l = c->ws<float>("omega_L", (size_t)n * lp);
+  float* omega_r = c->ws<float>("omega_R", (size_t)d * lp);
+  float* lm = c->ws<float>("L", (size_t)d * lp);
+  float* rt = c->ws<float>("Rt", (size_t)n * lp);
+  float* xc = c->ws<float>("Xcheck", (size_t)d * lp);
+  float* xht = c->ws<float>("XhatT", (size_t)n * lp);
+  float* xs = c->ws<float>("xs_ws", xstream_ws_floats(d, n, lp, c->nsm));
+  CK(cudaMemsetAsync(omega_l, 0, sizeof(float) * n * lp, c->stream));
+  CK(cudaMemsetAsync(omega_r, 0, sizeof(float) * d * lp, c->stream));
+  CK(cudaEventRecord(c->ev[2], c->stream));
+  gen_normals2(c, cfg.sketch_seed * 2, n, q, omega_l, cfg.sketch_seed * 2 + 1, d, omega_r, lp);
+  int passes = range_finder(c, X, q, lp, w, false, omega_l, lm, "L");
+  passes += range_finder(c, X, q, lp, w, true, omega_r, rt, "R");
+  launch_xs_tn(X.x, X.ldx, d, n, lm, lp, xht, xs, c->nsm, c->stream);  // X-hat^T = X^T L
+  launch_xs_nn(X.x, X.ldx, d, n, rt, lp, xc, xs, c->nsm, c->stream);   // X-check = X R^T
+  passes += 2;
+  CK(cudaEventRecord(c->ev[3], c->stream));
+  CK(cudaGetLastError());
+  st.xc = xc;
+  st.xht = xht;
+  st.lm = lm;
+  st.rt = rt;
+  t.x_passes = (uint64_t)passes;
+
+  // a_hat = L^T A, b_check = R B (solvers.cpp:219-220)
+  launch_compress_factors(st, 0, -1, c->stream);
+  launch_compress_factors(st, 1, -1, c->stream);
+  CK(cudaGetLastError());
+  c->sync();
+  t.compress_seconds = c->elapsed(2, 3);
+
+  std::mt19937_64 rng;
+  bool rng_ready = false;
+  auto get_rng = [&]() -> std::mt19937_64& {
+    if (!rng_ready) {
+      uint64_t consumed = 0;
+      CK(cudaMemcpy(&consumed, consumed_dev, sizeof(uint64_t), cudaMemcpyDeviceToHost));
+      rng.seed(cfg.seed);
+      rng.discard(consumed);
+      rng_ready = true;
+    }
+    return rng;
+  };
+
+  auto timed_error = [&]() {
+    CK(cudaEventRecord(c->ev[2], c->stream));
+    const double e = recon_error(c, X, st.a, st.b, k);
+    CK(cudaEventRecord(c->ev[3], c->stream));
+    c->sync();
+    t.error_seconds += c->elapsed(2, 3);
+    return e;
+  };
+
+  double previous = timed_error();  // solvers.cpp:223-229
+  if (!std::isfinite(previous)) {
+    t.status = CNMF_ABORTED;
+    std::snprintf(t.message, sizeof t.message, "non-finite objective at iteration 0");
+  } else {
+    push(0, previous, 0.0);
+  }
+  const uint64_t max_it = cfg.max_iterations, every = cfg.error_interval;
+  uint64_t it = 1;
+  while (t.status != CNMF_ABORTED && it <= max_it) {  // solvers.cpp:231-284
+    uint64_t e = ((it + every - 1) / every) * every;
+    if (e > max_it) e = max_it;
+    run_hals(c, hr, cfg.normalize_a, cfg.alpha, cfg.beta, (int64_t)it - 1, (int64_t)e, get_rng,
+             &t.update_seconds, &t.redraws);
+    t.iterations_run = e;
+    const double err = timed_error();
+    if (!std::isfinite(err)) {
+      t.status = CNMF_ABORTED;
+      std::snprintf(t.message, sizeof t.message, "non-finite objective at iteration %llu",
+                    (unsigned long long)e);
+      break;
+    }
+    push(e, err, t.update_seconds);
+    const bool converged = previous == 0.0 ? err == 0.0
+                                           : std::fabs(previous - err) / previous <
+                                                 cfg.rel_tolerance;
+    if (converged) {
+      t.status = CNMF_CONVERGED;
+      std::snprintf(t.message, sizeof t.message,
+                    "relative error decrease below tolerance at iteration %llu",
+                    (unsigned long long)e);
+      break;
+    }
+    previous = err;
+    it = e + 1;
+  }
+
+  // gini(B) (solvers.cpp:286-291) and the factors in reference layout.
+  {
+    const int64_t count = n * (int64_t)k;
+    const size_t gb = gini_ws_bytes(count);
+    void* gws = c->ws<char>("gini_ws", gb);
+    double* gout = c->ws<double>("gini_out", 1);
+    launch_gini(st.b, count, gout, gws, gb, c->stream);
+    launch_cm_to_rm(st.a, d, k, a_out, c->stream);
+    launch_cm_to_rm(st.b, n, k, b_out, c->stream);
+    CK(cudaGetLastError());
+    CK(cudaMemcpyAsync(&t.gini_b, gout, sizeof(double), cudaMemcpyDeviceToHost, c->stream));
+    c->sync();
+  }
+  *tr = t;
+}
+
+template <typename F>
+cnmf_status guarded(cnmf_context* c, F&& f) {
+  if (!c) return CNMF_ERR_CONFIG;
+  std::lock_guard<std::mutex> lock(c->mu);
+  try {
+    CK(cudaSetDevice(c->device));
+    f();
+    c->err.clear();
+    return CNMF_OK;
+  } catch (const Fail& e) {
+    c->err = e.what();
+    if (e.status == CNMF_ERR_CUDA) cudaGetLastError();
+    return e.status;
+  } catch (const std::exception& e) {
+    c->err = e.what();
+    return CNMF_ERR_CUDA;
+  }
+}
+
+float* padded(cnmf_context* c, const std::string& name, const float* src, int64_t rows, int l,
+              int lp) {
+  float* dst = c->ws<float>(name, (size_t)rows * lp);
+  launch_pad_cols(src, rows, l, dst, lp, c->stream);
+  return dst;
+}
+
+}  // namespace
+
+// =================================================================== C ABI ==
+extern "C" {
+
+int cnmf_abi_version(void) { return CNMF_B200_ABI_VERSION; }
+
+cnmf_status cnmf_context_create(int device, cnmf_context** out) {
+  if (!out) return CNMF_ERR_CONFIG;
+  *out = nullptr;
+  int count = 0;
+  if (cudaGetDeviceCount(&count) != cudaSuccess || count == 0) {
+    cudaGetLastError();
+    return CNMF_ERR_CUDA;
+  }
+  if (device < 0 || device >= count) return CNMF_ERR_CONFIG;
+  auto* c = new cnmf_context();
+  c->device = device;
+  if (cudaSetDevice(device) != cudaSuccess ||
+      cudaStreamCreateWithFlags(&c->stream, cudaStreamNonBlocking) != cudaSuccess ||
+      cudaDeviceGetAttribute(&c->nsm, cudaDevAttrMultiProcessorCount, device) != cudaSuccess ||
+      cudaMallocHost(&c->halt_host, sizeof(HaltInfo)) != cudaSuccess) {
+    delete c;
+    return CNMF_ERR_CUDA;
+  }
+  for (auto& e : c->ev)
+    if (cudaEventCreate(&e) != cudaSuccess) {
+      delete c;
+      return CNMF_ERR_CUDA;
+    }
+  *out = c;
+  return CNMF_OK;
+}
+
+void cnmf_context_destroy(cnmf_context* c) {
+  if (!c) return;
+  cudaSetDevice(c->device);
+  cudaStreamSynchronize(c->stream);
+  for (auto& kv : c->bufs)
+    if (kv.second.p) cudaFree(kv.second.p);
+  for (auto& e : c->ev)
+    if (e) cudaEventDestroy(e);
+  if (c->halt_host) cudaFreeHost(c->halt_host);
+  if (c->stream) cudaStreamDestroy(c->stream);
+  delete c;
+}
+
+const char* cnmf_context_last_error(const cnmf_context* c) { return c ? c->err.c_str() : ""; }
+
+void* cnmf_context_stream(cnmf_context* c) {
+  if (!c) return nullptr;
+  cudaStreamSynchronize(c->stream);
+  return (void*)c->stream;
+}
+
+void cnmf_solver_config_init(cnmf_solver_config* cfg) {
+  if (!cfg) return;
+  std::memset(cfg, 0, sizeof *cfg);
+  cfg->algorithm = CNMF_FASTHALS;  // SolverConfig::algorithm default
+  cfg->k = 2;
+  cfg->sketch_q = 0;
+  cfg->sketch_power_iterations = 4;
+  cfg->sketch_seed = 1;
+  cfg->alpha = 0.0;
+  cfg->beta = 0.0;
+  cfg->max_iterations = 200;
+  cfg->rel_tolerance = 1e-9;
+  cfg->error_interval = 5;
+  cfg->seed = 1;
+  cfg->normalize_a = 1;
+}
+
+cnmf_status cnmf_solver_config_validate(const cnmf_solver_config* cfg, uint64_t d, uint64_t n,
+                                        char* message, size_t cap) {
+  try {
+    if (!cfg) throw Fail(CNMF_ERR_CONFIG, "null config");
+    validate(*cfg, d, n);
+    if (message && cap) message[0] = 0;
+    return CNMF_OK;
+  } catch (const Fail& e) {
+    if (message && cap) std::snprintf(message, cap, "%s", e.what());
+    return e.status;
+  }
+}
+
+cnmf_status cnmf_run_device(cnmf_context* c, const float* x, uint64_t d, uint64_t n, uint64_t ldx,
+                            const cnmf_solver_config* cfg, float* a, float* b,
+                            cnmf_run_trace* trace) {
+  return guarded(c, [&] {
+    if (!cfg || !trace || !x || !a || !b) throw Fail(CNMF_ERR_CONFIG, "null argument");
+    run_device_impl(c, x, (int64_t)d, (int64_t)n, (int64_t)ldx, *cfg, a, b, trace);
+  });
+}
+
+cnmf_status cnmf_run(cnmf_context* c, const float* x, uint64_t d, uint64_t n, uint64_t ldx,
+                     const cnmf_solver_config* cfg, float* a_out, float* b_out,
+                     cnmf_run_trace* trace) {
+  return guarded(c, [&] {
+    if (!cfg || !trace || !x || !a_out || !b_out) throw Fail(CNMF_ERR_CONFIG, "null argument");
+    if (ldx < n) throw Fail(CNMF_ERR_DIMENSION, "ldx must be >= n");
+    validate(*cfg, d, n);
+    const int64_t lx = pad4((int64_t)n);
+    float* xd = c->ws<float>("x_host_copy", (size_t)d * lx);
+    if ((int64_t)n != lx)
+      CK(cudaMemsetAsync(xd, 0, sizeof(float) * d * lx, c->stream));
+    CK(cudaMemcpy2DAsync(xd, lx * sizeof(float), x, ldx * sizeof(float), n * sizeof(float), d,
+                         cudaMemcpyHostToDevice, c->stream));
+    float* ad = c->ws<float>("a_out_dev", (size_t)d * cfg->k);
+    float* bd = c->ws<float>("b_out_dev", (size_t)n * cfg->k);
+    run_device_impl(c, xd, (int64_t)d, (int64_t)n, lx, *cfg, ad, bd, trace);
+    CK(cudaMemcpyAsync(a_out, ad, sizeof(float) * d * cfg->k, cudaMemcpyDeviceToHost, c->stream));
+    CK(cudaMemcpyAsync(b_out, bd, sizeof(float) * n * cfg->k, cudaMemcpyDeviceToHost, c->stream));
+    c->sync();
+  });
+}
+
+cnmf_status cnmf_gaussian_sketch(cnmf_context* c, uint64_t rows, uint64_t cols, uint64_t seed,
+                                 float* out) {
+  return guarded(c, [&] {
+    gen_normals(c, seed, (int64_t)rows, (int64_t)cols, out, (int)cols, "sk");
+    c->sync();
+  });
+}
+
+cnmf_status cnmf_initialize(cnmf_context* c, uint64_t d, uint64_t n, uint64_t k, uint64_t seed,
+                            float* a, float* b) {
+  return guarded(c, [&] {
+    if (d == 0 || n == 0 || k == 0)
+      throw Fail(CNMF_ERR_CONFIG, "initialize requires positive dimensions");
+    float* acm = c->ws<float>("init_acm", d * k);
+    float* bcm = c->ws<float>("init_bcm", n * k);
+    gen_init(c, seed, (int64_t)d, (int64_t)n, (int)k, acm, bcm);
+    launch_cm_to_rm(acm, (int64_t)d, (int)k, a, c->stream);
+    launch_cm_to_rm(bcm, (int64_t)n, (int)k, b, c->stream);
+    CK(cudaGetLastError());
+    c->sync();
+  });
+}
+
+cnmf_status cnmf_powered_range_finder(cnmf_context* c, const float* x, uint64_t d, uint64_t n,
+                                      uint64_t ldx, uint64_t q, uint64_t w, uint64_t seed,
+                                      int transpose, float* basis) {
+  return guarded(c, [&] {
+    const uint64_t rows = transpose ? n : d, cols = transpose ? d : n;
+    if (q == 0 || q > std::min(rows, cols))
+      throw Fail(CNMF_ERR_CONFIG,
+                 "powered_range_finder: q must satisfy 1 <= q <= min(rows, cols)");
+    require_shapes(1, q);
+    const int lp = pad16((int)q);
+    const XView X = prepare_x(c, x, (int64_t)d, (int64_t)n, (int64_t)ldx);
+    float* om = c->ws<float>("prf_omega", cols * lp);
+    float* out = c->ws<float>("prf_basis", rows * lp);
+    CK(cudaMemsetAsync(om, 0, sizeof(float) * cols * lp, c->stream));
+    gen_normals(c, seed, (int64_t)cols, (int64_t)q, om, lp, "prf");
+    range_finder(c, X, (int)q, lp, w, transpose != 0, om, out, "prf");
+    launch_unpad_cols(out, (int64_t)rows, lp, basis, (int)q, c->stream);
+    CK(cudaGetLastError());
+    c->sync();
+  });
+}
+
+cnmf_status cnmf_build_projectors(cnmf_context* c, const float* x, uint64_t d, uint64_t n,
+                                  uint64_t ldx, uint64_t q, uint64_t w, uint64_t seed,
+                                  float* left, float* right) {
+  return guarded(c, [&] {
+    if (q == 0 || q > std::min(d, n))
+      throw Fail(CNMF_ERR_CONFIG,
+                 "powered_range_finder: q must satisfy 1 <= q <= min(rows, cols)");
+    require_shapes(1, q);
+    const int lp = pad16((int)q);
+    const XView X = prepare_x(c, x, (int64_t)d, (int64_t)n, (int64_t)ldx);
+    float* oml = c->ws<float>("omega_L", n * lp);
+    float* omr = c->ws<float>("omega_R", d * lp);
+    float* lm = c->ws<float>("L", d * lp);
+    float* rt = c->ws<float>("Rt", n * lp);
+    CK(cudaMemsetAsync(oml, 0, sizeof(float) * n * lp, c->stream));
+    CK(cudaMemsetAsync(omr, 0, sizeof(float) * d * lp, c->stream));
+    gen_normals2(c, seed * 2, (int64_t)n, (int64_t)q, oml, seed * 2 + 1, (int64_t)d, omr, lp);
+    range_finder(c, X, (int)q, lp, w, false, oml, lm, "L");
+    range_finder(c, X, (int)q, lp, w, true, omr, rt, "R");
+    launch_unpad_cols(lm, (int64_t)d, lp, left, (int)q, c->stream);
+    launch_transpose(rt, (int64_t)n, (int64_t)q, lp, right, (int64_t)n, c->stream);
+    CK(cudaGetLastError());
+    c->sync();
+  });
+}
+
+cnmf_status cnmf_compress(cnmf_context* c, const float* x, uint64_t d, uint64_t n, uint64_t ldx,
+                          const float* left, const float* right, uint64_t q, float* xhat,
+                          float* xcheck) {
+  return guarded(c, [&] {
+    require_shapes(1, q);
+    const int lp = pad16((int)q);
+    const XView X = prepare_x(c, x, (int64_t)d, (int64_t)n, (int64_t)ldx);
+    float* lm = padded(c, "cmp_L", left, (int64_t)d, (int)q, lp);
+    float* rtu = c->ws<float>("cmp_Rt_u", n * q);
+    launch_transpose(right, (int64_t)q, (int64_t)n, (int64_t)n, rtu, (int64_t)q, c->stream);
+    float* rt = padded(c, "cmp_Rt", rtu, (int64_t)n, (int)q, lp);
+    float* xht = c->ws<float>("cmp_XhT", n * lp);
+    float* xcp = c->ws<float>("cmp_Xc", d * lp);
+    float* xs = c->ws<float>("xs_ws", xstream_ws_floats((int64_t)d, (int64_t)n, lp, c->nsm));
+    launch_xs_tn(X.x, X.ldx, X.d, X.n, lm, lp, xht, xs, c->nsm, c->stream);
+    launch_xs_nn(X.x, X.ldx, X.d, X.n, rt, lp, xcp, xs, c->nsm, c->stream);
+    launch_transpose(xht, (int64_t)n, (int64_t)q, lp, xhat, (int64_t)n, c->stream);
+    launch_unpad_cols(xcp, (int64_t)d, lp, xcheck, (int)q, c->stream);
+    CK(cudaGetLastError());
+    c->sync();
+  });
+}
+
+cnmf_status cnmf_compress_factors(cnmf_context* c, const float* a, const float* b,
+                                  const float* left, const float* right, uint64_t d, uint64_t n,
+                                  uint64_t q, uint64_t k, double* a_hat, double* b_check) {
+  return guarded(c, [&] {
+    require_shapes(k, q);
+    const int lp = pad16((int)q);
+    HalsRun hr = make_hals(c, (int64_t)d, (int64_t)n, (int)q, lp, (int)k);
+    HalsState& st = hr.st;
+    st.lm = padded(c, "cf_L", left, (int64_t)d, (int)q, lp);
+    float* rtu = c->ws<float>("cf_Rt_u", n * q);
+    launch_transpose(right, (int64_t)q, (int64_t)n, (int64_t)n, rtu, (int64_t)q, c->stream);
+    st.rt = padded(c, "cf_Rt", rtu, (int64_t)n, (int)q, lp);
+    launch_rm_to_cm(a, (int64_t)d, (int)k, st.a, c->stream);
+    launch_rm_to_cm(b, (int64_t)n, (int)k, st.b, c->stream);
+    launch_compress_factors(st, 0, -1, c->stream);
+    launch_compress_factors(st, 1, -1, c->stream);
+    CK(cudaMemcpyAsync(a_hat, st.ahat, sizeof(double) * q * k, cudaMemcpyDeviceToDevice, c->stream));
+    CK(cudaMemcpyAsync(b_check, st.bchk, sizeof(double) * q * k, cudaMemcpyDeviceToDevice,
+                       c->stream));
+    CK(cudaGetLastError());
+    c->sync();
+  });
+}
+
+cnmf_status cnmf_fasthals_rp_steps(cnmf_context* c, const float* xhat, const float* xcheck,
+                                   const float* left, const float* right, uint64_t d,
+                                   uint64_t n, uint64_t q, uint64_t k, float* a, float* b,
+                                   double* a_hat, double* b_check, int normalize_a, double alpha,
+                                   double beta, uint64_t rng_seed, uint64_t steps,
+                                   uint64_t* redraws) {
+  return guarded(c, [&] {
+    require_shapes(k, q);
+    if (k == 0 || q == 0 || d == 0 || n == 0) throw Fail(CNMF_ERR_DIMENSION, "empty operand");
+    const int lp = pad16((int)q);
+    HalsRun hr = make_hals(c, (int64_t)d, (int64_t)n, (int)q, lp, (int)k);
+    HalsState& st = hr.st;
+    float* lm = padded(c, "st_L", left, (int64_t)d, (int)q, lp);
+    float* rtu = c->ws<float>("st_Rt_u", n * q);
+    launch_transpose(right, (int64_t)q, (int64_t)n, (int64_t)n, rtu, (int64_t)q, c->stream);
+    float* rt = padded(c, "st_Rt", rtu, (int64_t)n, (int)q, lp);
+    float* xhtu = c->ws<float>("st_XhT_u", n * q);
+    launch_transpose(xhat, (int64_t)q, (int64_t)n, (int64_t)n, xhtu, (int64_t)q, c->stream);
+    float* xht = padded(c, "st_XhT", xhtu, (int64_t)n, (int)q, lp);
+    float* xc = padded(c, "st_Xc", xcheck, (int64_t)d, (int)q, lp);
+    st.lm = lm;
+    st.rt = rt;
+    st.xht = xht;
+    st.xc = xc;
+    launch_rm_to_cm(a, (int64_t)d, (int)k, st.a, c->stream);
+    launch_rm_to_cm(b, (int64_t)n, (int)k, st.b, c->stream);
+    CK(cudaMemcpyAsync(st.ahat, a_hat, sizeof(double) * q * k, cudaMemcpyDeviceToDevice, c->stream));
+    CK(cudaMemcpyAsync(st.bchk, b_check, sizeof(double) * q * k, cudaMemcpyDeviceToDevice,
+                       c->stream));
+    CK(cudaGetLastError());
+    std::mt19937_64 rng(rng_seed);
+    double secs = 0.0;
+    uint64_t nr = 0;
+    run_hals(c, hr, normalize_a, alpha, beta, 0, (int64_t)steps,
+             [&]() -> std::mt19937_64& { return rng; }, &secs, &nr);
+    launch_cm_to_rm(st.a, (int64_t)d, (int)k, a, c->stream);
+    launch_cm_to_rm(st.b, (int64_t)n, (int)k, b, c->stream);
+    CK(cudaMemcpyAsync(a_hat, st.ahat, sizeof(double) * q * k, cudaMemcpyDeviceToDevice, c->stream));
+    CK(cudaMemcpyAsync(b_check, st.bchk, sizeof(double) * q * k, cudaMemcpyDeviceToDevice,
+                       c->stream));
+    CK(cudaGetLastError());
+    c->sync();
+    if (redraws) *redraws = nr;
+  });
+}
+
+cnmf_status cnmf_reconstruction_error(cnmf_context* c, const float* x, uint64_t d, uint64_t n,
+                                      uint64_t ldx, const float* a, const float* b, uint64_t k,
+                                      double* out) {
+  return guarded(c, [&] {
+    if (k == 0 || k > 128) throw Fail(CNMF_ERR_UNSUPPORTED, "k must be in [1, 128]");
+    const XView X = prepare_x(c, x, (int64_t)d, (int64_t)n, (int64_t)ldx);
+    float* acm = c->ws<float>("re_acm", d * k);
+    float* bcm = c->ws<float>("re_bcm", n * k);
+    launch_rm_to_cm(a, (int64_t)d, (int)k, acm, c->stream);
+    launch_rm_to_cm(b, (int64_t)n, (int)k, bcm, c->stream);
+    *out = recon_error(c, X, acm, bcm, (int)k);
+  });
+}
+
+cnmf_status cnmf_thin_qr(cnmf_context* c, const float* y, uint64_t rows, uint64_t l,
+                         float* q_out) {
+  return guarded(c, [&] {
+    if (rows < l)
+      throw Fail(CNMF_ERR_DIMENSION, "thin_qr: input must have at least as many rows as columns");
+    require_shapes(1, l);
+    const int lp = pad16((int)l);
+    float* yp = padded(c, "tq_y", y, (int64_t)rows, (int)l, lp);
+    float* qp = c->ws<float>("tq_q", rows * lp);
+    void* qws = c->ws<char>("tq_ws", qr_ws_bytes((int64_t)rows, lp, c->nsm));
+    launch_thin_qr(yp, (int64_t)rows, (int)l, lp, qp, qws, c->nsm, c->stream);
+    launch_unpad_cols(qp, (int64_t)rows, lp, q_out, (int)l, c->stream);
+    CK(cudaGetLastError());
+    c->sync();
+  });
+}
+
+cnmf_status cnmf_xs_nn(cnmf_context* c, const float* x, uint64_t d, uint64_t n, uint64_t ldx,
+                       const float* s, uint64_t l, float* y) {
+  return guarded(c, [&] {
+    require_shapes(1, l);
+    const int lp = pad16((int)l);
+    const XView X = prepare_x(c, x, (int64_t)d, (int64_t)n, (int64_t)ldx);
+    float* sp = padded(c, "xs_s", s, (int64_t)n, (int)l, lp);
+    float* yp = c->ws<float>("xs_y", d * lp);
+    float* ws = c->ws<float>("xs_ws", xstream_ws_floats((int64_t)d, (int64_t)n, lp, c->nsm));
+    launch_xs_nn(X.x, X.ldx, X.d, X.n, sp, lp, yp, ws, c->nsm, c->stream);
+    launch_unpad_cols(yp, (int64_t)d, lp, y, (int)l, c->stream);
+    CK(cudaGetLastError());
+    c->sync();
+  });
+}
+
+cnmf_status cnmf_xs_tn(cnmf_context* c, const float* x, uint64_t d, uint64_t n, uint64_t ldx,
+                       const float* t, uint64_t l, float* z) {
+  return guarded(c, [&] {
+    require_shapes(1, l);
+    const int lp = pad16((int)l);
+    const XView X = prepare_x(c, x, (int64_t)d, (int64_t)n, (int64_t)ldx);
+    float* tp = padded(c, "xs_t", t, (int64_t)d, (int)l, lp);
+    float* zp = c->ws<float>("xs_z", n * lp);
+    float* ws = c->ws<float>("xs_ws", xstream_ws_floats((int64_t)d, (int64_t)n, lp, c->nsm));
+    launch_xs_tn(X.x, X.ldx, X.d, X.n, tp, lp, zp, ws, c->nsm, c->stream);
+    launch_unpad_cols(zp, (int64_t)n, lp, z, (int)l, c->stream);
+    CK(cudaGetLastError());
+    c->sync();
+  });
+}
+
+cnmf_status cnmf_synth_x(cnmf_context* c, uint64_t d, uint64_t n, uint64_t rank, int factor_kind,
+                         int noise_kind, double sigma, uint64_t seed, uint64_t col_lo,
+                         uint64_t col_hi, uint64_t ldx, float* x) {
+  return guarded(c, [&] {
+    if (col_hi <= col_lo || col_hi > n || ldx < col_hi - col_lo)
+      throw Fail(CNMF_ERR_DIMENSION, "bad column range");
+    double* scratch = c->ws<double>(
+        "synth", synth_scratch_doubles((int64_t)d, (int64_t)(col_hi - col_lo), (int)rank));
+    launch_synth_x((int64_t)d, (int64_t)n, (int)rank, factor_kind, noise_kind, sigma, seed,
+                   (int64_t)col_lo, (int64_t)col_hi, (int64_t)ldx, x, scratch, c->stream);
+    CK(cudaGetLastError());
+    c->sync();
+  });
+}
+
+}  // extern "C"

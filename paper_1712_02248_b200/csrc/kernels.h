@@ -1,0 +1,135 @@
+// kernels.h -- host-side launchers for the cnmf-b200 device kernels.
+// Internal to the library (the public C ABI is include/cnmf_b200.h).
+#pragma once
+
+#include <cuda_runtime.h>
+#ifndef __CUDACC__
+#ifndef __host__
+#define __host__
+#define __device__
+#endif
+#endif
+#include <stdint.h>
+
+#include <algorithm>
+
+namespace cnmf {
+
+// Widths of every "l-wide" operand (sketches, bases, compressed views) are
+// padded to a multiple of 16 columns; padding columns hold zeros.
+__host__ __device__ inline int pad16(int l) { return (l + 15) & ~15; }
+
+// ---- rng.cu -------------------------------------------------------------
+struct MtJob {
+  uint64_t seed;
+  uint64_t nwords;
+  uint64_t* out;
+};
+struct MtJobs {
+  MtJob job[4];
+};
+void launch_mt_streams(const MtJobs& jobs, int njobs, cudaStream_t s);
+void launch_normal_map(const uint64_t* words, uint64_t count, int cols, int ld, float* out,
+                       int* flag, int nsm, cudaStream_t s);
+void launch_normal_exact(const uint64_t* words, uint64_t nwords, uint64_t count, int cols, int ld,
+                         float* out, int* flag, cudaStream_t s);
+void launch_uniform_init(const uint64_t* words, uint64_t d, uint64_t n, int k, float* a_cm,
+                         float* b_cm, int* flag, int nsm, cudaStream_t s);
+void launch_uniform_init_exact(const uint64_t* words, uint64_t nwords, uint64_t d, uint64_t n,
+                               int k, float* a_cm, float* b_cm, int* flag, uint64_t* consumed,
+                               cudaStream_t s);
+
+// ---- xstream.cu: the X-streaming contractions ----------------------------
+// Y (m x lp, ld lp) = X (m x n, ld ldx) * S (n x lp, ld lp)          ["NN"]
+// Z (n x lp, ld lp) = X^T * T (m x lp, ld lp)                         ["TN"]
+// lp is a multiple of 16 in [16, 128].  `ws` is scratch for split-K partials
+// (xstream_ws_floats() floats).  Deterministic: fixed-order split reduction.
+size_t xstream_ws_floats(int64_t m, int64_t n, int lp, int nsm);
+void launch_xs_nn(const float* x, int64_t ldx, int64_t m, int64_t n, const float* s, int lp,
+                  float* y, float* ws, int nsm, cudaStream_t st);
+void launch_xs_tn(const float* x, int64_t ldx, int64_t m, int64_t n, const float* t, int lp,
+                  float* z, float* ws, int nsm, cudaStream_t st);
+
+// ---- qr.cu: orthonormal basis with the span of Y --------------------------
+// CholeskyQR2 with fp64 Grams; Householder (reference qr.cpp semantics, fp64)
+// when the Cholesky factor is numerically singular.  Y and Q are rows x lp
+// (ld lp); columns >= l are zero on output.  q must not alias y.
+size_t qr_ws_bytes(int64_t rows, int lp, int nsm);
+void launch_thin_qr(const float* y, int64_t rows, int l, int lp, float* q, void* ws, int nsm,
+                    cudaStream_t st);
+
+// ---- metrics.cu ------------------------------------------------------------
+// check_data: flags[0] |= negative/non-finite; *norm_sq = ||X||_F^2 (fp64).
+size_t metrics_ws_bytes(int64_t d, int64_t n, int nsm);
+void launch_check_data(const float* x, int64_t ldx, int64_t d, int64_t n, int* flag,
+                       double* norm_sq, void* ws, int nsm, cudaStream_t st);
+// 1/2 ||X - A B^T||^2 with column-major A_cm (k x d), B_cm (k x n).
+void launch_recon_error(const float* x, int64_t ldx, int64_t d, int64_t n, const float* a_cm,
+                        const float* b_cm, int k, double* out, void* ws, int nsm,
+                        cudaStream_t st);
+size_t gini_ws_bytes(int64_t count);
+void launch_gini(const float* b_cm, int64_t count, double* out, void* ws, size_t ws_bytes,
+                 cudaStream_t st);
+// column-major (k x rows) -> row-major (rows x k), fp32
+void launch_cm_to_rm(const float* cm, int64_t rows, int k, float* rm, cudaStream_t st);
+void launch_rm_to_cm(const float* rm, int64_t rows, int k, float* cm, cudaStream_t st);
+// Copy an unpadded row-major (rows x l) matrix into an lp-padded one and back.
+void launch_pad_cols(const float* src, int64_t rows, int l, float* dst, int lp, cudaStream_t st);
+void launch_unpad_cols(const float* src, int64_t rows, int lp, float* dst, int l,
+                       cudaStream_t st);
+void launch_transpose(const float* src, int64_t rows, int64_t cols, int64_t lds, float* dst,
+                      int64_t ldd, cudaStream_t st);
+
+// ---- hals.cu: FastHALS-RP iterations ---------------------------------------
+struct HaltInfo {
+  int halted;  // 0 = ran to it_end
+  int iter;    // iteration (1-based) in which the event happened
+  int half;    // 0 = A half-sweep, 1 = B half-sweep
+  int column;
+  int kind;    // 1 dead B column (g_jj), 2 zero A column, 3 dead A column (w_jj), 4 zero B column
+  int pad[3];
+};
+enum { kEvDeadB = 1, kEvZeroA = 2, kEvDeadA = 3, kEvZeroB = 4 };
+
+struct HalsState {
+  int64_t d, n;
+  int l, lp, k;
+  const float* xc;   // X-check = X R^T, d x lp
+  const float* xht;  // X-hat^T = X^T L, n x lp
+  const float* lm;   // L, d x lp
+  const float* rt;   // R^T, n x lp
+  float* a;          // A, column-major k x d
+  float* b;          // B, column-major k x n
+  float* bold;       // B backup for the zero-column rollback, k x n
+  float* h;          // X-check B-check, column-major k x d
+  double* ahat;      // A-hat = L^T A, lp x k
+  double* bchk;      // B-check = R B, lp x k
+  double* g;         // B-check^T B-check, k x k
+  double* w;         // A-hat^T A-hat, k x k
+  double* part;      // [grid][lp*k] partial sums
+  double* npart;     // [k][grid] column-norm partials
+  int* zflag;        // [grid][k] non-zero-column flags
+  unsigned* bar;     // grid barrier (2 words)
+  HaltInfo* halt;
+};
+size_t hals_part_doubles(int grid, int lp, int k);
+int hals_grid(const HalsState& st, int nsm);
+// Runs iterations [it_begin, it_end) starting at (start_half, start_col).
+// Returns the cooperative-launch error, if any.
+// it_begin/it_end are 0-based; HaltInfo::iter reports the 1-based iteration.
+cudaError_t launch_hals(const HalsState& st, int normalize_a, double alpha, double beta,
+                        int it_begin, int it_end, int start_half, int start_col, int skip_dead,
+                        int grid, cudaStream_t s);
+// A-hat = L^T A and B-check = R B (all columns, or only column j >= 0).
+void launch_compress_factors(const HalsState& st, int which /*0 A-hat, 1 B-check*/, int column,
+                             cudaStream_t s);
+// a_j <- a_j / ||a_j|| (no-op on a zero column), fixed-order fp64 norm.
+void launch_normalize_column(float* a_cm, int64_t d, int j, cudaStream_t s);
+
+// ---- synth.cu: synthetic data (bench harness, BASELINE.json configs) ------
+void launch_synth_x(int64_t d, int64_t n, int rank, int factor_kind, int noise_kind, double sigma,
+                    uint64_t seed, int64_t col_lo, int64_t col_hi, int64_t ldx, float* x,
+                    double* scratch, cudaStream_t s);
+size_t synth_scratch_doubles(int64_t d, int64_t ncols, int rank);
+
+}  // namespace cnmf

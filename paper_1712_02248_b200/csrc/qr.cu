@@ -1,0 +1,304 @@
+// qr.cu -- orthonormal bases for the range finders.
+//
+// Reference: thin_qr (proj/src/qr.cpp:10-75), Householder with a
+// rank-deficiency floor of 1e-12 ||M||_F, called after every application of X
+// or X^T in range_finder_impl (proj/src/compression.cpp:32-40).  Only the
+// SPAN of Q enters FastHALS-RP (the step depends on L L^T and R^T R only,
+// solvers.cpp:421-443), so the device uses CholeskyQR2:
+//   G1 = Y^T Y (fp64) -> R1 = chol(G1) -> Q1 = Y R1^-1 -> G2 = Q1^T Q1 -> Q = Q1 R2^-1.
+// The first Gram must be fp64 (cond(Y) reaches ~1e5, so cond(G1) ~ 1e10).
+// When a Cholesky pivot shows Y numerically rank deficient, a single-CTA
+// fp64 Householder QR with the reference's floor and completion rule
+// replaces the result (rare path: exactly low-rank test data).
+#include "common.cuh"
+#include "kernels.h"
+
+namespace cnmf {
+
+namespace {
+
+constexpr int kGramRows = 64;
+
+struct QrWs {
+  double* part;    // [grid][lp*lp]
+  double* g;       // lp x lp
+  double* rinv64;  // lp x lp
+  float* rinv;     // lp x lp
+  float* q1;       // rows x lp
+  int* flag;
+  double* hw;      // rows x lp (Householder working copy / Q)
+  double* hv;      // rows x lp (reflectors)
+  float* xs_ws;    // split-K scratch for the apply step
+};
+
+int gram_grid(int64_t rows, int nsm) {
+  return (int)std::max<int64_t>(1, std::min<int64_t>(nsm, (rows + kGramRows - 1) / kGramRows));
+}
+
+QrWs carve(void* ws, int64_t rows, int lp, int nsm) {
+  QrWs w;
+  char* p = static_cast<char*>(ws);
+  auto take = [&](size_t bytes) {
+    char* r = p;
+    p += (bytes + 255) & ~size_t(255);
+    return r;
+  };
+  const int grid = gram_grid(rows, nsm);
+  w.part = (double*)take(sizeof(double) * grid * lp * lp);
+  w.g = (double*)take(sizeof(double) * lp * lp);
+  w.rinv64 = (double*)take(sizeof(double) * lp * lp);
+  w.rinv = (float*)take(sizeof(float) * lp * lp);
+  w.q1 = (float*)take(sizeof(float) * rows * lp);
+  w.flag = (int*)take(sizeof(int) * 4);
+  w.hw = (double*)take(sizeof(double) * rows * lp);
+  w.hv = (double*)take(sizeof(double) * rows * lp);
+  w.xs_ws = (float*)take(sizeof(float) * xstream_ws_floats(rows, lp, lp, nsm));
+  return w;
+}
+
+// Per-CTA fp64 partial of Y^T Y over its row chunks; upper-triangle 4x4
+// blocks, thread t owns blocks t, t+256, t+512.
+__global__ void __launch_bounds__(256) gram_kernel(const float* __restrict__ y, int64_t rows,
+                                                   int l, int lp, double* __restrict__ part) {
+  extern __shared__ __align__(16) float ys[];  // kGramRows x (lp + 4)
+  const int lps = lp + 4;
+  const int nbl = (l + 3) >> 2, nb = nbl * (nbl + 1) / 2;
+  int bi[3], bj[3];
+#pragma unroll
+  for (int t = 0; t < 3; ++t) {
+    int b = threadIdx.x + 256 * t;
+    bi[t] = -1;
+    bj[t] = -1;
+    if (b < nb) {
+      int i = 0;
+      while (b >= nbl - i) {
+        b -= nbl - i;
+        ++i;
+      }
+      bi[t] = i;
+      bj[t] = i + b;
+    }
+  }
+  double acc[3][16];
+#pragma unroll
+  for (int t = 0; t < 3; ++t)
+#pragma unroll
+    for (int e = 0; e < 16; ++e) acc[t][e] = 0.0;
+  const int64_t nchunks = (rows + kGramRows - 1) / kGramRows;
+  for (int64_t ch = blockIdx.x; ch < nchunks; ch += gridDim.x) {
+    const int64_t r0 = ch * kGramRows;
+    const int nr = (int)((rows - r0) < kGramRows ? (rows - r0) : kGramRows);
+    __syncthreads();
+    for (int e = threadIdx.x; e < kGramRows * (lp / 4); e += 256) {
+      const int r = e / (lp / 4), c4 = e - r * (lp / 4);
+      float4 v = make_float4(0.f, 0.f, 0.f, 0.f);
+      if (r < nr) v = *reinterpret_cast<const float4*>(y + (r0 + r) * lp + 4 * c4);
+      *reinterpret_cast<float4*>(ys + r * lps + 4 * c4) = v;
+    }
+    __syncthreads();
+#pragma unroll
+    for (int t = 0; t < 3; ++t) {
+      if (bi[t] < 0) continue;
+      for (int r = 0; r < nr; ++r) {
+        const float4 a = *reinterpret_cast<const float4*>(ys + r * lps + 4 * bi[t]);
+        const float4 b = *reinterpret_cast<const float4*>(ys + r * lps + 4 * bj[t]);
+        const double av[4] = {a.x, a.y, a.z, a.w}, bv[4] = {b.x, b.y, b.z, b.w};
+#pragma unroll
+        for (int i = 0; i < 4; ++i)
+#pragma unroll
+          for (int j = 0; j < 4; ++j) acc[t][4 * i + j] = fma(av[i], bv[j], acc[t][4 * i + j]);
+      }
+    }
+  }
+  double* dst = part + (int64_t)blockIdx.x * lp * lp;
+#pragma unroll
+  for (int t = 0; t < 3; ++t) {
+    if (bi[t] < 0) continue;
+#pragma unroll
+    for (int i = 0; i < 4; ++i)
+#pragma unroll
+      for (int j = 0; j < 4; ++j) dst[(4 * bi[t] + i) * lp + 4 * bj[t] + j] = acc[t][4 * i + j];
+  }
+}
+
+// G[a][b] (a <= b < l) = fixed-order sum of partials; mirrored; zero outside.
+__global__ void gram_reduce_kernel(const double* __restrict__ part, int grid, int l, int lp,
+                                   double* __restrict__ g) {
+  for (int e = blockIdx.x * blockDim.x + threadIdx.x; e < lp * lp; e += gridDim.x * blockDim.x) {
+    const int a = e / lp, b = e - a * lp;
+    double s = 0.0;
+    if (a < l && b < l) {
+      const int lo = min(a, b), hi = max(a, b);
+      for (int c = 0; c < grid; ++c) s += part[(int64_t)c * lp * lp + lo * lp + hi];
+    }
+    g[e] = s;
+  }
+}
+
+// Upper Cholesky G = R^T R and R^-1, one CTA.  flag |= 1 when a pivot is
+// non-positive or below 1e-13 of its original diagonal (Y numerically rank
+// deficient at fp32 resolution).
+__global__ void __launch_bounds__(256) chol_inv_kernel(const double* __restrict__ g, int l, int lp,
+                                                       double* __restrict__ rinv64,
+                                                       float* __restrict__ rinv,
+                                                       int* __restrict__ flag) {
+  extern __shared__ double gs[];  // l x l, then diag0[l]
+  double* diag0 = gs + l * l;
+  __shared__ int fail;
+  const int tid = threadIdx.x;
+  for (int e = tid; e < l * l; e += blockDim.x) gs[e] = g[(e / l) * lp + e % l];
+  for (int e = tid; e < l; e += blockDim.x) diag0[e] = g[e * lp + e];
+  for (int e = tid; e < lp * lp; e += blockDim.x) rinv[e] = 0.f;
+  if (tid == 0) fail = 0;
+  __syncthreads();
+  for (int j = 0; j < l; ++j) {
+    if (tid == 0) {
+      const double piv = gs[j * l + j];
+      if (!(piv > 1e-13 * diag0[j]) || !(piv > 0.0))
+        fail = 1;
+      else
+        gs[j * l + j] = sqrt(piv);
+    }
+    __syncthreads();
+    if (fail) break;
+    const double r = gs[j * l + j];
+    for (int c = j + 1 + tid; c < l; c += blockDim.x) gs[j * l + c] /= r;
+    __syncthreads();
+    const int m = l - j - 1;
+    for (int e = tid; e < m * m; e += blockDim.x) {
+      const int a = j + 1 + e / m, b = j + 1 + e % m;
+      if (a <= b) gs[a * l + b] -= gs[j * l + a] * gs[j * l + b];
+    }
+    __syncthreads();
+  }
+  if (fail) {
+    if (tid == 0) *flag = 1;
+    return;
+  }
+  // R^-1 column c by backward substitution (fp64), thread per column.
+  for (int c = tid; c < l; c += blockDim.x) {
+    double* x = rinv64 + (int64_t)c * lp;  // column c stored contiguously
+    x[c] = 1.0 / gs[c * l + c];
+    for (int i = c - 1; i >= 0; --i) {
+      double s = 0.0;
+      for (int q = i + 1; q <= c; ++q) s += gs[i * l + q] * x[q];
+      x[i] = -s / gs[i * l + i];
+    }
+    for (int i = 0; i <= c; ++i) rinv[i * lp + c] = (float)x[i];
+  }
+}
+
+// Householder QR with the reference's semantics (qr.cpp:10-75), fp64, one
+// CTA; runs only when the Cholesky path flagged the input.
+__global__ void __launch_bounds__(1024) householder_kernel(const float* __restrict__ y,
+                                                           int64_t rows, int l, int lp,
+                                                           double* __restrict__ w,
+                                                           double* __restrict__ v,
+                                                           float* __restrict__ q,
+                                                           const int* __restrict__ flag) {
+  if (*flag == 0) return;
+  __shared__ double red[32];
+  __shared__ unsigned char skip[128];
+  const int tid = threadIdx.x, nt = blockDim.x;
+  double s = 0.0;
+  for (int64_t e = tid; e < rows * l; e += nt) {
+    const double t = y[(e / l) * lp + e % l];
+    w[e] = t;
+    v[e] = 0.0;
+    s += t * t;
+  }
+  const double floor_ = 1e-12 * sqrt(block_sum(s, red));
+  for (int j = 0; j < l; ++j) {
+    s = 0.0;
+    for (int64_t i = j + tid; i < rows; i += nt) s += w[i * l + j] * w[i * l + j];
+    const double normx = sqrt(block_sum(s, red));
+    if (normx < floor_) {
+      for (int64_t i = j + tid; i < rows; i += nt) w[i * l + j] = 0.0;
+      if (tid == 0) skip[j] = 1;
+      __syncthreads();
+      continue;
+    }
+    if (tid == 0) skip[j] = 0;
+    const double wjj = w[(int64_t)j * l + j];
+    const double alpha = wjj >= 0.0 ? -normx : normx;
+    s = 0.0;
+    for (int64_t i = j + tid; i < rows; i += nt) {
+      const double t = w[i * l + j] - (i == j ? alpha : 0.0);
+      v[i * l + j] = t;
+      s += t * t;
+    }
+    const double vn = sqrt(block_sum(s, red));
+    for (int64_t i = j + tid; i < rows; i += nt) v[i * l + j] /= vn;
+    __syncthreads();
+    for (int c = j; c < l; ++c) {
+      s = 0.0;
+      for (int64_t i = j + tid; i < rows; i += nt) s += v[i * l + j] * w[i * l + c];
+      const double proj = 2.0 * block_sum(s, red);
+      for (int64_t i = j + tid; i < rows; i += nt) w[i * l + c] -= proj * v[i * l + j];
+      __syncthreads();
+    }
+  }
+  // Q = H_0 ... H_{l-1} applied to the identity slice (reverse order).
+  for (int64_t e = tid; e < rows * l; e += nt) w[e] = ((e / l) == (e % l)) ? 1.0 : 0.0;
+  __syncthreads();
+  for (int jj = l - 1; jj >= 0; --jj) {
+    if (skip[jj]) continue;
+    for (int c = 0; c < l; ++c) {
+      s = 0.0;
+      for (int64_t i = jj + tid; i < rows; i += nt) s += v[i * l + jj] * w[i * l + c];
+      const double proj = 2.0 * block_sum(s, red);
+      for (int64_t i = jj + tid; i < rows; i += nt) w[i * l + c] -= proj * v[i * l + jj];
+      __syncthreads();
+    }
+  }
+  for (int64_t e = tid; e < rows * lp; e += nt) {
+    const int64_t r = e / lp;
+    const int c = (int)(e % lp);
+    q[e] = c < l ? (float)w[r * l + c] : 0.f;
+  }
+}
+
+void gram(const float* y, int64_t rows, int l, int lp, const QrWs& w, int nsm,
+          cudaStream_t st) {
+  const int grid = gram_grid(rows, nsm);
+  const size_t smem = sizeof(float) * kGramRows * (lp + 4);
+  gram_kernel<<<grid, 256, smem, st>>>(y, rows, l, lp, w.part);
+  gram_reduce_kernel<<<(lp * lp + 255) / 256, 256, 0, st>>>(w.part, grid, l, lp, w.g);
+}
+
+void chol_inv(int l, int lp, const QrWs& w, cudaStream_t st) {
+  const size_t smem = sizeof(double) * (l * l + l);
+  static bool attr = false;
+  if (!attr) {
+    cudaFuncSetAttribute(chol_inv_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         (int)(sizeof(double) * (128 * 128 + 128)));
+    attr = true;
+  }
+  chol_inv_kernel<<<1, 256, smem, st>>>(w.g, l, lp, w.rinv64, w.rinv, w.flag);
+}
+
+}  // namespace
+
+size_t qr_ws_bytes(int64_t rows, int lp, int nsm) {
+  const int grid = gram_grid(rows, nsm);
+  auto r = [](size_t b) { return (b + 255) & ~size_t(255); };
+  return r(sizeof(double) * grid * lp * lp) + 2 * r(sizeof(double) * lp * lp) +
+         r(sizeof(float) * lp * lp) + r(sizeof(float) * rows * lp) + r(16) +
+         2 * r(sizeof(double) * rows * lp) + r(sizeof(float) * xstream_ws_floats(rows, lp, lp, nsm)) +
+         1024;
+}
+
+void launch_thin_qr(const float* y, int64_t rows, int l, int lp, float* q, void* ws, int nsm,
+                    cudaStream_t st) {
+  const QrWs w = carve(ws, rows, lp, nsm);
+  cudaMemsetAsync(w.flag, 0, sizeof(int), st);
+  gram(y, rows, l, lp, w, nsm, st);
+  chol_inv(l, lp, w, st);
+  launch_xs_nn(y, lp, rows, lp, w.rinv, lp, w.q1, w.xs_ws, nsm, st);
+  gram(w.q1, rows, l, lp, w, nsm, st);
+  chol_inv(l, lp, w, st);
+  launch_xs_nn(w.q1, lp, rows, lp, w.rinv, lp, q, w.xs_ws, nsm, st);
+  householder_kernel<<<1, 1024, 0, st>>>(y, rows, l, lp, w.hw, w.hv, q, w.flag);
+}
+
+}  // namespace cnmf

@@ -1,0 +1,196 @@
+// rng.cu -- the reference's seeded variate streams, generated on the device.
+//
+// Reference: cnmf::Rng (proj/include/cnmf/rng.hpp:13-60) = std::mt19937_64
+// plus fixed mappings:  uniform = (u64 >> 11) * 2^-53;  uniform_positive
+// rejects exact 0;  normal = Box-Muller (cos first, sin cached as spare).
+// gaussian_sketch (proj/src/compression.cpp:11-16) fills row-major from a
+// fresh Rng(seed); initialize (proj/src/solvers.cpp:206-211, 314-325) fills A
+// then B row-major with uniform_positive.
+//
+// MT19937-64 is sequential, so one CTA owns one engine and emits its raw
+// 64-bit stream 312 words per twist (156 threads, two words each).  The
+// mapping kernels are then fully parallel: normal e uses words 2*(e/2) and
+// 2*(e/2)+1 and uniform e uses word e, EXCEPT after a word whose 53-bit
+// uniform is exactly 0 (probability 2^-53 per draw), where the reference
+// rejects and re-draws.  The fast mappings detect that case and set a flag;
+// the host then re-runs the exact sequential mapping (single thread) so the
+// stream stays identical to the reference in every case.
+#include "common.cuh"
+#include "kernels.h"
+
+namespace cnmf {
+
+namespace {
+
+constexpr int kN = 312, kM = 156;
+constexpr uint64_t kUM = 0xFFFFFFFF80000000ULL, kLM = 0x7FFFFFFFULL;
+constexpr uint64_t kMatA = 0xB5026F5AA96619E9ULL;
+
+__device__ __forceinline__ uint64_t mix(uint64_t a, uint64_t b) {
+  const uint64_t y = (a & kUM) | (b & kLM);
+  return (y >> 1) ^ ((y & 1ULL) ? kMatA : 0ULL);
+}
+__device__ __forceinline__ uint64_t temper(uint64_t z) {
+  z ^= (z >> 29) & 0x5555555555555555ULL;
+  z ^= (z << 17) & 0x71D67FFFEDA60000ULL;
+  z ^= (z << 37) & 0xFFF7EEE000000000ULL;
+  z ^= z >> 43;
+  return z;
+}
+
+// One CTA per engine; blockDim.x == 160 (156 active in the twist).
+__global__ void __launch_bounds__(160) mt_stream_kernel(MtJobs jobs) {
+  const MtJob job = jobs.job[blockIdx.x];
+  __shared__ uint64_t mt[kN];
+  const int t = threadIdx.x;
+  if (t == 0) {
+    mt[0] = job.seed;
+    for (int i = 1; i < kN; ++i)
+      mt[i] = 6364136223846793005ULL * (mt[i - 1] ^ (mt[i - 1] >> 62)) + (uint64_t)i;
+  }
+  __syncthreads();
+  const uint64_t nblocks = (job.nwords + kN - 1) / kN;
+  for (uint64_t blk = 0; blk < nblocks; ++blk) {
+    uint64_t o0 = 0, o1 = 0, o156 = 0, o157 = 0, o311 = 0;
+    if (t < kM) {
+      o0 = mt[t];
+      o1 = mt[t + 1];
+      o156 = mt[t + kM];
+      if (t + kM + 1 < kN) o157 = mt[t + kM + 1];
+      if (t == 0) o311 = mt[kN - 1];
+    }
+    __syncthreads();
+    if (t < kM) {
+      const uint64_t nt = o156 ^ mix(o0, o1);  // i = t       (uses old values)
+      mt[t] = nt;
+      if (t + kM < kN - 1) mt[t + kM] = nt ^ mix(o156, o157);  // i = t+156 (new mt[i-156])
+    }
+    __syncthreads();
+    if (t == 0) mt[kN - 1] = mt[kM - 1] ^ mix(o311, mt[0]);  // i = 311 (new mt[0], mt[155])
+    __syncthreads();
+    if (t < kM) {
+      const uint64_t base = blk * kN;
+      if (base + t < job.nwords) job.out[base + t] = temper(mt[t]);
+      if (base + t + kM < job.nwords) job.out[base + t + kM] = temper(mt[t + kM]);
+    }
+    // next iteration's reads happen after its first __syncthreads
+    __syncthreads();
+  }
+}
+
+__device__ __forceinline__ double u53(uint64_t w) { return (double)(w >> 11) * 0x1.0p-53; }
+
+// normal e -> out[(e / cols) * ld + e % cols]
+__global__ void normal_map_kernel(const uint64_t* __restrict__ words, uint64_t count, int cols,
+                                  int ld, float* __restrict__ out, int* __restrict__ flag) {
+  const uint64_t npairs = (count + 1) / 2;
+  for (uint64_t p = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; p < npairs;
+       p += (uint64_t)gridDim.x * blockDim.x) {
+    const double u1 = u53(words[2 * p]);
+    const double u2 = u53(words[2 * p + 1]);
+    if (u1 == 0.0) *flag = 1;
+    const double radius = sqrt(-2.0 * log(u1));
+    const double angle = 2.0 * 3.141592653589793238462643383279502884 * u2;
+    double s, c;
+    sincos(angle, &s, &c);
+    const uint64_t e0 = 2 * p, e1 = 2 * p + 1;
+    out[(e0 / cols) * ld + e0 % cols] = (float)(radius * c);
+    if (e1 < count) out[(e1 / cols) * ld + e1 % cols] = (float)(radius * s);
+  }
+}
+
+// Exact sequential Box-Muller over the stream (zero-rejection path).
+__global__ void normal_exact_kernel(const uint64_t* __restrict__ words, uint64_t nwords,
+                                    uint64_t count, int cols, int ld, float* __restrict__ out,
+                                    int* __restrict__ flag) {
+  if (threadIdx.x != 0 || blockIdx.x != 0 || *flag == 0) return;
+  uint64_t pos = 0;
+  for (uint64_t e = 0; e < count; e += 2) {
+    double u1 = 0.0;
+    while (u1 == 0.0) {
+      if (pos >= nwords) { *flag = 2; return; }
+      u1 = u53(words[pos++]);
+    }
+    if (pos >= nwords) { *flag = 2; return; }
+    const double u2 = u53(words[pos++]);
+    const double radius = sqrt(-2.0 * log(u1));
+    const double angle = 2.0 * 3.141592653589793238462643383279502884 * u2;
+    double s, c;
+    sincos(angle, &s, &c);
+    out[(e / cols) * ld + e % cols] = (float)(radius * c);
+    if (e + 1 < count) out[((e + 1) / cols) * ld + (e + 1) % cols] = (float)(radius * s);
+  }
+  *flag = 3;  // served by the exact path
+}
+
+// uniform_positive e (A then B, both row-major d x k / n x k in the
+// reference) -> column-major device factors A_cm[c*d + i], B_cm[c*n + i].
+__global__ void uniform_init_kernel(const uint64_t* __restrict__ words, uint64_t d, uint64_t n,
+                                    int k, float* __restrict__ a_cm, float* __restrict__ b_cm,
+                                    int* __restrict__ flag) {
+  const uint64_t na = d * k, total = (d + n) * k;
+  for (uint64_t e = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; e < total;
+       e += (uint64_t)gridDim.x * blockDim.x) {
+    const double u = u53(words[e]);
+    if (u == 0.0) *flag = 1;
+    if (e < na)
+      a_cm[(e % k) * d + e / k] = (float)u;
+    else
+      b_cm[((e - na) % k) * n + (e - na) / k] = (float)u;
+  }
+}
+
+__global__ void uniform_init_exact_kernel(const uint64_t* __restrict__ words, uint64_t nwords,
+                                          uint64_t d, uint64_t n, int k, float* __restrict__ a_cm,
+                                          float* __restrict__ b_cm, int* __restrict__ flag,
+                                          uint64_t* __restrict__ consumed) {
+  if (threadIdx.x != 0 || blockIdx.x != 0 || *flag == 0) return;
+  const uint64_t na = d * k, total = (d + n) * k;
+  uint64_t pos = 0;
+  for (uint64_t e = 0; e < total; ++e) {
+    double u = 0.0;
+    while (u == 0.0) {
+      if (pos >= nwords) { *flag = 2; return; }
+      u = u53(words[pos++]);
+    }
+    if (e < na)
+      a_cm[(e % k) * d + e / k] = (float)u;
+    else
+      b_cm[((e - na) % k) * n + (e - na) / k] = (float)u;
+  }
+  *consumed = pos;
+  *flag = 3;
+}
+
+}  // namespace
+
+void launch_mt_streams(const MtJobs& jobs, int njobs, cudaStream_t s) {
+  mt_stream_kernel<<<njobs, 160, 0, s>>>(jobs);
+}
+
+void launch_normal_map(const uint64_t* words, uint64_t count, int cols, int ld, float* out,
+                       int* flag, int nsm, cudaStream_t s) {
+  const uint64_t npairs = (count + 1) / 2;
+  const int blocks = (int)std::min<uint64_t>((npairs + 255) / 256, (uint64_t)nsm * 8);
+  normal_map_kernel<<<blocks > 0 ? blocks : 1, 256, 0, s>>>(words, count, cols, ld, out, flag);
+}
+
+void launch_normal_exact(const uint64_t* words, uint64_t nwords, uint64_t count, int cols, int ld,
+                         float* out, int* flag, cudaStream_t s) {
+  normal_exact_kernel<<<1, 32, 0, s>>>(words, nwords, count, cols, ld, out, flag);
+}
+
+void launch_uniform_init(const uint64_t* words, uint64_t d, uint64_t n, int k, float* a_cm,
+                         float* b_cm, int* flag, int nsm, cudaStream_t s) {
+  const uint64_t total = (d + n) * (uint64_t)k;
+  const int blocks = (int)std::min<uint64_t>((total + 255) / 256, (uint64_t)nsm * 8);
+  uniform_init_kernel<<<blocks > 0 ? blocks : 1, 256, 0, s>>>(words, d, n, k, a_cm, b_cm, flag);
+}
+
+void launch_uniform_init_exact(const uint64_t* words, uint64_t nwords, uint64_t d, uint64_t n,
+                               int k, float* a_cm, float* b_cm, int* flag, uint64_t* consumed,
+                               cudaStream_t s) {
+  uniform_init_exact_kernel<<<1, 32, 0, s>>>(words, nwords, d, n, k, a_cm, b_cm, flag, consumed);
+}
+
+}  // namespace cnmf

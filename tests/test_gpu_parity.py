@@ -1,0 +1,389 @@
+"""GPU parity: the CUDA path (through the C ABI) against the CPU oracle.
+
+Tolerances (north_star: per-iteration relative error within 1e-4 relative;
+factors within a stated elementwise tolerance):
+  * RNG streams: bit-exact for uniform_positive (no transcendentals), fp32
+    rounding + <= 2 ulp for Box-Muller normals (device log/sincos vs glibc).
+  * X contractions: fp32 accumulation, rel. Frobenius <= 1e-5.
+  * Projectors: only their spans matter; compare the
+    projections L L^T and R^T R, Frobenius <= 1e-4.
+  * Trajectories: relative error sqrt(2 err / ||X||^2) within 1e-4 relative
+    at every recorded iteration; final A, B: rel. Frobenius <= 1e-3 and
+    max |delta| <= 1e-3 max|ref|.
+"""
+import numpy as np
+import pytest
+
+torch = pytest.importorskip("torch")
+pytestmark = pytest.mark.gpu
+
+TRAJ_RTOL = 1e-4
+FACTOR_RTOL = 1e-3
+
+
+def dev(a):
+    return torch.from_numpy(np.ascontiguousarray(a, dtype=np.float32)).cuda()
+
+
+def dev64(a):
+    return torch.from_numpy(np.ascontiguousarray(a, dtype=np.float64)).cuda()
+
+
+def host(t):
+    return t.detach().cpu().numpy()
+
+
+def rel_fro(a, b):
+    a = np.asarray(a, dtype=np.float64)
+    b = np.asarray(b, dtype=np.float64)
+    return np.linalg.norm(a - b) / max(np.linalg.norm(b), 1e-300)
+
+
+def random_nonneg(oracle, d, n, seed):
+    """test_solvers.cpp:24-29: Rng(seed).uniform() row-major."""
+    return oracle.draws(seed, 1, d * n).reshape(d, n)
+
+
+def rel_err(err, xnorm):
+    return np.sqrt(2.0 * np.asarray(err) / xnorm)
+
+
+# ---------------------------------------------------------------- streams --
+def test_gaussian_sketch_stream(ctx, oracle):
+    for rows, cols, seed in [(7, 5, 11), (1000, 30, 2), (301, 37, 3)]:
+        out = torch.empty((rows, cols), device="cuda")
+        ctx.gaussian_sketch(rows, cols, seed, out)
+        ref = oracle.gaussian_sketch(rows, cols, seed).astype(np.float32)
+        got = host(out)
+        assert np.allclose(got, ref, rtol=3e-7, atol=1e-7), np.abs(got - ref).max()
+
+
+def test_initialize_stream_bit_exact(ctx, oracle):
+    for d, n, k, seed in [(4, 3, 2, 99), (1000, 700, 20, 1), (37, 53, 7, 5)]:
+        a = torch.empty((d, k), device="cuda")
+        b = torch.empty((n, k), device="cuda")
+        ctx.initialize(d, n, k, seed, a, b)
+        ra, rb = oracle.initialize(d, n, k, seed)
+        assert np.array_equal(host(a), ra.astype(np.float32))
+        assert np.array_equal(host(b), rb.astype(np.float32))
+
+
+# ----------------------------------------------------------- contractions --
+@pytest.mark.parametrize("d,n,l", [(1000, 1000, 30), (333, 517, 17), (64, 4096, 128),
+                                   (5000, 37, 8), (1, 9, 3)])
+def test_xstream_contractions(ctx, d, n, l):
+    rng = np.random.default_rng(d * 7 + n)
+    x = rng.random((d, n), dtype=np.float32)
+    s = rng.standard_normal((n, l)).astype(np.float32)
+    t = rng.standard_normal((d, l)).astype(np.float32)
+    y = torch.empty((d, l), device="cuda")
+    z = torch.empty((n, l), device="cuda")
+    ctx.xs_nn(dev(x), dev(s), y)
+    ctx.xs_tn(dev(x), dev(t), z)
+    x64 = x.astype(np.float64)
+    assert rel_fro(host(y), x64 @ s.astype(np.float64)) < 1e-5
+    assert rel_fro(host(z), x64.T @ t.astype(np.float64)) < 1e-5
+
+
+def test_xstream_ragged_leading_dimension(ctx):
+    rng = np.random.default_rng(5)
+    big = rng.random((200, 131), dtype=np.float32)
+    x = dev(big)[:, :127]  # ldx = 131 (not a multiple of 4): padded copy path
+    s = rng.standard_normal((127, 24)).astype(np.float32)
+    y = torch.empty((200, 24), device="cuda")
+    ctx.xs_nn(x, dev(s), y)
+    assert rel_fro(host(y), big[:, :127].astype(np.float64) @ s) < 1e-5
+
+
+def test_xstream_deterministic(ctx):
+    rng = np.random.default_rng(9)
+    x = dev(rng.random((3000, 2000), dtype=np.float32))
+    s = dev(rng.standard_normal((2000, 40)).astype(np.float32))
+    y1 = torch.empty((3000, 40), device="cuda")
+    y2 = torch.empty((3000, 40), device="cuda")
+    ctx.xs_nn(x, s, y1)
+    ctx.xs_nn(x, s, y2)
+    assert torch.equal(y1, y2)
+
+
+# --------------------------------------------------------------------- QR --
+@pytest.mark.parametrize("rows,l", [(20, 6), (1000, 30), (10000, 36), (5000, 128)])
+def test_thin_qr_orthonormal_same_span(ctx, rows, l):
+    rng = np.random.default_rng(rows + l)
+    # ill-conditioned on purpose: column scales over 4 decades
+    y = rng.standard_normal((rows, l)) * np.logspace(0, -4, l)[None, :]
+    q = torch.empty((rows, l), device="cuda")
+    ctx.thin_qr(dev(y), q)
+    qh = host(q).astype(np.float64)
+    assert np.abs(qh.T @ qh - np.eye(l)).max() < 1e-5
+    y32 = y.astype(np.float32).astype(np.float64)
+    resid = y32 - qh @ (qh.T @ y32)
+    assert np.linalg.norm(resid) / np.linalg.norm(y32) < 1e-5
+
+
+def test_thin_qr_rank_deficient_falls_back(ctx, oracle):
+    rng = np.random.default_rng(3)
+    base = rng.random((60, 3))
+    y = np.concatenate([base, base @ rng.random((3, 4))], axis=1)  # rank 3, 7 columns
+    q = torch.empty((60, 7), device="cuda")
+    ctx.thin_qr(dev(y), q)
+    qh = host(q).astype(np.float64)
+    assert np.all(np.isfinite(qh))
+    assert np.abs(qh.T @ qh - np.eye(7)).max() < 1e-5
+    y32 = y.astype(np.float32).astype(np.float64)
+    assert np.linalg.norm(y32 - qh @ (qh.T @ y32)) / np.linalg.norm(y32) < 1e-5
+
+
+# ------------------------------------------------------------ compression --
+def test_build_projectors_span_parity(ctx, oracle):
+    """Only span(L), span(R^T) enter FastHALS-RP.  The captured signal subspace
+    must agree with the reference; the noise directions beyond the true rank
+    (singular values ~1e4 below the top) are fixed only to fp32 resolution,
+    so they are compared through the projection residual, not entrywise."""
+    x = oracle.synth_x(1000, 1000, 20, 0, 1, 0.01, 1)
+    x64 = x.astype(np.float64)
+    q, w, seed = 30, 2, 1
+    left = torch.empty((1000, q), device="cuda")
+    right = torch.empty((q, 1000), device="cuda")
+    ctx.build_projectors(dev(x), q, w, seed, left, right)
+    lr, rr = oracle.build_projectors(x64, q, w, seed)
+    lg, rg = host(left).astype(np.float64), host(right).astype(np.float64)
+    assert np.abs(lg.T @ lg - np.eye(q)).max() < 1e-5
+    assert np.abs(rg @ rg.T - np.eye(q)).max() < 1e-5
+    u, _, vt = np.linalg.svd(x64, full_matrices=False)
+    uk, vk = u[:, :20], vt[:20].T
+    assert np.linalg.norm((lg @ lg.T - lr @ lr.T) @ uk) < 1e-5
+    assert np.linalg.norm((rg.T @ rg - rr.T @ rr) @ vk) < 1e-5
+    res_g = np.linalg.norm(x64 - lg @ (lg.T @ x64))
+    res_r = np.linalg.norm(x64 - lr @ (lr.T @ x64))
+    assert abs(res_g - res_r) / res_r < 1e-4
+    res_g = np.linalg.norm(x64 - (x64 @ rg.T) @ rg)
+    res_r = np.linalg.norm(x64 - (x64 @ rr.T) @ rr)
+    assert abs(res_g - res_r) / res_r < 1e-4
+
+
+def test_compress_views_parity(ctx, oracle):
+    x = oracle.synth_x(700, 500, 10, 0, 1, 0.01, 2).astype(np.float64)
+    lr, rr = oracle.build_projectors(x, 16, 1, 3)
+    xhat_r, xcheck_r = oracle.compress(x, lr, rr)
+    xhat = torch.empty((16, 500), device="cuda")
+    xcheck = torch.empty((700, 16), device="cuda")
+    ctx.compress(dev(x), dev(lr), dev(rr), xhat, xcheck)
+    assert rel_fro(host(xhat), xhat_r) < 1e-5
+    assert rel_fro(host(xcheck), xcheck_r) < 1e-5
+
+
+def test_powered_range_finder_orthonormal(ctx, oracle):
+    x = random_nonneg(oracle, 20, 15, 3)
+    for w in (0, 2):
+        out = torch.empty((20, 6), device="cuda")
+        ctx.powered_range_finder(dev(x), 6, w, 7, False, out)
+        b = host(out).astype(np.float64)
+        assert np.abs(b.T @ b - np.eye(6)).max() < 1e-5
+        ref = oracle.range_finder(x, 6, w, 7)
+        assert np.linalg.norm(b @ b.T - ref @ ref.T) < 1e-4
+
+
+# ------------------------------------------------------------------ steps --
+def _step_fixture(oracle, d, n, k, q, w, data_seed, init_seed, sketch_seed):
+    x = oracle.synth_x(d, n, min(k, 10), 0, 1, 0.01, data_seed).astype(np.float64)
+    left, right = oracle.build_projectors(x, q, w, sketch_seed)
+    xhat, xcheck = oracle.compress(x, left, right)
+    a, b = oracle.initialize(d, n, k, init_seed)
+    ah, bc = oracle.compress_factors(a, b, left, right)
+    return x, left, right, xhat, xcheck, a, b, ah, bc
+
+
+def test_fasthals_rp_steps_parity(ctx, oracle):
+    x, left, right, xhat, xcheck, a, b, ah, bc = _step_fixture(oracle, 300, 240, 8, 20, 1, 4, 5, 6)
+    ta, tb, tah, tbc = dev(a), dev(b), dev64(ah), dev64(bc)
+    ctx.fasthals_rp_steps(dev(xhat), dev(xcheck), dev(left), dev(right), ta, tb, tah, tbc,
+                          True, 0.0, 0.0, 901, 5)
+    rng = oracle.rng(901)
+    for _ in range(5):
+        oracle.fasthals_rp_step(xhat, xcheck, a, b, ah, bc, left, right, True, 0.0, 0.0, rng)
+    assert rel_fro(host(ta), a) < FACTOR_RTOL
+    assert rel_fro(host(tb), b) < FACTOR_RTOL
+    assert rel_fro(host(tah), ah) < FACTOR_RTOL
+    assert rel_fro(host(tbc), bc) < FACTOR_RTOL
+
+
+@pytest.mark.parametrize("alpha,beta", [(0.2, 0.7), (0.0, 0.5), (1e-3, 0.0)])
+def test_penalized_steps_parity(ctx, oracle, alpha, beta):
+    x, left, right, xhat, xcheck, a, b, ah, bc = _step_fixture(oracle, 120, 90, 4, 10, 1, 7, 8, 9)
+    ta, tb, tah, tbc = dev(a), dev(b), dev64(ah), dev64(bc)
+    ctx.fasthals_rp_steps(dev(xhat), dev(xcheck), dev(left), dev(right), ta, tb, tah, tbc,
+                          True, alpha, beta, 3, 3)
+    rng = oracle.rng(3)
+    for _ in range(3):
+        oracle.fasthals_rp_step(xhat, xcheck, a, b, ah, bc, left, right, True, alpha, beta, rng)
+    assert rel_fro(host(ta), a) < FACTOR_RTOL
+    assert rel_fro(host(tb), b) < FACTOR_RTOL
+
+
+def test_zero_start_redraw_path(ctx, oracle):
+    """test_solvers.cpp:394-413: all-zero start on a square sketch stays finite;
+    every component is redrawn from the host Rng in the reference's order."""
+    x = random_nonneg(oracle, 12, 12, 9)
+    left, right = oracle.build_projectors(x, 12, 0, 5)
+    xhat, xcheck = oracle.compress(x, left, right)
+    a, b = np.zeros((12, 2)), np.zeros((12, 2))
+    ah, bc = oracle.compress_factors(a, b, left, right)
+    ta, tb, tah, tbc = dev(a), dev(b), dev64(ah), dev64(bc)
+    redraws = ctx.fasthals_rp_steps(dev(xhat), dev(xcheck), dev(left), dev(right), ta, tb, tah,
+                                    tbc, True, 0.0, 0.0, 3, 1)
+    rng = oracle.rng(3)
+    oracle.fasthals_rp_step(xhat, xcheck, a, b, ah, bc, left, right, True, 0.0, 0.0, rng)
+    assert redraws >= 2
+    assert np.all(np.isfinite(host(ta))) and np.all(np.isfinite(host(tb)))
+    assert rel_fro(host(ta), a) < FACTOR_RTOL
+    assert rel_fro(host(tb), b) < FACTOR_RTOL
+
+
+def test_square_sketch_reduces_to_dense_fasthals(ctx, oracle):
+    """test_solvers.cpp:356-370 / acceptance check 5 on the device."""
+    x = random_nonneg(oracle, 12, 12, 512)
+    left, right = oracle.build_projectors(x, 12, 0, 5)
+    xhat, xcheck = oracle.compress(x, left, right)
+    a, b = oracle.initialize(12, 12, 3, 612)
+    pa, pb = a.copy(), b.copy()
+    ah, bc = oracle.compress_factors(a, b, left, right)
+    ta, tb, tah, tbc = dev(a), dev(b), dev64(ah), dev64(bc)
+    rng = oracle.rng(902)
+    ctx.fasthals_rp_steps(dev(xhat), dev(xcheck), dev(left), dev(right), ta, tb, tah, tbc,
+                          True, 0.0, 0.0, 902, 5)
+    for _ in range(5):
+        oracle.fasthals_step(x, pa, pb, True, rng)
+    assert rel_fro(host(ta), pa) < 1e-5
+    assert rel_fro(host(tb), pb) < 1e-5
+
+
+# ---------------------------------------------------------------- metrics --
+def test_reconstruction_error_parity(ctx, oracle):
+    x = oracle.synth_x(777, 555, 9, 0, 1, 0.01, 4).astype(np.float64)
+    a, b = oracle.initialize(777, 555, 9, 2)
+    a32, b32 = a.astype(np.float32), b.astype(np.float32)
+    got = ctx.reconstruction_error(dev(x), dev(a32), dev(b32))
+    want = oracle.reconstruction_error(x, a32.astype(np.float64), b32.astype(np.float64))
+    assert abs(got - want) / want < 1e-6
+    assert ctx.reconstruction_error(dev(np.array([[1.0, 2.0], [3.0, 4.0]])),
+                                    dev(np.zeros((2, 1))), dev(np.zeros((2, 1)))) == 15.0
+
+
+# --------------------------------------------------------------------- run --
+def _run_both(ctx, oracle, x, **kw):
+    import paper_1712_02248_b200 as cb
+    cfg = cb.SolverConfig(algorithm=cb.FASTHALS_RP, k=kw["k"],
+                          sketch=cb.SketchConfig(kw["q"], kw["w"], kw.get("sketch_seed", 1)),
+                          max_iterations=kw["iters"], error_interval=kw.get("every", 1),
+                          rel_tolerance=kw.get("tol", 1e-300), seed=kw.get("seed", 1),
+                          alpha=kw.get("alpha", 0.0), beta=kw.get("beta", 0.0))
+    res = ctx.run(x, cfg)
+    ra, rb, rt = oracle.run(x.astype(np.float64), kw["k"], q=kw["q"], w=kw["w"],
+                            sketch_seed=kw.get("sketch_seed", 1), max_iterations=kw["iters"],
+                            error_interval=kw.get("every", 1), rel_tolerance=kw.get("tol", 1e-300),
+                            seed=kw.get("seed", 1), alpha=kw.get("alpha", 0.0),
+                            beta=kw.get("beta", 0.0))
+    return res, ra, rb, rt
+
+
+def test_run_c1_trajectory_parity(ctx, oracle):
+    """BASELINE configs[0] (C1) at full size: 1000x1000, k=20, l=30, w=2, 100 it."""
+    x = oracle.synth_x(1000, 1000, 20, 0, 1, 0.01, 1)
+    res, ra, rb, rt = _run_both(ctx, oracle, x, k=20, q=30, w=2, iters=100)
+    xn = float(np.sum(x.astype(np.float64) ** 2))
+    assert [r.iteration for r in res.trace.records] == rt.iterations
+    got = rel_err([r.error for r in res.trace.records], xn)
+    want = rel_err(rt.errors, xn)
+    assert np.max(np.abs(got - want) / want) < TRAJ_RTOL
+    assert rel_fro(res.a, ra) < FACTOR_RTOL and rel_fro(res.b, rb) < FACTOR_RTOL
+    assert np.abs(res.a - ra).max() <= FACTOR_RTOL * np.abs(ra).max()
+    assert np.abs(res.b - rb).max() <= FACTOR_RTOL * np.abs(rb).max()
+    assert res.trace.status == rt.status and res.trace.iterations_run == rt.iterations_run
+    assert abs(res.trace.gini_b - rt.gini_b) < 1e-4
+    assert res.trace.x_passes == 4 * 2 + 4
+
+
+def test_run_c2_trajectory_against_golden(ctx, oracle):
+    """BASELINE configs[1] (C2) at full size against the committed reference
+    trajectory (tests/golden/c2.npz, produced by the reference itself)."""
+    import os
+    import paper_1712_02248_b200 as cb
+    g = np.load(os.path.join(os.path.dirname(__file__), "golden", "c2.npz"))
+    x = oracle.synth_x(10000, 5000, 16, 1, 1, 0.05, 1)
+    x64 = x.astype(np.float64)
+    assert np.array_equal(np.array([x64.sum(), (x64 * x64).sum(), x64[0, 0], x64[-1, -1],
+                                    x64.max()]), g["x_summary"])
+    cfg = cb.SolverConfig(algorithm=cb.FASTHALS_RP, k=16, sketch=cb.SketchConfig(36, 2, 1),
+                          max_iterations=200, error_interval=1, rel_tolerance=1e-300, seed=1)
+    res = ctx.run(x, cfg)
+    xn = float(np.sum(x64 ** 2))
+    assert [r.iteration for r in res.trace.records] == list(g["iters"])
+    got = rel_err([r.error for r in res.trace.records], xn)
+    want = rel_err(g["errors"], xn)
+    assert np.max(np.abs(got - want) / want) < TRAJ_RTOL
+    assert np.allclose(np.linalg.norm(res.a.astype(np.float64), axis=0), g["a_colnorm"],
+                       rtol=FACTOR_RTOL)
+    assert np.allclose(np.linalg.norm(res.b.astype(np.float64), axis=0), g["b_colnorm"],
+                       rtol=FACTOR_RTOL)
+    assert rel_fro(res.a[:64], g["a_head"]) < FACTOR_RTOL
+    assert rel_fro(res.b[:64], g["b_head"]) < FACTOR_RTOL
+
+
+def test_run_penalized_cadence_parity(ctx, oracle):
+    x = oracle.synth_x(400, 300, 6, 1, 1, 0.05, 3)
+    res, ra, rb, rt = _run_both(ctx, oracle, x, k=6, q=12, w=1, iters=23, every=5, alpha=0.01,
+                                beta=0.1, seed=4, sketch_seed=2)
+    assert [r.iteration for r in res.trace.records] == [0, 5, 10, 15, 20, 23]
+    xn = float(np.sum(x.astype(np.float64) ** 2))
+    got = rel_err([r.error for r in res.trace.records], xn)
+    assert np.max(np.abs(got - rel_err(rt.errors, xn)) / rel_err(rt.errors, xn)) < TRAJ_RTOL
+    assert rel_fro(res.b, rb) < FACTOR_RTOL
+
+
+def test_run_converges_early_like_reference(ctx, oracle):
+    x = oracle.synth_x(200, 150, 3, 0, 1, 0.05, 5)
+    res, ra, rb, rt = _run_both(ctx, oracle, x, k=3, q=8, w=2, iters=300, every=1, tol=1e-3)
+    assert rt.status == 0
+    assert res.trace.status == 0
+    assert abs(res.trace.iterations_run - rt.iterations_run) <= max(3, rt.iterations_run // 10)
+    assert "iteration" in res.trace.message
+
+
+def test_run_is_pure_function(ctx, oracle):
+    """test_solvers.cpp:161-177: identical results run to run (bitwise)."""
+    import paper_1712_02248_b200 as cb
+    x = random_nonneg(oracle, 120, 90, 13).astype(np.float32)
+    cfg = cb.SolverConfig(algorithm=cb.FASTHALS_RP, k=2, sketch=cb.SketchConfig(5, 2, 4),
+                          max_iterations=30)
+    r1, r2 = ctx.run(x, cfg), ctx.run(x, cfg)
+    assert np.array_equal(r1.a, r2.a) and np.array_equal(r1.b, r2.b)
+    assert [r.error for r in r1.trace.records] == [r.error for r in r2.trace.records]
+
+
+def test_run_rejects_invalid_data_and_config(ctx):
+    import paper_1712_02248_b200 as cb
+    x = np.random.default_rng(0).random((6, 5)).astype(np.float32)
+    cfg = cb.SolverConfig(algorithm=cb.FASTHALS_RP, k=2, sketch=cb.SketchConfig(3, 1, 1))
+    bad = x.copy()
+    bad[2, 2] = -0.1
+    with pytest.raises(cb.InputError):
+        ctx.run(bad, cfg)
+    bad[2, 2] = np.nan
+    with pytest.raises(cb.InputError):
+        ctx.run(bad, cfg)
+    with pytest.raises(cb.ConfigError):
+        ctx.run(x, cb.SolverConfig(algorithm=cb.FASTHALS_RP, k=2, sketch=cb.SketchConfig(2, 1)))
+    with pytest.raises(cb.UnsupportedError):
+        ctx.run(x, cb.SolverConfig(algorithm=cb.MU, k=2))
+
+
+def test_run_zero_iterations_returns_init(ctx, oracle):
+    import paper_1712_02248_b200 as cb
+    x = random_nonneg(oracle, 6, 5, 11).astype(np.float32)
+    res = ctx.run(x, cb.SolverConfig(algorithm=cb.FASTHALS_RP, k=2,
+                                     sketch=cb.SketchConfig(3, 1, 1), max_iterations=0))
+    a, b = oracle.initialize(6, 5, 2, 1)
+    assert [r.iteration for r in res.trace.records] == [0]
+    assert np.array_equal(res.a, a.astype(np.float32))
+    assert np.array_equal(res.b, b.astype(np.float32))
