@@ -1,0 +1,338 @@
+#!/usr/bin/env python
+"""bench.py -- compress+HALS seconds of the FastHALS-RP hot path on B200.
+
+  python bench.py [--gpus N] [--steps K] [--warmup W] [--config c2] [--impl ours|reference]
+
+A step is one pass of the hot path over the configuration's synthetic X:
+build_projectors + compress_left/right (4w+4 X passes, Gaussian sketches
+generated on the device) followed by `iters` FastHALS-RP iterations -- the
+reference's cnmf::run(fasthals-rp) minus its untimed objective evaluations
+(proj/src/solvers.cpp:213-284).  One JSON line on rank 0.
+
+  value   compress+HALS seconds per step, device-timed (CUDA events inside the
+          library on its stream), X resident in HBM.
+  e2e     the same job through the public C ABI (cnmf_run) from pinned HOST
+          memory: H2D of X, check, init, compress, HALS, the two objective
+          evaluations run() always makes, Gini, D2H of A and B -- wall clock.
+  roofline  the X-stream contraction kernel (the compression GEMM): algorithmic
+          bytes per launch / CUDA-event launch time vs MEASURED_PEAKS.json HBM.
+  cpu_baseline  the reference itself (oracle/_ref, compiled from its sources)
+          on this host's cores, rank 0 at N=1 only.
+"""
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "compress+HALS seconds, X-stream GB/s and % roofline at 1/2/4/8 B200"
+L2_BYTES = 126 * 1024 * 1024
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=5)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--config", default="c2", choices=["c1", "c2", "c3", "c4", "c5"])
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-e2e", action="store_true")
+    return ap.parse_args()
+
+
+def peaks():
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
+            p = json.load(f)
+        return float(p["hbm_gbs"]), "measured"
+    except Exception:
+        return 6650.0, "fallback"
+
+
+def workload_desc(name, c):
+    kinds = {0: "Uniform[0,1)", 1: "Exponential(1)", 2: "Gamma(0.3,1)"}
+    noise = {0: "", 1: f" + |N(0,{c['sigma']})|", 2: " -> Poisson(W0 H0)"}[c["noise_kind"]]
+    return (f"{name.upper()}: X {c['d']}x{c['n']} fp32 = W0 H0 ({kinds[c['factor_kind']]}, "
+            f"rank {c['rank']}){noise}; k={c['k']}, l={c['q']}, q(power iters)={c['w']}, "
+            f"{c['iters']} FastHALS-RP iterations")
+
+
+# ----------------------------------------------------------------- clocks ---
+class ClockSampler:
+    """nvidia-smi clocks + throttle reasons sampled during the timed region."""
+
+    Q = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+         "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+         "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, gpu):
+        self.gpu = gpu
+        self.p = None
+
+    def __enter__(self):
+        try:
+            self.p = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.gpu), f"--query-gpu={self.Q}",
+                 "--format=csv,noheader,nounits", "-lms", "100"],
+                stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+        except Exception:
+            self.p = None
+        time.sleep(0.15)
+        return self
+
+    def __exit__(self, *a):
+        self.lines = []
+        if self.p is not None:
+            time.sleep(0.15)
+            self.p.terminate()
+            try:
+                out, _ = self.p.communicate(timeout=5)
+            except Exception:
+                self.p.kill()
+                out, _ = self.p.communicate()
+            self.lines = [ln for ln in out.splitlines() if ln.strip()]
+
+    def summary(self):
+        sm, mx, reasons = [], 0.0, set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for ln in self.lines:
+            f = [t.strip() for t in ln.split(",")]
+            if len(f) < 9:
+                continue
+            try:
+                sm.append(float(f[1]))
+                mx = max(mx, float(f[2]))
+            except ValueError:
+                continue
+            for nm, v in zip(names, f[5:9]):
+                if v.lower() == "active":
+                    reasons.add(nm)
+        if not sm:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": [], "samples": 0}
+        return {"sm_mhz": statistics.median(sm), "sm_max_mhz": mx, "reasons": sorted(reasons),
+                "samples": len(sm)}
+
+
+# -------------------------------------------------------- CPU reference leg ---
+def cpu_reference_sample(name, c, timed_steps=1):
+    """The reference (oracle/_ref) on the host: build_projectors + compress_* and
+    `iters` fasthals_rp_step calls.  Full workload when it fits ~30 s of CPU,
+    else per-pass column-slice + full-shape step timing, scaled (extrapolated)."""
+    import numpy as np
+
+    from oracle import REF_SO, Oracle, Reference
+    o = Oracle()
+    kind = "reference" if os.path.exists(REF_SO) else "port"
+    r = Reference() if kind == "reference" else None
+    d, n, k, q, w, iters = c["d"], c["n"], c["k"], c["q"], c["w"], c["iters"]
+    full = d * n <= 6e7
+    n_s = n if full else max(q + 1, min(n, int(6e6 // d) + 1))
+    x = o.synth_x(d, n, c["rank"], c["factor_kind"], c["noise_kind"], c["sigma"], 1,
+                  col_lo=0, col_hi=n_s).astype(np.float64)
+    vals = []
+    for _ in range(timed_steps):
+        if kind == "reference":
+            left, right, xhat, xcheck, t_comp = r.compress(x, q, w, 1)
+        else:
+            t0 = time.perf_counter()
+            left, right = o.build_projectors(x, q, w, 1)
+            xhat, xcheck = o.compress(x, left, right)
+            t_comp = time.perf_counter() - t0
+        t_comp *= n / n_s
+        if full:
+            a, b = o.initialize(d, n, k, 1)
+            ah, bc = o.compress_factors(a, b, left, right)
+            hs = iters
+        else:  # full-shape operands for the per-iteration cost (cost does not depend on values)
+            rng = np.random.default_rng(0)
+            xhat = rng.random((q, n)); xcheck = rng.random((d, q))
+            left = np.linalg.qr(rng.standard_normal((d, q)))[0]
+            right = np.linalg.qr(rng.standard_normal((n, q)))[0].T.copy()
+            a, b = o.initialize(d, n, k, 1)
+            ah, bc = o.compress_factors(a, b, left, right)
+            hs = 1
+        if kind == "reference":
+            t_h = r.fasthals_rp_steps(xhat, xcheck, left, right, a, b, ah, bc, 1, hs)
+        else:
+            t0 = time.perf_counter()
+            rg = o.rng(1)
+            for _ in range(hs):
+                o.fasthals_rp_step(xhat, xcheck, a, b, ah, bc, left, right, True, 0.0, 0.0, rg)
+            t_h = time.perf_counter() - t0
+        t_h *= iters / hs
+        vals.append(t_comp + t_h)
+    sample = (f"full {name.upper()} workload: build_projectors+compress_left/right on the "
+              f"{d}x{n} X and {iters} fasthals_rp_step calls, single thread (the reference "
+              f"solver is single-threaded)") if full else (
+              f"extrapolated: compression on a {d}x{n_s} column slice scaled by n/n_s "
+              f"(cost linear in n) + one full-shape fasthals_rp_step x {iters}")
+    return vals, kind, sample
+
+
+def run_reference_arm(args, name, c, rank):
+    if rank != 0:
+        return
+    # one untimed tiny sample as warm-up (CPU code has no JIT/caches to warm)
+    small = dict(c, d=200, n=150, rank=3, k=3, q=6, w=1, iters=2)
+    for _ in range(max(1, min(args.warmup, 1))):
+        cpu_reference_sample("warmup", small, 1)
+    vals, kind, sample = cpu_reference_sample(name, c, args.steps)
+    v = statistics.mean(vals)
+    line = {"metric": METRIC, "value": v, "unit": "s", "n_gpus": args.gpus, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": v * 1e3, "higher_is_better": False,
+            "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+            "impl": "reference",
+            "config": {"workload": workload_desc(name, c), "parallelism": "single host thread"},
+            "cpu_baseline": {"value": v, "unit": "s", "cores": 1, "kind": kind,
+                             "sample": sample},
+            "e2e": {"value": v, "unit": "s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(line), flush=True)
+
+
+# ------------------------------------------------------------ our arm -------
+def run_ours(args, name, c, rank, world, local_rank):
+    import numpy as np
+    import torch
+
+    import paper_1712_02248_b200 as cb
+
+    torch.cuda.set_device(local_rank)
+    ctx = cb.Context(local_rank)
+    d, n, k, q, w, iters = c["d"], c["n"], c["k"], c["q"], c["w"], c["iters"]
+    ldx = (n + 3) // 4 * 4
+    x = torch.empty((d, ldx), dtype=torch.float32, device="cuda")
+    ctx.synth_x(d, n, c["rank"], c["factor_kind"], c["noise_kind"], c["sigma"], 1, x)
+    xv = x[:, :n]
+    cfg = cb.SolverConfig(algorithm=cb.FASTHALS_RP, k=k, sketch=cb.SketchConfig(q, w, 1),
+                          max_iterations=iters, error_interval=iters, rel_tolerance=1e-300,
+                          seed=1)
+    a = torch.empty((d, k), device="cuda")
+    b = torch.empty((n, k), device="cuda")
+    flush = torch.empty(2 * L2_BYTES // 4, dtype=torch.float32, device="cuda")
+    stream = torch.cuda.ExternalStream(ctx.stream())
+    x_bytes = 4.0 * d * n
+    big = x_bytes > L2_BYTES
+
+    for _ in range(args.warmup):
+        ctx.run_device(xv, cfg, a, b)
+    torch.cuda.synchronize()
+    if world > 1:
+        torch.distributed.barrier()
+    steps, comp, upd, passes = [], [], [], []
+    launches0 = cb.launch_count()
+    with ClockSampler(local_rank) as clk:
+        for i in range(args.steps):
+            if not big:
+                flush.fill_(float(i))
+            torch.cuda.synchronize()
+            e0 = torch.cuda.Event(enable_timing=True)
+            e1 = torch.cuda.Event(enable_timing=True)
+            e0.record(stream)
+            _, _, tr = ctx.run_device(xv, cfg, a, b)
+            e1.record(stream)
+            e1.synchronize()
+            steps.append(e0.elapsed_time(e1) * 1e-3)
+            comp.append(tr.compress_seconds)
+            upd.append(tr.update_seconds)
+            passes.append(tr.x_passes)
+    torch.cuda.synchronize()
+    launches = cb.launch_count() - launches0
+    if world > 1:
+        torch.distributed.barrier()
+    value = statistics.mean([cc + uu for cc, uu in zip(comp, upd)])
+    ms_per_step = statistics.mean(steps) * 1e3
+    if world > 1:
+        t = torch.tensor([value, ms_per_step], dtype=torch.float64, device="cuda")
+        torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
+        value, ms_per_step = t.tolist()
+
+    # roofline of the X-stream contraction (dominant kernel of the compression half)
+    hbm, src = peaks()
+    t_nn = ctx.time_xstream(xv, q, 0, iters=10)
+    t_tn = ctx.time_xstream(xv, q, 1, iters=10)
+    alg_bytes = 4.0 * d * n + 4.0 * (d + n) * q
+    ach_nn = alg_bytes / t_nn / 1e9
+    ach_tn = alg_bytes / t_tn / 1e9
+    traffic = None
+    prof = os.path.join(ROOT, "profiles", f"traffic_{name}.json")
+    if os.path.exists(prof):
+        try:
+            traffic = json.load(open(prof)).get("bytes_per_launch")
+        except Exception:
+            traffic = None
+    mean_comp = statistics.mean(comp)
+    xstream_gbs = passes[0] * x_bytes / mean_comp / 1e9
+
+    line = {"metric": METRIC, "value": value, "unit": "s", "n_gpus": world,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms_per_step,
+            "higher_is_better": False, "scaling": "strong", "vs_baseline": None,
+            "dtype": "f32", "data": "synthetic",
+            "config": {"workload": workload_desc(name, c), "d": d, "n": n, "k": k, "l": q,
+                       "power_iterations": w, "iterations": iters,
+                       "parallelism": f"column-shard x{world}" if world > 1 else "1 GPU",
+                       "l2": ("inputs larger than L2 (X %.0f MB > 126 MB)" % (x_bytes / 1e6))
+                       if big else "L2 flushed (256 MB write) between timed steps"},
+            "compress_seconds": mean_comp, "hals_seconds": statistics.mean(upd),
+            "x_passes": passes[0], "x_stream_gbs": xstream_gbs,
+            "x_stream_gbs_fused_min": (2 * w + 2) * x_bytes / mean_comp / 1e9,
+            "roofline": {"bound": "hbm", "kernel": "xs_kernel (X*S, NN contraction)",
+                         "achieved": ach_nn, "peak": hbm, "unit": "GB/s",
+                         "frac": ach_nn / hbm, "traffic": traffic,
+                         "peak_source": f"{src} (MEASURED_PEAKS.json hbm_gbs)" if src ==
+                         "measured" else "fallback 6.65 TB/s (B200_PROFILING.md)",
+                         "launch_seconds": t_nn, "algorithmic_bytes": alg_bytes,
+                         "tn_achieved": ach_tn, "tn_frac": ach_tn / hbm,
+                         "tn_launch_seconds": t_tn},
+            "gpu_launches": int(launches),
+            "clocks": clk.summary()}
+
+    if not args.no_e2e:
+        xh = torch.empty((d, n), dtype=torch.float32, pin_memory=True)
+        xh.copy_(xv)
+        xnp = xh.numpy()
+        ctx.run(xnp, cfg)  # warm
+        e2e = []
+        for _ in range(max(1, min(args.steps, 3))):
+            t0 = time.perf_counter()
+            ctx.run(xnp, cfg)
+            e2e.append(time.perf_counter() - t0)
+        line["e2e"] = {"value": statistics.mean(e2e), "unit": "s",
+                       "h2d_bytes_per_step": int(4 * d * n),
+                       "d2h_bytes_per_step": int(4 * (d + n) * k)}
+
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        vals, kind, sample = cpu_reference_sample(name, c, 1)
+        line["cpu_baseline"] = {"value": vals[0], "unit": "s", "cores": 1, "kind": kind,
+                                "sample": sample}
+    if rank == 0:
+        print(json.dumps(line), flush=True)
+
+
+def main():
+    args = parse()
+    rank = int(os.environ.get("RANK", "0"))
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    local_rank = int(os.environ.get("LOCAL_RANK", "0"))
+    from paper_1712_02248_b200 import CONFIGS
+    c = CONFIGS[args.config]
+    if args.impl == "reference":
+        run_reference_arm(args, args.config, c, rank)
+        return
+    if world > 1:
+        import torch
+        torch.cuda.set_device(local_rank)
+        torch.distributed.init_process_group("nccl")
+    run_ours(args, args.config, c, rank, world, local_rank)
+    if world > 1:
+        import torch
+        torch.distributed.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

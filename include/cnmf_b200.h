@@ -186,6 +186,16 @@ cnmf_status cnmf_xs_nn(cnmf_context* ctx, const float* x, uint64_t d, uint64_t n
 cnmf_status cnmf_xs_tn(cnmf_context* ctx, const float* x, uint64_t d, uint64_t n, uint64_t ldx,
                        const float* t, uint64_t l, float* z);
 
+/* Instrumentation (bench harness). */
+/* Total device kernels this library has launched in this process. */
+uint64_t cnmf_launch_count(void);
+/* Average device time of ONE X-stream contraction launch (NN: transpose = 0,
+ * TN: transpose = 1) over `iters` back-to-back launches on the context
+ * stream, bracketed by CUDA events (the kernel of the compression half). */
+cnmf_status cnmf_time_xstream(cnmf_context* ctx, const float* x, uint64_t d, uint64_t n,
+                              uint64_t ldx, uint64_t l, int transpose, int iters,
+                              double* seconds_per_launch);
+
 /* Synthetic X for the BASELINE.json configs (bench harness, not the solver
  * path): columns [col_lo, col_hi) of the global d x n matrix into x (ld ldx).
  * factor_kind 0 Uniform, 1 Exponential, 2 Gamma(0.3); noise_kind 0 none,

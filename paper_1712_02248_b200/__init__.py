@@ -100,7 +100,8 @@ EXPORTS = [
     "cnmf_solver_config_validate", "cnmf_run", "cnmf_run_device", "cnmf_gaussian_sketch",
     "cnmf_initialize", "cnmf_powered_range_finder", "cnmf_build_projectors", "cnmf_compress",
     "cnmf_compress_factors", "cnmf_fasthals_rp_steps", "cnmf_reconstruction_error",
-    "cnmf_thin_qr", "cnmf_xs_nn", "cnmf_xs_tn", "cnmf_synth_x",
+    "cnmf_thin_qr", "cnmf_xs_nn", "cnmf_xs_tn", "cnmf_synth_x", "cnmf_launch_count",
+    "cnmf_time_xstream",
 ]
 
 
@@ -154,6 +155,8 @@ def load_library(path: str = LIB_PATH):
     L.cnmf_xs_tn.argtypes = [vp, fp, u64, u64, u64, fp, u64, fp]
     L.cnmf_synth_x.argtypes = [vp, u64, u64, u64, C.c_int, C.c_int, C.c_double, u64, u64, u64,
                                u64, fp]
+    L.cnmf_launch_count.restype = u64
+    L.cnmf_time_xstream.argtypes = [vp, fp, u64, u64, u64, u64, C.c_int, C.c_int, dp]
     if L.cnmf_abi_version() != 1:
         raise CudaError("libcnmf_b200.so ABI version mismatch")
     _lib = L
@@ -391,6 +394,13 @@ class Context:
                                       _ptr(out)))
         return out
 
+    def time_xstream(self, x, l, transpose, iters=10) -> float:
+        d, n = x.shape
+        out = C.c_double()
+        self._check(self.L.cnmf_time_xstream(self.h, _ptr(x), d, n, x.stride(0), l,
+                                             int(transpose), iters, C.byref(out)))
+        return out.value
+
     def synth_x(self, d, n, rank, factor_kind, noise_kind, sigma, seed, out, col_lo=0,
                 col_hi=None):
         col_hi = n if col_hi is None else col_hi
@@ -400,6 +410,11 @@ class Context:
 
 
 _default_ctx: Optional[Context] = None
+
+
+def launch_count() -> int:
+    """Device kernels launched by the library so far (this process)."""
+    return int(load_library().cnmf_launch_count())
 
 
 def default_context() -> Context:

@@ -848,6 +848,38 @@ cnmf_status cnmf_xs_tn(cnmf_context* c, const float* x, uint64_t d, uint64_t n, 
   });
 }
 
+uint64_t cnmf_launch_count(void) { return launch_count(); }
+
+cnmf_status cnmf_time_xstream(cnmf_context* c, const float* x, uint64_t d, uint64_t n,
+                              uint64_t ldx, uint64_t l, int transpose, int iters,
+                              double* seconds_per_launch) {
+  return guarded(c, [&] {
+    require_shapes(1, l);
+    if (iters < 1) throw Fail(CNMF_ERR_CONFIG, "iters must be positive");
+    const int lp = pad16((int)l);
+    const XView X = prepare_x(c, x, (int64_t)d, (int64_t)n, (int64_t)ldx);
+    const int64_t in_rows = transpose ? (int64_t)d : (int64_t)n;
+    const int64_t out_rows = transpose ? (int64_t)n : (int64_t)d;
+    float* s = c->ws<float>("tx_s", in_rows * lp);
+    float* y = c->ws<float>("tx_y", out_rows * lp);
+    float* ws = c->ws<float>("xs_ws", xstream_ws_floats((int64_t)d, (int64_t)n, lp, c->nsm));
+    gen_normals(c, 12345, in_rows, (int64_t)l, s, lp, "tx");
+    auto once = [&] {
+      if (transpose)
+        launch_xs_tn(X.x, X.ldx, X.d, X.n, s, lp, y, ws, c->nsm, c->stream);
+      else
+        launch_xs_nn(X.x, X.ldx, X.d, X.n, s, lp, y, ws, c->nsm, c->stream);
+    };
+    once();  // warm-up
+    CK(cudaEventRecord(c->ev[0], c->stream));
+    for (int i = 0; i < iters; ++i) once();
+    CK(cudaEventRecord(c->ev[1], c->stream));
+    CK(cudaGetLastError());
+    c->sync();
+    *seconds_per_launch = c->elapsed(0, 1) / iters;
+  });
+}
+
 cnmf_status cnmf_synth_x(cnmf_context* c, uint64_t d, uint64_t n, uint64_t rank, int factor_kind,
                          int noise_kind, double sigma, uint64_t seed, uint64_t col_lo,
                          uint64_t col_hi, uint64_t ldx, float* x) {

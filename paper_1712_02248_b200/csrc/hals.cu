@@ -473,12 +473,14 @@ cudaError_t launch_hals(const HalsState& st, int normalize_a, double alpha, doub
       cudaFuncSetAttribute(hals_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   if (e != cudaSuccess) return e;
   void* args[] = {&a};
+  note_launches(1);
   return cudaLaunchCooperativeKernel((const void*)hals_kernel, dim3(grid), dim3(kThreads), args,
                                      smem, s);
 }
 
 void launch_compress_factors(const HalsState& st, int which, int column, cudaStream_t s) {
   const dim3 grid(st.lp, column >= 0 ? 1 : st.k);
+  note_launches(1);
   if (which == 0)
     compress_factor_kernel<<<grid, 256, 0, s>>>(st.lm, st.d, st.lp, st.a, st.k, column, st.l,
                                                 st.ahat);
@@ -488,6 +490,7 @@ void launch_compress_factors(const HalsState& st, int which, int column, cudaStr
 }
 
 void launch_normalize_column(float* a_cm, int64_t d, int j, cudaStream_t s) {
+  note_launches(1);
   normalize_column_kernel<<<1, 1024, 0, s>>>(a_cm, d, j);
 }
 

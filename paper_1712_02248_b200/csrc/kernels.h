@@ -19,6 +19,10 @@ namespace cnmf {
 // padded to a multiple of 16 columns; padding columns hold zeros.
 __host__ __device__ inline int pad16(int l) { return (l + 15) & ~15; }
 
+// Number of device kernels launched by this library (all launchers count).
+void note_launches(int n);
+uint64_t launch_count();
+
 // ---- rng.cu -------------------------------------------------------------
 struct MtJob {
   uint64_t seed;

@@ -205,13 +205,19 @@ int blocks_for(int64_t work, int nsm) {
 
 }  // namespace
 
+static unsigned long long g_launches = 0;
+void note_launches(int n) { __atomic_fetch_add(&g_launches, (unsigned long long)n, __ATOMIC_RELAXED); }
+uint64_t launch_count() { return __atomic_load_n(&g_launches, __ATOMIC_RELAXED); }
+
 size_t metrics_ws_bytes(int64_t, int64_t, int nsm) { return sizeof(double) * (nsm * 16 + 64); }
 
 void launch_check_data(const float* x, int64_t ldx, int64_t d, int64_t n, int* flag,
                        double* norm_sq, void* ws, int nsm, cudaStream_t st) {
   const int grid = nsm * 4;
   double* part = static_cast<double*>(ws);
+  note_launches(1);
   check_data_kernel<<<grid, 256, 0, st>>>(x, ldx, d, n, flag, part);
+  note_launches(1);
   sum_partials_kernel<<<1, 32, 0, st>>>(part, grid, norm_sq, 1.0);
 }
 
@@ -228,7 +234,9 @@ void launch_recon_error(const float* x, int64_t ldx, int64_t d, int64_t n, const
     attr = true;
   }
   double* part = static_cast<double*>(ws);
+  note_launches(1);
   recon_error_kernel<<<grid, 256, smem, st>>>(x, ldx, d, n, a_cm, b_cm, k, part);
+  note_launches(1);
   sum_partials_kernel<<<1, 32, 0, st>>>(part, grid, out, 0.5);
 }
 
@@ -248,26 +256,33 @@ void launch_gini(const float* b_cm, int64_t count, double* out, void* ws, size_t
   size_t temp_bytes = ws_bytes - (size_t)(temp - p);
   cub::DeviceRadixSort::SortKeys(temp, temp_bytes, b_cm, sorted, (int)count, 0, 32, st);
   const int nb = (int)std::min<int64_t>(1024, std::max<int64_t>(1, (count + 255) / 256));
+  note_launches(1);
   gini_partial_kernel<<<nb, 256, 0, st>>>(sorted, b_cm, count, part);
+  note_launches(1);
   gini_final_kernel<<<1, 32, 0, st>>>(part, nb, count, out);
 }
 
 void launch_cm_to_rm(const float* cm, int64_t rows, int k, float* rm, cudaStream_t st) {
+  note_launches(1);
   cm_to_rm_kernel<<<blocks_for(rows * k, 148), 256, 0, st>>>(cm, rows, k, rm);
 }
 void launch_rm_to_cm(const float* rm, int64_t rows, int k, float* cm, cudaStream_t st) {
+  note_launches(1);
   rm_to_cm_kernel<<<blocks_for(rows * k, 148), 256, 0, st>>>(rm, rows, k, cm);
 }
 void launch_pad_cols(const float* src, int64_t rows, int l, float* dst, int lp, cudaStream_t st) {
+  note_launches(1);
   pad_cols_kernel<<<blocks_for(rows * lp, 148), 256, 0, st>>>(src, rows, l, dst, lp);
 }
 void launch_unpad_cols(const float* src, int64_t rows, int lp, float* dst, int l,
                        cudaStream_t st) {
+  note_launches(1);
   unpad_cols_kernel<<<blocks_for(rows * l, 148), 256, 0, st>>>(src, rows, lp, dst, l);
 }
 void launch_transpose(const float* src, int64_t rows, int64_t cols, int64_t lds, float* dst,
                       int64_t ldd, cudaStream_t st) {
   const dim3 grid((unsigned)((cols + 31) / 32), (unsigned)((rows + 31) / 32));
+  note_launches(1);
   transpose_kernel<<<grid, dim3(32, 8), 0, st>>>(src, rows, cols, lds, dst, ldd);
 }
 

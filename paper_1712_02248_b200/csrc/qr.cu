@@ -262,7 +262,9 @@ void gram(const float* y, int64_t rows, int l, int lp, const QrWs& w, int nsm,
           cudaStream_t st) {
   const int grid = gram_grid(rows, nsm);
   const size_t smem = sizeof(float) * kGramRows * (lp + 4);
+  note_launches(1);
   gram_kernel<<<grid, 256, smem, st>>>(y, rows, l, lp, w.part);
+  note_launches(1);
   gram_reduce_kernel<<<(lp * lp + 255) / 256, 256, 0, st>>>(w.part, grid, l, lp, w.g);
 }
 
@@ -274,6 +276,7 @@ void chol_inv(int l, int lp, const QrWs& w, cudaStream_t st) {
                          (int)(sizeof(double) * (128 * 128 + 128)));
     attr = true;
   }
+  note_launches(1);
   chol_inv_kernel<<<1, 256, smem, st>>>(w.g, l, lp, w.rinv64, w.rinv, w.flag);
 }
 
@@ -298,6 +301,7 @@ void launch_thin_qr(const float* y, int64_t rows, int l, int lp, float* q, void*
   gram(w.q1, rows, l, lp, w, nsm, st);
   chol_inv(l, lp, w, st);
   launch_xs_nn(w.q1, lp, rows, lp, w.rinv, lp, q, w.xs_ws, nsm, st);
+  note_launches(1);
   householder_kernel<<<1, 1024, 0, st>>>(y, rows, l, lp, w.hw, w.hv, q, w.flag);
 }
 

@@ -165,6 +165,7 @@ __global__ void uniform_init_exact_kernel(const uint64_t* __restrict__ words, ui
 }  // namespace
 
 void launch_mt_streams(const MtJobs& jobs, int njobs, cudaStream_t s) {
+  note_launches(1);
   mt_stream_kernel<<<njobs, 160, 0, s>>>(jobs);
 }
 
@@ -172,11 +173,13 @@ void launch_normal_map(const uint64_t* words, uint64_t count, int cols, int ld, 
                        int* flag, int nsm, cudaStream_t s) {
   const uint64_t npairs = (count + 1) / 2;
   const int blocks = (int)std::min<uint64_t>((npairs + 255) / 256, (uint64_t)nsm * 8);
+  note_launches(1);
   normal_map_kernel<<<blocks > 0 ? blocks : 1, 256, 0, s>>>(words, count, cols, ld, out, flag);
 }
 
 void launch_normal_exact(const uint64_t* words, uint64_t nwords, uint64_t count, int cols, int ld,
                          float* out, int* flag, cudaStream_t s) {
+  note_launches(1);
   normal_exact_kernel<<<1, 32, 0, s>>>(words, nwords, count, cols, ld, out, flag);
 }
 
@@ -184,12 +187,14 @@ void launch_uniform_init(const uint64_t* words, uint64_t d, uint64_t n, int k, f
                          float* b_cm, int* flag, int nsm, cudaStream_t s) {
   const uint64_t total = (d + n) * (uint64_t)k;
   const int blocks = (int)std::min<uint64_t>((total + 255) / 256, (uint64_t)nsm * 8);
+  note_launches(1);
   uniform_init_kernel<<<blocks > 0 ? blocks : 1, 256, 0, s>>>(words, d, n, k, a_cm, b_cm, flag);
 }
 
 void launch_uniform_init_exact(const uint64_t* words, uint64_t nwords, uint64_t d, uint64_t n,
                                int k, float* a_cm, float* b_cm, int* flag, uint64_t* consumed,
                                cudaStream_t s) {
+  note_launches(1);
   uniform_init_exact_kernel<<<1, 32, 0, s>>>(words, nwords, d, n, k, a_cm, b_cm, flag, consumed);
 }
 

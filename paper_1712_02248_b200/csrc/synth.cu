@@ -131,7 +131,9 @@ void launch_synth_x(int64_t d, int64_t n, int rank, int factor_kind, int noise_k
   const int64_t ncols = col_hi - col_lo;
   double* w0 = scratch;
   double* h0 = scratch + d * rank;
+  note_launches(1);
   factors_kernel<<<148 * 8, 256, 0, s>>>(d, n, rank, factor_kind, seed, col_lo, ncols, w0, h0);
+  note_launches(1);
   x_kernel<<<148 * 16, 256, 0, s>>>(d, n, rank, noise_kind, sigma, seed, col_lo, ncols, ldx, w0,
                                     h0, x);
 }

@@ -212,6 +212,7 @@ void dispatch(const float* x, int64_t ldx, int64_t m, int64_t n, const float* s,
                            cudaFuncAttributeMaxDynamicSharedMemorySize, smem);          \
       attr = true;                                                                      \
     }                                                                                   \
+    note_launches(1);                                                                   \
     xs_kernel<kTN, LPV><<<grid, 256, smem, st>>>(x, ldx, m, n, s, dst, p.kchunk);       \
     break;                                                                              \
   }
@@ -229,6 +230,7 @@ void dispatch(const float* x, int64_t ldx, int64_t m, int64_t n, const float* s,
   if (p.splits > 1) {
     const int64_t total4 = out_rows * lp / 4;
     const int blocks = (int)std::min<int64_t>((total4 + 255) / 256, (int64_t)nsm * 8);
+    note_launches(1);
     split_reduce_kernel<<<blocks, 256, 0, st>>>(reinterpret_cast<const float4*>(ws), p.splits,
                                                 total4, reinterpret_cast<float4*>(out));
   }
