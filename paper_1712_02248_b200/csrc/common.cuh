@@ -41,6 +41,58 @@ __device__ __forceinline__ double block_sum(double v, double* red) {
   return t;
 }
 
+__device__ __forceinline__ void st_release_u64(unsigned long long* p, unsigned long long v) {
+  asm volatile("st.release.gpu.global.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
+}
+__device__ __forceinline__ unsigned long long ld_acquire_u64(const unsigned long long* p) {
+  unsigned long long v;
+  asm volatile("ld.acquire.gpu.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
+  return v;
+}
+__device__ __forceinline__ unsigned long long ld_relaxed_u64(const unsigned long long* p) {
+  unsigned long long v;
+  asm volatile("ld.relaxed.gpu.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
+  return v;
+}
+__device__ __forceinline__ void fence_acq_rel_gpu() {
+  asm volatile("fence.acq_rel.gpu;" ::: "memory");
+}
+
+// Epoch-tagged all-to-all exchange for a cooperative launch (replaces a
+// counter barrier + a separate partial read).  Every CTA writes its payload
+// with plain stores, then publish() release-stores the epoch into its own
+// tag; wait_all() polls all G tags with acquire loads.  Tags and payloads are
+// double-buffered by epoch parity: a CTA can only publish epoch e+2 after all
+// CTAs published e+1, i.e. after everyone finished reading epoch e.
+__device__ __forceinline__ void xchg_publish(unsigned long long* tags, int cta,
+                                             unsigned long long epoch) {
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    fence_acq_rel_gpu();
+    st_release_u64(tags + cta, epoch);
+  }
+}
+__device__ __forceinline__ void xchg_wait(const unsigned long long* tags, int G,
+                                          unsigned long long epoch) {
+  if (threadIdx.x < 32) {
+    // Each lane checks all of its (<= 8) tags per round with relaxed loads
+    // issued together (one L2 round trip per round, no L1 invalidation), then
+    // one acquire fence once every tag shows the epoch.
+    for (;;) {
+      bool ready = true;
+#pragma unroll
+      for (int i = 0; i < 8; ++i) {
+        const int b = threadIdx.x + 32 * i;
+        if (b < G && ld_relaxed_u64(tags + b) < epoch) ready = false;
+      }
+      if (__all_sync(0xffffffffu, ready)) break;
+      __nanosleep(20);
+    }
+    fence_acq_rel_gpu();
+  }
+  __syncthreads();
+}
+
 // Sense-free generation barrier over all CTAs of a cooperative launch.
 // bar[0] = arrival count, bar[1] = generation.  Release/acquire at gpu
 // scope orders every global write before the barrier with every read after.

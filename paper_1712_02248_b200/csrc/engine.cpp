@@ -13,6 +13,7 @@
 
 #include <cmath>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <map>
 #include <mutex>
@@ -153,8 +154,8 @@ void gen_normals2(cnmf_context* c, uint64_t seed0, int64_t rows0, int64_t cols, 
 
 // initialize(d, n, k, seed) into column-major A_cm / B_cm; returns the
 // device counter of raw draws consumed (for positioning the host Rng).
-uint64_t* gen_init(cnmf_context* c, uint64_t seed, int64_t d, int64_t n, int k, float* a_cm,
-                   float* b_cm) {
+uint64_t* gen_init(cnmf_context* c, uint64_t seed, int64_t d, int64_t n, int k, double* a_cm,
+                   double* b_cm) {
   const uint64_t total = (uint64_t)(d + n) * k;
   const uint64_t nwords = total + 256;
   uint64_t* words = c->ws<uint64_t>("words_init", nwords);
@@ -210,6 +211,7 @@ int range_finder(cnmf_context* c, const XView& X, int q, int lp, uint64_t w, boo
 struct HalsRun {
   HalsState st;
   int grid;
+  unsigned long long epoch;  // next launch's exchange epoch base
 };
 
 HalsRun make_hals(cnmf_context* c, int64_t d, int64_t n, int l, int lp, int k) {
@@ -220,31 +222,38 @@ HalsRun make_hals(cnmf_context* c, int64_t d, int64_t n, int l, int lp, int k) {
   s.l = l;
   s.lp = lp;
   s.k = k;
-  s.a = c->ws<float>("A_cm", (size_t)k * d);
-  s.b = c->ws<float>("B_cm", (size_t)k * n);
-  s.bold = c->ws<float>("B_old", (size_t)k * n);
-  s.h = c->ws<float>("H_cm", (size_t)k * d);
+  s.a = c->ws<double>("A_cm", (size_t)k * d);
+  s.b = c->ws<double>("B_cm", (size_t)k * n);
+  s.bold = c->ws<double>("B_cm2", (size_t)k * n);
+  s.h = c->ws<double>("H_cm", (size_t)k * d);
   s.ahat = c->ws<double>("Ahat", (size_t)lp * k);
   s.bchk = c->ws<double>("Bchk", (size_t)lp * k);
-  s.g = c->ws<double>("Gk", (size_t)k * k);
-  s.w = c->ws<double>("Wk", (size_t)k * k);
   r.grid = hals_grid(s, c->nsm);
+  s.p = c->ws<double>("P_cm", (size_t)k * n);
+  s.gsc = c->ws<double>("hals_gsc", (size_t)r.grid * k * k);
+  s.wsc = c->ws<double>("hals_wsc", (size_t)r.grid * k * k);
   s.part = c->ws<double>("hals_part", hals_part_doubles(r.grid, lp, k));
-  s.npart = c->ws<double>("hals_npart", (size_t)k * r.grid);
-  s.zflag = c->ws<int>("hals_zflag", (size_t)k * r.grid);
-  s.bar = c->ws<unsigned>("hals_bar", 2);
+  s.npart = c->ws<double>("hals_npart", (size_t)2 * r.grid);
+  s.zpart = c->ws<unsigned>("hals_zpart", (size_t)4 * r.grid);
+  s.bar = c->ws<unsigned>("hals_bar", 64);
   s.halt = c->ws<HaltInfo>("hals_halt", 1);
-  CK(cudaMemsetAsync(s.bar, 0, 2 * sizeof(unsigned), c->stream));
+  s.prof = nullptr;
+  if (std::getenv("CNMF_PROFILE")) {
+    s.prof = c->ws<long long>("hals_prof", 32);
+    CK(cudaMemsetAsync(s.prof, 0, 32 * sizeof(long long), c->stream));
+  }
+  CK(cudaMemsetAsync(s.bar, 0, 64 * sizeof(unsigned), c->stream));
   CK(cudaMemsetAsync(s.ahat, 0, sizeof(double) * lp * k, c->stream));
   CK(cudaMemsetAsync(s.bchk, 0, sizeof(double) * lp * k, c->stream));
+  r.epoch = 0;  // barriers completed so far (the counter reads epoch * grid)
   return r;
 }
 
 // Draws reinit_column (solvers.cpp:28-31) from the host Rng into a device column.
-void redraw_column(cnmf_context* c, std::mt19937_64& rng, float* col_dev, int64_t rows) {
-  std::vector<float> v((size_t)rows);
-  for (int64_t i = 0; i < rows; ++i) v[(size_t)i] = (float)(uniform_positive(rng) * 1e-3);
-  CK(cudaMemcpyAsync(col_dev, v.data(), sizeof(float) * rows, cudaMemcpyHostToDevice, c->stream));
+void redraw_column(cnmf_context* c, std::mt19937_64& rng, double* col_dev, int64_t rows) {
+  std::vector<double> v((size_t)rows);
+  for (int64_t i = 0; i < rows; ++i) v[(size_t)i] = uniform_positive(rng) * 1e-3;
+  CK(cudaMemcpyAsync(col_dev, v.data(), sizeof(double) * rows, cudaMemcpyHostToDevice, c->stream));
   c->sync();  // v goes out of scope
 }
 
@@ -259,14 +268,16 @@ void run_hals(cnmf_context* c, HalsRun& hr, int normalize_a, double alpha, doubl
   int64_t begin = ib;
   for (;;) {
     CK(cudaEventRecord(c->ev[0], c->stream));
-    CK(launch_hals(st, normalize_a, alpha, beta, (int)begin, (int)ie, half, col, skip, hr.grid,
-                   c->stream));
+    CK(launch_hals(st, normalize_a, alpha, beta, (int)begin, (int)ie, half, col, skip, hr.epoch,
+                   hr.grid, c->stream));
     CK(cudaEventRecord(c->ev[1], c->stream));
     CK(cudaMemcpyAsync(c->halt_host, st.halt, sizeof(HaltInfo), cudaMemcpyDeviceToHost,
                        c->stream));
     c->sync();
     *update_seconds += c->elapsed(0, 1);
     const HaltInfo h = *c->halt_host;
+    hr.epoch = h.last_epoch;
+    if (h.pad) std::swap(st.b, st.bold);  // the kernel double-buffers B
     if (!h.halted) break;
     std::mt19937_64& rng = get_rng();
     const int j = h.column;
@@ -299,7 +310,8 @@ void run_hals(cnmf_context* c, HalsRun& hr, int normalize_a, double alpha, doubl
   }
 }
 
-double recon_error(cnmf_context* c, const XView& X, const float* a_cm, const float* b_cm, int k) {
+double recon_error(cnmf_context* c, const XView& X, const double* a_cm, const double* b_cm,
+                   int k) {
   double* out = c->ws<double>("err_out", 1);
   void* ws = c->ws<char>("metrics_ws", metrics_ws_bytes(X.d, X.n, c->nsm));
   launch_recon_error(X.x, X.ldx, X.d, X.n, a_cm, b_cm, k, out, ws, c->nsm, c->stream);
@@ -463,6 +475,21 @@ void run_device_impl(cnmf_context* c, const float* x_in, int64_t d, int64_t n, i
     it = e + 1;
   }
 
+  if (st.prof) {
+    long long pr[32];
+    CK(cudaMemcpy(pr, st.prof, sizeof pr, cudaMemcpyDeviceToHost));
+    static const char* names[17] = {"A prep+g", "A h", "A sweep", "A norm-xchg", "A partial",
+                                    "A xchg1", "A slice", "A xchg2", "A gram w", "B prep",
+                                    "B sweep", "B partial", "B xchg1", "B zero", "B slice",
+                                    "B xchg2", "B gram g"};
+    long long tot = 0;
+    for (int i = 0; i < 17; ++i) tot += pr[i];
+    const double its = (double)std::max<uint64_t>(1, t.iterations_run);
+    std::fprintf(stderr, "[cnmf profile] HALS CTA0 cycles per iteration (%.0f its):\n", its);
+    for (int i = 0; i < 17; ++i)
+      std::fprintf(stderr, "  %-12s %10.0f  %5.1f%%\n", names[i], (double)pr[i] / its,
+                   100.0 * pr[i] / std::max<long long>(1, tot));
+  }
   // gini(B) (solvers.cpp:286-291) and the factors in reference layout.
   {
     const int64_t count = n * (int64_t)k;
@@ -634,8 +661,8 @@ cnmf_status cnmf_initialize(cnmf_context* c, uint64_t d, uint64_t n, uint64_t k,
   return guarded(c, [&] {
     if (d == 0 || n == 0 || k == 0)
       throw Fail(CNMF_ERR_CONFIG, "initialize requires positive dimensions");
-    float* acm = c->ws<float>("init_acm", d * k);
-    float* bcm = c->ws<float>("init_bcm", n * k);
+    double* acm = c->ws<double>("init_acm", d * k);
+    double* bcm = c->ws<double>("init_bcm", n * k);
     gen_init(c, seed, (int64_t)d, (int64_t)n, (int)k, acm, bcm);
     launch_cm_to_rm(acm, (int64_t)d, (int)k, a, c->stream);
     launch_cm_to_rm(bcm, (int64_t)n, (int)k, b, c->stream);
@@ -791,8 +818,8 @@ cnmf_status cnmf_reconstruction_error(cnmf_context* c, const float* x, uint64_t 
   return guarded(c, [&] {
     if (k == 0 || k > 128) throw Fail(CNMF_ERR_UNSUPPORTED, "k must be in [1, 128]");
     const XView X = prepare_x(c, x, (int64_t)d, (int64_t)n, (int64_t)ldx);
-    float* acm = c->ws<float>("re_acm", d * k);
-    float* bcm = c->ws<float>("re_bcm", n * k);
+    double* acm = c->ws<double>("re_acm", d * k);
+    double* bcm = c->ws<double>("re_bcm", n * k);
     launch_rm_to_cm(a, (int64_t)d, (int)k, acm, c->stream);
     launch_rm_to_cm(b, (int64_t)n, (int)k, bcm, c->stream);
     *out = recon_error(c, X, acm, bcm, (int)k);

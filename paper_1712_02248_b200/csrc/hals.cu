@@ -28,8 +28,19 @@ namespace cnmf {
 namespace {
 
 constexpr int kThreads = 256;
-constexpr int kChunkB = 64;  // B rows per sweep chunk (4 threads per row)
+constexpr int kNB = 8;        // columns per block of the blocked sweeps
+constexpr int kMaxRPT = 3;    // A rows per thread (rows per CTA <= 768)
 constexpr double kDead = 1e-12;  // solvers.cpp:19
+
+// Precision.  The HALS state (A, B, h = X-check B-check, p = X-hat^T A-hat,
+// A-hat, B-check, g, w) is fp64 like the reference's; only the compressed
+// views and projectors (X-check, X-hat^T, L, R^T) are fp32.  Measured on the
+// C2 configuration: the trajectory passes through a locally unstable stretch
+// (iterations ~5-20) that amplifies per-iteration rounding ~5x per
+// iteration, so fp32 state or fp32 accumulation moves it by 1e-4 while fp64
+// state keeps it at the compression's 1e-6.  fp32 operands are converted
+// once when staged (F2F.F64.F32 issues at 1/4 the DFMA rate,
+// tools/ubench_fp64.cu).
 
 struct HalsArgs {
   HalsState st;
@@ -38,129 +49,297 @@ struct HalsArgs {
   int it_begin, it_end, start_half, start_col;
   int skip_dead;       // column whose dead check is skipped once (just redrawn), or -1
   int rows_a, rows_b;  // rows per CTA
+  unsigned long long epoch0;
 };
 
-__host__ __device__ inline int64_t align4(int64_t v) { return (v + 3) & ~int64_t(3); }
+// Stages rows [r0, r0 + 64) of a global fp32 matrix (ld lp) as fp64 into
+// stage (stride lp + 1), zero beyond nrows.  float4 loads, all issued first.
+__device__ __forceinline__ void stage64_f32(const float* __restrict__ in, int r0, int nrows,
+                                            int lp, double* stage) {
+  const int lpp = lp + 1, q4 = lp >> 2, total = 64 * q4;
+  float4 v[8];
+#pragma unroll
+  for (int u = 0; u < 8; ++u) {
+    const int e = threadIdx.x + kThreads * u;
+    v[u] = make_float4(0.f, 0.f, 0.f, 0.f);
+    if (e < total) {
+      const int rr = e / q4, c4 = e - rr * q4;
+      if (r0 + rr < nrows)
+        v[u] = __ldg(reinterpret_cast<const float4*>(in + (int64_t)(r0 + rr) * lp) + c4);
+    }
+  }
+#pragma unroll
+  for (int u = 0; u < 8; ++u) {
+    const int e = threadIdx.x + kThreads * u;
+    if (e < total) {
+      const int rr = e / q4, c4 = e - rr * q4;
+      double* d = stage + rr * lpp + 4 * c4;
+      d[0] = v[u].x;
+      d[1] = v[u].y;
+      d[2] = v[u].z;
+      d[3] = v[u].w;
+    }
+  }
+}
 
-// out(r, c) = sum_{l'} In[r, l'] * M[l', c] for r < nrows, c < k.
-// In: global rows with leading dimension lp; M: shared lp x k (row-major).
+// out(r, c) = sum_q In[r, q] * M[q, c] for r < nrows, c < k (fp64).  In:
+// global fp32 rows (ld lp) staged 64 at a time as fp64; M: shared fp64 lp x k.
+// Thread (rg, cg) owns rows rg + 16 i (i < 4) and columns cg + 16 t (t < 8).
 template <typename Out>
 __device__ void rows_times_small(const float* __restrict__ in, int nrows, int lp, int k,
-                                 const float* __restrict__ M, float* stage, Out out) {
+                                 const double* __restrict__ M, double* stage, Out out) {
   const int lpp = lp + 1;
-  const int r = threadIdx.x & 31, cg = threadIdx.x >> 5;
-  for (int r0 = 0; r0 < nrows; r0 += 32) {
+  const int rg = threadIdx.x & 15, cg = threadIdx.x >> 4;
+  const int nt = (k - cg + 15) >> 4;
+  for (int r0 = 0; r0 < nrows; r0 += 64) {
     __syncthreads();
-    for (int e = threadIdx.x; e < 32 * lp; e += kThreads) {
-      const int rr = e / lp, cc = e - rr * lp;
-      stage[rr * lpp + cc] = (r0 + rr < nrows) ? in[(int64_t)(r0 + rr) * lp + cc] : 0.f;
-    }
+    stage64_f32(in, r0, nrows, lp, stage);
     __syncthreads();
-    float acc[16];
+    double acc[4][8];
 #pragma unroll
-    for (int t = 0; t < 16; ++t) acc[t] = 0.f;
+    for (int i = 0; i < 4; ++i)
+#pragma unroll
+      for (int t = 0; t < 8; ++t) acc[i][t] = 0.0;
     for (int q = 0; q < lp; ++q) {
-      const float xv = stage[r * lpp + q];
-      const float* mrow = M + q * k;
+      double xv[4];
 #pragma unroll
-      for (int t = 0; t < 16; ++t) {
-        const int c = cg + 8 * t;
-        if (c < k) acc[t] = fmaf(xv, mrow[c], acc[t]);
+      for (int i = 0; i < 4; ++i) xv[i] = stage[(rg + 16 * i) * lpp + q];
+      const double* mrow = M + q * k + cg;
+#pragma unroll
+      for (int t = 0; t < 8; ++t) {
+        if (t < nt) {
+          const double mv = mrow[16 * t];
+#pragma unroll
+          for (int i = 0; i < 4; ++i) acc[i][t] = fma(xv[i], mv, acc[i][t]);
+        }
       }
     }
-    if (r0 + r < nrows) {
 #pragma unroll
-      for (int t = 0; t < 16; ++t) {
-        const int c = cg + 8 * t;
-        if (c < k) out(r0 + r, c, acc[t]);
+    for (int i = 0; i < 4; ++i) {
+      const int r = r0 + rg + 16 * i;
+      if (r < nrows) {
+#pragma unroll
+        for (int t = 0; t < 8; ++t)
+          if (t < nt) out(r, cg + 16 * t, acc[i][t]);
       }
     }
   }
   __syncthreads();
 }
 
-// Per-CTA partial P[l', c] = sum_r In[r, l'] * F(r, c), written as fp64 to
-// part (lp x k).  Thread t owns 4x4 output blocks t, t+256, t+512, t+768.
-template <typename FAcc>
+// Per-CTA partial P[l', c] = sum_r In[r, l'] * F[c][row0 + r] (fp64) into part
+// (global lp x k).  In: fp32 rows (ld lp); F: column-major fp64 state (ld
+// ldf).  Staged 32 rows at a time; 4x4 output blocks, one per thread; with
+// fewer blocks than threads the rows are split over `ng` groups combined in a
+// fixed order through `red` (may alias the staging).
 __device__ void small_partial(const float* __restrict__ in, int nrows, int l, int lp, int k,
-                              FAcc F, float* stage, double* __restrict__ part) {
-  const int lpp = lp + 1;
+                              const double* __restrict__ F, int64_t ldf, double* stage,
+                              double* fst, double* red, double* __restrict__ part) {
+  const int lpp = lp + 1, kp1 = k + 1;
   const int nbl = (l + 3) >> 2, nbc = (k + 3) >> 2, nb = nbl * nbc;
-  float acc[4][16];
+  const int ng = nb >= kThreads ? 1 : min(16, kThreads / nb);
+  for (int e = threadIdx.x; e < lp * k; e += kThreads) part[e] = 0.0;
+  for (int g0 = 0; g0 < nb; g0 += kThreads) {
+    const int slot = ng > 1 ? (int)threadIdx.x % nb : (int)threadIdx.x;
+    const int grp = ng > 1 ? (int)threadIdx.x / nb : 0;
+    const int b = g0 + slot;
+    const bool own = b < nb && grp < ng;
+    const int bl = own ? b / nbc : 0, bc = own ? b - bl * nbc : 0;
+    double acc[16];
 #pragma unroll
-  for (int t = 0; t < 4; ++t)
+    for (int i = 0; i < 16; ++i) acc[i] = 0.0;
+    for (int r0 = 0; r0 < nrows; r0 += 32) {
+      const int rmax = min(32, nrows - r0);
+      __syncthreads();
+      {
+        const int q4 = lp >> 2, total = 32 * q4;
+        float4 v[4];
 #pragma unroll
-    for (int i = 0; i < 16; ++i) acc[t][i] = 0.f;
-  for (int r0 = 0; r0 < nrows; r0 += 32) {
-    __syncthreads();
-    for (int e = threadIdx.x; e < 32 * lp; e += kThreads) {
-      const int rr = e / lp, cc = e - rr * lp;
-      stage[rr * lpp + cc] = (r0 + rr < nrows) ? in[(int64_t)(r0 + rr) * lp + cc] : 0.f;
-    }
-    __syncthreads();
-    const int rmax = min(32, nrows - r0);
+        for (int u = 0; u < 4; ++u) {
+          const int e = threadIdx.x + kThreads * u;
+          v[u] = make_float4(0.f, 0.f, 0.f, 0.f);
+          if (e < total) {
+            const int rr = e / q4, c4 = e - rr * q4;
+            if (rr < rmax)
+              v[u] = __ldg(reinterpret_cast<const float4*>(in + (int64_t)(r0 + rr) * lp) + c4);
+          }
+        }
+        double fv[16];
 #pragma unroll
-    for (int t = 0; t < 4; ++t) {
-      const int b = threadIdx.x + kThreads * t;
-      if (b >= nb) break;
-      const int bl = b / nbc, bc = b - bl * nbc;
-      for (int rr = 0; rr < rmax; ++rr) {
-        float xi[4], fj[4];
+        for (int u = 0; u < 16; ++u) {
+          const int e = threadIdx.x + kThreads * u;
+          const int c = e >> 5, rr = e & 31;
+          fv[u] = (c < k && rr < rmax) ? __ldcg(F + (int64_t)c * ldf + r0 + rr) : 0.0;
+        }
 #pragma unroll
-        for (int i = 0; i < 4; ++i) xi[i] = stage[rr * lpp + 4 * bl + i];
+        for (int u = 0; u < 4; ++u) {
+          const int e = threadIdx.x + kThreads * u;
+          if (e < total) {
+            const int rr = e / q4, c4 = e - rr * q4;
+            double* d = stage + rr * lpp + 4 * c4;
+            d[0] = v[u].x;
+            d[1] = v[u].y;
+            d[2] = v[u].z;
+            d[3] = v[u].w;
+          }
+        }
 #pragma unroll
-        for (int j = 0; j < 4; ++j) fj[j] = (4 * bc + j < k) ? F(r0 + rr, 4 * bc + j) : 0.f;
+        for (int u = 0; u < 16; ++u) {
+          const int e = threadIdx.x + kThreads * u;
+          const int c = e >> 5, rr = e & 31;
+          if (c < k) fst[rr * kp1 + c] = fv[u];
+        }
+      }
+      __syncthreads();
+      if (own) {
+        for (int rr = grp; rr < rmax; rr += ng) {
+          double xi[4], fj[4];
 #pragma unroll
-        for (int i = 0; i < 4; ++i)
+          for (int i = 0; i < 4; ++i) xi[i] = stage[rr * lpp + 4 * bl + i];
 #pragma unroll
-          for (int j = 0; j < 4; ++j) acc[t][4 * i + j] = fmaf(xi[i], fj[j], acc[t][4 * i + j]);
+          for (int j = 0; j < 4; ++j) fj[j] = (4 * bc + j < k) ? fst[rr * kp1 + 4 * bc + j] : 0.0;
+#pragma unroll
+          for (int i = 0; i < 4; ++i)
+#pragma unroll
+            for (int j = 0; j < 4; ++j) acc[4 * i + j] = fma(xi[i], fj[j], acc[4 * i + j]);
+        }
       }
     }
-  }
-  for (int e = threadIdx.x; e < lp * k; e += kThreads) part[e] = 0.0;
-  __syncthreads();
+    if (ng > 1) {
+      __syncthreads();
+      if (own)
 #pragma unroll
-  for (int t = 0; t < 4; ++t) {
-    const int b = threadIdx.x + kThreads * t;
-    if (b >= nb) break;
-    const int bl = b / nbc, bc = b - bl * nbc;
+        for (int i = 0; i < 16; ++i) red[(grp * nb + slot) * 16 + i] = acc[i];
+      __syncthreads();
+      if (own && grp == 0)
+        for (int g = 1; g < ng; ++g)
+#pragma unroll
+          for (int i = 0; i < 16; ++i) acc[i] += red[(g * nb + slot) * 16 + i];
+    }
+    if (own && grp == 0) {
+#pragma unroll
+      for (int i = 0; i < 4; ++i)
+#pragma unroll
+        for (int j = 0; j < 4; ++j) {
+          const int li = 4 * bl + i, cj = 4 * bc + j;
+          if (li < l && cj < k) part[li * k + cj] = acc[4 * i + j];
+        }
+    }
+  }
+  __syncthreads();
+}
+
+// Grid-wide barrier with payload visibility: every CTA's global writes made
+// before the call are visible to every CTA after it.  A monotonic arrival
+// counter (reset per run; `ep` counts barriers) -- measured as the cheapest
+// deterministic exchange on B200 (tools/ubench_allreduce.cu: ~2.9k cycles at
+// 4 CTAs, ~4.1k at 148, including the read of the per-CTA partials).
+__device__ __forceinline__ void exchange(const HalsState& S, int G, int /*cta*/,
+                                         unsigned long long& ep) {
+  ++ep;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    __threadfence();
+    atomicAdd(S.bar, 1u);
+    const unsigned target = (unsigned)(ep * (unsigned long long)G);
+    unsigned v;
+    do {
+      asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(S.bar) : "memory");
+    } while ((int)(v - target) < 0);
+  }
+  __syncthreads();
+}
+
+// All-reduce of one fp64 per CTA: partial -> barrier -> every CTA sums the G
+// partials in the same fixed order (lanes, then a warp tree).  Partials are
+// double-buffered by barrier parity.
+__device__ double allreduce(const HalsState& S, int G, int cta, unsigned long long& ep,
+                            double v, double* s_out) {
+  double* slot = S.npart + ((ep + 1) & 1ULL) * G;
+  if (threadIdx.x == 0) slot[cta] = v;
+  exchange(S, G, cta, ep);
+  if (threadIdx.x < 32) {
+    double t = 0.0;
+    for (int b = threadIdx.x; b < G; b += 32) t += __ldcg(slot + b);
+    t = warp_sum(t);
+    if (threadIdx.x == 0) *s_out = t;
+  }
+  __syncthreads();
+  return *s_out;
+}
+
+// After an exchange of per-CTA partials (G x nel doubles): CTA c reduces its
+// slice of entries in a fixed order (lanes over CTAs, then a warp tree).
+__device__ void slice_reduce(const double* __restrict__ part, int G, int nel,
+                             double* __restrict__ dst) {
+  const int per = (nel + G - 1) / G;
+  const int e0 = blockIdx.x * per, e1 = min(nel, e0 + per);
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  for (int e = e0 + wid; e < e1; e += kThreads / 32) {
+    double s = 0.0;
+#pragma unroll 5
+    for (int b = lane; b < G; b += 32) s += __ldcg(part + (int64_t)b * nel + e);
+    s = warp_sum(s);
+    if (lane == 0) dst[e] = s;
+  }
+}
+
+// Gram of a final lp x k fp64 matrix M (rows >= l are zero), fp64:
+// out[a*k+b] = sum_{l'<l} M[l',a] M[l',b], into this CTA's scratch.  `st` is
+// free shared memory for l x k4 doubles.
+__device__ void gram_to_scratch(const double* __restrict__ M, int l, int k, double* st,
+                                double* __restrict__ out) {
+  const int k4 = (k + 3) & ~3;
+  __syncthreads();
+  for (int e = threadIdx.x; e < l * k4; e += kThreads) {
+    const int r = e / k4, c = e - r * k4;
+    st[e] = c < k ? __ldcg(M + r * k + c) : 0.0;
+  }
+  __syncthreads();
+  const int nb4 = k4 >> 2, nb = nb4 * (nb4 + 1) / 2;
+  for (int b = threadIdx.x; b < nb; b += kThreads) {
+    int bi = 0, rem = b;
+    while (rem >= nb4 - bi) {
+      rem -= nb4 - bi;
+      ++bi;
+    }
+    const int bj = bi + rem;
+    double acc[16];
+#pragma unroll
+    for (int i = 0; i < 16; ++i) acc[i] = 0.0;
+    for (int r = 0; r < l; ++r) {
+      double xv[4], yv[4];
+#pragma unroll
+      for (int i = 0; i < 4; ++i) {
+        xv[i] = st[r * k4 + 4 * bi + i];
+        yv[i] = st[r * k4 + 4 * bj + i];
+      }
+#pragma unroll
+      for (int i = 0; i < 4; ++i)
+#pragma unroll
+        for (int j = 0; j < 4; ++j) acc[4 * i + j] = fma(xv[i], yv[j], acc[4 * i + j]);
+    }
 #pragma unroll
     for (int i = 0; i < 4; ++i)
 #pragma unroll
       for (int j = 0; j < 4; ++j) {
-        const int li = 4 * bl + i, cj = 4 * bc + j;
-        if (li < l && cj < k) part[li * k + cj] = (double)acc[t][4 * i + j];
+        const int a = 4 * bi + i, c = 4 * bj + j;
+        if (a < k && c < k) {
+          out[a * k + c] = acc[4 * i + j];
+          out[c * k + a] = acc[4 * i + j];
+        }
       }
   }
-}
-
-// Fixed-order sum of the grid's per-CTA partials into dst (lp x k).
-__device__ void reduce_partials(const double* __restrict__ part, int G, int n_el,
-                                double* __restrict__ dst) {
-  const int gt = blockIdx.x * kThreads + threadIdx.x, gs = gridDim.x * kThreads;
-  for (int e = gt; e < n_el; e += gs) {
-    double s = 0.0;
-    for (int b = 0; b < G; ++b) s += part[(int64_t)b * n_el + e];
-    dst[e] = s;
-  }
-}
-
-// gram[a*k+b] = sum_{l' < l} M[l'*k+a] * M[l'*k+b], fp64, grid-distributed.
-__device__ void gram_small(const double* __restrict__ M, int l, int k, double* __restrict__ gram) {
-  const int gt = blockIdx.x * kThreads + threadIdx.x, gs = gridDim.x * kThreads;
-  for (int e = gt; e < k * k; e += gs) {
-    const int a = e / k, b = e - a * k;
-    double s = 0.0;
-    for (int q = 0; q < l; ++q) s += M[q * k + a] * M[q * k + b];
-    gram[e] = s;
-  }
+  __syncthreads();
 }
 
 __global__ void __launch_bounds__(kThreads, 1) hals_kernel(const HalsArgs p) {
-  extern __shared__ __align__(16) float smem[];
-  __shared__ double red[kThreads / 32];
+  extern __shared__ __align__(16) double smem[];
+  __shared__ double red8[kThreads / 32];
   __shared__ double s_total;
-  __shared__ int zf[128];
+  __shared__ unsigned zmask[4];
+  __shared__ double s_diag[128];  // g_jj / w_jj (divisors and dead checks)
+  __shared__ long long s_prof[17];
 
   const HalsState& S = p.st;
   const int G = gridDim.x, cta = blockIdx.x, tid = threadIdx.x;
@@ -170,250 +349,319 @@ __global__ void __launch_bounds__(kThreads, 1) hals_kernel(const HalsArgs p) {
   const int64_t b_lo = min(n, (int64_t)cta * p.rows_b), b_hi = min(n, b_lo + p.rows_b);
   const int na = (int)(a_hi - a_lo), nbr = (int)(b_hi - b_lo);
   const int nel = lp * k;
+  double* gsc = S.gsc + (int64_t)cta * k * k;
+  double* wsc = S.wsc + (int64_t)cta * k * k;
 
-  // A-half shared layout
-  float* As = smem;                                       // rows_a x kp1
-  float* U = As + align4((int64_t)p.rows_a * kp1);        // max(lp*k, k*k)
-  float* stageA = U + align4(max(lp * k, k * k));         // 32 x lpp
-  // B-half shared layout
-  float* Ah = smem;                                       // lp x k
-  float* Ws = Ah + align4(lp * k);                        // k x k
-  float* Bs = Ws + align4(k * k);                         // kChunkB x kp1
-  float* stageB = Bs + align4(kChunkB * kp1);             // 32 x (max(lpp, kp1))
+  // shared layout: products use [M lp*k | stage 64*lpp]; sweeps use [g or w k*k];
+  // partials use [stage 32*lpp | fst 32*kp1] (+ group reduction aliasing it)
+  double* Ms = smem;
+  double* stage64 = smem + lp * k;
+  double* gw = smem;
+  double* stP = smem;
+  double* fsP = smem + 32 * lpp;
 
+  const bool prof = S.prof != nullptr && cta == 0;
+  long long t_last = 0;
+  if (prof && tid == 0) {
+    for (int i = 0; i < 17; ++i) s_prof[i] = 0;
+    t_last = clock64();
+  }
+#define HALS_PROF(id)                 \
+  if (prof && tid == 0) {             \
+    const long long now_ = clock64(); \
+    s_prof[id] += now_ - t_last;      \
+    t_last = now_;                    \
+  }
+  unsigned long long ep = p.epoch0;
+  bool have_g = false, have_w = false;
+  double* bcur = S.b;  // B as of the start of the B half
+  double* bnxt = S.bold;
   int half = p.start_half, col0 = p.start_col, skip = p.skip_dead;
+  const int rpt = (na + kThreads - 1) / kThreads;  // <= kMaxRPT (hals_grid)
+
   for (int it = p.it_begin; it < p.it_end; ++it) {
     if (half == 0) {
-      // ---- A half: g, h, sweep, A-hat --------------------------------
-      gram_small(S.bchk, l, k, S.g);
-      grid_barrier(S.bar, G);
-      for (int e = tid; e < lp * k; e += kThreads) U[e] = (float)S.bchk[e];
-      for (int e = tid; e < na * k; e += kThreads) {
-        const int c = e / na, r = e - c * na;
-        As[r * kp1 + c] = S.a[(int64_t)c * d + a_lo + r];
-      }
+      // ================= A half (solvers.cpp:419-439) =====================
+      if (!have_g) gram_to_scratch(S.bchk, l, k, smem, gsc);
+      // h = X-check B-check for this CTA's rows (solvers.cpp:421)
+      for (int e = tid; e < lp * k; e += kThreads) Ms[e] = __ldcg(S.bchk + e);
+      HALS_PROF(0);
+      rows_times_small(S.xc + a_lo * lp, na, lp, k, Ms, stage64,
+                       [&](int r, int c, double v) { S.h[(int64_t)c * d + a_lo + r] = v; });
+      for (int e = tid; e < k * k; e += kThreads) gw[e] = gsc[e];
       __syncthreads();
-      rows_times_small(S.xc + a_lo * lp, na, lp, k, U, stageA,
-                       [&](int r, int c, float v) { S.h[(int64_t)c * d + a_lo + r] = v; });
-      for (int e = tid; e < k * k; e += kThreads) U[e] = (float)S.g[e];
-      int jd = k;
+      for (int e = tid; e < k; e += kThreads) s_diag[e] = gw[e * k + e];
+      __syncthreads();
+      HALS_PROF(1);
       // solvers.cpp:424 checks g_jj once per column; a column redrawn for
       // this check is not re-checked (the reference uses `if`, not `while`).
+      int jd = k;
       for (int j = col0; j < k; ++j)
-        if (j != skip && S.g[j * k + j] < kDead) { jd = j; break; }
+        if (j != skip && s_diag[j] < kDead) { jd = j; break; }
       skip = -1;
+      // Blocked column sweep (solvers.cpp:423-437).  Thread owns rows
+      // tid + 256 i.  Per block of kNB columns: acc = A g[:, block] with the
+      // current A; inside the block each update adds the fp64 deltas of the
+      // block's earlier columns.  One all-reduce per column for the norm.
+      for (int jb = col0; jb < jd; jb += kNB) {
+        const int nbj = min(kNB, jd - jb);
+        double acc[kMaxRPT][kNB], dl[kMaxRPT][kNB];
+#pragma unroll
+        for (int i = 0; i < kMaxRPT; ++i)
+#pragma unroll
+          for (int t = 0; t < kNB; ++t) {
+            acc[i][t] = 0.0;
+            dl[i][t] = 0.0;
+          }
+        for (int c0 = 0; c0 < k; c0 += 8) {  // 8 columns of A in flight per row
+          double av8[kMaxRPT][8];
+#pragma unroll
+          for (int i = 0; i < kMaxRPT; ++i) {
+            const int r = tid + kThreads * i;
+            const bool ok = i < rpt && r < na;
+#pragma unroll
+            for (int cc = 0; cc < 8; ++cc)
+              av8[i][cc] = (ok && c0 + cc < k) ? __ldcg(S.a + (int64_t)(c0 + cc) * d + a_lo + r) : 0.0;
+          }
+#pragma unroll
+          for (int cc = 0; cc < 8; ++cc) {
+            if (c0 + cc >= k) break;
+            double gv[kNB];
+#pragma unroll
+            for (int t = 0; t < kNB; ++t) gv[t] = t < nbj ? gw[(c0 + cc) * k + jb + t] : 0.0;
+#pragma unroll
+            for (int i = 0; i < kMaxRPT; ++i)
+#pragma unroll
+              for (int t = 0; t < kNB; ++t) acc[i][t] = fma(av8[i][cc], gv[t], acc[i][t]);
+          }
+        }
+        double hv[kMaxRPT], av[kMaxRPT];
+#pragma unroll
+        for (int i = 0; i < kMaxRPT; ++i) {
+          const int r = tid + kThreads * i;
+          const bool ok = i < rpt && r < na;
+          hv[i] = ok ? __ldcg(S.h + (int64_t)jb * d + a_lo + r) : 0.0;
+          av[i] = ok ? __ldcg(S.a + (int64_t)jb * d + a_lo + r) : 0.0;
+        }
+        HALS_PROF(2);
+#pragma unroll
+        for (int t = 0; t < kNB; ++t) {
+          if (t >= nbj) break;
+          const int j = jb + t;
+          const double gjj = s_diag[j];
+          double nrm = 0.0, vv[kMaxRPT];
+#pragma unroll
+          for (int i = 0; i < kMaxRPT; ++i) {
+            vv[i] = 0.0;
+            const int r = tid + kThreads * i;
+            if (i < rpt && r < na) {  // solvers.cpp:430-434
+              double s = acc[i][t];
+#pragma unroll
+              for (int u = 0; u < kNB; ++u)
+                if (u < t) s = fma(dl[i][u], gw[(jb + u) * k + j], s);
+              const double v = av[i] + (hv[i] - s) / gjj;
+              vv[i] = v > 0.0 ? v : 0.0;
+              nrm = fma(vv[i], vv[i], nrm);
+            }
+          }
+          // prefetch the next column's h and a while the norm is reduced
+          double hn[kMaxRPT], an[kMaxRPT];
+#pragma unroll
+          for (int i = 0; i < kMaxRPT; ++i) {
+            const int r = tid + kThreads * i;
+            const bool ok = i < rpt && r < na && t + 1 < nbj;
+            hn[i] = ok ? __ldcg(S.h + (int64_t)(j + 1) * d + a_lo + r) : 0.0;
+            an[i] = ok ? __ldcg(S.a + (int64_t)(j + 1) * d + a_lo + r) : 0.0;
+          }
+          const double cta_nrm = block_sum(nrm, red8);
+          HALS_PROF(2);
+          const double total = allreduce(S, G, cta, ep, cta_nrm, &s_total);
+          HALS_PROF(3);
+          if (total == 0.0) {  // column emptied: host redraws a_j (solvers.cpp:435)
+#pragma unroll
+            for (int i = 0; i < kMaxRPT; ++i) {
+              const int r = tid + kThreads * i;
+              if (i < rpt && r < na) S.a[(int64_t)j * d + a_lo + r] = 0.0;
+            }
+            if (cta == 0 && tid == 0)
+              *S.halt = HaltInfo{1, it + 1, 0, j, kEvZeroA, bcur == S.bold, ep};
+            return;
+          }
+          const double nv = sqrt(total);
+#pragma unroll
+          for (int i = 0; i < kMaxRPT; ++i) {
+            const int r = tid + kThreads * i;
+            if (i < rpt && r < na) {  // solvers.cpp:436
+              const double nf = p.normalize_a ? vv[i] / nv : vv[i];
+              S.a[(int64_t)j * d + a_lo + r] = nf;
+              dl[i][t] = nf - av[i];
+            }
+            hv[i] = hn[i];
+            av[i] = an[i];
+          }
+        }
+      }
       __syncthreads();
-      const int q = tid & 3, rsub = tid >> 2;
-      for (int j = col0; j < jd; ++j) {
-        const float gjj = (float)S.g[j * k + j];
-        double nrm = 0.0;
-        for (int r0 = 0; r0 < na; r0 += kThreads / 4) {
-          const int r = r0 + rsub;
-          float s = 0.f;
-          if (r < na)
-            for (int c = q; c < k; c += 4) s = fmaf(As[r * kp1 + c], U[c * k + j], s);
-          s += __shfl_xor_sync(0xffffffffu, s, 1);
-          s += __shfl_xor_sync(0xffffffffu, s, 2);
-          if (r < na && q == 0) {
-            float v = As[r * kp1 + j] + (S.h[(int64_t)j * d + a_lo + r] - s) / gjj;
-            v = v > 0.f ? v : 0.f;
-            As[r * kp1 + j] = v;
-            nrm += (double)v * (double)v;
-          }
-        }
-        const double cta_nrm = block_sum(nrm, red);
-        if (tid == 0) S.npart[(int64_t)j * G + cta] = cta_nrm;
-        grid_barrier(S.bar, G);
-        if (tid == 0) {
-          double t = 0.0;
-          for (int b = 0; b < G; ++b) t += S.npart[(int64_t)j * G + b];
-          s_total = t;
-        }
-        __syncthreads();
-        const double total = s_total;
-        if (total == 0.0) {  // column emptied: host redraws a_j (solvers.cpp:435)
-          for (int e = tid; e < na * k; e += kThreads) {
-            const int c = e / na, r = e - c * na;
-            S.a[(int64_t)c * d + a_lo + r] = As[r * kp1 + c];
-          }
-          if (cta == 0 && tid == 0) *S.halt = HaltInfo{1, it + 1, 0, j, kEvZeroA, {0, 0, 0}};
-          return;
-        }
-        if (p.normalize_a) {
-          const float nv = (float)sqrt(total);
-          for (int r = tid; r < na; r += kThreads) As[r * kp1 + j] = As[r * kp1 + j] / nv;
-        }
-        __syncthreads();
-      }
-      for (int e = tid; e < na * k; e += kThreads) {
-        const int c = e / na, r = e - c * na;
-        S.a[(int64_t)c * d + a_lo + r] = As[r * kp1 + c];
-      }
       if (jd < k) {  // dead B column: host redraws b_jd (solvers.cpp:424-428)
-        if (cta == 0 && tid == 0) *S.halt = HaltInfo{1, it + 1, 0, jd, kEvDeadB, {0, 0, 0}};
+        if (cta == 0 && tid == 0)
+          *S.halt = HaltInfo{1, it + 1, 0, jd, kEvDeadB, bcur == S.bold, ep};
         return;
       }
-      small_partial(S.lm + a_lo * lp, na, l, lp, k,
-                    [&](int r, int c) { return As[r * kp1 + c]; }, stageA,
+      // A-hat = L^T A (solvers.cpp:438): partials, exchange, slice reduce, exchange
+      small_partial(S.lm + a_lo * lp, na, l, lp, k, S.a + a_lo, d, stP, fsP, smem,
                     S.part + (int64_t)cta * nel);
-      grid_barrier(S.bar, G);
-      reduce_partials(S.part, G, nel, S.ahat);
-      grid_barrier(S.bar, G);
+      HALS_PROF(4);
+      exchange(S, G, cta, ep);
+      HALS_PROF(5);
+      slice_reduce(S.part, G, nel, S.ahat);
+      HALS_PROF(6);
+      exchange(S, G, cta, ep);
+      HALS_PROF(7);
+      gram_to_scratch(S.ahat, l, k, smem, wsc);  // w = A-hat^T A-hat (solvers.cpp:443)
+      HALS_PROF(8);
+      have_w = true;
       half = 1;
       col0 = 0;
     }
-    // ---- B half: w, p, sweep, zero check, B-check ------------------------
-    gram_small(S.ahat, l, k, S.w);
-    grid_barrier(S.bar, G);
-    for (int e = tid; e < lp * k; e += kThreads) Ah[e] = (float)S.ahat[e];
-    for (int e = tid; e < k * k; e += kThreads) Ws[e] = (float)S.w[e];
-    if (tid < 128) zf[tid] = 0;
+    // ================== B half (solvers.cpp:440-455) =======================
+    if (!have_w) gram_to_scratch(S.ahat, l, k, smem, wsc);
+    // p = X-hat^T A-hat for this CTA's rows (solvers.cpp:442)
+    for (int e = tid; e < lp * k; e += kThreads) Ms[e] = __ldcg(S.ahat + e);
+    rows_times_small(S.xht + b_lo * lp, nbr, lp, k, Ms, stage64,
+                     [&](int r, int c, double v) { S.p[(int64_t)c * n + b_lo + r] = v; });
+    for (int e = tid; e < k * k; e += kThreads) gw[e] = wsc[e];
+    if (tid < 4) zmask[tid] = 0u;
+    __syncthreads();
+    for (int e = tid; e < k; e += kThreads) s_diag[e] = gw[e * k + e];
+    __syncthreads();
     int jd = k;
     for (int j = col0; j < k; ++j)
-      if (j != skip && S.w[j * k + j] < kDead) { jd = j; break; }
+      if (j != skip && s_diag[j] < kDead) { jd = j; break; }
     skip = -1;
-    __syncthreads();
+    HALS_PROF(9);
+    // columns before col0 were updated by an earlier launch: carry them over
+    for (int c = 0; c < col0; ++c)
+      for (int r = tid; r < nbr; r += kThreads)
+        bnxt[(int64_t)c * n + b_lo + r] = bcur[(int64_t)c * n + b_lo + r];
     const bool constrained = !(p.alpha == 0.0 && p.beta == 0.0);
-    const float alpha = (float)p.alpha, beta = (float)p.beta;
-    for (int c0 = 0; c0 < nbr; c0 += kChunkB) {
-      const int nr = min(kChunkB, nbr - c0);
-      __syncthreads();
-      for (int e = tid; e < nr * k; e += kThreads) {
-        const int c = e / nr, r = e - c * nr;
-        const int64_t gi = (int64_t)c * n + b_lo + c0 + r;
-        const float v = S.b[gi];
-        Bs[r * kp1 + c] = v;
-        S.bold[gi] = v;
-      }
-      // p rows for this chunk, written into the stage tail as [r][c] (kp1 stride)
-      float* Ps = stageB + 32 * max(lpp, kp1);
-      rows_times_small(S.xht + (b_lo + c0) * lp, nr, lp, k, Ah, stageB,
-                       [&](int r, int c, float v) { Ps[r * kp1 + c] = v; });
-      const int q = tid & 3, r = tid >> 2;
-      for (int j = col0; j < jd; ++j) {
-        const float wjj = Ws[j * k + j];
-        float s = 0.f;
-        if (r < nr)
-          for (int c = q; c < k; c += 4) s = fmaf(Bs[r * kp1 + c], Ws[c * k + j], s);
-        s += __shfl_xor_sync(0xffffffffu, s, 1);
-        s += __shfl_xor_sync(0xffffffffu, s, 2);
-        if (r < nr && q == 0) {
-          const float bij = Bs[r * kp1 + j], pij = Ps[r * kp1 + j];
-          float v = constrained ? (bij * wjj + pij - s - alpha) / (wjj + beta)
-                                : bij + (pij - s) / wjj;
-          v = v > 0.f ? v : 0.f;
-          Bs[r * kp1 + j] = v;
-          if (v != 0.f) zf[j] = 1;
+    for (int r = tid; r < nbr; r += kThreads) {  // one row per thread, rows are independent
+      const int64_t gr = b_lo + r;
+      for (int jb = col0; jb < jd; jb += kNB) {
+        const int nbj = min(kNB, jd - jb);
+        double acc[kNB], dl[kNB];
+#pragma unroll
+        for (int t = 0; t < kNB; ++t) {
+          acc[t] = 0.0;
+          dl[t] = 0.0;
         }
-        __syncwarp();
-      }
-      __syncthreads();
-      for (int e = tid; e < nr * k; e += kThreads) {
-        const int c = e / nr, rr = e - c * nr;
-        S.b[(int64_t)c * n + b_lo + c0 + rr] = Bs[rr * kp1 + c];
+        for (int c0 = 0; c0 < k; c0 += 8) {  // columns < jb already live in bnxt
+          double bv8[8];
+#pragma unroll
+          for (int cc = 0; cc < 8; ++cc) {
+            const int c = c0 + cc;
+            bv8[cc] = c < k ? __ldcg((c < jb ? bnxt : bcur) + (int64_t)c * n + gr) : 0.0;
+          }
+#pragma unroll
+          for (int cc = 0; cc < 8; ++cc) {
+            if (c0 + cc >= k) break;
+#pragma unroll
+            for (int t = 0; t < kNB; ++t)
+              if (t < nbj) acc[t] = fma(bv8[cc], gw[(c0 + cc) * k + jb + t], acc[t]);
+          }
+        }
+#pragma unroll
+        for (int t = 0; t < kNB; ++t) {
+          if (t >= nbj) break;
+          const int j = jb + t;
+          double s = acc[t];
+#pragma unroll
+          for (int u = 0; u < kNB; ++u)
+            if (u < t) s = fma(dl[u], gw[(jb + u) * k + j], s);
+          const double wjj = s_diag[j];
+          const double bij = __ldcg(bcur + (int64_t)j * n + gr);
+          const double pij = __ldcg(S.p + (int64_t)j * n + gr);
+          const double v = constrained ? (bij * wjj + pij - s - p.alpha) / (wjj + p.beta)  // 502-508
+                                       : bij + (pij - s) / wjj;                            // 480-490
+          const double vf = v > 0.0 ? v : 0.0;
+          bnxt[(int64_t)j * n + gr] = vf;
+          dl[t] = vf - bij;
+          if (vf != 0.0) atomicOr(&zmask[j >> 5], 1u << (j & 31));
+        }
       }
     }
     __syncthreads();
-    if (tid < k) S.zflag[(int64_t)cta * k + tid] = zf[tid];
-    grid_barrier(S.bar, G);
-    int j0 = k;
-    for (int j = col0; j < jd; ++j) {
-      int any = 0;
-      for (int b = 0; b < G && !any; ++b) any = S.zflag[(int64_t)b * k + j];
-      if (!any) { j0 = j; break; }
+    HALS_PROF(10);
+    if (tid < 4) S.zpart[cta * 4 + tid] = zmask[tid];
+    // B-check partial = R_rows B_rows, published together with the zero flags
+    small_partial(S.rt + b_lo * lp, nbr, l, lp, k, bnxt + b_lo, n, stP, fsP, smem,
+                  S.part + (int64_t)cta * nel);
+    HALS_PROF(11);
+    exchange(S, G, cta, ep);
+    HALS_PROF(12);
+    if (tid < 4) zmask[tid] = 0u;
+    __syncthreads();
+    for (int e = tid; e < G * 4; e += kThreads) {
+      const unsigned v = __ldcg(S.zpart + e);
+      if (v) atomicOr(&zmask[e & 3], v);
     }
-    if (j0 < jd) {  // b_j0 emptied: roll later columns back, host redraws (solvers.cpp:452)
-      for (int c = j0 + 1; c < jd; ++c)
+    __syncthreads();
+    int j0 = k;
+    for (int j = col0; j < jd; ++j)
+      if (!(zmask[j >> 5] & (1u << (j & 31)))) { j0 = j; break; }
+    if (j0 < jd || jd < k) {
+      // The new B lives in bnxt.  Columns after an emptied b_j0 were computed
+      // against the zero column, and columns from jd on were never reached:
+      // both keep their old values from bcur.
+      const int from = j0 < jd ? j0 + 1 : jd;
+      for (int c = from; c < k; ++c)
         for (int r = tid; r < nbr; r += kThreads) {
           const int64_t gi = (int64_t)c * n + b_lo + r;
-          S.b[gi] = S.bold[gi];
+          bnxt[gi] = bcur[gi];
         }
-      if (cta == 0 && tid == 0) *S.halt = HaltInfo{1, it + 1, 1, j0, kEvZeroB, {0, 0, 0}};
+      if (cta == 0 && tid == 0) {
+        // pad = 1 tells the host the current B is the second buffer
+        *S.halt = j0 < jd ? HaltInfo{1, it + 1, 1, j0, kEvZeroB, bnxt == S.bold, ep}
+                          : HaltInfo{1, it + 1, 1, jd, kEvDeadA, bnxt == S.bold, ep};
+      }
       return;
     }
-    if (jd < k) {  // dead A column: host redraws a_jd (solvers.cpp:445-449)
-      if (cta == 0 && tid == 0) *S.halt = HaltInfo{1, it + 1, 1, jd, kEvDeadA, {0, 0, 0}};
-      return;
-    }
-    {
-      float* Fs = stageB + 32 * max(lpp, kp1);  // 32 x kp1 staged B rows
-      const int nbl = (l + 3) >> 2, nbc = (k + 3) >> 2, nb = nbl * nbc;
-      float acc[4][16];
-#pragma unroll
-      for (int t = 0; t < 4; ++t)
-#pragma unroll
-        for (int i = 0; i < 16; ++i) acc[t][i] = 0.f;
-      for (int r0 = 0; r0 < nbr; r0 += 32) {
-        const int rmax = min(32, nbr - r0);
-        __syncthreads();
-        for (int e = tid; e < 32 * lp; e += kThreads) {
-          const int rr = e / lp, cc = e - rr * lp;
-          stageB[rr * lpp + cc] = rr < rmax ? S.rt[(b_lo + r0 + rr) * lp + cc] : 0.f;
-        }
-        for (int e = tid; e < 32 * k; e += kThreads) {
-          const int c = e >> 5, rr = e & 31;
-          Fs[rr * kp1 + c] = rr < rmax ? S.b[(int64_t)c * n + b_lo + r0 + rr] : 0.f;
-        }
-        __syncthreads();
-#pragma unroll
-        for (int t = 0; t < 4; ++t) {
-          const int b = tid + kThreads * t;
-          if (b >= nb) break;
-          const int bl = b / nbc, bc = b - bl * nbc;
-          for (int rr = 0; rr < rmax; ++rr) {
-            float xi[4], fj[4];
-#pragma unroll
-            for (int i = 0; i < 4; ++i) xi[i] = stageB[rr * lpp + 4 * bl + i];
-#pragma unroll
-            for (int jj = 0; jj < 4; ++jj)
-              fj[jj] = (4 * bc + jj < k) ? Fs[rr * kp1 + 4 * bc + jj] : 0.f;
-#pragma unroll
-            for (int i = 0; i < 4; ++i)
-#pragma unroll
-              for (int jj = 0; jj < 4; ++jj)
-                acc[t][4 * i + jj] = fmaf(xi[i], fj[jj], acc[t][4 * i + jj]);
-          }
-        }
-      }
-      double* part = S.part + (int64_t)cta * nel;
-      for (int e = tid; e < nel; e += kThreads) part[e] = 0.0;
-      __syncthreads();
-#pragma unroll
-      for (int t = 0; t < 4; ++t) {
-        const int b = tid + kThreads * t;
-        if (b >= nb) break;
-        const int bl = b / nbc, bc = b - bl * nbc;
-#pragma unroll
-        for (int i = 0; i < 4; ++i)
-#pragma unroll
-          for (int jj = 0; jj < 4; ++jj) {
-            const int li = 4 * bl + i, cj = 4 * bc + jj;
-            if (li < l && cj < k) part[li * k + cj] = (double)acc[t][4 * i + jj];
-          }
-      }
-    }
-    grid_barrier(S.bar, G);
-    reduce_partials(S.part, G, nel, S.bchk);
-    grid_barrier(S.bar, G);
+    HALS_PROF(13);
+    slice_reduce(S.part, G, nel, S.bchk);
+    HALS_PROF(14);
+    exchange(S, G, cta, ep);
+    HALS_PROF(15);
+    gram_to_scratch(S.bchk, l, k, smem, gsc);  // g for the next A half (solvers.cpp:422)
+    HALS_PROF(16);
+    have_g = true;
+    double* tb = bcur;
+    bcur = bnxt;
+    bnxt = tb;
     half = 0;
     col0 = 0;
   }
-  if (cta == 0 && tid == 0) *S.halt = HaltInfo{0, p.it_end, 0, 0, 0, {0, 0, 0}};
+  if (cta == 0 && tid == 0) {
+    *S.halt = HaltInfo{0, p.it_end, 0, 0, 0, bcur == S.bold, ep};
+    if (prof)
+      for (int i = 0; i < 17; ++i) S.prof[i] += s_prof[i];
+  }
+#undef HALS_PROF
 }
 
-size_t hals_smem_bytes(const HalsState& st, int rows_a) {
-  const int k = st.k, lp = st.lp, kp1 = k + 1, lpp = lp + 1;
-  const int64_t a_half = align4((int64_t)rows_a * kp1) + align4(std::max(lp * k, k * k)) +
-                         32 * lpp;
-  const int64_t b_half = align4(lp * k) + align4(k * k) + align4(kChunkB * kp1) +
-                         32 * std::max(lpp, kp1) + 32 * kp1 + (int64_t)kChunkB * kp1;
-  return (size_t)std::max(a_half, b_half) * sizeof(float);
+// Shared memory (bytes): the max over phases.
+size_t hals_smem_bytes(const HalsState& st, int /*rows_a*/) {
+  const int64_t k = st.k, lp = st.lp, l = st.l, kp1 = k + 1, lpp = lp + 1;
+  const int64_t k4 = (k + 3) & ~3;
+  const int64_t prod = lp * k + 64 * lpp;
+  const int64_t sweep = k * k;
+  const int64_t part = std::max<int64_t>(32 * lpp + 32 * kp1, 16 * kThreads);
+  const int64_t gram = l * k4;
+  return (size_t)std::max(std::max(prod, sweep), std::max(part, gram)) * sizeof(double);
 }
 
 // Column-wise compress_factor_a / compress_factor_b (compression.cpp:90-96):
 // one CTA per (l', c) output, fixed-order fp64 sum over the rows.
 __global__ void compress_factor_kernel(const float* __restrict__ basis, int64_t rows, int lp,
-                                       const float* __restrict__ f_cm, int k, int column,
+                                       const double* __restrict__ f_cm, int k, int column,
                                        int l, double* __restrict__ out) {
   __shared__ double red[32];
   const int li = blockIdx.x;
@@ -421,19 +669,19 @@ __global__ void compress_factor_kernel(const float* __restrict__ basis, int64_t 
   double s = 0.0;
   if (li < l)
     for (int64_t i = threadIdx.x; i < rows; i += blockDim.x)
-      s += (double)basis[i * lp + li] * (double)f_cm[(int64_t)c * rows + i];
+      s += (double)basis[i * lp + li] * f_cm[(int64_t)c * rows + i];
   s = block_sum(s, red);
   if (threadIdx.x == 0) out[li * k + c] = li < l ? s : 0.0;
 }
 
-__global__ void normalize_column_kernel(float* __restrict__ a_cm, int64_t d, int j) {
+__global__ void normalize_column_kernel(double* __restrict__ a_cm, int64_t d, int j) {
   __shared__ double red[32];
-  float* col = a_cm + (int64_t)j * d;
+  double* col = a_cm + (int64_t)j * d;
   double s = 0.0;
-  for (int64_t i = threadIdx.x; i < d; i += blockDim.x) s += (double)col[i] * (double)col[i];
+  for (int64_t i = threadIdx.x; i < d; i += blockDim.x) s += col[i] * col[i];
   s = block_sum(s, red);
   if (s == 0.0) return;
-  const float nv = (float)sqrt(s);
+  const double nv = sqrt(s);
   for (int64_t i = threadIdx.x; i < d; i += blockDim.x) col[i] = col[i] / nv;
 }
 
@@ -454,7 +702,7 @@ int hals_grid(const HalsState& st, int nsm) {
 
 cudaError_t launch_hals(const HalsState& st, int normalize_a, double alpha, double beta,
                         int it_begin, int it_end, int start_half, int start_col, int skip_dead,
-                        int grid, cudaStream_t s) {
+                        unsigned long long epoch0, int grid, cudaStream_t s) {
   HalsArgs a;
   a.st = st;
   a.normalize_a = normalize_a;
@@ -465,6 +713,7 @@ cudaError_t launch_hals(const HalsState& st, int normalize_a, double alpha, doub
   a.start_half = start_half;
   a.start_col = start_col;
   a.skip_dead = skip_dead;
+  a.epoch0 = epoch0;
   a.rows_a = rows_per_cta(st.d, grid);
   a.rows_b = rows_per_cta(st.n, grid);
   const size_t smem = hals_smem_bytes(st, a.rows_a);
@@ -489,7 +738,7 @@ void launch_compress_factors(const HalsState& st, int which, int column, cudaStr
                                                 st.bchk);
 }
 
-void launch_normalize_column(float* a_cm, int64_t d, int j, cudaStream_t s) {
+void launch_normalize_column(double* a_cm, int64_t d, int j, cudaStream_t s) {
   note_launches(1);
   normalize_column_kernel<<<1, 1024, 0, s>>>(a_cm, d, j);
 }

@@ -37,10 +37,10 @@ void launch_normal_map(const uint64_t* words, uint64_t count, int cols, int ld, 
                        int* flag, int nsm, cudaStream_t s);
 void launch_normal_exact(const uint64_t* words, uint64_t nwords, uint64_t count, int cols, int ld,
                          float* out, int* flag, cudaStream_t s);
-void launch_uniform_init(const uint64_t* words, uint64_t d, uint64_t n, int k, float* a_cm,
-                         float* b_cm, int* flag, int nsm, cudaStream_t s);
+void launch_uniform_init(const uint64_t* words, uint64_t d, uint64_t n, int k, double* a_cm,
+                         double* b_cm, int* flag, int nsm, cudaStream_t s);
 void launch_uniform_init_exact(const uint64_t* words, uint64_t nwords, uint64_t d, uint64_t n,
-                               int k, float* a_cm, float* b_cm, int* flag, uint64_t* consumed,
+                               int k, double* a_cm, double* b_cm, int* flag, uint64_t* consumed,
                                cudaStream_t s);
 
 // ---- xstream.cu: the X-streaming contractions ----------------------------
@@ -68,15 +68,15 @@ size_t metrics_ws_bytes(int64_t d, int64_t n, int nsm);
 void launch_check_data(const float* x, int64_t ldx, int64_t d, int64_t n, int* flag,
                        double* norm_sq, void* ws, int nsm, cudaStream_t st);
 // 1/2 ||X - A B^T||^2 with column-major A_cm (k x d), B_cm (k x n).
-void launch_recon_error(const float* x, int64_t ldx, int64_t d, int64_t n, const float* a_cm,
-                        const float* b_cm, int k, double* out, void* ws, int nsm,
+void launch_recon_error(const float* x, int64_t ldx, int64_t d, int64_t n, const double* a_cm,
+                        const double* b_cm, int k, double* out, void* ws, int nsm,
                         cudaStream_t st);
 size_t gini_ws_bytes(int64_t count);
-void launch_gini(const float* b_cm, int64_t count, double* out, void* ws, size_t ws_bytes,
+void launch_gini(const double* b_cm, int64_t count, double* out, void* ws, size_t ws_bytes,
                  cudaStream_t st);
-// column-major (k x rows) -> row-major (rows x k), fp32
-void launch_cm_to_rm(const float* cm, int64_t rows, int k, float* rm, cudaStream_t st);
-void launch_rm_to_cm(const float* rm, int64_t rows, int k, float* cm, cudaStream_t st);
+// fp64 column-major (k x rows) <-> fp32 row-major (rows x k)
+void launch_cm_to_rm(const double* cm, int64_t rows, int k, float* rm, cudaStream_t st);
+void launch_rm_to_cm(const float* rm, int64_t rows, int k, double* cm, cudaStream_t st);
 // Copy an unpadded row-major (rows x l) matrix into an lp-padded one and back.
 void launch_pad_cols(const float* src, int64_t rows, int l, float* dst, int lp, cudaStream_t st);
 void launch_unpad_cols(const float* src, int64_t rows, int lp, float* dst, int l,
@@ -91,7 +91,8 @@ struct HaltInfo {
   int half;    // 0 = A half-sweep, 1 = B half-sweep
   int column;
   int kind;    // 1 dead B column (g_jj), 2 zero A column, 3 dead A column (w_jj), 4 zero B column
-  int pad[3];
+  int pad;
+  unsigned long long last_epoch;  // exchange epoch reached (next launch starts above it)
 };
 enum { kEvDeadB = 1, kEvZeroA = 2, kEvDeadA = 3, kEvZeroB = 4 };
 
@@ -102,33 +103,36 @@ struct HalsState {
   const float* xht;  // X-hat^T = X^T L, n x lp
   const float* lm;   // L, d x lp
   const float* rt;   // R^T, n x lp
-  float* a;          // A, column-major k x d
-  float* b;          // B, column-major k x n
-  float* bold;       // B backup for the zero-column rollback, k x n
-  float* h;          // X-check B-check, column-major k x d
+  double* a;         // A, column-major k x d (fp64 state)
+  double* b;         // B, column-major k x n
+  double* bold;      // second B buffer (double-buffered B half), k x n
+  double* h;         // X-check B-check, column-major k x d
   double* ahat;      // A-hat = L^T A, lp x k
   double* bchk;      // B-check = R B, lp x k
-  double* g;         // B-check^T B-check, k x k
-  double* w;         // A-hat^T A-hat, k x k
+  double* p;         // X-hat^T A-hat, column-major k x n
+  double* gsc;       // [grid][k*k] per-CTA copy of g = B-check^T B-check (fp64)
+  double* wsc;       // [grid][k*k] per-CTA copy of w = A-hat^T A-hat (fp64)
   double* part;      // [grid][lp*k] partial sums
-  double* npart;     // [k][grid] column-norm partials
-  int* zflag;        // [grid][k] non-zero-column flags
-  unsigned* bar;     // grid barrier (2 words)
+  double* npart;     // [2][grid] column-norm partials (by exchange parity)
+  unsigned* zpart;   // [grid][4] non-zero-column bitmasks
+  unsigned* bar;     // monotonic grid-barrier arrival counter (reset per run)
   HaltInfo* halt;
+  long long* prof;   // optional per-phase clock64 sums (CTA 0), or null
 };
 size_t hals_part_doubles(int grid, int lp, int k);
 int hals_grid(const HalsState& st, int nsm);
 // Runs iterations [it_begin, it_end) starting at (start_half, start_col).
 // Returns the cooperative-launch error, if any.
 // it_begin/it_end are 0-based; HaltInfo::iter reports the 1-based iteration.
+// epoch0 must exceed every epoch of earlier launches (HaltInfo::last_epoch).
 cudaError_t launch_hals(const HalsState& st, int normalize_a, double alpha, double beta,
                         int it_begin, int it_end, int start_half, int start_col, int skip_dead,
-                        int grid, cudaStream_t s);
+                        unsigned long long epoch0, int grid, cudaStream_t s);
 // A-hat = L^T A and B-check = R B (all columns, or only column j >= 0).
 void launch_compress_factors(const HalsState& st, int which /*0 A-hat, 1 B-check*/, int column,
                              cudaStream_t s);
 // a_j <- a_j / ||a_j|| (no-op on a zero column), fixed-order fp64 norm.
-void launch_normalize_column(float* a_cm, int64_t d, int j, cudaStream_t s);
+void launch_normalize_column(double* a_cm, int64_t d, int j, cudaStream_t s);
 
 // ---- synth.cu: synthetic data (bench harness, BASELINE.json configs) ------
 void launch_synth_x(int64_t d, int64_t n, int rank, int factor_kind, int noise_kind, double sigma,

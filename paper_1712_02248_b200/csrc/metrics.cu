@@ -58,8 +58,8 @@ __global__ void sum_partials_kernel(const double* __restrict__ part, int count,
 // products over k, fp64 residual squares, fixed-order reductions.
 __global__ void __launch_bounds__(256) recon_error_kernel(const float* __restrict__ x, int64_t ldx,
                                                           int64_t d, int64_t n,
-                                                          const float* __restrict__ a_cm,
-                                                          const float* __restrict__ b_cm, int k,
+                                                          const double* __restrict__ a_cm,
+                                                          const double* __restrict__ b_cm, int k,
                                                           double* __restrict__ part) {
   extern __shared__ __align__(16) float sm[];
   float* As = sm;              // k x 64
@@ -73,8 +73,8 @@ __global__ void __launch_bounds__(256) recon_error_kernel(const float* __restric
     __syncthreads();
     for (int e = tid; e < k * kTile; e += 256) {
       const int c = e >> 6, r = e & 63;
-      As[e] = (i0 + r < d) ? a_cm[(int64_t)c * d + i0 + r] : 0.f;
-      Bs[e] = (j0 + r < n) ? b_cm[(int64_t)c * n + j0 + r] : 0.f;
+      As[e] = (i0 + r < d) ? (float)a_cm[(int64_t)c * d + i0 + r] : 0.f;
+      Bs[e] = (j0 + r < n) ? (float)b_cm[(int64_t)c * n + j0 + r] : 0.f;
     }
     __syncthreads();
     float pred[4][4];
@@ -113,16 +113,16 @@ __global__ void __launch_bounds__(256) recon_error_kernel(const float* __restric
   if (tid == 0) part[blockIdx.x] = s;
 }
 
-__global__ void gini_partial_kernel(const float* __restrict__ sorted,
-                                    const float* __restrict__ orig, int64_t count,
+__global__ void gini_partial_kernel(const double* __restrict__ sorted,
+                                    const double* __restrict__ orig, int64_t count,
                                     double* __restrict__ part) {
   __shared__ double red[8];
   double acc = 0.0, tot = 0.0;
   const double m = (double)count;
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < count;
        i += (int64_t)gridDim.x * blockDim.x) {
-    acc += (2.0 * (double)(i + 1) - m - 1.0) * (double)sorted[i];
-    tot += (double)orig[i];
+    acc += (2.0 * (double)(i + 1) - m - 1.0) * sorted[i];
+    tot += orig[i];
   }
   acc = block_sum(acc, red);
   tot = block_sum(tot, red);
@@ -145,18 +145,18 @@ __global__ void gini_final_kernel(const double* __restrict__ part, int nb, int64
                                     : acc / ((double)count * tot);
 }
 
-__global__ void cm_to_rm_kernel(const float* __restrict__ cm, int64_t rows, int k,
+__global__ void cm_to_rm_kernel(const double* __restrict__ cm, int64_t rows, int k,
                                 float* __restrict__ rm) {
   for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < rows * k;
        e += (int64_t)gridDim.x * blockDim.x) {
     const int64_t i = e / k;
     const int c = (int)(e - i * k);
-    rm[e] = cm[(int64_t)c * rows + i];
+    rm[e] = (float)cm[(int64_t)c * rows + i];
   }
 }
 
 __global__ void rm_to_cm_kernel(const float* __restrict__ rm, int64_t rows, int k,
-                                float* __restrict__ cm) {
+                                double* __restrict__ cm) {
   for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < rows * k;
        e += (int64_t)gridDim.x * blockDim.x) {
     const int64_t c = e / rows, i = e - c * rows;
@@ -221,8 +221,8 @@ void launch_check_data(const float* x, int64_t ldx, int64_t d, int64_t n, int* f
   sum_partials_kernel<<<1, 32, 0, st>>>(part, grid, norm_sq, 1.0);
 }
 
-void launch_recon_error(const float* x, int64_t ldx, int64_t d, int64_t n, const float* a_cm,
-                        const float* b_cm, int k, double* out, void* ws, int nsm,
+void launch_recon_error(const float* x, int64_t ldx, int64_t d, int64_t n, const double* a_cm,
+                        const double* b_cm, int k, double* out, void* ws, int nsm,
                         cudaStream_t st) {
   const int64_t tiles = ((d + kTile - 1) / kTile) * ((n + kTile - 1) / kTile);
   const int grid = (int)std::max<int64_t>(1, std::min<int64_t>(tiles, (int64_t)nsm * 4));
@@ -242,19 +242,19 @@ void launch_recon_error(const float* x, int64_t ldx, int64_t d, int64_t n, const
 
 size_t gini_ws_bytes(int64_t count) {
   size_t temp = 0;
-  cub::DeviceRadixSort::SortKeys(nullptr, temp, (const float*)nullptr, (float*)nullptr,
+  cub::DeviceRadixSort::SortKeys(nullptr, temp, (const double*)nullptr, (double*)nullptr,
                                  (int)count);
-  return temp + sizeof(float) * count + sizeof(double) * 2 * 1024 + 1024;
+  return temp + sizeof(double) * count + sizeof(double) * 2 * 1024 + 1024;
 }
 
-void launch_gini(const float* b_cm, int64_t count, double* out, void* ws, size_t ws_bytes,
+void launch_gini(const double* b_cm, int64_t count, double* out, void* ws, size_t ws_bytes,
                  cudaStream_t st) {
   char* p = static_cast<char*>(ws);
   double* part = reinterpret_cast<double*>(p);
-  float* sorted = reinterpret_cast<float*>(p + sizeof(double) * 2 * 1024);
-  char* temp = p + sizeof(double) * 2 * 1024 + ((sizeof(float) * count + 255) & ~size_t(255));
+  double* sorted = reinterpret_cast<double*>(p + sizeof(double) * 2 * 1024);
+  char* temp = p + sizeof(double) * 2 * 1024 + ((sizeof(double) * count + 255) & ~size_t(255));
   size_t temp_bytes = ws_bytes - (size_t)(temp - p);
-  cub::DeviceRadixSort::SortKeys(temp, temp_bytes, b_cm, sorted, (int)count, 0, 32, st);
+  cub::DeviceRadixSort::SortKeys(temp, temp_bytes, b_cm, sorted, (int)count, 0, 64, st);
   const int nb = (int)std::min<int64_t>(1024, std::max<int64_t>(1, (count + 255) / 256));
   note_launches(1);
   gini_partial_kernel<<<nb, 256, 0, st>>>(sorted, b_cm, count, part);
@@ -262,11 +262,11 @@ void launch_gini(const float* b_cm, int64_t count, double* out, void* ws, size_t
   gini_final_kernel<<<1, 32, 0, st>>>(part, nb, count, out);
 }
 
-void launch_cm_to_rm(const float* cm, int64_t rows, int k, float* rm, cudaStream_t st) {
+void launch_cm_to_rm(const double* cm, int64_t rows, int k, float* rm, cudaStream_t st) {
   note_launches(1);
   cm_to_rm_kernel<<<blocks_for(rows * k, 148), 256, 0, st>>>(cm, rows, k, rm);
 }
-void launch_rm_to_cm(const float* rm, int64_t rows, int k, float* cm, cudaStream_t st) {
+void launch_rm_to_cm(const float* rm, int64_t rows, int k, double* cm, cudaStream_t st) {
   note_launches(1);
   rm_to_cm_kernel<<<blocks_for(rows * k, 148), 256, 0, st>>>(rm, rows, k, cm);
 }

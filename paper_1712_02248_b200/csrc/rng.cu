@@ -126,7 +126,7 @@ __global__ void normal_exact_kernel(const uint64_t* __restrict__ words, uint64_t
 // uniform_positive e (A then B, both row-major d x k / n x k in the
 // reference) -> column-major device factors A_cm[c*d + i], B_cm[c*n + i].
 __global__ void uniform_init_kernel(const uint64_t* __restrict__ words, uint64_t d, uint64_t n,
-                                    int k, float* __restrict__ a_cm, float* __restrict__ b_cm,
+                                    int k, double* __restrict__ a_cm, double* __restrict__ b_cm,
                                     int* __restrict__ flag) {
   const uint64_t na = d * k, total = (d + n) * k;
   for (uint64_t e = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; e < total;
@@ -134,15 +134,15 @@ __global__ void uniform_init_kernel(const uint64_t* __restrict__ words, uint64_t
     const double u = u53(words[e]);
     if (u == 0.0) *flag = 1;
     if (e < na)
-      a_cm[(e % k) * d + e / k] = (float)u;
+      a_cm[(e % k) * d + e / k] = u;
     else
-      b_cm[((e - na) % k) * n + (e - na) / k] = (float)u;
+      b_cm[((e - na) % k) * n + (e - na) / k] = u;
   }
 }
 
 __global__ void uniform_init_exact_kernel(const uint64_t* __restrict__ words, uint64_t nwords,
-                                          uint64_t d, uint64_t n, int k, float* __restrict__ a_cm,
-                                          float* __restrict__ b_cm, int* __restrict__ flag,
+                                          uint64_t d, uint64_t n, int k, double* __restrict__ a_cm,
+                                          double* __restrict__ b_cm, int* __restrict__ flag,
                                           uint64_t* __restrict__ consumed) {
   if (threadIdx.x != 0 || blockIdx.x != 0 || *flag == 0) return;
   const uint64_t na = d * k, total = (d + n) * k;
@@ -154,9 +154,9 @@ __global__ void uniform_init_exact_kernel(const uint64_t* __restrict__ words, ui
       u = u53(words[pos++]);
     }
     if (e < na)
-      a_cm[(e % k) * d + e / k] = (float)u;
+      a_cm[(e % k) * d + e / k] = u;
     else
-      b_cm[((e - na) % k) * n + (e - na) / k] = (float)u;
+      b_cm[((e - na) % k) * n + (e - na) / k] = u;
   }
   *consumed = pos;
   *flag = 3;
@@ -183,8 +183,8 @@ void launch_normal_exact(const uint64_t* words, uint64_t nwords, uint64_t count,
   normal_exact_kernel<<<1, 32, 0, s>>>(words, nwords, count, cols, ld, out, flag);
 }
 
-void launch_uniform_init(const uint64_t* words, uint64_t d, uint64_t n, int k, float* a_cm,
-                         float* b_cm, int* flag, int nsm, cudaStream_t s) {
+void launch_uniform_init(const uint64_t* words, uint64_t d, uint64_t n, int k, double* a_cm,
+                         double* b_cm, int* flag, int nsm, cudaStream_t s) {
   const uint64_t total = (d + n) * (uint64_t)k;
   const int blocks = (int)std::min<uint64_t>((total + 255) / 256, (uint64_t)nsm * 8);
   note_launches(1);
@@ -192,7 +192,7 @@ void launch_uniform_init(const uint64_t* words, uint64_t d, uint64_t n, int k, f
 }
 
 void launch_uniform_init_exact(const uint64_t* words, uint64_t nwords, uint64_t d, uint64_t n,
-                               int k, float* a_cm, float* b_cm, int* flag, uint64_t* consumed,
+                               int k, double* a_cm, double* b_cm, int* flag, uint64_t* consumed,
                                cudaStream_t s) {
   note_launches(1);
   uniform_init_exact_kernel<<<1, 32, 0, s>>>(words, nwords, d, n, k, a_cm, b_cm, flag, consumed);

@@ -240,6 +240,41 @@ def test_zero_start_redraw_path(ctx, oracle):
     assert rel_fro(host(tb), b) < FACTOR_RTOL
 
 
+def test_emptied_columns_redraw_path(ctx, oracle):
+    """Zero compressed views: every A column empties (solvers.cpp:435) and every
+    B column empties (452); each is redrawn from the host Rng in the
+    reference's order, with the B-sweep rollback on the device."""
+    x = oracle.synth_x(40, 30, 3, 0, 1, 0.01, 8).astype(np.float64)
+    left, right = oracle.build_projectors(x, 6, 1, 2)
+    xhat, xcheck = np.zeros((6, 30)), np.zeros((40, 6))
+    a, b = oracle.initialize(40, 30, 3, 4)
+    ah, bc = oracle.compress_factors(a, b, left, right)
+    ta, tb, tah, tbc = dev(a), dev(b), dev64(ah), dev64(bc)
+    redraws = ctx.fasthals_rp_steps(dev(xhat), dev(xcheck), dev(left), dev(right), ta, tb, tah,
+                                    tbc, True, 0.0, 0.0, 77, 2)
+    rng = oracle.rng(77)
+    for _ in range(2):
+        oracle.fasthals_rp_step(xhat, xcheck, a, b, ah, bc, left, right, True, 0.0, 0.0, rng)
+    assert redraws >= 4
+    assert rel_fro(host(ta), a) < FACTOR_RTOL
+    assert rel_fro(host(tb), b) < FACTOR_RTOL
+    assert rel_fro(host(tbc), bc) < FACTOR_RTOL
+
+
+def test_heavy_l1_penalty_empties_b(ctx, oracle):
+    """alpha so large that every b_j clamps to zero each sweep (redraw path)."""
+    x, left, right, xhat, xcheck, a, b, ah, bc = _step_fixture(oracle, 80, 60, 4, 8, 1, 3, 4, 5)
+    ta, tb, tah, tbc = dev(a), dev(b), dev64(ah), dev64(bc)
+    redraws = ctx.fasthals_rp_steps(dev(xhat), dev(xcheck), dev(left), dev(right), ta, tb, tah,
+                                    tbc, True, 1e6, 0.0, 5, 3)
+    rng = oracle.rng(5)
+    for _ in range(3):
+        oracle.fasthals_rp_step(xhat, xcheck, a, b, ah, bc, left, right, True, 1e6, 0.0, rng)
+    assert redraws >= 12
+    assert rel_fro(host(ta), a) < FACTOR_RTOL
+    assert rel_fro(host(tb), b) < FACTOR_RTOL
+
+
 def test_square_sketch_reduces_to_dense_fasthals(ctx, oracle):
     """test_solvers.cpp:356-370 / acceptance check 5 on the device."""
     x = random_nonneg(oracle, 12, 12, 512)
