@@ -211,6 +211,7 @@ int range_finder(cnmf_context* c, const XView& X, int q, int lp, uint64_t w, boo
 struct HalsRun {
   HalsState st;
   int grid;
+  bool resident;  // shared-memory-resident kernel (hals_resident.cu)
   unsigned long long epoch;  // next launch's exchange epoch base
 };
 
@@ -228,7 +229,10 @@ HalsRun make_hals(cnmf_context* c, int64_t d, int64_t n, int l, int lp, int k) {
   s.h = c->ws<double>("H_cm", (size_t)k * d);
   s.ahat = c->ws<double>("Ahat", (size_t)lp * k);
   s.bchk = c->ws<double>("Bchk", (size_t)lp * k);
-  r.grid = hals_grid(s, c->nsm);
+  const char* mode = std::getenv("CNMF_HALS");
+  const int rgrid = (mode && std::string(mode) == "stream") ? 0 : hals_resident_grid(s, c->nsm);
+  r.resident = rgrid > 0;
+  r.grid = r.resident ? rgrid : hals_grid(s, c->nsm);
   s.p = c->ws<double>("P_cm", (size_t)k * n);
   s.gsc = c->ws<double>("hals_gsc", (size_t)r.grid * k * k);
   s.wsc = c->ws<double>("hals_wsc", (size_t)r.grid * k * k);
@@ -268,8 +272,12 @@ void run_hals(cnmf_context* c, HalsRun& hr, int normalize_a, double alpha, doubl
   int64_t begin = ib;
   for (;;) {
     CK(cudaEventRecord(c->ev[0], c->stream));
-    CK(launch_hals(st, normalize_a, alpha, beta, (int)begin, (int)ie, half, col, skip, hr.epoch,
-                   hr.grid, c->stream));
+    if (hr.resident)
+      CK(launch_hals_resident(st, normalize_a, alpha, beta, (int)begin, (int)ie, half, col, skip,
+                              hr.epoch, hr.grid, c->stream));
+    else
+      CK(launch_hals(st, normalize_a, alpha, beta, (int)begin, (int)ie, half, col, skip,
+                     hr.epoch, hr.grid, c->stream));
     CK(cudaEventRecord(c->ev[1], c->stream));
     CK(cudaMemcpyAsync(c->halt_host, st.halt, sizeof(HaltInfo), cudaMemcpyDeviceToHost,
                        c->stream));

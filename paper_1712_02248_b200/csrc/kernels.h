@@ -128,6 +128,13 @@ int hals_grid(const HalsState& st, int nsm);
 cudaError_t launch_hals(const HalsState& st, int normalize_a, double alpha, double beta,
                         int it_begin, int it_end, int start_half, int start_col, int skip_dead,
                         unsigned long long epoch0, int grid, cudaStream_t s);
+// Shared-memory-resident variant (hals_resident.cu): same contract; grid 0
+// means the configuration does not fit and the streaming kernel is used.
+int hals_resident_grid(const HalsState& st, int nsm);
+cudaError_t launch_hals_resident(const HalsState& st, int normalize_a, double alpha, double beta,
+                                 int it_begin, int it_end, int start_half, int start_col,
+                                 int skip_dead, unsigned long long epoch0, int grid,
+                                 cudaStream_t s);
 // A-hat = L^T A and B-check = R B (all columns, or only column j >= 0).
 void launch_compress_factors(const HalsState& st, int which /*0 A-hat, 1 B-check*/, int column,
                              cudaStream_t s);
