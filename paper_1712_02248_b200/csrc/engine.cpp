@@ -53,7 +53,9 @@ struct cnmf_context {
   int device = 0;
   int nsm = 148;
   cudaStream_t stream = nullptr;
+  cudaStream_t side = nullptr;                  // second stream (R-side range finder)
   cudaEvent_t ev[4] = {nullptr, nullptr, nullptr, nullptr};
+  cudaEvent_t fork = nullptr, join = nullptr;   // ordering between the two streams
   std::string err;
   std::mutex mu;
   std::map<std::string, DevBuf> bufs;
@@ -118,37 +120,18 @@ double uniform_positive(std::mt19937_64& e) {
 
 // gaussian_sketch(rows, cols, seed) into out (ld), on the device.
 void gen_normals(cnmf_context* c, uint64_t seed, int64_t rows, int64_t cols, float* out, int ld,
-                 const std::string& tag) {
+                 const std::string& tag, cudaStream_t st = nullptr) {
+  if (!st) st = c->stream;
   const uint64_t count = (uint64_t)rows * cols;
   const uint64_t nwords = 2 * ((count + 1) / 2) + 256;
   uint64_t* words = c->ws<uint64_t>("words_" + tag, nwords);
   int* flag = c->ws<int>("nflag_" + tag, 4);
-  CK(cudaMemsetAsync(flag, 0, sizeof(int), c->stream));
+  CK(cudaMemsetAsync(flag, 0, sizeof(int), st));
   MtJobs jobs{};
   jobs.job[0] = MtJob{seed, nwords, words};
-  launch_mt_streams(jobs, 1, c->stream);
-  launch_normal_map(words, count, (int)cols, ld, out, flag, c->nsm, c->stream);
-  launch_normal_exact(words, nwords, count, (int)cols, ld, out, flag, c->stream);
-  CK(cudaGetLastError());
-}
-
-// Two sketches generated concurrently (one MT engine per CTA).
-void gen_normals2(cnmf_context* c, uint64_t seed0, int64_t rows0, int64_t cols, float* out0,
-                  uint64_t seed1, int64_t rows1, float* out1, int ld) {
-  const uint64_t c0 = (uint64_t)rows0 * cols, c1 = (uint64_t)rows1 * cols;
-  const uint64_t n0 = 2 * ((c0 + 1) / 2) + 256, n1 = 2 * ((c1 + 1) / 2) + 256;
-  uint64_t* w0 = c->ws<uint64_t>("words_L", n0);
-  uint64_t* w1 = c->ws<uint64_t>("words_R", n1);
-  int* flag = c->ws<int>("nflag2", 4);
-  CK(cudaMemsetAsync(flag, 0, 2 * sizeof(int), c->stream));
-  MtJobs jobs{};
-  jobs.job[0] = MtJob{seed0, n0, w0};
-  jobs.job[1] = MtJob{seed1, n1, w1};
-  launch_mt_streams(jobs, 2, c->stream);
-  launch_normal_map(w0, c0, (int)cols, ld, out0, flag, c->nsm, c->stream);
-  launch_normal_exact(w0, n0, c0, (int)cols, ld, out0, flag, c->stream);
-  launch_normal_map(w1, c1, (int)cols, ld, out1, flag + 1, c->nsm, c->stream);
-  launch_normal_exact(w1, n1, c1, (int)cols, ld, out1, flag + 1, c->stream);
+  launch_mt_streams(jobs, 1, st);
+  launch_normal_map(words, count, (int)cols, ld, out, flag, c->nsm, st);
+  launch_normal_exact(words, nwords, count, (int)cols, ld, out, flag, st);
   CK(cudaGetLastError());
 }
 
@@ -182,29 +165,46 @@ struct XView {
 // range(X^T) (transpose = true); range_finder_impl, compression.cpp:23-42.
 // `omega` holds the sketch (op_cols x lp).  Returns the X passes made.
 int range_finder(cnmf_context* c, const XView& X, int q, int lp, uint64_t w, bool transpose,
-                 const float* omega, float* basis, const std::string& tag) {
+                 const float* omega, float* basis, const std::string& tag,
+                 cudaStream_t st = nullptr) {
+  if (!st) st = c->stream;
   const int64_t rows = transpose ? X.n : X.d, cols = transpose ? X.d : X.n;
   float* y = c->ws<float>("rf_y_" + tag, rows * lp);
   float* z = c->ws<float>("rf_z_" + tag, cols * lp);
   float* zq = c->ws<float>("rf_zq_" + tag, cols * lp);
-  float* xs = c->ws<float>("xs_ws", xstream_ws_floats(X.d, X.n, lp, c->nsm));
-  void* qws = c->ws<char>("qr_ws", qr_ws_bytes(std::max(X.d, X.n), lp, c->nsm));
+  float* xs = c->ws<float>("xs_ws_" + tag, xstream_ws_floats(X.d, X.n, lp, c->nsm));
+  void* qws = c->ws<char>("qr_ws_" + tag, qr_ws_bytes(std::max(X.d, X.n), lp, c->nsm));
   auto apply = [&](const float* s, float* out, bool tn) {
     if (tn)
-      launch_xs_tn(X.x, X.ldx, X.d, X.n, s, lp, out, xs, c->nsm, c->stream);
+      launch_xs_tn(X.x, X.ldx, X.d, X.n, s, lp, out, xs, c->nsm, st);
     else
-      launch_xs_nn(X.x, X.ldx, X.d, X.n, s, lp, out, xs, c->nsm, c->stream);
+      launch_xs_nn(X.x, X.ldx, X.d, X.n, s, lp, out, xs, c->nsm, st);
   };
   apply(omega, y, transpose);
-  launch_thin_qr(y, rows, q, lp, basis, qws, c->nsm, c->stream);
+  launch_thin_qr(y, rows, q, lp, basis, qws, c->nsm, st);
   for (uint64_t it = 0; it < w; ++it) {
     apply(basis, z, !transpose);
-    launch_thin_qr(z, cols, q, lp, zq, qws, c->nsm, c->stream);
+    launch_thin_qr(z, cols, q, lp, zq, qws, c->nsm, st);
     apply(zq, y, transpose);
-    launch_thin_qr(y, rows, q, lp, basis, qws, c->nsm, c->stream);
+    launch_thin_qr(y, rows, q, lp, basis, qws, c->nsm, st);
   }
   CK(cudaGetLastError());
   return 1 + 2 * (int)w;
+}
+
+// build_projectors_impl (compression.cpp:44-53): the L and R range finders
+// are independent, so they run concurrently on the context's two streams.
+int build_projectors_dev(cnmf_context* c, const XView& X, int q, int lp, uint64_t w,
+                         uint64_t seed, float* omega_l, float* omega_r, float* lm, float* rt) {
+  CK(cudaEventRecord(c->fork, c->stream));
+  CK(cudaStreamWaitEvent(c->side, c->fork, 0));
+  gen_normals(c, seed * 2, X.n, q, omega_l, lp, "L", c->stream);
+  gen_normals(c, seed * 2 + 1, X.d, q, omega_r, lp, "R", c->side);
+  int passes = range_finder(c, X, q, lp, w, false, omega_l, lm, "L", c->stream);
+  passes += range_finder(c, X, q, lp, w, true, omega_r, rt, "R", c->side);
+  CK(cudaEventRecord(c->join, c->side));
+  CK(cudaStreamWaitEvent(c->stream, c->join, 0));
+  return passes;
 }
 
 // ------------------------------------------------------------------ HALS ----
@@ -403,9 +403,7 @@ void run_device_impl(cnmf_context* c, const float* x_in, int64_t d, int64_t n, i
   CK(cudaMemsetAsync(omega_l, 0, sizeof(float) * n * lp, c->stream));
   CK(cudaMemsetAsync(omega_r, 0, sizeof(float) * d * lp, c->stream));
   CK(cudaEventRecord(c->ev[2], c->stream));
-  gen_normals2(c, cfg.sketch_seed * 2, n, q, omega_l, cfg.sketch_seed * 2 + 1, d, omega_r, lp);
-  int passes = range_finder(c, X, q, lp, w, false, omega_l, lm, "L");
-  passes += range_finder(c, X, q, lp, w, true, omega_r, rt, "R");
+  int passes = build_projectors_dev(c, X, q, lp, w, cfg.sketch_seed, omega_l, omega_r, lm, rt);
   launch_xs_tn(X.x, X.ldx, d, n, lm, lp, xht, xs, c->nsm, c->stream);  // X-hat^T = X^T L
   launch_xs_nn(X.x, X.ldx, d, n, rt, lp, xc, xs, c->nsm, c->stream);   // X-check = X R^T
   passes += 2;
@@ -560,6 +558,9 @@ cnmf_status cnmf_context_create(int device, cnmf_context** out) {
   c->device = device;
   if (cudaSetDevice(device) != cudaSuccess ||
       cudaStreamCreateWithFlags(&c->stream, cudaStreamNonBlocking) != cudaSuccess ||
+      cudaStreamCreateWithFlags(&c->side, cudaStreamNonBlocking) != cudaSuccess ||
+      cudaEventCreateWithFlags(&c->fork, cudaEventDisableTiming) != cudaSuccess ||
+      cudaEventCreateWithFlags(&c->join, cudaEventDisableTiming) != cudaSuccess ||
       cudaDeviceGetAttribute(&c->nsm, cudaDevAttrMultiProcessorCount, device) != cudaSuccess ||
       cudaMallocHost(&c->halt_host, sizeof(HaltInfo)) != cudaSuccess) {
     delete c;
@@ -583,6 +584,12 @@ void cnmf_context_destroy(cnmf_context* c) {
   for (auto& e : c->ev)
     if (e) cudaEventDestroy(e);
   if (c->halt_host) cudaFreeHost(c->halt_host);
+  if (c->side) {
+    cudaStreamSynchronize(c->side);
+    cudaStreamDestroy(c->side);
+  }
+  if (c->fork) cudaEventDestroy(c->fork);
+  if (c->join) cudaEventDestroy(c->join);
   if (c->stream) cudaStreamDestroy(c->stream);
   delete c;
 }
@@ -717,9 +724,7 @@ cnmf_status cnmf_build_projectors(cnmf_context* c, const float* x, uint64_t d, u
     float* rt = c->ws<float>("Rt", n * lp);
     CK(cudaMemsetAsync(oml, 0, sizeof(float) * n * lp, c->stream));
     CK(cudaMemsetAsync(omr, 0, sizeof(float) * d * lp, c->stream));
-    gen_normals2(c, seed * 2, (int64_t)n, (int64_t)q, oml, seed * 2 + 1, (int64_t)d, omr, lp);
-    range_finder(c, X, (int)q, lp, w, false, oml, lm, "L");
-    range_finder(c, X, (int)q, lp, w, true, omr, rt, "R");
+    build_projectors_dev(c, X, (int)q, lp, w, seed, oml, omr, lm, rt);
     launch_unpad_cols(lm, (int64_t)d, lp, left, (int)q, c->stream);
     launch_transpose(rt, (int64_t)n, (int64_t)q, lp, right, (int64_t)n, c->stream);
     CK(cudaGetLastError());

@@ -54,6 +54,14 @@ void launch_xs_nn(const float* x, int64_t ldx, int64_t m, int64_t n, const float
 void launch_xs_tn(const float* x, int64_t ldx, int64_t m, int64_t n, const float* t, int lp,
                   float* z, float* ws, int nsm, cudaStream_t st);
 
+// xstream_tc.cu: the same contractions on tcgen05 tensor cores (3xTF32,
+// TMA-staged operands, TMEM accumulators).  Returns false (nothing launched)
+// when the shape is outside its envelope (lp > 128, misaligned X).
+size_t xstream_tc_ws_floats(int64_t m, int64_t n, int lp, int nsm);
+void xstream_tc_set_debug(float* dbg);  // tools/tc_debug.cu only
+bool launch_xs_tc(bool tn, const float* x, int64_t ldx, int64_t m, int64_t n, const float* s,
+                  int lp, float* out, float* ws, int nsm, cudaStream_t st);
+
 // ---- qr.cu: orthonormal basis with the span of Y --------------------------
 // CholeskyQR2 with fp64 Grams; Householder (reference qr.cpp semantics, fp64)
 // when the Cholesky factor is numerically singular.  Y and Q are rows x lp

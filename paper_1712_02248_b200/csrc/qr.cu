@@ -121,70 +121,77 @@ __global__ void __launch_bounds__(256) gram_kernel(const float* __restrict__ y, 
   }
 }
 
-// G[a][b] (a <= b < l) = fixed-order sum of partials; mirrored; zero outside.
+// G[a][b] (a <= b < l) = fixed-order sum of partials (lanes over CTAs, then
+// a warp tree), mirrored; zero outside l x l.  One warp per entry.
 __global__ void gram_reduce_kernel(const double* __restrict__ part, int grid, int l, int lp,
                                    double* __restrict__ g) {
-  for (int e = blockIdx.x * blockDim.x + threadIdx.x; e < lp * lp; e += gridDim.x * blockDim.x) {
+  const int lane = threadIdx.x & 31;
+  const int w = (blockIdx.x * blockDim.x + threadIdx.x) >> 5, nw = (gridDim.x * blockDim.x) >> 5;
+  for (int e = w; e < lp * lp; e += nw) {
     const int a = e / lp, b = e - a * lp;
     double s = 0.0;
     if (a < l && b < l) {
       const int lo = min(a, b), hi = max(a, b);
-      for (int c = 0; c < grid; ++c) s += part[(int64_t)c * lp * lp + lo * lp + hi];
+      for (int c = lane; c < grid; c += 32) s += part[(int64_t)c * lp * lp + lo * lp + hi];
+      s = warp_sum(s);
     }
-    g[e] = s;
+    if (lane == 0) g[e] = s;
   }
 }
 
-// Upper Cholesky G = R^T R and R^-1, one CTA.  flag |= 1 when a pivot is
+// Upper Cholesky G = R^T R and R^-1 in one CTA (fp64, shared memory).  R is
+// kept in the upper triangle, R^-1 (column-major) in the strict lower
+// triangle: Rinv[i][c] lives at gs[c][i].  flag |= 1 when a pivot is
 // non-positive or below 1e-13 of its original diagonal (Y numerically rank
 // deficient at fp32 resolution).
-__global__ void __launch_bounds__(256) chol_inv_kernel(const double* __restrict__ g, int l, int lp,
-                                                       double* __restrict__ rinv64,
-                                                       float* __restrict__ rinv,
-                                                       int* __restrict__ flag) {
-  extern __shared__ double gs[];  // l x l, then diag0[l]
+__global__ void __launch_bounds__(1024) chol_inv_kernel(const double* __restrict__ g, int l,
+                                                        int lp, double* __restrict__ rinv64,
+                                                        float* __restrict__ rinv,
+                                                        int* __restrict__ flag) {
+  extern __shared__ double gs[];  // l x l, then diag0[l], rdiag[l]
   double* diag0 = gs + l * l;
-  __shared__ int fail;
-  const int tid = threadIdx.x;
-  for (int e = tid; e < l * l; e += blockDim.x) gs[e] = g[(e / l) * lp + e % l];
-  for (int e = tid; e < l; e += blockDim.x) diag0[e] = g[e * lp + e];
-  for (int e = tid; e < lp * lp; e += blockDim.x) rinv[e] = 0.f;
-  if (tid == 0) fail = 0;
+  double* rdiag = diag0 + l;
+  const int tid = threadIdx.x, nt = blockDim.x;
+  for (int e = tid; e < l * l; e += nt) gs[e] = g[(e / l) * lp + e % l];
+  for (int e = tid; e < l; e += nt) diag0[e] = g[e * lp + e];
+  for (int e = tid; e < lp * lp; e += nt) rinv[e] = 0.f;
   __syncthreads();
   for (int j = 0; j < l; ++j) {
+    const double piv = gs[j * l + j];
+    if (!(piv > 1e-13 * diag0[j]) || !(piv > 0.0)) {  // uniform across the CTA
+      if (tid == 0) *flag = 1;
+      return;
+    }
+    const double r = sqrt(piv);
+    __syncthreads();  // everyone has read the pivot
+    for (int c = j + 1 + tid; c < l; c += nt) gs[j * l + c] /= r;
     if (tid == 0) {
-      const double piv = gs[j * l + j];
-      if (!(piv > 1e-13 * diag0[j]) || !(piv > 0.0))
-        fail = 1;
-      else
-        gs[j * l + j] = sqrt(piv);
+      gs[j * l + j] = r;
+      rdiag[j] = 1.0 / r;
     }
     __syncthreads();
-    if (fail) break;
-    const double r = gs[j * l + j];
-    for (int c = j + 1 + tid; c < l; c += blockDim.x) gs[j * l + c] /= r;
-    __syncthreads();
     const int m = l - j - 1;
-    for (int e = tid; e < m * m; e += blockDim.x) {
+    for (int e = tid; e < m * m; e += nt) {
       const int a = j + 1 + e / m, b = j + 1 + e % m;
       if (a <= b) gs[a * l + b] -= gs[j * l + a] * gs[j * l + b];
     }
     __syncthreads();
   }
-  if (fail) {
-    if (tid == 0) *flag = 1;
-    return;
-  }
-  // R^-1 column c by backward substitution (fp64), thread per column.
-  for (int c = tid; c < l; c += blockDim.x) {
-    double* x = rinv64 + (int64_t)c * lp;  // column c stored contiguously
-    x[c] = 1.0 / gs[c * l + c];
-    for (int i = c - 1; i >= 0; --i) {
-      double s = 0.0;
-      for (int q = i + 1; q <= c; ++q) s += gs[i * l + q] * x[q];
-      x[i] = -s / gs[i * l + i];
+  // R^-1 by rows from the bottom: Rinv[i][c] = -(sum_{q=i+1..c} R[i][q] Rinv[q][c]) / R[i][i]
+  for (int i = l - 1; i >= 0; --i) {
+    for (int c = i + 1 + tid; c < l; c += nt) {
+      double s = gs[i * l + c] * rdiag[c];  // q = c term (Rinv[c][c] = 1/R[c][c])
+      for (int q = i + 1; q < c; ++q) s += gs[i * l + q] * gs[c * l + q];
+      gs[c * l + i] = -s * rdiag[i];
     }
-    for (int i = 0; i <= c; ++i) rinv[i * lp + c] = (float)x[i];
+    __syncthreads();
+  }
+  for (int e = tid; e < l * l; e += nt) {
+    const int i = e / l, c = e - i * l;
+    if (c < i) continue;
+    const double v = c == i ? rdiag[i] : gs[c * l + i];
+    rinv[i * lp + c] = (float)v;
+    rinv64[i * lp + c] = v;
   }
 }
 
@@ -265,19 +272,19 @@ void gram(const float* y, int64_t rows, int l, int lp, const QrWs& w, int nsm,
   note_launches(1);
   gram_kernel<<<grid, 256, smem, st>>>(y, rows, l, lp, w.part);
   note_launches(1);
-  gram_reduce_kernel<<<(lp * lp + 255) / 256, 256, 0, st>>>(w.part, grid, l, lp, w.g);
+  gram_reduce_kernel<<<(lp * lp + 7) / 8, 256, 0, st>>>(w.part, grid, l, lp, w.g);
 }
 
 void chol_inv(int l, int lp, const QrWs& w, cudaStream_t st) {
-  const size_t smem = sizeof(double) * (l * l + l);
+  const size_t smem = sizeof(double) * (l * l + 2 * l);
   static bool attr = false;
   if (!attr) {
     cudaFuncSetAttribute(chol_inv_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                         (int)(sizeof(double) * (128 * 128 + 128)));
+                         (int)(sizeof(double) * (128 * 128 + 256)));
     attr = true;
   }
   note_launches(1);
-  chol_inv_kernel<<<1, 256, smem, st>>>(w.g, l, lp, w.rinv64, w.rinv, w.flag);
+  chol_inv_kernel<<<1, 1024, smem, st>>>(w.g, l, lp, w.rinv64, w.rinv, w.flag);
 }
 
 }  // namespace

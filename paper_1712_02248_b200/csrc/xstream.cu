@@ -11,6 +11,9 @@
 // coalesced along rows), staged in shared memory and reused for all lp
 // output columns from registers.  Split-K partials are reduced in a fixed
 // order, so results are bitwise reproducible run to run.
+#include <cstdlib>
+#include <string>
+
 #include "common.cuh"
 #include "kernels.h"
 
@@ -242,16 +245,29 @@ size_t xstream_ws_floats(int64_t m, int64_t n, int lp, int nsm) {
   const SplitPlan a = plan(m, n, nsm), b = plan(n, m, nsm);
   const int64_t fa = a.splits > 1 ? (int64_t)a.splits * m * lp : 0;
   const int64_t fb = b.splits > 1 ? (int64_t)b.splits * n * lp : 0;
-  return (size_t)std::max<int64_t>(std::max(fa, fb), 4);
+  return std::max<size_t>((size_t)std::max<int64_t>(std::max(fa, fb), 4),
+                          xstream_tc_ws_floats(m, n, lp, nsm));
+}
+
+// The tcgen05 kernel (xstream_tc.cu) is the production path; this SIMT kernel
+// serves shapes outside its envelope and CNMF_XS=simt (A/B comparisons).
+static bool use_tc() {
+  static const int mode = [] {
+    const char* e = std::getenv("CNMF_XS");
+    return (e && std::string(e) == "simt") ? 0 : 1;
+  }();
+  return mode == 1;
 }
 
 void launch_xs_nn(const float* x, int64_t ldx, int64_t m, int64_t n, const float* s, int lp,
                   float* y, float* ws, int nsm, cudaStream_t st) {
+  if (use_tc() && launch_xs_tc(false, x, ldx, m, n, s, lp, y, ws, nsm, st)) return;
   dispatch<false>(x, ldx, m, n, s, lp, y, ws, nsm, st);
 }
 
 void launch_xs_tn(const float* x, int64_t ldx, int64_t m, int64_t n, const float* t, int lp,
                   float* z, float* ws, int nsm, cudaStream_t st) {
+  if (use_tc() && launch_xs_tc(true, x, ldx, m, n, t, lp, z, ws, nsm, st)) return;
   dispatch<true>(x, ldx, m, n, t, lp, z, ws, nsm, st);
 }
 
