@@ -38,8 +38,8 @@ namespace {
 
 constexpr int kBM = 128;     // output rows per unit (MMA M)
 constexpr int kBK = 32;      // K elements per stage (4 MMA k-steps of 8)
-constexpr int kThreadsTC = 320;  // warps 0-3 epilogue, 4 TMA, 5 MMA, 6-9 split
-constexpr int kWarpTMA = 4, kWarpMMA = 5, kWarpSplit0 = 6;
+constexpr int kThreadsTC = 352;  // warps 0-3 epilogue, 4 X TMA, 5 MMA, 6-9 split, 10 S TMA
+constexpr int kWarpTMA = 4, kWarpMMA = 5, kWarpSplit0 = 6, kWarpBTMA = 10;
 constexpr int kDrain = 4;         // K-blocks (16 MMA k-steps) per TMEM accumulation chain
 constexpr int kXBytes = kBM * kBK * 4;  // 16 KB per stage (x_hi), same for x_lo
 
@@ -145,28 +145,67 @@ __device__ __forceinline__ void tf32_split(float x, float& hi, float& lo) {
   lo = __uint_as_float(l);
 }
 
+// Shared-memory rings (bytes): X stages (TMA -> split warps), operand slots
+// (split warps -> MMA: x_hi, x_lo) and S slots (TMA -> MMA: s_hi, s_lo).  An X
+// stage is released as soon as the split warps have read it, so the TMA
+// producer runs kXStages * 16 KB ahead of the consumers instead of being held
+// through the MMA (the first version kept <= 32 KB of X in flight per SM).
+template <int L> struct TcRings {
+  static constexpr int kBBytes = kBK * L * 4;               // s_hi or s_lo per K-block
+  static constexpr int kOpStages = 2;
+  static constexpr int kBStages = 3;
+  static constexpr int kBudget = 225 * 1024;
+  static constexpr int kXStages =
+      (kBudget - kOpStages * 2 * kXBytes - kBStages * 2 * kBBytes) / kXBytes > 8
+          ? 8
+          : (kBudget - kOpStages * 2 * kXBytes - kBStages * 2 * kBBytes) / kXBytes;
+  static constexpr int kXOff = 0;
+  static constexpr int kOpOff = kXStages * kXBytes;
+  static constexpr int kBOff = kOpOff + kOpStages * 2 * kXBytes;
+  static constexpr int kBytes = kBOff + kBStages * 2 * kBBytes;
+};
+
+__device__ __forceinline__ float4 lds128(uint32_t a) {
+  float4 v;
+  asm volatile("ld.shared.v4.f32 {%0,%1,%2,%3}, [%4];"
+               : "=f"(v.x), "=f"(v.y), "=f"(v.z), "=f"(v.w)
+               : "r"(a));
+  return v;
+}
+__device__ __forceinline__ void sts128(uint32_t a, float4 v) {
+  asm volatile("st.shared.v4.f32 [%0], {%1,%2,%3,%4};" ::"r"(a), "f"(v.x), "f"(v.y), "f"(v.z),
+               "f"(v.w)
+               : "memory");
+}
+
 template <bool kTN, int L>  // L = padded width (multiple of 32, <= 128)
 __global__ void __launch_bounds__(kThreadsTC, 1)
     xs_tc_kernel(const __grid_constant__ CUtensorMap map_x, const __grid_constant__ CUtensorMap map_bh,
                  const __grid_constant__ CUtensorMap map_bl, const TcArgs args) {
-  constexpr int kStages = L <= 64 ? 4 : 3;
-  constexpr int kBBytes = kBK * L * 4;          // one of b_hi / b_lo per stage
-  constexpr int kStageBytes = 2 * kXBytes + 2 * kBBytes;
-  constexpr int kAccCols = 2 * L;               // per accumulator buffer
+  using R = TcRings<L>;
+  constexpr int kSX = R::kXStages, kSO = R::kOpStages, kSB = R::kBStages;
+  constexpr int kAccCols = 2 * L;  // per accumulator buffer
   constexpr uint32_t kTmemCols = 4 * L <= 32 ? 32 : (4 * L <= 64 ? 64 : (4 * L <= 128 ? 128 : (4 * L <= 256 ? 256 : 512)));
 
   extern __shared__ __align__(1024) uint8_t smem_raw[];
-  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
-  __shared__ __align__(8) uint64_t full[kStages], lo_ready[kStages], empty[kStages];
-  __shared__ __align__(8) uint64_t acc_full[2], acc_empty[2];
+  const uint32_t sbase = (smem_u32(smem_raw) + 1023u) & ~1023u;
+  __shared__ __align__(8) uint64_t xfull[kSX], xempty[kSX], opready[kSO], opempty[kSO];
+  __shared__ __align__(8) uint64_t bfull[kSB], bempty[kSB], acc_full[2], acc_empty[2];
   __shared__ uint32_t tmem_base;
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   if (threadIdx.x == 0) {
-    for (int s = 0; s < kStages; ++s) {
-      mbar_init(&full[s], 1);
-      mbar_init(&lo_ready[s], 4);
-      mbar_init(&empty[s], 1);
+    for (int s = 0; s < kSX; ++s) {
+      mbar_init(&xfull[s], 1);
+      mbar_init(&xempty[s], 4);
+    }
+    for (int s = 0; s < kSO; ++s) {
+      mbar_init(&opready[s], 4);
+      mbar_init(&opempty[s], 1);
+    }
+    for (int s = 0; s < kSB; ++s) {
+      mbar_init(&bfull[s], 1);
+      mbar_init(&bempty[s], 1);
     }
     for (int b = 0; b < 2; ++b) {
       mbar_init(&acc_full[b], 1);
@@ -187,17 +226,25 @@ __global__ void __launch_bounds__(kThreadsTC, 1)
   const uint32_t tmem = tmem_base;
 
   const int units = args.ntiles * args.nsplit;
-  auto stage_x = [&](int s) { return smem + s * kStageBytes; };
-  auto stage_lo = [&](int s) { return smem + s * kStageBytes + kXBytes; };
-  auto stage_b = [&](int s) { return smem + s * kStageBytes + 2 * kXBytes; };  // [b_hi | b_lo]
+  auto x_addr = [&](int s) { return sbase + R::kXOff + s * kXBytes; };
+  auto hi_addr = [&](int o) { return sbase + R::kOpOff + o * 2 * kXBytes; };
+  auto lo_addr = [&](int o) { return sbase + R::kOpOff + o * 2 * kXBytes + kXBytes; };
+  auto b_addr = [&](int b) { return sbase + R::kBOff + b * 2 * R::kBBytes; };  // [s_hi | s_lo]
   auto unit_k = [&](int u, int64_t& k0, int64_t& k1) {
     const int split = u / args.ntiles;
     k0 = (int64_t)split * args.kchunk;
     k1 = min(args.kdim, k0 + args.kchunk);
   };
+  auto tma = [&](uint32_t dst, const CUtensorMap* map, uint64_t* bar, int c0, int c1) {
+    asm volatile(
+        "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes"
+        " [%0], [%1, {%3, %4}], [%2];" ::"r"(dst),
+        "l"(reinterpret_cast<uint64_t>(map)), "r"(smem_u32(bar)), "r"(c0), "r"(c1)
+        : "memory");
+  };
 
   if (warp == kWarpTMA) {
-    // ---------------- TMA producer ----------------
+    // ---------------- X producer ----------------
     if (lane == 0) {
       int s = 0;
       uint32_t ph = 0;
@@ -206,23 +253,40 @@ __global__ void __launch_bounds__(kThreadsTC, 1)
         unit_k(u, k0, k1);
         const int row0 = (u % args.ntiles) * kBM;
         for (int64_t kk = k0; kk < k1; kk += kBK) {
-          mbar_wait(&empty[s], ph ^ 1);
-          mbar_expect_tx(&full[s], kXBytes + 2 * kBBytes);
+          mbar_wait(&xempty[s], ph ^ 1);
+          mbar_expect_tx(&xfull[s], kXBytes);
           if (!kTN) {
-            tma_load_2d(stage_x(s), &map_x, &full[s], (int)kk, row0);
+            tma(x_addr(s), &map_x, &xfull[s], (int)kk, row0);
           } else {
 #pragma unroll
             for (int a = 0; a < kBM / 32; ++a)
-              tma_load_2d(stage_x(s) + a * (kBK * 128), &map_x, &full[s], row0 + 32 * a, (int)kk);
+              tma(x_addr(s) + a * (kBK * 128), &map_x, &xfull[s], row0 + 32 * a, (int)kk);
           }
+          if (++s == kSX) {
+            s = 0;
+            ph ^= 1;
+          }
+        }
+      }
+    }
+  } else if (warp == kWarpBTMA) {
+    // ---------------- S producer (L2-resident small operand) ----------------
+    if (lane == 0) {
+      int b = 0;
+      uint32_t ph = 0;
+      for (int u = blockIdx.x; u < units; u += gridDim.x) {
+        int64_t k0, k1;
+        unit_k(u, k0, k1);
+        for (int64_t kk = k0; kk < k1; kk += kBK) {
+          mbar_wait(&bempty[b], ph ^ 1);
+          mbar_expect_tx(&bfull[b], 2 * R::kBBytes);
 #pragma unroll
           for (int a = 0; a < L / 32; ++a) {
-            tma_load_2d(stage_b(s) + a * (kBK * 128), &map_bh, &full[s], 32 * a, (int)kk);
-            tma_load_2d(stage_b(s) + (L / 32 + a) * (kBK * 128), &map_bl, &full[s], 32 * a,
-                        (int)kk);
+            tma(b_addr(b) + a * (kBK * 128), &map_bh, &bfull[b], 32 * a, (int)kk);
+            tma(b_addr(b) + (L / 32 + a) * (kBK * 128), &map_bl, &bfull[b], 32 * a, (int)kk);
           }
-          if (++s == kStages) {
-            s = 0;
+          if (++b == kSB) {
+            b = 0;
             ph ^= 1;
           }
         }
@@ -237,8 +301,8 @@ __global__ void __launch_bounds__(kThreadsTC, 1)
     if (lane == 0) {
       constexpr uint32_t idesc_full = idesc_tf32(2 * L, kTN, true);
       constexpr uint32_t idesc_hi = idesc_tf32(L, kTN, true);
-      int s = 0, ab = 0;
-      uint32_t ph = 0, aph = 0;
+      int o = 0, b = 0, ab = 0;
+      uint32_t oph = 0, bph = 0, aph = 0;
       for (int u = blockIdx.x; u < units; u += gridDim.x) {
         int64_t k0, k1;
         unit_k(u, k0, k1);
@@ -249,10 +313,10 @@ __global__ void __launch_bounds__(kThreadsTC, 1)
           const uint32_t d = tmem + ab * kAccCols;
           uint32_t acc = 0;
           for (int64_t kk = g0; kk < g1; kk += kBK) {
-            mbar_wait(&lo_ready[s], ph);
+            mbar_wait(&opready[o], oph);
+            mbar_wait(&bfull[b], bph);
             tc_fence_after();
-            const uint32_t xa = smem_u32(stage_x(s)), la = smem_u32(stage_lo(s)),
-                           ba = smem_u32(stage_b(s));
+            const uint32_t xa = hi_addr(o), la = lo_addr(o), ba = b_addr(b);
 #pragma unroll
             for (int ks = 0; ks < kBK / 8; ++ks) {
               const uint32_t aoff = kTN ? ks * 1024 : ks * 32;
@@ -263,10 +327,15 @@ __global__ void __launch_bounds__(kThreadsTC, 1)
               tc_mma_tf32(d, alo, bd, idesc_hi, 1u);
               acc = 1u;
             }
-            tc_commit(&empty[s]);  // frees the stage once these MMAs complete
-            if (++s == kStages) {
-              s = 0;
-              ph ^= 1;
+            tc_commit(&opempty[o]);  // operand slot and S slot free once these MMAs complete
+            tc_commit(&bempty[b]);
+            if (++o == kSO) {
+              o = 0;
+              oph ^= 1;
+            }
+            if (++b == kSB) {
+              b = 0;
+              bph ^= 1;
             }
           }
           tc_commit(&acc_full[ab]);
@@ -277,39 +346,47 @@ __global__ void __launch_bounds__(kThreadsTC, 1)
         }
       }
     }
-  } else if (warp >= kWarpSplit0) {
-    // ---------------- split warps: x_hi, x_lo ----------------
+  } else if (warp >= kWarpSplit0 && warp < kWarpSplit0 + 4) {
+    // ---------------- split warps: X stage -> (x_hi, x_lo) operand slot ----
     const int t = threadIdx.x - 32 * kWarpSplit0;  // 0..127
-    int s = 0;
-    uint32_t ph = 0;
+    constexpr int kPer = kXBytes / 16 / 128;       // float4 per thread per stage (8)
+    int s = 0, o = 0;
+    uint32_t xph = 0, oph = 0;
     for (int u = blockIdx.x; u < units; u += gridDim.x) {
       int64_t k0, k1;
       unit_k(u, k0, k1);
       for (int64_t kk = k0; kk < k1; kk += kBK) {
-        mbar_wait(&full[s], ph);
-        float4* xh = reinterpret_cast<float4*>(stage_x(s));  // rewritten in place as x_hi
-        float4* xl = reinterpret_cast<float4*>(stage_lo(s));
+        mbar_wait(&xfull[s], xph);
+        float4 v[kPer];
 #pragma unroll
-        for (int i = 0; i < kXBytes / 16 / 128; ++i) {
-          const float4 v = xh[t + 128 * i];
+        for (int i = 0; i < kPer; ++i) v[i] = lds128(x_addr(s) + 16 * (t + 128 * i));
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&xempty[s]);  // the X stage can be refilled now
+        mbar_wait(&opempty[o], oph ^ 1);
+#pragma unroll
+        for (int i = 0; i < kPer; ++i) {
           float4 h, l;
-          tf32_split(v.x, h.x, l.x);
-          tf32_split(v.y, h.y, l.y);
-          tf32_split(v.z, h.z, l.z);
-          tf32_split(v.w, h.w, l.w);
-          xh[t + 128 * i] = h;
-          xl[t + 128 * i] = l;
+          tf32_split(v[i].x, h.x, l.x);
+          tf32_split(v[i].y, h.y, l.y);
+          tf32_split(v[i].z, h.z, l.z);
+          tf32_split(v[i].w, h.w, l.w);
+          sts128(hi_addr(o) + 16 * (t + 128 * i), h);
+          sts128(lo_addr(o) + 16 * (t + 128 * i), l);
         }
         asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
         __syncwarp();
-        if (lane == 0) mbar_arrive(&lo_ready[s]);
-        if (++s == kStages) {
+        if (lane == 0) mbar_arrive(&opready[o]);
+        if (++s == kSX) {
           s = 0;
-          ph ^= 1;
+          xph ^= 1;
+        }
+        if (++o == kSO) {
+          o = 0;
+          oph ^= 1;
         }
       }
     }
-  } else {
+  } else if (warp < 4) {
     // ---------------- epilogue (warps 0..3): TMEM chunks -> registers -> global
     const int q = warp;  // TMEM lane quarter this warp may access
     int ab = 0;
@@ -450,10 +527,23 @@ TcPlan tc_plan(int64_t rows_out, int64_t kdim, int nsm) {
     p.nsplit = (int)((kdim + p.kchunk - 1) / p.kchunk);
     return p;
   }
-  // enough units for ~2 per SM, each at least 16 stages deep
-  int64_t splits = std::max<int64_t>(1, (2 * (int64_t)nsm + p.ntiles - 1) / p.ntiles);
-  splits = std::min<int64_t>(splits, std::max<int64_t>(1, kblocks / 16));
-  const int64_t per = (kblocks + splits - 1) / splits;
+  // Choose the K-split count that minimises the makespan of the persistent
+  // grid: ceil(units / G) rounds of ceil(kblocks / nsplit) K-blocks each, plus
+  // the partial-output traffic of extra splits (write + reduce read, in
+  // K-block equivalents: 128 rows x lp x 8 B per split vs 16 KB per K-block).
+  int64_t best_ns = 1;
+  double best = 1e300;
+  for (int64_t ns = 1; ns <= std::min<int64_t>(64, kblocks); ++ns) {
+    const int64_t per = (kblocks + ns - 1) / ns;
+    const int64_t units = (int64_t)p.ntiles * ((kblocks + per - 1) / per);
+    const int64_t rounds = (units + nsm - 1) / nsm;
+    const double cost = (double)rounds * (double)per + (ns > 1 ? (double)ns * (double)p.ntiles / nsm * 4.5 : 0.0) + 2.0 * rounds;
+    if (cost < best - 1e-9) {
+      best = cost;
+      best_ns = ns;
+    }
+  }
+  const int64_t per = (kblocks + best_ns - 1) / best_ns;
   p.kchunk = per * kBK;
   p.nsplit = (int)((kdim + p.kchunk - 1) / p.kchunk);
   return p;
@@ -462,8 +552,7 @@ TcPlan tc_plan(int64_t rows_out, int64_t kdim, int nsm) {
 template <bool kTN, int L>
 cudaError_t run_tc(const CUtensorMap& mx, const CUtensorMap& mh, const CUtensorMap& ml,
                    const TcArgs& a, int grid, cudaStream_t st) {
-  constexpr int kStages = L <= 64 ? 4 : 3;
-  constexpr int smem = kStages * (2 * kXBytes + 2 * kBK * L * 4) + 1024;
+  constexpr int smem = TcRings<L>::kBytes + 1024;
   static bool attr = false;
   if (!attr) {
     cudaFuncSetAttribute(xs_tc_kernel<kTN, L>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
