@@ -40,7 +40,11 @@ constexpr int kBM = 128;     // output rows per unit (MMA M)
 constexpr int kBK = 32;      // K elements per stage (4 MMA k-steps of 8)
 constexpr int kThreadsTC = 352;  // warps 0-3 epilogue, 4 X TMA, 5 MMA, 6-9 split, 10 S TMA
 constexpr int kWarpTMA = 4, kWarpMMA = 5, kWarpSplit0 = 6, kWarpBTMA = 10;
-constexpr int kDrain = 4;         // K-blocks (16 MMA k-steps) per TMEM accumulation chain
+#ifdef TC_DRAIN
+constexpr int kDrain = TC_DRAIN;
+#else
+constexpr int kDrain = 2;         // K-blocks per drain (8 k-steps x 3 MMAs per accumulation chain)
+#endif
 constexpr int kXBytes = kBM * kBK * 4;  // 16 KB per stage (x_hi), same for x_lo
 
 __device__ __forceinline__ uint32_t smem_u32(const void* p) {
@@ -65,6 +69,13 @@ __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
       "@!p bra WAIT_%=;\n\t}" ::"r"(smem_u32(bar)),
       "r"(parity)
       : "memory");
+}
+// Warp-collective wait: every lane polls, then the warp reconverges before
+// any .sync.aligned tcgen05 instruction (a lagging lane would make those
+// undefined -- observed as scattered wrong rows).
+__device__ __forceinline__ void mbar_wait_warp(uint64_t* bar, uint32_t parity) {
+  mbar_wait(bar, parity);
+  __syncwarp();
 }
 __device__ __forceinline__ void tma_load_2d(void* dst, const CUtensorMap* map, uint64_t* bar,
                                             int c0, int c1) {
@@ -133,6 +144,7 @@ struct TcArgs {
   int ntiles, nsplit, lp;
   float* out;        // [nsplit][rows_out][lp] or the final output when nsplit == 1
   float* dbg;        // optional debug dump (tools/tc_debug.cu), null in production
+  int mode;          // experiments only (CNMF_TC_MODE): bit0 skip MMAs, bit1 skip split TMEM stores, bit2 skip epilogue TMEM loads
 };
 
 // x -> (x_hi, x_lo) = (rna_tf32(x), rna_tf32(x - x_hi)); both exactly
@@ -145,37 +157,111 @@ __device__ __forceinline__ void tf32_split(float x, float& hi, float& lo) {
   lo = __uint_as_float(l);
 }
 
-// Shared-memory rings (bytes): X stages (TMA -> split warps), operand slots
-// (split warps -> MMA: x_hi, x_lo) and S slots (TMA -> MMA: s_hi, s_lo).  An X
-// stage is released as soon as the split warps have read it, so the TMA
-// producer runs kXStages * 16 KB ahead of the consumers instead of being held
-// through the MMA (the first version kept <= 32 KB of X in flight per SM).
+// Shared-memory rings: X stages (TMA -> split warps) and S stages (TMA ->
+// MMA: s_hi | s_lo).  The split warps write x_hi / x_lo straight into tensor
+// memory (tcgen05.st), and the MMA reads its A operand from there, so X costs
+// one TMA write plus one LDS pass of shared-memory bandwidth (the v2 kernel's
+// shared-memory operand slots cost four more and made it smem-bound).  An X
+// stage is released as soon as the split warps have read it.
 template <int L> struct TcRings {
-  static constexpr int kBBytes = kBK * L * 4;               // s_hi or s_lo per K-block
-  static constexpr int kOpStages = 2;
-  static constexpr int kBStages = 3;
+  static constexpr int kBBytes = kBK * L * 4;  // s_hi or s_lo per K-block
   static constexpr int kBudget = 225 * 1024;
-  static constexpr int kXStages =
-      (kBudget - kOpStages * 2 * kXBytes - kBStages * 2 * kBBytes) / kXBytes > 8
-          ? 8
-          : (kBudget - kOpStages * 2 * kXBytes - kBStages * 2 * kBBytes) / kXBytes;
+  // Both operands arrive with ~1.5-2k cycles of latency (X from HBM, S from
+  // L2, re-requested only when a stage frees), so the budget is split to keep
+  // several K-blocks of each in flight.
+#ifdef TC_XSTAGES
+  static constexpr int kXStages = TC_XSTAGES;
+#else
+  static constexpr int kXStages = L <= 32 ? 8 : (L <= 64 ? 6 : (L <= 96 ? 5 : 4));
+#endif
+  static constexpr int kBFit = (kBudget - kXStages * kXBytes) / (2 * kBBytes);
+  static constexpr int kBStages = kBFit > 8 ? 8 : kBFit;
   static constexpr int kXOff = 0;
-  static constexpr int kOpOff = kXStages * kXBytes;
-  static constexpr int kBOff = kOpOff + kOpStages * 2 * kXBytes;
+  static constexpr int kBOff = kXStages * kXBytes;
   static constexpr int kBytes = kBOff + kBStages * 2 * kBBytes;
+  // Tensor memory: two accumulator buffers of L columns (double-buffered
+  // drain), then the A slots of 64 columns (x_hi: 32, x_lo: 32; lane = tile
+  // row, column = k).
+  static constexpr int kChains = 1;
+  static constexpr int kAccCols = kChains * L;
+  static constexpr int kAOff = 2 * kAccCols;
+  static constexpr int kOpFit = (512 - kAOff) / 64;
+#ifdef TC_OPSTAGES
+  static constexpr int kOpStages = TC_OPSTAGES;
+#else
+  static constexpr int kOpStages = kOpFit > 4 ? 4 : kOpFit;
+#endif
+  static constexpr uint32_t kTmemNeed = kAOff + kOpStages * 64;
+  static constexpr uint32_t kTmemCols =
+      kTmemNeed <= 32 ? 32 : (kTmemNeed <= 64 ? 64 : (kTmemNeed <= 128 ? 128 : (kTmemNeed <= 256 ? 256 : 512)));
 };
 
 __device__ __forceinline__ float4 lds128(uint32_t a) {
   float4 v;
   asm volatile("ld.shared.v4.f32 {%0,%1,%2,%3}, [%4];"
                : "=f"(v.x), "=f"(v.y), "=f"(v.z), "=f"(v.w)
-               : "r"(a));
+               : "r"(a)
+               : "memory");  // must not sink below the mbarrier arrive that frees the stage
   return v;
 }
-__device__ __forceinline__ void sts128(uint32_t a, float4 v) {
-  asm volatile("st.shared.v4.f32 [%0], {%1,%2,%3,%4};" ::"r"(a), "f"(v.x), "f"(v.y), "f"(v.z),
-               "f"(v.w)
-               : "memory");
+__device__ __forceinline__ float lds32(uint32_t a) {
+  float v;
+  asm volatile("ld.shared.f32 %0, [%1];" : "=f"(v) : "r"(a) : "memory");
+  return v;
+}
+// rna_tf32 with integer ops (ALU pipe; cvt.rna.tf32 issues on the XU pipe,
+// which the v2 kernel saturated): add half an ulp to the magnitude, truncate.
+__device__ __forceinline__ uint32_t rna_tf32_bits(float x) {
+  return (__float_as_uint(x) + 0x1000u) & 0xFFFFE000u;
+}
+__device__ __forceinline__ void tf32_split_bits(float x, uint32_t& hi, uint32_t& lo) {
+  hi = rna_tf32_bits(x);
+  lo = rna_tf32_bits(x - __uint_as_float(hi));
+}
+__device__ __forceinline__ void tmem_st32(uint32_t taddr, const uint32_t (&v)[32]) {
+  asm volatile(
+      "tcgen05.st.sync.aligned.32x32b.x32.b32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,"
+      "%13,%14,%15,%16,%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31,%32};" ::"r"(taddr),
+      "r"(v[0]), "r"(v[1]), "r"(v[2]), "r"(v[3]), "r"(v[4]), "r"(v[5]), "r"(v[6]), "r"(v[7]),
+      "r"(v[8]), "r"(v[9]), "r"(v[10]), "r"(v[11]), "r"(v[12]), "r"(v[13]), "r"(v[14]),
+      "r"(v[15]), "r"(v[16]), "r"(v[17]), "r"(v[18]), "r"(v[19]), "r"(v[20]), "r"(v[21]),
+      "r"(v[22]), "r"(v[23]), "r"(v[24]), "r"(v[25]), "r"(v[26]), "r"(v[27]), "r"(v[28]),
+      "r"(v[29]), "r"(v[30]), "r"(v[31])
+      : "memory");
+}
+__device__ __forceinline__ void tc_mma_tf32_ts(uint32_t d_tmem, uint32_t a_tmem, uint64_t b_desc,
+                                               uint32_t idesc, uint32_t accumulate) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n\t"
+      "setp.ne.b32 p, %4, 0;\n\t"
+      "tcgen05.mma.cta_group::1.kind::tf32 [%0], [%1], %2, %3, p;\n\t}" ::"r"(d_tmem),
+      "r"(a_tmem), "l"(b_desc), "r"(idesc), "r"(accumulate)
+      : "memory");
+}
+
+// MMA / commit issued by a CONVERGED warp, predicated on lane 0 inside the asm
+// (the same lane for every MMA and commit: tcgen05.commit only tracks the
+// MMAs of the executing thread): issuing from divergent code (`if (lane == 0)`) makes the compiler wrap
+// every tcgen05 instruction in an ELECT / BRA.U.ANY waterfall loop that caps
+// issue at ~45 cycles per MMA (tools/ubench_tc.cu: 44.5 vs 16.6 cycles for an
+// N = 32 MMA), more than the MMA itself for the widths used here.
+__device__ __forceinline__ void mma_ts_elect(uint32_t d_tmem, uint32_t a_tmem, uint64_t b_desc,
+                                             uint32_t idesc, uint32_t accumulate) {
+  asm volatile(
+      "{\n\t.reg .pred p, e;\n\t"
+      "setp.ne.b32 p, %4, 0;\n\t"
+      "{\n\t.reg .u32 ln;\n\tmov.u32 ln, %%laneid;\n\tsetp.eq.u32 e, ln, 0;\n\t}\n\t"
+      "@e tcgen05.mma.cta_group::1.kind::tf32 [%0], [%1], %2, %3, p;\n\t}" ::"r"(d_tmem),
+      "r"(a_tmem), "l"(b_desc), "r"(idesc), "r"(accumulate)
+      : "memory");
+}
+__device__ __forceinline__ void commit_elect(uint64_t* bar) {
+  asm volatile(
+      "{\n\t.reg .pred e;\n\t"
+      "{\n\t.reg .u32 ln;\n\tmov.u32 ln, %%laneid;\n\tsetp.eq.u32 e, ln, 0;\n\t}\n\t"
+      "@e tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];\n\t}" ::"r"(
+          smem_u32(bar))
+      : "memory");
 }
 
 template <bool kTN, int L>  // L = padded width (multiple of 32, <= 128)
@@ -184,8 +270,7 @@ __global__ void __launch_bounds__(kThreadsTC, 1)
                  const __grid_constant__ CUtensorMap map_bl, const TcArgs args) {
   using R = TcRings<L>;
   constexpr int kSX = R::kXStages, kSO = R::kOpStages, kSB = R::kBStages;
-  constexpr int kAccCols = 2 * L;  // per accumulator buffer
-  constexpr uint32_t kTmemCols = 4 * L <= 32 ? 32 : (4 * L <= 64 ? 64 : (4 * L <= 128 ? 128 : (4 * L <= 256 ? 256 : 512)));
+  constexpr uint32_t kTmemCols = R::kTmemCols;
 
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   const uint32_t sbase = (smem_u32(smem_raw) + 1023u) & ~1023u;
@@ -227,8 +312,6 @@ __global__ void __launch_bounds__(kThreadsTC, 1)
 
   const int units = args.ntiles * args.nsplit;
   auto x_addr = [&](int s) { return sbase + R::kXOff + s * kXBytes; };
-  auto hi_addr = [&](int o) { return sbase + R::kOpOff + o * 2 * kXBytes; };
-  auto lo_addr = [&](int o) { return sbase + R::kOpOff + o * 2 * kXBytes + kXBytes; };
   auto b_addr = [&](int b) { return sbase + R::kBOff + b * 2 * R::kBBytes; };  // [s_hi | s_lo]
   auto unit_k = [&](int u, int64_t& k0, int64_t& k1) {
     const int split = u / args.ntiles;
@@ -245,6 +328,8 @@ __global__ void __launch_bounds__(kThreadsTC, 1)
 
   if (warp == kWarpTMA) {
     // ---------------- X producer ----------------
+    // NN: one 32 (k) x 128 (rows) box, SWIZZLE_128B (conflict-free row reads);
+    // TN: one 128 (rows of Z = columns of X) x 32 (k) box, no swizzle.
     if (lane == 0) {
       int s = 0;
       uint32_t ph = 0;
@@ -255,13 +340,8 @@ __global__ void __launch_bounds__(kThreadsTC, 1)
         for (int64_t kk = k0; kk < k1; kk += kBK) {
           mbar_wait(&xempty[s], ph ^ 1);
           mbar_expect_tx(&xfull[s], kXBytes);
-          if (!kTN) {
-            tma(x_addr(s), &map_x, &xfull[s], (int)kk, row0);
-          } else {
-#pragma unroll
-            for (int a = 0; a < kBM / 32; ++a)
-              tma(x_addr(s) + a * (kBK * 128), &map_x, &xfull[s], row0 + 32 * a, (int)kk);
-          }
+          if (!kTN) tma(x_addr(s), &map_x, &xfull[s], (int)kk, row0);
+          else tma(x_addr(s), &map_x, &xfull[s], row0, (int)kk);
           if (++s == kSX) {
             s = 0;
             ph ^= 1;
@@ -294,13 +374,14 @@ __global__ void __launch_bounds__(kThreadsTC, 1)
     }
   } else if (warp == kWarpMMA) {
     // ---------------- MMA issuer ----------------
-    // Every kDrain K-blocks the accumulator is handed to the epilogue (which
-    // sums the chunks in registers) and the other TMEM buffer takes over: the
-    // tensor core's fp32 accumulation error grows with the chain length
-    // (tools/tc_precision.py), so chains are kept to 16 k-steps.
-    if (lane == 0) {
-      constexpr uint32_t idesc_full = idesc_tf32(2 * L, kTN, true);
-      constexpr uint32_t idesc_hi = idesc_tf32(L, kTN, true);
+    // Per k-step three MMAs into one accumulator: x_hi s_hi, x_hi s_lo,
+    // x_lo s_hi (A from tensor memory).  Every kDrain K-blocks the
+    // accumulator goes to the epilogue (which sums the chunks in registers)
+    // and the other buffer takes over: the tensor core's fp32 accumulation
+    // error grows with the chain length (tools/tc_precision.py).
+    {  // the whole warp walks the schedule; the elected leader issues
+      constexpr uint32_t idesc = idesc_tf32(L, false, true);
+      constexpr uint32_t kLoOff = (L / 32) * (kBK * 128);
       int o = 0, b = 0, ab = 0;
       uint32_t oph = 0, bph = 0, aph = 0;
       for (int u = blockIdx.x; u < units; u += gridDim.x) {
@@ -308,27 +389,31 @@ __global__ void __launch_bounds__(kThreadsTC, 1)
         unit_k(u, k0, k1);
         for (int64_t g0 = k0; g0 < k1; g0 += (int64_t)kDrain * kBK) {
           const int64_t g1 = min(k1, g0 + (int64_t)kDrain * kBK);
-          mbar_wait(&acc_empty[ab], aph ^ 1);
+          mbar_wait_warp(&acc_empty[ab], aph ^ 1);
           tc_fence_after();
-          const uint32_t d = tmem + ab * kAccCols;
+          const uint32_t d = tmem + ab * R::kAccCols;
           uint32_t acc = 0;
           for (int64_t kk = g0; kk < g1; kk += kBK) {
             mbar_wait(&opready[o], oph);
-            mbar_wait(&bfull[b], bph);
+            mbar_wait_warp(&bfull[b], bph);
             tc_fence_after();
-            const uint32_t xa = hi_addr(o), la = lo_addr(o), ba = b_addr(b);
+            const uint32_t ahi = tmem + R::kAOff + 64 * o;
+            // descriptor address field is addr >> 4 in the low bits: k-step
+            // offsets (1 KB) are added to the base descriptors directly
+            const uint64_t bh = desc_mn(b_addr(b), kBK * 128);
+            const uint64_t bl = desc_mn(b_addr(b) + kLoOff, kBK * 128);
+            if (!(args.mode & 1)) {
 #pragma unroll
-            for (int ks = 0; ks < kBK / 8; ++ks) {
-              const uint32_t aoff = kTN ? ks * 1024 : ks * 32;
-              const uint64_t ahi = kTN ? desc_mn(xa + aoff, kBK * 128) : smem_desc(xa + aoff, 16, 1024);
-              const uint64_t alo = kTN ? desc_mn(la + aoff, kBK * 128) : smem_desc(la + aoff, 16, 1024);
-              const uint64_t bd = desc_mn(ba + ks * 1024, kBK * 128);
-              tc_mma_tf32(d, ahi, bd, idesc_full, acc);
-              tc_mma_tf32(d, alo, bd, idesc_hi, 1u);
-              acc = 1u;
+              for (int ks = 0; ks < kBK / 8; ++ks) {
+                const uint64_t koff = (uint64_t)(ks * 1024 >> 4);
+                mma_ts_elect(d, ahi + 8 * ks, bh + koff, idesc, acc);
+                mma_ts_elect(d, ahi + 8 * ks, bl + koff, idesc, 1u);
+                mma_ts_elect(d, ahi + 32 + 8 * ks, bh + koff, idesc, 1u);
+                acc = 1u;
+              }
             }
-            tc_commit(&opempty[o]);  // operand slot and S slot free once these MMAs complete
-            tc_commit(&bempty[b]);
+            commit_elect(&opempty[o]);  // A slot and S stage free once these MMAs complete
+            commit_elect(&bempty[b]);
             if (++o == kSO) {
               o = 0;
               oph ^= 1;
@@ -338,7 +423,7 @@ __global__ void __launch_bounds__(kThreadsTC, 1)
               bph ^= 1;
             }
           }
-          tc_commit(&acc_full[ab]);
+          commit_elect(&acc_full[ab]);
           if (++ab == 2) {
             ab = 0;
             aph ^= 1;
@@ -347,35 +432,54 @@ __global__ void __launch_bounds__(kThreadsTC, 1)
       }
     }
   } else if (warp >= kWarpSplit0 && warp < kWarpSplit0 + 4) {
-    // ---------------- split warps: X stage -> (x_hi, x_lo) operand slot ----
-    const int t = threadIdx.x - 32 * kWarpSplit0;  // 0..127
-    constexpr int kPer = kXBytes / 16 / 128;       // float4 per thread per stage (8)
+    // ---------------- split warps: X stage -> (x_hi, x_lo) in tensor memory ----
+    // Warp w may only access TMEM lanes 32 (w % 4) .. +31: it owns those tile
+    // rows; each thread splits its row's 32 K values.
+    const int q = warp & 3;
+    const int r = 32 * q + lane;  // tile row (TMEM lane)
     int s = 0, o = 0;
     uint32_t xph = 0, oph = 0;
     for (int u = blockIdx.x; u < units; u += gridDim.x) {
       int64_t k0, k1;
       unit_k(u, k0, k1);
       for (int64_t kk = k0; kk < k1; kk += kBK) {
-        mbar_wait(&xfull[s], xph);
-        float4 v[kPer];
+        mbar_wait_warp(&xfull[s], xph);
+        float v[32];
+        if (!kTN) {  // SWIZZLE_128B K-major: 16 B chunk c of row r at chunk c ^ (r & 7)
+          const uint32_t row = x_addr(s) + r * 128;
 #pragma unroll
-        for (int i = 0; i < kPer; ++i) v[i] = lds128(x_addr(s) + 16 * (t + 128 * i));
-        __syncwarp();
-        if (lane == 0) mbar_arrive(&xempty[s]);  // the X stage can be refilled now
-        mbar_wait(&opempty[o], oph ^ 1);
+          for (int c = 0; c < 8; ++c) {
+            const float4 t = lds128(row + ((c ^ (r & 7)) << 4));
+            v[4 * c] = t.x;
+            v[4 * c + 1] = t.y;
+            v[4 * c + 2] = t.z;
+            v[4 * c + 3] = t.w;
+          }
+        } else {  // unswizzled [k][128]: lanes read consecutive words
 #pragma unroll
-        for (int i = 0; i < kPer; ++i) {
-          float4 h, l;
-          tf32_split(v[i].x, h.x, l.x);
-          tf32_split(v[i].y, h.y, l.y);
-          tf32_split(v[i].z, h.z, l.z);
-          tf32_split(v[i].w, h.w, l.w);
-          sts128(hi_addr(o) + 16 * (t + 128 * i), h);
-          sts128(lo_addr(o) + 16 * (t + 128 * i), l);
+          for (int kq = 0; kq < 32; ++kq) v[kq] = lds32(x_addr(s) + kq * (kBM * 4) + r * 4);
         }
-        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+        uint32_t hi[32], lo[32];
+#pragma unroll
+        for (int j = 0; j < 32; ++j) tf32_split_bits(v[j], hi[j], lo[j]);
+        mbar_wait_warp(&opempty[o], oph ^ 1);
+        tc_fence_after();
+        if (!(args.mode & 2)) {
+          const uint32_t ta = tmem + ((uint32_t)(32 * q) << 16) + R::kAOff + 64 * o;
+          tmem_st32(ta, hi);
+          tmem_st32(ta + 32, lo);
+          asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
+        }
+        tc_fence_before();
         __syncwarp();
         if (lane == 0) mbar_arrive(&opready[o]);
+        // The X stage is released only here, after tcgen05.st has consumed
+        // the registers its values were loaded into: an mbarrier arrive does
+        // not wait for in-flight ld.shared, and the compiler is free to sink
+        // register arithmetic below it, so releasing right after the loads let
+        // the next TMA overwrite rows before their last chunks were read
+        // (tools/tc_units.cu found block b computed with block b + kXStages).
+        if (lane == 0) mbar_arrive(&xempty[s]);
         if (++s == kSX) {
           s = 0;
           xph ^= 1;
@@ -399,28 +503,26 @@ __global__ void __launch_bounds__(kThreadsTC, 1)
 #pragma unroll
       for (int c = 0; c < L; ++c) run[c] = 0.f;
       for (int64_t g0 = k0; g0 < k1; g0 += (int64_t)kDrain * kBK) {
-        mbar_wait(&acc_full[ab], aph);
+        mbar_wait_warp(&acc_full[ab], aph);
         tc_fence_after();
-        const uint32_t base = tmem + ab * kAccCols + ((uint32_t)(32 * q) << 16);
+        const uint32_t base = tmem + ab * R::kAccCols + ((uint32_t)(32 * q) << 16);
 #pragma unroll
-        for (int c = 0; c < L; c += 16) {
-          uint32_t h[16], o[16];
+        for (int c = 0; c < R::kAccCols; c += 32) {
+          if (args.mode & 4) break;
+          uint32_t h[32];
           asm volatile(
-              "tcgen05.ld.sync.aligned.32x32b.x16.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15}, [%16];"
+              "tcgen05.ld.sync.aligned.32x32b.x32.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,"
+              "%16,%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31}, [%32];"
               : "=r"(h[0]), "=r"(h[1]), "=r"(h[2]), "=r"(h[3]), "=r"(h[4]), "=r"(h[5]), "=r"(h[6]),
                 "=r"(h[7]), "=r"(h[8]), "=r"(h[9]), "=r"(h[10]), "=r"(h[11]), "=r"(h[12]),
-                "=r"(h[13]), "=r"(h[14]), "=r"(h[15])
+                "=r"(h[13]), "=r"(h[14]), "=r"(h[15]), "=r"(h[16]), "=r"(h[17]), "=r"(h[18]),
+                "=r"(h[19]), "=r"(h[20]), "=r"(h[21]), "=r"(h[22]), "=r"(h[23]), "=r"(h[24]),
+                "=r"(h[25]), "=r"(h[26]), "=r"(h[27]), "=r"(h[28]), "=r"(h[29]), "=r"(h[30]),
+                "=r"(h[31])
               : "r"(base + c));
-          asm volatile(
-              "tcgen05.ld.sync.aligned.32x32b.x16.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15}, [%16];"
-              : "=r"(o[0]), "=r"(o[1]), "=r"(o[2]), "=r"(o[3]), "=r"(o[4]), "=r"(o[5]), "=r"(o[6]),
-                "=r"(o[7]), "=r"(o[8]), "=r"(o[9]), "=r"(o[10]), "=r"(o[11]), "=r"(o[12]),
-                "=r"(o[13]), "=r"(o[14]), "=r"(o[15])
-              : "r"(base + L + c));
           asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
 #pragma unroll
-          for (int j = 0; j < 16; ++j)
-            run[c + j] += __uint_as_float(h[j]) + __uint_as_float(o[j]);
+          for (int j = 0; j < 32; ++j) run[(c + j) % L] += __uint_as_float(h[j]);
         }
         tc_fence_before();
         __syncwarp();
@@ -497,20 +599,19 @@ PFN_cuTensorMapEncodeTiled_v12000 encode_fn() {
   return fn;
 }
 
-// 2D fp32 row-major tensor (rows x cols, row pitch ld floats), 32 x box_rows
-// boxes with 128-byte swizzle.
+// 2D fp32 row-major tensor (rows x cols, row pitch ld floats), box_cols x
+// box_rows boxes.
 bool make_map(CUtensorMap* m, const float* base, int64_t rows, int64_t cols, int64_t ld,
-              int box_rows, bool mn_major) {
+              int box_cols, int box_rows, CUtensorMapSwizzle sw) {
   auto fn = encode_fn();
   if (!fn) return false;
   const cuuint64_t dims[2] = {(cuuint64_t)cols, (cuuint64_t)rows};
   const cuuint64_t strides[1] = {(cuuint64_t)(ld * 4)};
-  const cuuint32_t box[2] = {32, (cuuint32_t)box_rows};
+  const cuuint32_t box[2] = {(cuuint32_t)box_cols, (cuuint32_t)box_rows};
   const cuuint32_t estr[2] = {1, 1};
   return fn(m, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2, const_cast<float*>(base), dims, strides, box,
-            estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
-            mn_major ? CU_TENSOR_MAP_SWIZZLE_128B_ATOM_32B : CU_TENSOR_MAP_SWIZZLE_128B,
-            CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+            estr, CU_TENSOR_MAP_INTERLEAVE_NONE, sw, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+            CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
 }
 
 struct TcPlan {
@@ -587,8 +688,12 @@ bool launch_xs_tc(bool tn, const float* x, int64_t ldx, int64_t m, int64_t n, co
   split_tf32_kernel<<<std::min<int64_t>((kdim * L + 255) / 256, nsm * 8), 256, 0, st>>>(
       s, kdim, lp, L, hi, lo);
   CUtensorMap mx, mh, ml;
-  bool ok = tn ? make_map(&mx, x, m, n, ldx, kBK, true) : make_map(&mx, x, m, n, ldx, kBM, false);
-  ok = ok && make_map(&mh, hi, kdim, L, L, kBK, true) && make_map(&ml, lo, kdim, L, L, kBK, true);
+  // X: NN boxes 32 (k) x 128 (rows), 128 B swizzle; TN boxes 128 x 32 (k), unswizzled.
+  // S hi / lo: MN-major operand atoms, 32 x 32 boxes, 128 B swizzle with 32 B atoms.
+  bool ok = tn ? make_map(&mx, x, m, n, ldx, kBM, kBK, CU_TENSOR_MAP_SWIZZLE_NONE)
+               : make_map(&mx, x, m, n, ldx, kBK, kBM, CU_TENSOR_MAP_SWIZZLE_128B);
+  ok = ok && make_map(&mh, hi, kdim, L, L, 32, kBK, CU_TENSOR_MAP_SWIZZLE_128B_ATOM_32B) &&
+       make_map(&ml, lo, kdim, L, L, 32, kBK, CU_TENSOR_MAP_SWIZZLE_128B_ATOM_32B);
   if (!ok) return false;
   TcArgs a;
   a.rows_out = rows_out;
@@ -599,6 +704,7 @@ bool launch_xs_tc(bool tn, const float* x, int64_t ldx, int64_t m, int64_t n, co
   a.lp = lp;
   a.out = p.nsplit > 1 ? parts : out;
   a.dbg = g_tc_debug;
+  a.mode = std::getenv("CNMF_TC_MODE") ? std::atoi(std::getenv("CNMF_TC_MODE")) : 0;
   const int units = p.ntiles * p.nsplit;
   const int grid = std::min(units, nsm);
   cudaError_t e;

@@ -9,9 +9,11 @@ import paper_1712_02248_b200 as cb
 name = sys.argv[1] if len(sys.argv) > 1 else "c3"
 tn = int(sys.argv[2]) if len(sys.argv) > 2 else 0
 iters = int(sys.argv[3]) if len(sys.argv) > 3 else 10
+l_override = int(sys.argv[4]) if len(sys.argv) > 4 else 0
 c = cb.CONFIGS[name]
 ctx = cb.Context(0)
 d, n, q = c["d"], c["n"], c["q"]
+if l_override: q = l_override
 ldx = (n + 3) // 4 * 4
 x = torch.empty((d, ldx), dtype=torch.float32, device="cuda")
 ctx.synth_x(d, n, c["rank"], c["factor_kind"], c["noise_kind"], c["sigma"], 1, x)
