@@ -118,10 +118,12 @@ _lib = None
 
 
 def load_library(path: str = LIB_PATH):
-    """Load the C-ABI library; raises CudaError when it is missing."""
+    """Load the C-ABI library; raises CudaError when it is missing.
+    CNMF_LIB overrides the path (kernel-variant experiments only)."""
     global _lib
     if _lib is not None:
         return _lib
+    path = os.environ.get("CNMF_LIB", path)
     if not os.path.exists(path):
         raise CudaError(f"{path} is missing: build it with paper_1712_02248_b200.build()")
     L = C.CDLL(path)

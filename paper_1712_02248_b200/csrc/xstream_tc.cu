@@ -43,7 +43,7 @@ constexpr int kWarpTMA = 4, kWarpMMA = 5, kWarpSplit0 = 6, kWarpBTMA = 10;
 #ifdef TC_DRAIN
 constexpr int kDrain = TC_DRAIN;
 #else
-constexpr int kDrain = 2;         // K-blocks per drain (8 k-steps x 3 MMAs per accumulation chain)
+constexpr int kDrain = 4;         // K-blocks per drain (16 k-steps x 3 MMAs per accumulation chain)
 #endif
 constexpr int kXBytes = kBM * kBK * 4;  // 16 KB per stage (x_hi), same for x_lo
 
@@ -144,6 +144,7 @@ struct TcArgs {
   int ntiles, nsplit, lp;
   float* out;        // [nsplit][rows_out][lp] or the final output when nsplit == 1
   float* dbg;        // optional debug dump (tools/tc_debug.cu), null in production
+  int nmma;          // MMA N = lp rounded up to 16 (<= L): padding columns are not computed
   int mode;          // experiments only (CNMF_TC_MODE): bit0 skip MMAs, bit1 skip split TMEM stores, bit2 skip epilogue TMEM loads
 };
 
@@ -175,7 +176,11 @@ template <int L> struct TcRings {
   static constexpr int kXStages = L <= 32 ? 8 : (L <= 64 ? 6 : (L <= 96 ? 5 : 4));
 #endif
   static constexpr int kBFit = (kBudget - kXStages * kXBytes) / (2 * kBBytes);
+#ifdef TC_BSTAGES
+  static constexpr int kBStages = TC_BSTAGES;
+#else
   static constexpr int kBStages = kBFit > 8 ? 8 : kBFit;
+#endif
   static constexpr int kXOff = 0;
   static constexpr int kBOff = kXStages * kXBytes;
   static constexpr int kBytes = kBOff + kBStages * 2 * kBBytes;
@@ -264,6 +269,22 @@ __device__ __forceinline__ void commit_elect(uint64_t* bar) {
       : "memory");
 }
 
+// TC_TRACE builds (tools only): per-K-block event times of CTA 0 into args.dbg
+// as uint64 [event][block]: 0 X issue, 1 split got X, 2 split got A slot,
+// 3 split done, 4 MMA got operands, 5 MMA issued, 6 S issue, 7 MMA got A slot.
+#ifdef TC_TRACE
+#define TC_EV(ev, blk)                                                              \
+  do {                                                                              \
+    const int blk_ = (blk);                                                         \
+    if (blockIdx.x == 0 && args.dbg && blk_ < 4096)                                 \
+      reinterpret_cast<unsigned long long*>(args.dbg)[(ev) * 4096 + blk_] = clock64(); \
+  } while (0)
+#else
+#define TC_EV(ev, blk) \
+  do {                 \
+  } while (0)
+#endif
+
 template <bool kTN, int L>  // L = padded width (multiple of 32, <= 128)
 __global__ void __launch_bounds__(kThreadsTC, 1)
     xs_tc_kernel(const __grid_constant__ CUtensorMap map_x, const __grid_constant__ CUtensorMap map_bh,
@@ -331,6 +352,7 @@ __global__ void __launch_bounds__(kThreadsTC, 1)
     // NN: one 32 (k) x 128 (rows) box, SWIZZLE_128B (conflict-free row reads);
     // TN: one 128 (rows of Z = columns of X) x 32 (k) box, no swizzle.
     if (lane == 0) {
+      int nblk = 0;
       int s = 0;
       uint32_t ph = 0;
       for (int u = blockIdx.x; u < units; u += gridDim.x) {
@@ -339,6 +361,7 @@ __global__ void __launch_bounds__(kThreadsTC, 1)
         const int row0 = (u % args.ntiles) * kBM;
         for (int64_t kk = k0; kk < k1; kk += kBK) {
           mbar_wait(&xempty[s], ph ^ 1);
+          TC_EV(0, nblk++);
           mbar_expect_tx(&xfull[s], kXBytes);
           if (!kTN) tma(x_addr(s), &map_x, &xfull[s], (int)kk, row0);
           else tma(x_addr(s), &map_x, &xfull[s], row0, (int)kk);
@@ -352,6 +375,7 @@ __global__ void __launch_bounds__(kThreadsTC, 1)
   } else if (warp == kWarpBTMA) {
     // ---------------- S producer (L2-resident small operand) ----------------
     if (lane == 0) {
+      int nblk = 0;
       int b = 0;
       uint32_t ph = 0;
       for (int u = blockIdx.x; u < units; u += gridDim.x) {
@@ -359,6 +383,7 @@ __global__ void __launch_bounds__(kThreadsTC, 1)
         unit_k(u, k0, k1);
         for (int64_t kk = k0; kk < k1; kk += kBK) {
           mbar_wait(&bempty[b], ph ^ 1);
+          TC_EV(6, nblk++);
           mbar_expect_tx(&bfull[b], 2 * R::kBBytes);
 #pragma unroll
           for (int a = 0; a < L / 32; ++a) {
@@ -380,7 +405,8 @@ __global__ void __launch_bounds__(kThreadsTC, 1)
     // and the other buffer takes over: the tensor core's fp32 accumulation
     // error grows with the chain length (tools/tc_precision.py).
     {  // the whole warp walks the schedule; the elected leader issues
-      constexpr uint32_t idesc = idesc_tf32(L, false, true);
+      int nblk = 0;
+      const uint32_t idesc = idesc_tf32(args.nmma, false, true);
       constexpr uint32_t kLoOff = (L / 32) * (kBK * 128);
       int o = 0, b = 0, ab = 0;
       uint32_t oph = 0, bph = 0, aph = 0;
@@ -395,7 +421,9 @@ __global__ void __launch_bounds__(kThreadsTC, 1)
           uint32_t acc = 0;
           for (int64_t kk = g0; kk < g1; kk += kBK) {
             mbar_wait(&opready[o], oph);
+            if (lane == 0) TC_EV(7, nblk);
             mbar_wait_warp(&bfull[b], bph);
+            if (lane == 0) TC_EV(4, nblk);
             tc_fence_after();
             const uint32_t ahi = tmem + R::kAOff + 64 * o;
             // descriptor address field is addr >> 4 in the low bits: k-step
@@ -407,13 +435,17 @@ __global__ void __launch_bounds__(kThreadsTC, 1)
               for (int ks = 0; ks < kBK / 8; ++ks) {
                 const uint64_t koff = (uint64_t)(ks * 1024 >> 4);
                 mma_ts_elect(d, ahi + 8 * ks, bh + koff, idesc, acc);
+#ifndef TC_HH_ONLY
                 mma_ts_elect(d, ahi + 8 * ks, bl + koff, idesc, 1u);
                 mma_ts_elect(d, ahi + 32 + 8 * ks, bh + koff, idesc, 1u);
+#endif
                 acc = 1u;
               }
             }
             commit_elect(&opempty[o]);  // A slot and S stage free once these MMAs complete
             commit_elect(&bempty[b]);
+            if (lane == 0) TC_EV(5, nblk);
+            ++nblk;
             if (++o == kSO) {
               o = 0;
               oph ^= 1;
@@ -437,6 +469,7 @@ __global__ void __launch_bounds__(kThreadsTC, 1)
     // rows; each thread splits its row's 32 K values.
     const int q = warp & 3;
     const int r = 32 * q + lane;  // tile row (TMEM lane)
+    int nblk = 0;
     int s = 0, o = 0;
     uint32_t xph = 0, oph = 0;
     for (int u = blockIdx.x; u < units; u += gridDim.x) {
@@ -444,6 +477,7 @@ __global__ void __launch_bounds__(kThreadsTC, 1)
       unit_k(u, k0, k1);
       for (int64_t kk = k0; kk < k1; kk += kBK) {
         mbar_wait_warp(&xfull[s], xph);
+        if (q == 0 && lane == 0) TC_EV(1, nblk);
         float v[32];
         if (!kTN) {  // SWIZZLE_128B K-major: 16 B chunk c of row r at chunk c ^ (r & 7)
           const uint32_t row = x_addr(s) + r * 128;
@@ -463,6 +497,7 @@ __global__ void __launch_bounds__(kThreadsTC, 1)
 #pragma unroll
         for (int j = 0; j < 32; ++j) tf32_split_bits(v[j], hi[j], lo[j]);
         mbar_wait_warp(&opempty[o], oph ^ 1);
+        if (q == 0 && lane == 0) TC_EV(2, nblk);
         tc_fence_after();
         if (!(args.mode & 2)) {
           const uint32_t ta = tmem + ((uint32_t)(32 * q) << 16) + R::kAOff + 64 * o;
@@ -480,6 +515,8 @@ __global__ void __launch_bounds__(kThreadsTC, 1)
         // the next TMA overwrite rows before their last chunks were read
         // (tools/tc_units.cu found block b computed with block b + kXStages).
         if (lane == 0) mbar_arrive(&xempty[s]);
+        if (q == 0 && lane == 0) TC_EV(3, nblk);
+        ++nblk;
         if (++s == kSX) {
           s = 0;
           xph ^= 1;
@@ -705,6 +742,7 @@ bool launch_xs_tc(bool tn, const float* x, int64_t ldx, int64_t m, int64_t n, co
   a.out = p.nsplit > 1 ? parts : out;
   a.dbg = g_tc_debug;
   a.mode = std::getenv("CNMF_TC_MODE") ? std::atoi(std::getenv("CNMF_TC_MODE")) : 0;
+  a.nmma = (lp + 15) & ~15;
   const int units = p.ntiles * p.nsplit;
   const int grid = std::min(units, nsm);
   cudaError_t e;
