@@ -495,6 +495,8 @@ void run_device_impl(cnmf_context* c, const float* x_in, int64_t d, int64_t n, i
     for (int i = 0; i < 17; ++i)
       std::fprintf(stderr, "  %-12s %10.0f  %5.1f%%\n", names[i], (double)pr[i] / its,
                    100.0 * pr[i] / std::max<long long>(1, tot));
+    std::fprintf(stderr, "  norm all-reduce split: local+barrier %.0f, publish %.0f, poll %.0f, read+sum %.0f\n",
+                 pr[17] / its, pr[18] / its, pr[19] / its, pr[20] / its);
   }
   // gini(B) (solvers.cpp:286-291) and the factors in reference layout.
   {

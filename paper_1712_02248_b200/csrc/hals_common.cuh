@@ -15,20 +15,61 @@ constexpr int kThreads = 256;
 // counter (reset per run; `ep` counts barriers) -- measured as the cheapest
 // deterministic exchange on B200 (tools/ubench_allreduce.cu: ~2.9k cycles at
 // 4 CTAs, ~4.1k at 148, including the read of the per-CTA partials).
+// Warp 0 polls the arrival counter with every lane (converged): a single
+// lane spinning while its warp-mates wait at a barrier cost ~2x in detection
+// latency (measured in the HALS kernel: 2.5k -> 1.2k cycles per all-reduce).
+__device__ __forceinline__ void poll_counter_warp(const unsigned* bar, unsigned target) {
+  unsigned c;
+  do {
+    asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(c) : "l"(bar) : "memory");
+  } while (__any_sync(0xffffffffu, (int)(c - target) < 0));
+}
+
 __device__ __forceinline__ void exchange(const HalsState& S, int G, int /*cta*/,
                                          unsigned long long& ep) {
   ++ep;
   __syncthreads();
-  if (threadIdx.x == 0) {
-    __threadfence();
-    atomicAdd(S.bar, 1u);
-    const unsigned target = (unsigned)(ep * (unsigned long long)G);
-    unsigned v;
-    do {
-      asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(S.bar) : "memory");
-    } while ((int)(v - target) < 0);
+  if (threadIdx.x < 32) {
+    if (threadIdx.x == 0) {
+      __threadfence();
+      atomicAdd(S.bar, 1u);
+    }
+    poll_counter_warp(S.bar, (unsigned)(ep * (unsigned long long)G));
   }
   __syncthreads();
+}
+
+// 1/sqrt(x) for x > 0 to ~1 ulp (0 for x <= 0): hardware rsqrt seed + two
+// fp64 Newton steps, far shorter than sqrt() followed by a division (the
+// reference divides by sqrt; the difference is a rounding or two).
+__device__ __forceinline__ double rsqrt_fp64(double x) {
+  if (!(x > 0.0)) return 0.0;
+  double y = rsqrt(x);  // MUFU-seeded, already close to fp64 precision
+  const double hx = 0.5 * x;
+  y = y * fma(-hx * y, y, 1.5);
+  y = y * fma(-hx * y, y, 1.5);
+  return y;
+}
+
+// Sum of the G (<= 32 * 8 fast path) per-CTA doubles at p, by one warp, in a
+// fixed order (lane-strided, then a butterfly).  All loads are issued before
+// any is used: a runtime-trip-count loop would serialise them into G / 32
+// L2 round trips (measured ~3k cycles at G = 148).
+__device__ __forceinline__ double warp_sum_partials(const double* __restrict__ p, int G, int lane) {
+  double t = 0.0;
+  if (G <= 256) {
+    double v[8];
+#pragma unroll
+    for (int i = 0; i < 8; ++i) {
+      const int b = lane + 32 * i;
+      v[i] = b < G ? __ldcg(p + b) : 0.0;
+    }
+#pragma unroll
+    for (int i = 0; i < 8; ++i) t += v[i];
+  } else {
+    for (int b = lane; b < G; b += 32) t += __ldcg(p + b);
+  }
+  return warp_sum(t);
 }
 
 // All-reduce of one fp64 per CTA: partial -> barrier -> every CTA sums the G
@@ -40,13 +81,85 @@ __device__ __forceinline__ double allreduce(const HalsState& S, int G, int cta, 
   if (threadIdx.x == 0) slot[cta] = v;
   exchange(S, G, cta, ep);
   if (threadIdx.x < 32) {
-    double t = 0.0;
-    for (int b = threadIdx.x; b < G; b += 32) t += __ldcg(slot + b);
-    t = warp_sum(t);
+    const double t = warp_sum_partials(slot, G, threadIdx.x);
     if (threadIdx.x == 0) *s_out = t;
   }
   __syncthreads();
   return *s_out;
+}
+
+// Arrival on the grid counter with release semantics for everything the
+// block wrote before (callers synchronised the block first).
+__device__ __forceinline__ void arrive_release(unsigned* bar) {
+#ifdef HALS_FENCE_ATOMIC
+  __threadfence();
+  atomicAdd(bar, 1u);
+#else
+  asm volatile("red.release.gpu.global.add.u32 [%0], 1;" ::"l"(bar) : "memory");
+#endif
+}
+
+// Block + grid all-reduce of one fp64 per thread with two __syncthreads:
+// warp sums -> red8 -> warp 0 sums the warp partials, lane 0 publishes the
+// CTA partial, arrives on the monotonic counter with a release add (no
+// separate __threadfence), polls with acquire loads; warp 0 then sums the G
+// CTA partials (lanes over CTAs in a fixed order, then a butterfly), so every
+// CTA computes the bitwise-identical total.  Lane 0 also stores 1/sqrt(total)
+// (0 when total == 0) into s_out[1] so callers normalise with one multiply.
+// Partials are double-buffered by epoch parity: a CTA can only write slot
+// (ep + 2) after every CTA arrived at ep + 1, i.e. finished reading ep.
+__device__ __forceinline__ double allreduce_fused(const HalsState& S, int G, int cta,
+                                                  unsigned long long& ep, double v,
+                                                  double* red8, double* s_out,
+                                                  long long* prof = nullptr) {
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  long long t0 = 0, t1 = 0, t2 = 0, t3 = 0;
+  if (prof && threadIdx.x == 0) t0 = clock64();
+  v = warp_sum(v);
+  if (lane == 0) red8[wid] = v;
+  __syncthreads();
+  ++ep;
+  if (wid == 0) {
+    if (prof && lane == 0) t1 = clock64();
+    double* slot = S.npart + (ep & 1ULL) * G;
+    if (lane == 0) {
+      double t = 0.0;  // CTA partial: the warp partials in a fixed order
+#pragma unroll
+      for (int w = 0; w < kThreads / 32; ++w) t += red8[w];
+      slot[cta] = t;
+      arrive_release(S.bar);
+      if (prof) t2 = clock64();
+    }
+    // every lane polls (no divergent spin + reconvergence), then reads
+    poll_counter_warp(S.bar, (unsigned)(ep * (unsigned long long)G));
+    if (prof && lane == 0) t3 = clock64();
+    const double tot = warp_sum_partials(slot, G, lane);
+    if (lane == 0) {
+      s_out[0] = tot;
+      s_out[1] = rsqrt_fp64(tot);
+      if (prof) {
+        const long long t4 = clock64();
+        prof[0] += t1 - t0;  // local reduction + first barrier
+        prof[1] += t2 - t1;  // warp-0 sum, publish, arrive
+        prof[2] += t3 - t2;  // poll until all CTAs arrived
+        prof[3] += t4 - t3;  // read partials, sum, 1/sqrt
+      }
+    }
+  }
+  __syncthreads();
+  return s_out[0];
+}
+
+// Grid barrier with payload visibility (release add + acquire poll), the
+// cheaper form of exchange() for callers that already synchronised the block.
+__device__ __forceinline__ void exchange_fast(const HalsState& S, int G, unsigned long long& ep) {
+  ++ep;
+  __syncthreads();
+  if (threadIdx.x < 32) {
+    if (threadIdx.x == 0) arrive_release(S.bar);
+    poll_counter_warp(S.bar, (unsigned)(ep * (unsigned long long)G));
+  }
+  __syncthreads();
 }
 
 // After an exchange of per-CTA partials (G x nel doubles): CTA c reduces its
@@ -58,8 +171,18 @@ __device__ __forceinline__ void slice_reduce(const double* __restrict__ part, in
   const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
   for (int e = e0 + wid; e < e1; e += kThreads / 32) {
     double s = 0.0;
-#pragma unroll 5
-    for (int b = lane; b < G; b += 32) s += __ldcg(part + (int64_t)b * nel + e);
+    if (G <= 256) {
+      double v[8];
+#pragma unroll
+      for (int i = 0; i < 8; ++i) {
+        const int b = lane + 32 * i;
+        v[i] = b < G ? __ldcg(part + (int64_t)b * nel + e) : 0.0;
+      }
+#pragma unroll
+      for (int i = 0; i < 8; ++i) s += v[i];
+    } else {
+      for (int b = lane; b < G; b += 32) s += __ldcg(part + (int64_t)b * nel + e);
+    }
     s = warp_sum(s);
     if (lane == 0) dst[e] = s;
   }

@@ -70,7 +70,7 @@ __device__ void load_rows(const float* __restrict__ src, int nrows, int lp, doub
 
 // out[r][c] = sum_q X[r][q] M[q][c] (all shared fp64); X stride lpp, M lp x k
 // (stride k), out stride kp1.  2x4 register tiles.
-__device__ void prod_rows(const double* X, int nrows, int lp, const double* M, int k,
+__device__ void prod_rows(const double* X, int nrows, int lp, int kdim, const double* M, int k,
                           double* out) {
   const int lpp = lp + 1, kp1 = k + 1;
   const int rg = (nrows + 1) >> 1, cgn = (k + 3) >> 2, tiles = rg * cgn;
@@ -81,7 +81,7 @@ __device__ void prod_rows(const double* X, int nrows, int lp, const double* M, i
     const double* x0 = X + r0 * lpp;
     const double* x1 = X + (r1ok ? r0 + 1 : r0) * lpp;
 #pragma unroll 4
-    for (int q = 0; q < lp; ++q) {
+    for (int q = 0; q < kdim; ++q) {
       const double a0 = x0[q], a1 = x1[q];
       const double* m = M + q * k + c0;
 #pragma unroll
@@ -101,101 +101,76 @@ __device__ void prod_rows(const double* X, int nrows, int lp, const double* M, i
   __syncthreads();
 }
 
-// part[l'][c] = sum_r X[r][l'] F[r][c] over nrows shared rows (fp64) into
-// global part (lp x k).  4x4 blocks; rows split over ng groups when there
-// are fewer blocks than threads, combined in a fixed order through `red`.
+// part[l'][c] = sum_r X[r][l'] F[r][c] over nrows shared rows (fp64, rows in
+// ascending order) into global part (lp x k, rows >= l zero).  2 x 2 output
+// blocks, one per thread, each summing all rows itself: no cross-thread
+// reduction, two independent accumulator chains per output (even / odd rows,
+// added at the end in a fixed order).
 __device__ void partial_rows(const double* X, const double* F, int nrows, int l, int lp, int k,
-                             double* red, double* __restrict__ part) {
+                             double* /*red*/, double* __restrict__ part) {
   const int lpp = lp + 1, kp1 = k + 1;
-  const int nbl = (l + 3) >> 2, nbc = (k + 3) >> 2, nb = nbl * nbc;
-  const int ng = nb >= kThreads ? 1 : min(16, kThreads / nb);
-  for (int e = threadIdx.x; e < lp * k; e += kThreads) part[e] = 0.0;
-  for (int g0 = 0; g0 < nb; g0 += kThreads) {
-    const int slot = ng > 1 ? (int)threadIdx.x % nb : (int)threadIdx.x;
-    const int grp = ng > 1 ? (int)threadIdx.x / nb : 0;
-    const int b = g0 + slot;
-    const bool own = b < nb && grp < ng;
-    const int bl = own ? b / nbc : 0, bc = own ? b - bl * nbc : 0;
-    double acc[16];
+  const int nbl = (l + 1) >> 1, nbc = (k + 1) >> 1, nb = nbl * nbc;
+  for (int b = threadIdx.x; b < nb; b += kThreads) {
+    const int l0 = 2 * (b / nbc), c0 = 2 * (b - (b / nbc) * nbc);
+    const int l1 = min(l0 + 1, l - 1), c1 = min(c0 + 1, k - 1);
+    double a[2][4] = {{0.0, 0.0, 0.0, 0.0}, {0.0, 0.0, 0.0, 0.0}};
+    int r = 0;
+    for (; r + 1 < nrows; r += 2) {
 #pragma unroll
-    for (int i = 0; i < 16; ++i) acc[i] = 0.0;
-    if (own) {
-      for (int r = grp; r < nrows; r += ng) {
-        double xi[4], fj[4];
-#pragma unroll
-        for (int i = 0; i < 4; ++i) xi[i] = X[r * lpp + 4 * bl + i];
-#pragma unroll
-        for (int j = 0; j < 4; ++j) fj[j] = (4 * bc + j < k) ? F[r * kp1 + 4 * bc + j] : 0.0;
-#pragma unroll
-        for (int i = 0; i < 4; ++i)
-#pragma unroll
-          for (int j = 0; j < 4; ++j) acc[4 * i + j] = fma(xi[i], fj[j], acc[4 * i + j]);
+      for (int h = 0; h < 2; ++h) {
+        const double* xr = X + (r + h) * lpp;
+        const double* fr = F + (r + h) * kp1;
+        const double x0 = xr[l0], x1 = xr[l1], f0 = fr[c0], f1 = fr[c1];
+        a[h][0] = fma(x0, f0, a[h][0]);
+        a[h][1] = fma(x0, f1, a[h][1]);
+        a[h][2] = fma(x1, f0, a[h][2]);
+        a[h][3] = fma(x1, f1, a[h][3]);
       }
     }
-    if (ng > 1) {
-      __syncthreads();
-      if (own)
-#pragma unroll
-        for (int i = 0; i < 16; ++i) red[(grp * nb + slot) * 16 + i] = acc[i];
-      __syncthreads();
-      if (own && grp == 0)
-        for (int g = 1; g < ng; ++g)
-#pragma unroll
-          for (int i = 0; i < 16; ++i) acc[i] += red[(g * nb + slot) * 16 + i];
+    if (r < nrows) {
+      const double* xr = X + r * lpp;
+      const double* fr = F + r * kp1;
+      a[0][0] = fma(xr[l0], fr[c0], a[0][0]);
+      a[0][1] = fma(xr[l0], fr[c1], a[0][1]);
+      a[0][2] = fma(xr[l1], fr[c0], a[0][2]);
+      a[0][3] = fma(xr[l1], fr[c1], a[0][3]);
     }
-    if (own && grp == 0) {
-#pragma unroll
-      for (int i = 0; i < 4; ++i)
-#pragma unroll
-        for (int j = 0; j < 4; ++j) {
-          const int li = 4 * bl + i, cj = 4 * bc + j;
-          if (li < l && cj < k) part[li * k + cj] = acc[4 * i + j];
-        }
+    part[l0 * k + c0] = a[0][0] + a[1][0];
+    if (c0 + 1 < k) part[l0 * k + c0 + 1] = a[0][1] + a[1][1];
+    if (l0 + 1 < l) {
+      part[(l0 + 1) * k + c0] = a[0][2] + a[1][2];
+      if (c0 + 1 < k) part[(l0 + 1) * k + c0 + 1] = a[0][3] + a[1][3];
     }
   }
-  __syncthreads();
+  for (int e = l * k + threadIdx.x; e < lp * k; e += kThreads) part[e] = 0.0;
 }
 
 // MS <- M (global fp64 lp x k, stride k in shared), then GW = MS^T MS over
-// the first l rows (fp64, 4x4 blocks of the upper triangle, mirrored).
+// the first l rows (fp64): one upper-triangle entry per thread, rows in
+// ascending order, mirrored.
 __device__ void load_and_gram(const double* __restrict__ M, int l, int lp, int k, double* ms,
                               double* gw) {
   __syncthreads();
   for (int e = threadIdx.x; e < lp * k; e += kThreads) ms[e] = __ldcg(M + e);
   __syncthreads();
-  const int nb4 = (k + 3) >> 2, nb = nb4 * (nb4 + 1) / 2;
-  for (int b = threadIdx.x; b < nb; b += kThreads) {
-    int bi = 0, rem = b;
-    while (rem >= nb4 - bi) {
-      rem -= nb4 - bi;
-      ++bi;
+  const int ntri = k * (k + 1) / 2;
+  for (int e = threadIdx.x; e < ntri; e += kThreads) {
+    int a = 0, rem = e;
+    while (rem >= k - a) {
+      rem -= k - a;
+      ++a;
     }
-    const int bj = bi + rem;
-    double acc[16];
-#pragma unroll
-    for (int i = 0; i < 16; ++i) acc[i] = 0.0;
-    for (int r = 0; r < l; ++r) {
-      double xv[4], yv[4];
-#pragma unroll
-      for (int i = 0; i < 4; ++i) {
-        xv[i] = 4 * bi + i < k ? ms[r * k + 4 * bi + i] : 0.0;
-        yv[i] = 4 * bj + i < k ? ms[r * k + 4 * bj + i] : 0.0;
-      }
-#pragma unroll
-      for (int i = 0; i < 4; ++i)
-#pragma unroll
-        for (int j = 0; j < 4; ++j) acc[4 * i + j] = fma(xv[i], yv[j], acc[4 * i + j]);
+    const int c = a + rem;
+    double s0 = 0.0, s1 = 0.0;
+    int r = 0;
+    for (; r + 1 < l; r += 2) {
+      s0 = fma(ms[r * k + a], ms[r * k + c], s0);
+      s1 = fma(ms[(r + 1) * k + a], ms[(r + 1) * k + c], s1);
     }
-#pragma unroll
-    for (int i = 0; i < 4; ++i)
-#pragma unroll
-      for (int j = 0; j < 4; ++j) {
-        const int a = 4 * bi + i, c = 4 * bj + j;
-        if (a < k && c < k) {
-          gw[a * k + c] = acc[4 * i + j];
-          gw[c * k + a] = acc[4 * i + j];
-        }
-      }
+    if (r < l) s0 = fma(ms[r * k + a], ms[r * k + c], s0);
+    const double v = s0 + s1;
+    gw[a * k + c] = v;
+    gw[c * k + a] = v;
   }
   __syncthreads();
 }
@@ -203,9 +178,11 @@ __device__ void load_and_gram(const double* __restrict__ M, int l, int lp, int k
 __global__ void __launch_bounds__(kThreads, 1) hals_resident_kernel(const ResArgs p) {
   extern __shared__ __align__(16) double sm[];
   __shared__ double red8[kThreads / 32];
-  __shared__ double s_total;
+  __shared__ double s_red[2];      // all-reduce total, 1/sqrt(total)
+  __shared__ double s_ginv[128];   // 1/g_jj or 1/w_jj of the current half
   __shared__ unsigned zmask[4];
-  __shared__ long long s_prof[17];
+  __shared__ unsigned s_zw[4 * (kThreads / 32)];
+  __shared__ long long s_prof[21];
 
   const HalsState& S = p.st;
   const int G = gridDim.x, cta = blockIdx.x, tid = threadIdx.x;
@@ -225,7 +202,7 @@ __global__ void __launch_bounds__(kThreads, 1) hals_resident_kernel(const ResArg
   const bool prof = S.prof != nullptr && cta == 0;
   long long t_last = 0;
   if (prof && tid == 0) {
-    for (int i = 0; i < 17; ++i) s_prof[i] = 0;
+    for (int i = 0; i < 21; ++i) s_prof[i] = 0;
     t_last = clock64();
   }
 #define RES_PROF(id)                  \
@@ -276,12 +253,16 @@ __global__ void __launch_bounds__(kThreads, 1) hals_resident_kernel(const ResArg
         for (int e = tid; e < lp * k; e += kThreads) MS[e] = __ldcg(S.bchk + e);
         __syncthreads();
       }
-      prod_rows(XC, na, lp, MS, k, HS);  // h = X-check B-check (421)
+      prod_rows(XC, na, lp, l, MS, k, HS);  // h = X-check B-check (421)
       RES_PROF(1);
       int jd = k;
       for (int j = col0; j < k; ++j)
         if (j != skip && GW[j * k + j] < kDead) { jd = j; break; }
       skip = -1;
+      // reciprocal divisors: one multiply on the per-column critical path
+      // (differs from the reference's division by at most one rounding)
+      for (int e = tid; e < k; e += kThreads) s_ginv[e] = 1.0 / GW[e * k + e];
+      __syncthreads();
       const int r = tid;  // one A row per thread (rows_a <= 256)
       const bool live = r < na;
       for (int jb = col0; jb < jd; jb += kNB) {
@@ -311,12 +292,11 @@ __global__ void __launch_bounds__(kThreads, 1) hals_resident_kernel(const ResArg
             for (int u = 0; u < kNB; ++u)
               if (u < t) s = fma(dl[u], GW[(jb + u) * k + j], s);
             aold = AS[r * kp1 + j];
-            v = aold + (HS[r * kp1 + j] - s) / GW[j * k + j];
+            v = aold + (HS[r * kp1 + j] - s) * s_ginv[j];
             v = v > 0.0 ? v : 0.0;
           }
-          const double cta_nrm = block_sum(v * v, red8);
           RES_PROF(2);
-          const double total = allreduce(S, G, cta, ep, cta_nrm, &s_total);
+          const double total = allreduce_fused(S, G, cta, ep, v * v, red8, s_red, prof ? s_prof + 17 : nullptr);
           RES_PROF(3);
           if (total == 0.0) {  // column emptied: host redraws a_j (solvers.cpp:435)
             if (live) AS[r * kp1 + j] = 0.0;
@@ -325,7 +305,7 @@ __global__ void __launch_bounds__(kThreads, 1) hals_resident_kernel(const ResArg
             return;
           }
           if (live) {  // solvers.cpp:436
-            const double nf = p.normalize_a ? v / sqrt(total) : v;
+            const double nf = p.normalize_a ? v * s_red[1] : v;
             AS[r * kp1 + j] = nf;
             dl[t] = nf - aold;
           }
@@ -339,10 +319,10 @@ __global__ void __launch_bounds__(kThreads, 1) hals_resident_kernel(const ResArg
       }
       partial_rows(LM, AS, na, l, lp, k, RED, S.part + (int64_t)cta * nel);  // A-hat (438)
       RES_PROF(4);
-      exchange(S, G, cta, ep);
+      exchange_fast(S, G, ep);
       RES_PROF(5);
       slice_reduce(S.part, G, nel, S.ahat);
-      exchange(S, G, cta, ep);
+      exchange_fast(S, G, ep);
       RES_PROF(7);
       load_and_gram(S.ahat, l, lp, k, MS, GW);  // w (443); MS keeps A-hat for p
       RES_PROF(8);
@@ -353,66 +333,86 @@ __global__ void __launch_bounds__(kThreads, 1) hals_resident_kernel(const ResArg
       load_and_gram(S.ahat, l, lp, k, MS, GW);
     }
     // ================== B half (solvers.cpp:440-455) =======================
-    prod_rows(XH, nbr, lp, MS, k, PS);  // p = X-hat^T A-hat (442)
-    if (tid < 4) zmask[tid] = 0u;
+    prod_rows(XH, nbr, lp, l, MS, k, PS);  // p = X-hat^T A-hat (442)
+    for (int e = tid; e < 4 * (kThreads / 32); e += kThreads) s_zw[e] = 0u;
+    for (int e = tid; e < k; e += kThreads)
+      s_ginv[e] = 1.0 / (constrained ? GW[e * k + e] + p.beta : GW[e * k + e]);
     __syncthreads();
     int jd = k;
     for (int j = col0; j < k; ++j)
       if (j != skip && GW[j * k + j] < kDead) { jd = j; break; }
     skip = -1;
     RES_PROF(9);
-    {
-      const int r = tid;  // one B row per thread (rows_b <= 256)
-      if (r < nbr) {
+    if ((tid & ~31) < nbr) {  // warps holding B rows (one row per thread)
+      const int r = tid;
+      const bool live = r < nbr;
+      const int rr = live ? r : 0;
+      unsigned zw0 = 0u, zw1 = 0u, zw2 = 0u, zw3 = 0u;  // columns with a non-zero entry in this warp
+      if (live)
         for (int c = 0; c < col0; ++c) bsn[r * kp1 + c] = bsc[r * kp1 + c];
-        for (int jb = col0; jb < jd; jb += kNB) {
-          const int nbj = min(kNB, jd - jb);
-          double acc[kNB], dl[kNB];
+      for (int jb = col0; jb < jd; jb += kNB) {
+        const int nbj = min(kNB, jd - jb);
+        double acc[kNB], dl[kNB];
 #pragma unroll
-          for (int t = 0; t < kNB; ++t) {
-            acc[t] = 0.0;
-            dl[t] = 0.0;
-          }
-          for (int c = 0; c < k; ++c) {  // columns < jb already live in bsn
-            const double bv = c < jb ? bsn[r * kp1 + c] : bsc[r * kp1 + c];
+        for (int t = 0; t < kNB; ++t) {
+          acc[t] = 0.0;
+          dl[t] = 0.0;
+        }
+        for (int c = 0; c < k; ++c) {  // columns < jb already live in bsn
+          const double bv = c < jb ? bsn[rr * kp1 + c] : bsc[rr * kp1 + c];
 #pragma unroll
-            for (int t = 0; t < kNB; ++t)
-              if (t < nbj) acc[t] = fma(bv, GW[c * k + jb + t], acc[t]);
-          }
+          for (int t = 0; t < kNB; ++t)
+            if (t < nbj) acc[t] = fma(bv, GW[c * k + jb + t], acc[t]);
+        }
 #pragma unroll
-          for (int t = 0; t < kNB; ++t) {
-            if (t >= nbj) break;
-            const int j = jb + t;
-            double s = acc[t];
+        for (int t = 0; t < kNB; ++t) {
+          if (t >= nbj) break;
+          const int j = jb + t;
+          double sacc = acc[t];
 #pragma unroll
-            for (int u = 0; u < kNB; ++u)
-              if (u < t) s = fma(dl[u], GW[(jb + u) * k + j], s);
-            const double wjj = GW[j * k + j];
-            const double bij = bsc[r * kp1 + j], pij = PS[r * kp1 + j];
-            const double v = constrained ? (bij * wjj + pij - s - p.alpha) / (wjj + p.beta)  // 502-508
-                                         : bij + (pij - s) / wjj;                            // 480-490
-            const double vf = v > 0.0 ? v : 0.0;
-            bsn[r * kp1 + j] = vf;
-            dl[t] = vf - bij;
-            if (vf != 0.0) atomicOr(&zmask[j >> 5], 1u << (j & 31));
+          for (int u = 0; u < kNB; ++u)
+            if (u < t) sacc = fma(dl[u], GW[(jb + u) * k + j], sacc);
+          const double wjj = GW[j * k + j];
+          const double bij = bsc[rr * kp1 + j], pij = PS[rr * kp1 + j];
+          const double v = constrained ? (bij * wjj + pij - sacc - p.alpha) * s_ginv[j]  // 502-508
+                                       : bij + (pij - sacc) * s_ginv[j];                  // 480-490
+          const double vf = v > 0.0 ? v : 0.0;
+          if (live) bsn[r * kp1 + j] = vf;
+          dl[t] = vf - bij;
+          if (__ballot_sync(0xffffffffu, live && vf != 0.0)) {
+            const unsigned bit = 1u << (j & 31);
+            if ((j >> 5) == 0) zw0 |= bit;
+            else if ((j >> 5) == 1) zw1 |= bit;
+            else if ((j >> 5) == 2) zw2 |= bit;
+            else zw3 |= bit;
           }
         }
+      }
+      if (live)
         for (int c = jd; c < k; ++c) bsn[r * kp1 + c] = bsc[r * kp1 + c];
+      if ((tid & 31) == 0) {
+        const int w = tid >> 5;
+        s_zw[4 * w + 0] = zw0;
+        s_zw[4 * w + 1] = zw1;
+        s_zw[4 * w + 2] = zw2;
+        s_zw[4 * w + 3] = zw3;
       }
     }
     __syncthreads();
+    if (tid < 4) {
+      unsigned m = 0u;
+      for (int w = 0; w < kThreads / 32; ++w) m |= s_zw[4 * w + tid];
+      zmask[tid] = m;
+    }
     RES_PROF(10);
-    if (tid < 4) S.zpart[cta * 4 + tid] = zmask[tid];
+    // zero-column flags: one OR per CTA into S.zpart[0..3] (reset by CTA 0
+    // after the next exchange, and by the launcher), published by the exchange
+    if (tid < 4 && zmask[tid]) atomicOr(S.zpart + tid, zmask[tid]);
     partial_rows(RT, bsn, nbr, l, lp, k, RED, S.part + (int64_t)cta * nel);  // B-check (454)
     RES_PROF(11);
-    exchange(S, G, cta, ep);
+    exchange_fast(S, G, ep);
     RES_PROF(12);
-    if (tid < 4) zmask[tid] = 0u;
-    __syncthreads();
-    for (int e = tid; e < G * 4; e += kThreads) {
-      const unsigned v = __ldcg(S.zpart + e);
-      if (v) atomicOr(&zmask[e & 3], v);
-    }
+    if (tid < 4) zmask[tid] = __ldcg(S.zpart + tid);
     __syncthreads();
     int j0 = k;
     for (int j = col0; j < jd; ++j)
@@ -430,7 +430,8 @@ __global__ void __launch_bounds__(kThreads, 1) hals_resident_kernel(const ResArg
     }
     RES_PROF(13);
     slice_reduce(S.part, G, nel, S.bchk);
-    exchange(S, G, cta, ep);
+    exchange_fast(S, G, ep);
+    if (cta == 0 && tid < 4) S.zpart[tid] = 0u;  // every CTA has read the flags
     RES_PROF(15);
     load_and_gram(S.bchk, l, lp, k, MS, GW);  // g for the next A half (422)
     RES_PROF(16);
@@ -445,7 +446,7 @@ __global__ void __launch_bounds__(kThreads, 1) hals_resident_kernel(const ResArg
   if (cta == 0 && tid == 0) {
     *S.halt = HaltInfo{0, p.it_end, 0, 0, 0, 0, ep};
     if (prof)
-      for (int i = 0; i < 17; ++i) S.prof[i] += s_prof[i];
+      for (int i = 0; i < 21; ++i) S.prof[i] += s_prof[i];
   }
 #undef RES_PROF
 }
@@ -488,6 +489,8 @@ cudaError_t launch_hals_resident(const HalsState& st, int normalize_a, double al
   const size_t smem = (size_t)res_layout(a.rows_a, a.rows_b, st.lp, st.k).total * sizeof(double);
   cudaError_t e = cudaFuncSetAttribute(hals_resident_kernel,
                                        cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  if (e != cudaSuccess) return e;
+  e = cudaMemsetAsync(st.zpart, 0, 4 * sizeof(unsigned), s);  // zero-column flag words
   if (e != cudaSuccess) return e;
   void* args[] = {&a};
   note_launches(1);
