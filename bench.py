@@ -203,24 +203,33 @@ def run_ours(args, name, c, rank, world, local_rank):
     import paper_1712_02248_b200 as cb
 
     torch.cuda.set_device(local_rank)
-    ctx = cb.Context(local_rank)
     d, n, k, q, w, iters = c["d"], c["n"], c["k"], c["q"], c["w"], c["iters"]
-    ldx = (n + 3) // 4 * 4
+    if world > 1:
+        # column-sharded run: this rank holds X[:, lo:hi] (synthesised locally)
+        ctx = cb.ShardedContext.from_process_group(local_rank)
+        lo, hi = cb.shard_range(n, rank, world)
+    else:
+        ctx = cb.Context(local_rank)
+        lo, hi = 0, n
+    nloc = hi - lo
+    ldx = (nloc + 3) // 4 * 4
     x = torch.empty((d, ldx), dtype=torch.float32, device="cuda")
-    ctx.synth_x(d, n, c["rank"], c["factor_kind"], c["noise_kind"], c["sigma"], 1, x)
-    xv = x[:, :n]
+    ctx.synth_x(d, n, c["rank"], c["factor_kind"], c["noise_kind"], c["sigma"], 1, x, lo, hi)
+    xv = x[:, :nloc]
+    solve = (lambda xx, cc, aa=None, bb=None: ctx.run_sharded(xx, n, cc, aa, bb)) if world > 1 \
+        else (lambda xx, cc, aa=None, bb=None: ctx.run_device(xx, cc, aa, bb))
     cfg = cb.SolverConfig(algorithm=cb.FASTHALS_RP, k=k, sketch=cb.SketchConfig(q, w, 1),
                           max_iterations=iters, error_interval=iters, rel_tolerance=1e-300,
                           seed=1)
     a = torch.empty((d, k), device="cuda")
-    b = torch.empty((n, k), device="cuda")
+    b = torch.empty((nloc, k), device="cuda")
     flush = torch.empty(2 * L2_BYTES // 4, dtype=torch.float32, device="cuda")
     stream = torch.cuda.ExternalStream(ctx.stream())
-    x_bytes = 4.0 * d * n
+    x_bytes = 4.0 * d * nloc  # this GPU's X bytes
     big = x_bytes > L2_BYTES
 
     for _ in range(args.warmup):
-        ctx.run_device(xv, cfg, a, b)
+        solve(xv, cfg, a, b)
     torch.cuda.synchronize()
     if world > 1:
         torch.distributed.barrier()
@@ -234,7 +243,7 @@ def run_ours(args, name, c, rank, world, local_rank):
             e0 = torch.cuda.Event(enable_timing=True)
             e1 = torch.cuda.Event(enable_timing=True)
             e0.record(stream)
-            _, _, tr = ctx.run_device(xv, cfg, a, b)
+            _, _, tr = solve(xv, cfg, a, b)
             e1.record(stream)
             e1.synchronize()
             steps.append(e0.elapsed_time(e1) * 1e-3)
@@ -256,7 +265,7 @@ def run_ours(args, name, c, rank, world, local_rank):
     hbm, src = peaks()
     t_nn = ctx.time_xstream(xv, q, 0, iters=10)
     t_tn = ctx.time_xstream(xv, q, 1, iters=10)
-    alg_bytes = 4.0 * d * n + 4.0 * (d + n) * q
+    alg_bytes = 4.0 * d * nloc + 4.0 * (d + nloc) * q
     ach_nn = alg_bytes / t_nn / 1e9
     ach_tn = alg_bytes / t_tn / 1e9
     traffic = None
@@ -267,7 +276,7 @@ def run_ours(args, name, c, rank, world, local_rank):
         except Exception:
             traffic = None
     mean_comp = statistics.mean(comp)
-    xstream_gbs = passes[0] * x_bytes / mean_comp / 1e9
+    xstream_gbs = passes[0] * 4.0 * d * n / mean_comp / 1e9  # whole-job X bytes
 
     line = {"metric": METRIC, "value": value, "unit": "s", "n_gpus": world,
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms_per_step,
@@ -275,12 +284,12 @@ def run_ours(args, name, c, rank, world, local_rank):
             "dtype": "f32", "data": "synthetic",
             "config": {"workload": workload_desc(name, c), "d": d, "n": n, "k": k, "l": q,
                        "power_iterations": w, "iterations": iters,
-                       "parallelism": f"column-shard x{world}" if world > 1 else "1 GPU",
+                       "parallelism": f"X column-sharded over {world} GPUs (NCCL)" if world > 1 else "1 GPU",
                        "l2": ("inputs larger than L2 (X %.0f MB > 126 MB)" % (x_bytes / 1e6))
                        if big else "L2 flushed (256 MB write) between timed steps"},
             "compress_seconds": mean_comp, "hals_seconds": statistics.mean(upd),
             "x_passes": passes[0], "x_stream_gbs": xstream_gbs,
-            "x_stream_gbs_fused_min": (2 * w + 2) * x_bytes / mean_comp / 1e9,
+            "x_stream_gbs_fused_min": (2 * w + 2) * 4.0 * d * n / mean_comp / 1e9,
             "roofline": {"bound": "hbm", "kernel": "xs_kernel (X*S, NN contraction)",
                          "achieved": ach_nn, "peak": hbm, "unit": "GB/s",
                          "frac": ach_nn / hbm, "traffic": traffic,
@@ -293,18 +302,31 @@ def run_ours(args, name, c, rank, world, local_rank):
             "clocks": clk.summary()}
 
     if not args.no_e2e:
-        xh = torch.empty((d, n), dtype=torch.float32, pin_memory=True)
+        xh = torch.empty((d, nloc), dtype=torch.float32, pin_memory=True)
         xh.copy_(xv)
-        xnp = xh.numpy()
-        ctx.run(xnp, cfg)  # warm
+        if world == 1:
+            xnp = xh.numpy()
+            ctx.run(xnp, cfg)  # warm
         e2e = []
         for _ in range(max(1, min(args.steps, 3))):
+            if world > 1:
+                torch.distributed.barrier()
             t0 = time.perf_counter()
-            ctx.run(xnp, cfg)
+            if world == 1:
+                ctx.run(xnp, cfg)
+            else:  # host shard -> device, collective run, factors -> host
+                xd = xh.to("cuda", non_blocking=True)
+                aa, bb, _ = ctx.run_sharded(xd, n, cfg)
+                aa.cpu(), bb.cpu()
             e2e.append(time.perf_counter() - t0)
-        line["e2e"] = {"value": statistics.mean(e2e), "unit": "s",
+        ev = statistics.mean(e2e)
+        if world > 1:
+            t = torch.tensor([ev], dtype=torch.float64, device="cuda")
+            torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
+            ev = t.item()
+        line["e2e"] = {"value": ev, "unit": "s",
                        "h2d_bytes_per_step": int(4 * d * n),
-                       "d2h_bytes_per_step": int(4 * (d + n) * k)}
+                       "d2h_bytes_per_step": int(4 * (d * world + n) * k)}
 
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         vals, kind, sample = cpu_reference_sample(name, c, 1)

@@ -138,6 +138,26 @@ cnmf_status cnmf_run_device(cnmf_context* ctx, const float* x_dev, uint64_t d, u
                             uint64_t ldx, const cnmf_solver_config* cfg, float* a_dev,
                             float* b_dev, cnmf_run_trace* trace);
 
+/* ---- column-sharded multi-GPU run (one process per GPU, NCCL) ---------
+ * cnmf::run (solvers.hpp:104) with X column-sharded over `world` ranks:
+ * rank g holds columns [cnmf_shard_begin(n, g, world), cnmf_shard_begin(n,
+ * g + 1, world)).  Rank 0 calls cnmf_nccl_unique_id, the caller broadcasts
+ * the 128 bytes (e.g. over torch.distributed), every rank then creates its
+ * context.  All ranks must call cnmf_run_sharded_device collectively with
+ * the same d, n and config; each gets the full A (d x k) and its own rows of
+ * B (n_local x k).  Collectives: NCCL sum all-reduces of d x l sketch
+ * partials and l x l Gram partials in the compression, one (l + 1) x k
+ * all-reduce per HALS iteration (B-check partial + zero-column flags), an
+ * all-gather of B for the final Gini. */
+uint64_t cnmf_shard_begin(uint64_t n, int rank, int world);
+cnmf_status cnmf_nccl_unique_id(unsigned char id[128]);
+cnmf_status cnmf_context_create_sharded(int device, int rank, int world,
+                                        const unsigned char id[128], cnmf_context** out);
+cnmf_status cnmf_run_sharded_device(cnmf_context* ctx, const float* x_shard_dev, uint64_t d,
+                                    uint64_t n, uint64_t col_begin, uint64_t n_local,
+                                    uint64_t ldx, const cnmf_solver_config* cfg, float* a_dev,
+                                    float* b_local_dev, cnmf_run_trace* trace);
+
 /* ---- step-level entry points (all pointers are DEVICE pointers) ------- */
 
 /* gaussian_sketch(rows, cols, seed), compression.cpp:11-16; fp32 rounding

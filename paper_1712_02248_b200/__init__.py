@@ -101,7 +101,8 @@ EXPORTS = [
     "cnmf_initialize", "cnmf_powered_range_finder", "cnmf_build_projectors", "cnmf_compress",
     "cnmf_compress_factors", "cnmf_fasthals_rp_steps", "cnmf_reconstruction_error",
     "cnmf_thin_qr", "cnmf_xs_nn", "cnmf_xs_tn", "cnmf_synth_x", "cnmf_launch_count",
-    "cnmf_time_xstream",
+    "cnmf_time_xstream", "cnmf_shard_begin", "cnmf_nccl_unique_id", "cnmf_context_create_sharded",
+    "cnmf_run_sharded_device",
 ]
 
 
@@ -159,6 +160,12 @@ def load_library(path: str = LIB_PATH):
                                u64, fp]
     L.cnmf_launch_count.restype = u64
     L.cnmf_time_xstream.argtypes = [vp, fp, u64, u64, u64, u64, C.c_int, C.c_int, dp]
+    L.cnmf_shard_begin.argtypes = [u64, C.c_int, C.c_int]
+    L.cnmf_shard_begin.restype = u64
+    L.cnmf_nccl_unique_id.argtypes = [C.c_char_p]
+    L.cnmf_context_create_sharded.argtypes = [C.c_int, C.c_int, C.c_int, C.c_char_p, C.POINTER(vp)]
+    L.cnmf_run_sharded_device.argtypes = [vp, fp, u64, u64, u64, u64, u64, C.POINTER(_Config), fp,
+                                          fp, C.POINTER(_Trace)]
     if L.cnmf_abi_version() != 1:
         raise CudaError("libcnmf_b200.so ABI version mismatch")
     _lib = L
@@ -413,6 +420,63 @@ class Context:
 
 _default_ctx: Optional[Context] = None
 
+
+
+def shard_begin(n: int, rank: int, world: int) -> int:
+    """First column of rank's shard: floor(n * rank / world) (host-only, no GPU)."""
+    return int(load_library().cnmf_shard_begin(n, rank, world))
+
+
+def shard_range(n: int, rank: int, world: int):
+    return shard_begin(n, rank, world), shard_begin(n, rank + 1, world)
+
+
+class ShardedContext(Context):
+    """cnmf_context of one rank of a column-sharded run (NCCL communicator).
+
+    from_process_group() builds it on every rank of an initialised
+    torch.distributed group: rank 0 draws the NCCL unique id and broadcasts it.
+    """
+
+    def __init__(self, device: int, rank: int, world: int, unique_id: bytes):
+        self.L = load_library()
+        h = C.c_void_p()
+        st = self.L.cnmf_context_create_sharded(device, rank, world, bytes(unique_id), C.byref(h))
+        if st:
+            raise _ERRORS.get(st, CnmfError)(f"cannot create sharded context (rank {rank}/{world})")
+        self.h = h
+        self.rank, self.world = rank, world
+
+    @staticmethod
+    def unique_id() -> bytes:
+        buf = C.create_string_buffer(128)
+        st = load_library().cnmf_nccl_unique_id(buf)
+        if st:
+            raise _ERRORS.get(st, CnmfError)("ncclGetUniqueId failed")
+        return buf.raw
+
+    @classmethod
+    def from_process_group(cls, device: int):
+        import torch.distributed as dist
+        rank, world = dist.get_rank(), dist.get_world_size()
+        obj = [cls.unique_id() if rank == 0 else None]
+        dist.broadcast_object_list(obj, src=0)
+        return cls(device, rank, world, obj[0])
+
+    def run_sharded(self, x_shard, n: int, config: SolverConfig, a_out=None, b_out=None):
+        """Collective cnmf::run on this rank's columns of a d x n X (torch CUDA
+        tensor d x n_local, the columns [shard_begin(n, rank), shard_begin(n, rank+1)))."""
+        import torch
+        d, nloc = x_shard.shape
+        lo = shard_begin(n, self.rank, self.world)
+        a = a_out if a_out is not None else torch.empty((d, config.k), device=x_shard.device)
+        b = b_out if b_out is not None else torch.empty((nloc, config.k), device=x_shard.device)
+        cfg = config._c()
+        recs, tr = self._trace(config.max_iterations + 2)
+        self._check(self.L.cnmf_run_sharded_device(self.h, _ptr(x_shard), d, n, lo, nloc,
+                                                   x_shard.stride(0), C.byref(cfg), _ptr(a), _ptr(b),
+                                                   C.byref(tr)))
+        return a, b, self._result_trace(recs, tr)
 
 def launch_count() -> int:
     """Device kernels launched by the library so far (this process)."""

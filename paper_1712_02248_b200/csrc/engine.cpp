@@ -60,6 +60,8 @@ struct cnmf_context {
   std::mutex mu;
   std::map<std::string, DevBuf> bufs;
   HaltInfo* halt_host = nullptr;  // pinned
+  void* nccl = nullptr;           // ncclComm_t of a sharded context
+  int rank = 0, world = 1;
 
   template <typename T>
   T* ws(const std::string& name, size_t count) {
@@ -238,7 +240,8 @@ HalsRun make_hals(cnmf_context* c, int64_t d, int64_t n, int l, int lp, int k) {
   s.wsc = c->ws<double>("hals_wsc", (size_t)r.grid * k * k);
   s.part = c->ws<double>("hals_part", hals_part_doubles(r.grid, lp, k));
   s.npart = c->ws<double>("hals_npart", (size_t)2 * r.grid);
-  s.zpart = c->ws<unsigned>("hals_zpart", (size_t)4 * r.grid);
+  s.zpart = c->ws<unsigned>("hals_zpart", (size_t)4 * r.grid + 4);
+  s.sharded = 0;
   s.bar = c->ws<unsigned>("hals_bar", 64);
   s.halt = c->ws<HaltInfo>("hals_halt", 1);
   s.prof = nullptr;
@@ -514,6 +517,8 @@ void run_device_impl(cnmf_context* c, const float* x_in, int64_t d, int64_t n, i
   *tr = t;
 }
 
+#include "sharded.inc"
+
 template <typename F>
 cnmf_status guarded(cnmf_context* c, F&& f) {
   if (!c) return CNMF_ERR_CONFIG;
@@ -593,6 +598,7 @@ void cnmf_context_destroy(cnmf_context* c) {
   if (c->fork) cudaEventDestroy(c->fork);
   if (c->join) cudaEventDestroy(c->join);
   if (c->stream) cudaStreamDestroy(c->stream);
+  if (c->nccl && nccl_api().ok) nccl_api().commDestroy((ncclComm_t)c->nccl);
   delete c;
 }
 
@@ -662,6 +668,62 @@ cnmf_status cnmf_run(cnmf_context* c, const float* x, uint64_t d, uint64_t n, ui
     CK(cudaMemcpyAsync(a_out, ad, sizeof(float) * d * cfg->k, cudaMemcpyDeviceToHost, c->stream));
     CK(cudaMemcpyAsync(b_out, bd, sizeof(float) * n * cfg->k, cudaMemcpyDeviceToHost, c->stream));
     c->sync();
+  });
+}
+
+uint64_t cnmf_shard_begin(uint64_t n, int rank, int world) {
+  if (world < 1 || rank < 0 || rank > world) return 0;
+  return (uint64_t)shard_lo((int64_t)n, rank, world);
+}
+
+cnmf_status cnmf_nccl_unique_id(unsigned char id[128]) {
+  if (!id) return CNMF_ERR_CONFIG;
+  NcclApi& api = nccl_api();
+  if (!api.ok) return CNMF_ERR_NCCL;
+  ncclUniqueId u;
+  if (api.getUniqueId(&u) != ncclSuccess) return CNMF_ERR_NCCL;
+  static_assert(sizeof(ncclUniqueId) == 128, "ncclUniqueId is 128 bytes");
+  std::memcpy(id, &u, 128);
+  return CNMF_OK;
+}
+
+cnmf_status cnmf_context_create_sharded(int device, int rank, int world,
+                                        const unsigned char id[128], cnmf_context** out) {
+  if (!out || !id || world < 1 || rank < 0 || rank >= world) return CNMF_ERR_CONFIG;
+  const cnmf_status s = cnmf_context_create(device, out);
+  if (s != CNMF_OK) return s;
+  cnmf_context* c = *out;
+  NcclApi& api = nccl_api();
+  if (!api.ok) {
+    c->err = api.error;
+    cnmf_context_destroy(c);
+    *out = nullptr;
+    return CNMF_ERR_NCCL;
+  }
+  ncclUniqueId u;
+  std::memcpy(&u, id, 128);
+  ncclComm_t comm = nullptr;
+  cudaSetDevice(device);
+  if (api.commInitRank(&comm, world, u, rank) != ncclSuccess) {
+    cnmf_context_destroy(c);
+    *out = nullptr;
+    return CNMF_ERR_NCCL;
+  }
+  c->nccl = comm;
+  c->rank = rank;
+  c->world = world;
+  return CNMF_OK;
+}
+
+cnmf_status cnmf_run_sharded_device(cnmf_context* c, const float* x_shard, uint64_t d, uint64_t n,
+                                    uint64_t col_begin, uint64_t n_local, uint64_t ldx,
+                                    const cnmf_solver_config* cfg, float* a_dev, float* b_local_dev,
+                                    cnmf_run_trace* trace) {
+  return guarded(c, [&] {
+    if (!cfg || !trace || !x_shard || !a_dev || !b_local_dev)
+      throw Fail(CNMF_ERR_CONFIG, "null argument");
+    run_sharded_impl(c, x_shard, (int64_t)d, (int64_t)n, (int64_t)col_begin, (int64_t)n_local,
+                     (int64_t)ldx, *cfg, a_dev, b_local_dev, trace);
   });
 }
 

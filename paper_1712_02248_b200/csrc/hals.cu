@@ -551,6 +551,21 @@ __global__ void __launch_bounds__(kThreads, 1) hals_kernel(const HalsArgs p) {
       if (v) atomicOr(&zmask[e & 3], v);
     }
     __syncthreads();
+    if (S.sharded) {
+      // this rank's B-check partial; the host all-reduces it with the other
+      // ranks' and decides zero columns on the global mask.  bcur keeps the
+      // old B for a host-side rollback.
+      for (int c = jd; c < k; ++c)  // columns from a dead A column on were not reached
+        for (int r = tid; r < nbr; r += kThreads) {
+          const int64_t gi = (int64_t)c * n + b_lo + r;
+          bnxt[gi] = bcur[gi];
+        }
+      slice_reduce(S.part, G, nel, S.bchk);
+      exchange(S, G, cta, ep);
+      if (cta == 0 && tid < 4) S.zpart[4 * G + tid] = zmask[tid];
+      if (cta == 0 && tid == 0) *S.halt = HaltInfo{1, it + 1, 1, jd, kEvShard, bnxt == S.bold, ep};
+      return;
+    }
     int j0 = k;
     for (int j = col0; j < jd; ++j)
       if (!(zmask[j >> 5] & (1u << (j & 31)))) { j0 = j; break; }

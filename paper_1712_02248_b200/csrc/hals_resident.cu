@@ -414,6 +414,23 @@ __global__ void __launch_bounds__(kThreads, 1) hals_resident_kernel(const ResArg
     RES_PROF(12);
     if (tid < 4) zmask[tid] = __ldcg(S.zpart + tid);
     __syncthreads();
+    if (S.sharded) {
+      // this rank's B-check partial; the host all-reduces it with the other
+      // ranks' and decides zero columns on the global mask
+      slice_reduce(S.part, G, nel, S.bchk);
+      exchange_fast(S, G, ep);
+      if (cta == 0 && tid < 4) {
+        S.zpart[4 * G + tid] = zmask[tid];
+        S.zpart[tid] = 0u;
+      }
+      for (int e = tid; e < nbr * k; e += kThreads) {  // old B for a host-side rollback
+        const int c = e / nbr, r = e - c * nbr;
+        S.bold[(int64_t)c * n + b_lo + r] = bsc[r * kp1 + c];
+      }
+      write_back(bsn);
+      if (cta == 0 && tid == 0) *S.halt = HaltInfo{1, it + 1, 1, jd, kEvShard, 0, ep};
+      return;
+    }
     int j0 = k;
     for (int j = col0; j < jd; ++j)
       if (!(zmask[j >> 5] & (1u << (j & 31)))) { j0 = j; break; }

@@ -3,6 +3,8 @@
 #pragma once
 
 #include <cuda_runtime.h>
+
+#include <functional>
 #ifndef __CUDACC__
 #ifndef __host__
 #define __host__
@@ -67,6 +69,9 @@ bool launch_xs_tc(bool tn, const float* x, int64_t ldx, int64_t m, int64_t n, co
 // when the Cholesky factor is numerically singular.  Y and Q are rows x lp
 // (ld lp); columns >= l are zero on output.  q must not alias y.
 size_t qr_ws_bytes(int64_t rows, int lp, int nsm);
+void launch_thin_qr_dist(const float* y, int64_t rows, int l, int lp, float* q, void* ws, int nsm,
+                         cudaStream_t st, const std::function<void(double*, size_t)>& allreduce_g,
+                         int** flag_out);
 void launch_thin_qr(const float* y, int64_t rows, int l, int lp, float* q, void* ws, int nsm,
                     cudaStream_t st);
 
@@ -98,11 +103,12 @@ struct HaltInfo {
   int iter;    // iteration (1-based) in which the event happened
   int half;    // 0 = A half-sweep, 1 = B half-sweep
   int column;
-  int kind;    // 1 dead B column (g_jj), 2 zero A column, 3 dead A column (w_jj), 4 zero B column
+  int kind;    // 1 dead B column (g_jj), 2 zero A column, 3 dead A column (w_jj), 4 zero B column,
+               // 5 sharded: B half done on this rank (column = first dead-A column or k)
   int pad;
   unsigned long long last_epoch;  // exchange epoch reached (next launch starts above it)
 };
-enum { kEvDeadB = 1, kEvZeroA = 2, kEvDeadA = 3, kEvZeroB = 4 };
+enum { kEvDeadB = 1, kEvZeroA = 2, kEvDeadA = 3, kEvZeroB = 4, kEvShard = 5 };
 
 struct HalsState {
   int64_t d, n;
@@ -122,10 +128,14 @@ struct HalsState {
   double* wsc;       // [grid][k*k] per-CTA copy of w = A-hat^T A-hat (fp64)
   double* part;      // [grid][lp*k] partial sums
   double* npart;     // [2][grid] column-norm partials (by exchange parity)
-  unsigned* zpart;   // [grid][4] non-zero-column bitmasks
+  unsigned* zpart;   // [grid][4] non-zero-column bitmasks, then [4] the CTA-OR (sharded halt)
   unsigned* bar;     // monotonic grid-barrier arrival counter (reset per run)
   HaltInfo* halt;
   long long* prof;   // optional per-phase clock64 sums (CTA 0), or null
+  int sharded;       // 1: X column-sharded across ranks: after each B half the kernel halts
+                     // (kEvShard) with this rank's B-check partial in bchk, its non-zero
+                     // column mask in zpart[4 grid ..], the new B in b (resident kernel:
+                     // the old B in bold); the host all-reduces and runs the zero check
 };
 size_t hals_part_doubles(int grid, int lp, int k);
 int hals_grid(const HalsState& st, int nsm);

@@ -13,6 +13,8 @@
 #include "common.cuh"
 #include "kernels.h"
 
+#include <functional>
+
 namespace cnmf {
 
 namespace {
@@ -144,17 +146,29 @@ __global__ void gram_reduce_kernel(const double* __restrict__ part, int grid, in
 // triangle: Rinv[i][c] lives at gs[c][i].  flag |= 1 when a pivot is
 // non-positive or below 1e-13 of its original diagonal (Y numerically rank
 // deficient at fp32 resolution).
-__global__ void __launch_bounds__(1024) chol_inv_kernel(const double* __restrict__ g, int l,
-                                                        int lp, double* __restrict__ rinv64,
-                                                        float* __restrict__ rinv,
-                                                        int* __restrict__ flag) {
-  extern __shared__ double gs[];  // l x l, then diag0[l], rdiag[l]
+// Cholesky G = R^T R (R upper) and R^-1, fp64, one CTA of 128 threads.
+// Right-looking factorisation with two barriers per column: every thread
+// reads the pivot, row j is scaled by 1/r (the diagonal itself is kept in
+// rd[] so nothing rewrites gs[j][j] while others read it), then the trailing
+// update.  R^-1 is built column-parallel by back substitution -- column c by
+// thread c, no barriers: Rinv[c][c] = 1/r_c, Rinv[i][c] = -(sum_{q=i+1..c}
+// R[i][q] Rinv[q][c]) / r_i.  Fails (flag) if a pivot drops below
+// 1e-13 * its original diagonal (rank deficiency -> Householder fallback).
+__global__ void __launch_bounds__(128) chol_inv_kernel(const double* __restrict__ g, int l,
+                                                       int lp, double* __restrict__ rinv64,
+                                                       float* __restrict__ rinv,
+                                                       int* __restrict__ flag) {
+  extern __shared__ double gs[];  // l x l (R upper; R^-1 transposed into the lower part), diag0, rd, rdi
   double* diag0 = gs + l * l;
-  double* rdiag = diag0 + l;
+  double* rd = diag0 + l;
+  double* rdi = rd + l;
   const int tid = threadIdx.x, nt = blockDim.x;
   for (int e = tid; e < l * l; e += nt) gs[e] = g[(e / l) * lp + e % l];
   for (int e = tid; e < l; e += nt) diag0[e] = g[e * lp + e];
-  for (int e = tid; e < lp * lp; e += nt) rinv[e] = 0.f;
+  for (int e = tid; e < lp * lp; e += nt) {
+    rinv[e] = 0.f;
+    rinv64[e] = 0.0;
+  }
   __syncthreads();
   for (int j = 0; j < l; ++j) {
     const double piv = gs[j * l + j];
@@ -162,36 +176,35 @@ __global__ void __launch_bounds__(1024) chol_inv_kernel(const double* __restrict
       if (tid == 0) *flag = 1;
       return;
     }
-    const double r = sqrt(piv);
-    __syncthreads();  // everyone has read the pivot
-    for (int c = j + 1 + tid; c < l; c += nt) gs[j * l + c] /= r;
+    const double r = sqrt(piv), ir = 1.0 / r;
+    for (int c = j + 1 + tid; c < l; c += nt) gs[j * l + c] *= ir;
     if (tid == 0) {
-      gs[j * l + j] = r;
-      rdiag[j] = 1.0 / r;
+      rd[j] = r;
+      rdi[j] = ir;
     }
     __syncthreads();
     const int m = l - j - 1;
     for (int e = tid; e < m * m; e += nt) {
       const int a = j + 1 + e / m, b = j + 1 + e % m;
-      if (a <= b) gs[a * l + b] -= gs[j * l + a] * gs[j * l + b];
+      if (a <= b) gs[a * l + b] = fma(-gs[j * l + a], gs[j * l + b], gs[a * l + b]);
     }
     __syncthreads();
   }
-  // R^-1 by rows from the bottom: Rinv[i][c] = -(sum_{q=i+1..c} R[i][q] Rinv[q][c]) / R[i][i]
-  for (int i = l - 1; i >= 0; --i) {
-    for (int c = i + 1 + tid; c < l; c += nt) {
-      double s = gs[i * l + c] * rdiag[c];  // q = c term (Rinv[c][c] = 1/R[c][c])
-      for (int q = i + 1; q < c; ++q) s += gs[i * l + q] * gs[c * l + q];
-      gs[c * l + i] = -s * rdiag[i];
+  // thread c owns column c of R^-1, kept transposed in row c of gs's lower
+  // triangle (gs[c][i] = Rinv[i][c], i < c) -- untouched by the factorisation
+  for (int c = tid; c < l; c += nt) {
+    double* xc = gs + c * l;
+    for (int i = c - 1; i >= 0; --i) {
+      double sacc = gs[i * l + c] * rdi[c];  // q = c term
+      for (int q = i + 1; q < c; ++q) sacc = fma(gs[i * l + q], xc[q], sacc);
+      xc[i] = -sacc * rdi[i];
     }
-    __syncthreads();
-  }
-  for (int e = tid; e < l * l; e += nt) {
-    const int i = e / l, c = e - i * l;
-    if (c < i) continue;
-    const double v = c == i ? rdiag[i] : gs[c * l + i];
-    rinv[i * lp + c] = (float)v;
-    rinv64[i * lp + c] = v;
+    rinv[c * lp + c] = (float)rdi[c];
+    rinv64[c * lp + c] = rdi[c];
+    for (int i = 0; i < c; ++i) {
+      rinv[i * lp + c] = (float)xc[i];
+      rinv64[i * lp + c] = xc[i];
+    }
   }
 }
 
@@ -276,15 +289,15 @@ void gram(const float* y, int64_t rows, int l, int lp, const QrWs& w, int nsm,
 }
 
 void chol_inv(int l, int lp, const QrWs& w, cudaStream_t st) {
-  const size_t smem = sizeof(double) * (l * l + 2 * l);
+  const size_t smem = sizeof(double) * (l * l + 3 * l);
   static bool attr = false;
   if (!attr) {
     cudaFuncSetAttribute(chol_inv_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                         (int)(sizeof(double) * (128 * 128 + 256)));
+                         (int)(sizeof(double) * (128 * 128 + 3 * 128)));
     attr = true;
   }
   note_launches(1);
-  chol_inv_kernel<<<1, 1024, smem, st>>>(w.g, l, lp, w.rinv64, w.rinv, w.flag);
+  chol_inv_kernel<<<1, 128, smem, st>>>(w.g, l, lp, w.rinv64, w.rinv, w.flag);
 }
 
 }  // namespace
@@ -296,6 +309,28 @@ size_t qr_ws_bytes(int64_t rows, int lp, int nsm) {
          r(sizeof(float) * lp * lp) + r(sizeof(float) * rows * lp) + r(16) +
          2 * r(sizeof(double) * rows * lp) + r(sizeof(float) * xstream_ws_floats(rows, lp, lp, nsm)) +
          1024;
+}
+
+// CholeskyQR2 of a ROW-SHARDED matrix (each rank holds `rows` rows of Y):
+// the fp64 Gram of the local rows is completed by the caller's in-place sum
+// all-reduce across ranks (two lp x lp Gram all-reduces
+// per QR); R^-1 is then identical on every rank and applied locally.  No
+// Householder fallback here: *flag_out (device int) is set when a pivot
+// broke down and the caller gathers Y for the replicated path.
+void launch_thin_qr_dist(const float* y, int64_t rows, int l, int lp, float* q, void* ws, int nsm,
+                         cudaStream_t st, const std::function<void(double*, size_t)>& allreduce_g,
+                         int** flag_out) {
+  const QrWs w = carve(ws, rows, lp, nsm);
+  cudaMemsetAsync(w.flag, 0, sizeof(int), st);
+  gram(y, rows, l, lp, w, nsm, st);
+  allreduce_g(w.g, (size_t)lp * lp);
+  chol_inv(l, lp, w, st);
+  launch_xs_nn(y, lp, rows, lp, w.rinv, lp, w.q1, w.xs_ws, nsm, st);
+  gram(w.q1, rows, l, lp, w, nsm, st);
+  allreduce_g(w.g, (size_t)lp * lp);
+  chol_inv(l, lp, w, st);
+  launch_xs_nn(w.q1, lp, rows, lp, w.rinv, lp, q, w.xs_ws, nsm, st);
+  *flag_out = w.flag;
 }
 
 void launch_thin_qr(const float* y, int64_t rows, int l, int lp, float* q, void* ws, int nsm,

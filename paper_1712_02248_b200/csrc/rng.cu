@@ -7,8 +7,8 @@
 // fresh Rng(seed); initialize (proj/src/solvers.cpp:206-211, 314-325) fills A
 // then B row-major with uniform_positive.
 //
-// MT19937-64 is sequential, so one warp owns one engine and emits its raw
-// 64-bit stream 156 words per step.  The
+// MT19937-64 is sequential, so one CTA owns one engine and emits its raw
+// 64-bit stream 312 words per twist (156 threads, two words each).  The
 // mapping kernels are then fully parallel: normal e uses words 2*(e/2) and
 // 2*(e/2)+1 and uniform e uses word e, EXCEPT after a word whose 53-bit
 // uniform is exactly 0 (probability 2^-53 per draw), where the reference
@@ -38,52 +38,43 @@ __device__ __forceinline__ uint64_t temper(uint64_t z) {
   return z;
 }
 
-// One warp per engine.  The engine is run as its linear recurrence
-//   x[p + 312] = x[p + 156] ^ mix(x[p], x[p + 1])
-// over a 312-word shared-memory ring (slot p % 312): the 156 words
-// x[N .. N+155] depend only on x[N-312 .. N-1], so each step computes them in
-// parallel (about five per lane), reads before writes, two __syncwarp()s per
-// step and no block barrier.  Output word t is temper(x[312 + t]), exactly the
-// std::mt19937_64 sequence (first twist after seeding).
-__global__ void __launch_bounds__(32) mt_stream_kernel(MtJobs jobs) {
+// One CTA per engine; blockDim.x == 160 (156 active in the twist).
+__global__ void __launch_bounds__(160) mt_stream_kernel(MtJobs jobs) {
   const MtJob job = jobs.job[blockIdx.x];
-  __shared__ uint64_t x[kN];
-  const int lane = threadIdx.x;
-  if (lane == 0) {
-    x[0] = job.seed;
+  __shared__ uint64_t mt[kN];
+  const int t = threadIdx.x;
+  if (t == 0) {
+    mt[0] = job.seed;
     for (int i = 1; i < kN; ++i)
-      x[i] = 6364136223846793005ULL * (x[i - 1] ^ (x[i - 1] >> 62)) + (uint64_t)i;
+      mt[i] = 6364136223846793005ULL * (mt[i - 1] ^ (mt[i - 1] >> 62)) + (uint64_t)i;
   }
-  __syncwarp();
-  constexpr int kPer = (kM + 31) / 32;  // 5 words per lane per step
-  const uint64_t nsteps = (job.nwords + kM - 1) / kM;
-  int base = 0;  // (N - 312) % 312 for the current step, N = 312 + 156 * step
-  for (uint64_t step = 0; step < nsteps; ++step) {
-    uint64_t v[kPer];
-#pragma unroll
-    for (int r = 0; r < kPer; ++r) {
-      const int i = lane + 32 * r;
-      if (i < kM) {
-        const int j = base + i;  // < 312 + 156
-        const int s0 = j >= kN ? j - kN : j;
-        const int s1 = j + 1 >= kN ? j + 1 - kN : j + 1;
-        const int s2 = j + kM >= kN ? j + kM - kN : j + kM;
-        v[r] = x[s2] ^ mix(x[s0], x[s1]);
-      }
+  __syncthreads();
+  const uint64_t nblocks = (job.nwords + kN - 1) / kN;
+  for (uint64_t blk = 0; blk < nblocks; ++blk) {
+    uint64_t o0 = 0, o1 = 0, o156 = 0, o157 = 0, o311 = 0;
+    if (t < kM) {
+      o0 = mt[t];
+      o1 = mt[t + 1];
+      o156 = mt[t + kM];
+      if (t + kM + 1 < kN) o157 = mt[t + kM + 1];
+      if (t == 0) o311 = mt[kN - 1];
     }
-    __syncwarp();
-    const uint64_t out0 = step * kM;
-#pragma unroll
-    for (int r = 0; r < kPer; ++r) {
-      const int i = lane + 32 * r;
-      if (i < kM) {
-        const int j = base + i;
-        x[j >= kN ? j - kN : j] = v[r];
-        if (out0 + i < job.nwords) job.out[out0 + i] = temper(v[r]);
-      }
+    __syncthreads();
+    if (t < kM) {
+      const uint64_t nt = o156 ^ mix(o0, o1);  // i = t       (uses old values)
+      mt[t] = nt;
+      if (t + kM < kN - 1) mt[t + kM] = nt ^ mix(o156, o157);  // i = t+156 (new mt[i-156])
     }
-    __syncwarp();
-    base = base + kM >= kN ? base + kM - kN : base + kM;
+    __syncthreads();
+    if (t == 0) mt[kN - 1] = mt[kM - 1] ^ mix(o311, mt[0]);  // i = 311 (new mt[0], mt[155])
+    __syncthreads();
+    if (t < kM) {
+      const uint64_t base = blk * kN;
+      if (base + t < job.nwords) job.out[base + t] = temper(mt[t]);
+      if (base + t + kM < job.nwords) job.out[base + t + kM] = temper(mt[t + kM]);
+    }
+    // next iteration's reads happen after its first __syncthreads
+    __syncthreads();
   }
 }
 
@@ -175,7 +166,7 @@ __global__ void uniform_init_exact_kernel(const uint64_t* __restrict__ words, ui
 
 void launch_mt_streams(const MtJobs& jobs, int njobs, cudaStream_t s) {
   note_launches(1);
-  mt_stream_kernel<<<njobs, 32, 0, s>>>(jobs);
+  mt_stream_kernel<<<njobs, 160, 0, s>>>(jobs);
 }
 
 void launch_normal_map(const uint64_t* words, uint64_t count, int cols, int ld, float* out,
