@@ -422,3 +422,20 @@ def test_run_zero_iterations_returns_init(ctx, oracle):
     assert [r.iteration for r in res.trace.records] == [0]
     assert np.array_equal(res.a, a.astype(np.float32))
     assert np.array_equal(res.b, b.astype(np.float32))
+
+
+def test_run_c4_shape_class_parity(ctx, oracle):
+    """BASELINE configs[3] (C4) shape class at a size the oracle finishes in
+    seconds: Gamma(0.3,1) factors, Poisson counts (exact zeros), k=100,
+    l=120 (the 128-wide tensor-core tiles, the streaming HALS kernel with
+    k=100 sequential column norms), q=1."""
+    x = oracle.synth_x(1200, 1600, 100, 2, 2, 0.0, 1)
+    assert (x == 0).mean() > 0.0  # count data with exact zeros
+    res, ra, rb, rt = _run_both(ctx, oracle, x, k=100, q=120, w=1, iters=8, every=2)
+    xn = float(np.sum(x.astype(np.float64) ** 2))
+    assert [r.iteration for r in res.trace.records] == rt.iterations
+    got = rel_err([r.error for r in res.trace.records], xn)
+    want = rel_err(rt.errors, xn)
+    assert np.max(np.abs(got - want) / want) < TRAJ_RTOL
+    assert rel_fro(res.a, ra) < FACTOR_RTOL and rel_fro(res.b, rb) < FACTOR_RTOL
+    assert res.trace.status == rt.status and res.trace.iterations_run == rt.iterations_run
