@@ -136,15 +136,40 @@ def cpu_reference_sample(name, c, timed_steps=1):
     x = o.synth_x(d, n, c["rank"], c["factor_kind"], c["noise_kind"], c["sigma"], 1,
                   col_lo=0, col_hi=n_s).astype(np.float64)
     vals = []
+    impl = r if kind == "reference" else o
     for _ in range(timed_steps):
-        if kind == "reference":
-            left, right, xhat, xcheck, t_comp = r.compress(x, q, w, 1)
+        if full:
+            if kind == "reference":
+                left, right, xhat, xcheck, t_comp = r.compress(x, q, w, 1)
+            else:
+                t0 = time.perf_counter()
+                left, right = o.build_projectors(x, q, w, 1)
+                xhat, xcheck = o.compress(x, left, right)
+                t_comp = time.perf_counter() - t0
         else:
+            # compress = (2w + 2) NN and (2w + 2) TN X contractions (linear in n:
+            # timed on the column slice, scaled by n / n_s) + (1 + 2w) thin QRs of
+            # d x q and of n x q bases (timed at full shape) + the two sketches
+            rng = np.random.default_rng(0)
+            s_n = rng.standard_normal((n_s, q))
+            t_d = rng.standard_normal((d, q))
             t0 = time.perf_counter()
-            left, right = o.build_projectors(x, q, w, 1)
-            xhat, xcheck = o.compress(x, left, right)
-            t_comp = time.perf_counter() - t0
-        t_comp *= n / n_s
+            impl.matmul(x, s_n)
+            t_nn = time.perf_counter() - t0
+            t0 = time.perf_counter()
+            impl.matmul(x, t_d, tl=True)
+            t_tn = time.perf_counter() - t0
+            t0 = time.perf_counter()
+            impl.thin_qr(rng.standard_normal((d, q)))
+            t_qd = time.perf_counter() - t0
+            t0 = time.perf_counter()
+            impl.thin_qr(rng.standard_normal((n, q)))
+            t_qn = time.perf_counter() - t0
+            t0 = time.perf_counter()
+            impl.gaussian_sketch(n, q, 2)
+            impl.gaussian_sketch(d, q, 3)
+            t_sk = time.perf_counter() - t0
+            t_comp = (2 * w + 2) * (t_nn + t_tn) * (n / n_s) + (1 + 2 * w) * (t_qd + t_qn) + t_sk
         if full:
             a, b = o.initialize(d, n, k, 1)
             ah, bc = o.compress_factors(a, b, left, right)
@@ -170,8 +195,9 @@ def cpu_reference_sample(name, c, timed_steps=1):
     sample = (f"full {name.upper()} workload: build_projectors+compress_left/right on the "
               f"{d}x{n} X and {iters} fasthals_rp_step calls, single thread (the reference "
               f"solver is single-threaded)") if full else (
-              f"extrapolated: compression on a {d}x{n_s} column slice scaled by n/n_s "
-              f"(cost linear in n) + one full-shape fasthals_rp_step x {iters}")
+              f"extrapolated: the {4 * w + 4} X contractions timed on a {d}x{n_s} column slice "
+              f"and scaled by n/n_s (cost linear in n), {2 + 4 * w} thin QRs at full shape, the "
+              f"two sketches, + one full-shape fasthals_rp_step x {iters}; single thread")
     return vals, kind, sample
 
 
