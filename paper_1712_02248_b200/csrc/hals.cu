@@ -53,171 +53,186 @@ struct HalsArgs {
   unsigned long long epoch0;
 };
 
-// Stages rows [r0, r0 + 64) of a global fp32 matrix (ld lp) as fp64 into
-// stage (stride lp + 1), zero beyond nrows.  float4 loads, all issued first.
-__device__ __forceinline__ void stage64_f32(const float* __restrict__ in, int r0, int nrows,
-                                            int lp, double* stage) {
-  const int lpp = lp + 1, q4 = lp >> 2, total = 64 * q4;
-  float4 v[8];
-#pragma unroll
-  for (int u = 0; u < 8; ++u) {
-    const int e = threadIdx.x + kThreads * u;
-    v[u] = make_float4(0.f, 0.f, 0.f, 0.f);
-    if (e < total) {
-      const int rr = e / q4, c4 = e - rr * q4;
-      if (r0 + rr < nrows)
-        v[u] = __ldg(reinterpret_cast<const float4*>(in + (int64_t)(r0 + rr) * lp) + c4);
-    }
-  }
-#pragma unroll
-  for (int u = 0; u < 8; ++u) {
-    const int e = threadIdx.x + kThreads * u;
-    if (e < total) {
-      const int rr = e / q4, c4 = e - rr * q4;
-      double* d = stage + rr * lpp + 4 * c4;
-      d[0] = v[u].x;
-      d[1] = v[u].y;
-      d[2] = v[u].z;
-      d[3] = v[u].w;
-    }
-  }
-}
+// ---- streamed products ----------------------------------------------------
+// Both routines stream the CTA's rows of an fp32 matrix (ld lp) in 64-row
+// stages converted to fp64 in shared memory (stride lp + 1: conflict-free
+// column reads), with the NEXT stage prefetched into registers while the
+// current one is computed, and 4 x 4 register tiles whose warps span rows
+// (X reads conflict-free, M / F reads broadcast): ~64 FMAs per shared-memory
+// wavefront, the DFMA rate.
+constexpr int kSR = 64;                 // rows per stage
+constexpr int kPF = 8;                  // float4 per thread per stage (lp <= 128)
 
-// out(r, c) = sum_q In[r, q] * M[q, c] for r < nrows, c < k (fp64).  In:
-// global fp32 rows (ld lp) staged 64 at a time as fp64; M: shared fp64 lp x k.
-// Thread (rg, cg) owns rows rg + 16 i (i < 4) and columns cg + 16 t (t < 8).
-template <typename Out>
-__device__ void rows_times_small(const float* __restrict__ in, int nrows, int lp, int k,
-                                 const double* __restrict__ M, double* stage, Out out) {
-  const int lpp = lp + 1;
-  const int rg = threadIdx.x & 15, cg = threadIdx.x >> 4;
-  const int nt = (k - cg + 15) >> 4;
-  for (int r0 = 0; r0 < nrows; r0 += 64) {
-    __syncthreads();
-    stage64_f32(in, r0, nrows, lp, stage);
-    __syncthreads();
-    double acc[4][8];
+struct StagePrefetch {
+  float4 v[kPF];
+  __device__ __forceinline__ void load(const float* __restrict__ in, int r0, int nrows, int lp) {
+    const int q4 = lp >> 2, total = kSR * q4;
 #pragma unroll
-    for (int i = 0; i < 4; ++i)
-#pragma unroll
-      for (int t = 0; t < 8; ++t) acc[i][t] = 0.0;
-    for (int q = 0; q < lp; ++q) {
-      double xv[4];
-#pragma unroll
-      for (int i = 0; i < 4; ++i) xv[i] = stage[(rg + 16 * i) * lpp + q];
-      const double* mrow = M + q * k + cg;
-#pragma unroll
-      for (int t = 0; t < 8; ++t) {
-        if (t < nt) {
-          const double mv = mrow[16 * t];
-#pragma unroll
-          for (int i = 0; i < 4; ++i) acc[i][t] = fma(xv[i], mv, acc[i][t]);
-        }
+    for (int u = 0; u < kPF; ++u) {
+      const int e = threadIdx.x + kThreads * u;
+      v[u] = make_float4(0.f, 0.f, 0.f, 0.f);
+      if (e < total) {
+        const int rr = e / q4, c4 = e - rr * q4;
+        if (r0 + rr < nrows)
+          v[u] = __ldg(reinterpret_cast<const float4*>(in + (int64_t)(r0 + rr) * lp) + c4);
       }
     }
+  }
+  __device__ __forceinline__ void store(int lp, double* stage) const {
+    const int lpp = lp + 1, q4 = lp >> 2, total = kSR * q4;
 #pragma unroll
-    for (int i = 0; i < 4; ++i) {
-      const int r = r0 + rg + 16 * i;
-      if (r < nrows) {
+    for (int u = 0; u < kPF; ++u) {
+      const int e = threadIdx.x + kThreads * u;
+      if (e < total) {
+        const int rr = e / q4, c4 = e - rr * q4;
+        double* dd = stage + rr * lpp + 4 * c4;
+        dd[0] = v[u].x;
+        dd[1] = v[u].y;
+        dd[2] = v[u].z;
+        dd[3] = v[u].w;
+      }
+    }
+  }
+};
+
+// out(r, c) = sum_{q < kdim} In[r, q] M[q, c] (fp64, q ascending) for r < nrows,
+// c < k.  M: shared fp64 (lp x k).  Thread tile: rows rg + 16 i (i < 4) of the
+// stage, columns 4 cg .. 4 cg + 3.
+template <typename Out>
+__device__ void rows_times_small(const float* __restrict__ in, int nrows, int lp, int kdim, int k,
+                                 const double* __restrict__ M, double* stage, Out out) {
+  const int lpp = lp + 1;
+  const int ncg = (k + 3) >> 2, ntile = 16 * ncg;
+  const int nst = (nrows + kSR - 1) / kSR;
+  StagePrefetch pf;
+  if (nst > 0) pf.load(in, 0, nrows, lp);
+  for (int st = 0; st < nst; ++st) {
+    const int r0 = st * kSR;
+    __syncthreads();
+    pf.store(lp, stage);
+    __syncthreads();
+    if (st + 1 < nst) pf.load(in, r0 + kSR, nrows, lp);  // in flight during the compute
+    for (int t = threadIdx.x; t < ntile; t += kThreads) {
+      const int rg = t & 15, cg = t >> 4;
+      const int c0 = 4 * cg;
+      double acc[4][4];
 #pragma unroll
-        for (int t = 0; t < 8; ++t)
-          if (t < nt) out(r, cg + 16 * t, acc[i][t]);
+      for (int i = 0; i < 4; ++i)
+#pragma unroll
+        for (int j = 0; j < 4; ++j) acc[i][j] = 0.0;
+      const double* x0 = stage + rg * lpp;
+#pragma unroll 2
+      for (int q = 0; q < kdim; ++q) {
+        double xv[4], mv[4];
+#pragma unroll
+        for (int i = 0; i < 4; ++i) xv[i] = x0[16 * i * lpp + q];
+#pragma unroll
+        for (int j = 0; j < 4; ++j) mv[j] = c0 + j < k ? M[q * k + c0 + j] : 0.0;
+#pragma unroll
+        for (int i = 0; i < 4; ++i)
+#pragma unroll
+          for (int j = 0; j < 4; ++j) acc[i][j] = fma(xv[i], mv[j], acc[i][j]);
+      }
+#pragma unroll
+      for (int i = 0; i < 4; ++i) {
+        const int r = r0 + rg + 16 * i;
+        if (r < nrows) {
+#pragma unroll
+          for (int j = 0; j < 4; ++j)
+            if (c0 + j < k) out(r, c0 + j, acc[i][j]);
+        }
       }
     }
   }
   __syncthreads();
 }
 
-// Per-CTA partial P[l', c] = sum_r In[r, l'] * F[c][row0 + r] (fp64) into part
-// (global lp x k).  In: fp32 rows (ld lp); F: column-major fp64 state (ld
-// ldf).  Staged 32 rows at a time; 4x4 output blocks, one per thread; with
-// fewer blocks than threads the rows are split over `ng` groups combined in a
-// fixed order through `red` (may alias the staging).
+// Per-CTA partial P[l', c] = sum_r In[r, l'] * F[c][row0 + r] (fp64, rows in
+// ascending order) into part (global lp x k, rows >= l zero).  In: fp32 rows
+// (ld lp), register-prefetched like rows_times_small; F: column-major fp64
+// state (ld ldf), copied by cp.async into a double-buffered row-major stage
+// (fst: 2 x kSR x (k + 1)).  4 x 4 output tiles accumulate in registers
+// across all stages (several passes when l x k needs more than one tile per
+// thread).
+__device__ __forceinline__ void cp_async8(double* dst, const double* src) {
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"(
+                   static_cast<uint32_t>(__cvta_generic_to_shared(dst))),
+               "l"(src)
+               : "memory");
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
+__device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wait_group 0;" ::: "memory"); }
+
 __device__ void small_partial(const float* __restrict__ in, int nrows, int l, int lp, int k,
                               const double* __restrict__ F, int64_t ldf, double* stage,
-                              double* fst, double* red, double* __restrict__ part) {
+                              double* fst, double* /*red*/, double* __restrict__ part,
+                              long long* prof = nullptr) {
+  long long tp = 0;
+  if (prof && threadIdx.x == 0) tp = clock64();
   const int lpp = lp + 1, kp1 = k + 1;
   const int nbl = (l + 3) >> 2, nbc = (k + 3) >> 2, nb = nbl * nbc;
-  const int ng = nb >= kThreads ? 1 : min(16, kThreads / nb);
-  for (int e = threadIdx.x; e < lp * k; e += kThreads) part[e] = 0.0;
-  for (int g0 = 0; g0 < nb; g0 += kThreads) {
-    const int slot = ng > 1 ? (int)threadIdx.x % nb : (int)threadIdx.x;
-    const int grp = ng > 1 ? (int)threadIdx.x / nb : 0;
-    const int b = g0 + slot;
-    const bool own = b < nb && grp < ng;
-    const int bl = own ? b / nbc : 0, bc = own ? b - bl * nbc : 0;
+  const int nst = (nrows + kSR - 1) / kSR;
+  const int fsz = kSR * kp1;
+  auto copy_f = [&](int r0, double* dst) {  // zero-filled beyond nrows
+    for (int e = threadIdx.x; e < kSR * k; e += kThreads) {
+      const int c = e / kSR, rr = e - c * kSR;
+      if (r0 + rr < nrows) cp_async8(dst + rr * kp1 + c, F + (int64_t)c * ldf + r0 + rr);
+      else dst[rr * kp1 + c] = 0.0;
+    }
+    cp_async_commit();
+  };
+  for (int b0 = 0; b0 < nb; b0 += kThreads) {
+    const int b = b0 + threadIdx.x;
+    const bool own = b < nb;
+    const int bl = own ? b / nbc : 0, bc = own ? b - (b / nbc) * nbc : 0;
     double acc[16];
 #pragma unroll
     for (int i = 0; i < 16; ++i) acc[i] = 0.0;
-    for (int r0 = 0; r0 < nrows; r0 += 32) {
-      const int rmax = min(32, nrows - r0);
-      __syncthreads();
-      {
-        const int q4 = lp >> 2, total = 32 * q4;
-        float4 v[4];
-#pragma unroll
-        for (int u = 0; u < 4; ++u) {
-          const int e = threadIdx.x + kThreads * u;
-          v[u] = make_float4(0.f, 0.f, 0.f, 0.f);
-          if (e < total) {
-            const int rr = e / q4, c4 = e - rr * q4;
-            if (rr < rmax)
-              v[u] = __ldg(reinterpret_cast<const float4*>(in + (int64_t)(r0 + rr) * lp) + c4);
-          }
-        }
-        double fv[16];
-#pragma unroll
-        for (int u = 0; u < 16; ++u) {
-          const int e = threadIdx.x + kThreads * u;
-          const int c = e >> 5, rr = e & 31;
-          fv[u] = (c < k && rr < rmax) ? __ldcg(F + (int64_t)c * ldf + r0 + rr) : 0.0;
-        }
-#pragma unroll
-        for (int u = 0; u < 4; ++u) {
-          const int e = threadIdx.x + kThreads * u;
-          if (e < total) {
-            const int rr = e / q4, c4 = e - rr * q4;
-            double* d = stage + rr * lpp + 4 * c4;
-            d[0] = v[u].x;
-            d[1] = v[u].y;
-            d[2] = v[u].z;
-            d[3] = v[u].w;
-          }
-        }
-#pragma unroll
-        for (int u = 0; u < 16; ++u) {
-          const int e = threadIdx.x + kThreads * u;
-          const int c = e >> 5, rr = e & 31;
-          if (c < k) fst[rr * kp1 + c] = fv[u];
-        }
+    StagePrefetch pf;
+    __syncthreads();  // previous users of stage / fst are done
+    if (nst > 0) {
+      pf.load(in, 0, nrows, lp);
+      copy_f(0, fst);
+    }
+    for (int st = 0; st < nst; ++st) {
+      const int r0 = st * kSR;
+      double* fcur = fst + (st & 1) * fsz;
+      __syncthreads();  // stage (X) free
+      pf.store(lp, stage);
+      cp_async_wait_all();
+      __syncthreads();  // X stage and F stage st visible
+      if (prof && threadIdx.x == 0) {
+        const long long t = clock64();
+        prof[0] += t - tp;
+        tp = t;
       }
-      __syncthreads();
+      if (st + 1 < nst) {
+        pf.load(in, r0 + kSR, nrows, lp);
+        copy_f(r0 + kSR, fst + ((st + 1) & 1) * fsz);
+      }
       if (own) {
-        for (int rr = grp; rr < rmax; rr += ng) {
+        // stages are zero-filled past nrows: a fixed trip count the
+        // compiler can unroll and software-pipeline
+#pragma unroll 4
+        for (int rr = 0; rr < kSR; ++rr) {
           double xi[4], fj[4];
 #pragma unroll
           for (int i = 0; i < 4; ++i) xi[i] = stage[rr * lpp + 4 * bl + i];
 #pragma unroll
-          for (int j = 0; j < 4; ++j) fj[j] = (4 * bc + j < k) ? fst[rr * kp1 + 4 * bc + j] : 0.0;
+          for (int j = 0; j < 4; ++j) fj[j] = 4 * bc + j < k ? fcur[rr * kp1 + 4 * bc + j] : 0.0;
 #pragma unroll
           for (int i = 0; i < 4; ++i)
 #pragma unroll
             for (int j = 0; j < 4; ++j) acc[4 * i + j] = fma(xi[i], fj[j], acc[4 * i + j]);
         }
       }
+      if (prof && threadIdx.x == 0) {
+        const long long t = clock64();
+        prof[1] += t - tp;
+        tp = t;
+      }
     }
-    if (ng > 1) {
-      __syncthreads();
-      if (own)
-#pragma unroll
-        for (int i = 0; i < 16; ++i) red[(grp * nb + slot) * 16 + i] = acc[i];
-      __syncthreads();
-      if (own && grp == 0)
-        for (int g = 1; g < ng; ++g)
-#pragma unroll
-          for (int i = 0; i < 16; ++i) acc[i] += red[(g * nb + slot) * 16 + i];
-    }
-    if (own && grp == 0) {
+    if (own) {
 #pragma unroll
       for (int i = 0; i < 4; ++i)
 #pragma unroll
@@ -227,6 +242,7 @@ __device__ void small_partial(const float* __restrict__ in, int nrows, int l, in
         }
     }
   }
+  for (int e = l * k + threadIdx.x; e < lp * k; e += kThreads) part[e] = 0.0;
   __syncthreads();
 }
 
@@ -285,7 +301,9 @@ __global__ void __launch_bounds__(kThreads, 1) hals_kernel(const HalsArgs p) {
   __shared__ double s_total;
   __shared__ unsigned zmask[4];
   __shared__ double s_diag[128];  // g_jj / w_jj (divisors and dead checks)
-  __shared__ long long s_prof[17];
+  __shared__ double s_ginv[128];  // 1 / g_jj (A half)
+  __shared__ double s_red[2];     // norm all-reduce: total, 1/sqrt(total)
+  __shared__ long long s_prof[21];
 
   const HalsState& S = p.st;
   const int G = gridDim.x, cta = blockIdx.x, tid = threadIdx.x;
@@ -304,12 +322,12 @@ __global__ void __launch_bounds__(kThreads, 1) hals_kernel(const HalsArgs p) {
   double* stage64 = smem + lp * k;
   double* gw = smem;
   double* stP = smem;
-  double* fsP = smem + 32 * lpp;
+  double* fsP = smem + kSR * lpp;
 
   const bool prof = S.prof != nullptr && cta == 0;
   long long t_last = 0;
   if (prof && tid == 0) {
-    for (int i = 0; i < 17; ++i) s_prof[i] = 0;
+    for (int i = 0; i < 21; ++i) s_prof[i] = 0;
     t_last = clock64();
   }
 #define HALS_PROF(id)                 \
@@ -332,11 +350,14 @@ __global__ void __launch_bounds__(kThreads, 1) hals_kernel(const HalsArgs p) {
       // h = X-check B-check for this CTA's rows (solvers.cpp:421)
       for (int e = tid; e < lp * k; e += kThreads) Ms[e] = __ldcg(S.bchk + e);
       HALS_PROF(0);
-      rows_times_small(S.xc + a_lo * lp, na, lp, k, Ms, stage64,
+      rows_times_small(S.xc + a_lo * lp, na, lp, l, k, Ms, stage64,
                        [&](int r, int c, double v) { S.h[(int64_t)c * d + a_lo + r] = v; });
       for (int e = tid; e < k * k; e += kThreads) gw[e] = gsc[e];
       __syncthreads();
-      for (int e = tid; e < k; e += kThreads) s_diag[e] = gw[e * k + e];
+      for (int e = tid; e < k; e += kThreads) {
+        s_diag[e] = gw[e * k + e];
+        s_ginv[e] = 1.0 / gw[e * k + e];
+      }
       __syncthreads();
       HALS_PROF(1);
       // solvers.cpp:424 checks g_jj once per column; a column redrawn for
@@ -394,7 +415,7 @@ __global__ void __launch_bounds__(kThreads, 1) hals_kernel(const HalsArgs p) {
         for (int t = 0; t < kNB; ++t) {
           if (t >= nbj) break;
           const int j = jb + t;
-          const double gjj = s_diag[j];
+          const double ginv = s_ginv[j];
           double nrm = 0.0, vv[kMaxRPT];
 #pragma unroll
           for (int i = 0; i < kMaxRPT; ++i) {
@@ -405,7 +426,7 @@ __global__ void __launch_bounds__(kThreads, 1) hals_kernel(const HalsArgs p) {
 #pragma unroll
               for (int u = 0; u < kNB; ++u)
                 if (u < t) s = fma(dl[i][u], gw[(jb + u) * k + j], s);
-              const double v = av[i] + (hv[i] - s) / gjj;
+              const double v = av[i] + (hv[i] - s) * ginv;
               vv[i] = v > 0.0 ? v : 0.0;
               nrm = fma(vv[i], vv[i], nrm);
             }
@@ -419,9 +440,8 @@ __global__ void __launch_bounds__(kThreads, 1) hals_kernel(const HalsArgs p) {
             hn[i] = ok ? __ldcg(S.h + (int64_t)(j + 1) * d + a_lo + r) : 0.0;
             an[i] = ok ? __ldcg(S.a + (int64_t)(j + 1) * d + a_lo + r) : 0.0;
           }
-          const double cta_nrm = block_sum(nrm, red8);
           HALS_PROF(2);
-          const double total = allreduce(S, G, cta, ep, cta_nrm, &s_total);
+          const double total = allreduce_fused(S, G, cta, ep, nrm, red8, s_red);
           HALS_PROF(3);
           if (total == 0.0) {  // column emptied: host redraws a_j (solvers.cpp:435)
 #pragma unroll
@@ -433,12 +453,12 @@ __global__ void __launch_bounds__(kThreads, 1) hals_kernel(const HalsArgs p) {
               *S.halt = HaltInfo{1, it + 1, 0, j, kEvZeroA, bcur == S.bold, ep};
             return;
           }
-          const double nv = sqrt(total);
+          const double inv_nrm = s_red[1];
 #pragma unroll
           for (int i = 0; i < kMaxRPT; ++i) {
             const int r = tid + kThreads * i;
             if (i < rpt && r < na) {  // solvers.cpp:436
-              const double nf = p.normalize_a ? vv[i] / nv : vv[i];
+              const double nf = p.normalize_a ? vv[i] * inv_nrm : vv[i];
               S.a[(int64_t)j * d + a_lo + r] = nf;
               dl[i][t] = nf - av[i];
             }
@@ -455,7 +475,7 @@ __global__ void __launch_bounds__(kThreads, 1) hals_kernel(const HalsArgs p) {
       }
       // A-hat = L^T A (solvers.cpp:438): partials, exchange, slice reduce, exchange
       small_partial(S.lm + a_lo * lp, na, l, lp, k, S.a + a_lo, d, stP, fsP, smem,
-                    S.part + (int64_t)cta * nel);
+                    S.part + (int64_t)cta * nel, prof ? s_prof + 17 : nullptr);
       HALS_PROF(4);
       exchange(S, G, cta, ep);
       HALS_PROF(5);
@@ -473,7 +493,7 @@ __global__ void __launch_bounds__(kThreads, 1) hals_kernel(const HalsArgs p) {
     if (!have_w) gram_to_scratch(S.ahat, l, k, smem, wsc);
     // p = X-hat^T A-hat for this CTA's rows (solvers.cpp:442)
     for (int e = tid; e < lp * k; e += kThreads) Ms[e] = __ldcg(S.ahat + e);
-    rows_times_small(S.xht + b_lo * lp, nbr, lp, k, Ms, stage64,
+    rows_times_small(S.xht + b_lo * lp, nbr, lp, l, k, Ms, stage64,
                      [&](int r, int c, double v) { S.p[(int64_t)c * n + b_lo + r] = v; });
     for (int e = tid; e < k * k; e += kThreads) gw[e] = wsc[e];
     if (tid < 4) zmask[tid] = 0u;
@@ -603,7 +623,7 @@ __global__ void __launch_bounds__(kThreads, 1) hals_kernel(const HalsArgs p) {
   if (cta == 0 && tid == 0) {
     *S.halt = HaltInfo{0, p.it_end, 0, 0, 0, bcur == S.bold, ep};
     if (prof)
-      for (int i = 0; i < 17; ++i) S.prof[i] += s_prof[i];
+      for (int i = 0; i < 21; ++i) S.prof[i] += s_prof[i];
   }
 #undef HALS_PROF
 }
@@ -614,7 +634,7 @@ size_t hals_smem_bytes(const HalsState& st, int /*rows_a*/) {
   const int64_t k4 = (k + 3) & ~3;
   const int64_t prod = lp * k + 64 * lpp;
   const int64_t sweep = k * k;
-  const int64_t part = std::max<int64_t>(32 * lpp + 32 * kp1, 16 * kThreads);
+  const int64_t part = kSR * lpp + 2 * kSR * kp1;  // X stage + double-buffered F stage
   const int64_t gram = l * k4;
   return (size_t)std::max(std::max(prod, sweep), std::max(part, gram)) * sizeof(double);
 }
