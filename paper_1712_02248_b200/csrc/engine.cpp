@@ -266,10 +266,12 @@ void redraw_column(cnmf_context* c, std::mt19937_64& rng, double* col_dev, int64
 
 // Runs 0-based iterations [ib, ie) with halt/redraw servicing.  `rng` is
 // produced lazily (positioning the host stream costs a discard).
+// recheck_dead: HALS-RP redraws a dead component until it is alive
+// (solvers.cpp:366-372, `while`); FastHALS-RP checks once (424, `if`).
 template <typename RngFn>
 void run_hals(cnmf_context* c, HalsRun& hr, int normalize_a, double alpha, double beta,
               int64_t ib, int64_t ie, RngFn&& get_rng, double* update_seconds,
-              uint64_t* redraws) {
+              uint64_t* redraws, bool recheck_dead = false) {
   HalsState& st = hr.st;
   int half = 0, col = 0, skip = -1;
   int64_t begin = ib;
@@ -296,7 +298,7 @@ void run_hals(cnmf_context* c, HalsRun& hr, int normalize_a, double alpha, doubl
       case kEvDeadB:  // solvers.cpp:424-428
         redraw_column(c, rng, st.b + (int64_t)j * st.n, st.n);
         launch_compress_factors(st, 1, j, c->stream);
-        half = 0; col = j; skip = j;
+        half = 0; col = j; skip = recheck_dead ? -1 : j;
         break;
       case kEvZeroA:  // solvers.cpp:435-436
         redraw_column(c, rng, st.a + (int64_t)j * st.d, st.d);
@@ -306,7 +308,7 @@ void run_hals(cnmf_context* c, HalsRun& hr, int normalize_a, double alpha, doubl
       case kEvDeadA:  // solvers.cpp:445-449
         redraw_column(c, rng, st.a + (int64_t)j * st.d, st.d);
         launch_compress_factors(st, 0, j, c->stream);
-        half = 1; col = j; skip = j;
+        half = 1; col = j; skip = recheck_dead ? -1 : j;
         break;
       case kEvZeroB:  // solvers.cpp:452
         redraw_column(c, rng, st.b + (int64_t)j * st.n, st.n);
@@ -351,8 +353,14 @@ void run_device_impl(cnmf_context* c, const float* x_in, int64_t d, int64_t n, i
                      const cnmf_solver_config& cfg, float* a_out, float* b_out,
                      cnmf_run_trace* tr) {
   validate(cfg, d, n);
-  if (cfg.algorithm != CNMF_FASTHALS_RP)
-    throw Fail(CNMF_ERR_UNSUPPORTED, "this build implements the fasthals-rp path only");
+  // FastHALS-RP, and HALS-RP: its column updates (solvers.cpp:357-401) equal
+  // FastHALS-RP's with A unnormalised in exact arithmetic, so
+  // the same kernels run it with normalize_a off and dead components
+  // re-checked after a redraw.
+  if (cfg.algorithm != CNMF_FASTHALS_RP && cfg.algorithm != CNMF_HALS_RP)
+    throw Fail(CNMF_ERR_UNSUPPORTED, "this build implements the fasthals-rp and hals-rp paths");
+  const bool hals_rp = cfg.algorithm == CNMF_HALS_RP;
+  const int normalize_a = hals_rp ? 0 : cfg.normalize_a;  // normalize_a: fasthals only (solvers.hpp:24)
   require_shapes(cfg.k, cfg.sketch_q);
   const int k = (int)cfg.k, q = (int)cfg.sketch_q, lp = pad16(q);
   const uint64_t w = cfg.sketch_power_iterations;
@@ -365,7 +373,8 @@ void run_device_impl(cnmf_context* c, const float* x_in, int64_t d, int64_t n, i
   t.alpha = cfg.alpha;
   t.beta = cfg.beta;
   t.seed = cfg.seed;
-  t.estimate_flops_per_iteration = 2.0 * (double)d * k * q;  // metrics.cpp:45
+  t.estimate_flops_per_iteration = hals_rp ? 4.0 * (double)d * n * k * q   // metrics.cpp:44
+                                           : 2.0 * (double)d * k * q;        // metrics.cpp:45
   t.estimate_memory_floats = (2.0 * q + k) * ((double)d + (double)n);
   auto push = [&](uint64_t it, double err, double el) {
     if (t.records_count < t.records_capacity) t.records[t.records_count] = {it, err, el};
@@ -459,8 +468,8 @@ void run_device_impl(cnmf_context* c, const float* x_in, int64_t d, int64_t n, i
   while (t.status != CNMF_ABORTED && it <= max_it) {  // solvers.cpp:231-284
     uint64_t e = ((it + every - 1) / every) * every;
     if (e > max_it) e = max_it;
-    run_hals(c, hr, cfg.normalize_a, cfg.alpha, cfg.beta, (int64_t)it - 1, (int64_t)e, get_rng,
-             &t.update_seconds, &t.redraws);
+    run_hals(c, hr, normalize_a, cfg.alpha, cfg.beta, (int64_t)it - 1, (int64_t)e, get_rng,
+             &t.update_seconds, &t.redraws, hals_rp);
     t.iterations_run = e;
     const double err = timed_error();
     if (!std::isfinite(err)) {

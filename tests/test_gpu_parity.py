@@ -439,3 +439,28 @@ def test_run_c4_shape_class_parity(ctx, oracle):
     assert np.max(np.abs(got - want) / want) < TRAJ_RTOL
     assert rel_fro(res.a, ra) < FACTOR_RTOL and rel_fro(res.b, rb) < FACTOR_RTOL
     assert res.trace.status == rt.status and res.trace.iterations_run == rt.iterations_run
+
+
+@pytest.mark.parametrize("alpha,beta", [(0.0, 0.0), (0.3, 0.05)])
+def test_run_hals_rp_matches_reference(ctx, reference, alpha, beta):
+    """algorithm = hals-rp (solvers.cpp:357-401), served by the FastHALS-RP
+    kernels with A unnormalised and dead components re-checked after a
+    redraw: trajectory and factors against the compiled reference's own
+    hals_rp run (including the constrained b update, 466-478)."""
+    import paper_1712_02248_b200 as cb
+    from oracle import Oracle
+    x = Oracle().synth_x(600, 500, 10, 0, 1, 0.01, 1)
+    cfg = cb.SolverConfig(algorithm=cb.HALS_RP, k=10, sketch=cb.SketchConfig(20, 2, 1),
+                          max_iterations=40, error_interval=1, rel_tolerance=1e-300, seed=1,
+                          alpha=alpha, beta=beta)
+    res = ctx.run(x, cfg)
+    ra, rb, rt = reference.run(x.astype(np.float64), 10, q=20, w=2, sketch_seed=1,
+                               max_iterations=40, error_interval=1, rel_tolerance=1e-300,
+                               seed=1, alpha=alpha, beta=beta, algorithm=cb.HALS_RP)
+    xn = float(np.sum(x.astype(np.float64) ** 2))
+    assert [r.iteration for r in res.trace.records] == list(rt.iterations)
+    got = rel_err([r.error for r in res.trace.records], xn)
+    want = rel_err(rt.errors, xn)
+    assert np.max(np.abs(got - want) / want) < TRAJ_RTOL
+    assert rel_fro(res.a, ra) < FACTOR_RTOL and rel_fro(res.b, rb) < FACTOR_RTOL
+    assert res.trace.status == rt.status
