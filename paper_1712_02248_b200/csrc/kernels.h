@@ -5,6 +5,7 @@
 #include <cuda_runtime.h>
 
 #include <functional>
+#include <vector>
 #ifndef __CUDACC__
 #ifndef __host__
 #define __host__
@@ -35,6 +36,13 @@ struct MtJobs {
   MtJob job[4];
 };
 void launch_mt_streams(const MtJobs& jobs, int njobs, cudaStream_t s);
+// Jump-ahead generation (rng.cu + mt_jump.cpp): the same stream as one engine,
+// in K parallel segments of J outputs.
+bool mt_jump_available();
+bool mt_jump_polys(uint64_t J, int K, std::vector<uint64_t>& out);
+void launch_mt_jump(uint64_t seed, uint64_t nwords, uint64_t J, int K, const uint64_t* polys,
+                    uint64_t* ws, uint64_t* out, cudaStream_t s);
+size_t mt_jump_ws_words(int K);
 void launch_normal_map(const uint64_t* words, uint64_t count, int cols, int ld, float* out,
                        int* flag, int nsm, cudaStream_t s);
 void launch_normal_exact(const uint64_t* words, uint64_t nwords, uint64_t count, int cols, int ld,

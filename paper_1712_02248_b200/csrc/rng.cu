@@ -38,42 +38,108 @@ __device__ __forceinline__ uint64_t temper(uint64_t z) {
   return z;
 }
 
-// One CTA per engine; blockDim.x == 160 (156 active in the twist).
-__global__ void __launch_bounds__(160) mt_stream_kernel(MtJobs jobs) {
-  const MtJob job = jobs.job[blockIdx.x];
-  __shared__ uint64_t mt[kN];
-  const int t = threadIdx.x;
+// One 312-word twist of the state in shared memory, in place (blockDim >=
+// 156; threads >= 156 only take part in the barriers).  Before: mt holds
+// x_p .. x_p+311; after: x_p+312 .. x_p+623.
+__device__ __forceinline__ void mt_twist(uint64_t* mt, int t) {
+  uint64_t o0 = 0, o1 = 0, o156 = 0, o157 = 0, o311 = 0;
+  if (t < kM) {
+    o0 = mt[t];
+    o1 = mt[t + 1];
+    o156 = mt[t + kM];
+    if (t + kM + 1 < kN) o157 = mt[t + kM + 1];
+    if (t == 0) o311 = mt[kN - 1];
+  }
+  __syncthreads();
+  if (t < kM) {
+    const uint64_t nt = o156 ^ mix(o0, o1);  // i = t       (uses old values)
+    mt[t] = nt;
+    if (t + kM < kN - 1) mt[t + kM] = nt ^ mix(o156, o157);  // i = t+156 (new mt[i-156])
+  }
+  __syncthreads();
+  if (t == 0) mt[kN - 1] = mt[kM - 1] ^ mix(o311, mt[0]);  // i = 311 (new mt[0], mt[155])
+  __syncthreads();
+}
+
+__device__ __forceinline__ void mt_seed(uint64_t* mt, uint64_t seed, int t) {
   if (t == 0) {
-    mt[0] = job.seed;
+    mt[0] = seed;
     for (int i = 1; i < kN; ++i)
       mt[i] = 6364136223846793005ULL * (mt[i - 1] ^ (mt[i - 1] >> 62)) + (uint64_t)i;
   }
   __syncthreads();
+}
+
+// One CTA per engine; blockDim.x == 160 (156 active in the twist).  Output
+// word t is temper(x_312+t) (raw = 1: x_312+t itself).
+__global__ void __launch_bounds__(160) mt_stream_kernel(MtJobs jobs, int raw) {
+  const MtJob job = jobs.job[blockIdx.x];
+  __shared__ uint64_t mt[kN];
+  const int t = threadIdx.x;
+  mt_seed(mt, job.seed, t);
   const uint64_t nblocks = (job.nwords + kN - 1) / kN;
   for (uint64_t blk = 0; blk < nblocks; ++blk) {
-    uint64_t o0 = 0, o1 = 0, o156 = 0, o157 = 0, o311 = 0;
-    if (t < kM) {
-      o0 = mt[t];
-      o1 = mt[t + 1];
-      o156 = mt[t + kM];
-      if (t + kM + 1 < kN) o157 = mt[t + kM + 1];
-      if (t == 0) o311 = mt[kN - 1];
-    }
-    __syncthreads();
-    if (t < kM) {
-      const uint64_t nt = o156 ^ mix(o0, o1);  // i = t       (uses old values)
-      mt[t] = nt;
-      if (t + kM < kN - 1) mt[t + kM] = nt ^ mix(o156, o157);  // i = t+156 (new mt[i-156])
-    }
-    __syncthreads();
-    if (t == 0) mt[kN - 1] = mt[kM - 1] ^ mix(o311, mt[0]);  // i = 311 (new mt[0], mt[155])
-    __syncthreads();
+    mt_twist(mt, t);
     if (t < kM) {
       const uint64_t base = blk * kN;
-      if (base + t < job.nwords) job.out[base + t] = temper(mt[t]);
-      if (base + t + kM < job.nwords) job.out[base + t + kM] = temper(mt[t + kM]);
+      const uint64_t w0 = mt[t], w1 = mt[t + kM];
+      if (base + t < job.nwords) job.out[base + t] = raw ? w0 : temper(w0);
+      if (base + t + kM < job.nwords) job.out[base + t + kM] = raw ? w1 : temper(w1);
     }
-    // next iteration's reads happen after its first __syncthreads
+    __syncthreads();  // next twist reads after this block's outputs are taken
+  }
+}
+
+// ---- jump-ahead (parallel segments of one stream) -------------------------
+// Segment k of the output stream starts at output kJ, whose raw word is
+// x_312+kJ.  Its 312 starting words x_312+kJ+w = XOR over the set bits i of
+// c_k = x^(kJ) mod phi of x_312+i+w (mt_jump.cpp), i.e. a GF(2) convolution
+// of the raw prefix x_312 .. x_312+19967+311 with c_k.  CTA b builds the
+// state of segment k = b + 1 from the prefix held in shared memory.
+constexpr int kJumpPoly = 312;                  // words per polynomial (19968 bits)
+constexpr int kJumpPrefix = 64 * kJumpPoly + kN;  // raw words the convolution reads
+
+__global__ void __launch_bounds__(kN) mt_jump_state_kernel(const uint64_t* __restrict__ prefix,
+                                                           const uint64_t* __restrict__ polys,
+                                                           uint64_t* __restrict__ states) {
+  extern __shared__ uint64_t pre[];  // kJumpPrefix words
+  __shared__ uint64_t cpoly[kJumpPoly];
+  const int k = blockIdx.x + 1, w = threadIdx.x;
+  for (int e = w; e < kJumpPrefix; e += blockDim.x) pre[e] = prefix[e];
+  for (int e = w; e < kJumpPoly; e += blockDim.x) cpoly[e] = polys[(size_t)k * kJumpPoly + e];
+  __syncthreads();
+  uint64_t acc = 0;
+  for (int cw = 0; cw < kJumpPoly; ++cw) {
+    uint64_t bits = cpoly[cw];
+    while (bits) {
+      const int b = __ffsll(bits) - 1;
+      bits &= bits - 1;
+      acc ^= pre[64 * cw + b + w];
+    }
+  }
+  states[(size_t)blockIdx.x * kN + w] = acc;
+}
+
+// CTA k emits outputs [kJ, min((k + 1) J, nwords)): the segment's starting
+// words (segment 0: the prefix itself), tempered, then twists onward.
+__global__ void __launch_bounds__(160) mt_segment_kernel(const uint64_t* __restrict__ prefix,
+                                                         const uint64_t* __restrict__ states,
+                                                         uint64_t J, uint64_t nwords,
+                                                         uint64_t* __restrict__ out) {
+  __shared__ uint64_t mt[kN];
+  const int t = threadIdx.x, k = blockIdx.x;
+  const uint64_t s0 = (uint64_t)k * J;
+  if (s0 >= nwords) return;
+  const uint64_t cnt = min(J, nwords - s0);
+  const uint64_t* src = k == 0 ? prefix : states + (size_t)(k - 1) * kN;
+  for (int e = t; e < kN; e += blockDim.x) mt[e] = src[e];
+  __syncthreads();
+  for (uint64_t base = 0; base < cnt; base += kN) {
+    if (base) mt_twist(mt, t);
+    if (t < kM) {
+      if (base + t < cnt) out[s0 + base + t] = temper(mt[t]);
+      if (base + t + kM < cnt) out[s0 + base + t + kM] = temper(mt[t + kM]);
+    }
     __syncthreads();
   }
 }
@@ -166,8 +232,34 @@ __global__ void uniform_init_exact_kernel(const uint64_t* __restrict__ words, ui
 
 void launch_mt_streams(const MtJobs& jobs, int njobs, cudaStream_t s) {
   note_launches(1);
-  mt_stream_kernel<<<njobs, 160, 0, s>>>(jobs);
+  mt_stream_kernel<<<njobs, 160, 0, s>>>(jobs, 0);
 }
+
+// nwords outputs of Rng(seed) in K = ceil(nwords / J) parallel segments;
+// polys: K x 312 words (x^(kJ) mod phi, k = 0 .. K-1) on the device;
+// ws: 312 * (64 + 2) + 312 * K words of scratch.
+void launch_mt_jump(uint64_t seed, uint64_t nwords, uint64_t J, int K, const uint64_t* polys,
+                    uint64_t* ws, uint64_t* out, cudaStream_t s) {
+  uint64_t* prefix = ws;                   // kJumpPrefix raw words
+  uint64_t* states = ws + kJumpPrefix + 8;  // (K - 1) x 312
+  MtJobs jobs{};
+  jobs.job[0] = MtJob{seed, (uint64_t)kJumpPrefix, prefix};
+  note_launches(1);
+  mt_stream_kernel<<<1, 160, 0, s>>>(jobs, 1);
+  if (K > 1) {
+    static bool attr = false;
+    const int smem = (int)(sizeof(uint64_t) * kJumpPrefix);
+    if (!attr) {
+      cudaFuncSetAttribute(mt_jump_state_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+      attr = true;
+    }
+    note_launches(1);
+    mt_jump_state_kernel<<<K - 1, kN, smem, s>>>(prefix, polys, states);
+  }
+  note_launches(1);
+  mt_segment_kernel<<<K, 160, 0, s>>>(prefix, states, J, nwords, out);
+}
+size_t mt_jump_ws_words(int K) { return (size_t)kJumpPrefix + 8 + (size_t)kN * (K > 1 ? K - 1 : 1); }
 
 void launch_normal_map(const uint64_t* words, uint64_t count, int cols, int ld, float* out,
                        int* flag, int nsm, cudaStream_t s) {

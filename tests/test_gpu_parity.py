@@ -68,6 +68,33 @@ def test_initialize_stream_bit_exact(ctx, oracle):
         assert np.array_equal(host(b), rb.astype(np.float32))
 
 
+@pytest.mark.parametrize("d,n,k", [(90000, 60000, 8), (500000, 100000, 10)])
+def test_jump_ahead_stream_bit_exact(ctx, oracle, d, n, k, monkeypatch):
+    """Streams of >= 2^20 words are generated in parallel segments from
+    mt19937_64 jump-ahead states (mt_jump.cpp / rng.cu): bitwise the
+    reference's serial stream (1.2M words -> 37 segments; 6M -> 92)."""
+    a = torch.empty((d, k), device="cuda")
+    b = torch.empty((n, k), device="cuda")
+    ctx.initialize(d, n, k, 7, a, b)
+    ra, rb = oracle.initialize(d, n, k, 7)
+    assert np.array_equal(host(a), ra.astype(np.float32))
+    assert np.array_equal(host(b), rb.astype(np.float32))
+    monkeypatch.setenv("CNMF_MT_SERIAL", "1")  # the serial device engine agrees too
+    a2 = torch.empty_like(a)
+    b2 = torch.empty_like(b)
+    ctx.initialize(d, n, k, 7, a2, b2)
+    assert torch.equal(a, a2) and torch.equal(b, b2)
+
+
+def test_jump_ahead_gaussian_sketch(ctx, oracle):
+    rows, cols, seed = 200000, 40, 3  # 8M normals, jump-ahead segments
+    out = torch.empty((rows, cols), device="cuda")
+    ctx.gaussian_sketch(rows, cols, seed, out)
+    ref = oracle.gaussian_sketch(rows, cols, seed).astype(np.float32)
+    got = host(out)
+    assert np.allclose(got, ref, rtol=3e-7, atol=1e-7), np.abs(got - ref).max()
+
+
 # ----------------------------------------------------------- contractions --
 @pytest.mark.parametrize("d,n,l", [(1000, 1000, 30), (333, 517, 17), (64, 4096, 128),
                                    (5000, 37, 8), (1, 9, 3)])

@@ -12,5 +12,5 @@ for f in rng xstream xstream_tc qr hals hals_resident metrics synth; do
 done
 wait
 /usr/local/cuda/bin/nvcc -gencode arch=compute_100a,code=sm_100a -shared -cudart static \
-  -o $O/libcnmf_b200.so $O/*.o $R/build/engine.o
+  -o $O/libcnmf_b200.so $O/*.o $R/build/engine.o $R/build/mt_jump.o -ldl
 echo "built $1"
