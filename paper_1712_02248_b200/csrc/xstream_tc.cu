@@ -77,34 +77,11 @@ __device__ __forceinline__ void mbar_wait_warp(uint64_t* bar, uint32_t parity) {
   mbar_wait(bar, parity);
   __syncwarp();
 }
-__device__ __forceinline__ void tma_load_2d(void* dst, const CUtensorMap* map, uint64_t* bar,
-                                            int c0, int c1) {
-  asm volatile(
-      "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes"
-      " [%0], [%1, {%3, %4}], [%2];" ::"r"(smem_u32(dst)),
-      "l"(reinterpret_cast<uint64_t>(map)), "r"(smem_u32(bar)), "r"(c0), "r"(c1)
-      : "memory");
-}
 __device__ __forceinline__ void tc_fence_before() {
   asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
 }
 __device__ __forceinline__ void tc_fence_after() {
   asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
-}
-__device__ __forceinline__ void tc_commit(uint64_t* bar) {
-  asm volatile(
-      "tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(
-          smem_u32(bar))
-      : "memory");
-}
-__device__ __forceinline__ void tc_mma_tf32(uint32_t d_tmem, uint64_t a_desc, uint64_t b_desc,
-                                            uint32_t idesc, uint32_t accumulate) {
-  asm volatile(
-      "{\n\t.reg .pred p;\n\t"
-      "setp.ne.b32 p, %4, 0;\n\t"
-      "tcgen05.mma.cta_group::1.kind::tf32 [%0], %1, %2, %3, p;\n\t}" ::"r"(d_tmem),
-      "l"(a_desc), "l"(b_desc), "r"(idesc), "r"(accumulate)
-      : "memory");
 }
 // Shared-memory matrix descriptor (sm_100, version 1).  K-major operands use
 // SWIZZLE_128B (layout 2: 8 rows x 128 B atoms, 16 B granules); MN-major
@@ -145,18 +122,8 @@ struct TcArgs {
   float* out;        // [nsplit][rows_out][lp] or the final output when nsplit == 1
   float* dbg;        // optional debug dump (tools/tc_debug.cu), null in production
   int nmma;          // MMA N = lp rounded up to 16 (<= L): padding columns are not computed
-  int mode;          // experiments only (CNMF_TC_MODE): bit0 skip MMAs, bit1 skip split TMEM stores, bit2 skip epilogue TMEM loads
 };
 
-// x -> (x_hi, x_lo) = (rna_tf32(x), rna_tf32(x - x_hi)); both exactly
-// representable in tf32, so the tensor core's operand conversion is exact.
-__device__ __forceinline__ void tf32_split(float x, float& hi, float& lo) {
-  uint32_t h, l;
-  asm("cvt.rna.tf32.f32 %0, %1;" : "=r"(h) : "f"(x));
-  hi = __uint_as_float(h);
-  asm("cvt.rna.tf32.f32 %0, %1;" : "=r"(l) : "f"(x - hi));
-  lo = __uint_as_float(l);
-}
 
 // Shared-memory rings: X stages (TMA -> split warps) and S stages (TMA ->
 // MMA: s_hi | s_lo).  The split warps write x_hi / x_lo straight into tensor
@@ -232,15 +199,6 @@ __device__ __forceinline__ void tmem_st32(uint32_t taddr, const uint32_t (&v)[32
       "r"(v[15]), "r"(v[16]), "r"(v[17]), "r"(v[18]), "r"(v[19]), "r"(v[20]), "r"(v[21]),
       "r"(v[22]), "r"(v[23]), "r"(v[24]), "r"(v[25]), "r"(v[26]), "r"(v[27]), "r"(v[28]),
       "r"(v[29]), "r"(v[30]), "r"(v[31])
-      : "memory");
-}
-__device__ __forceinline__ void tc_mma_tf32_ts(uint32_t d_tmem, uint32_t a_tmem, uint64_t b_desc,
-                                               uint32_t idesc, uint32_t accumulate) {
-  asm volatile(
-      "{\n\t.reg .pred p;\n\t"
-      "setp.ne.b32 p, %4, 0;\n\t"
-      "tcgen05.mma.cta_group::1.kind::tf32 [%0], [%1], %2, %3, p;\n\t}" ::"r"(d_tmem),
-      "r"(a_tmem), "l"(b_desc), "r"(idesc), "r"(accumulate)
       : "memory");
 }
 
@@ -430,17 +388,13 @@ __global__ void __launch_bounds__(kThreadsTC, 1)
             // offsets (1 KB) are added to the base descriptors directly
             const uint64_t bh = desc_mn(b_addr(b), kBK * 128);
             const uint64_t bl = desc_mn(b_addr(b) + kLoOff, kBK * 128);
-            if (!(args.mode & 1)) {
 #pragma unroll
-              for (int ks = 0; ks < kBK / 8; ++ks) {
-                const uint64_t koff = (uint64_t)(ks * 1024 >> 4);
-                mma_ts_elect(d, ahi + 8 * ks, bh + koff, idesc, acc);
-#ifndef TC_HH_ONLY
-                mma_ts_elect(d, ahi + 8 * ks, bl + koff, idesc, 1u);
-                mma_ts_elect(d, ahi + 32 + 8 * ks, bh + koff, idesc, 1u);
-#endif
-                acc = 1u;
-              }
+            for (int ks = 0; ks < kBK / 8; ++ks) {
+              const uint64_t koff = (uint64_t)(ks * 1024 >> 4);
+              mma_ts_elect(d, ahi + 8 * ks, bh + koff, idesc, acc);
+              mma_ts_elect(d, ahi + 8 * ks, bl + koff, idesc, 1u);
+              mma_ts_elect(d, ahi + 32 + 8 * ks, bh + koff, idesc, 1u);
+              acc = 1u;
             }
             commit_elect(&opempty[o]);  // A slot and S stage free once these MMAs complete
             commit_elect(&bempty[b]);
@@ -499,7 +453,7 @@ __global__ void __launch_bounds__(kThreadsTC, 1)
         mbar_wait_warp(&opempty[o], oph ^ 1);
         if (q == 0 && lane == 0) TC_EV(2, nblk);
         tc_fence_after();
-        if (!(args.mode & 2)) {
+        {
           const uint32_t ta = tmem + ((uint32_t)(32 * q) << 16) + R::kAOff + 64 * o;
           tmem_st32(ta, hi);
           tmem_st32(ta + 32, lo);
@@ -545,7 +499,6 @@ __global__ void __launch_bounds__(kThreadsTC, 1)
         const uint32_t base = tmem + ab * R::kAccCols + ((uint32_t)(32 * q) << 16);
 #pragma unroll
         for (int c = 0; c < R::kAccCols; c += 32) {
-          if (args.mode & 4) break;
           uint32_t h[32];
           asm volatile(
               "tcgen05.ld.sync.aligned.32x32b.x32.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,"
@@ -741,7 +694,6 @@ bool launch_xs_tc(bool tn, const float* x, int64_t ldx, int64_t m, int64_t n, co
   a.lp = lp;
   a.out = p.nsplit > 1 ? parts : out;
   a.dbg = g_tc_debug;
-  a.mode = std::getenv("CNMF_TC_MODE") ? std::atoi(std::getenv("CNMF_TC_MODE")) : 0;
   a.nmma = (lp + 15) & ~15;
   const int units = p.ntiles * p.nsplit;
   const int grid = std::min(units, nsm);
