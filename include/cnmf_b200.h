@@ -172,7 +172,11 @@ cnmf_status cnmf_initialize(cnmf_context* ctx, uint64_t d, uint64_t n, uint64_t 
 cnmf_status cnmf_powered_range_finder(cnmf_context* ctx, const float* x, uint64_t d, uint64_t n,
                                       uint64_t ldx, uint64_t q, uint64_t power_iterations,
                                       uint64_t seed, int transpose, float* basis);
-/* build_projectors (compression.cpp:44-53): left d x q, right q x n. */
+/* build_projectors (compression.cpp:44-53): left d x q, right q x n.
+ * Bases handed out by cnmf_powered_range_finder, cnmf_build_projectors and
+ * cnmf_thin_qr carry the reference's Householder column signs (qr.cpp:35);
+ * cnmf_run skips that pass (FastHALS-RP uses L, R only through
+ * sign-invariant products). */
 cnmf_status cnmf_build_projectors(cnmf_context* ctx, const float* x, uint64_t d, uint64_t n,
                                   uint64_t ldx, uint64_t q, uint64_t power_iterations,
                                   uint64_t seed, float* left, float* right);
@@ -223,6 +227,35 @@ cnmf_status cnmf_time_xstream(cnmf_context* ctx, const float* x, uint64_t d, uin
 cnmf_status cnmf_synth_x(cnmf_context* ctx, uint64_t d, uint64_t n, uint64_t rank,
                          int factor_kind, int noise_kind, double sigma, uint64_t seed,
                          uint64_t col_lo, uint64_t col_hi, uint64_t ldx, float* x);
+
+/* ---- host-side data formats around the path (no device, no context) ----
+ * The front end's inputs and reports; fp64 host code,
+ * bitwise the reference's results.  `msg` (may be NULL) receives the error
+ * text of a failing call. */
+
+/* cnmf::CostEstimate, metrics.hpp:20-28. */
+typedef struct cnmf_cost_estimate {
+  int32_t algorithm;
+  uint64_t d, n, k, q;
+  double flops_per_iteration;
+  double memory_floats;
+} cnmf_cost_estimate;
+
+/* estimate_cost(algorithm, d, n, k, q), metrics.cpp:20-50. */
+cnmf_status cnmf_estimate_cost(int algorithm, uint64_t d, uint64_t n, uint64_t k, uint64_t q,
+                               cnmf_cost_estimate* out, char* msg, size_t msg_cap);
+/* generate_synthetic(SyntheticSpec), data_io.cpp:383-415: d x n row-major
+ * fp64 into out (caller-owned, d * n doubles). */
+cnmf_status cnmf_generate_synthetic(uint64_t d, uint64_t n, uint64_t true_rank, double decay_p,
+                                    double noise_level, uint64_t seed, double* out, char* msg,
+                                    size_t msg_cap);
+/* pairwise_distortion(x, left, sample_pairs, seed), metrics.cpp:123-155,
+ * with the projected columns L^T X given as xhat (q x n fp32, the output of
+ * cnmf_compress): host x is d x n row-major fp64. */
+cnmf_status cnmf_pairwise_distortion(const double* x, uint64_t d, uint64_t n, const float* xhat,
+                                     uint64_t q, uint64_t sample_pairs, uint64_t seed,
+                                     double* max_relative, double* mean_relative, char* msg,
+                                     size_t msg_cap);
 
 #ifdef __cplusplus
 }

@@ -265,6 +265,8 @@ class Reference:
         L.ref_initialize.argtypes = [_sz, _sz, _sz, _u64, _dp, _dp]
         L.ref_matmul.argtypes = [_dp, _sz, _sz, _dp, _sz, _sz, C.c_int, C.c_int, _dp]
         L.ref_thin_qr.argtypes = [_dp, _sz, _sz, _dp, _dp]
+        L.ref_pairwise_distortion.argtypes = [_dp, _sz, _sz, _dp, _sz, _sz, _u64, _dp, _dp]
+        L.ref_generate_synthetic.argtypes = [_sz, _sz, _sz, C.c_double, C.c_double, _u64, _dp]
         L.ref_powered_range_finder.argtypes = [_dp, _sz, _sz, _sz, _sz, _u64, _dp]
         L.ref_build_projectors.argtypes = [_dp, _sz, _sz, _sz, _sz, _u64, _dp, _dp]
         L.ref_compress.argtypes = [_dp, _sz, _sz, _sz, _sz, _u64, _dp, _dp, _dp, _dp, _dp]
@@ -289,6 +291,20 @@ class Reference:
     def gaussian_sketch(self, rows, cols, seed):
         out = np.empty((rows, cols))
         self.lib.ref_gaussian_sketch(rows, cols, _u64(seed), _d(out))
+        return out
+
+    def pairwise_distortion(self, x, left, pairs, seed):
+        x = np.ascontiguousarray(x, dtype=np.float64)
+        left = np.ascontiguousarray(left, dtype=np.float64)
+        mx, mean = np.zeros(1), np.zeros(1)
+        self._check(self.lib.ref_pairwise_distortion(_d(x), x.shape[0], x.shape[1], _d(left),
+                                                     left.shape[1], pairs, _u64(seed), _d(mx),
+                                                     _d(mean)))
+        return float(mx[0]), float(mean[0])
+
+    def generate_synthetic(self, d, n, rank, decay, noise, seed):
+        out = np.empty((d, n))
+        self._check(self.lib.ref_generate_synthetic(d, n, rank, decay, noise, _u64(seed), _d(out)))
         return out
 
     def initialize(self, d, n, k, seed):

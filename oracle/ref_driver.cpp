@@ -13,6 +13,7 @@
 #include <string>
 
 #include "cnmf/compression.hpp"
+#include "cnmf/data_io.hpp"
 #include "cnmf/errors.hpp"
 #include "cnmf/metrics.hpp"
 #include "cnmf/qr.hpp"
@@ -227,6 +228,32 @@ int ref_run(const double* x, std::size_t d, std::size_t n, int algorithm, std::s
     *status = static_cast<int>(r.trace.status);
     *iterations_run = r.trace.iterations_run;
     std::snprintf(message, message_cap, "%s", r.trace.message.c_str());
+  });
+}
+
+// generate_synthetic (data_io.cpp:383-415): d x n, row-major.
+int ref_generate_synthetic(std::size_t d, std::size_t n, std::size_t rank, double decay,
+                           double noise, std::uint64_t seed, double* out) {
+  return guarded([&] {
+    SyntheticSpec spec;
+    spec.d = d;
+    spec.n = n;
+    spec.true_rank = rank;
+    spec.decay_p = decay;
+    spec.noise_level = noise;
+    spec.seed = seed;
+    unwrap(generate_synthetic(spec), out);
+  });
+}
+
+// pairwise_distortion (metrics.cpp:123-155): left is d x q row-major.
+int ref_pairwise_distortion(const double* x, std::size_t d, std::size_t n, const double* left,
+                            std::size_t q, std::size_t pairs, std::uint64_t seed,
+                            double* max_relative, double* mean_relative) {
+  return guarded([&] {
+    const DistortionStats s = pairwise_distortion(wrap(x, d, n), wrap(left, d, q), pairs, seed);
+    *max_relative = s.max_relative;
+    *mean_relative = s.mean_relative;
   });
 }
 

@@ -53,6 +53,14 @@ class InputError(CnmfError, ValueError):
     """cnmf::InputError (std::invalid_argument)."""
 
 
+class IoError(CnmfError, RuntimeError):
+    """cnmf::IoError (std::runtime_error): files that cannot be read or written."""
+
+
+class ParseError(IoError):
+    """cnmf::ParseError (an IoError): malformed input files."""
+
+
 class CudaError(CnmfError, RuntimeError):
     """Device failure or no usable CUDA device (the product never falls back to the CPU)."""
 
@@ -75,6 +83,12 @@ class _Config(C.Structure):
                 ("alpha", C.c_double), ("beta", C.c_double), ("max_iterations", C.c_uint64),
                 ("rel_tolerance", C.c_double), ("error_interval", C.c_uint64),
                 ("seed", C.c_uint64), ("normalize_a", C.c_int32)]
+
+
+class _Cost(C.Structure):
+    _fields_ = [("algorithm", C.c_int32), ("d", C.c_uint64), ("n", C.c_uint64),
+                ("k", C.c_uint64), ("q", C.c_uint64), ("flops_per_iteration", C.c_double),
+                ("memory_floats", C.c_double)]
 
 
 class _Record(C.Structure):
@@ -102,7 +116,8 @@ EXPORTS = [
     "cnmf_compress_factors", "cnmf_fasthals_rp_steps", "cnmf_reconstruction_error",
     "cnmf_thin_qr", "cnmf_xs_nn", "cnmf_xs_tn", "cnmf_synth_x", "cnmf_launch_count",
     "cnmf_time_xstream", "cnmf_shard_begin", "cnmf_nccl_unique_id", "cnmf_context_create_sharded",
-    "cnmf_run_sharded_device",
+    "cnmf_run_sharded_device", "cnmf_estimate_cost", "cnmf_generate_synthetic",
+    "cnmf_pairwise_distortion",
 ]
 
 
@@ -166,6 +181,12 @@ def load_library(path: str = LIB_PATH):
     L.cnmf_context_create_sharded.argtypes = [C.c_int, C.c_int, C.c_int, C.c_char_p, C.POINTER(vp)]
     L.cnmf_run_sharded_device.argtypes = [vp, fp, u64, u64, u64, u64, u64, C.POINTER(_Config), fp,
                                           fp, C.POINTER(_Trace)]
+    L.cnmf_estimate_cost.argtypes = [C.c_int, u64, u64, u64, u64, C.POINTER(_Cost), C.c_char_p,
+                                     C.c_size_t]
+    L.cnmf_generate_synthetic.argtypes = [u64, u64, u64, C.c_double, C.c_double, u64, vp,
+                                          C.c_char_p, C.c_size_t]
+    L.cnmf_pairwise_distortion.argtypes = [vp, u64, u64, vp, u64, u64, u64, dp, dp, C.c_char_p,
+                                           C.c_size_t]
     if L.cnmf_abi_version() != 1:
         raise CudaError("libcnmf_b200.so ABI version mismatch")
     _lib = L
@@ -477,6 +498,61 @@ class ShardedContext(Context):
                                                    x_shard.stride(0), C.byref(cfg), _ptr(a), _ptr(b),
                                                    C.byref(tr)))
         return a, b, self._result_trace(recs, tr)
+
+# ---- host-side data formats around the path (no device) --------------------
+def _host_check(st: int, msg) -> None:
+    if st:
+        raise _ERRORS.get(st, CnmfError)(msg.value.decode())
+
+
+@dataclass
+class CostEstimate:
+    """cnmf::CostEstimate (metrics.hpp:15-23)."""
+    algorithm: int
+    d: int
+    n: int
+    k: int
+    q: int
+    flops_per_iteration: float
+    memory_floats: float
+
+
+def estimate_cost(algorithm, d: int, n: int, k: int, q: int) -> CostEstimate:
+    """cnmf::estimate_cost (metrics.cpp:20-50)."""
+    algo = ALGORITHM_NAMES[algorithm] if isinstance(algorithm, str) else int(algorithm)
+    out, msg = _Cost(), C.create_string_buffer(256)
+    _host_check(load_library().cnmf_estimate_cost(algo, d, n, k, q, C.byref(out), msg, 256), msg)
+    return CostEstimate(out.algorithm, out.d, out.n, out.k, out.q, out.flops_per_iteration,
+                        out.memory_floats)
+
+
+def generate_synthetic(d: int, n: int, true_rank: int = 1, decay_p: float = 0.0,
+                       noise_level: float = 0.0, seed: int = 1) -> np.ndarray:
+    """cnmf::generate_synthetic (data_io.cpp:383-415): d x n float64, bitwise the reference's."""
+    d, n = int(d), int(n)
+    out = np.empty((max(d, 0), max(n, 0)), dtype=np.float64)
+    msg = C.create_string_buffer(256)
+    _host_check(load_library().cnmf_generate_synthetic(d, n, true_rank, decay_p, noise_level,
+                                                       seed, out.ctypes.data, msg, 256), msg)
+    return out
+
+
+def pairwise_distortion(x: np.ndarray, xhat: np.ndarray, sample_pairs: int, seed: int):
+    """cnmf::pairwise_distortion (metrics.cpp:123-155) with the projected
+    columns L^T X given as xhat (q x n, the cnmf_compress output).
+    Returns (max_relative, mean_relative)."""
+    x = np.ascontiguousarray(x, dtype=np.float64)
+    xhat = np.ascontiguousarray(xhat, dtype=np.float32)
+    d, n = x.shape
+    if xhat.shape[1] != n:
+        raise DimensionError("pairwise_distortion: projector rows must match data rows")
+    mx, mean = C.c_double(), C.c_double()
+    msg = C.create_string_buffer(256)
+    _host_check(load_library().cnmf_pairwise_distortion(
+        x.ctypes.data, d, n, xhat.ctypes.data, xhat.shape[0], sample_pairs, seed, C.byref(mx),
+        C.byref(mean), msg, 256), msg)
+    return mx.value, mean.value
+
 
 def launch_count() -> int:
     """Device kernels launched by the library so far (this process)."""

@@ -193,9 +193,11 @@ struct XView {
 // Orthonormal basis (rows x lp) of range(X) (transpose = false) or of
 // range(X^T) (transpose = true); range_finder_impl, compression.cpp:23-42.
 // `omega` holds the sketch (op_cols x lp).  Returns the X passes made.
+// canonical = true: the basis gets the reference's Householder column signs
+// (launch_householder_signs), for the entry points that hand bases out.
 int range_finder(cnmf_context* c, const XView& X, int q, int lp, uint64_t w, bool transpose,
                  const float* omega, float* basis, const std::string& tag,
-                 cudaStream_t st = nullptr) {
+                 cudaStream_t st = nullptr, bool canonical = false) {
   if (!st) st = c->stream;
   const int64_t rows = transpose ? X.n : X.d, cols = transpose ? X.d : X.n;
   float* y = c->ws<float>("rf_y_" + tag, rows * lp);
@@ -217,6 +219,8 @@ int range_finder(cnmf_context* c, const XView& X, int q, int lp, uint64_t w, boo
     apply(zq, y, transpose);
     launch_thin_qr(y, rows, q, lp, basis, qws, c->nsm, st);
   }
+  if (canonical)
+    launch_householder_signs(basis, rows, q, lp, c->ws<float>("hh_sgn_" + tag, 128), c->nsm, st);
   CK(cudaGetLastError());
   return 1 + 2 * (int)w;
 }
@@ -224,13 +228,14 @@ int range_finder(cnmf_context* c, const XView& X, int q, int lp, uint64_t w, boo
 // build_projectors_impl (compression.cpp:44-53): the L and R range finders
 // are independent, so they run concurrently on the context's two streams.
 int build_projectors_dev(cnmf_context* c, const XView& X, int q, int lp, uint64_t w,
-                         uint64_t seed, float* omega_l, float* omega_r, float* lm, float* rt) {
+                         uint64_t seed, float* omega_l, float* omega_r, float* lm, float* rt,
+                         bool canonical = false) {
   CK(cudaEventRecord(c->fork, c->stream));
   CK(cudaStreamWaitEvent(c->side, c->fork, 0));
   gen_normals(c, seed * 2, X.n, q, omega_l, lp, "L", c->stream);
   gen_normals(c, seed * 2 + 1, X.d, q, omega_r, lp, "R", c->side);
-  int passes = range_finder(c, X, q, lp, w, false, omega_l, lm, "L", c->stream);
-  passes += range_finder(c, X, q, lp, w, true, omega_r, rt, "R", c->side);
+  int passes = range_finder(c, X, q, lp, w, false, omega_l, lm, "L", c->stream, canonical);
+  passes += range_finder(c, X, q, lp, w, true, omega_r, rt, "R", c->side, canonical);
   CK(cudaEventRecord(c->join, c->side));
   CK(cudaStreamWaitEvent(c->stream, c->join, 0));
   return passes;
@@ -801,7 +806,7 @@ cnmf_status cnmf_powered_range_finder(cnmf_context* c, const float* x, uint64_t 
     float* out = c->ws<float>("prf_basis", rows * lp);
     CK(cudaMemsetAsync(om, 0, sizeof(float) * cols * lp, c->stream));
     gen_normals(c, seed, (int64_t)cols, (int64_t)q, om, lp, "prf");
-    range_finder(c, X, (int)q, lp, w, transpose != 0, om, out, "prf");
+    range_finder(c, X, (int)q, lp, w, transpose != 0, om, out, "prf", nullptr, true);
     launch_unpad_cols(out, (int64_t)rows, lp, basis, (int)q, c->stream);
     CK(cudaGetLastError());
     c->sync();
@@ -824,7 +829,7 @@ cnmf_status cnmf_build_projectors(cnmf_context* c, const float* x, uint64_t d, u
     float* rt = c->ws<float>("Rt", n * lp);
     CK(cudaMemsetAsync(oml, 0, sizeof(float) * n * lp, c->stream));
     CK(cudaMemsetAsync(omr, 0, sizeof(float) * d * lp, c->stream));
-    build_projectors_dev(c, X, (int)q, lp, w, seed, oml, omr, lm, rt);
+    build_projectors_dev(c, X, (int)q, lp, w, seed, oml, omr, lm, rt, true);
     launch_unpad_cols(lm, (int64_t)d, lp, left, (int)q, c->stream);
     launch_transpose(rt, (int64_t)n, (int64_t)q, lp, right, (int64_t)n, c->stream);
     CK(cudaGetLastError());
@@ -950,6 +955,8 @@ cnmf_status cnmf_thin_qr(cnmf_context* c, const float* y, uint64_t rows, uint64_
     float* qp = c->ws<float>("tq_q", rows * lp);
     void* qws = c->ws<char>("tq_ws", qr_ws_bytes((int64_t)rows, lp, c->nsm));
     launch_thin_qr(yp, (int64_t)rows, (int)l, lp, qp, qws, c->nsm, c->stream);
+    launch_householder_signs(qp, (int64_t)rows, (int)l, lp, c->ws<float>("hh_sgn_tq", 128),
+                             c->nsm, c->stream);
     launch_unpad_cols(qp, (int64_t)rows, lp, q_out, (int)l, c->stream);
     CK(cudaGetLastError());
     c->sync();

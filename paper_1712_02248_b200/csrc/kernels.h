@@ -82,6 +82,12 @@ void launch_thin_qr_dist(const float* y, int64_t rows, int l, int lp, float* q, 
                          int** flag_out);
 void launch_thin_qr(const float* y, int64_t rows, int l, int lp, float* q, void* ws, int nsm,
                     cudaStream_t st);
+// Flip the columns of an orthonormal q (rows x lp, l used) to the reference's
+// Householder signs (qr.cpp:35); sgn: l floats of device scratch.  Only the
+// step-level entry points that return bases need it: FastHALS-RP uses L, R
+// only through sign-invariant products.
+void launch_householder_signs(float* q, int64_t rows, int l, int lp, float* sgn, int nsm,
+                              cudaStream_t st);
 
 // ---- metrics.cu ------------------------------------------------------------
 // check_data: flags[0] |= negative/non-finite; *norm_sq = ||X||_F^2 (fp64).

@@ -278,6 +278,49 @@ __global__ void __launch_bounds__(1024) householder_kernel(const float* __restri
   }
 }
 
+// Column signs s that turn an orthonormal factor M with positive R diagonal
+// (CholeskyQR2's) into the reference's Householder factor M diag(s)
+// (qr.cpp:35: alpha_j = -sign(w_jj) |x_j|, R_jj = alpha_j).  Householder's
+// Q depends only on the nested column spans of its input (right-multiplying
+// by any nonsingular upper-triangular T rescales each step's column by T_jj
+// and leaves every reflector I - 2 v v^T unchanged), so Q_house(Y) =
+// Q_house(M) = M diag(s).  For orthonormal M the reduced columns stay unit
+// and mutually orthogonal, so each step touches only the top l x l block:
+// w = T_jj, alpha = -sign(w), |v|^2 = 2 (1 + |w|), and for c > j
+// T_rc += 2 alpha T_jc (T_rj - alpha delta_rj) / |v|^2.  One CTA, fp64.
+__global__ void __launch_bounds__(256) householder_signs_kernel(const float* __restrict__ q, int l,
+                                                                int lp, float* __restrict__ sgn) {
+  extern __shared__ double hs_t[];
+  double* coef = hs_t + l * l;
+  const int tid = threadIdx.x, nt = blockDim.x;
+  for (int e = tid; e < l * l; e += nt) hs_t[e] = q[(e / l) * lp + e % l];
+  __syncthreads();
+  for (int j = 0; j < l; ++j) {
+    const double w = hs_t[j * l + j];
+    const double alpha = w >= 0.0 ? -1.0 : 1.0;
+    const double inv = 1.0 / (2.0 * (1.0 + fabs(w)));
+    for (int c = j + 1 + tid; c < l; c += nt) coef[c] = 2.0 * alpha * hs_t[j * l + c] * inv;
+    if (tid == 0) sgn[j] = (float)alpha;
+    __syncthreads();
+    const int m = l - j - 1;
+    for (int e = tid; e < (l - j) * m; e += nt) {
+      const int r = j + e / m, c = j + 1 + e % m;
+      hs_t[r * l + c] += coef[c] * (hs_t[r * l + j] - (r == j ? alpha : 0.0));
+    }
+    __syncthreads();
+  }
+}
+
+__global__ void scale_cols_kernel(float* __restrict__ q, int64_t rows, int l, int lp,
+                                  const float* __restrict__ sgn) {
+  const int64_t total = rows * lp;
+  for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < total;
+       e += (int64_t)gridDim.x * blockDim.x) {
+    const int c = (int)(e % lp);
+    if (c < l) q[e] *= sgn[c];
+  }
+}
+
 void gram(const float* y, int64_t rows, int l, int lp, const QrWs& w, int nsm,
           cudaStream_t st) {
   const int grid = gram_grid(rows, nsm);
@@ -345,6 +388,22 @@ void launch_thin_qr(const float* y, int64_t rows, int l, int lp, float* q, void*
   launch_xs_nn(w.q1, lp, rows, lp, w.rinv, lp, q, w.xs_ws, nsm, st);
   note_launches(1);
   householder_kernel<<<1, 1024, 0, st>>>(y, rows, l, lp, w.hw, w.hv, q, w.flag);
+}
+
+void launch_householder_signs(float* q, int64_t rows, int l, int lp, float* sgn, int nsm,
+                              cudaStream_t st) {
+  const size_t smem = sizeof(double) * (l * l + l);
+  static bool attr = false;
+  if (!attr) {
+    cudaFuncSetAttribute(householder_signs_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         (int)(sizeof(double) * (128 * 128 + 128)));
+    attr = true;
+  }
+  note_launches(2);
+  householder_signs_kernel<<<1, 256, smem, st>>>(q, l, lp, sgn);
+  const int64_t total = rows * lp;
+  const int grid = (int)std::min<int64_t>((total + 255) / 256, 4 * nsm);
+  scale_cols_kernel<<<grid, 256, 0, st>>>(q, rows, l, lp, sgn);
 }
 
 }  // namespace cnmf

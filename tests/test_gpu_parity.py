@@ -11,6 +11,8 @@ factors within a stated elementwise tolerance):
     at every recorded iteration; final A, B: rel. Frobenius <= 1e-3 and
     max |delta| <= 1e-3 max|ref|.
 """
+import os
+
 import numpy as np
 import pytest
 
@@ -159,6 +161,40 @@ def test_thin_qr_rank_deficient_falls_back(ctx, oracle):
     assert np.abs(qh.T @ qh - np.eye(7)).max() < 1e-5
     y32 = y.astype(np.float32).astype(np.float64)
     assert np.linalg.norm(y32 - qh @ (qh.T @ y32)) / np.linalg.norm(y32) < 1e-5
+
+
+@pytest.mark.parametrize("rows,l", [(20, 6), (1000, 30), (5000, 128)])
+def test_thin_qr_householder_signs_entrywise(ctx, oracle, rows, l):
+    """thin_qr's Q equals the reference's Householder Q entrywise, signs
+    included (qr.cpp:35): the device CholeskyQR2 factor gets its column signs
+    from launch_householder_signs."""
+    rng = np.random.default_rng(7 * rows + l)
+    y = rng.standard_normal((rows, l)) + 0.5   # well conditioned, mixed-sign diagonals
+    y[:, ::3] *= -1.0
+    q = torch.empty((rows, l), device="cuda")
+    ctx.thin_qr(dev(y), q)
+    qr, _ = oracle.thin_qr(y.astype(np.float32).astype(np.float64))
+    assert np.abs(host(q) - qr).max() < 1e-5
+
+
+def test_bases_match_reference_entrywise(ctx, oracle):
+    """build_projectors / powered_range_finder hand out the reference's bases
+    entrywise (tests/golden/small.npz is the reference's own output) where
+    the spectrum is resolved in fp32."""
+    g = np.load(os.path.join(os.path.dirname(__file__), "golden", "small.npz"))
+    x = oracle.synth_x(60, 45, 5, 0, 1, 0.01, 3)
+    left = torch.empty((60, 10), device="cuda")
+    right = torch.empty((10, 45), device="cuda")
+    ctx.build_projectors(dev(x), 10, 2, 4, left, right)
+    assert np.abs(host(left) - g["left"]).max() < 1e-4
+    assert np.abs(host(right) - g["right"]).max() < 1e-4
+    x64 = x.astype(np.float64)
+    for transpose in (False, True):
+        rows = 45 if transpose else 60
+        basis = torch.empty((rows, 7), device="cuda")
+        ctx.powered_range_finder(dev(x), 7, 1, 11, transpose, basis)
+        ref = oracle.range_finder(x64, 7, 1, 11, transpose)
+        assert np.abs(host(basis) - ref).max() < 1e-4, transpose
 
 
 # ------------------------------------------------------------ compression --
