@@ -249,7 +249,8 @@ struct HalsRun {
   unsigned long long epoch;  // next launch's exchange epoch base
 };
 
-HalsRun make_hals(cnmf_context* c, int64_t d, int64_t n, int l, int lp, int k) {
+HalsRun make_hals(cnmf_context* c, int64_t d, int64_t n, int l, int lp, int k,
+                  bool allow_resident = true) {
   HalsRun r;
   HalsState& s = r.st;
   s.d = d;
@@ -264,7 +265,11 @@ HalsRun make_hals(cnmf_context* c, int64_t d, int64_t n, int l, int lp, int k) {
   s.ahat = c->ws<double>("Ahat", (size_t)lp * k);
   s.bchk = c->ws<double>("Bchk", (size_t)lp * k);
   const char* mode = std::getenv("CNMF_HALS");
-  const int rgrid = (mode && std::string(mode) == "stream") ? 0 : hals_resident_grid(s, c->nsm);
+  s.dense = 0;
+  s.hd = s.pd = s.gd = s.wd = nullptr;
+  const int rgrid = (!allow_resident || (mode && std::string(mode) == "stream"))
+                        ? 0
+                        : hals_resident_grid(s, c->nsm);
   r.resident = rgrid > 0;
   r.grid = r.resident ? rgrid : hals_grid(s, c->nsm);
   s.p = c->ws<double>("P_cm", (size_t)k * n);
@@ -355,6 +360,200 @@ void run_hals(cnmf_context* c, HalsRun& hr, int normalize_a, double alpha, doubl
   }
 }
 
+// ------------------------------------------------ uncompressed solvers -----
+// Products for the uncompressed updates (dense.cu): the factor converted to a
+// row-major fp64 operand, its X contraction and its Gram.
+struct DenseBufs {
+  double *sb, *sa, *y, *z, *g, *w, *xs_ws, *gram_ws, *tmp;
+  int lp;
+};
+
+DenseBufs make_dense(cnmf_context* c, int64_t d, int64_t n, int k) {
+  DenseBufs b;
+  b.lp = pad16(k);
+  b.sb = c->ws<double>("dn_sB", (size_t)n * b.lp);
+  b.sa = c->ws<double>("dn_sA", (size_t)d * b.lp);
+  b.y = c->ws<double>("dn_Y", (size_t)d * b.lp);
+  b.z = c->ws<double>("dn_Z", (size_t)n * b.lp);
+  b.g = c->ws<double>("dn_G", (size_t)k * k);
+  b.w = c->ws<double>("dn_W", (size_t)k * k);
+  b.xs_ws = c->ws<double>("dn_xs_ws", xs64_ws_doubles(d, n, b.lp, c->nsm));
+  b.gram_ws = c->ws<double>("dn_gram_ws", gram_cm_ws_doubles(std::max(d, n), k, c->nsm));
+  b.tmp = c->ws<double>("dn_tmp", (size_t)k * std::max(d, n));
+  return b;
+}
+
+// p = X B (d x lp) and g = B^T B for an A half (solvers.cpp:154-155)
+void dense_prepare_a(cnmf_context* c, const XView& X, const double* b_cm, int k, DenseBufs& db) {
+  launch_cm_to_rm_pad64(b_cm, X.n, k, db.lp, db.sb, c->nsm, c->stream);
+  launch_xs64_nn(X.x, X.ldx, X.d, X.n, db.sb, db.lp, db.y, db.xs_ws, c->nsm, c->stream);
+  launch_gram_cm(b_cm, X.n, k, db.g, db.gram_ws, c->nsm, c->stream);
+}
+
+// p = X^T A (n x lp) and w = A^T A for a B half (solvers.cpp:175-176)
+void dense_prepare_b(cnmf_context* c, const XView& X, const double* a_cm, int k, DenseBufs& db) {
+  launch_cm_to_rm_pad64(a_cm, X.d, k, db.lp, db.sa, c->nsm, c->stream);
+  launch_xs64_tn(X.x, X.ldx, X.d, X.n, db.sa, db.lp, db.z, db.xs_ws, c->nsm, c->stream);
+  launch_gram_cm(a_cm, X.d, k, db.w, db.gram_ws, c->nsm, c->stream);
+}
+
+// FastHALS (fasthals_step, solvers.cpp:146-187) and HALS (hals_step,
+// 96-131 -- the same column updates with A unnormalised and dead components
+// re-checked after a redraw): iterations [ib, ie) queued as one half-sweep
+// launch of the streaming HALS kernel per half, each preceded by its products,
+// with no host synchronisation until the end of the range.  A halt (dead or
+// emptied component) turns the launches queued behind it into no-ops; the
+// host then replays the pointer state up to the halted launch, draws the
+// column from the run Rng and resumes there (products are recomputed before
+// every launch, which is refresh_cross_products, solvers.cpp:133-144).
+template <typename RngFn>
+void run_dense_hals(cnmf_context* c, HalsRun& hr, const XView& X, DenseBufs& db, int normalize_a,
+                    int64_t ib, int64_t ie, RngFn&& get_rng, double* update_seconds,
+                    uint64_t* redraws, bool recheck_dead) {
+  HalsState& st = hr.st;
+  const int k = st.k;
+  st.dense = 1;
+  st.hd = db.y;
+  st.pd = db.z;
+  st.gd = db.g;
+  st.wd = db.w;
+  int half = 0, col = 0, skip = -1;
+  int64_t begin = ib;
+  for (;;) {
+    CK(cudaMemsetAsync(st.halt, 0, sizeof(HaltInfo), c->stream));
+    CK(cudaEventRecord(c->ev[0], c->stream));
+    double* b = st.b;
+    double* bold = st.bold;
+    {
+      int h0 = half, c0 = col, s0 = skip;
+      for (int64_t it = begin; it < ie; ++it) {
+        for (int h = h0; h < 2; ++h) {
+          HalsState s2 = st;
+          s2.b = b;
+          s2.bold = bold;
+          if (h == 0)
+            dense_prepare_a(c, X, b, k, db);
+          else
+            dense_prepare_b(c, X, st.a, k, db);
+          CK(launch_hals(s2, normalize_a, 0.0, 0.0, (int)it, (int)it + 1, h, c0, s0, hr.epoch,
+                         hr.grid, c->stream));
+          if (h == 1) std::swap(b, bold);  // the B half leaves the new B in the second buffer
+          c0 = 0;
+          s0 = -1;
+        }
+        h0 = 0;
+      }
+    }
+    CK(cudaEventRecord(c->ev[1], c->stream));
+    CK(cudaMemcpyAsync(c->halt_host, st.halt, sizeof(HaltInfo), cudaMemcpyDeviceToHost,
+                       c->stream));
+    c->sync();
+    *update_seconds += c->elapsed(0, 1);
+    const HaltInfo h = *c->halt_host;
+    if (h.last_epoch) hr.epoch = h.last_epoch;
+    if (!h.halted) {
+      st.b = b;
+      st.bold = bold;
+      break;
+    }
+    // pointer state at the halted launch: one swap per B half queued before it
+    {
+      b = st.b;
+      bold = st.bold;
+      bool found = false;
+      int h0 = half;
+      for (int64_t it = begin; it < ie && !found; ++it) {
+        for (int hh = h0; hh < 2; ++hh) {
+          if (it == h.iter - 1 && hh == h.half) {
+            found = true;
+            break;
+          }
+          if (hh == 1) std::swap(b, bold);
+        }
+        h0 = 0;
+      }
+      if (!found) throw Fail(CNMF_ERR_CUDA, "halt record outside the queued range");
+      st.b = b;
+      st.bold = bold;
+    }
+    if (h.pad) std::swap(st.b, st.bold);
+    std::mt19937_64& rng = get_rng();
+    const int j = h.column;
+    switch (h.kind) {
+      case kEvDeadB:  // solvers.cpp:159-162
+        redraw_column(c, rng, st.b + (int64_t)j * st.n, st.n);
+        half = 0; col = j; skip = recheck_dead ? -1 : j;
+        break;
+      case kEvZeroA:  // solvers.cpp:168-169
+        redraw_column(c, rng, st.a + (int64_t)j * st.d, st.d);
+        if (normalize_a) launch_normalize_column(st.a, st.d, j, c->stream);
+        half = 0; col = j + 1; skip = -1;
+        break;
+      case kEvDeadA:  // solvers.cpp:178-181
+        redraw_column(c, rng, st.a + (int64_t)j * st.d, st.d);
+        half = 1; col = j; skip = recheck_dead ? -1 : j;
+        break;
+      case kEvZeroB:  // solvers.cpp:185
+        redraw_column(c, rng, st.b + (int64_t)j * st.n, st.n);
+        half = 1; col = j + 1; skip = -1;
+        break;
+      default:
+        throw Fail(CNMF_ERR_CUDA, "corrupt halt record from the HALS kernel");
+    }
+    CK(cudaGetLastError());
+    begin = h.iter - 1;
+    ++*redraws;
+  }
+}
+
+// mu_step (solvers.cpp:55-64, 327-330): A .*= X B ./ (A B^T B + eps), then B
+// against the new A.  Out of place through a scratch factor.
+void run_mu(cnmf_context* c, HalsState& st, const XView& X, DenseBufs& db, int64_t iters,
+            double* update_seconds) {
+  const int k = st.k;
+  CK(cudaEventRecord(c->ev[0], c->stream));
+  for (int64_t it = 0; it < iters; ++it) {
+    dense_prepare_a(c, X, st.b, k, db);
+    launch_mu_update(st.a, X.d, k, db.y, db.lp, db.g, 0, db.tmp, c->nsm, c->stream);
+    CK(cudaMemcpyAsync(st.a, db.tmp, sizeof(double) * k * X.d, cudaMemcpyDeviceToDevice,
+                       c->stream));
+    dense_prepare_b(c, X, st.a, k, db);
+    launch_mu_update(st.b, X.n, k, db.z, db.lp, db.w, 0, db.tmp, c->nsm, c->stream);
+    CK(cudaMemcpyAsync(st.b, db.tmp, sizeof(double) * k * X.n, cudaMemcpyDeviceToDevice,
+                       c->stream));
+  }
+  CK(cudaEventRecord(c->ev[1], c->stream));
+  CK(cudaGetLastError());
+  c->sync();
+  *update_seconds += c->elapsed(0, 1);
+}
+
+// mu_rp_step (solvers.cpp:337-346): semi-NMF halves against the compressed
+// cross products X-check B-check and X-hat^T A-hat, then A-hat / B-check.
+void run_mu_rp(cnmf_context* c, HalsState& st, DenseBufs& db, int64_t iters,
+               double* update_seconds) {
+  const int k = st.k;
+  CK(cudaEventRecord(c->ev[0], c->stream));
+  for (int64_t it = 0; it < iters; ++it) {
+    launch_rows_small64(st.xc, st.d, st.l, st.lp, st.bchk, k, db.y, k, c->nsm, c->stream);
+    launch_gram_cm(st.bchk, st.lp, k, db.g, db.gram_ws, c->nsm, c->stream, true);
+    launch_mu_update(st.a, st.d, k, db.y, k, db.g, 1, db.tmp, c->nsm, c->stream);
+    CK(cudaMemcpyAsync(st.a, db.tmp, sizeof(double) * k * st.d, cudaMemcpyDeviceToDevice,
+                       c->stream));
+    launch_compress_factors(st, 0, -1, c->stream);
+    launch_rows_small64(st.xht, st.n, st.l, st.lp, st.ahat, k, db.z, k, c->nsm, c->stream);
+    launch_gram_cm(st.ahat, st.lp, k, db.w, db.gram_ws, c->nsm, c->stream, true);
+    launch_mu_update(st.b, st.n, k, db.z, k, db.w, 1, db.tmp, c->nsm, c->stream);
+    CK(cudaMemcpyAsync(st.b, db.tmp, sizeof(double) * k * st.n, cudaMemcpyDeviceToDevice,
+                       c->stream));
+    launch_compress_factors(st, 1, -1, c->stream);
+  }
+  CK(cudaEventRecord(c->ev[1], c->stream));
+  CK(cudaGetLastError());
+  c->sync();
+  *update_seconds += c->elapsed(0, 1);
+}
+
 double recon_error(cnmf_context* c, const XView& X, const double* a_cm, const double* b_cm,
                    int k) {
   double* out = c->ws<double>("err_out", 1);
@@ -385,17 +584,24 @@ void run_device_impl(cnmf_context* c, const float* x_in, int64_t d, int64_t n, i
                      const cnmf_solver_config& cfg, float* a_out, float* b_out,
                      cnmf_run_trace* tr) {
   validate(cfg, d, n);
-  // FastHALS-RP, and HALS-RP: its column updates (solvers.cpp:357-401) equal
-  // FastHALS-RP's with A unnormalised in exact arithmetic, so
-  // the same kernels run it with normalize_a off and dead components
-  // re-checked after a redraw.
-  if (cfg.algorithm != CNMF_FASTHALS_RP && cfg.algorithm != CNMF_HALS_RP)
-    throw Fail(CNMF_ERR_UNSUPPORTED, "this build implements the fasthals-rp and hals-rp paths");
-  const bool hals_rp = cfg.algorithm == CNMF_HALS_RP;
-  const int normalize_a = hals_rp ? 0 : cfg.normalize_a;  // normalize_a: fasthals only (solvers.hpp:24)
-  require_shapes(cfg.k, cfg.sketch_q);
-  const int k = (int)cfg.k, q = (int)cfg.sketch_q, lp = pad16(q);
-  const uint64_t w = cfg.sketch_power_iterations;
+  // All six solvers of run_impl (solvers.cpp:231-253):
+  //  * fasthals-rp on the fused HALS kernels (the north-star path);
+  //  * hals-rp: its column updates (solvers.cpp:357-401) equal FastHALS-RP's
+  //    with A unnormalised in exact arithmetic, so the same
+  //    kernels run it with normalize_a off and dead components re-checked;
+  //  * fasthals / hals: the same sweeps against fp64 X B, X^T A products
+  //    (dense.cu), one half-sweep launch per half;
+  //  * mu / mu-rp: multiplicative / semi-NMF updates (dense.cu).
+  const int algo = cfg.algorithm;
+  const bool compressed = algo == CNMF_MU_RP || algo == CNMF_HALS_RP || algo == CNMF_FASTHALS_RP;
+  const bool hals_rp = algo == CNMF_HALS_RP;
+  const bool recheck = algo == CNMF_HALS_RP || algo == CNMF_HALS;  // `while`, solvers.cpp:103,366
+  // normalize_a: the fasthals variants only (solvers.hpp:24)
+  const int normalize_a = (algo == CNMF_FASTHALS_RP || algo == CNMF_FASTHALS) ? cfg.normalize_a : 0;
+  require_shapes(cfg.k, compressed ? cfg.sketch_q : cfg.k);
+  const int k = (int)cfg.k, q = compressed ? (int)cfg.sketch_q : 0;
+  const int lp = compressed ? pad16(q) : pad16(k);
+  const uint64_t w = compressed ? cfg.sketch_power_iterations : 0;
 
   cnmf_run_trace t{};
   t.records = tr->records;
@@ -405,9 +611,16 @@ void run_device_impl(cnmf_context* c, const float* x_in, int64_t d, int64_t n, i
   t.alpha = cfg.alpha;
   t.beta = cfg.beta;
   t.seed = cfg.seed;
-  t.estimate_flops_per_iteration = hals_rp ? 4.0 * (double)d * n * k * q   // metrics.cpp:44
-                                           : 2.0 * (double)d * k * q;        // metrics.cpp:45
-  t.estimate_memory_floats = (2.0 * q + k) * ((double)d + (double)n);
+  {
+    cnmf_cost_estimate ce{};
+    char msg[128];
+    if (cnmf_estimate_cost(algo, (uint64_t)d, (uint64_t)n, (uint64_t)k, (uint64_t)q, &ce, msg,
+                           sizeof msg) != CNMF_OK)
+      throw Fail(CNMF_ERR_CONFIG, msg);
+    t.estimate_flops_per_iteration = ce.flops_per_iteration;  // metrics.cpp:20-50
+    t.estimate_memory_floats = ce.memory_floats;
+  }
+  (void)hals_rp;
   auto push = [&](uint64_t it, double err, double el) {
     if (t.records_count < t.records_capacity) t.records[t.records_count] = {it, err, el};
     ++t.records_count;
@@ -430,13 +643,18 @@ void run_device_impl(cnmf_context* c, const float* x_in, int64_t d, int64_t n, i
     if (hflag) throw Fail(CNMF_ERR_INPUT, "solver input must be entrywise non-negative and finite");
   }
 
-  HalsRun hr = make_hals(c, d, n, q, lp, k);
+  const bool dense_hals = algo == CNMF_FASTHALS || algo == CNMF_HALS;
+  HalsRun hr = compressed ? make_hals(c, d, n, q, lp, k, algo != CNMF_MU_RP)
+                          : make_hals(c, d, n, k, lp, k, false);
   HalsState& st = hr.st;
+  DenseBufs db{};
+  if (!compressed || algo == CNMF_MU_RP) db = make_dense(c, d, n, k);
 
   // Rng rng(seed); A then B uniform_positive (solvers.cpp:206-211).
   uint64_t* consumed_dev = gen_init(c, cfg.seed, d, n, k, st.a, st.b);
 
   // ---- compression (build_projectors + compress_left/right) ----
+  if (compressed) {
   float* omega_l = c->ws<float>("omega_L", (size_t)n * lp);
   float* omega_r = c->ws<float>("omega_R", (size_t)d * lp);
   float* lm = c->ws<float>("L", (size_t)d * lp);
@@ -465,6 +683,7 @@ void run_device_impl(cnmf_context* c, const float* x_in, int64_t d, int64_t n, i
   CK(cudaGetLastError());
   c->sync();
   t.compress_seconds = c->elapsed(2, 3);
+  }
 
   std::mt19937_64 rng;
   bool rng_ready = false;
@@ -500,8 +719,16 @@ void run_device_impl(cnmf_context* c, const float* x_in, int64_t d, int64_t n, i
   while (t.status != CNMF_ABORTED && it <= max_it) {  // solvers.cpp:231-284
     uint64_t e = ((it + every - 1) / every) * every;
     if (e > max_it) e = max_it;
-    run_hals(c, hr, normalize_a, cfg.alpha, cfg.beta, (int64_t)it - 1, (int64_t)e, get_rng,
-             &t.update_seconds, &t.redraws, hals_rp);
+    if (dense_hals)
+      run_dense_hals(c, hr, X, db, normalize_a, (int64_t)it - 1, (int64_t)e, get_rng,
+                     &t.update_seconds, &t.redraws, recheck);
+    else if (algo == CNMF_MU)
+      run_mu(c, st, X, db, (int64_t)(e - it + 1), &t.update_seconds);
+    else if (algo == CNMF_MU_RP)
+      run_mu_rp(c, st, db, (int64_t)(e - it + 1), &t.update_seconds);
+    else
+      run_hals(c, hr, normalize_a, cfg.alpha, cfg.beta, (int64_t)it - 1, (int64_t)e, get_rng,
+               &t.update_seconds, &t.redraws, recheck);
     t.iterations_run = e;
     const double err = timed_error();
     if (!std::isfinite(err)) {

@@ -336,6 +336,7 @@ __global__ void __launch_bounds__(kThreads, 1) hals_kernel(const HalsArgs p) {
     s_prof[id] += now_ - t_last;      \
     t_last = now_;                    \
   }
+  if (S.dense && __ldcg(&S.halt->halted)) return;  // queued behind a halt: no-op
   unsigned long long ep = p.epoch0;
   bool have_g = false, have_w = false;
   double* bcur = S.b;  // B as of the start of the B half
@@ -346,13 +347,17 @@ __global__ void __launch_bounds__(kThreads, 1) hals_kernel(const HalsArgs p) {
   for (int it = p.it_begin; it < p.it_end; ++it) {
     if (half == 0) {
       // ================= A half (solvers.cpp:419-439) =====================
-      if (!have_g) gram_to_scratch(S.bchk, l, k, smem, gsc);
-      // h = X-check B-check for this CTA's rows (solvers.cpp:421)
-      for (int e = tid; e < lp * k; e += kThreads) Ms[e] = __ldcg(S.bchk + e);
-      HALS_PROF(0);
-      rows_times_small(S.xc + a_lo * lp, na, lp, l, k, Ms, stage64,
-                       [&](int r, int c, double v) { S.h[(int64_t)c * d + a_lo + r] = v; });
-      for (int e = tid; e < k * k; e += kThreads) gw[e] = gsc[e];
+      if (S.dense) {  // p = X B, g = B^T B prepared by the host (solvers.cpp:154-155)
+        for (int e = tid; e < k * k; e += kThreads) gw[e] = __ldcg(S.gd + e);
+      } else {
+        if (!have_g) gram_to_scratch(S.bchk, l, k, smem, gsc);
+        // h = X-check B-check for this CTA's rows (solvers.cpp:421)
+        for (int e = tid; e < lp * k; e += kThreads) Ms[e] = __ldcg(S.bchk + e);
+        HALS_PROF(0);
+        rows_times_small(S.xc + a_lo * lp, na, lp, l, k, Ms, stage64,
+                         [&](int r, int c, double v) { S.h[(int64_t)c * d + a_lo + r] = v; });
+        for (int e = tid; e < k * k; e += kThreads) gw[e] = gsc[e];
+      }
       __syncthreads();
       for (int e = tid; e < k; e += kThreads) {
         s_diag[e] = gw[e * k + e];
@@ -407,7 +412,9 @@ __global__ void __launch_bounds__(kThreads, 1) hals_kernel(const HalsArgs p) {
         for (int i = 0; i < kMaxRPT; ++i) {
           const int r = tid + kThreads * i;
           const bool ok = i < rpt && r < na;
-          hv[i] = ok ? __ldcg(S.h + (int64_t)jb * d + a_lo + r) : 0.0;
+          hv[i] = ok ? (S.dense ? __ldcg(S.hd + (a_lo + r) * lp + jb)
+                                : __ldcg(S.h + (int64_t)jb * d + a_lo + r))
+                     : 0.0;
           av[i] = ok ? __ldcg(S.a + (int64_t)jb * d + a_lo + r) : 0.0;
         }
         HALS_PROF(2);
@@ -437,7 +444,9 @@ __global__ void __launch_bounds__(kThreads, 1) hals_kernel(const HalsArgs p) {
           for (int i = 0; i < kMaxRPT; ++i) {
             const int r = tid + kThreads * i;
             const bool ok = i < rpt && r < na && t + 1 < nbj;
-            hn[i] = ok ? __ldcg(S.h + (int64_t)(j + 1) * d + a_lo + r) : 0.0;
+            hn[i] = ok ? (S.dense ? __ldcg(S.hd + (a_lo + r) * lp + j + 1)
+                                  : __ldcg(S.h + (int64_t)(j + 1) * d + a_lo + r))
+                       : 0.0;
             an[i] = ok ? __ldcg(S.a + (int64_t)(j + 1) * d + a_lo + r) : 0.0;
           }
           HALS_PROF(2);
@@ -473,6 +482,10 @@ __global__ void __launch_bounds__(kThreads, 1) hals_kernel(const HalsArgs p) {
           *S.halt = HaltInfo{1, it + 1, 0, jd, kEvDeadB, bcur == S.bold, ep};
         return;
       }
+      if (S.dense) {  // one half per launch
+        if (cta == 0 && tid == 0) *S.halt = HaltInfo{0, it + 1, 0, 0, 0, bcur == S.bold, ep};
+        return;
+      }
       // A-hat = L^T A (solvers.cpp:438): partials, exchange, slice reduce, exchange
       small_partial(S.lm + a_lo * lp, na, l, lp, k, S.a + a_lo, d, stP, fsP, smem,
                     S.part + (int64_t)cta * nel, prof ? s_prof + 17 : nullptr);
@@ -490,12 +503,16 @@ __global__ void __launch_bounds__(kThreads, 1) hals_kernel(const HalsArgs p) {
       col0 = 0;
     }
     // ================== B half (solvers.cpp:440-455) =======================
-    if (!have_w) gram_to_scratch(S.ahat, l, k, smem, wsc);
-    // p = X-hat^T A-hat for this CTA's rows (solvers.cpp:442)
-    for (int e = tid; e < lp * k; e += kThreads) Ms[e] = __ldcg(S.ahat + e);
-    rows_times_small(S.xht + b_lo * lp, nbr, lp, l, k, Ms, stage64,
-                     [&](int r, int c, double v) { S.p[(int64_t)c * n + b_lo + r] = v; });
-    for (int e = tid; e < k * k; e += kThreads) gw[e] = wsc[e];
+    if (S.dense) {  // p = X^T A, w = A^T A prepared by the host (solvers.cpp:175-176)
+      for (int e = tid; e < k * k; e += kThreads) gw[e] = __ldcg(S.wd + e);
+    } else {
+      if (!have_w) gram_to_scratch(S.ahat, l, k, smem, wsc);
+      // p = X-hat^T A-hat for this CTA's rows (solvers.cpp:442)
+      for (int e = tid; e < lp * k; e += kThreads) Ms[e] = __ldcg(S.ahat + e);
+      rows_times_small(S.xht + b_lo * lp, nbr, lp, l, k, Ms, stage64,
+                       [&](int r, int c, double v) { S.p[(int64_t)c * n + b_lo + r] = v; });
+      for (int e = tid; e < k * k; e += kThreads) gw[e] = wsc[e];
+    }
     if (tid < 4) zmask[tid] = 0u;
     __syncthreads();
     for (int e = tid; e < k; e += kThreads) s_diag[e] = gw[e * k + e];
@@ -545,7 +562,7 @@ __global__ void __launch_bounds__(kThreads, 1) hals_kernel(const HalsArgs p) {
             if (u < t) s = fma(dl[u], gw[(jb + u) * k + j], s);
           const double wjj = s_diag[j];
           const double bij = __ldcg(bcur + (int64_t)j * n + gr);
-          const double pij = __ldcg(S.p + (int64_t)j * n + gr);
+          const double pij = S.dense ? __ldcg(S.pd + gr * lp + j) : __ldcg(S.p + (int64_t)j * n + gr);
           const double v = constrained ? (bij * wjj + pij - s - p.alpha) / (wjj + p.beta)  // 502-508
                                        : bij + (pij - s) / wjj;                            // 480-490
           const double vf = v > 0.0 ? v : 0.0;
@@ -559,8 +576,9 @@ __global__ void __launch_bounds__(kThreads, 1) hals_kernel(const HalsArgs p) {
     HALS_PROF(10);
     if (tid < 4) S.zpart[cta * 4 + tid] = zmask[tid];
     // B-check partial = R_rows B_rows, published together with the zero flags
-    small_partial(S.rt + b_lo * lp, nbr, l, lp, k, bnxt + b_lo, n, stP, fsP, smem,
-                  S.part + (int64_t)cta * nel);
+    if (!S.dense)
+      small_partial(S.rt + b_lo * lp, nbr, l, lp, k, bnxt + b_lo, n, stP, fsP, smem,
+                    S.part + (int64_t)cta * nel);
     HALS_PROF(11);
     exchange(S, G, cta, ep);
     HALS_PROF(12);
@@ -607,13 +625,15 @@ __global__ void __launch_bounds__(kThreads, 1) hals_kernel(const HalsArgs p) {
       return;
     }
     HALS_PROF(13);
-    slice_reduce(S.part, G, nel, S.bchk);
-    HALS_PROF(14);
-    exchange(S, G, cta, ep);
-    HALS_PROF(15);
-    gram_to_scratch(S.bchk, l, k, smem, gsc);  // g for the next A half (solvers.cpp:422)
-    HALS_PROF(16);
-    have_g = true;
+    if (!S.dense) {
+      slice_reduce(S.part, G, nel, S.bchk);
+      HALS_PROF(14);
+      exchange(S, G, cta, ep);
+      HALS_PROF(15);
+      gram_to_scratch(S.bchk, l, k, smem, gsc);  // g for the next A half (solvers.cpp:422)
+      HALS_PROF(16);
+      have_g = true;
+    }
     double* tb = bcur;
     bcur = bnxt;
     bnxt = tb;

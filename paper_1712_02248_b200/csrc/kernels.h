@@ -146,6 +146,17 @@ struct HalsState {
   unsigned* bar;     // monotonic grid-barrier arrival counter (reset per run)
   HaltInfo* halt;
   long long* prof;   // optional per-phase clock64 sums (CTA 0), or null
+  // Uncompressed FastHALS / HALS (dense = 1, streaming kernel only): each
+  // launch runs ONE half-sweep of one iteration against host-prepared
+  // products -- hd = X B (d x lp fp64 row-major) and gd = B^T B (k x k) for
+  // the A half, pd = X^T A (n x lp) and wd = A^T A for the B half -- with no
+  // compressed factors; a launch finding the halt record set returns at once
+  // (launches queued behind a halt are no-ops).
+  int dense;
+  const double* hd;
+  const double* pd;
+  const double* gd;
+  const double* wd;
   int sharded;       // 1: X column-sharded across ranks: after each B half the kernel halts
                      // (kEvShard) with this rank's B-check partial in bchk, its non-zero
                      // column mask in zpart[4 grid ..], the new B in b (resident kernel:
@@ -172,6 +183,29 @@ void launch_compress_factors(const HalsState& st, int which /*0 A-hat, 1 B-check
                              cudaStream_t s);
 // a_j <- a_j / ||a_j|| (no-op on a zero column), fixed-order fp64 norm.
 void launch_normalize_column(double* a_cm, int64_t d, int j, cudaStream_t s);
+
+// ---- dense.cu: the uncompressed solvers (fp64 CUDA-core contractions) ----
+// out (rows x lp fp64, row-major) = X S (NN, rows = m) or X^T T (TN, rows = n);
+// s: K x lp fp64 row-major (lp a multiple of 16, <= 128); ws: xs64_ws_doubles.
+size_t xs64_ws_doubles(int64_t m, int64_t n, int lp, int nsm);
+void launch_xs64_nn(const float* x, int64_t ldx, int64_t m, int64_t n, const double* s, int lp,
+                    double* out, double* ws, int nsm, cudaStream_t st);
+void launch_xs64_tn(const float* x, int64_t ldx, int64_t m, int64_t n, const double* t, int lp,
+                    double* out, double* ws, int nsm, cudaStream_t st);
+// g (k x k) = F^T F of a column-major k x rows fp64 factor (row_major: a
+// rows x k row-major one), fixed-order fp64.
+size_t gram_cm_ws_doubles(int64_t rows, int k, int nsm);
+void launch_gram_cm(const double* f_cm, int64_t rows, int k, double* g, double* ws, int nsm,
+                    cudaStream_t st, bool row_major = false);
+void launch_cm_to_rm_pad64(const double* f_cm, int64_t rows, int k, int lp, double* out,
+                           int nsm, cudaStream_t st);
+// mu_update_half (semi = 0) / semi_nmf_half (semi = 1) of a column-major
+// factor: t_out = t_in .* f(num, t_in g) (solvers.cpp:55-93).
+void launch_mu_update(const double* t_in, int64_t rows, int k, const double* num, int ldn,
+                      const double* g, int semi, double* t_out, int nsm, cudaStream_t st);
+// out (rows x k, ld ldo, fp64) = in (rows x lp fp32, first l columns) m (l x k fp64)
+void launch_rows_small64(const float* in, int64_t rows, int l, int lp, const double* m, int k,
+                         double* out, int ldo, int nsm, cudaStream_t st);
 
 // ---- synth.cu: synthetic data (bench harness, BASELINE.json configs) ------
 void launch_synth_x(int64_t d, int64_t n, int rank, int factor_kind, int noise_kind, double sigma,

@@ -472,8 +472,9 @@ def test_run_rejects_invalid_data_and_config(ctx):
         ctx.run(bad, cfg)
     with pytest.raises(cb.ConfigError):
         ctx.run(x, cb.SolverConfig(algorithm=cb.FASTHALS_RP, k=2, sketch=cb.SketchConfig(2, 1)))
-    with pytest.raises(cb.UnsupportedError):
-        ctx.run(x, cb.SolverConfig(algorithm=cb.MU, k=2))
+    big = np.random.default_rng(1).random((140, 140)).astype(np.float32)
+    with pytest.raises(cb.UnsupportedError):   # valid for the reference, k > 128 not built here
+        ctx.run(big, cb.SolverConfig(algorithm=cb.MU, k=129))
 
 
 def test_run_zero_iterations_returns_init(ctx, oracle):
@@ -552,3 +553,67 @@ def test_run_tiny_shapes(ctx, oracle, d, n, k, q, w):
     got = rel_err([r.error for r in res.trace.records][:m], xn)
     want = rel_err(rt.errors[:m], xn)
     assert np.max(np.abs(got - want) / np.maximum(want, 1e-12)) < 1e-3
+
+
+# ------------------------------------------- the other solvers of run_impl --
+@pytest.mark.parametrize("algo,q,normalize", [("fasthals", 0, True), ("fasthals", 0, False),
+                                              ("hals", 0, True), ("mu", 0, True),
+                                              ("mu-rp", 20, True)])
+def test_run_other_algorithms_match_reference(ctx, reference, algo, q, normalize):
+    """fasthals / hals (dense.cu products + the HALS sweep kernel in dense
+    mode), mu and mu-rp (dense.cu multiplicative / semi-NMF updates) against
+    the compiled reference's own run (solvers.cpp:231-253)."""
+    import paper_1712_02248_b200 as cb
+    from oracle import Oracle
+    x = Oracle().synth_x(600, 500, 10, 0, 1, 0.01, 1)
+    a_id = cb.ALGORITHM_NAMES[algo]
+    cfg = cb.SolverConfig(algorithm=a_id, k=10, sketch=cb.SketchConfig(q, 2, 1),
+                          max_iterations=40, error_interval=1, rel_tolerance=1e-300, seed=1,
+                          normalize_a=normalize)
+    res = ctx.run(x, cfg)
+    ra, rb, rt = reference.run(x.astype(np.float64), 10, q=q, w=2, sketch_seed=1,
+                               max_iterations=40, error_interval=1, rel_tolerance=1e-300,
+                               seed=1, normalize_a=normalize, algorithm=a_id)
+    xn = float(np.sum(x.astype(np.float64) ** 2))
+    assert [r.iteration for r in res.trace.records] == list(rt.iterations)
+    got = rel_err([r.error for r in res.trace.records], xn)
+    want = rel_err(rt.errors, xn)
+    assert np.max(np.abs(got - want) / want) < TRAJ_RTOL
+    assert rel_fro(res.a, ra) < FACTOR_RTOL and rel_fro(res.b, rb) < FACTOR_RTOL
+    assert res.trace.status == rt.status
+    assert res.trace.power_iterations == (2 if q else 0)
+
+
+def test_run_dense_fasthals_against_golden(ctx, oracle):
+    """The reference's own dense fasthals run on the small golden case
+    (tests/golden/small.npz, k = 4, 30 iterations, error every 5)."""
+    import paper_1712_02248_b200 as cb
+    g = np.load(os.path.join(os.path.dirname(__file__), "golden", "small.npz"))
+    x = oracle.synth_x(60, 45, 5, 0, 1, 0.01, 3)
+    res = ctx.run(x, cb.SolverConfig(algorithm=cb.FASTHALS, k=4, max_iterations=30))
+    assert [r.iteration for r in res.trace.records] == g["dense_iters"].tolist()
+    got = np.array([r.error for r in res.trace.records])
+    assert np.max(np.abs(got - g["dense_errors"]) / g["dense_errors"]) < TRAJ_RTOL
+    assert rel_fro(res.a, g["dense_a"]) < FACTOR_RTOL
+    assert rel_fro(res.b, g["dense_b"]) < FACTOR_RTOL
+
+
+@pytest.mark.parametrize("algo", ["fasthals", "hals"])
+def test_run_dense_redraws_match_reference(ctx, reference, algo):
+    """k far above the data's rank empties components: the dense sweeps halt,
+    the host draws the column from the run Rng and resumes, as the reference
+    does (solvers.cpp:103-131, 158-186)."""
+    import paper_1712_02248_b200 as cb
+    from oracle import Oracle
+    x = Oracle().synth_x(40, 30, 2, 0, 0, 0.0, 5)
+    a_id = cb.ALGORITHM_NAMES[algo]
+    cfg = cb.SolverConfig(algorithm=a_id, k=12, max_iterations=25, error_interval=1,
+                          rel_tolerance=1e-300, seed=3)
+    res = ctx.run(x, cfg)
+    assert res.trace.redraws > 0
+    ra, rb, rt = reference.run(x.astype(np.float64), 12, max_iterations=25, error_interval=1,
+                               rel_tolerance=1e-300, seed=3, algorithm=a_id)
+    m = min(len(res.trace.records), len(rt.iterations))
+    got = np.array([r.error for r in res.trace.records][:m])
+    want = np.array(rt.errors[:m])
+    assert np.max(np.abs(got - want) / np.maximum(want, 1e-12 * want[0])) < 1e-3
