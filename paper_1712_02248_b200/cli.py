@@ -11,6 +11,8 @@ Mirrors the reference tool's subcommands that sit on the compressed path
   project     cmd_project    cli.cpp:516-553  xhat.csv, xcheck.csv,
               distortion.json
   estimate    cmd_estimate   cli.cpp:555-570  cost model as JSON on stdout
+  compare     cmd_compare    cli.cpp:328-409  runs.csv, runs_summary.csv, table.csv
+  sweep       cmd_sweep      cli.cpp:411-514  sweep_runs.csv, sweep.csv
 
 with the same option names and defaults (cli.cpp:43-81, 644-755), the same
 `--config` key=value files (cli.cpp:573-634: '#'/';' comment lines, the last
@@ -22,10 +24,12 @@ nlohmann-style JSON with sorted keys and NaN -> null), atomic writes
 
 The factorization itself is the C-ABI library on the GPU (fp32 storage, see
 DESIGN.md); inputs are dense CSV (data_io.cpp:75-106) or the reference's
-synthetic generator (bitwise, cnmf_generate_synthetic).  The reference's
-`compare` and `sweep` subcommands run the uncompressed algorithms as well,
-and the sparse / image / corpus formats feed the sparse path; both are
-outside this build (scope) and are rejected with exit code 2.
+synthetic generator (bitwise, cnmf_generate_synthetic).  The sparse / image
+/ corpus formats feed the reference's sparse path, which is outside this
+build (scope): they are rejected with exit code 2.  Runs of a
+compare / sweep plan execute one after another on the device (`--jobs` is
+accepted; the reference's output bytes do not depend on it either,
+cli.cpp:229-247).
 """
 from __future__ import annotations
 
@@ -302,19 +306,27 @@ _SOLVER = {"k": ("uint", 2), "q": ("uint", 0), "w": ("uint", 4), "iters": ("uint
            "tol": ("float", 1e-9), "error-interval": ("uint", 5),
            "no-normalize": ("flag", False)}
 _PENALTIES = {"alpha": ("float", 0.0), "beta": ("float", 0.0)}
+_SEEDS = {"seeds": ("uints", [1, 2, 3, 4, 5]), "jobs": ("uint", 1)}
 SUBCOMMANDS = {
     "factorize": {**_DATASET, **_SOLVER, **_PENALTIES, "out": ("str", ""),
                   "algo": ("str", "fasthals"), "seed": ("uint", 1)},
+    "compare": {**_DATASET, **_SOLVER, "out": ("str", ""), **_SEEDS},
+    "sweep": {**_DATASET, **_SOLVER, **_PENALTIES, "out": ("str", ""),
+              "algo": ("str", "fasthals"), **_SEEDS, "k-grid": ("uints", []),
+              "q-grid": ("uints", []), "w-grid": ("uints", []), "alpha-grid": ("floats", []),
+              "beta-grid": ("floats", [])},
     "project": {**_DATASET, "out": ("str", ""), "q": ("uint", 0), "w": ("uint", 4),
                 "seed": ("uint", 1), "pairs": ("uint", 200)},
     "estimate": {"algo": ("str", "fasthals"), "rows": ("uint", 0), "cols": ("uint", 0),
                  "k": ("uint", 2), "q": ("uint", 0), "config": ("str", "")},
 }
-_OUT_OF_SCOPE = ("compare", "sweep")
 
 
 def _convert(name: str, kind: str, value: str):
     try:
+        if kind in ("uints", "floats"):   # comma-delimited lists (CLI11 ->delimiter(','))
+            one = "uint" if kind == "uints" else "float"
+            return [_convert(name, one, v) for v in value.split(",")]
         if kind == "uint":
             v = int(value.strip(), 10)
             if v < 0:
@@ -355,7 +367,10 @@ def parse_args(sub: str, argv: Sequence[str]) -> Tuple[Dict[str, object], set]:
                 if i >= len(argv):
                     raise UsageError(f"--{name} requires a value")
                 raw = argv[i]
-            vals[name] = _convert(name, kind, raw)
+            v = _convert(name, kind, raw)
+            if kind in ("uints", "floats") and name in given:
+                v = vals[name] + v                 # repeated list options accumulate
+            vals[name] = v
         given.add(name)
         i += 1
     return vals, given
@@ -422,7 +437,8 @@ def _usage(sub: Optional[str] = None) -> str:
     lines = ["compressed non-negative matrix factorization toolkit (B200)",
              "usage: python -m paper_1712_02248_b200.cli SUBCOMMAND [OPTIONS]"]
     for s in subs:
-        opts = " ".join(f"[--{k}]" if v[0] == "flag" else f"[--{k} V]"
+        opts = " ".join(f"[--{k}]" if v[0] == "flag" else
+                        f"[--{k} V,V..]" if v[0] in ("uints", "floats") else f"[--{k} V]"
                         for k, v in SUBCOMMANDS[s].items())
         lines.append(f"  {s} {opts}")
     return "\n".join(lines)
@@ -459,7 +475,8 @@ def make_config(o: Dict[str, object], seed: int) -> SolverConfig:
     """make_config (cli.cpp:120-135): the run seed drives the init and the sketch."""
     return SolverConfig(algorithm=parse_algorithm(o["algo"]), k=o["k"],
                         sketch=SketchConfig(q=o["q"], power_iterations=o["w"], seed=seed),
-                        alpha=o["alpha"], beta=o["beta"], max_iterations=o["iters"],
+                        alpha=o.get("alpha", 0.0), beta=o.get("beta", 0.0),
+                        max_iterations=o["iters"],
                         rel_tolerance=o["tol"], error_interval=o["error-interval"], seed=seed,
                         normalize_a=not o["no-normalize"])
 
@@ -563,7 +580,151 @@ def cmd_estimate(o: Dict[str, object]) -> int:
     return 0
 
 
-_COMMANDS = {"factorize": cmd_factorize, "project": cmd_project, "estimate": cmd_estimate}
+def median(values: List[float]) -> float:
+    """median (metrics.cpp:157-162)."""
+    if not values:
+        raise InputError("median: empty input")
+    v = sorted(values)
+    mid = len(v) // 2
+    return v[mid] if len(v) % 2 == 1 else 0.5 * (v[mid - 1] + v[mid])
+
+
+class Outcome:
+    """execute (cli.cpp:249-272): never raises; failures are recorded."""
+
+    def __init__(self, x32: np.ndarray, cfg: SolverConfig):
+        self.trace, self.ok, self.input_failure = None, False, False
+        try:
+            res = _context().run(x32, cfg)
+            self.trace, self.ok = res.trace, True
+            self.status, self.message = STATUS_NAMES[res.trace.status], res.trace.message
+        except (ConfigError, InputError, IoError, UnsupportedError) as e:
+            self.input_failure, self.status, self.message = True, "error", str(e)
+        except Exception as e:  # noqa: BLE001 -- runtime failures are recorded, not raised
+            self.status, self.message = "error", str(e)
+
+    def final_error(self) -> float:
+        if not self.ok or not self.trace.records:
+            return float("nan")
+        return self.trace.records[-1].error
+
+
+def sanitize_cell(s: str) -> str:
+    """cli.cpp:275-279."""
+    return s.replace(",", ";").replace("\n", ";").replace("\r", ";")
+
+
+def plan_exit_code(results: List[Outcome]) -> int:
+    """cli.cpp:282-292: input problems dominate runtime failures."""
+    any_input = any(not r.ok and r.input_failure for r in results)
+    any_runtime = any((not r.ok and not r.input_failure) or
+                      (r.ok and r.trace.status == ABORTED) for r in results)
+    return 2 if any_input else 1 if any_runtime else 0
+
+
+def report_failures(results: List[Outcome], labels: List[str]) -> None:
+    for r, label in zip(results, labels):
+        if not r.ok or r.trace.status == ABORTED:
+            print(f"cnmf: {label}: {r.status}" + (f": {r.message}" if r.message else ""),
+                  file=sys.stderr)
+
+
+COMPARE_ORDER = ["mu", "hals", "fasthals", "mu-rp", "hals-rp", "fasthals-rp"]  # cli.cpp:334-336
+
+
+def cmd_compare(o: Dict[str, object]) -> int:
+    """cmd_compare (cli.cpp:328-409): every algorithm over every seed."""
+    if not o["out"]:
+        raise ConfigError("--out is required")
+    x = load_dataset(o)
+    d, n = x.shape
+    x32 = x.astype(np.float32)
+    plan = [(a, sd) for a in COMPARE_ORDER for sd in o["seeds"]]
+    results = []
+    for a, sd in plan:
+        o2 = dict(o, algo=a)
+        results.append(Outcome(x32, make_config(o2, sd)))
+    runs = TRACE_HEADER
+    summary = "algorithm,seed,final_error,gini_b,iterations_run,status\n"
+    labels = []
+    for (a, sd), r in zip(plan, results):
+        labels.append(f"{a} seed {sd}")
+        if r.ok:
+            runs += trace_csv_rows(a, sd, r.trace)
+        summary += (f"{a},{sd},{fmt(r.final_error())},"
+                    f"{fmt(r.trace.gini_b if r.ok else float('nan'))},"
+                    f"{r.trace.iterations_run if r.ok else 0},{sanitize_cell(r.status)}\n")
+    table = "algorithm,flops_per_iter,median_seconds_per_update,memory_floats\n"
+    for a in COMPARE_ORDER:
+        flops = memory = float("nan")
+        try:
+            e = estimate_cost(a, d, n, o["k"], o["q"] if a.endswith("-rp") else 0)
+            flops, memory = e.flops_per_iteration, e.memory_floats
+        except Exception:  # noqa: BLE001 -- invalid geometry for this variant
+            pass
+        secs = [r.trace.update_seconds / r.trace.iterations_run
+                for (pa, _), r in zip(plan, results)
+                if pa == a and r.ok and r.trace.iterations_run > 0]
+        table += f"{a},{fmt(flops)},{fmt(median(secs) if secs else float('nan'))},{fmt(memory)}\n"
+    out = o["out"]
+    os.makedirs(out, exist_ok=True)
+    write_text_atomic(os.path.join(out, "runs.csv"), runs)
+    write_text_atomic(os.path.join(out, "runs_summary.csv"), summary)
+    write_text_atomic(os.path.join(out, "table.csv"), table)
+    report_failures(results, labels)
+    return plan_exit_code(results)
+
+
+def cmd_sweep(o: Dict[str, object]) -> int:
+    """cmd_sweep (cli.cpp:411-514): the (k, q, w, alpha, beta) grid of one
+    algorithm over every seed, with per-cell medians."""
+    if not o["out"]:
+        raise ConfigError("--out is required")
+    x = load_dataset(o)
+    x32 = x.astype(np.float32)
+    grid = lambda key, one: o[key] if o[key] else [o[one]]  # noqa: E731
+    cells = [(k, q, w, al, be) for k in grid("k-grid", "k") for q in grid("q-grid", "q")
+             for w in grid("w-grid", "w") for al in grid("alpha-grid", "alpha")
+             for be in grid("beta-grid", "beta")]
+    plan = [(ci, sd) for ci in range(len(cells)) for sd in o["seeds"]]
+    name = CANONICAL[parse_algorithm(o["algo"])]
+    results = []
+    for ci, sd in plan:
+        k, q, w, al, be = cells[ci]
+        cfg = make_config(o, sd)
+        cfg.k, cfg.sketch.q, cfg.sketch.power_iterations = k, q, w
+        cfg.alpha, cfg.beta = float(al), float(be)
+        results.append(Outcome(x32, cfg))
+
+    def prefix(c):
+        k, q, w, al, be = c
+        return f"{name},{k},{q},{w},{fmt(float(al))},{fmt(float(be))}"
+
+    raw = "algorithm,k,q,w,alpha,beta,seed,final_error,gini_b,iterations_run,status\n"
+    labels = []
+    for (ci, sd), r in zip(plan, results):
+        labels.append(f"{name} k={cells[ci][0]} seed {sd}")
+        raw += (f"{prefix(cells[ci])},{sd},{fmt(r.final_error())},"
+                f"{fmt(r.trace.gini_b if r.ok else float('nan'))},"
+                f"{r.trace.iterations_run if r.ok else 0},{sanitize_cell(r.status)}\n")
+    sheet = "algorithm,k,q,w,alpha,beta,median_final_error,median_gini_b\n"
+    for ci, c in enumerate(cells):
+        errs = [r.final_error() for (pc, _), r in zip(plan, results)
+                if pc == ci and r.ok and math.isfinite(r.final_error())]
+        ginis = [r.trace.gini_b for (pc, _), r in zip(plan, results)
+                 if pc == ci and r.ok and math.isfinite(r.trace.gini_b)]
+        sheet += (f"{prefix(c)},{fmt(median(errs) if errs else float('nan'))},"
+                  f"{fmt(median(ginis) if ginis else float('nan'))}\n")
+    out = o["out"]
+    os.makedirs(out, exist_ok=True)
+    write_text_atomic(os.path.join(out, "sweep_runs.csv"), raw)
+    write_text_atomic(os.path.join(out, "sweep.csv"), sheet)
+    report_failures(results, labels)
+    return plan_exit_code(results)
+
+
+_COMMANDS = {"factorize": cmd_factorize, "project": cmd_project, "estimate": cmd_estimate,
+             "compare": cmd_compare, "sweep": cmd_sweep}
 
 
 def run(args: Sequence[str]) -> int:
@@ -573,10 +734,6 @@ def run(args: Sequence[str]) -> int:
         print(_usage())
         return 0 if args else 2
     sub, rest = args[0], args[1:]
-    if sub in _OUT_OF_SCOPE:
-        print(f"cnmf: {sub} runs the uncompressed algorithms too; not part of this build",
-              file=sys.stderr)
-        return 2
     if sub not in SUBCOMMANDS:
         print(f"cnmf: unknown subcommand '{sub}'\n{_usage()}", file=sys.stderr)
         return 2

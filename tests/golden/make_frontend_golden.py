@@ -74,7 +74,10 @@ def frontend(r):
                                 max_iterations=7, error_interval=5, rel_tolerance=1e-300),
                     "hrp": dict(algorithm=HALS_RP, k=2, q=5, w=2, seed=5, sketch_seed=5,
                                 max_iterations=30, error_interval=3, rel_tolerance=1e-300,
-                                alpha=0.01, beta=0.02)}.items():
+                                alpha=0.01, beta=0.02),
+                    # test_cli.cpp:85-130: the default algorithm, default tolerance
+                    "fhd": dict(algorithm=4, k=2, seed=3, sketch_seed=3, max_iterations=40,
+                                error_interval=5, rel_tolerance=1e-9, w=0)}.items():
         a, b, t = r.run(x, **kw)
         g[f"run_{tag}_a"], g[f"run_{tag}_b"] = a, b
         g[f"run_{tag}_iter"] = np.array(t.iterations, dtype=np.int64)

@@ -150,6 +150,17 @@ def test_dense_csv_failures(tmp_path):
 
 
 # ----------------------------------------------------------- options/config --
+def test_list_options_and_median():
+    vals, given = cli.parse_args("sweep", ["--seeds", "3,1", "--k-grid", "2,3", "--k-grid=4",
+                                           "--alpha-grid", "0,0.1"])
+    assert vals["seeds"] == [3, 1] and vals["k-grid"] == [2, 3, 4]
+    assert vals["alpha-grid"] == [0.0, 0.1] and vals["q-grid"] == []
+    assert cli.median([3.0, 1.0, 2.0]) == 2.0 and cli.median([4.0, 1.0]) == 2.5
+    with pytest.raises(cb.InputError):
+        cli.median([])
+    assert cli.sanitize_cell("a,b\nc") == "a;b;c"
+
+
 def test_read_config_file(tmp_path):
     p = tmp_path / "run.cfg"
     p.write_text("# comment\n; also a comment\n\n k = 3 \niters=7\nk=4\n")
@@ -218,7 +229,7 @@ def test_bad_invocations_exit_2_and_write_nothing(tmp_path, capsys):
     assert cli.run(["estimate", "--rows", "10"]) == 2
     assert cli.run(["factorize", "--k", "-1", "--out", out]) == 2
     assert cli.run(["project"] + SYNTH + ["--out", str(tmp_path / "p")]) == 2   # --q missing
-    assert cli.run(["compare"] + SYNTH + ["--out", str(tmp_path / "d")]) == 2
+    assert cli.run(["compare"] + SYNTH + ["--seeds", "1,x", "--out", str(tmp_path / "d")]) == 2
     assert cli.run(["factorize", "--format", "mm", "--input", "x.mtx", "--out", out]) == 2
     assert cli.run([]) == 2
     assert cli.run(["--help"]) == 0
