@@ -24,109 +24,94 @@ namespace {
 
 constexpr int kBK = 8;     // reduction depth per stage
 constexpr int kXT = 256;   // threads per X-stream CTA
+constexpr int kNS = 3;     // cp.async pipeline stages
+constexpr int kNNS = 12;   // NN X-tile row stride (floats): conflict-free 16-byte reads
 
 template <int LP>
 struct Xs64Shape {
   static constexpr int CG = LP / 16;        // 16-column groups
   static constexpr int RS = kXT / CG;       // row stride between a thread's 4 rows
   static constexpr int BM = 4 * RS;         // output rows per CTA
-  static constexpr int XF4 = (2 * BM + kXT - 1) / kXT;  // X float4 per thread per stage
-  static constexpr size_t smem = sizeof(double) * 2 * kBK * (BM + LP);
+  // per stage: X tile (fp32; NN [BM][kNNS], TN [kBK][BM]) + S tile (fp64 [kBK][LP])
+  static constexpr int XF = BM * kNNS;      // floats (>= kBK * BM for TN)
+  static constexpr size_t stage_bytes = sizeof(float) * XF + sizeof(double) * kBK * LP;
+  static constexpr size_t smem = kNS * stage_bytes;
 };
+
+__device__ __forceinline__ void cp_async16(void* dst, const void* src, int src_bytes) {
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;" ::"r"(
+                   static_cast<uint32_t>(__cvta_generic_to_shared(dst))),
+               "l"(src), "r"(src_bytes)
+               : "memory");
+}
+
+// fp32 -> fp64 on the integer pipe (exact for zero and normal numbers; the
+// FP64 conversion unit issues at 1/4 the DFMA rate and would cost ~25% here).
+// Subnormal inputs take the F2F path.
+__device__ __forceinline__ double f2d_int(float f) {
+  const uint32_t u = __float_as_uint(f), a = u & 0x7fffffffu;
+  if (a < 0x00800000u && a != 0u) return (double)f;
+  const uint32_t hi = (u & 0x80000000u) | (a ? (a >> 3) + 0x38000000u : 0u);
+  return __hiloint2double((int)hi, (int)(u << 29));
+}
 
 // out[s][r][c] (s = blockIdx.y split) = sum over the split's K range of
 // op(X)[r][k] S[k][c]; op(X) = X (NN: r < m, K = n) or X^T (TN: r < n, K = m).
 // Thread tile: rows rg + RS i (i < 4) x columns 16 cg .. 16 cg + 15 (threads
-// beyond RS * CG only load).  X staged as fp64 [kBK][BM], S as [kBK][LP];
-// both double-buffered through registers, one barrier per stage.
+// beyond RS * CG only copy).  X (fp32) and S (fp64) stream through a
+// 3-stage cp.async ring; X is widened to fp64 in registers.
 template <bool kTN, int LP>
 __global__ void __launch_bounds__(kXT, 1) xs64_kernel(const float* __restrict__ x, int64_t ldx,
                                                       int64_t m, int64_t n,
                                                       const double* __restrict__ s,
-                                                      double* __restrict__ out, int64_t kchunk) {
+                                                      double* __restrict__ out, int64_t kchunk,
+                                                      const int* __restrict__ halt) {
+  if (halt && *(volatile const int*)halt) return;  // queued behind a HALS halt
   using Sh = Xs64Shape<LP>;
-  constexpr int CG = Sh::CG, RS = Sh::RS, BM = Sh::BM, XF4 = Sh::XF4;
-  constexpr int SD2 = kBK * LP / 2;  // double2 of S per stage
-  constexpr int SPT = (SD2 + kXT - 1) / kXT;
-  extern __shared__ __align__(16) double xs64_smem[];
-  double* Xs = xs64_smem;                // [2][kBK][BM]
-  double* Ss = xs64_smem + 2 * kBK * BM;  // [2][kBK][LP]
+  constexpr int CG = Sh::CG, RS = Sh::RS, BM = Sh::BM;
+  extern __shared__ __align__(16) unsigned char xs64_smem[];
   const int tid = threadIdx.x, cg = tid % CG, rg = tid / CG;
   const bool computes = rg < RS;
   const int64_t out_rows = kTN ? n : m, K = kTN ? m : n;
   const int64_t row0 = (int64_t)blockIdx.x * BM;
   const int64_t kbeg = (int64_t)blockIdx.y * kchunk, kend = min(K, kbeg + kchunk);
   double* dst = out + (int64_t)blockIdx.y * out_rows * LP;
+  auto xbuf = [&](int b) { return reinterpret_cast<float*>(xs64_smem + b * Sh::stage_bytes); };
+  auto sbuf = [&](int b) {
+    return reinterpret_cast<double*>(xs64_smem + b * Sh::stage_bytes + sizeof(float) * Sh::XF);
+  };
 
-  float4 px[XF4];
-  double2 ps[SPT];
-  auto load = [&](int64_t k0) {
-#pragma unroll
-    for (int u = 0; u < XF4; ++u) {
-      const int e = tid + kXT * u;
-      float4 v = make_float4(0.f, 0.f, 0.f, 0.f);
-      if (e < 2 * BM) {
-        if (!kTN) {  // row e / 2, k offset 4 (e % 2)
-          const int64_t gr = row0 + (e >> 1), gk = k0 + 4 * (e & 1);
-          if (gr < m && gk < kend) {
-            const float* src = x + gr * ldx + gk;
-            if (gk + 3 < kend) {
-              v = __ldg(reinterpret_cast<const float4*>(src));
-            } else {
-              v.x = src[0];
-              if (gk + 1 < kend) v.y = src[1];
-              if (gk + 2 < kend) v.z = src[2];
-            }
-          }
-        } else {     // k offset e / (BM / 4), rows 4 (e % (BM / 4)) ..
-          const int64_t gk = k0 + e / (BM / 4), gr = row0 + 4 * (e % (BM / 4));
-          if (gk < kend && gr < n) {
-            const float* src = x + gk * ldx + gr;
-            if (gr + 3 < n) {
-              v = __ldg(reinterpret_cast<const float4*>(src));
-            } else {
-              v.x = src[0];
-              if (gr + 1 < n) v.y = src[1];
-              if (gr + 2 < n) v.z = src[2];
-            }
-          }
+  auto issue = [&](int64_t k0, int b) {
+    float* xs = xbuf(b);
+    for (int e = tid; e < 2 * BM; e += kXT) {  // 16-byte chunks of X
+      const float* src = x;
+      int bytes = 0;
+      float* d;
+      if (!kTN) {  // row e / 2, k quad e % 2
+        const int r = e >> 1, q = e & 1;
+        const int64_t gr = row0 + r, gk = k0 + 4 * q;
+        d = xs + r * kNNS + 4 * q;
+        if (gr < m && gk < kend) {
+          src = x + gr * ldx + gk;
+          bytes = (int)(4 * (kend - gk < 4 ? kend - gk : 4));
+        }
+      } else {     // k row e / (BM / 4), column quad e % (BM / 4)
+        const int kk = e / (BM / 4), c4 = e % (BM / 4);
+        const int64_t gk = k0 + kk, gr = row0 + 4 * c4;
+        d = xs + kk * BM + 4 * c4;
+        if (gk < kend && gr < n) {
+          src = x + gk * ldx + gr;
+          bytes = (int)(4 * (n - gr < 4 ? n - gr : 4));
         }
       }
-      px[u] = v;
+      cp_async16(d, src, bytes);
     }
-#pragma unroll
-    for (int u = 0; u < SPT; ++u) {
-      const int e = tid + kXT * u;
+    double* ss = sbuf(b);
+    for (int e = tid; e < kBK * LP / 2; e += kXT) {  // 16-byte chunks of S
       const int kk = e / (LP / 2), c2 = e % (LP / 2);
       const int64_t gk = k0 + kk;
-      ps[u] = (e < SD2 && gk < kend) ? __ldg(reinterpret_cast<const double2*>(s + gk * LP) + c2)
-                                     : make_double2(0.0, 0.0);
-    }
-  };
-  auto store = [&](int buf) {
-    double* xb = Xs + buf * kBK * BM;
-#pragma unroll
-    for (int u = 0; u < XF4; ++u) {
-      const int e = tid + kXT * u;
-      if (e < 2 * BM) {
-        if (!kTN) {
-          const int r = e >> 1, k4 = 4 * (e & 1);
-          xb[(k4 + 0) * BM + r] = px[u].x;
-          xb[(k4 + 1) * BM + r] = px[u].y;
-          xb[(k4 + 2) * BM + r] = px[u].z;
-          xb[(k4 + 3) * BM + r] = px[u].w;
-        } else {
-          const int kk = e / (BM / 4), c = 4 * (e % (BM / 4));
-          double2* d2 = reinterpret_cast<double2*>(xb + kk * BM + c);
-          d2[0] = make_double2(px[u].x, px[u].y);
-          d2[1] = make_double2(px[u].z, px[u].w);
-        }
-      }
-    }
-#pragma unroll
-    for (int u = 0; u < SPT; ++u) {
-      const int e = tid + kXT * u;
-      if (e < SD2) reinterpret_cast<double2*>(Ss + buf * kBK * LP)[e] = ps[u];
+      cp_async16(ss + kk * LP + 2 * c2, gk < kend ? s + gk * LP + 2 * c2 : s,
+                 gk < kend ? 16 : 0);
     }
   };
 
@@ -137,32 +122,54 @@ __global__ void __launch_bounds__(kXT, 1) xs64_kernel(const float* __restrict__ 
     for (int c = 0; c < 16; ++c) acc[i][c] = 0.0;
 
   const int64_t nst = (kend - kbeg + kBK - 1) / kBK;
-  if (nst > 0) load(kbeg);
+#pragma unroll
+  for (int p = 0; p < kNS - 1; ++p) {
+    if (p < nst) issue(kbeg + p * kBK, p);
+    asm volatile("cp.async.commit_group;" ::: "memory");
+  }
   for (int64_t st = 0; st < nst; ++st) {
-    const int buf = (int)(st & 1);
-    store(buf);
-    __syncthreads();  // also orders this store after every read of buf two stages ago
-    if (st + 1 < nst) load(kbeg + (st + 1) * kBK);
-    if (computes) {
-      const double* xb = Xs + buf * kBK * BM + rg;
-      const double* sb = Ss + buf * kBK * LP + 16 * cg;
+    asm volatile("cp.async.wait_group %0;" ::"n"(kNS - 2) : "memory");
+    __syncthreads();  // stage st visible to all; stage st - 1 fully consumed
+    if (st + kNS - 1 < nst) issue(kbeg + (st + kNS - 1) * kBK, (int)((st + kNS - 1) % kNS));
+    asm volatile("cp.async.commit_group;" ::: "memory");
+    if (!computes) continue;
+    const int b = (int)(st % kNS);
+    const float* xs = xbuf(b);
+    const double* sb = sbuf(b) + 16 * cg;
 #pragma unroll
-      for (int kk = 0; kk < kBK; ++kk) {
-        double xv[4];
+    for (int q = 0; q < kBK / 4; ++q) {
+      double xv[4][4];  // [row][kk in quad]
 #pragma unroll
-        for (int i = 0; i < 4; ++i) xv[i] = xb[kk * BM + RS * i];
+      for (int i = 0; i < 4; ++i) {
+        float4 f;
+        if (!kTN) {
+          f = *reinterpret_cast<const float4*>(xs + (rg + RS * i) * kNNS + 4 * q);
+        } else {
+          const float* col = xs + rg + RS * i;
+          f = make_float4(col[(4 * q + 0) * BM], col[(4 * q + 1) * BM], col[(4 * q + 2) * BM],
+                          col[(4 * q + 3) * BM]);
+        }
+        xv[i][0] = f2d_int(f.x);
+        xv[i][1] = f2d_int(f.y);
+        xv[i][2] = f2d_int(f.z);
+        xv[i][3] = f2d_int(f.w);
+      }
+#pragma unroll
+      for (int t = 0; t < 4; ++t) {
+        const double* srow = sb + (4 * q + t) * LP;
 #pragma unroll
         for (int c2 = 0; c2 < 8; ++c2) {
-          const double2 sv = reinterpret_cast<const double2*>(sb + kk * LP)[c2];
+          const double2 sv = reinterpret_cast<const double2*>(srow)[c2];
 #pragma unroll
           for (int i = 0; i < 4; ++i) {
-            acc[i][2 * c2] = fma(xv[i], sv.x, acc[i][2 * c2]);
-            acc[i][2 * c2 + 1] = fma(xv[i], sv.y, acc[i][2 * c2 + 1]);
+            acc[i][2 * c2] = fma(xv[i][t], sv.x, acc[i][2 * c2]);
+            acc[i][2 * c2 + 1] = fma(xv[i][t], sv.y, acc[i][2 * c2 + 1]);
           }
         }
       }
     }
   }
+  asm volatile("cp.async.wait_group 0;" ::: "memory");
   if (computes) {
 #pragma unroll
     for (int i = 0; i < 4; ++i) {
@@ -177,7 +184,8 @@ __global__ void __launch_bounds__(kXT, 1) xs64_kernel(const float* __restrict__ 
 }
 
 __global__ void reduce_splits64_kernel(const double* __restrict__ part, int splits, int64_t total,
-                                       double* __restrict__ out) {
+                                       double* __restrict__ out, const int* __restrict__ halt) {
+  if (halt && *(volatile const int*)halt) return;
   for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < total;
        e += (int64_t)gridDim.x * blockDim.x) {
     double s = 0.0;
@@ -195,7 +203,9 @@ constexpr int kGR = 32;  // rows per stage
 __global__ void __launch_bounds__(256) gram_cm_kernel(const double* __restrict__ f, int64_t rows,
                                                       int k, int64_t cs, int64_t rs,
                                                       int64_t rows_per_cta,
-                                                      double* __restrict__ part) {
+                                                      double* __restrict__ part,
+                                                      const int* __restrict__ halt) {
+  if (halt && *(volatile const int*)halt) return;
   extern __shared__ __align__(16) double gst[];
   const int k4 = (k + 3) & ~3, nb4 = k4 >> 2, nb = nb4 * (nb4 + 1) / 2;
   const int64_t r0 = (int64_t)blockIdx.x * rows_per_cta, r1 = min(rows, r0 + rows_per_cta);
@@ -259,7 +269,8 @@ __global__ void __launch_bounds__(256) gram_cm_kernel(const double* __restrict__
 
 // column-major k x rows fp64 -> row-major rows x lp fp64, zero-padded columns
 __global__ void cm_to_rm_pad64_kernel(const double* __restrict__ f, int64_t rows, int k, int lp,
-                                      double* __restrict__ out) {
+                                      double* __restrict__ out, const int* __restrict__ halt) {
+  if (halt && *(volatile const int*)halt) return;
   const int64_t total = rows * lp;
   for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < total;
        e += (int64_t)gridDim.x * blockDim.x) {
@@ -330,15 +341,29 @@ __global__ void rows_small64_kernel(const float* __restrict__ in, int64_t rows, 
   }
 }
 
+// Split-K plan: fewest waves per unit of K work, cost(s) = ceil(tiles s / nsm) / s
+// (+ a small charge per split for the partial-sum traffic).
+int64_t xs64_splits(int64_t tiles, int64_t K, int nsm) {
+  int64_t best = 1;
+  double best_cost = 1e300;
+  const int64_t smax = std::max<int64_t>(1, std::min<int64_t>(64, K / (4 * kBK)));
+  for (int64_t sp = 1; sp <= smax; ++sp) {
+    const double cost = (double)((tiles * sp + nsm - 1) / nsm) / (double)sp + 0.002 * (double)sp;
+    if (cost < best_cost) {
+      best_cost = cost;
+      best = sp;
+    }
+  }
+  return best;
+}
+
 template <bool kTN, int LP>
 void xs64_launch(const float* x, int64_t ldx, int64_t m, int64_t n, const double* s, double* out,
-                 double* ws, int nsm, cudaStream_t st) {
+                 double* ws, int nsm, cudaStream_t st, const int* halt) {
   using Sh = Xs64Shape<LP>;
   const int64_t out_rows = kTN ? n : m, K = kTN ? m : n;
   const int64_t tiles = (out_rows + Sh::BM - 1) / Sh::BM;
-  // one wave of one CTA per SM (the kernel is fp64-FMA bound with 8 warps)
-  int64_t splits = std::max<int64_t>(1, ((int64_t)nsm + tiles - 1) / tiles);
-  splits = std::min<int64_t>(splits, std::max<int64_t>(1, K / (4 * kBK)));
+  int64_t splits = xs64_splits(tiles, K, nsm);
   const int64_t kchunk = ((K + splits - 1) / splits + kBK - 1) / kBK * kBK;
   splits = (K + kchunk - 1) / kchunk;
   static bool attr = false;
@@ -350,75 +375,88 @@ void xs64_launch(const float* x, int64_t ldx, int64_t m, int64_t n, const double
   double* dst = splits > 1 ? ws : out;
   note_launches(1);
   xs64_kernel<kTN, LP><<<dim3((unsigned)tiles, (unsigned)splits), kXT, Sh::smem, st>>>(
-      x, ldx, m, n, s, dst, kchunk);
+      x, ldx, m, n, s, dst, kchunk, halt);
   if (splits > 1) {
     const int64_t total = out_rows * LP;
     note_launches(1);
     reduce_splits64_kernel<<<(unsigned)std::min<int64_t>((total + 255) / 256, 8 * nsm), 256, 0,
-                             st>>>(ws, (int)splits, total, out);
+                             st>>>(ws, (int)splits, total, out, halt);
   }
 }
 
 template <bool kTN>
 void xs64_dispatch(const float* x, int64_t ldx, int64_t m, int64_t n, const double* s, int lp,
-                   double* out, double* ws, int nsm, cudaStream_t st) {
+                   double* out, double* ws, int nsm, cudaStream_t st, const int* halt) {
   switch (lp) {
-    case 16: xs64_launch<kTN, 16>(x, ldx, m, n, s, out, ws, nsm, st); break;
-    case 32: xs64_launch<kTN, 32>(x, ldx, m, n, s, out, ws, nsm, st); break;
-    case 48: xs64_launch<kTN, 48>(x, ldx, m, n, s, out, ws, nsm, st); break;
-    case 64: xs64_launch<kTN, 64>(x, ldx, m, n, s, out, ws, nsm, st); break;
-    case 80: xs64_launch<kTN, 80>(x, ldx, m, n, s, out, ws, nsm, st); break;
-    case 96: xs64_launch<kTN, 96>(x, ldx, m, n, s, out, ws, nsm, st); break;
-    case 112: xs64_launch<kTN, 112>(x, ldx, m, n, s, out, ws, nsm, st); break;
-    case 128: xs64_launch<kTN, 128>(x, ldx, m, n, s, out, ws, nsm, st); break;
+    case 16: xs64_launch<kTN, 16>(x, ldx, m, n, s, out, ws, nsm, st, halt); break;
+    case 32: xs64_launch<kTN, 32>(x, ldx, m, n, s, out, ws, nsm, st, halt); break;
+    case 48: xs64_launch<kTN, 48>(x, ldx, m, n, s, out, ws, nsm, st, halt); break;
+    case 64: xs64_launch<kTN, 64>(x, ldx, m, n, s, out, ws, nsm, st, halt); break;
+    case 80: xs64_launch<kTN, 80>(x, ldx, m, n, s, out, ws, nsm, st, halt); break;
+    case 96: xs64_launch<kTN, 96>(x, ldx, m, n, s, out, ws, nsm, st, halt); break;
+    case 112: xs64_launch<kTN, 112>(x, ldx, m, n, s, out, ws, nsm, st, halt); break;
+    case 128: xs64_launch<kTN, 128>(x, ldx, m, n, s, out, ws, nsm, st, halt); break;
     default: break;  // callers pad to a multiple of 16 <= 128
   }
 }
 
-int gram_grid(int64_t rows, int nsm) {
-  return (int)std::max<int64_t>(1, std::min<int64_t>(nsm, (rows + 255) / 256));
+// One 32-row stage per CTA where the k x k tiles leave most threads idle
+// (small k: the per-CTA work is a short dependent chain, so spread the rows);
+// one CTA per SM at most once every thread owns a tile.
+int gram_grid(int64_t rows, int k, int nsm) {
+  const int nb4 = (k + 3) / 4, nb = nb4 * (nb4 + 1) / 2;
+  const int64_t cap = nb >= 128 ? nsm : 4 * (int64_t)nsm;
+  return (int)std::max<int64_t>(1, std::min<int64_t>(cap, (rows + 31) / 32));
 }
 
 }  // namespace
 
 size_t xs64_ws_doubles(int64_t m, int64_t n, int lp, int nsm) {
-  // split-K partials: splits <= ceil(nsm / tiles), so splits * rows <=
-  // (nsm + tiles) * BM <= nsm * 1024 + rows + 1024
-  const int64_t rows = std::max(m, n);
-  return (size_t)(((int64_t)nsm * 1024 + rows + 1024) * lp);
+  // split-K partials of either orientation, with the launch's own plan
+  const int64_t bm = 4 * (kXT / (lp / 16));
+  size_t most = 0;
+  for (int tn = 0; tn < 2; ++tn) {
+    const int64_t rows = tn ? n : m, K = tn ? m : n;
+    const int64_t tiles = (rows + bm - 1) / bm;
+    int64_t sp = xs64_splits(tiles, K, nsm);
+    const int64_t kchunk = ((K + sp - 1) / sp + kBK - 1) / kBK * kBK;
+    sp = (K + kchunk - 1) / kchunk;
+    if (sp > 1) most = std::max(most, (size_t)(sp * rows * lp));
+  }
+  return std::max<size_t>(most, 1);
 }
 
 void launch_xs64_nn(const float* x, int64_t ldx, int64_t m, int64_t n, const double* s, int lp,
-                    double* out, double* ws, int nsm, cudaStream_t st) {
-  xs64_dispatch<false>(x, ldx, m, n, s, lp, out, ws, nsm, st);
+                    double* out, double* ws, int nsm, cudaStream_t st, const int* halt) {
+  xs64_dispatch<false>(x, ldx, m, n, s, lp, out, ws, nsm, st, halt);
 }
 
 void launch_xs64_tn(const float* x, int64_t ldx, int64_t m, int64_t n, const double* t, int lp,
-                    double* out, double* ws, int nsm, cudaStream_t st) {
-  xs64_dispatch<true>(x, ldx, m, n, t, lp, out, ws, nsm, st);
+                    double* out, double* ws, int nsm, cudaStream_t st, const int* halt) {
+  xs64_dispatch<true>(x, ldx, m, n, t, lp, out, ws, nsm, st, halt);
 }
 
 size_t gram_cm_ws_doubles(int64_t rows, int k, int nsm) {
-  return (size_t)gram_grid(rows, nsm) * k * k;
+  return (size_t)gram_grid(rows, k, nsm) * k * k;
 }
 
 void launch_gram_cm(const double* f_cm, int64_t rows, int k, double* g, double* ws, int nsm,
-                    cudaStream_t st, bool row_major) {
-  const int grid = gram_grid(rows, nsm);
+                    cudaStream_t st, bool row_major, const int* halt) {
+  const int grid = gram_grid(rows, k, nsm);
   const int64_t per = (rows + grid - 1) / grid;
   const int k4 = (k + 3) & ~3;
   note_launches(2);
   gram_cm_kernel<<<grid, 256, sizeof(double) * kGR * k4, st>>>(
-      f_cm, rows, k, row_major ? 1 : rows, row_major ? k : 1, per, ws);
-  reduce_splits64_kernel<<<(k * k + 255) / 256, 256, 0, st>>>(ws, grid, (int64_t)k * k, g);
+      f_cm, rows, k, row_major ? 1 : rows, row_major ? k : 1, per, ws, halt);
+  reduce_splits64_kernel<<<(k * k + 255) / 256, 256, 0, st>>>(ws, grid, (int64_t)k * k, g, halt);
 }
 
 void launch_cm_to_rm_pad64(const double* f_cm, int64_t rows, int k, int lp, double* out,
-                           int nsm, cudaStream_t st) {
+                           int nsm, cudaStream_t st, const int* halt) {
   const int64_t total = rows * lp;
   note_launches(1);
   cm_to_rm_pad64_kernel<<<(unsigned)std::min<int64_t>((total + 255) / 256, 8 * nsm), 256, 0,
-                          st>>>(f_cm, rows, k, lp, out);
+                          st>>>(f_cm, rows, k, lp, out, halt);
 }
 
 void launch_mu_update(const double* t_in, int64_t rows, int k, const double* num, int ldn,

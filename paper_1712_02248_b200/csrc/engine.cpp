@@ -383,18 +383,21 @@ DenseBufs make_dense(cnmf_context* c, int64_t d, int64_t n, int k) {
   return b;
 }
 
-// p = X B (d x lp) and g = B^T B for an A half (solvers.cpp:154-155)
-void dense_prepare_a(cnmf_context* c, const XView& X, const double* b_cm, int k, DenseBufs& db) {
-  launch_cm_to_rm_pad64(b_cm, X.n, k, db.lp, db.sb, c->nsm, c->stream);
-  launch_xs64_nn(X.x, X.ldx, X.d, X.n, db.sb, db.lp, db.y, db.xs_ws, c->nsm, c->stream);
-  launch_gram_cm(b_cm, X.n, k, db.g, db.gram_ws, c->nsm, c->stream);
+// p = X B (d x lp) and g = B^T B for an A half (solvers.cpp:154-155).
+// halt: the dense HALS halt flag (the launches become no-ops behind a halt).
+void dense_prepare_a(cnmf_context* c, const XView& X, const double* b_cm, int k, DenseBufs& db,
+                     const int* halt = nullptr) {
+  launch_cm_to_rm_pad64(b_cm, X.n, k, db.lp, db.sb, c->nsm, c->stream, halt);
+  launch_xs64_nn(X.x, X.ldx, X.d, X.n, db.sb, db.lp, db.y, db.xs_ws, c->nsm, c->stream, halt);
+  launch_gram_cm(b_cm, X.n, k, db.g, db.gram_ws, c->nsm, c->stream, false, halt);
 }
 
 // p = X^T A (n x lp) and w = A^T A for a B half (solvers.cpp:175-176)
-void dense_prepare_b(cnmf_context* c, const XView& X, const double* a_cm, int k, DenseBufs& db) {
-  launch_cm_to_rm_pad64(a_cm, X.d, k, db.lp, db.sa, c->nsm, c->stream);
-  launch_xs64_tn(X.x, X.ldx, X.d, X.n, db.sa, db.lp, db.z, db.xs_ws, c->nsm, c->stream);
-  launch_gram_cm(a_cm, X.d, k, db.w, db.gram_ws, c->nsm, c->stream);
+void dense_prepare_b(cnmf_context* c, const XView& X, const double* a_cm, int k, DenseBufs& db,
+                     const int* halt = nullptr) {
+  launch_cm_to_rm_pad64(a_cm, X.d, k, db.lp, db.sa, c->nsm, c->stream, halt);
+  launch_xs64_tn(X.x, X.ldx, X.d, X.n, db.sa, db.lp, db.z, db.xs_ws, c->nsm, c->stream, halt);
+  launch_gram_cm(a_cm, X.d, k, db.w, db.gram_ws, c->nsm, c->stream, false, halt);
 }
 
 // FastHALS (fasthals_step, solvers.cpp:146-187) and HALS (hals_step,
@@ -431,10 +434,11 @@ void run_dense_hals(cnmf_context* c, HalsRun& hr, const XView& X, DenseBufs& db,
           HalsState s2 = st;
           s2.b = b;
           s2.bold = bold;
+          const int* hflag = &st.halt->halted;
           if (h == 0)
-            dense_prepare_a(c, X, b, k, db);
+            dense_prepare_a(c, X, b, k, db, hflag);
           else
-            dense_prepare_b(c, X, st.a, k, db);
+            dense_prepare_b(c, X, st.a, k, db, hflag);
           CK(launch_hals(s2, normalize_a, 0.0, 0.0, (int)it, (int)it + 1, h, c0, s0, hr.epoch,
                          hr.grid, c->stream));
           if (h == 1) std::swap(b, bold);  // the B half leaves the new B in the second buffer

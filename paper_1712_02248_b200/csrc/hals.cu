@@ -483,7 +483,11 @@ __global__ void __launch_bounds__(kThreads, 1) hals_kernel(const HalsArgs p) {
         return;
       }
       if (S.dense) {  // one half per launch
-        if (cta == 0 && tid == 0) *S.halt = HaltInfo{0, it + 1, 0, 0, 0, bcur == S.bold, ep};
+        if (cta == 0 && tid == 0) {
+          *S.halt = HaltInfo{0, it + 1, 0, 0, 0, bcur == S.bold, ep};
+          if (prof)
+            for (int i = 0; i < 21; ++i) S.prof[i] += s_prof[i];
+        }
         return;
       }
       // A-hat = L^T A (solvers.cpp:438): partials, exchange, slice reduce, exchange
@@ -552,6 +556,16 @@ __global__ void __launch_bounds__(kThreads, 1) hals_kernel(const HalsArgs p) {
               if (t < nbj) acc[t] = fma(bv8[cc], gw[(c0 + cc) * k + jb + t], acc[t]);
           }
         }
+        // the block's b and p values are loaded up front: the column chain
+        // below then waits on arithmetic only
+        double bb[kNB], pb[kNB];
+#pragma unroll
+        for (int t = 0; t < kNB; ++t) {
+          const int j = jb + t;
+          bb[t] = t < nbj ? __ldcg(bcur + (int64_t)j * n + gr) : 0.0;
+          pb[t] = t < nbj ? (S.dense ? __ldcg(S.pd + gr * lp + j) : __ldcg(S.p + (int64_t)j * n + gr))
+                          : 0.0;
+        }
 #pragma unroll
         for (int t = 0; t < kNB; ++t) {
           if (t >= nbj) break;
@@ -561,8 +575,8 @@ __global__ void __launch_bounds__(kThreads, 1) hals_kernel(const HalsArgs p) {
           for (int u = 0; u < kNB; ++u)
             if (u < t) s = fma(dl[u], gw[(jb + u) * k + j], s);
           const double wjj = s_diag[j];
-          const double bij = __ldcg(bcur + (int64_t)j * n + gr);
-          const double pij = S.dense ? __ldcg(S.pd + gr * lp + j) : __ldcg(S.p + (int64_t)j * n + gr);
+          const double bij = bb[t];
+          const double pij = pb[t];
           const double v = constrained ? (bij * wjj + pij - s - p.alpha) / (wjj + p.beta)  // 502-508
                                        : bij + (pij - s) / wjj;                            // 480-490
           const double vf = v > 0.0 ? v : 0.0;

@@ -188,17 +188,19 @@ void launch_normalize_column(double* a_cm, int64_t d, int j, cudaStream_t s);
 // out (rows x lp fp64, row-major) = X S (NN, rows = m) or X^T T (TN, rows = n);
 // s: K x lp fp64 row-major (lp a multiple of 16, <= 128); ws: xs64_ws_doubles.
 size_t xs64_ws_doubles(int64_t m, int64_t n, int lp, int nsm);
+// halt (nullable): a device flag; when set the launch is a no-op (products
+// queued behind a halted dense HALS sweep, engine.cpp run_dense_hals).
 void launch_xs64_nn(const float* x, int64_t ldx, int64_t m, int64_t n, const double* s, int lp,
-                    double* out, double* ws, int nsm, cudaStream_t st);
+                    double* out, double* ws, int nsm, cudaStream_t st, const int* halt = nullptr);
 void launch_xs64_tn(const float* x, int64_t ldx, int64_t m, int64_t n, const double* t, int lp,
-                    double* out, double* ws, int nsm, cudaStream_t st);
+                    double* out, double* ws, int nsm, cudaStream_t st, const int* halt = nullptr);
 // g (k x k) = F^T F of a column-major k x rows fp64 factor (row_major: a
 // rows x k row-major one), fixed-order fp64.
 size_t gram_cm_ws_doubles(int64_t rows, int k, int nsm);
 void launch_gram_cm(const double* f_cm, int64_t rows, int k, double* g, double* ws, int nsm,
-                    cudaStream_t st, bool row_major = false);
+                    cudaStream_t st, bool row_major = false, const int* halt = nullptr);
 void launch_cm_to_rm_pad64(const double* f_cm, int64_t rows, int k, int lp, double* out,
-                           int nsm, cudaStream_t st);
+                           int nsm, cudaStream_t st, const int* halt = nullptr);
 // mu_update_half (semi = 0) / semi_nmf_half (semi = 1) of a column-major
 // factor: t_out = t_in .* f(num, t_in g) (solvers.cpp:55-93).
 void launch_mu_update(const double* t_in, int64_t rows, int k, const double* num, int ldn,
