@@ -211,13 +211,15 @@ int range_finder(cnmf_context* c, const XView& X, int q, int lp, uint64_t w, boo
     else
       launch_xs_nn(X.x, X.ldx, X.d, X.n, s, lp, out, xs, c->nsm, st);
   };
+  // intermediate re-orthonormalisations take one Cholesky pass (they only
+  // carry a span into the next X pass); the basis handed on takes two
   apply(omega, y, transpose);
-  launch_thin_qr(y, rows, q, lp, basis, qws, c->nsm, st);
+  launch_thin_qr(y, rows, q, lp, basis, qws, c->nsm, st, w == 0 ? 2 : 1);
   for (uint64_t it = 0; it < w; ++it) {
     apply(basis, z, !transpose);
-    launch_thin_qr(z, cols, q, lp, zq, qws, c->nsm, st);
+    launch_thin_qr(z, cols, q, lp, zq, qws, c->nsm, st, 1);
     apply(zq, y, transpose);
-    launch_thin_qr(y, rows, q, lp, basis, qws, c->nsm, st);
+    launch_thin_qr(y, rows, q, lp, basis, qws, c->nsm, st, it + 1 == w ? 2 : 1);
   }
   if (canonical)
     launch_householder_signs(basis, rows, q, lp, c->ws<float>("hh_sgn_" + tag, 128), c->nsm, st);

@@ -79,9 +79,13 @@ bool launch_xs_tc(bool tn, const float* x, int64_t ldx, int64_t m, int64_t n, co
 size_t qr_ws_bytes(int64_t rows, int lp, int nsm);
 void launch_thin_qr_dist(const float* y, int64_t rows, int l, int lp, float* q, void* ws, int nsm,
                          cudaStream_t st, const std::function<void(double*, size_t)>& allreduce_g,
-                         int** flag_out);
+                         int** flag_out, int passes = 2);
+// passes = 2: CholeskyQR2 (the bases handed on); passes = 1: one Cholesky
+// pass, for the intermediate re-orthonormalisations of the range finder,
+// which only carry a span into the next X pass (span and nested flag are
+// the same; the final QR restores full orthogonality).
 void launch_thin_qr(const float* y, int64_t rows, int l, int lp, float* q, void* ws, int nsm,
-                    cudaStream_t st);
+                    cudaStream_t st, int passes = 2);
 // Flip the columns of an orthonormal q (rows x lp, l used) to the reference's
 // Householder signs (qr.cpp:35); sgn: l floats of device scratch.  Only the
 // step-level entry points that return bases need it: FastHALS-RP uses L, R

@@ -147,13 +147,15 @@ __global__ void gram_reduce_kernel(const double* __restrict__ part, int grid, in
 // non-positive or below 1e-13 of its original diagonal (Y numerically rank
 // deficient at fp32 resolution).
 // Cholesky G = R^T R (R upper) and R^-1, fp64, one CTA of 128 threads.
-// Right-looking factorisation with two barriers per column: every thread
-// reads the pivot, row j is scaled by 1/r (the diagonal itself is kept in
-// rd[] so nothing rewrites gs[j][j] while others read it), then the trailing
-// update.  R^-1 is built column-parallel by back substitution -- column c by
-// thread c, no barriers: Rinv[c][c] = 1/r_c, Rinv[i][c] = -(sum_{q=i+1..c}
-// R[i][q] Rinv[q][c]) / r_i.  Fails (flag) if a pivot drops below
-// 1e-13 * its original diagonal (rank deficiency -> Householder fallback).
+// Right-looking factorisation, one barrier per column: every thread reads
+// the pivot p_j and row j (left unscaled), and the trailing upper triangle
+// takes g_ab -= g_ja g_jb / p_j -- warps over rows a, lanes over columns b
+// (no index division).  Row j is final after step j; R_jb = g_jb / sqrt(p_j)
+// is applied afterwards in one parallel pass.  R^-1 is built column-parallel
+// by back substitution -- column c by thread c, two accumulator chains:
+// Rinv[c][c] = 1/r_c, Rinv[i][c] = -(sum_{q=i+1..c} R[i][q] Rinv[q][c]) / r_i.
+// Fails (flag) if a pivot drops below 1e-13 * its original diagonal (rank
+// deficiency -> Householder fallback).
 __global__ void __launch_bounds__(128) chol_inv_kernel(const double* __restrict__ g, int l,
                                                        int lp, double* __restrict__ rinv64,
                                                        float* __restrict__ rinv,
@@ -162,13 +164,9 @@ __global__ void __launch_bounds__(128) chol_inv_kernel(const double* __restrict_
   double* diag0 = gs + l * l;
   double* rd = diag0 + l;
   double* rdi = rd + l;
-  const int tid = threadIdx.x, nt = blockDim.x;
+  const int tid = threadIdx.x, nt = blockDim.x, lane = tid & 31, warp = tid >> 5, nw = nt >> 5;
   for (int e = tid; e < l * l; e += nt) gs[e] = g[(e / l) * lp + e % l];
   for (int e = tid; e < l; e += nt) diag0[e] = g[e * lp + e];
-  for (int e = tid; e < lp * lp; e += nt) {
-    rinv[e] = 0.f;
-    rinv64[e] = 0.0;
-  }
   __syncthreads();
   for (int j = 0; j < l; ++j) {
     const double piv = gs[j * l + j];
@@ -176,28 +174,43 @@ __global__ void __launch_bounds__(128) chol_inv_kernel(const double* __restrict_
       if (tid == 0) *flag = 1;
       return;
     }
-    const double r = sqrt(piv), ir = 1.0 / r;
-    for (int c = j + 1 + tid; c < l; c += nt) gs[j * l + c] *= ir;
-    if (tid == 0) {
-      rd[j] = r;
-      rdi[j] = ir;
-    }
-    __syncthreads();
-    const int m = l - j - 1;
-    for (int e = tid; e < m * m; e += nt) {
-      const int a = j + 1 + e / m, b = j + 1 + e % m;
-      if (a <= b) gs[a * l + b] = fma(-gs[j * l + a], gs[j * l + b], gs[a * l + b]);
+    const double ip = 1.0 / piv;
+    const double* rowj = gs + j * l;
+    for (int a = j + 1 + warp; a < l; a += nw) {
+      const double f = rowj[a] * ip;
+      double* rowa = gs + a * l;
+      for (int b = a + lane; b < l; b += 32) rowa[b] = fma(-f, rowj[b], rowa[b]);
     }
     __syncthreads();
   }
+  for (int j = tid; j < l; j += nt) {
+    const double pj = gs[j * l + j];
+    const double ir = 1.0 / sqrt(pj);
+    rdi[j] = ir;
+    rd[j] = pj * ir;
+  }
+  __syncthreads();
+  for (int i = warp; i < l; i += nw)
+    for (int b = i + 1 + lane; b < l; b += 32) gs[i * l + b] *= rdi[i];
+  for (int e = tid; e < lp * lp; e += nt) {  // padding and the lower triangle stay zero
+    rinv[e] = 0.f;
+    rinv64[e] = 0.0;
+  }
+  __syncthreads();
   // thread c owns column c of R^-1, kept transposed in row c of gs's lower
   // triangle (gs[c][i] = Rinv[i][c], i < c) -- untouched by the factorisation
   for (int c = tid; c < l; c += nt) {
     double* xc = gs + c * l;
     for (int i = c - 1; i >= 0; --i) {
-      double sacc = gs[i * l + c] * rdi[c];  // q = c term
-      for (int q = i + 1; q < c; ++q) sacc = fma(gs[i * l + q], xc[q], sacc);
-      xc[i] = -sacc * rdi[i];
+      const double* ri = gs + i * l;
+      double s0 = ri[c] * rdi[c], s1 = 0.0;  // q = c term
+      int q = i + 1;
+      for (; q + 1 < c; q += 2) {
+        s0 = fma(ri[q], xc[q], s0);
+        s1 = fma(ri[q + 1], xc[q + 1], s1);
+      }
+      if (q < c) s0 = fma(ri[q], xc[q], s0);
+      xc[i] = -(s0 + s1) * rdi[i];
     }
     rinv[c * lp + c] = (float)rdi[c];
     rinv64[c * lp + c] = rdi[c];
@@ -362,30 +375,38 @@ size_t qr_ws_bytes(int64_t rows, int lp, int nsm) {
 // broke down and the caller gathers Y for the replicated path.
 void launch_thin_qr_dist(const float* y, int64_t rows, int l, int lp, float* q, void* ws, int nsm,
                          cudaStream_t st, const std::function<void(double*, size_t)>& allreduce_g,
-                         int** flag_out) {
+                         int** flag_out, int passes) {
   const QrWs w = carve(ws, rows, lp, nsm);
   cudaMemsetAsync(w.flag, 0, sizeof(int), st);
   gram(y, rows, l, lp, w, nsm, st);
   allreduce_g(w.g, (size_t)lp * lp);
   chol_inv(l, lp, w, st);
-  launch_xs_nn(y, lp, rows, lp, w.rinv, lp, w.q1, w.xs_ws, nsm, st);
-  gram(w.q1, rows, l, lp, w, nsm, st);
-  allreduce_g(w.g, (size_t)lp * lp);
-  chol_inv(l, lp, w, st);
-  launch_xs_nn(w.q1, lp, rows, lp, w.rinv, lp, q, w.xs_ws, nsm, st);
+  if (passes >= 2) {
+    launch_xs_nn(y, lp, rows, lp, w.rinv, lp, w.q1, w.xs_ws, nsm, st);
+    gram(w.q1, rows, l, lp, w, nsm, st);
+    allreduce_g(w.g, (size_t)lp * lp);
+    chol_inv(l, lp, w, st);
+    launch_xs_nn(w.q1, lp, rows, lp, w.rinv, lp, q, w.xs_ws, nsm, st);
+  } else {
+    launch_xs_nn(y, lp, rows, lp, w.rinv, lp, q, w.xs_ws, nsm, st);
+  }
   *flag_out = w.flag;
 }
 
 void launch_thin_qr(const float* y, int64_t rows, int l, int lp, float* q, void* ws, int nsm,
-                    cudaStream_t st) {
+                    cudaStream_t st, int passes) {
   const QrWs w = carve(ws, rows, lp, nsm);
   cudaMemsetAsync(w.flag, 0, sizeof(int), st);
   gram(y, rows, l, lp, w, nsm, st);
   chol_inv(l, lp, w, st);
-  launch_xs_nn(y, lp, rows, lp, w.rinv, lp, w.q1, w.xs_ws, nsm, st);
-  gram(w.q1, rows, l, lp, w, nsm, st);
-  chol_inv(l, lp, w, st);
-  launch_xs_nn(w.q1, lp, rows, lp, w.rinv, lp, q, w.xs_ws, nsm, st);
+  if (passes >= 2) {
+    launch_xs_nn(y, lp, rows, lp, w.rinv, lp, w.q1, w.xs_ws, nsm, st);
+    gram(w.q1, rows, l, lp, w, nsm, st);
+    chol_inv(l, lp, w, st);
+    launch_xs_nn(w.q1, lp, rows, lp, w.rinv, lp, q, w.xs_ws, nsm, st);
+  } else {
+    launch_xs_nn(y, lp, rows, lp, w.rinv, lp, q, w.xs_ws, nsm, st);
+  }
   note_launches(1);
   householder_kernel<<<1, 1024, 0, st>>>(y, rows, l, lp, w.hw, w.hv, q, w.flag);
 }
