@@ -228,6 +228,18 @@ cnmf_status cnmf_synth_x(cnmf_context* ctx, uint64_t d, uint64_t n, uint64_t ran
                          int factor_kind, int noise_kind, double sigma, uint64_t seed,
                          uint64_t col_lo, uint64_t col_hi, uint64_t ldx, float* x);
 
+/* run(const SparseMatrix&, const SolverConfig&) (solvers.hpp:105,
+ * solvers.cpp:515-517): X given in CSR on the host (SparseMatrix layout,
+ * matrix.hpp:34-44 -- d + 1 row offsets, column indices strictly increasing
+ * within a row, fp32 values).  Every algorithm of cnmf_run; the X
+ * contractions, check_data and the objective (metrics.cpp:79-102) run on the
+ * stored entries only.  Structure errors raise CNMF_ERR_DIMENSION with the
+ * messages of SparseMatrix::validate (matrix.cpp:37-56). */
+cnmf_status cnmf_run_csr(cnmf_context* ctx, const uint64_t* row_offsets,
+                         const uint64_t* col_indices, const float* values, uint64_t d, uint64_t n,
+                         const cnmf_solver_config* cfg, float* a_out, float* b_out,
+                         cnmf_run_trace* trace);
+
 /* ---- host-side data formats around the path (no device, no context) ----
  * The front end's inputs and reports; fp64 host code,
  * bitwise the reference's results.  `msg` (may be NULL) receives the error

@@ -265,6 +265,7 @@ class Reference:
         L.ref_initialize.argtypes = [_sz, _sz, _sz, _u64, _dp, _dp]
         L.ref_matmul.argtypes = [_dp, _sz, _sz, _dp, _sz, _sz, C.c_int, C.c_int, _dp]
         L.ref_thin_qr.argtypes = [_dp, _sz, _sz, _dp, _dp]
+        L.ref_set_csr.argtypes = [_sz, _sz, C.c_void_p, C.c_void_p, _dp]
         L.ref_pairwise_distortion.argtypes = [_dp, _sz, _sz, _dp, _sz, _sz, _u64, _dp, _dp]
         L.ref_generate_synthetic.argtypes = [_sz, _sz, _sz, C.c_double, C.c_double, _u64, _dp]
         L.ref_powered_range_finder.argtypes = [_dp, _sz, _sz, _sz, _sz, _u64, _dp]
@@ -378,8 +379,19 @@ class Reference:
     def run(self, x, k, q=0, w=4, sketch_seed=1, alpha=0.0, beta=0.0, max_iterations=200,
             rel_tolerance=1e-9, error_interval=5, seed=1, normalize_a=True,
             algorithm=FASTHALS_RP):
-        x = np.ascontiguousarray(x, dtype=np.float64)
-        d, n = x.shape
+        xp = None
+        if hasattr(x, "tocsr"):  # run(const SparseMatrix&, ...) (solvers.cpp:515-517)
+            csr = x.tocsr()
+            csr.sort_indices()
+            d, n = csr.shape
+            rp = np.ascontiguousarray(csr.indptr, dtype=np.uint64)
+            ci = np.ascontiguousarray(csr.indices, dtype=np.uint64)
+            vals = np.ascontiguousarray(csr.data, dtype=np.float64)
+            self._check(self.lib.ref_set_csr(d, n, rp.ctypes.data, ci.ctypes.data, _d(vals)))
+        else:
+            x = np.ascontiguousarray(x, dtype=np.float64)
+            d, n = x.shape
+            xp = _d(x)
         cap = max_iterations + 2
         it = (_sz * cap)()
         er, el = np.zeros(cap), np.zeros(cap)
@@ -388,7 +400,7 @@ class Reference:
         status = C.c_int()
         msg = C.create_string_buffer(256)
         a, b = np.empty((d, k)), np.empty((n, k))
-        self._check(self.lib.ref_run(_d(x), d, n, algorithm, k, q, w, _u64(sketch_seed), alpha,
+        self._check(self.lib.ref_run(xp, d, n, algorithm, k, q, w, _u64(sketch_seed), alpha,
                                      beta, max_iterations, rel_tolerance, error_interval,
                                      _u64(seed), int(normalize_a), _d(a), _d(b), it, _d(er),
                                      _d(el), cap, C.byref(cnt), C.byref(upd), C.byref(gini),

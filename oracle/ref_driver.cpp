@@ -193,6 +193,24 @@ double ref_reconstruction_error(const double* x, std::size_t d, std::size_t n, c
   return reconstruction_error(wrap(x, d, n), f);
 }
 
+namespace {
+SparseMatrix g_csr;  // the CSR input of the next ref_run with x == nullptr
+}
+
+// run(SparseMatrix) input: stored here, consumed by ref_run(x = nullptr, ...).
+int ref_set_csr(std::size_t d, std::size_t n, const std::size_t* row_offsets,
+                const std::size_t* col_indices, const double* values) {
+  return guarded([&] {
+    g_csr = SparseMatrix{};
+    g_csr.rows = d;
+    g_csr.cols = n;
+    g_csr.row_offsets.assign(row_offsets, row_offsets + d + 1);
+    g_csr.col_indices.assign(col_indices, col_indices + row_offsets[d]);
+    g_csr.values.assign(values, values + row_offsets[d]);
+    g_csr.validate();
+  });
+}
+
 int ref_run(const double* x, std::size_t d, std::size_t n, int algorithm, std::size_t k,
             std::size_t q, std::size_t w, std::uint64_t sketch_seed, double alpha, double beta,
             std::size_t max_iterations, double rel_tolerance, std::size_t error_interval,
@@ -214,7 +232,7 @@ int ref_run(const double* x, std::size_t d, std::size_t n, int algorithm, std::s
     cfg.error_interval = error_interval;
     cfg.seed = seed;
     cfg.normalize_a = normalize_a != 0;
-    const RunResult r = run(wrap(x, d, n), cfg);
+    const RunResult r = x ? run(wrap(x, d, n), cfg) : run(g_csr, cfg);
     unwrap(r.factors.a, a_out);
     unwrap(r.factors.b, b_out);
     *rec_count = r.trace.records.size();

@@ -117,7 +117,7 @@ EXPORTS = [
     "cnmf_thin_qr", "cnmf_xs_nn", "cnmf_xs_tn", "cnmf_synth_x", "cnmf_launch_count",
     "cnmf_time_xstream", "cnmf_shard_begin", "cnmf_nccl_unique_id", "cnmf_context_create_sharded",
     "cnmf_run_sharded_device", "cnmf_estimate_cost", "cnmf_generate_synthetic",
-    "cnmf_pairwise_distortion",
+    "cnmf_pairwise_distortion", "cnmf_run_csr",
 ]
 
 
@@ -181,6 +181,8 @@ def load_library(path: str = LIB_PATH):
     L.cnmf_context_create_sharded.argtypes = [C.c_int, C.c_int, C.c_int, C.c_char_p, C.POINTER(vp)]
     L.cnmf_run_sharded_device.argtypes = [vp, fp, u64, u64, u64, u64, u64, C.POINTER(_Config), fp,
                                           fp, C.POINTER(_Trace)]
+    L.cnmf_run_csr.argtypes = [vp, vp, vp, vp, u64, u64, C.POINTER(_Config), fp, fp,
+                               C.POINTER(_Trace)]
     L.cnmf_estimate_cost.argtypes = [C.c_int, u64, u64, u64, u64, C.POINTER(_Cost), C.c_char_p,
                                      C.c_size_t]
     L.cnmf_generate_synthetic.argtypes = [u64, u64, u64, C.c_double, C.c_double, u64, vp,
@@ -337,6 +339,31 @@ class Context:
         b = np.empty((n, config.k), dtype=np.float32)
         self._check(self.L.cnmf_run(self.h, _ptr(x), d, n, n, C.byref(cfg), _ptr(a), _ptr(b),
                                     C.byref(tr)))
+        return RunResult(a, b, self._result_trace(recs, tr))
+
+    def run_sparse(self, x, config: SolverConfig) -> RunResult:
+        """cnmf::run(const SparseMatrix&, ...) with X in host CSR form: a
+        scipy.sparse matrix or a (indptr, indices, data, (d, n)) tuple."""
+        if isinstance(x, tuple):
+            indptr, indices, data, (d, n) = x
+        else:
+            csr = x.tocsr()
+            csr.sort_indices()
+            indptr, indices, data = csr.indptr, csr.indices, csr.data
+            d, n = csr.shape
+        indptr = np.ascontiguousarray(indptr, dtype=np.uint64)
+        indices = np.ascontiguousarray(indices, dtype=np.uint64)
+        data = np.ascontiguousarray(data, dtype=np.float32)
+        if indptr.shape[0] != d + 1:
+            raise DimensionError("sparse matrix: row_offsets size must be rows + 1")
+        if indptr[-1] != data.shape[0] or indices.shape[0] != data.shape[0]:
+            raise DimensionError("sparse matrix: index/value arrays disagree")
+        cfg = config._c()
+        recs, tr = self._trace(config.max_iterations + 2)
+        a = np.empty((d, config.k), dtype=np.float32)
+        b = np.empty((n, config.k), dtype=np.float32)
+        self._check(self.L.cnmf_run_csr(self.h, _ptr(indptr), _ptr(indices), _ptr(data), d, n,
+                                        C.byref(cfg), _ptr(a), _ptr(b), C.byref(tr)))
         return RunResult(a, b, self._result_trace(recs, tr))
 
     def run_device(self, x, config: SolverConfig, a_out=None, b_out=None):

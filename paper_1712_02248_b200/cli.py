@@ -23,10 +23,11 @@ nlohmann-style JSON with sorted keys and NaN -> null), atomic writes
 2 usage / configuration / input / IO error; cli.cpp:759-799).
 
 The factorization itself is the C-ABI library on the GPU (fp32 storage, see
-DESIGN.md); inputs are dense CSV (data_io.cpp:75-106) or the reference's
-synthetic generator (bitwise, cnmf_generate_synthetic).  The sparse / image
-/ corpus formats feed the reference's sparse path, which is outside this
-build (scope): they are rejected with exit code 2.  Runs of a
+DESIGN.md); inputs are dense CSV (data_io.cpp:75-106), Matrix Market
+coordinate files run through the CSR path (data_io.cpp:228-288, cnmf_run_csr)
+or the reference's synthetic generator (bitwise, cnmf_generate_synthetic).
+Image directories and text corpora are outside this build (scope)
+and are rejected with exit code 2.  Runs of a
 compare / sweep plan execute one after another on the device (`--jobs` is
 accepted; the reference's output bytes do not depend on it either,
 cli.cpp:229-247).
@@ -295,6 +296,100 @@ def _strtod_whole(token: str, where: str) -> float:
         raise ParseError(f"{where}: cannot parse '{token}' as a number") from None
 
 
+def load_matrix_market(path: str):
+    """load_matrix_market (data_io.cpp:228-288) + sparse_from_triplets
+    (matrix.cpp:58-92): coordinate real|integer general, 1-based entries,
+    duplicates summed, entries summing to zero dropped -> scipy CSR (fp64)."""
+    import scipy.sparse as sparse
+    try:
+        f = open(path, "r", newline="")
+    except OSError:
+        raise IoError(f"cannot open {path} for reading") from None
+    with f:
+        lines = f.read().split("\n")
+    if lines and lines[-1] == "":
+        lines.pop()
+    strip = lambda t: t[:-1] if t.endswith("\r") else t  # noqa: E731
+    if not lines:
+        raise ParseError(f"{path}: line 1: missing banner")
+    ban = strip(lines[0]).split()
+    if (len(ban) != 5 or ban[0] != "%%MatrixMarket" or ban[1] != "matrix"
+            or ban[2] != "coordinate" or ban[3] not in ("real", "integer") or ban[4] != "general"):
+        raise ParseError(f"{path}: line 1: expected banner '%%MatrixMarket matrix coordinate "
+                         "real general'")
+    ln = 1
+    while True:
+        if ln >= len(lines):
+            raise ParseError(f"{path}: missing size line")
+        line = strip(lines[ln])
+        ln += 1
+        t = line.lstrip(" \t")
+        if t and t[0] != "%":
+            break
+    try:
+        tok = line.split()
+        rows, cols, entries = int(tok[0]), int(tok[1]), int(tok[2])
+        if min(rows, cols, entries) < 0:
+            raise ValueError
+    except (ValueError, IndexError):
+        raise ParseError(f"{path}: line {ln}: malformed size line") from None
+    if rows == 0 or cols == 0:
+        raise ParseError(f"{path}: line {ln}: zero matrix dimension")
+    ri, cj, vals = [], [], []
+    for e in range(entries):
+        if ln >= len(lines):
+            raise ParseError(f"{path}: unexpected end of file after {e} of {entries} entries")
+        line = strip(lines[ln])
+        ln += 1
+        where = f"{path}: line {ln}"
+        tok = line.split()
+        try:
+            i, j = int(tok[0]), int(tok[1])
+            vt = tok[2]
+        except (ValueError, IndexError):
+            raise ParseError(f"{where}: malformed entry") from None
+        if i < 1 or i > rows or j < 1 or j > cols:
+            raise ParseError(f"{where}: index out of range")
+        v = _strtod_whole(vt, where)
+        if not math.isfinite(v):
+            raise InputError(f"{where}: non-finite value")
+        if v < 0.0:
+            raise InputError(f"{where}: negative value {vt}")
+        ri.append(i - 1)
+        cj.append(j - 1)
+        vals.append(v)
+    ri, cj, vals = np.array(ri, np.int64), np.array(cj, np.int64), np.array(vals, np.float64)
+    order = np.lexsort((cj, ri))  # by row, then column (stable: duplicates keep file order)
+    ri, cj, vals = ri[order], cj[order], vals[order]
+    keep_r, keep_c, keep_v = [], [], []
+    e = 0
+    while e < len(vals):
+        f2, tot = e, 0.0
+        while f2 < len(vals) and ri[f2] == ri[e] and cj[f2] == cj[e]:
+            tot += vals[f2]
+            f2 += 1
+        if tot != 0.0:
+            keep_r.append(ri[e])
+            keep_c.append(cj[e])
+            keep_v.append(tot)
+        e = f2
+    return sparse.csr_matrix((np.array(keep_v, np.float64), (np.array(keep_r, np.int64),
+                                                             np.array(keep_c, np.int64))),
+                             shape=(rows, cols))
+
+
+def save_matrix_market_text(m) -> str:
+    """save_matrix_market (data_io.cpp:290-299)."""
+    m = m.tocsr()
+    m.sort_indices()
+    out = ["%%MatrixMarket matrix coordinate real general\n",
+           f"{m.shape[0]} {m.shape[1]} {m.nnz}\n"]
+    for i in range(m.shape[0]):
+        for p in range(m.indptr[i], m.indptr[i + 1]):
+            out.append(f"{i + 1} {m.indices[p] + 1} {fmt(m.data[p])}\n")
+    return "".join(out)
+
+
 # ---------------------------------------------------------------- options --
 # name -> (kind, default); kinds: str, uint, float, flag (cli.cpp:43-81)
 _DATASET = {"input": ("str", ""), "format": ("str", "csv"), "csv-header": ("flag", False),
@@ -467,8 +562,10 @@ def load_dataset(o: Dict[str, object]) -> np.ndarray:
     if fmt_name == "synthetic":
         return generate_synthetic(o["rows"], o["cols"], o["rank"], o["decay"], o["noise"],
                                   o["data-seed"])
-    raise UnsupportedError(f"dataset format {fmt_name} feeds the sparse / corpus path, which "
-                           "this build does not include (dense csv and synthetic only)")
+    if fmt_name == "mm":
+        return load_matrix_market(o["input"])
+    raise UnsupportedError(f"dataset format {fmt_name} (image directories and text corpora) "
+                           "is not part of this build (csv, mm and synthetic are)")
 
 
 def make_config(o: Dict[str, object], seed: int) -> SolverConfig:
@@ -484,6 +581,20 @@ def make_config(o: Dict[str, object], seed: int) -> SolverConfig:
 def _context():
     from . import default_context
     return default_context()
+
+
+def is_sparse(x) -> bool:
+    return hasattr(x, "tocsr")
+
+
+def solve(x, cfg: SolverConfig):
+    """cli.cpp:137-139: the dense or the sparse run (x: fp32 ndarray or CSR)."""
+    return _context().run_sparse(x, cfg) if is_sparse(x) else _context().run(x, cfg)
+
+
+def device_input(x):
+    """fp32 dense rows, or the CSR as is (values go to fp32 on upload)."""
+    return x if is_sparse(x) else x.astype(np.float32)
 
 
 def summary_json(cfg: SolverConfig, t) -> dict:
@@ -518,7 +629,7 @@ def cmd_factorize(o: Dict[str, object]) -> int:
     x = load_dataset(o)
     cfg = make_config(o, o["seed"])
     cfg.validate(*x.shape)
-    res = _context().run(x.astype(np.float32), cfg)
+    res = solve(device_input(x), cfg)
     out = o["out"]
     os.makedirs(out, exist_ok=True)
     write_text_atomic(os.path.join(out, "a.csv"), dense_csv_text(res.a))
@@ -545,6 +656,10 @@ def cmd_project(o: Dict[str, object]) -> int:
     if q == 0:
         raise ConfigError("--q is required")
     x = load_dataset(o)
+    if is_sparse(x):
+        # the distortion metric walks dense columns anyway (cli.cpp:528-532);
+        # the views of the densified matrix are the same products
+        x = x.toarray()
     d, n = x.shape
     if q > min(d, n):
         raise ConfigError("powered_range_finder: q must satisfy 1 <= q <= min(rows, cols)")
@@ -595,7 +710,7 @@ class Outcome:
     def __init__(self, x32: np.ndarray, cfg: SolverConfig):
         self.trace, self.ok, self.input_failure = None, False, False
         try:
-            res = _context().run(x32, cfg)
+            res = solve(x32, cfg)
             self.trace, self.ok = res.trace, True
             self.status, self.message = STATUS_NAMES[res.trace.status], res.trace.message
         except (ConfigError, InputError, IoError, UnsupportedError) as e:
@@ -638,7 +753,7 @@ def cmd_compare(o: Dict[str, object]) -> int:
         raise ConfigError("--out is required")
     x = load_dataset(o)
     d, n = x.shape
-    x32 = x.astype(np.float32)
+    x32 = device_input(x)
     plan = [(a, sd) for a in COMPARE_ORDER for sd in o["seeds"]]
     results = []
     for a, sd in plan:
@@ -681,7 +796,7 @@ def cmd_sweep(o: Dict[str, object]) -> int:
     if not o["out"]:
         raise ConfigError("--out is required")
     x = load_dataset(o)
-    x32 = x.astype(np.float32)
+    x32 = device_input(x)
     grid = lambda key, one: o[key] if o[key] else [o[one]]  # noqa: E731
     cells = [(k, q, w, al, be) for k in grid("k-grid", "k") for q in grid("q-grid", "q")
              for w in grid("w-grid", "w") for al in grid("alpha-grid", "alpha")

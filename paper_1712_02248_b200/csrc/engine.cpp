@@ -130,7 +130,11 @@ double uniform_positive(std::mt19937_64& e) {
 // one small CTA co-runs with the other stream's kernels.
 void gen_words(cnmf_context* c, uint64_t seed, uint64_t nwords, uint64_t* words,
                const std::string& tag, cudaStream_t st) {
-  if (nwords >= (uint64_t)1 << 20 && !std::getenv("CNMF_MT_SERIAL") && mt_jump_available()) {
+  static const uint64_t jump_min = [] {
+    const char* e = std::getenv("CNMF_MT_JUMP_MIN");  // threshold override (experiments)
+    return e ? (uint64_t)std::strtoull(e, nullptr, 10) : (uint64_t)1 << 20;
+  }();
+  if (nwords >= jump_min && !std::getenv("CNMF_MT_SERIAL") && mt_jump_available()) {
     uint64_t J = (uint64_t)1 << 15;
     while (J * (uint64_t)c->nsm < nwords) J <<= 1;
     const int K = (int)((nwords + J - 1) / J);
@@ -185,10 +189,23 @@ uint64_t* gen_init(cnmf_context* c, uint64_t seed, int64_t d, int64_t n, int k, 
 }
 
 // ---------------------------------------------------------- compression -----
+// X as the solvers see it: dense fp32 rows (x, ldx) or CSR (sp != nullptr).
 struct XView {
   const float* x;
   int64_t ldx, d, n;
+  const CsrView* sp = nullptr;
 };
+
+// The X contractions of every solver, dense or CSR.
+void x_times(cnmf_context* c, const XView& X, bool transpose, const float* s, int lp, float* out,
+             float* xs_ws, cudaStream_t st) {
+  if (X.sp)
+    launch_csr_spmm_f32(*X.sp, transpose, s, lp, lp, out, lp, c->nsm, st);
+  else if (transpose)
+    launch_xs_tn(X.x, X.ldx, X.d, X.n, s, lp, out, xs_ws, c->nsm, st);
+  else
+    launch_xs_nn(X.x, X.ldx, X.d, X.n, s, lp, out, xs_ws, c->nsm, st);
+}
 
 // Orthonormal basis (rows x lp) of range(X) (transpose = false) or of
 // range(X^T) (transpose = true); range_finder_impl, compression.cpp:23-42.
@@ -205,12 +222,7 @@ int range_finder(cnmf_context* c, const XView& X, int q, int lp, uint64_t w, boo
   float* zq = c->ws<float>("rf_zq_" + tag, cols * lp);
   float* xs = c->ws<float>("xs_ws_" + tag, xstream_ws_floats(X.d, X.n, lp, c->nsm));
   void* qws = c->ws<char>("qr_ws_" + tag, qr_ws_bytes(std::max(X.d, X.n), lp, c->nsm));
-  auto apply = [&](const float* s, float* out, bool tn) {
-    if (tn)
-      launch_xs_tn(X.x, X.ldx, X.d, X.n, s, lp, out, xs, c->nsm, st);
-    else
-      launch_xs_nn(X.x, X.ldx, X.d, X.n, s, lp, out, xs, c->nsm, st);
-  };
+  auto apply = [&](const float* s, float* out, bool tn) { x_times(c, X, tn, s, lp, out, xs, st); };
   // intermediate re-orthonormalisations take one Cholesky pass (they only
   // carry a span into the next X pass); the basis handed on takes two
   apply(omega, y, transpose);
@@ -390,7 +402,10 @@ DenseBufs make_dense(cnmf_context* c, int64_t d, int64_t n, int k) {
 void dense_prepare_a(cnmf_context* c, const XView& X, const double* b_cm, int k, DenseBufs& db,
                      const int* halt = nullptr) {
   launch_cm_to_rm_pad64(b_cm, X.n, k, db.lp, db.sb, c->nsm, c->stream, halt);
-  launch_xs64_nn(X.x, X.ldx, X.d, X.n, db.sb, db.lp, db.y, db.xs_ws, c->nsm, c->stream, halt);
+  if (X.sp)
+    launch_csr_spmm_f64(*X.sp, false, db.sb, db.lp, db.lp, db.y, db.lp, c->nsm, c->stream, halt);
+  else
+    launch_xs64_nn(X.x, X.ldx, X.d, X.n, db.sb, db.lp, db.y, db.xs_ws, c->nsm, c->stream, halt);
   launch_gram_cm(b_cm, X.n, k, db.g, db.gram_ws, c->nsm, c->stream, false, halt);
 }
 
@@ -398,7 +413,10 @@ void dense_prepare_a(cnmf_context* c, const XView& X, const double* b_cm, int k,
 void dense_prepare_b(cnmf_context* c, const XView& X, const double* a_cm, int k, DenseBufs& db,
                      const int* halt = nullptr) {
   launch_cm_to_rm_pad64(a_cm, X.d, k, db.lp, db.sa, c->nsm, c->stream, halt);
-  launch_xs64_tn(X.x, X.ldx, X.d, X.n, db.sa, db.lp, db.z, db.xs_ws, c->nsm, c->stream, halt);
+  if (X.sp)
+    launch_csr_spmm_f64(*X.sp, true, db.sa, db.lp, db.lp, db.z, db.lp, c->nsm, c->stream, halt);
+  else
+    launch_xs64_tn(X.x, X.ldx, X.d, X.n, db.sa, db.lp, db.z, db.xs_ws, c->nsm, c->stream, halt);
   launch_gram_cm(a_cm, X.d, k, db.w, db.gram_ws, c->nsm, c->stream, false, halt);
 }
 
@@ -563,6 +581,21 @@ void run_mu_rp(cnmf_context* c, HalsState& st, DenseBufs& db, int64_t iters,
 double recon_error(cnmf_context* c, const XView& X, const double* a_cm, const double* b_cm,
                    int k) {
   double* out = c->ws<double>("err_out", 1);
+  if (X.sp) {  // 0.5|X|^2 - <X, A B^T> + 0.5 tr((A^T A)(B^T B)) (metrics.cpp:79-102)
+    double* ata = c->ws<double>("sp_ata", (size_t)k * k);
+    double* btb = c->ws<double>("sp_btb", (size_t)k * k);
+    double* gws = c->ws<double>("sp_gram_ws", gram_cm_ws_doubles(std::max(X.d, X.n), k, c->nsm));
+    double* ows = c->ws<double>("sp_obj_ws", csr_metrics_ws_doubles(c->nsm));
+    launch_gram_cm(a_cm, X.d, k, ata, gws, c->nsm, c->stream);
+    launch_gram_cm(b_cm, X.n, k, btb, gws, c->nsm, c->stream);
+    launch_csr_objective(*X.sp, a_cm, b_cm, k, c->ws<double>("xnorm", 1), ata, btb, out, ows,
+                         c->nsm, c->stream);
+    CK(cudaGetLastError());
+    double v = 0.0;
+    CK(cudaMemcpyAsync(&v, out, sizeof(double), cudaMemcpyDeviceToHost, c->stream));
+    c->sync();
+    return v;
+  }
   void* ws = c->ws<char>("metrics_ws", metrics_ws_bytes(X.d, X.n, c->nsm));
   launch_recon_error(X.x, X.ldx, X.d, X.n, a_cm, b_cm, k, out, ws, c->nsm, c->stream);
   CK(cudaGetLastError());
@@ -586,9 +619,9 @@ XView prepare_x(cnmf_context* c, const float* x, int64_t d, int64_t n, int64_t l
 }
 
 // --------------------------------------------------------------- run() ------
-void run_device_impl(cnmf_context* c, const float* x_in, int64_t d, int64_t n, int64_t ldx,
-                     const cnmf_solver_config& cfg, float* a_out, float* b_out,
-                     cnmf_run_trace* tr) {
+void run_device_impl(cnmf_context* c, const XView& X, const cnmf_solver_config& cfg,
+                     float* a_out, float* b_out, cnmf_run_trace* tr) {
+  const int64_t d = X.d, n = X.n;
   validate(cfg, d, n);
   // All six solvers of run_impl (solvers.cpp:231-253):
   //  * fasthals-rp on the fused HALS kernels (the north-star path);
@@ -632,7 +665,6 @@ void run_device_impl(cnmf_context* c, const float* x_in, int64_t d, int64_t n, i
     ++t.records_count;
   };
 
-  const XView X = prepare_x(c, x_in, d, n, ldx);
 
   // check_data (solvers.cpp:47-52) + ||X||^2
   {
@@ -640,7 +672,11 @@ void run_device_impl(cnmf_context* c, const float* x_in, int64_t d, int64_t n, i
     double* nrm = c->ws<double>("xnorm", 1);
     void* ws = c->ws<char>("metrics_ws", metrics_ws_bytes(d, n, c->nsm));
     CK(cudaMemsetAsync(flag, 0, sizeof(int), c->stream));
-    launch_check_data(X.x, X.ldx, d, n, flag, nrm, ws, c->nsm, c->stream);
+    if (X.sp)
+      launch_csr_check(*X.sp, flag, nrm, c->ws<double>("sp_check_ws", csr_metrics_ws_doubles(c->nsm)),
+                       c->nsm, c->stream);
+    else
+      launch_check_data(X.x, X.ldx, d, n, flag, nrm, ws, c->nsm, c->stream);
     CK(cudaGetLastError());
     int hflag = 0;
     CK(cudaMemcpyAsync(&hflag, flag, sizeof(int), cudaMemcpyDeviceToHost, c->stream));
@@ -672,8 +708,8 @@ void run_device_impl(cnmf_context* c, const float* x_in, int64_t d, int64_t n, i
   CK(cudaMemsetAsync(omega_r, 0, sizeof(float) * d * lp, c->stream));
   CK(cudaEventRecord(c->ev[2], c->stream));
   int passes = build_projectors_dev(c, X, q, lp, w, cfg.sketch_seed, omega_l, omega_r, lm, rt);
-  launch_xs_tn(X.x, X.ldx, d, n, lm, lp, xht, xs, c->nsm, c->stream);  // X-hat^T = X^T L
-  launch_xs_nn(X.x, X.ldx, d, n, rt, lp, xc, xs, c->nsm, c->stream);   // X-check = X R^T
+  x_times(c, X, true, lm, lp, xht, xs, c->stream);   // X-hat^T = X^T L
+  x_times(c, X, false, rt, lp, xc, xs, c->stream);   // X-check = X R^T
   passes += 2;
   CK(cudaEventRecord(c->ev[3], c->stream));
   CK(cudaGetLastError());
@@ -919,7 +955,79 @@ cnmf_status cnmf_run_device(cnmf_context* c, const float* x, uint64_t d, uint64_
                             cnmf_run_trace* trace) {
   return guarded(c, [&] {
     if (!cfg || !trace || !x || !a || !b) throw Fail(CNMF_ERR_CONFIG, "null argument");
-    run_device_impl(c, x, (int64_t)d, (int64_t)n, (int64_t)ldx, *cfg, a, b, trace);
+    validate(*cfg, d, n);
+    run_device_impl(c, prepare_x(c, x, (int64_t)d, (int64_t)n, (int64_t)ldx), *cfg, a, b, trace);
+  });
+}
+
+cnmf_status cnmf_run_csr(cnmf_context* c, const uint64_t* row_offsets, const uint64_t* col_indices,
+                         const float* values, uint64_t d, uint64_t n,
+                         const cnmf_solver_config* cfg, float* a_out, float* b_out,
+                         cnmf_run_trace* trace) {
+  return guarded(c, [&] {
+    if (!cfg || !trace || !row_offsets || !a_out || !b_out) throw Fail(CNMF_ERR_CONFIG, "null argument");
+    validate(*cfg, d, n);
+    if (n > (uint64_t)INT32_MAX || d > (uint64_t)INT32_MAX)
+      throw Fail(CNMF_ERR_UNSUPPORTED, "sparse input: dimensions must be below 2^31");
+    // structure checks of SparseMatrix::validate (matrix.cpp:37-56); stored
+    // values only need to pass check_data (solvers.cpp:47-52), as in run_impl
+    const uint64_t nnz = row_offsets[d];
+    if (row_offsets[0] != 0)
+      throw Fail(CNMF_ERR_DIMENSION, "sparse matrix: row_offsets endpoints malformed");
+    if (nnz && (!col_indices || !values)) throw Fail(CNMF_ERR_CONFIG, "null argument");
+    for (uint64_t i = 0; i < d; ++i) {
+      if (row_offsets[i] > row_offsets[i + 1])
+        throw Fail(CNMF_ERR_DIMENSION, "sparse matrix: row_offsets must be non-decreasing");
+      for (uint64_t p = row_offsets[i]; p < row_offsets[i + 1]; ++p) {
+        if (col_indices[p] >= n)
+          throw Fail(CNMF_ERR_DIMENSION, "sparse matrix: column index out of range");
+        if (p > row_offsets[i] && col_indices[p] <= col_indices[p - 1])
+          throw Fail(CNMF_ERR_DIMENSION,
+                     "sparse matrix: column indices must be strictly increasing per row");
+      }
+    }
+    // host CSR of X^T: a counting sort by column, rows ascending inside a column
+    std::vector<int64_t> rp(d + 1), trp(n + 1, 0);
+    std::vector<int32_t> ci(nnz), tci(nnz);
+    std::vector<float> tv(nnz);
+    for (uint64_t i = 0; i <= d; ++i) rp[i] = (int64_t)row_offsets[i];
+    for (uint64_t p = 0; p < nnz; ++p) {
+      ci[p] = (int32_t)col_indices[p];
+      ++trp[col_indices[p] + 1];
+    }
+    for (uint64_t j = 0; j < n; ++j) trp[j + 1] += trp[j];
+    {
+      std::vector<int64_t> fill(trp.begin(), trp.end() - 1);
+      for (uint64_t i = 0; i < d; ++i)
+        for (uint64_t p = row_offsets[i]; p < row_offsets[i + 1]; ++p) {
+          const int64_t q = fill[col_indices[p]]++;
+          tci[q] = (int32_t)i;
+          tv[q] = values[p];
+        }
+    }
+    auto up = [&](const char* tag, const void* src, size_t bytes) {
+      void* dst = c->ws<char>(tag, std::max<size_t>(bytes, 16));
+      if (bytes) CK(cudaMemcpyAsync(dst, src, bytes, cudaMemcpyHostToDevice, c->stream));
+      return dst;
+    };
+    CsrView view;  // referenced by the XView for the duration of the run
+    view.d = (int64_t)d;
+    view.n = (int64_t)n;
+    view.nnz = (int64_t)nnz;
+    view.rp = (const int64_t*)up("csr_rp", rp.data(), sizeof(int64_t) * (d + 1));
+    view.ci = (const int32_t*)up("csr_ci", ci.data(), sizeof(int32_t) * nnz);
+    view.v = (const float*)up("csr_v", values, sizeof(float) * nnz);
+    view.t_rp = (const int64_t*)up("csr_trp", trp.data(), sizeof(int64_t) * (n + 1));
+    view.t_ci = (const int32_t*)up("csr_tci", tci.data(), sizeof(int32_t) * nnz);
+    view.t_v = (const float*)up("csr_tv", tv.data(), sizeof(float) * nnz);
+    c->sync();  // the host vectors go out of scope
+    XView X{nullptr, 0, (int64_t)d, (int64_t)n, &view};
+    float* ad = c->ws<float>("a_out_dev", (size_t)d * cfg->k);
+    float* bd = c->ws<float>("b_out_dev", (size_t)n * cfg->k);
+    run_device_impl(c, X, *cfg, ad, bd, trace);
+    CK(cudaMemcpyAsync(a_out, ad, sizeof(float) * d * cfg->k, cudaMemcpyDeviceToHost, c->stream));
+    CK(cudaMemcpyAsync(b_out, bd, sizeof(float) * n * cfg->k, cudaMemcpyDeviceToHost, c->stream));
+    c->sync();
   });
 }
 
@@ -938,7 +1046,7 @@ cnmf_status cnmf_run(cnmf_context* c, const float* x, uint64_t d, uint64_t n, ui
                          cudaMemcpyHostToDevice, c->stream));
     float* ad = c->ws<float>("a_out_dev", (size_t)d * cfg->k);
     float* bd = c->ws<float>("b_out_dev", (size_t)n * cfg->k);
-    run_device_impl(c, xd, (int64_t)d, (int64_t)n, lx, *cfg, ad, bd, trace);
+    run_device_impl(c, prepare_x(c, xd, (int64_t)d, (int64_t)n, lx), *cfg, ad, bd, trace);
     CK(cudaMemcpyAsync(a_out, ad, sizeof(float) * d * cfg->k, cudaMemcpyDeviceToHost, c->stream));
     CK(cudaMemcpyAsync(b_out, bd, sizeof(float) * n * cfg->k, cudaMemcpyDeviceToHost, c->stream));
     c->sync();

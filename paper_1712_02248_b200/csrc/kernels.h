@@ -213,6 +213,33 @@ void launch_mu_update(const double* t_in, int64_t rows, int k, const double* num
 void launch_rows_small64(const float* in, int64_t rows, int l, int lp, const double* m, int k,
                          double* out, int ldo, int nsm, cudaStream_t st);
 
+// ---- sparse.cu: CSR input ------------------------------
+// X (d x n) as CSR plus the CSR of X^T (built on the host), device pointers.
+struct CsrView {
+  int64_t d, n, nnz;
+  const int64_t* rp;    // d + 1 row offsets
+  const int32_t* ci;    // column indices, ascending within a row
+  const float* v;
+  const int64_t* t_rp;  // X^T: n + 1 offsets
+  const int32_t* t_ci;  // row indices, ascending within a column
+  const float* t_v;
+};
+// out (rows x ldo; columns >= l zero) = X S (transpose = false, rows = d) or
+// X^T S (rows = n), S row-major with ld lds; fp64 accumulation.
+void launch_csr_spmm_f32(const CsrView& x, bool transpose, const float* s, int lds, int l,
+                         float* out, int ldo, int nsm, cudaStream_t st);
+void launch_csr_spmm_f64(const CsrView& x, bool transpose, const double* s, int lds, int l,
+                         double* out, int ldo, int nsm, cudaStream_t st,
+                         const int* halt = nullptr);
+size_t csr_metrics_ws_doubles(int nsm);
+// check_data (flag |= negative / non-finite value) and ||X||^2
+void launch_csr_check(const CsrView& x, int* flag, double* norm_sq, double* ws, int nsm,
+                      cudaStream_t st);
+// the sparse objective (metrics.cpp:79-102) given ||X||^2, A^T A and B^T B
+void launch_csr_objective(const CsrView& x, const double* a_cm, const double* b_cm, int k,
+                          const double* xnorm, const double* ata, const double* btb, double* out,
+                          double* ws, int nsm, cudaStream_t st);
+
 // ---- synth.cu: synthetic data (bench harness, BASELINE.json configs) ------
 void launch_synth_x(int64_t d, int64_t n, int rank, int factor_kind, int noise_kind, double sigma,
                     uint64_t seed, int64_t col_lo, int64_t col_hi, int64_t ldx, float* x,

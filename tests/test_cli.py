@@ -264,3 +264,54 @@ def test_artifact_writers_format(tmp_path):
     assert math.isnan(cli.summary_json(cfg, cb.RunTrace([], *([0.0] * 3), 0.0, cb.ABORTED, 0, 0,
                                                         0.0, 0.0, 3, 0.0, 0.0, 0.0, 0, 0,
                                                         "x"))["final_error"])
+
+
+# ------------------------------------------------------------ Matrix Market --
+def _mm(tmp_path, text, name="m.mtx"):
+    p = tmp_path / name
+    p.write_text(text)
+    return str(p)
+
+
+def test_matrix_market_loader_semantics(tmp_path):
+    """load_matrix_market (data_io.cpp:228-288) + sparse_from_triplets
+    (matrix.cpp:58-92): comments before the size line, 1-based entries,
+    duplicates summed, zero sums dropped, rows sorted."""
+    text = ("%%MatrixMarket matrix coordinate real general\n% comment\n\n  % indented\n"
+            "3 4 6\n3 1 2.5\n1 2 1\n1 2 0.5\n2 4 0\n1 1 7\n3 4 1e-3\n")
+    m = cli.load_matrix_market(_mm(tmp_path, text))
+    assert m.shape == (3, 4) and m.nnz == 4
+    assert m.toarray().tolist() == [[7.0, 1.5, 0.0, 0.0], [0.0, 0.0, 0.0, 0.0],
+                                    [2.5, 0.0, 0.0, 1e-3]]
+    assert m.indptr.tolist() == [0, 2, 2, 4]
+    back = cli.load_matrix_market(_mm(tmp_path, cli.save_matrix_market_text(m), "b.mtx"))
+    assert (back != m).nnz == 0
+    ints = "%%MatrixMarket matrix coordinate integer general\n2 2 1\n2 2 5\n"
+    assert cli.load_matrix_market(_mm(tmp_path, ints, "i.mtx")).toarray()[1, 1] == 5.0
+
+
+def test_matrix_market_loader_errors(tmp_path):
+    bad = {
+        "": (cb.ParseError, "missing banner"),
+        "%%MatrixMarket matrix array real general\n2 2\n": (cb.ParseError, "banner"),
+        "%%MatrixMarket matrix coordinate complex general\n": (cb.ParseError, "banner"),
+        "%%MatrixMarket matrix coordinate real symmetric\n": (cb.ParseError, "banner"),
+        "%%MatrixMarket matrix coordinate real general\n% only comments\n":
+            (cb.ParseError, "missing size line"),
+        "%%MatrixMarket matrix coordinate real general\n2 x 1\n": (cb.ParseError, "line 2"),
+        "%%MatrixMarket matrix coordinate real general\n0 2 0\n": (cb.ParseError, "zero"),
+        "%%MatrixMarket matrix coordinate real general\n2 2 2\n1 1 1\n":
+            (cb.ParseError, "after 1 of 2"),
+        "%%MatrixMarket matrix coordinate real general\n2 2 1\n3 1 1\n":
+            (cb.ParseError, "out of range"),
+        "%%MatrixMarket matrix coordinate real general\n2 2 1\n1 1\n": (cb.ParseError, "malformed"),
+        "%%MatrixMarket matrix coordinate real general\n2 2 1\n1 1 x\n": (cb.ParseError, "parse"),
+        "%%MatrixMarket matrix coordinate real general\n2 2 1\n1 1 -2\n": (cb.InputError, "negative"),
+        "%%MatrixMarket matrix coordinate real general\n2 2 1\n1 1 inf\n":
+            (cb.InputError, "non-finite"),
+    }
+    for i, (text, (exc, msg)) in enumerate(bad.items()):
+        with pytest.raises(exc, match=msg):
+            cli.load_matrix_market(_mm(tmp_path, text, f"b{i}.mtx"))
+    with pytest.raises(cb.IoError):
+        cli.load_matrix_market(str(tmp_path / "missing.mtx"))
