@@ -160,38 +160,42 @@ __global__ void __launch_bounds__(128) chol_inv_kernel(const double* __restrict_
                                                        int lp, double* __restrict__ rinv64,
                                                        float* __restrict__ rinv,
                                                        int* __restrict__ flag) {
-  extern __shared__ double gs[];  // l x l (R upper; R^-1 transposed into the lower part), diag0, rd, rdi
-  double* diag0 = gs + l * l;
+  // gs: l rows of stride ls (R upper; R^-1 transposed into the lower part),
+  // then diag0, rd, rdi.  The odd row stride keeps the column-parallel back
+  // substitution (thread c walks row c) free of bank conflicts.
+  extern __shared__ double gs[];
+  const int ls = l | 1;
+  double* diag0 = gs + l * ls;
   double* rd = diag0 + l;
   double* rdi = rd + l;
   const int tid = threadIdx.x, nt = blockDim.x, lane = tid & 31, warp = tid >> 5, nw = nt >> 5;
-  for (int e = tid; e < l * l; e += nt) gs[e] = g[(e / l) * lp + e % l];
+  for (int e = tid; e < l * l; e += nt) gs[(e / l) * ls + e % l] = g[(e / l) * lp + e % l];
   for (int e = tid; e < l; e += nt) diag0[e] = g[e * lp + e];
   __syncthreads();
   for (int j = 0; j < l; ++j) {
-    const double piv = gs[j * l + j];
+    const double piv = gs[j * ls + j];
     if (!(piv > 1e-13 * diag0[j]) || !(piv > 0.0)) {  // uniform across the CTA
       if (tid == 0) *flag = 1;
       return;
     }
     const double ip = 1.0 / piv;
-    const double* rowj = gs + j * l;
+    const double* rowj = gs + j * ls;
     for (int a = j + 1 + warp; a < l; a += nw) {
       const double f = rowj[a] * ip;
-      double* rowa = gs + a * l;
+      double* rowa = gs + a * ls;
       for (int b = a + lane; b < l; b += 32) rowa[b] = fma(-f, rowj[b], rowa[b]);
     }
     __syncthreads();
   }
   for (int j = tid; j < l; j += nt) {
-    const double pj = gs[j * l + j];
+    const double pj = gs[j * ls + j];
     const double ir = 1.0 / sqrt(pj);
     rdi[j] = ir;
     rd[j] = pj * ir;
   }
   __syncthreads();
   for (int i = warp; i < l; i += nw)
-    for (int b = i + 1 + lane; b < l; b += 32) gs[i * l + b] *= rdi[i];
+    for (int b = i + 1 + lane; b < l; b += 32) gs[i * ls + b] *= rdi[i];
   for (int e = tid; e < lp * lp; e += nt) {  // padding and the lower triangle stay zero
     rinv[e] = 0.f;
     rinv64[e] = 0.0;
@@ -200,9 +204,9 @@ __global__ void __launch_bounds__(128) chol_inv_kernel(const double* __restrict_
   // thread c owns column c of R^-1, kept transposed in row c of gs's lower
   // triangle (gs[c][i] = Rinv[i][c], i < c) -- untouched by the factorisation
   for (int c = tid; c < l; c += nt) {
-    double* xc = gs + c * l;
+    double* xc = gs + c * ls;
     for (int i = c - 1; i >= 0; --i) {
-      const double* ri = gs + i * l;
+      const double* ri = gs + i * ls;
       double s0 = ri[c] * rdi[c], s1 = 0.0;  // q = c term
       int q = i + 1;
       for (; q + 1 < c; q += 2) {
@@ -345,11 +349,11 @@ void gram(const float* y, int64_t rows, int l, int lp, const QrWs& w, int nsm,
 }
 
 void chol_inv(int l, int lp, const QrWs& w, cudaStream_t st) {
-  const size_t smem = sizeof(double) * (l * l + 3 * l);
+  const size_t smem = sizeof(double) * (l * (l | 1) + 3 * l);
   static bool attr = false;
   if (!attr) {
     cudaFuncSetAttribute(chol_inv_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                         (int)(sizeof(double) * (128 * 128 + 3 * 128)));
+                         (int)(sizeof(double) * (128 * 129 + 3 * 128)));
     attr = true;
   }
   note_launches(1);
