@@ -447,6 +447,12 @@ void run_dense_hals(cnmf_context* c, HalsRun& hr, const XView& X, DenseBufs& db,
     CK(cudaEventRecord(c->ev[0], c->stream));
     double* b = st.b;
     double* bold = st.bold;
+    // Each queued launch starts at the exchange epoch the launches before it
+    // reach when they run to completion: an A half from column c0 makes k - c0
+    // norm all-reduces, a B half one exchange (a launch that halts instead
+    // turns the rest of the queue into no-ops, and the host resumes from the
+    // halt record's epoch).
+    unsigned long long ep_q = hr.epoch;
     {
       int h0 = half, c0 = col, s0 = skip;
       for (int64_t it = begin; it < ie; ++it) {
@@ -459,8 +465,9 @@ void run_dense_hals(cnmf_context* c, HalsRun& hr, const XView& X, DenseBufs& db,
             dense_prepare_a(c, X, b, k, db, hflag);
           else
             dense_prepare_b(c, X, st.a, k, db, hflag);
-          CK(launch_hals(s2, normalize_a, 0.0, 0.0, (int)it, (int)it + 1, h, c0, s0, hr.epoch,
+          CK(launch_hals(s2, normalize_a, 0.0, 0.0, (int)it, (int)it + 1, h, c0, s0, ep_q,
                          hr.grid, c->stream));
+          ep_q += h == 0 ? (unsigned long long)(k - c0) : 1ULL;
           if (h == 1) std::swap(b, bold);  // the B half leaves the new B in the second buffer
           c0 = 0;
           s0 = -1;
@@ -476,6 +483,8 @@ void run_dense_hals(cnmf_context* c, HalsRun& hr, const XView& X, DenseBufs& db,
     const HaltInfo h = *c->halt_host;
     if (h.last_epoch) hr.epoch = h.last_epoch;
     if (!h.halted) {
+      if (h.last_epoch != ep_q)
+        throw Fail(CNMF_ERR_CUDA, "dense HALS: exchange epoch bookkeeping mismatch");
       st.b = b;
       st.bold = bold;
       break;

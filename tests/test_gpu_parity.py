@@ -617,3 +617,19 @@ def test_run_dense_redraws_match_reference(ctx, reference, algo):
     got = np.array([r.error for r in res.trace.records][:m])
     want = np.array(rt.errors[:m])
     assert np.max(np.abs(got - want) / np.maximum(want, 1e-12 * want[0])) < 1e-3
+
+
+@pytest.mark.parametrize("algo", ["fasthals", "hals", "mu", "fasthals-rp"])
+def test_runs_are_bitwise_reproducible(ctx, oracle, algo):
+    """Every reduction is in a fixed order, and the queued dense half-sweep
+    launches must each start at the right grid-barrier epoch: two identical
+    runs give identical bits (a barrier that passes early shows up here)."""
+    import paper_1712_02248_b200 as cb
+    x = oracle.synth_x(700, 500, 8, 0, 1, 0.01, 9)
+    rp = algo.endswith("-rp")
+    cfg = cb.SolverConfig(algorithm=cb.ALGORITHM_NAMES[algo], k=8,
+                          sketch=cb.SketchConfig(16 if rp else 0, 1, 2), max_iterations=30,
+                          error_interval=10, rel_tolerance=1e-300, seed=5)
+    r1, r2 = ctx.run(x, cfg), ctx.run(x, cfg)
+    assert np.array_equal(r1.a, r2.a) and np.array_equal(r1.b, r2.b)
+    assert [r.error for r in r1.trace.records] == [r.error for r in r2.trace.records]
