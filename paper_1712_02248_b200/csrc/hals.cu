@@ -95,6 +95,17 @@ struct StagePrefetch {
   }
 };
 
+// FP64 tensor-core MMA, D (8 x 8) += A (8 x 4, row) B (4 x 8, col): lane
+// (g = lane / 4, t = lane % 4) supplies A[g][t] and B[t][g] and holds
+// D[g][2t], D[g][2t + 1] (tools/ubench_dmma.cu: 37 TFLOP/s, the DFMA rate,
+// from two operand registers per 256 FMAs instead of shared-memory-bound
+// register tiles).
+__device__ __forceinline__ void dmma(double& d0, double& d1, double a, double b) {
+  asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0, %1}, {%2}, {%3}, {%0, %1};"
+               : "+d"(d0), "+d"(d1)
+               : "d"(a), "d"(b));
+}
+
 // out(r, c) = sum_{q < kdim} In[r, q] M[q, c] (fp64, q ascending) for r < nrows,
 // c < k.  M: shared fp64 (lp x k).  Thread tile: rows rg + 16 i (i < 4) of the
 // stage, columns 4 cg .. 4 cg + 3.
@@ -151,9 +162,9 @@ __device__ void rows_times_small(const float* __restrict__ in, int nrows, int lp
 // ascending order) into part (global lp x k, rows >= l zero).  In: fp32 rows
 // (ld lp), register-prefetched like rows_times_small; F: column-major fp64
 // state (ld ldf), copied by cp.async into a double-buffered row-major stage
-// (fst: 2 x kSR x (k + 1)).  4 x 4 output tiles accumulate in registers
-// across all stages (several passes when l x k needs more than one tile per
-// thread).
+// (fst: 2 x kSR x (k + 1)).  8 x 8 output tiles on the FP64 tensor cores
+// (dmma), up to 8 per warp accumulating in registers across all stages
+// (several passes when l x k needs more tiles than that).
 __device__ __forceinline__ void cp_async8(double* dst, const double* src) {
   asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"(
                    static_cast<uint32_t>(__cvta_generic_to_shared(dst))),
@@ -167,10 +178,13 @@ __device__ void small_partial(const float* __restrict__ in, int nrows, int l, in
                               const double* __restrict__ F, int64_t ldf, double* stage,
                               double* fst, double* /*red*/, double* __restrict__ part,
                               long long* prof = nullptr) {
+  constexpr int kTPW = 8;  // 8 x 8 output tiles per warp per pass over the rows
   long long tp = 0;
   if (prof && threadIdx.x == 0) tp = clock64();
   const int lpp = lp + 1, kp1 = k + 1;
-  const int nbl = (l + 3) >> 2, nbc = (k + 3) >> 2, nb = nbl * nbc;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int g = lane >> 2, t4 = lane & 3;
+  const int nlt = (l + 7) >> 3, nct = (k + 7) >> 3, ntile = nlt * nct;
   const int nst = (nrows + kSR - 1) / kSR;
   const int fsz = kSR * kp1;
   auto copy_f = [&](int r0, double* dst) {  // zero-filled beyond nrows
@@ -181,13 +195,10 @@ __device__ void small_partial(const float* __restrict__ in, int nrows, int l, in
     }
     cp_async_commit();
   };
-  for (int b0 = 0; b0 < nb; b0 += kThreads) {
-    const int b = b0 + threadIdx.x;
-    const bool own = b < nb;
-    const int bl = own ? b / nbc : 0, bc = own ? b - (b / nbc) * nbc : 0;
-    double acc[16];
+  for (int p0 = 0; p0 < ntile; p0 += kTPW * (kThreads / 32)) {
+    double acc[kTPW][2];
 #pragma unroll
-    for (int i = 0; i < 16; ++i) acc[i] = 0.0;
+    for (int u = 0; u < kTPW; ++u) acc[u][0] = acc[u][1] = 0.0;
     StagePrefetch pf;
     __syncthreads();  // previous users of stage / fst are done
     if (nst > 0) {
@@ -210,20 +221,19 @@ __device__ void small_partial(const float* __restrict__ in, int nrows, int l, in
         pf.load(in, r0 + kSR, nrows, lp);
         copy_f(r0 + kSR, fst + ((st + 1) & 1) * fsz);
       }
-      if (own) {
-        // stages are zero-filled past nrows: a fixed trip count the
-        // compiler can unroll and software-pipeline
+      // stages are zero-filled past nrows: a fixed trip count
+#pragma unroll
+      for (int u = 0; u < kTPW; ++u) {
+        const int tI = p0 + warp + (kThreads / 32) * u;
+        if (tI >= ntile) break;  // warp-uniform
+        const int l0 = (tI / nct) * 8, c0 = (tI % nct) * 8;
+        const bool bok = c0 + g < k;
 #pragma unroll 4
-        for (int rr = 0; rr < kSR; ++rr) {
-          double xi[4], fj[4];
-#pragma unroll
-          for (int i = 0; i < 4; ++i) xi[i] = stage[rr * lpp + 4 * bl + i];
-#pragma unroll
-          for (int j = 0; j < 4; ++j) fj[j] = 4 * bc + j < k ? fcur[rr * kp1 + 4 * bc + j] : 0.0;
-#pragma unroll
-          for (int i = 0; i < 4; ++i)
-#pragma unroll
-            for (int j = 0; j < 4; ++j) acc[4 * i + j] = fma(xi[i], fj[j], acc[4 * i + j]);
+        for (int rs = 0; rs < kSR; rs += 4) {
+          const int rr = rs + t4;
+          const double av = stage[rr * lpp + l0 + g];             // A[g][t] = In[rr][l0 + g]
+          const double bv = bok ? fcur[rr * kp1 + c0 + g] : 0.0;  // B[t][g] = F[rr][c0 + g]
+          dmma(acc[u][0], acc[u][1], av, bv);
         }
       }
       if (prof && threadIdx.x == 0) {
@@ -232,14 +242,15 @@ __device__ void small_partial(const float* __restrict__ in, int nrows, int l, in
         tp = t;
       }
     }
-    if (own) {
 #pragma unroll
-      for (int i = 0; i < 4; ++i)
-#pragma unroll
-        for (int j = 0; j < 4; ++j) {
-          const int li = 4 * bl + i, cj = 4 * bc + j;
-          if (li < l && cj < k) part[li * k + cj] = acc[4 * i + j];
-        }
+    for (int u = 0; u < kTPW; ++u) {
+      const int tI = p0 + warp + (kThreads / 32) * u;
+      if (tI >= ntile) break;
+      const int li = (tI / nct) * 8 + g, c = (tI % nct) * 8 + 2 * t4;
+      if (li < l) {
+        if (c < k) part[li * k + c] = acc[u][0];
+        if (c + 1 < k) part[li * k + c + 1] = acc[u][1];
+      }
     }
   }
   for (int e = l * k + threadIdx.x; e < lp * k; e += kThreads) part[e] = 0.0;
