@@ -22,19 +22,20 @@ namespace cnmf {
 
 namespace {
 
-constexpr int kBK = 8;     // reduction depth per stage
-constexpr int kXT = 256;   // threads per X-stream CTA
+constexpr int kBK = 32;    // reduction depth per stage (8 MMA k-steps of 4)
+constexpr int kXT = 256;   // threads per X-stream CTA (8 warps: 4 row groups x 2 column halves)
 constexpr int kNS = 3;     // cp.async pipeline stages
-constexpr int kNNS = 12;   // NN X-tile row stride (floats): conflict-free 16-byte reads
+constexpr int kNNS = kBK + 4;   // NN X-tile row stride (floats): conflict-free fragment reads
+constexpr int kXBM = 128;  // output rows per CTA
+constexpr int kTNS = kXBM + 8;  // TN X-tile row stride (floats)
 
 template <int LP>
 struct Xs64Shape {
-  static constexpr int CG = LP / 16;        // 16-column groups
-  static constexpr int RS = kXT / CG;       // row stride between a thread's 4 rows
-  static constexpr int BM = 4 * RS;         // output rows per CTA
-  // per stage: X tile (fp32; NN [BM][kNNS], TN [kBK][BM]) + S tile (fp64 [kBK][LP])
-  static constexpr int XF = BM * kNNS;      // floats (>= kBK * BM for TN)
-  static constexpr size_t stage_bytes = sizeof(float) * XF + sizeof(double) * kBK * LP;
+  static constexpr int BM = kXBM;
+  static constexpr int TN = LP / 16;        // 8-column MMA tiles per warp (half the columns)
+  static constexpr int SLD = LP + 2;        // S-tile row stride (doubles)
+  static constexpr int XF = (kXBM * kNNS > kBK * kTNS) ? kXBM * kNNS : kBK * kTNS;  // floats
+  static constexpr size_t stage_bytes = sizeof(float) * XF + sizeof(double) * kBK * SLD;
   static constexpr size_t smem = kNS * stage_bytes;
 };
 
@@ -46,8 +47,8 @@ __device__ __forceinline__ void cp_async16(void* dst, const void* src, int src_b
 }
 
 // fp32 -> fp64 on the integer pipe (exact for zero and normal numbers; the
-// FP64 conversion unit issues at 1/4 the DFMA rate and would cost ~25% here).
-// Subnormal inputs take the F2F path.
+// FP64 conversion unit issues at 1/4 the DFMA rate).  Subnormal inputs take
+// the F2F path.
 __device__ __forceinline__ double f2d_int(float f) {
   const uint32_t u = __float_as_uint(f), a = u & 0x7fffffffu;
   if (a < 0x00800000u && a != 0u) return (double)f;
@@ -55,11 +56,23 @@ __device__ __forceinline__ double f2d_int(float f) {
   return __hiloint2double((int)hi, (int)(u << 29));
 }
 
+// FP64 tensor-core MMA, D (8 x 8) += A (8 x 4, row) B (4 x 8, col): lane
+// (g = lane / 4, t = lane % 4) supplies A[g][t], B[t][g] and holds D[g][2t],
+// D[g][2t + 1] (tools/ubench_dmma.cu).
+__device__ __forceinline__ void dmma(double& d0, double& d1, double a, double b) {
+  asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0, %1}, {%2}, {%3}, {%0, %1};"
+               : "+d"(d0), "+d"(d1)
+               : "d"(a), "d"(b));
+}
+
 // out[s][r][c] (s = blockIdx.y split) = sum over the split's K range of
 // op(X)[r][k] S[k][c]; op(X) = X (NN: r < m, K = n) or X^T (TN: r < n, K = m).
-// Thread tile: rows rg + RS i (i < 4) x columns 16 cg .. 16 cg + 15 (threads
-// beyond RS * CG only copy).  X (fp32) and S (fp64) stream through a
-// 3-stage cp.async ring; X is widened to fp64 in registers.
+// On the FP64 tensor cores: warp (wm, wn) owns rows 32 wm .. 32 wm + 31 and
+// columns wn LP/2 .. of the CTA's 128 x LP tile as 4 x LP/16 MMA tiles; per
+// k-step it loads one A value per m-tile (fp32, widened on the integer pipe)
+// and one B value per n-tile -- two operand registers per 256 FMAs, where a
+// SIMT fp64 tile moved 2.5 bytes of shared memory per FMA.  X (fp32) and S
+// (fp64) stream through a 3-stage cp.async ring.
 template <bool kTN, int LP>
 __global__ void __launch_bounds__(kXT, 1) xs64_kernel(const float* __restrict__ x, int64_t ldx,
                                                       int64_t m, int64_t n,
@@ -68,12 +81,13 @@ __global__ void __launch_bounds__(kXT, 1) xs64_kernel(const float* __restrict__ 
                                                       const int* __restrict__ halt) {
   if (halt && *(volatile const int*)halt) return;  // queued behind a HALS halt
   using Sh = Xs64Shape<LP>;
-  constexpr int CG = Sh::CG, RS = Sh::RS, BM = Sh::BM;
+  constexpr int TN = Sh::TN, SLD = Sh::SLD;
   extern __shared__ __align__(16) unsigned char xs64_smem[];
-  const int tid = threadIdx.x, cg = tid % CG, rg = tid / CG;
-  const bool computes = rg < RS;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int g = lane >> 2, t4 = lane & 3;
+  const int wm = warp & 3, wn = warp >> 2;
   const int64_t out_rows = kTN ? n : m, K = kTN ? m : n;
-  const int64_t row0 = (int64_t)blockIdx.x * BM;
+  const int64_t row0 = (int64_t)blockIdx.x * kXBM;
   const int64_t kbeg = (int64_t)blockIdx.y * kchunk, kend = min(K, kbeg + kchunk);
   double* dst = out + (int64_t)blockIdx.y * out_rows * LP;
   auto xbuf = [&](int b) { return reinterpret_cast<float*>(xs64_smem + b * Sh::stage_bytes); };
@@ -83,22 +97,22 @@ __global__ void __launch_bounds__(kXT, 1) xs64_kernel(const float* __restrict__ 
 
   auto issue = [&](int64_t k0, int b) {
     float* xs = xbuf(b);
-    for (int e = tid; e < 2 * BM; e += kXT) {  // 16-byte chunks of X
+    for (int e = tid; e < kXBM * kBK / 4; e += kXT) {  // 16-byte chunks of X
       const float* src = x;
       int bytes = 0;
       float* d;
-      if (!kTN) {  // row e / 2, k quad e % 2
-        const int r = e >> 1, q = e & 1;
+      if (!kTN) {  // row e / 8, k quad e % 8
+        const int r = e >> 3, q = e & 7;
         const int64_t gr = row0 + r, gk = k0 + 4 * q;
         d = xs + r * kNNS + 4 * q;
         if (gr < m && gk < kend) {
           src = x + gr * ldx + gk;
           bytes = (int)(4 * (kend - gk < 4 ? kend - gk : 4));
         }
-      } else {     // k row e / (BM / 4), column quad e % (BM / 4)
-        const int kk = e / (BM / 4), c4 = e % (BM / 4);
+      } else {     // k row e / 32, column quad e % 32
+        const int kk = e >> 5, c4 = e & 31;
         const int64_t gk = k0 + kk, gr = row0 + 4 * c4;
-        d = xs + kk * BM + 4 * c4;
+        d = xs + kk * kTNS + 4 * c4;
         if (gk < kend && gr < n) {
           src = x + gk * ldx + gr;
           bytes = (int)(4 * (n - gr < 4 ? n - gr : 4));
@@ -110,16 +124,15 @@ __global__ void __launch_bounds__(kXT, 1) xs64_kernel(const float* __restrict__ 
     for (int e = tid; e < kBK * LP / 2; e += kXT) {  // 16-byte chunks of S
       const int kk = e / (LP / 2), c2 = e % (LP / 2);
       const int64_t gk = k0 + kk;
-      cp_async16(ss + kk * LP + 2 * c2, gk < kend ? s + gk * LP + 2 * c2 : s,
-                 gk < kend ? 16 : 0);
+      cp_async16(ss + kk * SLD + 2 * c2, gk < kend ? s + gk * LP + 2 * c2 : s, gk < kend ? 16 : 0);
     }
   };
 
-  double acc[4][16];
+  double acc[4][TN][2];
 #pragma unroll
   for (int i = 0; i < 4; ++i)
 #pragma unroll
-    for (int c = 0; c < 16; ++c) acc[i][c] = 0.0;
+    for (int j = 0; j < TN; ++j) acc[i][j][0] = acc[i][j][1] = 0.0;
 
   const int64_t nst = (kend - kbeg + kBK - 1) / kBK;
 #pragma unroll
@@ -132,54 +145,35 @@ __global__ void __launch_bounds__(kXT, 1) xs64_kernel(const float* __restrict__ 
     __syncthreads();  // stage st visible to all; stage st - 1 fully consumed
     if (st + kNS - 1 < nst) issue(kbeg + (st + kNS - 1) * kBK, (int)((st + kNS - 1) % kNS));
     asm volatile("cp.async.commit_group;" ::: "memory");
-    if (!computes) continue;
     const int b = (int)(st % kNS);
     const float* xs = xbuf(b);
-    const double* sb = sbuf(b) + 16 * cg;
+    const double* sb = sbuf(b) + wn * (LP / 2) + g;
 #pragma unroll
-    for (int q = 0; q < kBK / 4; ++q) {
-      double xv[4][4];  // [row][kk in quad]
+    for (int ks = 0; ks < kBK / 4; ++ks) {
+      const int kk = 4 * ks + t4;
+      double av[4], bv[TN];
 #pragma unroll
       for (int i = 0; i < 4; ++i) {
-        float4 f;
-        if (!kTN) {
-          f = *reinterpret_cast<const float4*>(xs + (rg + RS * i) * kNNS + 4 * q);
-        } else {
-          const float* col = xs + rg + RS * i;
-          f = make_float4(col[(4 * q + 0) * BM], col[(4 * q + 1) * BM], col[(4 * q + 2) * BM],
-                          col[(4 * q + 3) * BM]);
-        }
-        xv[i][0] = f2d_int(f.x);
-        xv[i][1] = f2d_int(f.y);
-        xv[i][2] = f2d_int(f.z);
-        xv[i][3] = f2d_int(f.w);
+        const int r = 32 * wm + 8 * i + g;
+        av[i] = f2d_int(kTN ? xs[kk * kTNS + r] : xs[r * kNNS + kk]);
       }
 #pragma unroll
-      for (int t = 0; t < 4; ++t) {
-        const double* srow = sb + (4 * q + t) * LP;
+      for (int j = 0; j < TN; ++j) bv[j] = sb[kk * SLD + 8 * j];
 #pragma unroll
-        for (int c2 = 0; c2 < 8; ++c2) {
-          const double2 sv = reinterpret_cast<const double2*>(srow)[c2];
+      for (int i = 0; i < 4; ++i)
 #pragma unroll
-          for (int i = 0; i < 4; ++i) {
-            acc[i][2 * c2] = fma(xv[i][t], sv.x, acc[i][2 * c2]);
-            acc[i][2 * c2 + 1] = fma(xv[i][t], sv.y, acc[i][2 * c2 + 1]);
-          }
-        }
-      }
+        for (int j = 0; j < TN; ++j) dmma(acc[i][j][0], acc[i][j][1], av[i], bv[j]);
     }
   }
   asm volatile("cp.async.wait_group 0;" ::: "memory");
-  if (computes) {
 #pragma unroll
-    for (int i = 0; i < 4; ++i) {
-      const int64_t r = row0 + rg + RS * i;
-      if (r < out_rows) {
-        double2* o = reinterpret_cast<double2*>(dst + r * LP + 16 * cg);
+  for (int i = 0; i < 4; ++i) {
+    const int64_t r = row0 + 32 * wm + 8 * i + g;
+    if (r < out_rows)
 #pragma unroll
-        for (int c2 = 0; c2 < 8; ++c2) o[c2] = make_double2(acc[i][2 * c2], acc[i][2 * c2 + 1]);
-      }
-    }
+      for (int j = 0; j < TN; ++j)
+        *reinterpret_cast<double2*>(dst + r * LP + wn * (LP / 2) + 8 * j + 2 * t4) =
+            make_double2(acc[i][j][0], acc[i][j][1]);
   }
 }
 
@@ -413,7 +407,7 @@ int gram_grid(int64_t rows, int k, int nsm) {
 
 size_t xs64_ws_doubles(int64_t m, int64_t n, int lp, int nsm) {
   // split-K partials of either orientation, with the launch's own plan
-  const int64_t bm = 4 * (kXT / (lp / 16));
+  const int64_t bm = kXBM;
   size_t most = 0;
   for (int tn = 0; tn < 2; ++tn) {
     const int64_t rows = tn ? n : m, K = tn ? m : n;
