@@ -301,6 +301,8 @@ HalsRun make_hals(cnmf_context* c, int64_t d, int64_t n, int l, int lp, int k,
     CK(cudaMemsetAsync(s.prof, 0, 32 * sizeof(long long), c->stream));
   }
   CK(cudaMemsetAsync(s.bar, 0, 64 * sizeof(unsigned), c->stream));
+  // the norm all-reduce's tagged slots start as +0.0, which no first use accepts
+  CK(cudaMemsetAsync(s.npart, 0, sizeof(double) * 2 * r.grid, c->stream));
   CK(cudaMemsetAsync(s.ahat, 0, sizeof(double) * lp * k, c->stream));
   CK(cudaMemsetAsync(s.bchk, 0, sizeof(double) * lp * k, c->stream));
   r.epoch = 0;  // barriers completed so far (the counter reads epoch * grid)

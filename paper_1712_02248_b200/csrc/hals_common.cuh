@@ -99,6 +99,59 @@ __device__ __forceinline__ void arrive_release(unsigned* bar) {
 #endif
 }
 
+// Tagged slots for the per-column norm all-reduce: the partial (>= 0) is
+// stored with its sign bit set on every other use of its buffer, so one
+// 64-bit store carries both the value and its freshness and the arrival
+// needs no release fence (the counter only says "everyone has written";
+// a reader that still sees last use's sign re-reads that slot).  The first
+// use of a buffer is the negative one: the zeroed slots never match it.
+__device__ __forceinline__ bool tag_neg(unsigned long long ep) { return ((ep >> 1) & 1ULL) == 0; }
+
+__device__ __forceinline__ void st_tagged(double* slot, double v, bool neg) {
+  const double t = neg ? -v : v;
+  asm volatile("st.relaxed.gpu.global.f64 [%0], %1;" ::"l"(slot), "d"(t) : "memory");
+}
+
+__device__ __forceinline__ double ld_relaxed(const double* p) {
+  double v;
+  asm volatile("ld.relaxed.gpu.global.f64 %0, [%1];" : "=d"(v) : "l"(p) : "memory");
+  return v;
+}
+
+// Sum of the G tagged partials (fixed order, as warp_sum_partials), waiting
+// for every slot to carry this use's tag.
+__device__ __forceinline__ double warp_sum_tagged(const double* __restrict__ p, int G, int lane,
+                                                  bool neg) {
+  double t = 0.0;
+  for (int b0 = 0; b0 < G; b0 += 256) {
+    double v[8];
+#pragma unroll
+    for (int i = 0; i < 8; ++i) {
+      const int b = b0 + lane + 32 * i;
+      v[i] = b < G ? ld_relaxed(p + b) : (neg ? -0.0 : 0.0);
+    }
+    for (;;) {
+      bool stale = false;
+#pragma unroll
+      for (int i = 0; i < 8; ++i) {
+        const int b = b0 + lane + 32 * i;
+        if (b < G && (signbit(v[i]) != 0) != neg) {
+          stale = true;
+          v[i] = ld_relaxed(p + b);
+        }
+      }
+      if (!__any_sync(0xffffffffu, stale)) break;
+    }
+#pragma unroll
+    for (int i = 0; i < 8; ++i) t += fabs(v[i]);
+  }
+  return warp_sum(t);
+}
+
+__device__ __forceinline__ void arrive_relaxed(unsigned* bar) {
+  asm volatile("red.relaxed.gpu.global.add.u32 [%0], 1;" ::"l"(bar) : "memory");
+}
+
 // Block + grid all-reduce of one fp64 per thread with two __syncthreads:
 // warp sums -> red8 -> warp 0 sums the warp partials, lane 0 publishes the
 // CTA partial, arrives on the monotonic counter with a release add (no
@@ -122,18 +175,19 @@ __device__ __forceinline__ double allreduce_fused(const HalsState& S, int G, int
   if (wid == 0) {
     if (prof && lane == 0) t1 = clock64();
     double* slot = S.npart + (ep & 1ULL) * G;
+    const bool neg = tag_neg(ep);
     if (lane == 0) {
       double t = 0.0;  // CTA partial: the warp partials in a fixed order
 #pragma unroll
       for (int w = 0; w < kThreads / 32; ++w) t += red8[w];
-      slot[cta] = t;
-      arrive_release(S.bar);
+      st_tagged(slot + cta, t, neg);
+      arrive_relaxed(S.bar);
       if (prof) t2 = clock64();
     }
     // every lane polls (no divergent spin + reconvergence), then reads
     poll_counter_warp(S.bar, (unsigned)(ep * (unsigned long long)G));
     if (prof && lane == 0) t3 = clock64();
-    const double tot = warp_sum_partials(slot, G, lane);
+    const double tot = warp_sum_tagged(slot, G, lane, neg);
     if (lane == 0) {
       s_out[0] = tot;
       s_out[1] = rsqrt_fp64(tot);
