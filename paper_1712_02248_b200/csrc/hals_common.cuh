@@ -25,6 +25,13 @@ __device__ __forceinline__ void poll_counter_warp(const unsigned* bar, unsigned 
   } while (__any_sync(0xffffffffu, (int)(c - target) < 0));
 }
 
+__device__ __forceinline__ void poll_counter_warp_relaxed(const unsigned* bar, unsigned target) {
+  unsigned c;
+  do {
+    asm volatile("ld.relaxed.gpu.global.u32 %0, [%1];" : "=r"(c) : "l"(bar) : "memory");
+  } while (__any_sync(0xffffffffu, (int)(c - target) < 0));
+}
+
 __device__ __forceinline__ void exchange(const HalsState& S, int G, int /*cta*/,
                                          unsigned long long& ep) {
   ++ep;
@@ -184,8 +191,9 @@ __device__ __forceinline__ double allreduce_fused(const HalsState& S, int G, int
       arrive_relaxed(S.bar);
       if (prof) t2 = clock64();
     }
-    // every lane polls (no divergent spin + reconvergence), then reads
-    poll_counter_warp(S.bar, (unsigned)(ep * (unsigned long long)G));
+    // every lane polls (no divergent spin + reconvergence), then reads; the
+    // tags, not acquire ordering, vouch for the slot values
+    poll_counter_warp_relaxed(S.bar, (unsigned)(ep * (unsigned long long)G));
     if (prof && lane == 0) t3 = clock64();
     const double tot = warp_sum_tagged(slot, G, lane, neg);
     if (lane == 0) {
