@@ -286,6 +286,9 @@ HalsRun make_hals(cnmf_context* c, int64_t d, int64_t n, int l, int lp, int k,
                         : hals_resident_grid(s, c->nsm);
   r.resident = rgrid > 0;
   r.grid = r.resident ? rgrid : hals_grid(s, c->nsm);
+  if (!r.resident && (d + r.grid - 1) / r.grid > 6 * 256)
+    throw Fail(CNMF_ERR_UNSUPPORTED,
+               "this build's streaming HALS kernel supports at most 1536 rows of A per SM");
   s.p = c->ws<double>("P_cm", (size_t)k * n);
   s.gsc = c->ws<double>("hals_gsc", (size_t)r.grid * k * k);
   s.wsc = c->ws<double>("hals_wsc", (size_t)r.grid * k * k);

@@ -20,6 +20,8 @@
 // (the reference draws it from the run's host Rng), so the kernel halts at
 // exactly the reference's event point, records it in HaltInfo, and the host
 // draws the column, uploads it and resumes (engine.cpp).
+#include <type_traits>
+
 #include "common.cuh"
 #include "hals_common.cuh"
 #include "kernels.h"
@@ -30,7 +32,11 @@ namespace {
 
 using namespace hals_detail;
 constexpr int kNB = 8;        // columns per block of the blocked sweeps
-constexpr int kMaxRPT = 3;    // A rows per thread (rows per CTA <= 768)
+constexpr int kRB = 3;        // B rows per thread per pass of the B sweep
+// A rows per thread: the A sweep keeps its rows' block state in registers
+// across the per-column grid all-reduces, so the kernel is instantiated for
+// up to 3 (rows per CTA <= 768) or 6 (<= 1536) rows per thread.
+constexpr int kMaxRPTLarge = 6;
 constexpr double kDead = 1e-12;  // solvers.cpp:19
 
 // Precision.  The HALS state (A, B, h = X-check B-check, p = X-hat^T A-hat,
@@ -65,27 +71,30 @@ constexpr int kPF = 8;                  // float4 per thread per stage (lp <= 12
 
 struct StagePrefetch {
   float4 v[kPF];
-  __device__ __forceinline__ void load(const float* __restrict__ in, int r0, int nrows, int lp) {
+  int rr[kPF], c4[kPF];  // this thread's (row, float4 column) per slot; rr = kSR when idle
+  __device__ __forceinline__ void init(int lp) {  // once per product: no per-stage division
     const int q4 = lp >> 2, total = kSR * q4;
 #pragma unroll
     for (int u = 0; u < kPF; ++u) {
       const int e = threadIdx.x + kThreads * u;
+      rr[u] = e < total ? e / q4 : kSR;
+      c4[u] = e < total ? e - rr[u] * q4 : 0;
+    }
+  }
+  __device__ __forceinline__ void load(const float* __restrict__ in, int r0, int nrows, int lp) {
+#pragma unroll
+    for (int u = 0; u < kPF; ++u) {
       v[u] = make_float4(0.f, 0.f, 0.f, 0.f);
-      if (e < total) {
-        const int rr = e / q4, c4 = e - rr * q4;
-        if (r0 + rr < nrows)
-          v[u] = __ldg(reinterpret_cast<const float4*>(in + (int64_t)(r0 + rr) * lp) + c4);
-      }
+      if (rr[u] < kSR && r0 + rr[u] < nrows)
+        v[u] = __ldg(reinterpret_cast<const float4*>(in + (int64_t)(r0 + rr[u]) * lp) + c4[u]);
     }
   }
   __device__ __forceinline__ void store(int lp, double* stage) const {
-    const int lpp = lp + 1, q4 = lp >> 2, total = kSR * q4;
+    const int lpp = lp + 1;
 #pragma unroll
     for (int u = 0; u < kPF; ++u) {
-      const int e = threadIdx.x + kThreads * u;
-      if (e < total) {
-        const int rr = e / q4, c4 = e - rr * q4;
-        double* dd = stage + rr * lpp + 4 * c4;
+      if (rr[u] < kSR) {
+        double* dd = stage + rr[u] * lpp + 4 * c4[u];
         dd[0] = v[u].x;
         dd[1] = v[u].y;
         dd[2] = v[u].z;
@@ -116,6 +125,7 @@ __device__ void rows_times_small(const float* __restrict__ in, int nrows, int lp
   const int ncg = (k + 3) >> 2, ntile = 16 * ncg;
   const int nst = (nrows + kSR - 1) / kSR;
   StagePrefetch pf;
+  pf.init(lp);
   if (nst > 0) pf.load(in, 0, nrows, lp);
   for (int st = 0; st < nst; ++st) {
     const int r0 = st * kSR;
@@ -200,6 +210,7 @@ __device__ void small_partial(const float* __restrict__ in, int nrows, int l, in
 #pragma unroll
     for (int u = 0; u < kTPW; ++u) acc[u][0] = acc[u][1] = 0.0;
     StagePrefetch pf;
+    pf.init(lp);
     __syncthreads();  // previous users of stage / fst are done
     if (nst > 0) {
       pf.load(in, 0, nrows, lp);
@@ -306,6 +317,27 @@ __device__ void gram_to_scratch(const double* __restrict__ M, int l, int k, doub
   __syncthreads();
 }
 
+// g / w in shared memory: k x kg, row stride kg = k rounded up to 8 with zero
+// padding, so a block's 8 coefficients of one row are two aligned 32-byte
+// halves (four 16-byte vector loads, broadcast across the warp).
+__device__ __forceinline__ void load_gram(double* gw, const double* __restrict__ src, int k, int kg,
+                                          bool cg) {
+  for (int e = threadIdx.x; e < k * kg; e += kThreads) {
+    const int r = e / kg, c = e - r * kg;
+    gw[e] = c < k ? (cg ? __ldcg(src + r * k + c) : src[r * k + c]) : 0.0;
+  }
+}
+__device__ __forceinline__ void load8(const double* p, double (&v)[8]) {
+  const double2* q = reinterpret_cast<const double2*>(p);
+#pragma unroll
+  for (int u = 0; u < 4; ++u) {
+    const double2 t = q[u];
+    v[2 * u] = t.x;
+    v[2 * u + 1] = t.y;
+  }
+}
+
+template <int RPT>
 __global__ void __launch_bounds__(kThreads, 1) hals_kernel(const HalsArgs p) {
   extern __shared__ __align__(16) double smem[];
   __shared__ double red8[kThreads / 32];
@@ -318,7 +350,7 @@ __global__ void __launch_bounds__(kThreads, 1) hals_kernel(const HalsArgs p) {
 
   const HalsState& S = p.st;
   const int G = gridDim.x, cta = blockIdx.x, tid = threadIdx.x;
-  const int k = S.k, lp = S.lp, l = S.l, kp1 = k + 1, lpp = lp + 1;
+  const int k = S.k, lp = S.lp, l = S.l, kp1 = k + 1, lpp = lp + 1, kg = (k + 7) & ~7;
   const int64_t d = S.d, n = S.n;
   const int64_t a_lo = min(d, (int64_t)cta * p.rows_a), a_hi = min(d, a_lo + p.rows_a);
   const int64_t b_lo = min(n, (int64_t)cta * p.rows_b), b_hi = min(n, b_lo + p.rows_b);
@@ -353,13 +385,13 @@ __global__ void __launch_bounds__(kThreads, 1) hals_kernel(const HalsArgs p) {
   double* bcur = S.b;  // B as of the start of the B half
   double* bnxt = S.bold;
   int half = p.start_half, col0 = p.start_col, skip = p.skip_dead;
-  const int rpt = (na + kThreads - 1) / kThreads;  // <= kMaxRPT (hals_grid)
+  const int rpt = (na + kThreads - 1) / kThreads;  // <= RPT (launch_hals)
 
   for (int it = p.it_begin; it < p.it_end; ++it) {
     if (half == 0) {
       // ================= A half (solvers.cpp:419-439) =====================
       if (S.dense) {  // p = X B, g = B^T B prepared by the host (solvers.cpp:154-155)
-        for (int e = tid; e < k * k; e += kThreads) gw[e] = __ldcg(S.gd + e);
+        load_gram(gw, S.gd, k, kg, true);
       } else {
         if (!have_g) gram_to_scratch(S.bchk, l, k, smem, gsc);
         // h = X-check B-check for this CTA's rows (solvers.cpp:421)
@@ -367,12 +399,12 @@ __global__ void __launch_bounds__(kThreads, 1) hals_kernel(const HalsArgs p) {
         HALS_PROF(0);
         rows_times_small(S.xc + a_lo * lp, na, lp, l, k, Ms, stage64,
                          [&](int r, int c, double v) { S.h[(int64_t)c * d + a_lo + r] = v; });
-        for (int e = tid; e < k * k; e += kThreads) gw[e] = gsc[e];
+        load_gram(gw, gsc, k, kg, false);
       }
       __syncthreads();
       for (int e = tid; e < k; e += kThreads) {
-        s_diag[e] = gw[e * k + e];
-        s_ginv[e] = 1.0 / gw[e * k + e];
+        s_diag[e] = gw[e * kg + e];
+        s_ginv[e] = 1.0 / gw[e * kg + e];
       }
       __syncthreads();
       HALS_PROF(1);
@@ -383,76 +415,73 @@ __global__ void __launch_bounds__(kThreads, 1) hals_kernel(const HalsArgs p) {
         if (j != skip && s_diag[j] < kDead) { jd = j; break; }
       skip = -1;
       // Blocked column sweep (solvers.cpp:423-437).  Thread owns rows
-      // tid + 256 i.  Per block of kNB columns: acc = A g[:, block] with the
-      // current A; inside the block each update adds the fp64 deltas of the
-      // block's earlier columns.  One all-reduce per column for the norm.
-      for (int jb = col0; jb < jd; jb += kNB) {
-        const int nbj = min(kNB, jd - jb);
-        double acc[kMaxRPT][kNB], dl[kMaxRPT][kNB];
+      // tid + 256 i.  Blocks are 8-aligned columns [jb, jb + 8) (the first
+      // one starts at col0 after a resume).  Per block: acc = A g[:, block]
+      // with the current A; when a column is final its delta is folded into
+      // the block's later accumulators (the reference's running A g_j, with
+      // the same fp64 operation order as summing the deltas per column).
+      // One all-reduce per column for the norm.
+      for (int jb = col0 & ~(kNB - 1); jb < jd; jb += kNB) {
+        const int t0 = max(col0 - jb, 0), nbj = min(kNB, jd - jb);
+        double acc[RPT][kNB];
 #pragma unroll
-        for (int i = 0; i < kMaxRPT; ++i)
+        for (int i = 0; i < RPT; ++i)
 #pragma unroll
-          for (int t = 0; t < kNB; ++t) {
-            acc[i][t] = 0.0;
-            dl[i][t] = 0.0;
-          }
-        for (int c0 = 0; c0 < k; c0 += 8) {  // 8 columns of A in flight per row
-          double av8[kMaxRPT][8];
+          for (int t = 0; t < kNB; ++t) acc[i][t] = 0.0;
+        for (int c0 = 0; c0 < k; c0 += 4) {  // 4 columns of A in flight per row
+          double av4[RPT][4];
 #pragma unroll
-          for (int i = 0; i < kMaxRPT; ++i) {
+          for (int i = 0; i < RPT; ++i) {
             const int r = tid + kThreads * i;
             const bool ok = i < rpt && r < na;
 #pragma unroll
-            for (int cc = 0; cc < 8; ++cc)
-              av8[i][cc] = (ok && c0 + cc < k) ? __ldcg(S.a + (int64_t)(c0 + cc) * d + a_lo + r) : 0.0;
+            for (int cc = 0; cc < 4; ++cc)
+              av4[i][cc] = (ok && c0 + cc < k) ? __ldcg(S.a + (int64_t)(c0 + cc) * d + a_lo + r) : 0.0;
           }
 #pragma unroll
-          for (int cc = 0; cc < 8; ++cc) {
+          for (int cc = 0; cc < 4; ++cc) {
             if (c0 + cc >= k) break;
-            double gv[kNB];
+            double gv[kNB];  // padded columns (>= k) are zero
+            load8(gw + (c0 + cc) * kg + jb, gv);
 #pragma unroll
-            for (int t = 0; t < kNB; ++t) gv[t] = t < nbj ? gw[(c0 + cc) * k + jb + t] : 0.0;
+            for (int i = 0; i < RPT; ++i)
 #pragma unroll
-            for (int i = 0; i < kMaxRPT; ++i)
-#pragma unroll
-              for (int t = 0; t < kNB; ++t) acc[i][t] = fma(av8[i][cc], gv[t], acc[i][t]);
+              for (int t = 0; t < kNB; ++t) acc[i][t] = fma(av4[i][cc], gv[t], acc[i][t]);
           }
         }
-        double hv[kMaxRPT], av[kMaxRPT];
+        double hv[RPT], av[RPT];
 #pragma unroll
-        for (int i = 0; i < kMaxRPT; ++i) {
+        for (int i = 0; i < RPT; ++i) {
           const int r = tid + kThreads * i;
           const bool ok = i < rpt && r < na;
-          hv[i] = ok ? (S.dense ? __ldcg(S.hd + (a_lo + r) * lp + jb)
-                                : __ldcg(S.h + (int64_t)jb * d + a_lo + r))
+          const int j = jb + t0;
+          hv[i] = ok ? (S.dense ? __ldcg(S.hd + (a_lo + r) * lp + j)
+                                : __ldcg(S.h + (int64_t)j * d + a_lo + r))
                      : 0.0;
-          av[i] = ok ? __ldcg(S.a + (int64_t)jb * d + a_lo + r) : 0.0;
+          av[i] = ok ? __ldcg(S.a + (int64_t)j * d + a_lo + r) : 0.0;
         }
         HALS_PROF(2);
 #pragma unroll
         for (int t = 0; t < kNB; ++t) {
+          if (t < t0) continue;
           if (t >= nbj) break;
           const int j = jb + t;
           const double ginv = s_ginv[j];
-          double nrm = 0.0, vv[kMaxRPT];
+          double nrm = 0.0, vv[RPT];
 #pragma unroll
-          for (int i = 0; i < kMaxRPT; ++i) {
+          for (int i = 0; i < RPT; ++i) {
             vv[i] = 0.0;
             const int r = tid + kThreads * i;
             if (i < rpt && r < na) {  // solvers.cpp:430-434
-              double s = acc[i][t];
-#pragma unroll
-              for (int u = 0; u < kNB; ++u)
-                if (u < t) s = fma(dl[i][u], gw[(jb + u) * k + j], s);
-              const double v = av[i] + (hv[i] - s) * ginv;
+              const double v = av[i] + (hv[i] - acc[i][t]) * ginv;
               vv[i] = v > 0.0 ? v : 0.0;
               nrm = fma(vv[i], vv[i], nrm);
             }
           }
           // prefetch the next column's h and a while the norm is reduced
-          double hn[kMaxRPT], an[kMaxRPT];
+          double hn[RPT], an[RPT];
 #pragma unroll
-          for (int i = 0; i < kMaxRPT; ++i) {
+          for (int i = 0; i < RPT; ++i) {
             const int r = tid + kThreads * i;
             const bool ok = i < rpt && r < na && t + 1 < nbj;
             hn[i] = ok ? (S.dense ? __ldcg(S.hd + (a_lo + r) * lp + j + 1)
@@ -465,7 +494,7 @@ __global__ void __launch_bounds__(kThreads, 1) hals_kernel(const HalsArgs p) {
           HALS_PROF(3);
           if (total == 0.0) {  // column emptied: host redraws a_j (solvers.cpp:435)
 #pragma unroll
-            for (int i = 0; i < kMaxRPT; ++i) {
+            for (int i = 0; i < RPT; ++i) {
               const int r = tid + kThreads * i;
               if (i < rpt && r < na) S.a[(int64_t)j * d + a_lo + r] = 0.0;
             }
@@ -474,13 +503,18 @@ __global__ void __launch_bounds__(kThreads, 1) hals_kernel(const HalsArgs p) {
             return;
           }
           const double inv_nrm = s_red[1];
+          double gr[kNB];  // row j of g: the later columns' coefficients of a_j
+          load8(gw + j * kg + jb, gr);
 #pragma unroll
-          for (int i = 0; i < kMaxRPT; ++i) {
+          for (int i = 0; i < RPT; ++i) {
             const int r = tid + kThreads * i;
             if (i < rpt && r < na) {  // solvers.cpp:436
               const double nf = p.normalize_a ? vv[i] * inv_nrm : vv[i];
               S.a[(int64_t)j * d + a_lo + r] = nf;
-              dl[i][t] = nf - av[i];
+              const double dlt = nf - av[i];
+#pragma unroll
+              for (int u = 0; u < kNB; ++u)
+                if (u > t) acc[i][u] = fma(dlt, gr[u], acc[i][u]);
             }
             hv[i] = hn[i];
             av[i] = an[i];
@@ -519,18 +553,18 @@ __global__ void __launch_bounds__(kThreads, 1) hals_kernel(const HalsArgs p) {
     }
     // ================== B half (solvers.cpp:440-455) =======================
     if (S.dense) {  // p = X^T A, w = A^T A prepared by the host (solvers.cpp:175-176)
-      for (int e = tid; e < k * k; e += kThreads) gw[e] = __ldcg(S.wd + e);
+      load_gram(gw, S.wd, k, kg, true);
     } else {
       if (!have_w) gram_to_scratch(S.ahat, l, k, smem, wsc);
       // p = X-hat^T A-hat for this CTA's rows (solvers.cpp:442)
       for (int e = tid; e < lp * k; e += kThreads) Ms[e] = __ldcg(S.ahat + e);
       rows_times_small(S.xht + b_lo * lp, nbr, lp, l, k, Ms, stage64,
                        [&](int r, int c, double v) { S.p[(int64_t)c * n + b_lo + r] = v; });
-      for (int e = tid; e < k * k; e += kThreads) gw[e] = wsc[e];
+      load_gram(gw, wsc, k, kg, false);
     }
     if (tid < 4) zmask[tid] = 0u;
     __syncthreads();
-    for (int e = tid; e < k; e += kThreads) s_diag[e] = gw[e * k + e];
+    for (int e = tid; e < k; e += kThreads) s_diag[e] = gw[e * kg + e];
     __syncthreads();
     int jd = k;
     for (int j = col0; j < k; ++j)
@@ -542,61 +576,100 @@ __global__ void __launch_bounds__(kThreads, 1) hals_kernel(const HalsArgs p) {
       for (int r = tid; r < nbr; r += kThreads)
         bnxt[(int64_t)c * n + b_lo + r] = bcur[(int64_t)c * n + b_lo + r];
     const bool constrained = !(p.alpha == 0.0 && p.beta == 0.0);
-    for (int r = tid; r < nbr; r += kThreads) {  // one row per thread, rows are independent
-      const int64_t gr = b_lo + r;
-      for (int jb = col0; jb < jd; jb += kNB) {
-        const int nbj = min(kNB, jd - jb);
-        double acc[kNB], dl[kNB];
-#pragma unroll
-        for (int t = 0; t < kNB; ++t) {
-          acc[t] = 0.0;
-          dl[t] = 0.0;
+    // Rows are independent: kRB rows per thread per pass (rows rb0 + tid +
+    // 256 i), 8-aligned column blocks as in the A half, deltas folded into
+    // the block's later accumulators, zero-column flags by warp ballot.
+    // (RB = 1 when the CTA has at most 256 rows: no idle row slots)
+    auto b_sweep = [&](auto rb_const) {
+      constexpr int RB = decltype(rb_const)::value;
+      for (int rb0 = 0; rb0 < nbr; rb0 += kThreads * RB) {  // CTA-uniform trip count
+        int64_t gr[RB];
+        bool okr[RB];
+  #pragma unroll
+        for (int i = 0; i < RB; ++i) {
+          const int r = rb0 + tid + kThreads * i;
+          okr[i] = r < nbr;
+          gr[i] = b_lo + (okr[i] ? r : 0);
         }
-        for (int c0 = 0; c0 < k; c0 += 8) {  // columns < jb already live in bnxt
-          double bv8[8];
-#pragma unroll
-          for (int cc = 0; cc < 8; ++cc) {
-            const int c = c0 + cc;
-            bv8[cc] = c < k ? __ldcg((c < jb ? bnxt : bcur) + (int64_t)c * n + gr) : 0.0;
+        for (int jb = col0 & ~(kNB - 1); jb < jd; jb += kNB) {
+          const int t0 = max(col0 - jb, 0), nbj = min(kNB, jd - jb);
+          const int jbe = jb + t0;  // columns < jbe already live in bnxt
+          double acc[RB][kNB];
+  #pragma unroll
+          for (int i = 0; i < RB; ++i)
+  #pragma unroll
+            for (int t = 0; t < kNB; ++t) acc[i][t] = 0.0;
+          for (int c0 = 0; c0 < k; c0 += 4) {
+            double bv4[RB][4];
+  #pragma unroll
+            for (int i = 0; i < RB; ++i)
+  #pragma unroll
+              for (int cc = 0; cc < 4; ++cc) {
+                const int c = c0 + cc;
+                bv4[i][cc] = (okr[i] && c < k) ? __ldcg((c < jbe ? bnxt : bcur) + (int64_t)c * n + gr[i]) : 0.0;
+              }
+  #pragma unroll
+            for (int cc = 0; cc < 4; ++cc) {
+              if (c0 + cc >= k) break;
+              double gv[kNB];
+              load8(gw + (c0 + cc) * kg + jb, gv);
+  #pragma unroll
+              for (int i = 0; i < RB; ++i)
+  #pragma unroll
+                for (int t = 0; t < kNB; ++t) acc[i][t] = fma(bv4[i][cc], gv[t], acc[i][t]);
+            }
           }
-#pragma unroll
-          for (int cc = 0; cc < 8; ++cc) {
-            if (c0 + cc >= k) break;
-#pragma unroll
-            for (int t = 0; t < kNB; ++t)
-              if (t < nbj) acc[t] = fma(bv8[cc], gw[(c0 + cc) * k + jb + t], acc[t]);
+          // b and p of the next column are loaded one step ahead: the column
+          // chain waits on arithmetic only
+          double bb[RB], pb[RB];
+          auto load_bp = [&](int j, double (&bo)[RB], double (&po)[RB]) {
+  #pragma unroll
+            for (int i = 0; i < RB; ++i) {
+              const bool ok = okr[i] && j < jb + nbj;
+              bo[i] = ok ? __ldcg(bcur + (int64_t)j * n + gr[i]) : 0.0;
+              po[i] = ok ? (S.dense ? __ldcg(S.pd + gr[i] * lp + j) : __ldcg(S.p + (int64_t)j * n + gr[i]))
+                         : 0.0;
+            }
+          };
+          load_bp(jbe, bb, pb);
+  #pragma unroll
+          for (int t = 0; t < kNB; ++t) {
+            if (t < t0) continue;
+            if (t >= nbj) break;
+            const int j = jb + t;
+            const double wjj = s_diag[j];
+            double bn[RB], pn[RB];
+            load_bp(j + 1, bn, pn);
+            double grow[kNB];
+            load8(gw + j * kg + jb, grow);
+            bool nz = false;
+  #pragma unroll
+            for (int i = 0; i < RB; ++i) {
+              const double s = acc[i][t];
+              const double bij = bb[i];
+              const double pij = pb[i];
+              const double v = constrained ? (bij * wjj + pij - s - p.alpha) / (wjj + p.beta)  // 502-508
+                                           : bij + (pij - s) / wjj;                            // 480-490
+              const double vf = v > 0.0 ? v : 0.0;
+              if (okr[i]) {
+                bnxt[(int64_t)j * n + gr[i]] = vf;
+                nz |= vf != 0.0;
+              }
+              const double dlt = vf - bij;
+  #pragma unroll
+              for (int u = 0; u < kNB; ++u)
+                if (u > t) acc[i][u] = fma(dlt, grow[u], acc[i][u]);
+              bb[i] = bn[i];
+              pb[i] = pn[i];
+            }
+            const unsigned bal = __ballot_sync(0xffffffffu, nz);
+            if ((tid & 31) == 0 && bal) atomicOr(&zmask[j >> 5], 1u << (j & 31));
           }
-        }
-        // the block's b and p values are loaded up front: the column chain
-        // below then waits on arithmetic only
-        double bb[kNB], pb[kNB];
-#pragma unroll
-        for (int t = 0; t < kNB; ++t) {
-          const int j = jb + t;
-          bb[t] = t < nbj ? __ldcg(bcur + (int64_t)j * n + gr) : 0.0;
-          pb[t] = t < nbj ? (S.dense ? __ldcg(S.pd + gr * lp + j) : __ldcg(S.p + (int64_t)j * n + gr))
-                          : 0.0;
-        }
-#pragma unroll
-        for (int t = 0; t < kNB; ++t) {
-          if (t >= nbj) break;
-          const int j = jb + t;
-          double s = acc[t];
-#pragma unroll
-          for (int u = 0; u < kNB; ++u)
-            if (u < t) s = fma(dl[u], gw[(jb + u) * k + j], s);
-          const double wjj = s_diag[j];
-          const double bij = bb[t];
-          const double pij = pb[t];
-          const double v = constrained ? (bij * wjj + pij - s - p.alpha) / (wjj + p.beta)  // 502-508
-                                       : bij + (pij - s) / wjj;                            // 480-490
-          const double vf = v > 0.0 ? v : 0.0;
-          bnxt[(int64_t)j * n + gr] = vf;
-          dl[t] = vf - bij;
-          if (vf != 0.0) atomicOr(&zmask[j >> 5], 1u << (j & 31));
         }
       }
-    }
+    };
+    if (nbr <= kThreads) b_sweep(std::integral_constant<int, 1>{});
+    else b_sweep(std::integral_constant<int, kRB>{});
     __syncthreads();
     HALS_PROF(10);
     if (tid < 4) S.zpart[cta * 4 + tid] = zmask[tid];
@@ -678,7 +751,7 @@ size_t hals_smem_bytes(const HalsState& st, int /*rows_a*/) {
   const int64_t k = st.k, lp = st.lp, l = st.l, kp1 = k + 1, lpp = lp + 1;
   const int64_t k4 = (k + 3) & ~3;
   const int64_t prod = lp * k + 64 * lpp;
-  const int64_t sweep = k * k;
+  const int64_t sweep = k * ((k + 7) & ~7);
   const int64_t part = kSR * lpp + 2 * kSR * kp1;  // X stage + double-buffered F stage
   const int64_t gram = l * k4;
   return (size_t)std::max(std::max(prod, sweep), std::max(part, gram)) * sizeof(double);
@@ -744,13 +817,15 @@ cudaError_t launch_hals(const HalsState& st, int normalize_a, double alpha, doub
   a.rows_b = rows_per_cta(st.n, grid);
   const size_t smem = hals_smem_bytes(st, a.rows_a);
   if (smem > 227 * 1024) return cudaErrorInvalidConfiguration;
-  cudaError_t e =
-      cudaFuncSetAttribute(hals_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  // rows per thread of the A sweep (register-resident across the column chain)
+  const int rpt = (a.rows_a + kThreads - 1) / kThreads;
+  if (rpt > kMaxRPTLarge) return cudaErrorInvalidConfiguration;
+  const void* fn = rpt <= 3 ? (const void*)hals_kernel<3> : (const void*)hals_kernel<kMaxRPTLarge>;
+  cudaError_t e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   if (e != cudaSuccess) return e;
   void* args[] = {&a};
   note_launches(1);
-  return cudaLaunchCooperativeKernel((const void*)hals_kernel, dim3(grid), dim3(kThreads), args,
-                                     smem, s);
+  return cudaLaunchCooperativeKernel(fn, dim3(grid), dim3(kThreads), args, smem, s);
 }
 
 void launch_compress_factors(const HalsState& st, int which, int column, cudaStream_t s) {

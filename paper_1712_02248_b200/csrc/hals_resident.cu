@@ -9,6 +9,8 @@
 // and the only global traffic is the per-column norm all-reduce and the
 // A-hat / B-check partials.  A and B are written back when the launch ends
 // or halts.
+#include <cstdlib>
+
 #include "common.cuh"
 #include "hals_common.cuh"
 #include "kernels.h"
@@ -471,6 +473,13 @@ __global__ void __launch_bounds__(kThreads, 1) hals_resident_kernel(const ResArg
 }  // namespace
 
 int hals_resident_grid(const HalsState& st, int nsm) {
+  if (const char* e = std::getenv("CNMF_RES_GRID")) {  // experiments only (tools/)
+    const int g = std::atoi(e);
+    const int ra = (int)((st.d + g - 1) / g), rb = (int)((st.n + g - 1) / g);
+    if (g >= 1 && g <= nsm && ra <= kThreads && rb <= kThreads &&
+        res_layout(ra, rb, st.lp, st.k).total * (int64_t)sizeof(double) <= 220 * 1024)
+      return g;
+  }
   for (int g = std::max(1, (int)((std::max(st.d, st.n) + kThreads - 1) / kThreads)); g <= nsm;
        ++g) {
     const int ra = (int)((st.d + g - 1) / g), rb = (int)((st.n + g - 1) / g);

@@ -28,6 +28,7 @@
 #include <cudaTypedefs.h>
 
 #include <cstdlib>
+#include <utility>
 
 #include "common.cuh"
 #include "kernels.h"
@@ -332,6 +333,10 @@ __global__ void __launch_bounds__(kThreadsTC, 1)
     }
   } else if (warp == kWarpBTMA) {
     // ---------------- S producer (L2-resident small operand) ----------------
+    // This kernel is a programmatic dependent launch behind the S split
+    // kernel: everything else (TMEM, barriers, the X stream into the ring and
+    // the X splits) starts while the split runs; only S waits for it.
+    asm volatile("griddepcontrol.wait;" ::: "memory");
     if (lane == 0) {
       int nblk = 0;
       int b = 0;
@@ -544,6 +549,7 @@ __global__ void __launch_bounds__(kThreadsTC, 1)
 // split so the tensor core's truncation of the operands is exact.
 __global__ void split_tf32_kernel(const float* __restrict__ s, int64_t rows, int lp, int L,
                                   float* __restrict__ hi, float* __restrict__ lo) {
+  asm volatile("griddepcontrol.launch_dependents;");
   for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < rows * L;
        e += (int64_t)gridDim.x * blockDim.x) {
     const int64_t r = e / L;
@@ -560,6 +566,9 @@ __global__ void split_tf32_kernel(const float* __restrict__ s, int64_t rows, int
 
 __global__ void tc_split_reduce_kernel(const float4* __restrict__ part, int splits, int64_t total4,
                                        float4* __restrict__ out) {
+  // programmatic dependent launch behind xs_tc_kernel: launched while its
+  // last CTAs drain, reads the partials only once it has completed
+  asm volatile("griddepcontrol.wait;" ::: "memory");
   for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < total4;
        e += (int64_t)gridDim.x * blockDim.x) {
     float4 acc = part[e];
@@ -602,6 +611,25 @@ bool make_map(CUtensorMap* m, const float* base, int64_t rows, int64_t cols, int
   return fn(m, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2, const_cast<float*>(base), dims, strides, box,
             estr, CU_TENSOR_MAP_INTERLEAVE_NONE, sw, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
             CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+}
+
+// Launch with programmatic stream serialization (PDL): the kernel may start
+// before its predecessor in the stream completes; it must execute
+// griddepcontrol.wait before touching anything that predecessor writes.
+template <typename... KArgs, typename... Args>
+cudaError_t launch_pdl(void (*kern)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t st,
+                       Args&&... args) {
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = grid;
+  cfg.blockDim = block;
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = st;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  return cudaLaunchKernelEx(&cfg, kern, std::forward<Args>(args)...);
 }
 
 struct TcPlan {
@@ -650,8 +678,8 @@ cudaError_t run_tc(const CUtensorMap& mx, const CUtensorMap& mh, const CUtensorM
     attr = true;
   }
   note_launches(1);
-  xs_tc_kernel<kTN, L><<<grid, kThreadsTC, smem, st>>>(mx, mh, ml, a);
-  return cudaGetLastError();
+  return launch_pdl(xs_tc_kernel<kTN, L>, dim3(grid), dim3(kThreadsTC), (size_t)smem, st, mx, mh,
+                    ml, a);
 }
 
 }  // namespace
@@ -713,9 +741,11 @@ bool launch_xs_tc(bool tn, const float* x, int64_t ldx, int64_t m, int64_t n, co
   if (p.nsplit > 1) {
     const int64_t total4 = rows_out * lp / 4;
     note_launches(1);
-    tc_split_reduce_kernel<<<(int)std::min<int64_t>((total4 + 255) / 256, (int64_t)nsm * 8), 256,
-                             0, st>>>(reinterpret_cast<const float4*>(parts), p.nsplit, total4,
-                                      reinterpret_cast<float4*>(out));
+    if (launch_pdl(tc_split_reduce_kernel,
+                   dim3((int)std::min<int64_t>((total4 + 255) / 256, (int64_t)nsm * 8)), dim3(256),
+                   0, st, reinterpret_cast<const float4*>(parts), p.nsplit, total4,
+                   reinterpret_cast<float4*>(out)) != cudaSuccess)
+      return false;
   }
   return true;
 }
