@@ -475,6 +475,7 @@ __global__ void __launch_bounds__(kThreadsTC, 1)
         // (tools/tc_units.cu found block b computed with block b + kXStages).
         if (lane == 0) mbar_arrive(&xempty[s]);
         if (q == 0 && lane == 0) TC_EV(3, nblk);
+        if (lane == 0) TC_EV(8 + q, nblk);  // per-quarter split done (tools/tc_trace.cu)
         ++nblk;
         if (++s == kSX) {
           s = 0;

@@ -15,11 +15,11 @@ int main(int argc, char** argv) {
   for (size_t i = 0; i < s.size(); ++i) s[i] = (float)((i * 40503u) % 2000) / 1000.f - 1.f;
   float *dx, *ds, *dy, *dw, *dbg;
   cudaMalloc(&dx, x.size() * 4); cudaMalloc(&ds, s.size() * 4); cudaMalloc(&dy, m * lp * 4);
-  cudaMalloc(&dw, xstream_tc_ws_floats(m, n, lp, 148) * 4); cudaMalloc(&dbg, 8 * 4096 * 8);
+  cudaMalloc(&dw, xstream_tc_ws_floats(m, n, lp, 148) * 4); cudaMalloc(&dbg, 12 * 4096 * 8);
   cudaMemcpy(dx, x.data(), x.size() * 4, cudaMemcpyHostToDevice);
   cudaMemcpy(ds, s.data(), s.size() * 4, cudaMemcpyHostToDevice);
   launch_xs_tc(false, dx, n, m, n, ds, lp, dy, dw, 148, 0);  // warm
-  cudaMemset(dbg, 0, 8 * 4096 * 8);
+  cudaMemset(dbg, 0, 12 * 4096 * 8);
   xstream_tc_set_debug(dbg);
   cudaEvent_t e0, e1; cudaEventCreate(&e0); cudaEventCreate(&e1);
   cudaEventRecord(e0);
@@ -27,7 +27,7 @@ int main(int argc, char** argv) {
   cudaEventRecord(e1);
   cudaDeviceSynchronize();
   float ms; cudaEventElapsedTime(&ms, e0, e1);
-  std::vector<unsigned long long> t(8 * 4096);
+  std::vector<unsigned long long> t(12 * 4096);
   cudaMemcpy(t.data(), dbg, t.size() * 8, cudaMemcpyDeviceToHost);
   int nb = 0; while (nb < 4096 && t[5 * 4096 + nb]) ++nb;
   printf("%.1f us, %.0f GB/s; CTA0 blocks %d\n", ms * 1e3, 4.0 * m * n / (ms * 1e-3) / 1e9, nb);
@@ -49,5 +49,11 @@ int main(int argc, char** argv) {
   }
   printf("steady-state means (cycles): X latency %.0f, split waits A slot %.0f, split store %.0f, handoff to MMA %.0f, MMA issue interval %.0f\n",
          a[0] / cnt, a[1] / cnt, a[2] / cnt, a[3] / cnt, a[4] / cnt);
+  // per-quarter split completion relative to the MMA's view of opready
+  double qd[4] = {0, 0, 0, 0};
+  for (int b = nb / 4; b < 3 * nb / 4; ++b)
+    for (int q = 0; q < 4; ++q) qd[q] += (double)((long long)t[7 * 4096 + b] - (long long)t[(8 + q) * 4096 + b]);
+  printf("MMA sees opready minus split quarter done (cycles): q0 %.0f q1 %.0f q2 %.0f q3 %.0f\n",
+         qd[0] / cnt, qd[1] / cnt, qd[2] / cnt, qd[3] / cnt);
   return 0;
 }

@@ -184,9 +184,14 @@ int main() {
   long long* d;
   cudaMalloc(&d, 16);
   cudaMalloc(&g_src, (size_t)4 << 28);
+  run<128, 1, true, true, true, 0, 2>(d); run<128, 1, true, true, true, 4, 2>(d);
   run<96, 1, true, true, true, 0, 2>(d); run<96, 1, true, true, true, 4, 2>(d);
+  run<80, 1, true, true, true, 0, 2>(d); run<80, 1, true, true, true, 4, 2>(d);
+  run<80, 2, true, true, true, 0, 2>(d);
   run<64, 1, true, true, true, 0, 2>(d); run<64, 1, true, true, true, 4, 2>(d);
+  run<48, 1, true, true, true, 0, 2>(d); run<48, 1, true, true, true, 4, 2>(d);
   run<32, 1, true, true, true, 0, 2>(d); run<32, 1, true, true, true, 4, 2>(d);
+  run<256, 1, true, true, true, 0, 2>(d); run<256, 1, false, true, false, 0, 2>(d);
   cudaError_t e = cudaDeviceSynchronize();
   printf("status: %s\n", cudaGetErrorString(e));
   return 0;
