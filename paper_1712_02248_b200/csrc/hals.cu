@@ -104,6 +104,7 @@ struct StagePrefetch {
   }
 };
 
+
 // FP64 tensor-core MMA, D (8 x 8) += A (8 x 4, row) B (4 x 8, col): lane
 // (g = lane / 4, t = lane % 4) supplies A[g][t] and B[t][g] and holds
 // D[g][2t], D[g][2t + 1] (tools/ubench_dmma.cu: 37 TFLOP/s, the DFMA rate,
@@ -115,56 +116,92 @@ __device__ __forceinline__ void dmma(double& d0, double& d1, double a, double b)
                : "d"(a), "d"(b));
 }
 
-// out(r, c) = sum_{q < kdim} In[r, q] M[q, c] (fp64, q ascending) for r < nrows,
-// c < k.  M: shared fp64 (lp x k).  Thread tile: rows rg + 16 i (i < 4) of the
-// stage, columns 4 cg .. 4 cg + 3.
+__device__ __forceinline__ void cp_async8(double* dst, const double* src) {
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"(
+                   static_cast<uint32_t>(__cvta_generic_to_shared(dst))),
+               "l"(src)
+               : "memory");
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
+__device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wait_group 0;" ::: "memory"); }
+// 16-byte global -> shared copy; src_bytes = 0 zero-fills the destination
+__device__ __forceinline__ void cp_async16(void* dst, const void* src, int src_bytes) {
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;" ::"r"(
+                   static_cast<uint32_t>(__cvta_generic_to_shared(dst))),
+               "l"(src), "r"(src_bytes)
+               : "memory");
+}
+template <int N>
+__device__ __forceinline__ void cp_async_wait() { asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory"); }
+
+// out(r, c) = sum_{q < kdim} In[r, q] M[q, c] (fp64) for r < nrows, c < k.
+// M: shared fp64 (lp x k).  The fp32 rows stream through a ring of kRing raw
+// 64-row stages filled by cp.async (several stages in flight per SM: the
+// one-stage register prefetch left the phase latency-bound far below both
+// HBM and DMMA rates), row stride lp + 4 floats (conflict-free A fragments).
+// On the FP64 tensor cores: a warp item is one 8-column tile of M times 4 of
+// the stage's 8 row tiles (four accumulator chains sharing each B fragment);
+// A fragments are widened from fp32 in registers.
+constexpr int kRing = 3;
+__host__ __device__ constexpr int rts_stage_floats(int lp) { return kSR * (lp + 4); }
 template <typename Out>
 __device__ void rows_times_small(const float* __restrict__ in, int nrows, int lp, int kdim, int k,
-                                 const double* __restrict__ M, double* stage, Out out) {
-  const int lpp = lp + 1;
-  const int ncg = (k + 3) >> 2, ntile = 16 * ncg;
+                                 const double* __restrict__ M, float* ring, Out out) {
+  const int lps = lp + 4, sfl = rts_stage_floats(lp);
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int g = lane >> 2, t4 = lane & 3;
+  const int nct = (k + 7) >> 3, nqs = (kdim + 3) >> 2;
+  const int nitems = 2 * nct;  // (column tile, row-tile half)
   const int nst = (nrows + kSR - 1) / kSR;
-  StagePrefetch pf;
-  pf.init(lp);
-  if (nst > 0) pf.load(in, 0, nrows, lp);
+  const int q4 = lp >> 2, nchunk = kSR * q4;
+  auto issue = [&](int st) {  // always commits a group (empty past the end)
+    if (st < nst) {
+      float* dst = ring + (st % kRing) * sfl;
+      const int r0 = st * kSR;
+      for (int e = threadIdx.x; e < nchunk; e += kThreads) {
+        const int rr = e / q4, c4 = e - rr * q4;
+        const bool ok = r0 + rr < nrows;
+        cp_async16(dst + rr * lps + 4 * c4, in + (int64_t)(ok ? r0 + rr : 0) * lp + 4 * c4, ok ? 16 : 0);
+      }
+    }
+    cp_async_commit();
+  };
+#pragma unroll
+  for (int i = 0; i < kRing - 1; ++i) issue(i);
   for (int st = 0; st < nst; ++st) {
+    cp_async_wait<kRing - 2>();  // this thread's copies of stage st have landed
+    __syncthreads();             // everyone's have; the slot refilled below is free
+    issue(st + kRing - 1);
+    const float* stg = ring + (st % kRing) * sfl;
     const int r0 = st * kSR;
-    __syncthreads();
-    pf.store(lp, stage);
-    __syncthreads();
-    if (st + 1 < nst) pf.load(in, r0 + kSR, nrows, lp);  // in flight during the compute
-    for (int t = threadIdx.x; t < ntile; t += kThreads) {
-      const int rg = t & 15, cg = t >> 4;
-      const int c0 = 4 * cg;
-      double acc[4][4];
+    for (int it = warp; it < nitems; it += kThreads / 32) {
+      const int ct = it >> 1, rh = it & 1;
+      const int cb = ct * 8 + g;  // this lane's B-fragment column
+      const double* bp = M + t4 * k + cb;
+      const bool bok = cb < k;
+      double acc[4][2];
 #pragma unroll
-      for (int i = 0; i < 4; ++i)
-#pragma unroll
-        for (int j = 0; j < 4; ++j) acc[i][j] = 0.0;
-      const double* x0 = stage + rg * lpp;
+      for (int i = 0; i < 4; ++i) acc[i][0] = acc[i][1] = 0.0;
+      const float* a0 = stg + (rh * 32 + g) * lps + t4;
 #pragma unroll 2
-      for (int q = 0; q < kdim; ++q) {
-        double xv[4], mv[4];
-#pragma unroll
-        for (int i = 0; i < 4; ++i) xv[i] = x0[16 * i * lpp + q];
-#pragma unroll
-        for (int j = 0; j < 4; ++j) mv[j] = c0 + j < k ? M[q * k + c0 + j] : 0.0;
+      for (int qs = 0; qs < nqs; ++qs) {
+        const double bq = bok ? bp[4 * qs * k] : 0.0;
 #pragma unroll
         for (int i = 0; i < 4; ++i)
-#pragma unroll
-          for (int j = 0; j < 4; ++j) acc[i][j] = fma(xv[i], mv[j], acc[i][j]);
+          dmma(acc[i][0], acc[i][1], (double)a0[i * 8 * lps + 4 * qs], bq);
       }
+      const int c0 = ct * 8 + 2 * t4;
 #pragma unroll
       for (int i = 0; i < 4; ++i) {
-        const int r = r0 + rg + 16 * i;
+        const int r = r0 + rh * 32 + i * 8 + g;
         if (r < nrows) {
-#pragma unroll
-          for (int j = 0; j < 4; ++j)
-            if (c0 + j < k) out(r, c0 + j, acc[i][j]);
+          if (c0 < k) out(r, c0, acc[i][0]);
+          if (c0 + 1 < k) out(r, c0 + 1, acc[i][1]);
         }
       }
     }
   }
+  cp_async_wait<0>();
   __syncthreads();
 }
 
@@ -175,33 +212,48 @@ __device__ void rows_times_small(const float* __restrict__ in, int nrows, int lp
 // (fst: 2 x kSR x (k + 1)).  8 x 8 output tiles on the FP64 tensor cores
 // (dmma), up to 8 per warp accumulating in registers across all stages
 // (several passes when l x k needs more tiles than that).
-__device__ __forceinline__ void cp_async8(double* dst, const double* src) {
-  asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"(
-                   static_cast<uint32_t>(__cvta_generic_to_shared(dst))),
-               "l"(src)
-               : "memory");
-}
-__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
-__device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wait_group 0;" ::: "memory"); }
 
-__device__ void small_partial(const float* __restrict__ in, int nrows, int l, int lp, int k,
-                              const double* __restrict__ F, int64_t ldf, double* stage,
-                              double* fst, double* /*red*/, double* __restrict__ part,
-                              long long* prof = nullptr) {
-  constexpr int kTPW = 8;  // 8 x 8 output tiles per warp per pass over the rows
-  long long tp = 0;
-  if (prof && threadIdx.x == 0) tp = clock64();
-  const int lpp = lp + 1, kp1 = k + 1;
+// Stages of the partial products: kSRP rows of the fp32 input (row stride
+// lps_partial: A-fragment reads conflict-free) and of the column-major fp64
+// factor (per column kSRP + 4 doubles), kRing deep, both filled by cp.async.
+constexpr int kSRP = 32;
+constexpr int kFS = kSRP + 4;
+__host__ __device__ constexpr int lps_partial(int lp) { return lp + (8 - lp % 32 + 32) % 32; }
+__host__ __device__ constexpr int64_t partial_stage_bytes(int lp, int k) {
+  return (int64_t)kSRP * lps_partial(lp) * 4 + (int64_t)k * kFS * 8;
+}
+
+template <int kTPW>  // 8 x 8 output tiles per warp per pass over the rows
+__device__ __noinline__ void small_partial_t(const float* __restrict__ in, int nrows, int l, int lp, int k,
+                                const double* __restrict__ F, int64_t ldf, double* ringd,
+                                double* __restrict__ part) {
+  const int lps = lps_partial(lp);
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const int g = lane >> 2, t4 = lane & 3;
   const int nlt = (l + 7) >> 3, nct = (k + 7) >> 3, ntile = nlt * nct;
-  const int nst = (nrows + kSR - 1) / kSR;
-  const int fsz = kSR * kp1;
-  auto copy_f = [&](int r0, double* dst) {  // zero-filled beyond nrows
-    for (int e = threadIdx.x; e < kSR * k; e += kThreads) {
-      const int c = e / kSR, rr = e - c * kSR;
-      if (r0 + rr < nrows) cp_async8(dst + rr * kp1 + c, F + (int64_t)c * ldf + r0 + rr);
-      else dst[rr * kp1 + c] = 0.0;
+  const int nst = (nrows + kSRP - 1) / kSRP;
+  const int q4 = lp >> 2, nchunk = kSRP * q4;
+  const int64_t sbytes = partial_stage_bytes(lp, k);
+  char* ring = reinterpret_cast<char*>(ringd);
+  auto xst = [&](int st) { return reinterpret_cast<float*>(ring + (st % kRing) * sbytes); };
+  auto fst = [&](int st) {
+    return reinterpret_cast<double*>(ring + (st % kRing) * sbytes + (int64_t)kSRP * lps * 4);
+  };
+  auto issue = [&](int st) {  // always commits a group (empty past the end)
+    if (st < nst) {
+      const int r0 = st * kSRP;
+      float* xd = xst(st);
+      for (int e = threadIdx.x; e < nchunk; e += kThreads) {
+        const int rr = e / q4, c4 = e - rr * q4;
+        const bool ok = r0 + rr < nrows;
+        cp_async16(xd + rr * lps + 4 * c4, in + (int64_t)(ok ? r0 + rr : 0) * lp + 4 * c4, ok ? 16 : 0);
+      }
+      double* fd = fst(st);
+      for (int e = threadIdx.x; e < kSRP * k; e += kThreads) {  // coalesced along each column
+        const int c = e / kSRP, rr = e - c * kSRP;
+        if (r0 + rr < nrows) cp_async8(fd + c * kFS + rr, F + (int64_t)c * ldf + r0 + rr);
+        else fd[c * kFS + rr] = 0.0;
+      }
     }
     cp_async_commit();
   };
@@ -209,29 +261,15 @@ __device__ void small_partial(const float* __restrict__ in, int nrows, int l, in
     double acc[kTPW][2];
 #pragma unroll
     for (int u = 0; u < kTPW; ++u) acc[u][0] = acc[u][1] = 0.0;
-    StagePrefetch pf;
-    pf.init(lp);
-    __syncthreads();  // previous users of stage / fst are done
-    if (nst > 0) {
-      pf.load(in, 0, nrows, lp);
-      copy_f(0, fst);
-    }
+    __syncthreads();  // previous users of the ring are done
+#pragma unroll
+    for (int i = 0; i < kRing - 1; ++i) issue(i);
     for (int st = 0; st < nst; ++st) {
-      const int r0 = st * kSR;
-      double* fcur = fst + (st & 1) * fsz;
-      __syncthreads();  // stage (X) free
-      pf.store(lp, stage);
-      cp_async_wait_all();
-      __syncthreads();  // X stage and F stage st visible
-      if (prof && threadIdx.x == 0) {
-        const long long t = clock64();
-        prof[0] += t - tp;
-        tp = t;
-      }
-      if (st + 1 < nst) {
-        pf.load(in, r0 + kSR, nrows, lp);
-        copy_f(r0 + kSR, fst + ((st + 1) & 1) * fsz);
-      }
+      cp_async_wait<kRing - 2>();
+      __syncthreads();  // stage st visible to all; the slot refilled below is free
+      issue(st + kRing - 1);
+      const float* xs = xst(st);
+      const double* fs = fst(st);
       // stages are zero-filled past nrows: a fixed trip count
 #pragma unroll
       for (int u = 0; u < kTPW; ++u) {
@@ -239,20 +277,17 @@ __device__ void small_partial(const float* __restrict__ in, int nrows, int l, in
         if (tI >= ntile) break;  // warp-uniform
         const int l0 = (tI / nct) * 8, c0 = (tI % nct) * 8;
         const bool bok = c0 + g < k;
-#pragma unroll 4
-        for (int rs = 0; rs < kSR; rs += 4) {
-          const int rr = rs + t4;
-          const double av = stage[rr * lpp + l0 + g];             // A[g][t] = In[rr][l0 + g]
-          const double bv = bok ? fcur[rr * kp1 + c0 + g] : 0.0;  // B[t][g] = F[rr][c0 + g]
+        const float* xa = xs + t4 * lps + l0 + g;
+        const double* fb = fs + (bok ? (c0 + g) * kFS : 0) + t4;
+#pragma unroll
+        for (int rs = 0; rs < kSRP; rs += 4) {
+          const double av = (double)xa[rs * lps];      // A[g][t] = In[rs + t][l0 + g]
+          const double bv = bok ? fb[rs] : 0.0;        // B[t][g] = F[rs + t][c0 + g]
           dmma(acc[u][0], acc[u][1], av, bv);
         }
       }
-      if (prof && threadIdx.x == 0) {
-        const long long t = clock64();
-        prof[1] += t - tp;
-        tp = t;
-      }
     }
+    cp_async_wait<0>();
 #pragma unroll
     for (int u = 0; u < kTPW; ++u) {
       const int tI = p0 + warp + (kThreads / 32) * u;
@@ -268,51 +303,57 @@ __device__ void small_partial(const float* __restrict__ in, int nrows, int l, in
   __syncthreads();
 }
 
+// One pass over the rows whenever the l x k tile grid fits 128 tiles, two up
+// to 256 (8 tiles per warp streamed the rows 4x at C4: 195 tiles; 32 tiles
+// per warp spilled).
+__device__ void small_partial(const float* __restrict__ in, int nrows, int l, int lp, int k,
+                              const double* __restrict__ F, int64_t ldf, double* ring,
+                              double* __restrict__ part) {
+  const int ntile = ((l + 7) >> 3) * ((k + 7) >> 3);
+  if (ntile <= 8 * (kThreads / 32))
+    small_partial_t<8>(in, nrows, l, lp, k, F, ldf, ring, part);
+  else
+    small_partial_t<16>(in, nrows, l, lp, k, F, ldf, ring, part);
+}
+
 // Gram of a final lp x k fp64 matrix M (rows >= l are zero), fp64:
 // out[a*k+b] = sum_{l'<l} M[l',a] M[l',b], into this CTA's scratch.  `st` is
-// free shared memory for l x k4 doubles.
-__device__ void gram_to_scratch(const double* __restrict__ M, int l, int k, double* st,
+// free shared memory for l4 x k8 doubles.  8 x 8 tiles of the upper triangle
+// on the FP64 tensor cores (two fragment loads per DMMA), mirrored.
+__device__ __noinline__ void gram_to_scratch(const double* __restrict__ M, int l, int k, double* st,
                                 double* __restrict__ out) {
-  const int k4 = (k + 3) & ~3;
+  const int k8 = (k + 7) & ~7, l4 = (l + 3) & ~3;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int g = lane >> 2, t4 = lane & 3;
   __syncthreads();
-  for (int e = threadIdx.x; e < l * k4; e += kThreads) {
-    const int r = e / k4, c = e - r * k4;
-    st[e] = c < k ? __ldcg(M + r * k + c) : 0.0;
+  for (int e = threadIdx.x; e < l4 * k8; e += kThreads) {
+    const int r = e / k8, c = e - r * k8;
+    st[e] = (r < l && c < k) ? __ldcg(M + r * k + c) : 0.0;
   }
   __syncthreads();
-  const int nb4 = k4 >> 2, nb = nb4 * (nb4 + 1) / 2;
-  for (int b = threadIdx.x; b < nb; b += kThreads) {
-    int bi = 0, rem = b;
-    while (rem >= nb4 - bi) {
-      rem -= nb4 - bi;
-      ++bi;
+  const int nkt = k8 >> 3, ntri = nkt * (nkt + 1) / 2, nqs = l4 >> 2;
+  for (int tI = warp; tI < ntri; tI += kThreads / 32) {
+    int ai = 0, rem = tI;
+    while (rem >= nkt - ai) {
+      rem -= nkt - ai;
+      ++ai;
     }
-    const int bj = bi + rem;
-    double acc[16];
+    const int bi = ai + rem;
+    double d0 = 0.0, d1 = 0.0;
+    const double* pa = st + t4 * k8 + ai * 8 + g;
+    const double* pb = st + t4 * k8 + bi * 8 + g;
+#pragma unroll 4
+    for (int qs = 0; qs < nqs; ++qs) dmma(d0, d1, pa[4 * qs * k8], pb[4 * qs * k8]);
+    const int a = ai * 8 + g, c = bi * 8 + 2 * t4;
+    const double v[2] = {d0, d1};
 #pragma unroll
-    for (int i = 0; i < 16; ++i) acc[i] = 0.0;
-    for (int r = 0; r < l; ++r) {
-      double xv[4], yv[4];
-#pragma unroll
-      for (int i = 0; i < 4; ++i) {
-        xv[i] = st[r * k4 + 4 * bi + i];
-        yv[i] = st[r * k4 + 4 * bj + i];
+    for (int j = 0; j < 2; ++j) {
+      const int cc = c + j;
+      if (a < k && cc < k && (ai < bi || a <= cc)) {
+        out[a * k + cc] = v[j];
+        out[cc * k + a] = v[j];
       }
-#pragma unroll
-      for (int i = 0; i < 4; ++i)
-#pragma unroll
-        for (int j = 0; j < 4; ++j) acc[4 * i + j] = fma(xv[i], yv[j], acc[4 * i + j]);
     }
-#pragma unroll
-    for (int i = 0; i < 4; ++i)
-#pragma unroll
-      for (int j = 0; j < 4; ++j) {
-        const int a = 4 * bi + i, c = 4 * bj + j;
-        if (a < k && c < k) {
-          out[a * k + c] = acc[4 * i + j];
-          out[c * k + a] = acc[4 * i + j];
-        }
-      }
   }
   __syncthreads();
 }
@@ -362,10 +403,8 @@ __global__ void __launch_bounds__(kThreads, 1) hals_kernel(const HalsArgs p) {
   // shared layout: products use [M lp*k | stage 64*lpp]; sweeps use [g or w k*k];
   // partials use [stage 32*lpp | fst 32*kp1] (+ group reduction aliasing it)
   double* Ms = smem;
-  double* stage64 = smem + lp * k;
+  float* ring64 = reinterpret_cast<float*>(smem + lp * k);  // rows_times_small stages
   double* gw = smem;
-  double* stP = smem;
-  double* fsP = smem + kSR * lpp;
 
   const bool prof = S.prof != nullptr && cta == 0;
   long long t_last = 0;
@@ -397,7 +436,7 @@ __global__ void __launch_bounds__(kThreads, 1) hals_kernel(const HalsArgs p) {
         // h = X-check B-check for this CTA's rows (solvers.cpp:421)
         for (int e = tid; e < lp * k; e += kThreads) Ms[e] = __ldcg(S.bchk + e);
         HALS_PROF(0);
-        rows_times_small(S.xc + a_lo * lp, na, lp, l, k, Ms, stage64,
+        rows_times_small(S.xc + a_lo * lp, na, lp, l, k, Ms, ring64,
                          [&](int r, int c, double v) { S.h[(int64_t)c * d + a_lo + r] = v; });
         load_gram(gw, gsc, k, kg, false);
       }
@@ -536,8 +575,8 @@ __global__ void __launch_bounds__(kThreads, 1) hals_kernel(const HalsArgs p) {
         return;
       }
       // A-hat = L^T A (solvers.cpp:438): partials, exchange, slice reduce, exchange
-      small_partial(S.lm + a_lo * lp, na, l, lp, k, S.a + a_lo, d, stP, fsP, smem,
-                    S.part + (int64_t)cta * nel, prof ? s_prof + 17 : nullptr);
+      small_partial(S.lm + a_lo * lp, na, l, lp, k, S.a + a_lo, d, smem,
+                    S.part + (int64_t)cta * nel);
       HALS_PROF(4);
       exchange(S, G, cta, ep);
       HALS_PROF(5);
@@ -558,7 +597,7 @@ __global__ void __launch_bounds__(kThreads, 1) hals_kernel(const HalsArgs p) {
       if (!have_w) gram_to_scratch(S.ahat, l, k, smem, wsc);
       // p = X-hat^T A-hat for this CTA's rows (solvers.cpp:442)
       for (int e = tid; e < lp * k; e += kThreads) Ms[e] = __ldcg(S.ahat + e);
-      rows_times_small(S.xht + b_lo * lp, nbr, lp, l, k, Ms, stage64,
+      rows_times_small(S.xht + b_lo * lp, nbr, lp, l, k, Ms, ring64,
                        [&](int r, int c, double v) { S.p[(int64_t)c * n + b_lo + r] = v; });
       load_gram(gw, wsc, k, kg, false);
     }
@@ -675,7 +714,7 @@ __global__ void __launch_bounds__(kThreads, 1) hals_kernel(const HalsArgs p) {
     if (tid < 4) S.zpart[cta * 4 + tid] = zmask[tid];
     // B-check partial = R_rows B_rows, published together with the zero flags
     if (!S.dense)
-      small_partial(S.rt + b_lo * lp, nbr, l, lp, k, bnxt + b_lo, n, stP, fsP, smem,
+      small_partial(S.rt + b_lo * lp, nbr, l, lp, k, bnxt + b_lo, n, smem,
                     S.part + (int64_t)cta * nel);
     HALS_PROF(11);
     exchange(S, G, cta, ep);
@@ -750,10 +789,10 @@ __global__ void __launch_bounds__(kThreads, 1) hals_kernel(const HalsArgs p) {
 size_t hals_smem_bytes(const HalsState& st, int /*rows_a*/) {
   const int64_t k = st.k, lp = st.lp, l = st.l, kp1 = k + 1, lpp = lp + 1;
   const int64_t k4 = (k + 3) & ~3;
-  const int64_t prod = lp * k + 64 * lpp;
+  const int64_t prod = lp * k + (kRing * (int64_t)rts_stage_floats((int)lp) + 1) / 2;
   const int64_t sweep = k * ((k + 7) & ~7);
-  const int64_t part = kSR * lpp + 2 * kSR * kp1;  // X stage + double-buffered F stage
-  const int64_t gram = l * k4;
+  const int64_t part = (kRing * partial_stage_bytes((int)lp, (int)k) + 7) / 8;  // cp.async ring
+  const int64_t gram = ((l + 3) & ~3) * ((k + 7) & ~7);
   return (size_t)std::max(std::max(prod, sweep), std::max(part, gram)) * sizeof(double);
 }
 
