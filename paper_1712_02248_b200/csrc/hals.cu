@@ -638,15 +638,21 @@ __global__ void __launch_bounds__(kThreads, 1) hals_kernel(const HalsArgs p) {
           for (int i = 0; i < RB; ++i)
   #pragma unroll
             for (int t = 0; t < kNB; ++t) acc[i][t] = 0.0;
-          for (int c0 = 0; c0 < k; c0 += 4) {
-            double bv4[RB][4];
+          // software-pipelined: the next 4 columns' loads are in flight while
+          // the current 4 are multiplied (the loop was latency-bound)
+          double bv4[RB][4], bvn[RB][4];
+          auto load4 = [&](int c0, double (&dst)[RB][4]) {
   #pragma unroll
             for (int i = 0; i < RB; ++i)
   #pragma unroll
               for (int cc = 0; cc < 4; ++cc) {
                 const int c = c0 + cc;
-                bv4[i][cc] = (okr[i] && c < k) ? __ldcg((c < jbe ? bnxt : bcur) + (int64_t)c * n + gr[i]) : 0.0;
+                dst[i][cc] = (okr[i] && c < k) ? __ldcg((c < jbe ? bnxt : bcur) + (int64_t)c * n + gr[i]) : 0.0;
               }
+          };
+          load4(0, bv4);
+          for (int c0 = 0; c0 < k; c0 += 4) {
+            if (c0 + 4 < k) load4(c0 + 4, bvn);
   #pragma unroll
             for (int cc = 0; cc < 4; ++cc) {
               if (c0 + cc >= k) break;
@@ -657,6 +663,10 @@ __global__ void __launch_bounds__(kThreads, 1) hals_kernel(const HalsArgs p) {
   #pragma unroll
                 for (int t = 0; t < kNB; ++t) acc[i][t] = fma(bv4[i][cc], gv[t], acc[i][t]);
             }
+  #pragma unroll
+            for (int i = 0; i < RB; ++i)
+  #pragma unroll
+              for (int cc = 0; cc < 4; ++cc) bv4[i][cc] = bvn[i][cc];
           }
           // b and p of the next column are loaded one step ahead: the column
           // chain waits on arithmetic only
