@@ -20,6 +20,7 @@
 // (the reference draws it from the run's host Rng), so the kernel halts at
 // exactly the reference's event point, records it in HaltInfo, and the host
 // draws the column, uploads it and resumes (engine.cpp).
+#include <cstdlib>
 #include <type_traits>
 
 #include "common.cuh"
@@ -462,6 +463,7 @@ __global__ void __launch_bounds__(kThreads, 1) hals_kernel(const HalsArgs p) {
       // One all-reduce per column for the norm.
       for (int jb = col0 & ~(kNB - 1); jb < jd; jb += kNB) {
         const int t0 = max(col0 - jb, 0), nbj = min(kNB, jd - jb);
+        if (t0 >= nbj) continue;  // resumed at col0 == jd: nothing left in this block
         double acc[RPT][kNB];
 #pragma unroll
         for (int i = 0; i < RPT; ++i)
@@ -632,6 +634,7 @@ __global__ void __launch_bounds__(kThreads, 1) hals_kernel(const HalsArgs p) {
         }
         for (int jb = col0 & ~(kNB - 1); jb < jd; jb += kNB) {
           const int t0 = max(col0 - jb, 0), nbj = min(kNB, jd - jb);
+          if (t0 >= nbj) continue;  // resumed at col0 == jd: nothing left in this block
           const int jbe = jb + t0;  // columns < jbe already live in bnxt
           double acc[RB][kNB];
   #pragma unroll
@@ -869,7 +872,8 @@ cudaError_t launch_hals(const HalsState& st, int normalize_a, double alpha, doub
   // rows per thread of the A sweep (register-resident across the column chain)
   const int rpt = (a.rows_a + kThreads - 1) / kThreads;
   if (rpt > kMaxRPTLarge) return cudaErrorInvalidConfiguration;
-  const void* fn = rpt <= 3 ? (const void*)hals_kernel<3> : (const void*)hals_kernel<kMaxRPTLarge>;
+  const bool large = rpt > 3 || std::getenv("CNMF_HALS_RPT6") != nullptr;  // env: tests only
+  const void* fn = large ? (const void*)hals_kernel<kMaxRPTLarge> : (const void*)hals_kernel<3>;
   cudaError_t e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   if (e != cudaSuccess) return e;
   void* args[] = {&a};
