@@ -580,11 +580,11 @@ __global__ void __launch_bounds__(kThreads, 1) hals_kernel(const HalsArgs p) {
       small_partial(S.lm + a_lo * lp, na, l, lp, k, S.a + a_lo, d, smem,
                     S.part + (int64_t)cta * nel);
       HALS_PROF(4);
-      exchange(S, G, cta, ep);
+      exchange_fast(S, G, ep);
       HALS_PROF(5);
       slice_reduce(S.part, G, nel, S.ahat);
       HALS_PROF(6);
-      exchange(S, G, cta, ep);
+      exchange_fast(S, G, ep);
       HALS_PROF(7);
       gram_to_scratch(S.ahat, l, k, smem, wsc);  // w = A-hat^T A-hat (solvers.cpp:443)
       HALS_PROF(8);
@@ -730,7 +730,7 @@ __global__ void __launch_bounds__(kThreads, 1) hals_kernel(const HalsArgs p) {
       small_partial(S.rt + b_lo * lp, nbr, l, lp, k, bnxt + b_lo, n, smem,
                     S.part + (int64_t)cta * nel);
     HALS_PROF(11);
-    exchange(S, G, cta, ep);
+    exchange_fast(S, G, ep);
     HALS_PROF(12);
     if (tid < 4) zmask[tid] = 0u;
     __syncthreads();
@@ -749,7 +749,7 @@ __global__ void __launch_bounds__(kThreads, 1) hals_kernel(const HalsArgs p) {
           bnxt[gi] = bcur[gi];
         }
       slice_reduce(S.part, G, nel, S.bchk);
-      exchange(S, G, cta, ep);
+      exchange_fast(S, G, ep);
       if (cta == 0 && tid < 4) S.zpart[4 * G + tid] = zmask[tid];
       if (cta == 0 && tid == 0) *S.halt = HaltInfo{1, it + 1, 1, jd, kEvShard, bnxt == S.bold, ep};
       return;
@@ -778,7 +778,7 @@ __global__ void __launch_bounds__(kThreads, 1) hals_kernel(const HalsArgs p) {
     if (!S.dense) {
       slice_reduce(S.part, G, nel, S.bchk);
       HALS_PROF(14);
-      exchange(S, G, cta, ep);
+      exchange_fast(S, G, ep);
       HALS_PROF(15);
       gram_to_scratch(S.bchk, l, k, smem, gsc);  // g for the next A half (solvers.cpp:422)
       HALS_PROF(16);

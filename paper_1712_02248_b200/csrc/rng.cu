@@ -99,17 +99,25 @@ __global__ void __launch_bounds__(160) mt_stream_kernel(MtJobs jobs, int raw) {
 constexpr int kJumpPoly = 312;                  // words per polynomial (19968 bits)
 constexpr int kJumpPrefix = 64 * kJumpPoly + kN;  // raw words the convolution reads
 
-__global__ void __launch_bounds__(kN) mt_jump_state_kernel(const uint64_t* __restrict__ prefix,
-                                                           const uint64_t* __restrict__ polys,
-                                                           uint64_t* __restrict__ states) {
-  extern __shared__ uint64_t pre[];  // kJumpPrefix words
+// Segment k's starting state = sum over the set bits of its jump polynomial
+// of the prefix shifted by the bit's position (GF(2), XOR).  kJumpGroups
+// thread groups of 312 split the polynomial's words round-robin and their
+// partial XORs are combined at the end (XOR is exact and order-free: bitwise
+// the serial result); one group per CTA left the kernel latency-bound at
+// ~60 us, which kept streams below 2^20 words on the serial engine.
+constexpr int kJumpGroups = 3;
+__global__ void __launch_bounds__(kN * kJumpGroups) mt_jump_state_kernel(
+    const uint64_t* __restrict__ prefix, const uint64_t* __restrict__ polys,
+    uint64_t* __restrict__ states) {
+  extern __shared__ uint64_t pre[];  // kJumpPrefix words, then kJumpGroups x kN partials
   __shared__ uint64_t cpoly[kJumpPoly];
-  const int k = blockIdx.x + 1, w = threadIdx.x;
-  for (int e = w; e < kJumpPrefix; e += blockDim.x) pre[e] = prefix[e];
-  for (int e = w; e < kJumpPoly; e += blockDim.x) cpoly[e] = polys[(size_t)k * kJumpPoly + e];
+  const int k = blockIdx.x + 1;
+  const int grp = threadIdx.x / kN, w = threadIdx.x - grp * kN;
+  for (int e = threadIdx.x; e < kJumpPrefix; e += blockDim.x) pre[e] = prefix[e];
+  for (int e = threadIdx.x; e < kJumpPoly; e += blockDim.x) cpoly[e] = polys[(size_t)k * kJumpPoly + e];
   __syncthreads();
   uint64_t acc = 0;
-  for (int cw = 0; cw < kJumpPoly; ++cw) {
+  for (int cw = grp; cw < kJumpPoly; cw += kJumpGroups) {
     uint64_t bits = cpoly[cw];
     while (bits) {
       const int b = __ffsll(bits) - 1;
@@ -117,7 +125,14 @@ __global__ void __launch_bounds__(kN) mt_jump_state_kernel(const uint64_t* __res
       acc ^= pre[64 * cw + b + w];
     }
   }
-  states[(size_t)blockIdx.x * kN + w] = acc;
+  uint64_t* part = pre + kJumpPrefix;
+  part[grp * kN + w] = acc;
+  __syncthreads();
+  if (grp == 0) {
+#pragma unroll
+    for (int g = 1; g < kJumpGroups; ++g) acc ^= part[g * kN + w];
+    states[(size_t)blockIdx.x * kN + w] = acc;
+  }
 }
 
 // CTA k emits outputs [kJ, min((k + 1) J, nwords)): the segment's starting
@@ -248,13 +263,13 @@ void launch_mt_jump(uint64_t seed, uint64_t nwords, uint64_t J, int K, const uin
   mt_stream_kernel<<<1, 160, 0, s>>>(jobs, 1);
   if (K > 1) {
     static bool attr = false;
-    const int smem = (int)(sizeof(uint64_t) * kJumpPrefix);
+    const int smem = (int)(sizeof(uint64_t) * (kJumpPrefix + kJumpGroups * kN));
     if (!attr) {
       cudaFuncSetAttribute(mt_jump_state_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
       attr = true;
     }
     note_launches(1);
-    mt_jump_state_kernel<<<K - 1, kN, smem, s>>>(prefix, polys, states);
+    mt_jump_state_kernel<<<K - 1, kN * kJumpGroups, smem, s>>>(prefix, polys, states);
   }
   note_launches(1);
   mt_segment_kernel<<<K, 160, 0, s>>>(prefix, states, J, nwords, out);
