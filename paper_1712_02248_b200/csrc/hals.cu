@@ -140,9 +140,10 @@ __device__ __forceinline__ void cp_async_wait() { asm volatile("cp.async.wait_gr
 // 64-row stages filled by cp.async (several stages in flight per SM: the
 // one-stage register prefetch left the phase latency-bound far below both
 // HBM and DMMA rates), row stride lp + 4 floats (conflict-free A fragments).
-// On the FP64 tensor cores: a warp item is one 8-column tile of M times 4 of
-// the stage's 8 row tiles (four accumulator chains sharing each B fragment);
-// A fragments are widened from fp32 in registers.
+// On the FP64 tensor cores: a warp item is two 8-column tiles of M times 4 of
+// the stage's 8 row tiles (eight accumulator chains; each A fragment is
+// widened from fp32 once and used for both column tiles; at k = 50 the 8
+// items cover the 8 warps in one round).
 constexpr int kRing = 3;
 __host__ __device__ constexpr int rts_stage_floats(int lp) { return kSR * (lp + 4); }
 template <typename Out>
@@ -152,7 +153,8 @@ __device__ void rows_times_small(const float* __restrict__ in, int nrows, int lp
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const int g = lane >> 2, t4 = lane & 3;
   const int nct = (k + 7) >> 3, nqs = (kdim + 3) >> 2;
-  const int nitems = 2 * nct;  // (column tile, row-tile half)
+  const int ncp = (nct + 1) >> 1;  // column-tile pairs
+  const int nitems = 2 * ncp;      // (column-tile pair, row-tile half)
   const int nst = (nrows + kSR - 1) / kSR;
   const int q4 = lp >> 2, nchunk = kSR * q4;
   auto issue = [&](int st) {  // always commits a group (empty past the end)
@@ -176,28 +178,39 @@ __device__ void rows_times_small(const float* __restrict__ in, int nrows, int lp
     const float* stg = ring + (st % kRing) * sfl;
     const int r0 = st * kSR;
     for (int it = warp; it < nitems; it += kThreads / 32) {
-      const int ct = it >> 1, rh = it & 1;
-      const int cb = ct * 8 + g;  // this lane's B-fragment column
-      const double* bp = M + t4 * k + cb;
-      const bool bok = cb < k;
-      double acc[4][2];
+      const int cp = it >> 1, rh = it & 1;
+      // this lane's B-fragment columns in the pair's two tiles
+      const int cb0 = cp * 16 + g, cb1 = cb0 + 8;
+      const bool bok0 = cb0 < k, bok1 = cb1 < k;
+      const double* bp0 = M + t4 * k + (bok0 ? cb0 : 0);
+      const double* bp1 = M + t4 * k + (bok1 ? cb1 : 0);
+      double acc[2][4][2];
 #pragma unroll
-      for (int i = 0; i < 4; ++i) acc[i][0] = acc[i][1] = 0.0;
+      for (int h = 0; h < 2; ++h)
+#pragma unroll
+        for (int i = 0; i < 4; ++i) acc[h][i][0] = acc[h][i][1] = 0.0;
       const float* a0 = stg + (rh * 32 + g) * lps + t4;
 #pragma unroll 2
       for (int qs = 0; qs < nqs; ++qs) {
-        const double bq = bok ? bp[4 * qs * k] : 0.0;
+        const double b0 = bok0 ? bp0[4 * qs * k] : 0.0;
+        const double b1 = bok1 ? bp1[4 * qs * k] : 0.0;
 #pragma unroll
-        for (int i = 0; i < 4; ++i)
-          dmma(acc[i][0], acc[i][1], (double)a0[i * 8 * lps + 4 * qs], bq);
+        for (int i = 0; i < 4; ++i) {
+          const double av = (double)a0[i * 8 * lps + 4 * qs];  // widened once, used twice
+          dmma(acc[0][i][0], acc[0][i][1], av, b0);
+          dmma(acc[1][i][0], acc[1][i][1], av, b1);
+        }
       }
-      const int c0 = ct * 8 + 2 * t4;
 #pragma unroll
-      for (int i = 0; i < 4; ++i) {
-        const int r = r0 + rh * 32 + i * 8 + g;
-        if (r < nrows) {
-          if (c0 < k) out(r, c0, acc[i][0]);
-          if (c0 + 1 < k) out(r, c0 + 1, acc[i][1]);
+      for (int h = 0; h < 2; ++h) {
+        const int c0 = cp * 16 + h * 8 + 2 * t4;
+#pragma unroll
+        for (int i = 0; i < 4; ++i) {
+          const int r = r0 + rh * 32 + i * 8 + g;
+          if (r < nrows) {
+            if (c0 < k) out(r, c0, acc[h][i][0]);
+            if (c0 + 1 < k) out(r, c0 + 1, acc[h][i][1]);
+          }
         }
       }
     }
