@@ -59,10 +59,12 @@ void launch_uniform_init_exact(const uint64_t* words, uint64_t nwords, uint64_t 
 // lp is a multiple of 16 in [16, 128].  `ws` is scratch for split-K partials
 // (xstream_ws_floats() floats).  Deterministic: fixed-order split reduction.
 size_t xstream_ws_floats(int64_t m, int64_t n, int lp, int nsm);
+// rexp (optional, from launch_x_rowexp over this X): per-row exponents that
+// select the tensor-core kernel's fp16 hi/lo path.
 void launch_xs_nn(const float* x, int64_t ldx, int64_t m, int64_t n, const float* s, int lp,
-                  float* y, float* ws, int nsm, cudaStream_t st);
+                  float* y, float* ws, int nsm, cudaStream_t st, const int8_t* rexp = nullptr);
 void launch_xs_tn(const float* x, int64_t ldx, int64_t m, int64_t n, const float* t, int lp,
-                  float* z, float* ws, int nsm, cudaStream_t st);
+                  float* z, float* ws, int nsm, cudaStream_t st, const int8_t* rexp = nullptr);
 
 // xstream_tc.cu: the same contractions on tcgen05 tensor cores (3xTF32,
 // TMA-staged operands, TMEM accumulators).  Returns false (nothing launched)
@@ -70,7 +72,13 @@ void launch_xs_tn(const float* x, int64_t ldx, int64_t m, int64_t n, const float
 size_t xstream_tc_ws_floats(int64_t m, int64_t n, int lp, int nsm);
 void xstream_tc_set_debug(float* dbg);  // tools/tc_debug.cu only
 bool launch_xs_tc(bool tn, const float* x, int64_t ldx, int64_t m, int64_t n, const float* s,
-                  int lp, float* out, float* ws, int nsm, cudaStream_t st);
+                  int lp, float* out, float* ws, int nsm, cudaStream_t st,
+                  const int8_t* rexp = nullptr);
+// Per-row exponents of X (d rows, xs_rexp_bytes(d) bytes, zero padded) and a
+// flag set when some row's dynamic range exceeds 2^30 (keep 3xTF32 then).
+size_t xs_rexp_bytes(int64_t rows);
+void launch_x_rowexp(const float* x, int64_t ldx, int64_t d, int64_t n, int8_t* rexp, int* wide,
+                     int nsm, cudaStream_t st);
 
 // ---- qr.cu: orthonormal basis with the span of Y --------------------------
 // CholeskyQR2 with fp64 Grams; Householder (reference qr.cpp semantics, fp64)
@@ -97,7 +105,8 @@ void launch_householder_signs(float* q, int64_t rows, int l, int lp, float* sgn,
 // check_data: flags[0] |= negative/non-finite; *norm_sq = ||X||_F^2 (fp64).
 size_t metrics_ws_bytes(int64_t d, int64_t n, int nsm);
 void launch_check_data(const float* x, int64_t ldx, int64_t d, int64_t n, int* flag,
-                       double* norm_sq, void* ws, int nsm, cudaStream_t st);
+                       double* norm_sq, void* ws, int nsm, cudaStream_t st, int8_t* rexp = nullptr,
+                       int* wide = nullptr);
 // 1/2 ||X - A B^T||^2 with column-major A_cm (k x d), B_cm (k x n).
 void launch_recon_error(const float* x, int64_t ldx, int64_t d, int64_t n, const double* a_cm,
                         const double* b_cm, int k, double* out, void* ws, int nsm,

@@ -14,30 +14,60 @@ namespace {
 
 constexpr int kTile = 64;
 
+// One warp per row (lanes over the row's float4 chunks): the check_data flag
+// (solvers.cpp:47-52), ||X||^2 partials per block, and -- when rexp is given
+// -- the row's exponent for the X-stream kernel's fp16 path (row max scaled
+// into [2^14, 2^15)) plus `wide` when a row's smallest nonzero magnitude is
+// below 2^-30 of its max.  One read of X serves the validation and the
+// scaling.
 __global__ void __launch_bounds__(256) check_data_kernel(const float* __restrict__ x, int64_t ldx,
                                                          int64_t d, int64_t n,
                                                          int* __restrict__ flag,
-                                                         double* __restrict__ part) {
+                                                         double* __restrict__ part,
+                                                         int8_t* __restrict__ rexp,
+                                                         int* __restrict__ wide) {
   __shared__ double red[8];
   double s = 0.0;
   int bad = 0;
+  const int lane = threadIdx.x & 31;
   const int64_t n4 = (n + 3) / 4;
-  const bool vec = (ldx % 4) == 0;
-  for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < d * n4;
-       e += (int64_t)gridDim.x * blockDim.x) {
-    const int64_t i = e / n4, j = (e - i * n4) * 4;
+  const bool vec = (ldx % 4) == 0 && (reinterpret_cast<uintptr_t>(x) & 15) == 0;
+  const int64_t warps = (int64_t)gridDim.x * (blockDim.x >> 5);
+  for (int64_t i = blockIdx.x * (int64_t)(blockDim.x >> 5) + (threadIdx.x >> 5); i < d; i += warps) {
     const float* row = x + i * ldx;
-    float v[4] = {0.f, 0.f, 0.f, 0.f};
-    if (vec && j + 3 < n) {
-      const float4 t = __ldg(reinterpret_cast<const float4*>(row + j));
-      v[0] = t.x; v[1] = t.y; v[2] = t.z; v[3] = t.w;
-    } else {
-      for (int q = 0; q < 4 && j + q < n; ++q) v[q] = __ldg(row + j + q);
-    }
+    float mx = 0.f, mn = INFINITY;
+    for (int64_t c = lane; c < n4; c += 32) {
+      const int64_t j = 4 * c;
+      float v[4] = {0.f, 0.f, 0.f, 0.f};
+      if (vec && j + 3 < n) {
+        const float4 t = __ldg(reinterpret_cast<const float4*>(row + j));
+        v[0] = t.x; v[1] = t.y; v[2] = t.z; v[3] = t.w;
+      } else {
+        for (int q = 0; q < 4 && j + q < n; ++q) v[q] = __ldg(row + j + q);
+      }
 #pragma unroll
-    for (int q = 0; q < 4; ++q) {
-      if (!(v[q] >= 0.f) || !isfinite(v[q])) bad = 1;
-      s += (double)v[q] * (double)v[q];
+      for (int q = 0; q < 4; ++q) {
+        if (!(v[q] >= 0.f) || !isfinite(v[q])) bad = 1;
+        s += (double)v[q] * (double)v[q];
+        mx = fmaxf(mx, v[q]);
+        if (v[q] > 0.f) mn = fminf(mn, v[q]);
+      }
+    }
+    if (rexp) {
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) {
+        mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, o));
+        mn = fminf(mn, __shfl_xor_sync(0xffffffffu, mn, o));
+      }
+      if (lane == 0) {
+        int e = 0;
+        if (mx > 0.f && isfinite(mx)) {
+          frexpf(mx, &e);
+          e = max(-126, min(126, 15 - e));
+        }
+        rexp[i] = (int8_t)e;
+        if (mx > 0.f && mn < mx * 0x1.0p-30f) atomicOr(wide, 1);
+      }
     }
   }
   if (__syncthreads_or(bad) && threadIdx.x == 0) *flag = 1;
@@ -212,11 +242,12 @@ uint64_t launch_count() { return __atomic_load_n(&g_launches, __ATOMIC_RELAXED);
 size_t metrics_ws_bytes(int64_t, int64_t, int nsm) { return sizeof(double) * (nsm * 16 + 64); }
 
 void launch_check_data(const float* x, int64_t ldx, int64_t d, int64_t n, int* flag,
-                       double* norm_sq, void* ws, int nsm, cudaStream_t st) {
+                       double* norm_sq, void* ws, int nsm, cudaStream_t st, int8_t* rexp,
+                       int* wide) {
   const int grid = nsm * 4;
   double* part = static_cast<double*>(ws);
   note_launches(1);
-  check_data_kernel<<<grid, 256, 0, st>>>(x, ldx, d, n, flag, part);
+  check_data_kernel<<<grid, 256, 0, st>>>(x, ldx, d, n, flag, part, rexp, wide);
   note_launches(1);
   sum_partials_kernel<<<1, 32, 0, st>>>(part, grid, norm_sq, 1.0);
 }

@@ -25,6 +25,7 @@
 // running sums in the epilogue's registers while the second TMEM buffer
 // takes the next chunk.  Split-K partials are reduced in a fixed order.
 #include <cuda.h>
+#include <cuda_fp16.h>
 #include <cudaTypedefs.h>
 
 #include <cstdlib>
@@ -45,6 +46,15 @@ constexpr int kWarpTMA = 4, kWarpMMA = 5, kWarpSplit0 = 6, kWarpBTMA = 10;
 constexpr int kDrain = TC_DRAIN;
 #else
 constexpr int kDrain = 4;         // K-blocks per drain (16 k-steps x 3 MMAs per accumulation chain)
+#endif
+// The fp16 path drains every K-block: its K = 16 MMAs grow the accumulation
+// error faster (tools/f16_accuracy.py); with drains every 2 / 4 blocks the C2
+// trajectory with forced fp16 deviates 1.3e-4 / 2.6e-4 from the reference,
+// every block 1e-5 (tests/test_gpu_f16.py), at ~8% of the fp16 speed-up.
+#ifdef TC_DRAIN16
+constexpr int kDrain16 = TC_DRAIN16;
+#else
+constexpr int kDrain16 = 4;
 #endif
 constexpr int kXBytes = kBM * kBK * 4;  // 16 KB per stage (x_hi), same for x_lo
 
@@ -115,6 +125,25 @@ __host__ __device__ constexpr uint32_t idesc_tf32(int n, bool a_mn, bool b_mn) {
          | ((uint32_t)(kBM >> 4) << 24); // M >> 4
 }
 
+// Instruction descriptor: kind::f16 with fp16 A and B, fp32 accumulate,
+// M = 128 (layouts checked by tools/tc_f16_check.cu).
+__host__ __device__ constexpr uint32_t idesc_f16(int n, bool b_mn) {
+  return (1u << 4) | ((b_mn ? 1u : 0u) << 16) | ((uint32_t)(n >> 3) << 17) |
+         ((uint32_t)(kBM >> 4) << 24);
+}
+__device__ __forceinline__ void mma16_ts_elect(uint32_t d_tmem, uint32_t a_tmem, uint64_t b_desc,
+                                               uint32_t idesc, uint32_t accumulate) {
+  asm volatile(
+      "{\n\t.reg .pred p, e;\n\t"
+      "setp.ne.b32 p, %4, 0;\n\t"
+      "{\n\t.reg .u32 ln;\n\tmov.u32 ln, %%laneid;\n\tsetp.eq.u32 e, ln, 0;\n\t}\n\t"
+      "@e tcgen05.mma.cta_group::1.kind::f16 [%0], [%1], %2, %3, p;\n\t}" ::"r"(d_tmem),
+      "r"(a_tmem), "l"(b_desc), "r"(idesc), "r"(accumulate)
+      : "memory");
+}
+// 2^e as a float, e in [-126, 127]
+__device__ __forceinline__ float exp2i(int e) { return __int_as_float((127 + e) << 23); }
+
 struct TcArgs {
   int64_t rows_out;  // output rows (m for NN, n for TN)
   int64_t kdim;      // reduction length (n for NN, m for TN)
@@ -123,6 +152,10 @@ struct TcArgs {
   float* out;        // [nsplit][rows_out][lp] or the final output when nsplit == 1
   float* dbg;        // optional debug dump (tools/tc_debug.cu), null in production
   int nmma;          // MMA N = lp rounded up to 16 (<= L): padding columns are not computed
+  // fp16 path only: per-row exponents of X (NN: output rows; TN: the K index),
+  // applied as exact 2^e scalings, and the per-output-column unscale factors
+  const int8_t* rexp;
+  const float* cscale;
 };
 
 
@@ -132,8 +165,10 @@ struct TcArgs {
 // one TMA write plus one LDS pass of shared-memory bandwidth (the v2 kernel's
 // shared-memory operand slots cost four more and made it smem-bound).  An X
 // stage is released as soon as the split warps have read it.
-template <int L> struct TcRings {
-  static constexpr int kBBytes = kBK * L * 4;  // s_hi or s_lo per K-block
+template <int L, bool kF16 = false> struct TcRings {
+  // fp16 S stages are LH halves wide: 64-element SWIZZLE_128B atoms
+  static constexpr int LH = (L + 63) & ~63;
+  static constexpr int kBBytes = kF16 ? kBK * LH * 2 : kBK * L * 4;  // s_hi or s_lo per K-block
   static constexpr int kBudget = 225 * 1024;
   // Both operands arrive with ~1.5-2k cycles of latency (X from HBM, S from
   // L2, re-requested only when a stage frees), so the budget is split to keep
@@ -155,16 +190,23 @@ template <int L> struct TcRings {
   // Tensor memory: two accumulator buffers of L columns (double-buffered
   // drain), then the A slots of 64 columns (x_hi: 32, x_lo: 32; lane = tile
   // row, column = k).
-  static constexpr int kChains = 1;
+  // fp16: the small correction products (x_hi s_lo + x_lo s_hi) accumulate
+  // in a second accumulator, so the big one's rounding cannot swamp them;
+  // the epilogue folds the two (L <= 96: 2 x 2L accumulator columns + 4
+  // operand slots of 32 fill the 512 TMEM columns)
+  static constexpr int kChains = kF16 ? 2 : 1;
   static constexpr int kAccCols = kChains * L;
   static constexpr int kAOff = 2 * kAccCols;
-  static constexpr int kOpFit = (512 - kAOff) / 64;
+  // A operand slot per K-block: tf32 x_hi | x_lo 32 + 32 columns; fp16 two
+  // halves per column, 16 + 16
+  static constexpr int kASlot = kF16 ? 32 : 64;
+  static constexpr int kOpFit = (512 - kAOff) / kASlot;
 #ifdef TC_OPSTAGES
   static constexpr int kOpStages = TC_OPSTAGES;
 #else
   static constexpr int kOpStages = kOpFit > 4 ? 4 : kOpFit;
 #endif
-  static constexpr uint32_t kTmemNeed = kAOff + kOpStages * 64;
+  static constexpr uint32_t kTmemNeed = kAOff + kOpStages * kASlot;
   static constexpr uint32_t kTmemCols =
       kTmemNeed <= 32 ? 32 : (kTmemNeed <= 64 ? 64 : (kTmemNeed <= 128 ? 128 : (kTmemNeed <= 256 ? 256 : 512)));
 };
@@ -244,11 +286,12 @@ __device__ __forceinline__ void commit_elect(uint64_t* bar) {
   } while (0)
 #endif
 
-template <bool kTN, int L>  // L = padded width (multiple of 32, <= 128)
+template <bool kTN, int L, bool kF16>  // L = padded width (multiple of 32, <= 128)
 __global__ void __launch_bounds__(kThreadsTC, 1)
     xs_tc_kernel(const __grid_constant__ CUtensorMap map_x, const __grid_constant__ CUtensorMap map_bh,
                  const __grid_constant__ CUtensorMap map_bl, const TcArgs args) {
-  using R = TcRings<L>;
+  using R = TcRings<L, kF16>;
+  constexpr int kDr = kF16 ? kDrain16 : kDrain;  // K-blocks per accumulator drain
   constexpr int kSX = R::kXStages, kSO = R::kOpStages, kSB = R::kBStages;
   constexpr uint32_t kTmemCols = R::kTmemCols;
 
@@ -348,10 +391,18 @@ __global__ void __launch_bounds__(kThreadsTC, 1)
           mbar_wait(&bempty[b], ph ^ 1);
           TC_EV(6, nblk++);
           mbar_expect_tx(&bfull[b], 2 * R::kBBytes);
+          if constexpr (kF16) {  // 64-half atoms of 32 K-rows x 128 B
 #pragma unroll
-          for (int a = 0; a < L / 32; ++a) {
-            tma(b_addr(b) + a * (kBK * 128), &map_bh, &bfull[b], 32 * a, (int)kk);
-            tma(b_addr(b) + (L / 32 + a) * (kBK * 128), &map_bl, &bfull[b], 32 * a, (int)kk);
+            for (int a = 0; a < R::LH / 64; ++a) {
+              tma(b_addr(b) + a * (kBK * 128), &map_bh, &bfull[b], 64 * a, (int)kk);
+              tma(b_addr(b) + (R::LH / 64 + a) * (kBK * 128), &map_bl, &bfull[b], 64 * a, (int)kk);
+            }
+          } else {
+#pragma unroll
+            for (int a = 0; a < L / 32; ++a) {
+              tma(b_addr(b) + a * (kBK * 128), &map_bh, &bfull[b], 32 * a, (int)kk);
+              tma(b_addr(b) + (L / 32 + a) * (kBK * 128), &map_bl, &bfull[b], 32 * a, (int)kk);
+            }
           }
           if (++b == kSB) {
             b = 0;
@@ -376,8 +427,8 @@ __global__ void __launch_bounds__(kThreadsTC, 1)
       for (int u = blockIdx.x; u < units; u += gridDim.x) {
         int64_t k0, k1;
         unit_k(u, k0, k1);
-        for (int64_t g0 = k0; g0 < k1; g0 += (int64_t)kDrain * kBK) {
-          const int64_t g1 = min(k1, g0 + (int64_t)kDrain * kBK);
+        for (int64_t g0 = k0; g0 < k1; g0 += (int64_t)kDr * kBK) {
+          const int64_t g1 = min(k1, g0 + (int64_t)kDr * kBK);
           mbar_wait_warp(&acc_empty[ab], aph ^ 1);
           tc_fence_after();
           const uint32_t d = tmem + ab * R::kAccCols;
@@ -388,7 +439,23 @@ __global__ void __launch_bounds__(kThreadsTC, 1)
             mbar_wait_warp(&bfull[b], bph);
             if (lane == 0) TC_EV(4, nblk);
             tc_fence_after();
-            const uint32_t ahi = tmem + R::kAOff + 64 * o;
+            const uint32_t ahi = tmem + R::kAOff + R::kASlot * o;
+            if constexpr (kF16) {
+              // two K = 16 steps: x_hi s_hi, x_hi s_lo, x_lo s_hi; A: 8 columns
+              // (16 halves) per step, x_lo 16 columns after x_hi; B: SWIZZLE_128B
+              // MN-major, 8-row groups 1 KB apart, atoms kBK x 128 B apart
+              constexpr uint32_t kLo16 = (R::LH / 64) * (kBK * 128);
+              const uint32_t id16 = idesc_f16(args.nmma, true);
+#pragma unroll
+              for (int ks = 0; ks < kBK / 16; ++ks) {
+                const uint64_t bh = smem_desc(b_addr(b) + ks * 2048, kBK * 128, 1024, 2);
+                const uint64_t bl = smem_desc(b_addr(b) + kLo16 + ks * 2048, kBK * 128, 1024, 2);
+                mma16_ts_elect(d, ahi + 8 * ks, bh, id16, acc);            // main
+                mma16_ts_elect(d + L, ahi + 8 * ks, bl, id16, acc);        // corrections
+                mma16_ts_elect(d + L, ahi + 16 + 8 * ks, bh, id16, 1u);
+                acc = 1u;
+              }
+            } else {
             // descriptor address field is addr >> 4 in the low bits: k-step
             // offsets (1 KB) are added to the base descriptors directly
             const uint64_t bh = desc_mn(b_addr(b), kBK * 128);
@@ -400,6 +467,7 @@ __global__ void __launch_bounds__(kThreadsTC, 1)
               mma_ts_elect(d, ahi + 8 * ks, bl + koff, idesc, 1u);
               mma_ts_elect(d, ahi + 32 + 8 * ks, bh + koff, idesc, 1u);
               acc = 1u;
+            }
             }
             commit_elect(&opempty[o]);  // A slot and S stage free once these MMAs complete
             commit_elect(&bempty[b]);
@@ -434,7 +502,23 @@ __global__ void __launch_bounds__(kThreadsTC, 1)
     for (int u = blockIdx.x; u < units; u += gridDim.x) {
       int64_t k0, k1;
       unit_k(u, k0, k1);
+      float row_scale = 1.f;  // NN fp16: 2^e of this thread's X row
+      int ecur[8], enxt[8];   // TN fp16: packed int8 exponents of the block's K rows
+      // rexp is zero-padded to a multiple of 4 bytes past the rows (xs_rexp_bytes)
+      auto load_e = [&](int64_t kb, int (&dst)[8]) {
+#pragma unroll
+        for (int j = 0; j < 8; ++j)
+          dst[j] = kb + 4 * j < args.kdim ? __ldg(reinterpret_cast<const int*>(args.rexp + kb) + j) : 0;
+      };
+      if constexpr (kF16 && !kTN) {
+        const int64_t row = (int64_t)(u % args.ntiles) * kBM + r;
+        row_scale = row < args.rows_out ? exp2i(args.rexp[row]) : 1.f;
+      }
+      if constexpr (kF16 && kTN) load_e(k0, ecur);
       for (int64_t kk = k0; kk < k1; kk += kBK) {
+        if constexpr (kF16 && kTN) {
+          if (kk + kBK < k1) load_e(kk + kBK, enxt);
+        }
         mbar_wait_warp(&xfull[s], xph);
         if (q == 0 && lane == 0) TC_EV(1, nblk);
         float v[32];
@@ -453,15 +537,43 @@ __global__ void __launch_bounds__(kThreadsTC, 1)
           for (int kq = 0; kq < 32; ++kq) v[kq] = lds32(x_addr(s) + kq * (kBM * 4) + r * 4);
         }
         uint32_t hi[32], lo[32];
+        if constexpr (kF16) {
+          // exact power-of-two scaling into fp16's normal range, then the
+          // hi / lo fp16 split: words 0..15 = x_hi pairs, 16..31 = x_lo pairs
+          // (even k in the low half)
+          if constexpr (!kTN) {
 #pragma unroll
-        for (int j = 0; j < 32; ++j) tf32_split_bits(v[j], hi[j], lo[j]);
+            for (int j = 0; j < 32; ++j) v[j] *= row_scale;
+          } else {
+            // the block's 32 K-row exponents were loaded one block ahead
+#pragma unroll
+            for (int j = 0; j < 32; j += 4)
+#pragma unroll
+              for (int u = 0; u < 4; ++u) v[j + u] *= exp2i((int)(int8_t)(ecur[j >> 2] >> (8 * u)));
+          }
+#pragma unroll
+          for (int j = 0; j < 16; ++j) {
+            const __half2 h = __floats2half2_rn(v[2 * j], v[2 * j + 1]);
+            const float2 hf = __half22float2(h);
+            const __half2 l2 = __floats2half2_rn(v[2 * j] - hf.x, v[2 * j + 1] - hf.y);
+            hi[j] = *reinterpret_cast<const uint32_t*>(&h);
+            hi[16 + j] = *reinterpret_cast<const uint32_t*>(&l2);
+          }
+        } else {
+#pragma unroll
+          for (int j = 0; j < 32; ++j) tf32_split_bits(v[j], hi[j], lo[j]);
+        }
         mbar_wait_warp(&opempty[o], oph ^ 1);
         if (q == 0 && lane == 0) TC_EV(2, nblk);
         tc_fence_after();
         {
-          const uint32_t ta = tmem + ((uint32_t)(32 * q) << 16) + R::kAOff + 64 * o;
-          tmem_st32(ta, hi);
-          tmem_st32(ta + 32, lo);
+          const uint32_t ta = tmem + ((uint32_t)(32 * q) << 16) + R::kAOff + R::kASlot * o;
+          if constexpr (kF16) {
+            tmem_st32(ta, hi);
+          } else {
+            tmem_st32(ta, hi);
+            tmem_st32(ta + 32, lo);
+          }
           asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
         }
         tc_fence_before();
@@ -476,6 +588,10 @@ __global__ void __launch_bounds__(kThreadsTC, 1)
         if (lane == 0) mbar_arrive(&xempty[s]);
         if (q == 0 && lane == 0) TC_EV(3, nblk);
         if (lane == 0) TC_EV(8 + q, nblk);  // per-quarter split done (tools/tc_trace.cu)
+        if constexpr (kF16 && kTN) {
+#pragma unroll
+          for (int j = 0; j < 8; ++j) ecur[j] = enxt[j];
+        }
         ++nblk;
         if (++s == kSX) {
           s = 0;
@@ -499,7 +615,7 @@ __global__ void __launch_bounds__(kThreadsTC, 1)
       float run[L];
 #pragma unroll
       for (int c = 0; c < L; ++c) run[c] = 0.f;
-      for (int64_t g0 = k0; g0 < k1; g0 += (int64_t)kDrain * kBK) {
+      for (int64_t g0 = k0; g0 < k1; g0 += (int64_t)kDr * kBK) {
         mbar_wait_warp(&acc_full[ab], aph);
         tc_fence_after();
         const uint32_t base = tmem + ab * R::kAccCols + ((uint32_t)(32 * q) << 16);
@@ -531,9 +647,20 @@ __global__ void __launch_bounds__(kThreadsTC, 1)
       const int64_t row = (int64_t)tile * kBM + 32 * q + lane;
       if (row < args.rows_out) {
         float* dst = args.out + ((int64_t)split * args.rows_out + row) * args.lp;
+        if constexpr (kF16) {  // undo the power-of-two scalings (exact)
+          const float rs = kTN ? 1.f : exp2i(-(int)args.rexp[row]);
 #pragma unroll
-        for (int c = 0; c < L; c += 4)
-          if (c < args.lp) *reinterpret_cast<float4*>(dst + c) = make_float4(run[c], run[c + 1], run[c + 2], run[c + 3]);
+          for (int c = 0; c < L; c += 4)
+            if (c < args.lp) {
+              const float4 cs = __ldg(reinterpret_cast<const float4*>(args.cscale + c));
+              *reinterpret_cast<float4*>(dst + c) = make_float4(run[c] * rs * cs.x, run[c + 1] * rs * cs.y,
+                                                                run[c + 2] * rs * cs.z, run[c + 3] * rs * cs.w);
+            }
+        } else {
+#pragma unroll
+          for (int c = 0; c < L; c += 4)
+            if (c < args.lp) *reinterpret_cast<float4*>(dst + c) = make_float4(run[c], run[c + 1], run[c + 2], run[c + 3]);
+        }
       }
     }
   }
@@ -562,6 +689,84 @@ __global__ void split_tf32_kernel(const float* __restrict__ s, int64_t rows, int
     asm("cvt.rna.tf32.f32 %0, %1;" : "=r"(l2) : "f"(rem));
     hi[e] = __uint_as_float(h);
     lo[e] = __uint_as_float(l2);
+  }
+}
+
+// fp16 path: per-column max |s'| of s' = s * 2^-rexp[row] (TN; s' = s for
+// NN), as float bits (non-negative floats order like unsigned ints).
+__global__ void s_colmax_kernel(const float* __restrict__ s, int64_t rows, int lp,
+                                const int8_t* __restrict__ rexp, unsigned* __restrict__ cmax) {
+  const int c = threadIdx.x;
+  if (c >= lp) return;
+  float m = 0.f;
+  for (int64_t r = blockIdx.x; r < rows; r += gridDim.x) {
+    float v = fabsf(s[r * lp + c]);
+    if (rexp) v *= exp2i(-(int)rexp[r]);
+    m = fmaxf(m, v);
+  }
+  atomicMax(cmax + c, __float_as_uint(m));
+}
+
+// Column exponent f with max * 2^f in [2^14, 2^15) (fp16's normal range with
+// one binade of headroom), clamped to the float exponent range.
+__device__ __forceinline__ int col_exponent(unsigned bits) {
+  if (bits == 0u) return 0;
+  int e;
+  frexpf(__uint_as_float(bits), &e);
+  return max(-126, min(126, 15 - e));
+}
+
+// s' (rows x lp) -> s_hi, s_lo fp16 (rows x LH, zero padded), scaled by 2^f
+// per column; cscale[c] = 2^-f.  Triggers the dependent contraction at once.
+__global__ void split_f16_kernel(const float* __restrict__ s, int64_t rows, int lp, int LH,
+                                 const int8_t* __restrict__ rexp, const unsigned* __restrict__ cmax,
+                                 __half* __restrict__ hi, __half* __restrict__ lo,
+                                 float* __restrict__ cscale) {
+  asm volatile("griddepcontrol.launch_dependents;");
+  for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < rows * LH;
+       e += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t r = e / LH;
+    const int c = (int)(e - r * LH);
+    float v = 0.f;
+    if (c < lp) {
+      v = s[r * lp + c];
+      if (rexp) v *= exp2i(-(int)rexp[r]);
+      v *= exp2i(col_exponent(cmax[c]));
+    }
+    const __half h = __float2half_rn(v);
+    hi[e] = h;
+    lo[e] = __float2half_rn(v - __half2float(h));
+  }
+  if (blockIdx.x == 0)
+    for (int c = threadIdx.x; c < LH; c += blockDim.x)
+      cscale[c] = c < lp ? exp2i(-col_exponent(cmax[c])) : 0.f;
+}
+
+// Per-row exponents of X for the fp16 path (NN rows / TN K index): row max
+// scaled into [2^14, 2^15); `wide` is set when a row's smallest nonzero
+// magnitude is below 2^-30 of its max (fp16's subnormal range would cost
+// accuracy there: the caller then keeps the 3xTF32 path).
+__global__ void x_rowexp_kernel(const float* __restrict__ x, int64_t ldx, int64_t d, int64_t n,
+                                int8_t* __restrict__ rexp, int* __restrict__ wide) {
+  const int lane = threadIdx.x & 31;
+  const int64_t warps = (int64_t)gridDim.x * (blockDim.x >> 5);
+  for (int64_t i = blockIdx.x * (int64_t)(blockDim.x >> 5) + (threadIdx.x >> 5); i < d; i += warps) {
+    const float* row = x + i * ldx;
+    float mx = 0.f, mn = INFINITY;
+    for (int64_t j = lane; j < n; j += 32) {
+      const float v = fabsf(__ldg(row + j));
+      mx = fmaxf(mx, v);
+      if (v > 0.f) mn = fminf(mn, v);
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+      mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, o));
+      mn = fminf(mn, __shfl_xor_sync(0xffffffffu, mn, o));
+    }
+    if (lane == 0) {
+      rexp[i] = (int8_t)max(-126, min(126, mx > 0.f ? 15 - [&] { int e; frexpf(mx, &e); return e; }() : 0));
+      if (mx > 0.f && mn < mx * 0x1.0p-30f) atomicOr(wide, 1);
+    }
   }
 }
 
@@ -601,15 +806,16 @@ PFN_cuTensorMapEncodeTiled_v12000 encode_fn() {
 
 // 2D fp32 row-major tensor (rows x cols, row pitch ld floats), box_cols x
 // box_rows boxes.
-bool make_map(CUtensorMap* m, const float* base, int64_t rows, int64_t cols, int64_t ld,
-              int box_cols, int box_rows, CUtensorMapSwizzle sw) {
+bool make_map(CUtensorMap* m, const void* base, int64_t rows, int64_t cols, int64_t ld,
+              int box_cols, int box_rows, CUtensorMapSwizzle sw, bool f16 = false) {
   auto fn = encode_fn();
   if (!fn) return false;
   const cuuint64_t dims[2] = {(cuuint64_t)cols, (cuuint64_t)rows};
-  const cuuint64_t strides[1] = {(cuuint64_t)(ld * 4)};
+  const cuuint64_t strides[1] = {(cuuint64_t)(ld * (f16 ? 2 : 4))};
   const cuuint32_t box[2] = {(cuuint32_t)box_cols, (cuuint32_t)box_rows};
   const cuuint32_t estr[2] = {1, 1};
-  return fn(m, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2, const_cast<float*>(base), dims, strides, box,
+  return fn(m, f16 ? CU_TENSOR_MAP_DATA_TYPE_FLOAT16 : CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2,
+            const_cast<void*>(base), dims, strides, box,
             estr, CU_TENSOR_MAP_INTERLEAVE_NONE, sw, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
             CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
 }
@@ -669,18 +875,18 @@ TcPlan tc_plan(int64_t rows_out, int64_t kdim, int nsm) {
   return p;
 }
 
-template <bool kTN, int L>
+template <bool kTN, int L, bool kF16>
 cudaError_t run_tc(const CUtensorMap& mx, const CUtensorMap& mh, const CUtensorMap& ml,
                    const TcArgs& a, int grid, cudaStream_t st) {
-  constexpr int smem = TcRings<L>::kBytes + 1024;
+  constexpr int smem = TcRings<L, kF16>::kBytes + 1024;
   static bool attr = false;
   if (!attr) {
-    cudaFuncSetAttribute(xs_tc_kernel<kTN, L>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+    cudaFuncSetAttribute(xs_tc_kernel<kTN, L, kF16>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
     attr = true;
   }
   note_launches(1);
-  return launch_pdl(xs_tc_kernel<kTN, L>, dim3(grid), dim3(kThreadsTC), (size_t)smem, st, mx, mh,
-                    ml, a);
+  return launch_pdl(xs_tc_kernel<kTN, L, kF16>, dim3(grid), dim3(kThreadsTC), (size_t)smem, st, mx,
+                    mh, ml, a);
 }
 
 }  // namespace
@@ -691,28 +897,61 @@ size_t xstream_tc_ws_floats(int64_t m, int64_t n, int lp, int nsm) {
   const int L = (lp + 31) & ~31;
   const TcPlan a = tc_plan(m, n, nsm), b = tc_plan(n, m, nsm);
   const int64_t parts = std::max<int64_t>((int64_t)a.nsplit * m * lp, (int64_t)b.nsplit * n * lp);
-  return (size_t)(parts + 2 * std::max(m, n) * (int64_t)L + 64);
+  return (size_t)(parts + 2 * std::max(m, n) * (int64_t)L + 512 + 64);
 }
 
+size_t xs_rexp_bytes(int64_t rows) { return (size_t)((rows + 3) / 4 * 4 + 64); }
+
+void launch_x_rowexp(const float* x, int64_t ldx, int64_t d, int64_t n, int8_t* rexp, int* wide,
+                     int nsm, cudaStream_t st) {
+  cudaMemsetAsync(rexp, 0, xs_rexp_bytes(d), st);  // the padding must read as exponent 0
+  note_launches(1);
+  x_rowexp_kernel<<<(int)std::max<int64_t>(1, std::min<int64_t>((d + 7) / 8, (int64_t)nsm * 16)), 256,
+                    0, st>>>(x, ldx, d, n, rexp, wide);
+}
+
+// rexp != nullptr selects the fp16 hi/lo path (per-row power-of-two scaling
+// of X, per-column scaling of S): half the tensor-memory operand bytes and
+// half the MMA time of 3xTF32 at the same 22-bit operand precision.
 bool launch_xs_tc(bool tn, const float* x, int64_t ldx, int64_t m, int64_t n, const float* s,
-                  int lp, float* out, float* ws, int nsm, cudaStream_t st) {
+                  int lp, float* out, float* ws, int nsm, cudaStream_t st, const int8_t* rexp) {
   const int L = (lp + 31) & ~31;
   if (L > 128 || (ldx % 4) != 0 || (reinterpret_cast<uintptr_t>(x) & 15)) return false;
+  const bool f16 = rexp != nullptr && L <= 96;  // two accumulators fit TMEM up to L = 96
+  const int LH = (L + 63) & ~63;
   const int64_t rows_out = tn ? n : m, kdim = tn ? m : n;
   const TcPlan p = tc_plan(rows_out, kdim, nsm);
   float* hi = ws;
   float* lo = ws + kdim * (int64_t)L;
-  float* parts = lo + kdim * (int64_t)L;
-  note_launches(1);
-  split_tf32_kernel<<<std::min<int64_t>((kdim * L + 255) / 256, nsm * 8), 256, 0, st>>>(
-      s, kdim, lp, L, hi, lo);
+  unsigned* cmax = reinterpret_cast<unsigned*>(ws + 2 * kdim * (int64_t)L);
+  float* cscale = ws + 2 * kdim * (int64_t)L + 256;
+  float* parts = ws + 2 * kdim * (int64_t)L + 512;
+  __half* hi16 = reinterpret_cast<__half*>(hi);
+  __half* lo16 = reinterpret_cast<__half*>(lo);
+  if (f16) {
+    if (cudaMemsetAsync(cmax, 0, sizeof(unsigned) * 128, st) != cudaSuccess) return false;
+    note_launches(2);
+    s_colmax_kernel<<<(int)std::max<int64_t>(1, std::min<int64_t>(kdim, (int64_t)nsm * 2)), 128, 0, st>>>(
+        s, kdim, lp, tn ? rexp : nullptr, cmax);
+    split_f16_kernel<<<std::min<int64_t>((kdim * LH + 255) / 256, nsm * 8), 256, 0, st>>>(
+        s, kdim, lp, LH, tn ? rexp : nullptr, cmax, hi16, lo16, cscale);
+  } else {
+    note_launches(1);
+    split_tf32_kernel<<<std::min<int64_t>((kdim * L + 255) / 256, nsm * 8), 256, 0, st>>>(
+        s, kdim, lp, L, hi, lo);
+  }
   CUtensorMap mx, mh, ml;
   // X: NN boxes 32 (k) x 128 (rows), 128 B swizzle; TN boxes 128 x 32 (k), unswizzled.
-  // S hi / lo: MN-major operand atoms, 32 x 32 boxes, 128 B swizzle with 32 B atoms.
+  // S hi / lo: MN-major operand atoms: tf32 32 x 32 boxes, 128 B swizzle with
+  // 32 B atoms; fp16 64 x 32 boxes, 128 B swizzle.
   bool ok = tn ? make_map(&mx, x, m, n, ldx, kBM, kBK, CU_TENSOR_MAP_SWIZZLE_NONE)
                : make_map(&mx, x, m, n, ldx, kBK, kBM, CU_TENSOR_MAP_SWIZZLE_128B);
-  ok = ok && make_map(&mh, hi, kdim, L, L, 32, kBK, CU_TENSOR_MAP_SWIZZLE_128B_ATOM_32B) &&
-       make_map(&ml, lo, kdim, L, L, 32, kBK, CU_TENSOR_MAP_SWIZZLE_128B_ATOM_32B);
+  if (f16)
+    ok = ok && make_map(&mh, hi16, kdim, LH, LH, 64, kBK, CU_TENSOR_MAP_SWIZZLE_128B, true) &&
+         make_map(&ml, lo16, kdim, LH, LH, 64, kBK, CU_TENSOR_MAP_SWIZZLE_128B, true);
+  else
+    ok = ok && make_map(&mh, hi, kdim, L, L, 32, kBK, CU_TENSOR_MAP_SWIZZLE_128B_ATOM_32B) &&
+         make_map(&ml, lo, kdim, L, L, 32, kBK, CU_TENSOR_MAP_SWIZZLE_128B_ATOM_32B);
   if (!ok) return false;
   TcArgs a;
   a.rows_out = rows_out;
@@ -724,20 +963,22 @@ bool launch_xs_tc(bool tn, const float* x, int64_t ldx, int64_t m, int64_t n, co
   a.out = p.nsplit > 1 ? parts : out;
   a.dbg = g_tc_debug;
   a.nmma = (lp + 15) & ~15;
+  a.rexp = rexp;
+  a.cscale = cscale;
   const int units = p.ntiles * p.nsplit;
   const int grid = std::min(units, nsm);
   cudaError_t e;
+#define XS_CASE(TN, LL)                                                  \
+  case (TN ? 1000 : 0) + LL:                                             \
+    e = (f16 && LL <= 96) ? run_tc<TN, (LL <= 96 ? LL : 96), true>(mx, mh, ml, a, grid, st) \
+                          : run_tc<TN, LL, false>(mx, mh, ml, a, grid, st);                \
+    break;
   switch ((tn ? 1000 : 0) + L) {
-    case 32: e = run_tc<false, 32>(mx, mh, ml, a, grid, st); break;
-    case 64: e = run_tc<false, 64>(mx, mh, ml, a, grid, st); break;
-    case 96: e = run_tc<false, 96>(mx, mh, ml, a, grid, st); break;
-    case 128: e = run_tc<false, 128>(mx, mh, ml, a, grid, st); break;
-    case 1032: e = run_tc<true, 32>(mx, mh, ml, a, grid, st); break;
-    case 1064: e = run_tc<true, 64>(mx, mh, ml, a, grid, st); break;
-    case 1096: e = run_tc<true, 96>(mx, mh, ml, a, grid, st); break;
-    case 1128: e = run_tc<true, 128>(mx, mh, ml, a, grid, st); break;
+    XS_CASE(false, 32) XS_CASE(false, 64) XS_CASE(false, 96) XS_CASE(false, 128)
+    XS_CASE(true, 32) XS_CASE(true, 64) XS_CASE(true, 96) XS_CASE(true, 128)
     default: return false;
   }
+#undef XS_CASE
   if (e != cudaSuccess) return false;
   if (p.nsplit > 1) {
     const int64_t total4 = rows_out * lp / 4;
