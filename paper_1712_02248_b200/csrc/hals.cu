@@ -382,6 +382,16 @@ __device__ __forceinline__ void load_gram(double* gw, const double* __restrict__
     gw[e] = c < k ? (cg ? __ldcg(src + r * k + c) : src[r * k + c]) : 0.0;
   }
 }
+template <int N>
+__device__ __forceinline__ void loadn(const double* p, double (&v)[N]) {
+  const double2* q = reinterpret_cast<const double2*>(p);
+#pragma unroll
+  for (int u = 0; u < N / 2; ++u) {
+    const double2 t = q[u];
+    v[2 * u] = t.x;
+    v[2 * u + 1] = t.y;
+  }
+}
 __device__ __forceinline__ void load8(const double* p, double (&v)[8]) {
   const double2* q = reinterpret_cast<const double2*>(p);
 #pragma unroll
@@ -392,7 +402,10 @@ __device__ __forceinline__ void load8(const double* p, double (&v)[8]) {
   }
 }
 
-template <int RPT>
+// RPT: A rows per thread; NB: columns per sweep block (16 halves the sweeps'
+// re-reads of A and B -- one pass over all k columns per block -- where the
+// registers allow it; the 6-row instance keeps 8).
+template <int RPT, int NB>
 __global__ void __launch_bounds__(kThreads, 1) hals_kernel(const HalsArgs p) {
   extern __shared__ __align__(16) double smem[];
   __shared__ double red8[kThreads / 32];
@@ -405,7 +418,7 @@ __global__ void __launch_bounds__(kThreads, 1) hals_kernel(const HalsArgs p) {
 
   const HalsState& S = p.st;
   const int G = gridDim.x, cta = blockIdx.x, tid = threadIdx.x;
-  const int k = S.k, lp = S.lp, l = S.l, kp1 = k + 1, lpp = lp + 1, kg = (k + 7) & ~7;
+  const int k = S.k, lp = S.lp, l = S.l, kp1 = k + 1, lpp = lp + 1, kg = (k + 15) & ~15;
   const int64_t d = S.d, n = S.n;
   const int64_t a_lo = min(d, (int64_t)cta * p.rows_a), a_hi = min(d, a_lo + p.rows_a);
   const int64_t b_lo = min(n, (int64_t)cta * p.rows_b), b_hi = min(n, b_lo + p.rows_b);
@@ -474,14 +487,14 @@ __global__ void __launch_bounds__(kThreads, 1) hals_kernel(const HalsArgs p) {
       // the block's later accumulators (the reference's running A g_j, with
       // the same fp64 operation order as summing the deltas per column).
       // One all-reduce per column for the norm.
-      for (int jb = col0 & ~(kNB - 1); jb < jd; jb += kNB) {
-        const int t0 = max(col0 - jb, 0), nbj = min(kNB, jd - jb);
+      for (int jb = col0 & ~(NB - 1); jb < jd; jb += NB) {
+        const int t0 = max(col0 - jb, 0), nbj = min(NB, jd - jb);
         if (t0 >= nbj) continue;  // resumed at col0 == jd: nothing left in this block
-        double acc[RPT][kNB];
+        double acc[RPT][NB];
 #pragma unroll
         for (int i = 0; i < RPT; ++i)
 #pragma unroll
-          for (int t = 0; t < kNB; ++t) acc[i][t] = 0.0;
+          for (int t = 0; t < NB; ++t) acc[i][t] = 0.0;
         for (int c0 = 0; c0 < k; c0 += 4) {  // 4 columns of A in flight per row
           double av4[RPT][4];
 #pragma unroll
@@ -495,12 +508,12 @@ __global__ void __launch_bounds__(kThreads, 1) hals_kernel(const HalsArgs p) {
 #pragma unroll
           for (int cc = 0; cc < 4; ++cc) {
             if (c0 + cc >= k) break;
-            double gv[kNB];  // padded columns (>= k) are zero
-            load8(gw + (c0 + cc) * kg + jb, gv);
+            double gv[NB];  // padded columns (>= k) are zero
+            loadn<NB>(gw + (c0 + cc) * kg + jb, gv);
 #pragma unroll
             for (int i = 0; i < RPT; ++i)
 #pragma unroll
-              for (int t = 0; t < kNB; ++t) acc[i][t] = fma(av4[i][cc], gv[t], acc[i][t]);
+              for (int t = 0; t < NB; ++t) acc[i][t] = fma(av4[i][cc], gv[t], acc[i][t]);
           }
         }
         double hv[RPT], av[RPT];
@@ -516,7 +529,7 @@ __global__ void __launch_bounds__(kThreads, 1) hals_kernel(const HalsArgs p) {
         }
         HALS_PROF(2);
 #pragma unroll
-        for (int t = 0; t < kNB; ++t) {
+        for (int t = 0; t < NB; ++t) {
           if (t < t0) continue;
           if (t >= nbj) break;
           const int j = jb + t;
@@ -557,8 +570,8 @@ __global__ void __launch_bounds__(kThreads, 1) hals_kernel(const HalsArgs p) {
             return;
           }
           const double inv_nrm = s_red[1];
-          double gr[kNB];  // row j of g: the later columns' coefficients of a_j
-          load8(gw + j * kg + jb, gr);
+          double gr[NB];  // row j of g: the later columns' coefficients of a_j
+          loadn<NB>(gw + j * kg + jb, gr);
 #pragma unroll
           for (int i = 0; i < RPT; ++i) {
             const int r = tid + kThreads * i;
@@ -567,7 +580,7 @@ __global__ void __launch_bounds__(kThreads, 1) hals_kernel(const HalsArgs p) {
               S.a[(int64_t)j * d + a_lo + r] = nf;
               const double dlt = nf - av[i];
 #pragma unroll
-              for (int u = 0; u < kNB; ++u)
+              for (int u = 0; u < NB; ++u)
                 if (u > t) acc[i][u] = fma(dlt, gr[u], acc[i][u]);
             }
             hv[i] = hn[i];
@@ -645,15 +658,15 @@ __global__ void __launch_bounds__(kThreads, 1) hals_kernel(const HalsArgs p) {
           okr[i] = r < nbr;
           gr[i] = b_lo + (okr[i] ? r : 0);
         }
-        for (int jb = col0 & ~(kNB - 1); jb < jd; jb += kNB) {
-          const int t0 = max(col0 - jb, 0), nbj = min(kNB, jd - jb);
+        for (int jb = col0 & ~(NB - 1); jb < jd; jb += NB) {
+          const int t0 = max(col0 - jb, 0), nbj = min(NB, jd - jb);
           if (t0 >= nbj) continue;  // resumed at col0 == jd: nothing left in this block
           const int jbe = jb + t0;  // columns < jbe already live in bnxt
-          double acc[RB][kNB];
+          double acc[RB][NB];
   #pragma unroll
           for (int i = 0; i < RB; ++i)
   #pragma unroll
-            for (int t = 0; t < kNB; ++t) acc[i][t] = 0.0;
+            for (int t = 0; t < NB; ++t) acc[i][t] = 0.0;
           // software-pipelined: the next 4 columns' loads are in flight while
           // the current 4 are multiplied (the loop was latency-bound)
           double bv4[RB][4], bvn[RB][4];
@@ -672,12 +685,12 @@ __global__ void __launch_bounds__(kThreads, 1) hals_kernel(const HalsArgs p) {
   #pragma unroll
             for (int cc = 0; cc < 4; ++cc) {
               if (c0 + cc >= k) break;
-              double gv[kNB];
-              load8(gw + (c0 + cc) * kg + jb, gv);
+              double gv[NB];
+              loadn<NB>(gw + (c0 + cc) * kg + jb, gv);
   #pragma unroll
               for (int i = 0; i < RB; ++i)
   #pragma unroll
-                for (int t = 0; t < kNB; ++t) acc[i][t] = fma(bv4[i][cc], gv[t], acc[i][t]);
+                for (int t = 0; t < NB; ++t) acc[i][t] = fma(bv4[i][cc], gv[t], acc[i][t]);
             }
   #pragma unroll
             for (int i = 0; i < RB; ++i)
@@ -698,15 +711,15 @@ __global__ void __launch_bounds__(kThreads, 1) hals_kernel(const HalsArgs p) {
           };
           load_bp(jbe, bb, pb);
   #pragma unroll
-          for (int t = 0; t < kNB; ++t) {
+          for (int t = 0; t < NB; ++t) {
             if (t < t0) continue;
             if (t >= nbj) break;
             const int j = jb + t;
             const double wjj = s_diag[j];
             double bn[RB], pn[RB];
             load_bp(j + 1, bn, pn);
-            double grow[kNB];
-            load8(gw + j * kg + jb, grow);
+            double grow[NB];
+            loadn<NB>(gw + j * kg + jb, grow);
             bool nz = false;
   #pragma unroll
             for (int i = 0; i < RB; ++i) {
@@ -722,7 +735,7 @@ __global__ void __launch_bounds__(kThreads, 1) hals_kernel(const HalsArgs p) {
               }
               const double dlt = vf - bij;
   #pragma unroll
-              for (int u = 0; u < kNB; ++u)
+              for (int u = 0; u < NB; ++u)
                 if (u > t) acc[i][u] = fma(dlt, grow[u], acc[i][u]);
               bb[i] = bn[i];
               pb[i] = pn[i];
@@ -816,7 +829,7 @@ size_t hals_smem_bytes(const HalsState& st, int /*rows_a*/) {
   const int64_t k = st.k, lp = st.lp, l = st.l, kp1 = k + 1, lpp = lp + 1;
   const int64_t k4 = (k + 3) & ~3;
   const int64_t prod = lp * k + (kRing * (int64_t)rts_stage_floats((int)lp) + 1) / 2;
-  const int64_t sweep = k * ((k + 7) & ~7);
+  const int64_t sweep = k * ((k + 15) & ~15);
   const int64_t part = (kRing * partial_stage_bytes((int)lp, (int)k) + 7) / 8;  // cp.async ring
   const int64_t gram = ((l + 3) & ~3) * ((k + 7) & ~7);
   return (size_t)std::max(std::max(prod, sweep), std::max(part, gram)) * sizeof(double);
@@ -886,7 +899,7 @@ cudaError_t launch_hals(const HalsState& st, int normalize_a, double alpha, doub
   const int rpt = (a.rows_a + kThreads - 1) / kThreads;
   if (rpt > kMaxRPTLarge) return cudaErrorInvalidConfiguration;
   const bool large = rpt > 3 || std::getenv("CNMF_HALS_RPT6") != nullptr;  // env: tests only
-  const void* fn = large ? (const void*)hals_kernel<kMaxRPTLarge> : (const void*)hals_kernel<3>;
+  const void* fn = large ? (const void*)hals_kernel<kMaxRPTLarge, 8> : (const void*)hals_kernel<3, 16>;
   cudaError_t e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   if (e != cudaSuccess) return e;
   void* args[] = {&a};
