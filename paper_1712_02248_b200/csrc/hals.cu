@@ -61,49 +61,12 @@ struct HalsArgs {
 };
 
 // ---- streamed products ----------------------------------------------------
-// Both routines stream the CTA's rows of an fp32 matrix (ld lp) in 64-row
-// stages converted to fp64 in shared memory (stride lp + 1: conflict-free
-// column reads), with the NEXT stage prefetched into registers while the
-// current one is computed, and 4 x 4 register tiles whose warps span rows
-// (X reads conflict-free, M / F reads broadcast): ~64 FMAs per shared-memory
-// wavefront, the DFMA rate.
+// The row products (rows_times_small) and the partials (small_partial)
+// stream the CTA's rows of an fp32 matrix (ld lp) through 3-deep cp.async
+// rings and multiply on the FP64 tensor cores (m8n8k4 DMMA, fp32 operands
+// widened in registers); see each routine for its warp tiling.
 constexpr int kSR = 64;                 // rows per stage
-constexpr int kPF = 8;                  // float4 per thread per stage (lp <= 128)
 
-struct StagePrefetch {
-  float4 v[kPF];
-  int rr[kPF], c4[kPF];  // this thread's (row, float4 column) per slot; rr = kSR when idle
-  __device__ __forceinline__ void init(int lp) {  // once per product: no per-stage division
-    const int q4 = lp >> 2, total = kSR * q4;
-#pragma unroll
-    for (int u = 0; u < kPF; ++u) {
-      const int e = threadIdx.x + kThreads * u;
-      rr[u] = e < total ? e / q4 : kSR;
-      c4[u] = e < total ? e - rr[u] * q4 : 0;
-    }
-  }
-  __device__ __forceinline__ void load(const float* __restrict__ in, int r0, int nrows, int lp) {
-#pragma unroll
-    for (int u = 0; u < kPF; ++u) {
-      v[u] = make_float4(0.f, 0.f, 0.f, 0.f);
-      if (rr[u] < kSR && r0 + rr[u] < nrows)
-        v[u] = __ldg(reinterpret_cast<const float4*>(in + (int64_t)(r0 + rr[u]) * lp) + c4[u]);
-    }
-  }
-  __device__ __forceinline__ void store(int lp, double* stage) const {
-    const int lpp = lp + 1;
-#pragma unroll
-    for (int u = 0; u < kPF; ++u) {
-      if (rr[u] < kSR) {
-        double* dd = stage + rr[u] * lpp + 4 * c4[u];
-        dd[0] = v[u].x;
-        dd[1] = v[u].y;
-        dd[2] = v[u].z;
-        dd[3] = v[u].w;
-      }
-    }
-  }
-};
 
 
 // FP64 tensor-core MMA, D (8 x 8) += A (8 x 4, row) B (4 x 8, col): lane
