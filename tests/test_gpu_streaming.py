@@ -4,9 +4,10 @@ CNMF_HALS=stream, against the CPU oracle (the restatement of
 proj/src/solvers.cpp:414-509, pinned to the compiled reference in
 tests/test_oracle.py).
 
-  * redraw halts inside an 8-column block (k = 12, every column emptied):
-    the kernel resumes at an unaligned column and the sweeps start from an
-    8-aligned block with the already-updated columns skipped;
+  * redraw halts inside a sweep block (k = 12 and k = 40, every column
+    emptied): the kernel resumes at unaligned columns and the sweeps start
+    from an aligned block with the already-updated columns skipped;
+  * k = 100 (several 16-column blocks, 128-wide views);
   * penalised B updates (solvers.cpp:502-508) with k > 8;
   * A heights above 768 rows per SM (d = 120000 on 148 SMs): the 6-rows-per-
     thread instance of the A sweep (BASELINE configs[4] height class).
@@ -70,7 +71,7 @@ def test_streaming_steps_k20(ctx, oracle, stream):
 def test_streaming_emptied_columns_unaligned_resume(ctx, oracle, stream):
     """Zero compressed views with k = 12: every A and B column empties and is
     redrawn, so the kernel halts and resumes at columns 1..11 (inside the
-    8-column blocks) in both halves (solvers.cpp:435, 452)."""
+    sweep blocks) in both halves (solvers.cpp:435, 452)."""
     x = oracle.synth_x(300, 200, 4, 0, 1, 0.01, 8).astype(np.float64)
     left, right = oracle.build_projectors(x, 14, 1, 2)
     xhat, xcheck = np.zeros((14, 200)), np.zeros((300, 14))
@@ -84,6 +85,40 @@ def test_streaming_emptied_columns_unaligned_resume(ctx, oracle, stream):
         oracle.fasthals_rp_step(xhat, xcheck, a, b, ah, bc, left, right, True, 0.0, 0.0, rng)
     assert redraws >= 24
     for got, want in ((ta, a), (tb, b), (tbc, bc)):
+        assert rel_fro(host(got), want) < FACTOR_RTOL
+
+
+def test_streaming_emptied_columns_many_blocks(ctx, oracle, stream):
+    """k = 40 (three 16-column sweep blocks, the last partial) with zero
+    views: every column of both halves empties and is redrawn, so the kernel
+    resumes at every in-block position of every block."""
+    x = oracle.synth_x(500, 400, 6, 0, 1, 0.01, 9).astype(np.float64)
+    left, right = oracle.build_projectors(x, 44, 1, 3)
+    xhat, xcheck = np.zeros((44, 400)), np.zeros((500, 44))
+    a, b = oracle.initialize(500, 400, 40, 6)
+    ah, bc = oracle.compress_factors(a, b, left, right)
+    ta, tb, tah, tbc = dev(a), dev(b), dev64(ah), dev64(bc)
+    redraws = ctx.fasthals_rp_steps(dev(xhat), dev(xcheck), dev(left), dev(right), ta, tb, tah,
+                                    tbc, True, 0.0, 0.0, 13, 1)
+    rng = oracle.rng(13)
+    oracle.fasthals_rp_step(xhat, xcheck, a, b, ah, bc, left, right, True, 0.0, 0.0, rng)
+    assert redraws >= 80
+    for got, want in ((ta, a), (tb, b), (tbc, bc)):
+        assert rel_fro(host(got), want) < FACTOR_RTOL
+
+
+def test_streaming_steps_k100(ctx, oracle, stream):
+    """k = 100, l = 110 (the C4 class: seven 16-column blocks, 128-wide
+    views) -- plain steps against the oracle."""
+    _, left, right, xhat, xcheck, a, b, ah, bc = _fixture(oracle, 900, 700, 100, 110, 1, 2, 3, 4,
+                                                          rank=20)
+    ta, tb, tah, tbc = dev(a), dev(b), dev64(ah), dev64(bc)
+    ctx.fasthals_rp_steps(dev(xhat), dev(xcheck), dev(left), dev(right), ta, tb, tah, tbc,
+                          True, 0.0, 0.0, 8, 3)
+    rng = oracle.rng(8)
+    for _ in range(3):
+        oracle.fasthals_rp_step(xhat, xcheck, a, b, ah, bc, left, right, True, 0.0, 0.0, rng)
+    for got, want in ((ta, a), (tb, b), (tah, ah), (tbc, bc)):
         assert rel_fro(host(got), want) < FACTOR_RTOL
 
 
