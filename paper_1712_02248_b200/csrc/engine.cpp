@@ -121,18 +121,18 @@ double uniform_positive(std::mt19937_64& e) {
   return v;
 }
 
-// nwords outputs of Rng(seed) into words.  Long streams use jump-ahead: K
-// segments of J outputs generated in parallel from states computed with the
-// GF(2) jump polynomials (mt_jump.cpp, rng.cu) -- bitwise the same stream;
-// J = the next power of two >= max(32768, nwords / nsm), so K <= nsm.  Below
-// 2^20 words the single-CTA engine wins (measured: C2's 360K-word sketch
-// 1.87 vs 2.19 ms of compression; C3 32.0 -> 26.8 ms with jump-ahead): its
-// one small CTA co-runs with the other stream's kernels.
+// nwords outputs of Rng(seed) into words.  Streams of 2^16 words and more
+// use jump-ahead: K segments of J outputs generated in parallel from states
+// computed with the GF(2) jump polynomials (mt_jump.cpp, rng.cu) -- bitwise
+// the same stream; J = the next power of two >= max(32768, nwords / nsm), so
+// K <= nsm.  With the set-bit-list state kernel spread over about one wave of
+// CTAs, C2's 360K-word sketch takes 132 us instead of the serial engine's
+// 548 us (C2 compression 1.49 -> 1.15 ms); shorter streams stay serial.
 void gen_words(cnmf_context* c, uint64_t seed, uint64_t nwords, uint64_t* words,
                const std::string& tag, cudaStream_t st) {
   static const uint64_t jump_min = [] {
     const char* e = std::getenv("CNMF_MT_JUMP_MIN");  // threshold override (experiments)
-    return e ? (uint64_t)std::strtoull(e, nullptr, 10) : (uint64_t)1 << 20;
+    return e ? (uint64_t)std::strtoull(e, nullptr, 10) : (uint64_t)1 << 16;
   }();
   if (nwords >= jump_min && !std::getenv("CNMF_MT_SERIAL") && mt_jump_available()) {
     uint64_t J = (uint64_t)1 << 15;

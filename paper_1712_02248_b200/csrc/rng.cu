@@ -100,38 +100,78 @@ constexpr int kJumpPoly = 312;                  // words per polynomial (19968 b
 constexpr int kJumpPrefix = 64 * kJumpPoly + kN;  // raw words the convolution reads
 
 // Segment k's starting state = sum over the set bits of its jump polynomial
-// of the prefix shifted by the bit's position (GF(2), XOR).  kJumpGroups
-// thread groups of 312 split the polynomial's words round-robin and their
-// partial XORs are combined at the end (XOR is exact and order-free: bitwise
-// the serial result); one group per CTA left the kernel latency-bound at
-// ~60 us, which kept streams below 2^20 words on the serial engine.
+// of the prefix shifted by the bit's position (GF(2), XOR).  The CTA first
+// lists the polynomial's set-bit positions in shared memory (a block scan of
+// the words' popcounts), then each of kJumpGroups thread groups of 312 XORs
+// its share of the list with four independent accumulators; the groups'
+// partials are combined at the end.  XOR is exact and order-free: bitwise
+// the serial result.  (Peeling bits with ffs in a per-word while loop made
+// every step wait on the previous one: 480 us per CTA.)
 constexpr int kJumpGroups = 3;
-__global__ void __launch_bounds__(kN * kJumpGroups) mt_jump_state_kernel(
+constexpr int kJumpThreads = kN * kJumpGroups;
+size_t jump_state_smem() {
+  return sizeof(uint64_t) * (kJumpPrefix + kJumpGroups * kN) + sizeof(uint16_t) * 64 * kJumpPoly;
+}
+// `parts` CTAs share one segment (block b: segment b / parts + 1, part
+// b % parts), each XORing a slice of the position list into the zeroed
+// state with atomicXor -- so short streams fill the GPU too.
+__global__ void __launch_bounds__(kJumpThreads) mt_jump_state_kernel(
     const uint64_t* __restrict__ prefix, const uint64_t* __restrict__ polys,
-    uint64_t* __restrict__ states) {
-  extern __shared__ uint64_t pre[];  // kJumpPrefix words, then kJumpGroups x kN partials
-  __shared__ uint64_t cpoly[kJumpPoly];
-  const int k = blockIdx.x + 1;
-  const int grp = threadIdx.x / kN, w = threadIdx.x - grp * kN;
-  for (int e = threadIdx.x; e < kJumpPrefix; e += blockDim.x) pre[e] = prefix[e];
-  for (int e = threadIdx.x; e < kJumpPoly; e += blockDim.x) cpoly[e] = polys[(size_t)k * kJumpPoly + e];
-  __syncthreads();
-  uint64_t acc = 0;
-  for (int cw = grp; cw < kJumpPoly; cw += kJumpGroups) {
-    uint64_t bits = cpoly[cw];
-    while (bits) {
-      const int b = __ffsll(bits) - 1;
-      bits &= bits - 1;
-      acc ^= pre[64 * cw + b + w];
-    }
-  }
+    uint64_t* __restrict__ states, int parts) {
+  extern __shared__ uint64_t pre[];  // kJumpPrefix words, kJumpGroups x kN partials, positions
   uint64_t* part = pre + kJumpPrefix;
+  uint16_t* pos = reinterpret_cast<uint16_t*>(part + kJumpGroups * kN);
+  __shared__ int wsum[kJumpThreads / 32];
+  __shared__ int npos;
+  const int seg = blockIdx.x / parts, prt = blockIdx.x - seg * parts;
+  const int k = seg + 1, tid = threadIdx.x;
+  const int grp = tid / kN, w = tid - grp * kN;
+  const int lane = tid & 31, wid = tid >> 5;
+  for (int e = tid; e < kJumpPrefix; e += blockDim.x) pre[e] = prefix[e];
+  // set-bit positions of c_k in ascending order: thread t < 312 owns word t
+  const uint64_t word = tid < kJumpPoly ? polys[(size_t)k * kJumpPoly + tid] : 0ull;
+  const int cnt = __popcll(word);
+  int incl = cnt;  // inclusive scan: warps, then the warp totals
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    const int v = __shfl_up_sync(0xffffffffu, incl, o);
+    if (lane >= o) incl += v;
+  }
+  if (lane == 31) wsum[wid] = incl;
+  __syncthreads();
+  if (tid == 0) {
+    int run = 0;
+    for (int i = 0; i < kJumpThreads / 32; ++i) {
+      const int t = wsum[i];
+      wsum[i] = run;
+      run += t;
+    }
+    npos = run;
+  }
+  __syncthreads();
+  int off = wsum[wid] + incl - cnt;
+  for (uint64_t bits = word; bits; bits &= bits - 1) pos[off++] = (uint16_t)(64 * tid + __ffsll(bits) - 1);
+  __syncthreads();
+  const int n = npos;
+  const int p0 = prt * n / parts, p1 = (prt + 1) * n / parts;  // this CTA's slice
+  const int i0 = p0 + grp * (p1 - p0) / kJumpGroups, i1 = p0 + (grp + 1) * (p1 - p0) / kJumpGroups;
+  uint64_t a0 = 0, a1 = 0, a2 = 0, a3 = 0;
+  int i = i0;
+  for (; i + 3 < i1; i += 4) {
+    a0 ^= pre[pos[i] + w];
+    a1 ^= pre[pos[i + 1] + w];
+    a2 ^= pre[pos[i + 2] + w];
+    a3 ^= pre[pos[i + 3] + w];
+  }
+  for (; i < i1; ++i) a0 ^= pre[pos[i] + w];
+  uint64_t acc = (a0 ^ a1) ^ (a2 ^ a3);
   part[grp * kN + w] = acc;
   __syncthreads();
   if (grp == 0) {
 #pragma unroll
     for (int g = 1; g < kJumpGroups; ++g) acc ^= part[g * kN + w];
-    states[(size_t)blockIdx.x * kN + w] = acc;
+    atomicXor(reinterpret_cast<unsigned long long*>(states + (size_t)seg * kN + w),
+              (unsigned long long)acc);
   }
 }
 
@@ -263,13 +303,15 @@ void launch_mt_jump(uint64_t seed, uint64_t nwords, uint64_t J, int K, const uin
   mt_stream_kernel<<<1, 160, 0, s>>>(jobs, 1);
   if (K > 1) {
     static bool attr = false;
-    const int smem = (int)(sizeof(uint64_t) * (kJumpPrefix + kJumpGroups * kN));
+    const int smem = (int)jump_state_smem();
     if (!attr) {
       cudaFuncSetAttribute(mt_jump_state_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
       attr = true;
     }
     note_launches(1);
-    mt_jump_state_kernel<<<K - 1, kN * kJumpGroups, smem, s>>>(prefix, polys, states);
+    const int parts = std::max(1, 148 / (K - 1));  // about one wave of CTAs
+    cudaMemsetAsync(states, 0, sizeof(uint64_t) * kN * (K - 1), s);
+    mt_jump_state_kernel<<<(K - 1) * parts, kJumpThreads, smem, s>>>(prefix, polys, states, parts);
   }
   note_launches(1);
   mt_segment_kernel<<<K, 160, 0, s>>>(prefix, states, J, nwords, out);
