@@ -180,10 +180,15 @@ __global__ void __launch_bounds__(128) chol_inv_kernel(const double* __restrict_
     }
     const double ip = 1.0 / piv;
     const double* rowj = gs + j * ls;
-    for (int a = j + 1 + warp; a < l; a += nw) {
+    // trailing update, element-parallel: thread (ty, tx) of an 8 x 16 grid
+    // (nt = 128) strides over the rows / columns after j, upper triangle
+    // kept -- the same fma per element as a row walk, without a dependent
+    // chain per row or an index division per element
+    const int ty = tid >> 4, tx = tid & 15;
+    for (int a = j + 1 + ty; a < l; a += 8) {
       const double f = rowj[a] * ip;
       double* rowa = gs + a * ls;
-      for (int b = a + lane; b < l; b += 32) rowa[b] = fma(-f, rowj[b], rowa[b]);
+      for (int b = a + ((tx - a) & 15); b < l; b += 16) rowa[b] = fma(-f, rowj[b], rowa[b]);
     }
     __syncthreads();
   }
