@@ -39,11 +39,22 @@ def parse():
     ap.add_argument("--gpus", type=int, default=1)
     ap.add_argument("--steps", type=int, default=5)
     ap.add_argument("--warmup", type=int, default=3)
-    ap.add_argument("--config", default="c2", choices=["c1", "c2", "c3", "c4", "c5"])
+    ap.add_argument("--config", default="c4", choices=["c1", "c2", "c3", "c4", "c5"])
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
     return ap.parse_args()
+
+
+def fp64_peak_tflops():
+    """FP64 tensor-core (DMMA) peak measured on this pool by tools/ubench_dmma.cu
+    (profiles/fp64_peak.json); MEASURED_PEAKS.json carries no fp64 figure."""
+    try:
+        with open(os.path.join(ROOT, "profiles", "fp64_peak.json")) as f:
+            p = json.load(f)
+        return float(p["tflops"]), p.get("source", "profiles/fp64_peak.json")
+    except Exception:
+        return 37.0, "round-1 DMMA microbenchmark (tools/ubench_dmma.cu), not re-measured"
 
 
 def peaks():
@@ -120,85 +131,153 @@ class ClockSampler:
 
 
 # -------------------------------------------------------- CPU reference leg ---
+def host_cpu():
+    """CPU model and core count of this host (lscpu / nproc)."""
+    model = "unknown"
+    try:
+        out = subprocess.run(["lscpu"], capture_output=True, text=True, timeout=10).stdout
+        for ln in out.splitlines():
+            if ln.startswith("Model name:"):
+                model = ln.split(":", 1)[1].strip()
+                break
+    except Exception:
+        pass
+    return model, os.cpu_count() or 1
+
+
+class PinnedCore:
+    """Pins this process to one host core for the single-threaded reference
+    (taskset -c 0)."""
+
+    def __init__(self, core=0):
+        self.core = core
+
+    def __enter__(self):
+        try:
+            self.old = os.sched_getaffinity(0)
+            os.sched_setaffinity(0, {self.core})
+        except Exception:
+            self.old = None
+        return self
+
+    def __exit__(self, *a):
+        if self.old is not None:
+            os.sched_setaffinity(0, self.old)
+
+
 def cpu_reference_sample(name, c, timed_steps=1):
-    """The reference (oracle/_ref) on the host: build_projectors + compress_* and
-    `iters` fasthals_rp_step calls.  Full workload when it fits ~30 s of CPU,
-    else per-pass column-slice + full-shape step timing, scaled (extrapolated)."""
+    """The reference (oracle/_ref, its own sources) on one pinned host core:
+    build_projectors + compress_left/right and `iters` fasthals_rp_step calls.
+
+    C1/C2 run the full workload.  Larger configs are extrapolated from
+    bounded samples, each operation's cost being linear in the dimension it
+    is sliced along: the X contractions exactly as the reference calls them
+    (compression.cpp:23-84: (1+2w) X*S, (1+2w) X^T*T, compress_left L^T X,
+    compress_right X R^T) on a column slice, scaled by n / n_s; the (1+2w)
+    thin_qr of d x q and of n x q bases on row slices, scaled by rows; the two
+    Gaussian sketches on row slices; one fasthals_rp_step on a (d, n) / f
+    shape, scaled by (d + n) / (d_s + n_s) (its cost is (d + n)(4lk + 2k^2) +
+    O(lk^2)).  About 4-8 s of CPU per sample."""
     import numpy as np
 
     from oracle import REF_SO, Oracle, Reference
     o = Oracle()
     kind = "reference" if os.path.exists(REF_SO) else "port"
     r = Reference() if kind == "reference" else None
+    impl = r if kind == "reference" else o
     d, n, k, q, w, iters = c["d"], c["n"], c["k"], c["q"], c["w"], c["iters"]
     full = d * n <= 6e7
-    n_s = n if full else max(q + 1, min(n, int(6e6 // d) + 1))
-    x = o.synth_x(d, n, c["rank"], c["factor_kind"], c["noise_kind"], c["sigma"], 1,
-                  col_lo=0, col_hi=n_s).astype(np.float64)
     vals = []
-    impl = r if kind == "reference" else o
-    for _ in range(timed_steps):
+    with PinnedCore(0):
         if full:
-            if kind == "reference":
-                left, right, xhat, xcheck, t_comp = r.compress(x, q, w, 1)
-            else:
-                t0 = time.perf_counter()
-                left, right = o.build_projectors(x, q, w, 1)
-                xhat, xcheck = o.compress(x, left, right)
-                t_comp = time.perf_counter() - t0
+            x = o.synth_x(d, n, c["rank"], c["factor_kind"], c["noise_kind"], c["sigma"],
+                          1).astype(np.float64)
         else:
-            # compress = (2w + 2) NN and (2w + 2) TN X contractions (linear in n:
-            # timed on the column slice, scaled by n / n_s) + (1 + 2w) thin QRs of
-            # d x q and of n x q bases (timed at full shape) + the two sketches
+            n_s = max(q + 1, min(n, int(4e6 // d) + 1))
+            x = o.synth_x(d, n, c["rank"], c["factor_kind"], c["noise_kind"], c["sigma"], 1,
+                          col_lo=0, col_hi=n_s).astype(np.float64)
+        for _ in range(timed_steps):
+            if full:
+                if kind == "reference":
+                    left, right, xhat, xcheck, t_comp = r.compress(x, q, w, 1)
+                else:
+                    t0 = time.perf_counter()
+                    left, right = o.build_projectors(x, q, w, 1)
+                    xhat, xcheck = o.compress(x, left, right)
+                    t_comp = time.perf_counter() - t0
+                a, b = o.initialize(d, n, k, 1)
+                ah, bc = o.compress_factors(a, b, left, right)
+                if kind == "reference":
+                    t_h = r.fasthals_rp_steps(xhat, xcheck, left, right, a, b, ah, bc, 1, iters)
+                else:
+                    t0 = time.perf_counter()
+                    rg = o.rng(1)
+                    for _ in range(iters):
+                        o.fasthals_rp_step(xhat, xcheck, a, b, ah, bc, left, right, True, 0.0,
+                                           0.0, rg)
+                    t_h = time.perf_counter() - t0
+                vals.append(t_comp + t_h)
+                continue
             rng = np.random.default_rng(0)
+
+            def timed(f, *args, **kw):
+                t0 = time.perf_counter()
+                f(*args, **kw)
+                return time.perf_counter() - t0
+
             s_n = rng.standard_normal((n_s, q))
             t_d = rng.standard_normal((d, q))
-            t0 = time.perf_counter()
-            impl.matmul(x, s_n)
-            t_nn = time.perf_counter() - t0
-            t0 = time.perf_counter()
-            impl.matmul(x, t_d, tl=True)
-            t_tn = time.perf_counter() - t0
-            t0 = time.perf_counter()
-            impl.thin_qr(rng.standard_normal((d, q)))
-            t_qd = time.perf_counter() - t0
-            t0 = time.perf_counter()
-            impl.thin_qr(rng.standard_normal((n, q)))
-            t_qn = time.perf_counter() - t0
-            t0 = time.perf_counter()
-            impl.gaussian_sketch(n, q, 2)
-            impl.gaussian_sketch(d, q, 3)
-            t_sk = time.perf_counter() - t0
-            t_comp = (2 * w + 2) * (t_nn + t_tn) * (n / n_s) + (1 + 2 * w) * (t_qd + t_qn) + t_sk
-        if full:
-            a, b = o.initialize(d, n, k, 1)
+            r_s = rng.standard_normal((q, n_s))
+            t_nn = timed(impl.matmul, x, s_n)                 # X * S      (matrix.cpp:105-116)
+            t_tn = timed(impl.matmul, x, t_d, tl=True)        # X^T * T    (129-140)
+            t_cl = timed(impl.matmul, t_d, x, tl=True)        # L^T X      (compress_left)
+            t_cr = timed(impl.matmul, x, r_s, tr=True)        # X R^T      (compress_right, NT)
+            t_x = ((1 + 2 * w) * (t_nn + t_tn) + t_cl + t_cr) * (n / n_s)
+            rows_q = max(q + 1, int(1.5e6 // q))
+            t_qr = 0.0
+            for rows in (d, n):
+                rs_ = min(rows, rows_q)
+                t_qr += (1 + 2 * w) * timed(impl.thin_qr, rng.standard_normal((rs_, q))) * (rows / rs_)
+            t_sk = 0.0
+            for rows, seed in ((n, 2), (d, 3)):
+                rs_ = min(rows, rows_q)
+                t_sk += timed(impl.gaussian_sketch, rs_, q, seed) * (rows / rs_)
+            t_comp = t_x + t_qr + t_sk
+            f = max(1.0, ((d + n) * k * (4 * q + 2 * k)) / 2e9)
+            ds, ns = max(q + 1, int(d / f)), max(q + 1, int(n / f))
+            xh = rng.random((q, ns))
+            xc = rng.random((ds, q))
+            left = np.linalg.qr(rng.standard_normal((ds, q)))[0]
+            right = np.linalg.qr(rng.standard_normal((ns, q)))[0].T.copy()
+            a, b = o.initialize(ds, ns, k, 1)
             ah, bc = o.compress_factors(a, b, left, right)
-            hs = iters
-        else:  # full-shape operands for the per-iteration cost (cost does not depend on values)
-            rng = np.random.default_rng(0)
-            xhat = rng.random((q, n)); xcheck = rng.random((d, q))
-            left = np.linalg.qr(rng.standard_normal((d, q)))[0]
-            right = np.linalg.qr(rng.standard_normal((n, q)))[0].T.copy()
-            a, b = o.initialize(d, n, k, 1)
-            ah, bc = o.compress_factors(a, b, left, right)
-            hs = 1
-        if kind == "reference":
-            t_h = r.fasthals_rp_steps(xhat, xcheck, left, right, a, b, ah, bc, 1, hs)
-        else:
-            t0 = time.perf_counter()
-            rg = o.rng(1)
-            for _ in range(hs):
-                o.fasthals_rp_step(xhat, xcheck, a, b, ah, bc, left, right, True, 0.0, 0.0, rg)
-            t_h = time.perf_counter() - t0
-        t_h *= iters / hs
-        vals.append(t_comp + t_h)
-    sample = (f"full {name.upper()} workload: build_projectors+compress_left/right on the "
-              f"{d}x{n} X and {iters} fasthals_rp_step calls, single thread (the reference "
-              f"solver is single-threaded)") if full else (
-              f"extrapolated: the {4 * w + 4} X contractions timed on a {d}x{n_s} column slice "
-              f"and scaled by n/n_s (cost linear in n), {2 + 4 * w} thin QRs at full shape, the "
-              f"two sketches, + one full-shape fasthals_rp_step x {iters}; single thread")
+            if kind == "reference":
+                t_step = r.fasthals_rp_steps(xh, xc, left, right, a, b, ah, bc, 1, 1)
+            else:
+                t0 = time.perf_counter()
+                o.fasthals_rp_step(xh, xc, a, b, ah, bc, left, right, True, 0.0, 0.0, o.rng(1))
+                t_step = time.perf_counter() - t0
+            vals.append(t_comp + t_step * ((d + n) / (ds + ns)) * iters)
+    if full:
+        sample = (f"full {name.upper()} workload: build_projectors+compress_left/right on the "
+                  f"{d}x{n} X and {iters} fasthals_rp_step calls, one thread pinned to core 0 "
+                  f"(the reference solver is single-threaded)")
+    else:
+        sample = (f"extrapolated from bounded samples on one pinned core: the reference's "
+                  f"{4 * w + 4} X contractions ((1+2w) X*S, (1+2w) X^T*T, L^T X, X R^T) on a "
+                  f"{d}x{n_s} column slice scaled by n/n_s; {2 + 4 * w} thin_qr and the two "
+                  f"sketches on <= {rows_q}-row slices scaled by rows; one fasthals_rp_step at "
+                  f"{ds}x{ns} scaled by (d+n)/(d_s+n_s), x {iters} iterations")
     return vals, kind, sample
+
+
+def config_dict(name, c, parallelism, extra=None):
+    """The workload description both arms print (same keys: same_config)."""
+    out = {"workload": workload_desc(name, c), "d": c["d"], "n": c["n"], "k": c["k"],
+           "l": c["q"], "power_iterations": c["w"], "iterations": c["iters"],
+           "parallelism": parallelism}
+    out.update(extra or {})
+    return out
 
 
 def run_reference_arm(args, name, c, rank):
@@ -210,13 +289,15 @@ def run_reference_arm(args, name, c, rank):
         cpu_reference_sample("warmup", small, 1)
     vals, kind, sample = cpu_reference_sample(name, c, args.steps)
     v = statistics.mean(vals)
+    model, ncpu = host_cpu()
     line = {"metric": METRIC, "value": v, "unit": "s", "n_gpus": args.gpus, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": v * 1e3, "higher_is_better": False,
             "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
             "impl": "reference",
-            "config": {"workload": workload_desc(name, c), "parallelism": "single host thread"},
+            "config": config_dict(name, c, "single host thread (the reference is single-threaded)"),
             "cpu_baseline": {"value": v, "unit": "s", "cores": 1, "kind": kind,
-                             "sample": sample},
+                             "sample": sample, "host_cpu": model, "host_cores": ncpu,
+                             "pinning": "sched_setaffinity core 0 (taskset -c 0)"},
             "e2e": {"value": v, "unit": "s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
     print(json.dumps(line), flush=True)
 
@@ -276,6 +357,7 @@ def run_ours(args, name, c, rank, world, local_rank):
             comp.append(tr.compress_seconds)
             upd.append(tr.update_seconds)
             passes.append(tr.x_passes)
+            redraws = tr.redraws
     torch.cuda.synchronize()
     launches = cb.launch_count() - launches0
     if world > 1:
@@ -287,8 +369,15 @@ def run_ours(args, name, c, rank, world, local_rank):
         torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
         value, ms_per_step = t.tolist()
 
-    # roofline of the X-stream contraction (dominant kernel of the compression half)
+    # roofline of the dominant kernel: the persistent FastHALS-RP kernel (HALS is
+    # 75-90% of `value` at C2-C4), fp64 on the FP64 tensor cores (DMMA); and of
+    # the compression GEMM, the X-stream contraction (HBM-bound).
     hbm, src = peaks()
+    fp64_peak, fp64_src = fp64_peak_tflops()
+    upd_mean = statistics.mean(upd)
+    hals_flops = (4.0 * (d + nloc) * q * k + 2.0 * (d + nloc) * k * k + 4.0 * q * k * k)
+    hals_bytes = 4.0 * (2 * d * q + 2 * q * nloc) + 8.0 * 3 * (d + nloc) * k
+    t_iter = upd_mean / iters
     t_nn = ctx.time_xstream(xv, q, 0, iters=10)
     t_tn = ctx.time_xstream(xv, q, 1, iters=10)
     alg_bytes = 4.0 * d * nloc + 4.0 * (d + nloc) * q
@@ -301,29 +390,51 @@ def run_ours(args, name, c, rank, world, local_rank):
             traffic = json.load(open(prof)).get("bytes_per_launch")
         except Exception:
             traffic = None
+    hals_traffic = None
+    prof = os.path.join(ROOT, "profiles", f"hals_traffic_{name}.json")
+    if os.path.exists(prof):
+        try:
+            hals_traffic = json.load(open(prof)).get("bytes_per_iteration")
+        except Exception:
+            hals_traffic = None
     mean_comp = statistics.mean(comp)
     xstream_gbs = passes[0] * 4.0 * d * n / mean_comp / 1e9  # whole-job X bytes
+    peak_note = (f"{src} (MEASURED_PEAKS.json hbm_gbs)" if src == "measured"
+                 else "fallback 6.65 TB/s (B200_PROFILING.md)")
 
     line = {"metric": METRIC, "value": value, "unit": "s", "n_gpus": world,
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms_per_step,
             "higher_is_better": False, "scaling": "strong", "vs_baseline": None,
             "dtype": "f32", "data": "synthetic",
-            "config": {"workload": workload_desc(name, c), "d": d, "n": n, "k": k, "l": q,
-                       "power_iterations": w, "iterations": iters,
-                       "parallelism": f"X column-sharded over {world} GPUs (NCCL)" if world > 1 else "1 GPU",
-                       "l2": ("inputs larger than L2 (X %.0f MB > 126 MB)" % (x_bytes / 1e6))
-                       if big else "L2 flushed (256 MB write) between timed steps"},
-            "compress_seconds": mean_comp, "hals_seconds": statistics.mean(upd),
+            "config": config_dict(name, c, f"X column-sharded over {world} GPUs (NCCL)"
+                                  if world > 1 else "1 GPU",
+                                  {"l2": ("inputs larger than L2 (X %.0f MB > 126 MB)"
+                                          % (x_bytes / 1e6)) if big else
+                                   "L2 flushed (256 MB write) between timed steps"}),
+            "compress_seconds": mean_comp, "hals_seconds": upd_mean,
+            "hals_ms_per_iteration": t_iter * 1e3,
+            "redraws_per_run": redraws,
             "x_passes": passes[0], "x_stream_gbs": xstream_gbs,
             "x_stream_gbs_fused_min": (2 * w + 2) * 4.0 * d * n / mean_comp / 1e9,
-            "roofline": {"bound": "hbm", "kernel": "xs_kernel (X*S, NN contraction)",
-                         "achieved": ach_nn, "peak": hbm, "unit": "GB/s",
-                         "frac": ach_nn / hbm, "traffic": traffic,
-                         "peak_source": f"{src} (MEASURED_PEAKS.json hbm_gbs)" if src ==
-                         "measured" else "fallback 6.65 TB/s (B200_PROFILING.md)",
-                         "launch_seconds": t_nn, "algorithmic_bytes": alg_bytes,
-                         "tn_achieved": ach_tn, "tn_frac": ach_tn / hbm,
-                         "tn_launch_seconds": t_tn},
+            "roofline": {"bound": "tensor",
+                         "kernel": "hals_kernel / hals_resident_kernel (persistent FastHALS-RP "
+                                   "iteration, fp64 DMMA)",
+                         "unit": "TFLOP/s", "achieved": hals_flops / t_iter / 1e12,
+                         "peak": fp64_peak, "frac": hals_flops / t_iter / 1e12 / fp64_peak,
+                         "traffic": hals_traffic, "peak_source": fp64_src,
+                         "per": "one HALS iteration (device time of the iteration range "
+                                "/ iterations, redraw servicing included)",
+                         "algorithmic_flops": hals_flops,
+                         "hbm_view": {"algorithmic_bytes": hals_bytes,
+                                      "achieved_gbs": hals_bytes / t_iter / 1e9, "peak": hbm,
+                                      "frac": hals_bytes / t_iter / 1e9 / hbm}},
+            "roofline_xstream": {"bound": "hbm", "kernel": "xs_tc_kernel (X*S, NN contraction)",
+                                 "achieved": ach_nn, "peak": hbm, "unit": "GB/s",
+                                 "frac": ach_nn / hbm, "traffic": traffic,
+                                 "peak_source": peak_note,
+                                 "launch_seconds": t_nn, "algorithmic_bytes": alg_bytes,
+                                 "tn_achieved": ach_tn, "tn_frac": ach_tn / hbm,
+                                 "tn_launch_seconds": t_tn},
             "gpu_launches": int(launches),
             "clocks": clk.summary()}
 
@@ -341,7 +452,7 @@ def run_ours(args, name, c, rank, world, local_rank):
             if world == 1:
                 ctx.run(xnp, cfg)
             else:  # host shard -> device, collective run, factors -> host
-                xd = xh.to("cuda", non_blocking=True)
+                xd = xh.to("cuda")
                 aa, bb, _ = ctx.run_sharded(xd, n, cfg)
                 aa.cpu(), bb.cpu()
             e2e.append(time.perf_counter() - t0)
@@ -356,14 +467,30 @@ def run_ours(args, name, c, rank, world, local_rank):
 
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         vals, kind, sample = cpu_reference_sample(name, c, 1)
+        model, ncpu = host_cpu()
         line["cpu_baseline"] = {"value": vals[0], "unit": "s", "cores": 1, "kind": kind,
-                                "sample": sample}
+                                "sample": sample, "host_cpu": model, "host_cores": ncpu,
+                                "pinning": "sched_setaffinity core 0 (taskset -c 0)"}
     if rank == 0:
         print(json.dumps(line), flush=True)
 
 
+def self_launch(args):
+    """--gpus N without torchrun: re-run this script as N ranks (one per GPU)."""
+    import socket
+    with socket.socket() as sk:
+        sk.bind(("127.0.0.1", 0))
+        port = sk.getsockname()[1]
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1",
+           f"--nproc-per-node={args.gpus}", "--master-addr=127.0.0.1",
+           f"--master-port={port}", os.path.abspath(__file__)] + sys.argv[1:]
+    return subprocess.call(cmd)
+
+
 def main():
     args = parse()
+    if args.gpus > 1 and "WORLD_SIZE" not in os.environ:
+        sys.exit(self_launch(args))
     rank = int(os.environ.get("RANK", "0"))
     world = int(os.environ.get("WORLD_SIZE", "1"))
     local_rank = int(os.environ.get("LOCAL_RANK", "0"))

@@ -31,7 +31,7 @@
 extern "C" {
 #endif
 
-#define CNMF_B200_ABI_VERSION 1
+#define CNMF_B200_ABI_VERSION 2
 
 typedef enum cnmf_status {
   CNMF_OK = 0,
@@ -78,11 +78,14 @@ typedef struct cnmf_solver_config {
   int32_t normalize_a;
 } cnmf_solver_config;
 
-/* cnmf::RunRecord, metrics.hpp:56-60. */
+/* cnmf::RunRecord, metrics.hpp:56-60, plus the run Rng's position. */
 typedef struct cnmf_run_record {
   uint64_t iteration;
   double error;            /* 1/2 ||X - A B^T||_F^2 */
   double elapsed_seconds;  /* cumulative update time at this record */
+  uint64_t rng_draws;      /* raw mt19937_64 draws the dead-component redraws
+                              (reinit_column, solvers.cpp:28-31) took from the
+                              run Rng up to this record (initialize()'s excluded) */
 } cnmf_run_record;
 
 /* cnmf::RunTrace (metrics.hpp:70-84) plus device timing.  `records` is
@@ -92,7 +95,8 @@ typedef struct cnmf_run_trace {
   cnmf_run_record* records;
   uint64_t records_capacity;
   uint64_t records_count;
-  double update_seconds;      /* device time inside the update steps (CUDA events) */
+  double update_seconds;      /* device time of the update steps (CUDA events around each
+                                 iteration range, redraw servicing included) */
   double compress_seconds;    /* device time of build_projectors + compress_* (RNG included) */
   double error_seconds;       /* device time of objective evaluations */
   double gini_b;
@@ -105,7 +109,8 @@ typedef struct cnmf_run_trace {
   double estimate_flops_per_iteration; /* estimate_cost, metrics.cpp:20-50 */
   double estimate_memory_floats;
   double x_norm_sq;           /* ||X||_F^2 (for relative errors)   */
-  uint64_t redraws;           /* dead-component redraws served from the host Rng */
+  uint64_t redraws;           /* dead-component redraws (served on the device from the
+                                 run Rng's stream) */
   uint64_t x_passes;          /* X-streaming contractions performed */
   char message[256];
 } cnmf_run_trace;
@@ -153,6 +158,20 @@ uint64_t cnmf_shard_begin(uint64_t n, int rank, int world);
 cnmf_status cnmf_nccl_unique_id(unsigned char id[128]);
 cnmf_status cnmf_context_create_sharded(int device, int rank, int world,
                                         const unsigned char id[128], cnmf_context** out);
+/* Host-staged collectives: a sharded context whose cross-rank combines go
+ * through the caller instead of NCCL (device buffer -> host, callback, host
+ * -> device; synchronous).  A test / debugging transport: it lets world-size
+ * > 1 runs share one GPU (NCCL refuses two ranks on one device), e.g. with
+ * torch.distributed gloo behind the callbacks.  Callbacks return 0 on
+ * success.  dtype: 0 fp32, 1 fp64; op: 0 sum, 1 max. */
+typedef struct cnmf_host_collectives {
+  int (*allreduce)(void* buf, uint64_t count, int dtype, int op, void* user);
+  /* `bytes` from every rank, concatenated in rank order into recv */
+  int (*allgather)(const void* send, void* recv, uint64_t bytes, void* user);
+  void* user;
+} cnmf_host_collectives;
+cnmf_status cnmf_context_create_hosted(int device, int rank, int world,
+                                       const cnmf_host_collectives* coll, cnmf_context** out);
 cnmf_status cnmf_run_sharded_device(cnmf_context* ctx, const float* x_shard_dev, uint64_t d,
                                     uint64_t n, uint64_t col_begin, uint64_t n_local,
                                     uint64_t ldx, const cnmf_solver_config* cfg, float* a_dev,

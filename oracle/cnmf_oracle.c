@@ -843,38 +843,57 @@ double orc_synth_factor_entry(uint64_t seed, uint64_t stream, uint64_t index, in
   return synth_gamma(synth_key(seed, stream + 3), index, 0.3);
 }
 
-/* Fills x (d x ldx fp32, columns [col_lo, col_hi) of the global d x n
- * matrix), zero in the padding columns.  noise_kind 0: none, 1: sigma|N|,
- * 2: Poisson(W0 H0). */
-void orc_synth_x(size_t d, size_t n, size_t rank, int factor_kind, int noise_kind,
-                 double sigma, uint64_t seed, size_t col_lo, size_t col_hi, size_t ldx,
-                 float* x) {
-  double* w0 = dalloc(d * rank);
-  double* h0 = dalloc(rank * (col_hi - col_lo));
+/* Rows [row_lo, row_hi) and columns [col_lo, col_hi) of the global d x n
+ * matrix into xf (fp32, ld ldx, zero in the padding columns) or, when xf is
+ * NULL, into xd (fp64 holding the same fp32-rounded values).  Entries depend
+ * only on their global (i, j), so any blocking gives the same bytes.
+ * noise_kind 0: none, 1: sigma|N|, 2: Poisson(W0 H0). */
+void orc_synth_x_block(size_t d, size_t n, size_t rank, int factor_kind, int noise_kind,
+                       double sigma, uint64_t seed, size_t row_lo, size_t row_hi,
+                       size_t col_lo, size_t col_hi, size_t ldx, float* xf, double* xd) {
   const size_t nc = col_hi - col_lo;
-  for (size_t i = 0; i < d * rank; ++i) w0[i] = orc_synth_factor_entry(seed, 1, i, factor_kind);
+  double* w0 = dalloc((row_hi - row_lo) * rank);
+  double* h0 = dalloc(rank * nc);
+  (void)d;
+  for (size_t i = row_lo; i < row_hi; ++i)
+    for (size_t r = 0; r < rank; ++r)
+      w0[(i - row_lo) * rank + r] = orc_synth_factor_entry(seed, 1, i * rank + r, factor_kind);
   for (size_t r = 0; r < rank; ++r)
     for (size_t j = 0; j < nc; ++j)
       h0[r * nc + j] = orc_synth_factor_entry(seed, 2, r * n + col_lo + j, factor_kind);
   const uint64_t knoise = synth_key(seed, 3), kpois = synth_key(seed, 6);
   double* acc = dalloc(nc);
-  for (size_t i = 0; i < d; ++i) {
+  for (size_t i = row_lo; i < row_hi; ++i) {
     for (size_t j = 0; j < nc; ++j) acc[j] = 0.0;
     for (size_t r = 0; r < rank; ++r) {
-      const double w = w0[i * rank + r];
+      const double w = w0[(i - row_lo) * rank + r];
       const double* hr = h0 + r * nc;
       for (size_t j = 0; j < nc; ++j) acc[j] = acc[j] + w * hr[j];
     }
+    const size_t o = (i - row_lo) * ldx;
     for (size_t j = 0; j < nc; ++j) {
       const uint64_t gidx = (uint64_t)i * n + col_lo + j;
       double v = acc[j];
       if (noise_kind == 1) v = v + sigma * fabs(synth_normal(knoise, gidx));
       if (noise_kind == 2) v = synth_poisson(kpois, gidx, v);
-      x[i * ldx + j] = (float)v;
+      if (xf) xf[o + j] = (float)v;
+      else xd[o + j] = (double)(float)v;
     }
-    for (size_t j = nc; j < ldx; ++j) x[i * ldx + j] = 0.0f;
+    for (size_t j = nc; j < ldx; ++j) {
+      if (xf) xf[o + j] = 0.0f;
+      else xd[o + j] = 0.0;
+    }
   }
   free(acc);
   free(w0);
   free(h0);
+}
+
+/* Fills x (d x ldx fp32, columns [col_lo, col_hi) of the global d x n
+ * matrix), zero in the padding columns. */
+void orc_synth_x(size_t d, size_t n, size_t rank, int factor_kind, int noise_kind,
+                 double sigma, uint64_t seed, size_t col_lo, size_t col_hi, size_t ldx,
+                 float* x) {
+  orc_synth_x_block(d, n, rank, factor_kind, noise_kind, sigma, seed, 0, d, col_lo, col_hi,
+                    ldx, x, NULL);
 }

@@ -93,7 +93,7 @@ class _Cost(C.Structure):
 
 class _Record(C.Structure):
     _fields_ = [("iteration", C.c_uint64), ("error", C.c_double),
-                ("elapsed_seconds", C.c_double)]
+                ("elapsed_seconds", C.c_double), ("rng_draws", C.c_uint64)]
 
 
 class _Trace(C.Structure):
@@ -117,7 +117,7 @@ EXPORTS = [
     "cnmf_thin_qr", "cnmf_xs_nn", "cnmf_xs_tn", "cnmf_synth_x", "cnmf_launch_count",
     "cnmf_time_xstream", "cnmf_shard_begin", "cnmf_nccl_unique_id", "cnmf_context_create_sharded",
     "cnmf_run_sharded_device", "cnmf_estimate_cost", "cnmf_generate_synthetic",
-    "cnmf_pairwise_distortion", "cnmf_run_csr",
+    "cnmf_pairwise_distortion", "cnmf_run_csr", "cnmf_context_create_hosted",
 ]
 
 
@@ -179,6 +179,8 @@ def load_library(path: str = LIB_PATH):
     L.cnmf_shard_begin.restype = u64
     L.cnmf_nccl_unique_id.argtypes = [C.c_char_p]
     L.cnmf_context_create_sharded.argtypes = [C.c_int, C.c_int, C.c_int, C.c_char_p, C.POINTER(vp)]
+    L.cnmf_context_create_hosted.argtypes = [C.c_int, C.c_int, C.c_int, C.POINTER(_HostColl),
+                                             C.POINTER(vp)]
     L.cnmf_run_sharded_device.argtypes = [vp, fp, u64, u64, u64, u64, u64, C.POINTER(_Config), fp,
                                           fp, C.POINTER(_Trace)]
     L.cnmf_run_csr.argtypes = [vp, vp, vp, vp, u64, u64, C.POINTER(_Config), fp, fp,
@@ -189,7 +191,7 @@ def load_library(path: str = LIB_PATH):
                                           C.c_char_p, C.c_size_t]
     L.cnmf_pairwise_distortion.argtypes = [vp, u64, u64, vp, u64, u64, u64, dp, dp, C.c_char_p,
                                            C.c_size_t]
-    if L.cnmf_abi_version() != 1:
+    if L.cnmf_abi_version() != 2:
         raise CudaError("libcnmf_b200.so ABI version mismatch")
     _lib = L
     return L
@@ -239,6 +241,7 @@ class RunRecord:
     iteration: int
     error: float
     elapsed_seconds: float
+    rng_draws: int = 0  # raw draws the redraws took from the run Rng so far
 
 
 @dataclass
@@ -282,6 +285,26 @@ def _ptr(t) -> int:
     return t.data_ptr()
 
 
+def _check_device_operands(x, a, b, d, n, k):
+    """X (d x n) and the factor outputs A (d x k), B (n x k) as the C ABI reads
+    them: fp32 CUDA tensors, unit column stride, contiguous factors.  Also
+    orders the library's stream after torch's current stream: X or the
+    outputs may have been produced by torch work still in flight."""
+    import torch
+    for name, t, shape in (("x", x, (d, n)), ("a_out", a, (d, k)), ("b_out", b, (n, k))):
+        if not (isinstance(t, torch.Tensor) and t.is_cuda and t.dtype == torch.float32):
+            raise DimensionError(f"{name} must be a float32 CUDA tensor")
+        if tuple(t.shape) != shape or (t.dim() == 2 and shape[1] > 1 and t.stride(1) != 1):
+            raise DimensionError(f"{name} must be {shape[0]} x {shape[1]} with unit column stride")
+        if t.device != x.device:
+            raise DimensionError(f"{name} is on {t.device}, X on {x.device}")
+    if not (a.is_contiguous() and b.is_contiguous()):
+        raise DimensionError("a_out and b_out must be contiguous")
+    if x.stride(0) < n:
+        raise DimensionError("x row stride is shorter than its width")
+    torch.cuda.current_stream(x.device).synchronize()
+
+
 class Context:
     """One CUDA device + stream (cnmf_context)."""
 
@@ -322,7 +345,8 @@ class Context:
     @staticmethod
     def _result_trace(recs, tr) -> RunTrace:
         n = min(tr.records_count, tr.records_capacity)
-        return RunTrace([RunRecord(recs[i].iteration, recs[i].error, recs[i].elapsed_seconds)
+        return RunTrace([RunRecord(recs[i].iteration, recs[i].error, recs[i].elapsed_seconds,
+                                   recs[i].rng_draws)
                          for i in range(n)], tr.update_seconds, tr.compress_seconds,
                         tr.error_seconds, tr.gini_b, tr.status, tr.iterations_run,
                         tr.power_iterations, tr.alpha, tr.beta, tr.seed,
@@ -373,6 +397,7 @@ class Context:
         ldx = x.stride(0)
         a = a_out if a_out is not None else torch.empty((d, config.k), device=x.device)
         b = b_out if b_out is not None else torch.empty((n, config.k), device=x.device)
+        _check_device_operands(x, a, b, d, n, config.k)
         cfg = config._c()
         recs, tr = self._trace(config.max_iterations + 2)
         self._check(self.L.cnmf_run_device(self.h, _ptr(x), d, n, ldx, C.byref(cfg), _ptr(a),
@@ -519,12 +544,67 @@ class ShardedContext(Context):
         lo = shard_begin(n, self.rank, self.world)
         a = a_out if a_out is not None else torch.empty((d, config.k), device=x_shard.device)
         b = b_out if b_out is not None else torch.empty((nloc, config.k), device=x_shard.device)
+        _check_device_operands(x_shard, a, b, d, nloc, config.k)
         cfg = config._c()
         recs, tr = self._trace(config.max_iterations + 2)
         self._check(self.L.cnmf_run_sharded_device(self.h, _ptr(x_shard), d, n, lo, nloc,
                                                    x_shard.stride(0), C.byref(cfg), _ptr(a), _ptr(b),
                                                    C.byref(tr)))
         return a, b, self._result_trace(recs, tr)
+
+_AllreduceFn = C.CFUNCTYPE(C.c_int, C.c_void_p, C.c_uint64, C.c_int, C.c_int, C.c_void_p)
+_AllgatherFn = C.CFUNCTYPE(C.c_int, C.c_void_p, C.c_void_p, C.c_uint64, C.c_void_p)
+
+
+class _HostColl(C.Structure):
+    _fields_ = [("allreduce", _AllreduceFn), ("allgather", _AllgatherFn), ("user", C.c_void_p)]
+
+
+class HostedShardedContext(ShardedContext):
+    """A rank of a column-sharded run whose collectives are host-staged
+    through torch.distributed (cnmf_context_create_hosted) instead of NCCL --
+    e.g. a gloo group of two processes sharing ONE GPU, where NCCL cannot run
+    (tests).  Same kernels, same run_sharded_impl as the NCCL context."""
+
+    def __init__(self, device: int, group=None):
+        import torch
+        import torch.distributed as dist
+        self.L = load_library()
+        rank, world = dist.get_rank(group), dist.get_world_size(group)
+
+        def allreduce(buf, count, dtype, op, _user):
+            try:
+                ct = C.c_double if dtype == 1 else C.c_float
+                arr = np.ctypeslib.as_array(C.cast(buf, C.POINTER(ct)), shape=(count,))
+                t = torch.from_numpy(arr)
+                dist.all_reduce(t, op=dist.ReduceOp.MAX if op else dist.ReduceOp.SUM,
+                                group=group)
+                return 0
+            except Exception:  # noqa: BLE001 -- reported to the library as a failure
+                return 1
+
+        def allgather(send, recv, nbytes, _user):
+            try:
+                src = torch.from_numpy(np.ctypeslib.as_array(
+                    C.cast(send, C.POINTER(C.c_uint8)), shape=(nbytes,)).copy())
+                parts = [torch.empty(nbytes, dtype=torch.uint8) for _ in range(world)]
+                dist.all_gather(parts, src, group=group)
+                dst = np.ctypeslib.as_array(C.cast(recv, C.POINTER(C.c_uint8)),
+                                            shape=(nbytes * world,))
+                for g, part in enumerate(parts):
+                    dst[g * nbytes:(g + 1) * nbytes] = part.numpy()
+                return 0
+            except Exception:  # noqa: BLE001
+                return 1
+
+        self._cb = _HostColl(_AllreduceFn(allreduce), _AllgatherFn(allgather), None)
+        h = C.c_void_p()
+        st = self.L.cnmf_context_create_hosted(device, rank, world, C.byref(self._cb), C.byref(h))
+        if st:
+            raise _ERRORS.get(st, CnmfError)(f"cannot create hosted context (rank {rank}/{world})")
+        self.h = h
+        self.rank, self.world = rank, world
+
 
 # ---- host-side data formats around the path (no device) --------------------
 def _host_check(st: int, msg) -> None:

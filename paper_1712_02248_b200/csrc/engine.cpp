@@ -60,7 +60,10 @@ struct cnmf_context {
   std::mutex mu;
   std::map<std::string, DevBuf> bufs;
   HaltInfo* halt_host = nullptr;  // pinned
+  uint64_t* pos_host = nullptr;   // pinned (the run stream's position)
   void* nccl = nullptr;           // ncclComm_t of a sharded context
+  cnmf_host_collectives hosted{}; // host-staged collectives of a sharded context (tests)
+  std::vector<char> host_stage;
   std::map<std::string, bool> filled;  // device copies uploaded once (jump polynomials)
   int rank = 0, world = 1;
 
@@ -170,22 +173,109 @@ void gen_normals(cnmf_context* c, uint64_t seed, int64_t rows, int64_t cols, flo
   CK(cudaGetLastError());
 }
 
-// initialize(d, n, k, seed) into column-major A_cm / B_cm; returns the
-// device counter of raw draws consumed (for positioning the host Rng).
-uint64_t* gen_init(cnmf_context* c, uint64_t seed, int64_t d, int64_t n, int k, double* a_cm,
-                   double* b_cm) {
+// The run's Rng (solvers.cpp:204-211, one generator for initialize() and
+// every later reinit_column, 28-31) on the device: one word buffer holds the
+// stream's first `nwords` raw outputs; `pos` (device) is the next unused
+// word.  initialize() fills A then B from words [0, (d+n)k + rejections);
+// each redraw takes the next rows from pos on (launch_redraw_fill), so the
+// host never generates or uploads a column.  When a redraw would run past
+// the buffer it is regenerated longer (same prefix).
+struct RunStream {
+  cnmf_context* c = nullptr;
+  uint64_t seed = 0;
+  uint64_t nwords = 0;
+  uint64_t* words = nullptr;
+  uint64_t* pos = nullptr;     // device: next unused raw word
+  int* flag = nullptr;         // device scratch of the fill kernels
+  uint64_t init_end = 0;       // raw words initialize() used (host, after settle)
+  uint64_t pos_host = 0;       // host copy of *pos (refreshed by sync_pos / take_pos)
+  uint64_t* pos_pinned = nullptr;
+  bool pending = true;         // init_end not read back yet
+
+  // queues the D2H copy of *pos (read it after the stream syncs)
+  void queue_pos() {
+    CK(cudaMemcpyAsync(pos_pinned, pos, sizeof(uint64_t), cudaMemcpyDeviceToHost, c->stream));
+  }
+  void take_pos() { pos_host = *pos_pinned; }
+  void sync_pos() {
+    queue_pos();
+    c->sync();
+    take_pos();
+  }
+  // reads initialize()'s draw count back once (syncs the stream)
+  void settle() {
+    if (!pending) return;
+    c->sync();
+    take_pos();
+    init_end = pos_host;
+    pending = false;
+  }
+  uint64_t draws() const { return pos_host - init_end; }
+  void grow(uint64_t need) {
+    uint64_t nw = std::max<uint64_t>(2 * nwords, need + (need >> 2) + 4096);
+    // the buffer is rewritten from the seed: the same prefix, longer
+    c->sync();
+    words = c->ws<uint64_t>("words_run", nw);
+    gen_words(c, seed, nw, words, "run", c->stream);
+    nwords = nw;
+  }
+  // reinit_column of a rows_total-long column, keeping [off, off + count) in
+  // col (count < rows_total: a sharded rank's slice of a B column).  pos_host
+  // must be current (every caller syncs on the halt record first).
+  void redraw(double* col, uint64_t rows_total, uint64_t off, uint64_t count) {
+    if (pos_host + rows_total + 64 > nwords) grow(pos_host + rows_total + 64);
+    launch_redraw_fill(words, nwords, pos, rows_total, off, count, col, flag, c->nsm, c->stream);
+    CK(cudaGetLastError());
+  }
+  void redraw(double* col, uint64_t rows) { redraw(col, rows, 0, rows); }
+};
+
+// initialize(d, n, k, seed) into column-major A_cm / B_cm (solvers.cpp:
+// 206-211), the stream generated with room for `reserve` redraw draws.
+RunStream gen_init(cnmf_context* c, uint64_t seed, int64_t d, int64_t n, int k, double* a_cm,
+                   double* b_cm, uint64_t reserve) {
   const uint64_t total = (uint64_t)(d + n) * k;
-  const uint64_t nwords = total + 256;
-  uint64_t* words = c->ws<uint64_t>("words_init", nwords);
+  RunStream rs;
+  rs.c = c;
+  rs.seed = seed;
+  rs.nwords = total + 256 + reserve;
+  rs.words = c->ws<uint64_t>("words_run", rs.nwords);
   int* flag = c->ws<int>("iflag", 4);
-  uint64_t* consumed = c->ws<uint64_t>("iconsumed", 1);
-  CK(cudaMemsetAsync(flag, 0, sizeof(int), c->stream));
-  CK(cudaMemcpyAsync(consumed, &total, sizeof(uint64_t), cudaMemcpyHostToDevice, c->stream));
-  gen_words(c, seed, nwords, words, "init", c->stream);
-  launch_uniform_init(words, d, n, k, a_cm, b_cm, flag, c->nsm, c->stream);
-  launch_uniform_init_exact(words, nwords, d, n, k, a_cm, b_cm, flag, consumed, c->stream);
+  rs.flag = flag + 1;
+  rs.pos = c->ws<uint64_t>("iconsumed", 1);
+  rs.pos_pinned = c->pos_host;
+  CK(cudaMemsetAsync(flag, 0, 2 * sizeof(int), c->stream));
+  CK(cudaMemcpyAsync(rs.pos, &total, sizeof(uint64_t), cudaMemcpyHostToDevice, c->stream));
+  gen_words(c, seed, rs.nwords, rs.words, "run", c->stream);
+  launch_uniform_init(rs.words, d, n, k, a_cm, b_cm, flag, c->nsm, c->stream);
+  launch_uniform_init_exact(rs.words, rs.nwords, d, n, k, a_cm, b_cm, flag, rs.pos, c->stream);
   CK(cudaGetLastError());
-  return consumed;
+  rs.queue_pos();  // read back by settle() at the next synchronisation
+  return rs;
+}
+
+// A fresh Rng(seed) on the device (step-level API: no initialize() draws).
+RunStream fresh_stream(cnmf_context* c, uint64_t seed, uint64_t reserve) {
+  RunStream rs;
+  rs.c = c;
+  rs.seed = seed;
+  rs.nwords = reserve + 256;
+  rs.words = c->ws<uint64_t>("words_run", rs.nwords);
+  int* flag = c->ws<int>("iflag", 4);
+  rs.flag = flag + 1;
+  rs.pos = c->ws<uint64_t>("iconsumed", 1);
+  rs.pos_pinned = c->pos_host;
+  CK(cudaMemsetAsync(flag, 0, 2 * sizeof(int), c->stream));
+  CK(cudaMemsetAsync(rs.pos, 0, sizeof(uint64_t), c->stream));
+  gen_words(c, seed, rs.nwords, rs.words, "run", c->stream);
+  rs.pending = false;
+  return rs;
+}
+
+// Redraw reserve generated with the init stream: a few columns of the longer
+// side (more are generated on demand).
+uint64_t redraw_reserve(int64_t d, int64_t n) {
+  return std::max<uint64_t>(1u << 20, 4 * (uint64_t)std::max(d, n));
 }
 
 // ---------------------------------------------------------- compression -----
@@ -293,10 +383,14 @@ struct HalsRun {
   int grid;
   bool resident;  // shared-memory-resident kernel (hals_resident.cu)
   unsigned long long epoch;  // next launch's exchange epoch base
+  unsigned long long nr = 0; // norm all-reduces done so far (HalsState::nr0 of the next launch)
 };
 
+// grid_rows (> 0): choose the grid and kernel as if B had grid_rows rows
+// (sharded runs: every rank must use the same launch shape, so the A half it
+// runs replicated splits its rows -- and rounds -- identically everywhere).
 HalsRun make_hals(cnmf_context* c, int64_t d, int64_t n, int l, int lp, int k,
-                  bool allow_resident = true) {
+                  bool allow_resident = true, int64_t grid_rows = 0) {
   HalsRun r;
   HalsState& s = r.st;
   s.d = d;
@@ -313,11 +407,13 @@ HalsRun make_hals(cnmf_context* c, int64_t d, int64_t n, int l, int lp, int k,
   const char* mode = std::getenv("CNMF_HALS");
   s.dense = 0;
   s.hd = s.pd = s.gd = s.wd = nullptr;
+  if (grid_rows > 0) s.n = grid_rows;
   const int rgrid = (!allow_resident || (mode && std::string(mode) == "stream"))
                         ? 0
                         : hals_resident_grid(s, c->nsm);
   r.resident = rgrid > 0;
   r.grid = r.resident ? rgrid : hals_grid(s, c->nsm);
+  s.n = n;
   if (!r.resident && (d + r.grid - 1) / r.grid > 6 * 256)
     throw Fail(CNMF_ERR_UNSUPPORTED,
                "this build's streaming HALS kernel supports at most 1536 rows of A per SM");
@@ -328,6 +424,7 @@ HalsRun make_hals(cnmf_context* c, int64_t d, int64_t n, int l, int lp, int k,
   s.npart = c->ws<double>("hals_npart", (size_t)2 * r.grid);
   s.zpart = c->ws<unsigned>("hals_zpart", (size_t)4 * r.grid + 4);
   s.sharded = 0;
+  s.nr0 = 0;
   s.bar = c->ws<unsigned>("hals_bar", 64);
   s.halt = c->ws<HaltInfo>("hals_halt", 1);
   s.prof = nullptr;
@@ -336,7 +433,8 @@ HalsRun make_hals(cnmf_context* c, int64_t d, int64_t n, int l, int lp, int k,
     CK(cudaMemsetAsync(s.prof, 0, 32 * sizeof(long long), c->stream));
   }
   CK(cudaMemsetAsync(s.bar, 0, 64 * sizeof(unsigned), c->stream));
-  // the norm all-reduce's tagged slots start as +0.0, which no first use accepts
+  // the norm all-reduce's tagged slots start as +0.0, which the first use of
+  // either buffer (negative tag, nr = 0 and 1) does not accept
   CK(cudaMemsetAsync(s.npart, 0, sizeof(double) * 2 * r.grid, c->stream));
   CK(cudaMemsetAsync(s.ahat, 0, sizeof(double) * lp * k, c->stream));
   CK(cudaMemsetAsync(s.bchk, 0, sizeof(double) * lp * k, c->stream));
@@ -344,62 +442,59 @@ HalsRun make_hals(cnmf_context* c, int64_t d, int64_t n, int l, int lp, int k,
   return r;
 }
 
-// Draws reinit_column (solvers.cpp:28-31) from the host Rng into a device column.
-void redraw_column(cnmf_context* c, std::mt19937_64& rng, double* col_dev, int64_t rows) {
-  std::vector<double> v((size_t)rows);
-  for (int64_t i = 0; i < rows; ++i) v[(size_t)i] = uniform_positive(rng) * 1e-3;
-  CK(cudaMemcpyAsync(col_dev, v.data(), sizeof(double) * rows, cudaMemcpyHostToDevice, c->stream));
-  c->sync();  // v goes out of scope
-}
-
-// Runs 0-based iterations [ib, ie) with halt/redraw servicing.  `rng` is
-// produced lazily (positioning the host stream costs a discard).
+// Runs 0-based iterations [ib, ie) with halt/redraw servicing.  A halt
+// (dead or emptied component) is served on the device: the column is drawn
+// from the run stream (RunStream::redraw), its compressed view refreshed, and
+// the kernel relaunched at the reference's event point.  update_seconds
+// brackets the whole range, halts included (solvers.cpp:235-259 times the
+// whole step, redraws and cross-product refreshes included).
 // recheck_dead: HALS-RP redraws a dead component until it is alive
 // (solvers.cpp:366-372, `while`); FastHALS-RP checks once (424, `if`).
-template <typename RngFn>
 void run_hals(cnmf_context* c, HalsRun& hr, int normalize_a, double alpha, double beta,
-              int64_t ib, int64_t ie, RngFn&& get_rng, double* update_seconds,
-              uint64_t* redraws, bool recheck_dead = false) {
+              int64_t ib, int64_t ie, RunStream& rs, double* update_seconds, uint64_t* redraws,
+              bool recheck_dead = false) {
   HalsState& st = hr.st;
   int half = 0, col = 0, skip = -1;
   int64_t begin = ib;
+  rs.settle();
+  CK(cudaEventRecord(c->ev[0], c->stream));
   for (;;) {
-    CK(cudaEventRecord(c->ev[0], c->stream));
+    st.nr0 = hr.nr;
     if (hr.resident)
       CK(launch_hals_resident(st, normalize_a, alpha, beta, (int)begin, (int)ie, half, col, skip,
                               hr.epoch, hr.grid, c->stream));
     else
       CK(launch_hals(st, normalize_a, alpha, beta, (int)begin, (int)ie, half, col, skip,
                      hr.epoch, hr.grid, c->stream));
-    CK(cudaEventRecord(c->ev[1], c->stream));
     CK(cudaMemcpyAsync(c->halt_host, st.halt, sizeof(HaltInfo), cudaMemcpyDeviceToHost,
                        c->stream));
+    rs.queue_pos();
     c->sync();
-    *update_seconds += c->elapsed(0, 1);
+    rs.take_pos();
     const HaltInfo h = *c->halt_host;
     hr.epoch = h.last_epoch;
+    hr.nr = h.last_nr;
     if (h.pad) std::swap(st.b, st.bold);  // the kernel double-buffers B
     if (!h.halted) break;
-    std::mt19937_64& rng = get_rng();
     const int j = h.column;
     switch (h.kind) {
       case kEvDeadB:  // solvers.cpp:424-428
-        redraw_column(c, rng, st.b + (int64_t)j * st.n, st.n);
+        rs.redraw(st.b + (int64_t)j * st.n, st.n);
         launch_compress_factors(st, 1, j, c->stream);
         half = 0; col = j; skip = recheck_dead ? -1 : j;
         break;
       case kEvZeroA:  // solvers.cpp:435-436
-        redraw_column(c, rng, st.a + (int64_t)j * st.d, st.d);
+        rs.redraw(st.a + (int64_t)j * st.d, st.d);
         if (normalize_a) launch_normalize_column(st.a, st.d, j, c->stream);
         half = 0; col = j + 1; skip = -1;
         break;
       case kEvDeadA:  // solvers.cpp:445-449
-        redraw_column(c, rng, st.a + (int64_t)j * st.d, st.d);
+        rs.redraw(st.a + (int64_t)j * st.d, st.d);
         launch_compress_factors(st, 0, j, c->stream);
         half = 1; col = j; skip = recheck_dead ? -1 : j;
         break;
       case kEvZeroB:  // solvers.cpp:452
-        redraw_column(c, rng, st.b + (int64_t)j * st.n, st.n);
+        rs.redraw(st.b + (int64_t)j * st.n, st.n);
         half = 1; col = j + 1; skip = -1;
         break;
       default:
@@ -409,6 +504,9 @@ void run_hals(cnmf_context* c, HalsRun& hr, int normalize_a, double alpha, doubl
     begin = h.iter - 1;
     ++*redraws;
   }
+  CK(cudaEventRecord(c->ev[1], c->stream));
+  c->sync();
+  *update_seconds += c->elapsed(0, 1);
 }
 
 // ------------------------------------------------ uncompressed solvers -----
@@ -466,9 +564,8 @@ void dense_prepare_b(cnmf_context* c, const XView& X, const double* a_cm, int k,
 // host then replays the pointer state up to the halted launch, draws the
 // column from the run Rng and resumes there (products are recomputed before
 // every launch, which is refresh_cross_products, solvers.cpp:133-144).
-template <typename RngFn>
 void run_dense_hals(cnmf_context* c, HalsRun& hr, const XView& X, DenseBufs& db, int normalize_a,
-                    int64_t ib, int64_t ie, RngFn&& get_rng, double* update_seconds,
+                    int64_t ib, int64_t ie, RunStream& rs, double* update_seconds,
                     uint64_t* redraws, bool recheck_dead) {
   HalsState& st = hr.st;
   const int k = st.k;
@@ -479,9 +576,10 @@ void run_dense_hals(cnmf_context* c, HalsRun& hr, const XView& X, DenseBufs& db,
   st.wd = db.w;
   int half = 0, col = 0, skip = -1;
   int64_t begin = ib;
+  rs.settle();
+  CK(cudaEventRecord(c->ev[0], c->stream));
   for (;;) {
     CK(cudaMemsetAsync(st.halt, 0, sizeof(HaltInfo), c->stream));
-    CK(cudaEventRecord(c->ev[0], c->stream));
     double* b = st.b;
     double* bold = st.bold;
     // Each queued launch starts at the exchange epoch the launches before it
@@ -489,7 +587,7 @@ void run_dense_hals(cnmf_context* c, HalsRun& hr, const XView& X, DenseBufs& db,
     // norm all-reduces, a B half one exchange (a launch that halts instead
     // turns the rest of the queue into no-ops, and the host resumes from the
     // halt record's epoch).
-    unsigned long long ep_q = hr.epoch;
+    unsigned long long ep_q = hr.epoch, nr_q = hr.nr;
     {
       int h0 = half, c0 = col, s0 = skip;
       for (int64_t it = begin; it < ie; ++it) {
@@ -497,6 +595,7 @@ void run_dense_hals(cnmf_context* c, HalsRun& hr, const XView& X, DenseBufs& db,
           HalsState s2 = st;
           s2.b = b;
           s2.bold = bold;
+          s2.nr0 = nr_q;
           const int* hflag = &st.halt->halted;
           if (h == 0)
             dense_prepare_a(c, X, b, k, db, hflag);
@@ -505,6 +604,7 @@ void run_dense_hals(cnmf_context* c, HalsRun& hr, const XView& X, DenseBufs& db,
           CK(launch_hals(s2, normalize_a, 0.0, 0.0, (int)it, (int)it + 1, h, c0, s0, ep_q,
                          hr.grid, c->stream));
           ep_q += h == 0 ? (unsigned long long)(k - c0) : 1ULL;
+          nr_q += h == 0 ? (unsigned long long)(k - c0) : 0ULL;  // one norm all-reduce per column
           if (h == 1) std::swap(b, bold);  // the B half leaves the new B in the second buffer
           c0 = 0;
           s0 = -1;
@@ -512,15 +612,18 @@ void run_dense_hals(cnmf_context* c, HalsRun& hr, const XView& X, DenseBufs& db,
         h0 = 0;
       }
     }
-    CK(cudaEventRecord(c->ev[1], c->stream));
     CK(cudaMemcpyAsync(c->halt_host, st.halt, sizeof(HaltInfo), cudaMemcpyDeviceToHost,
                        c->stream));
+    rs.queue_pos();
     c->sync();
-    *update_seconds += c->elapsed(0, 1);
+    rs.take_pos();
     const HaltInfo h = *c->halt_host;
-    if (h.last_epoch) hr.epoch = h.last_epoch;
+    if (h.last_epoch) {
+      hr.epoch = h.last_epoch;
+      hr.nr = h.last_nr;
+    }
     if (!h.halted) {
-      if (h.last_epoch != ep_q)
+      if (h.last_epoch != ep_q || h.last_nr != nr_q)
         throw Fail(CNMF_ERR_CUDA, "dense HALS: exchange epoch bookkeeping mismatch");
       st.b = b;
       st.bold = bold;
@@ -547,24 +650,23 @@ void run_dense_hals(cnmf_context* c, HalsRun& hr, const XView& X, DenseBufs& db,
       st.bold = bold;
     }
     if (h.pad) std::swap(st.b, st.bold);
-    std::mt19937_64& rng = get_rng();
     const int j = h.column;
     switch (h.kind) {
       case kEvDeadB:  // solvers.cpp:159-162
-        redraw_column(c, rng, st.b + (int64_t)j * st.n, st.n);
+        rs.redraw(st.b + (int64_t)j * st.n, st.n);
         half = 0; col = j; skip = recheck_dead ? -1 : j;
         break;
       case kEvZeroA:  // solvers.cpp:168-169
-        redraw_column(c, rng, st.a + (int64_t)j * st.d, st.d);
+        rs.redraw(st.a + (int64_t)j * st.d, st.d);
         if (normalize_a) launch_normalize_column(st.a, st.d, j, c->stream);
         half = 0; col = j + 1; skip = -1;
         break;
       case kEvDeadA:  // solvers.cpp:178-181
-        redraw_column(c, rng, st.a + (int64_t)j * st.d, st.d);
+        rs.redraw(st.a + (int64_t)j * st.d, st.d);
         half = 1; col = j; skip = recheck_dead ? -1 : j;
         break;
       case kEvZeroB:  // solvers.cpp:185
-        redraw_column(c, rng, st.b + (int64_t)j * st.n, st.n);
+        rs.redraw(st.b + (int64_t)j * st.n, st.n);
         half = 1; col = j + 1; skip = -1;
         break;
       default:
@@ -574,6 +676,9 @@ void run_dense_hals(cnmf_context* c, HalsRun& hr, const XView& X, DenseBufs& db,
     begin = h.iter - 1;
     ++*redraws;
   }
+  CK(cudaEventRecord(c->ev[1], c->stream));
+  c->sync();
+  *update_seconds += c->elapsed(0, 1);
 }
 
 // mu_step (solvers.cpp:55-64, 327-330): A .*= X B ./ (A B^T B + eps), then B
@@ -707,8 +812,8 @@ void run_device_impl(cnmf_context* c, const XView& X0, const cnmf_solver_config&
     t.estimate_memory_floats = ce.memory_floats;
   }
   (void)hals_rp;
-  auto push = [&](uint64_t it, double err, double el) {
-    if (t.records_count < t.records_capacity) t.records[t.records_count] = {it, err, el};
+  auto push = [&](uint64_t it, double err, double el, uint64_t draws) {
+    if (t.records_count < t.records_capacity) t.records[t.records_count] = {it, err, el, draws};
     ++t.records_count;
   };
 
@@ -746,7 +851,7 @@ void run_device_impl(cnmf_context* c, const XView& X0, const cnmf_solver_config&
   if (!compressed || algo == CNMF_MU_RP) db = make_dense(c, d, n, k);
 
   // Rng rng(seed); A then B uniform_positive (solvers.cpp:206-211).
-  uint64_t* consumed_dev = gen_init(c, cfg.seed, d, n, k, st.a, st.b);
+  RunStream rs = gen_init(c, cfg.seed, d, n, k, st.a, st.b, redraw_reserve(d, n));
 
   // ---- compression (build_projectors + compress_left/right) ----
   if (compressed) {
@@ -780,19 +885,6 @@ void run_device_impl(cnmf_context* c, const XView& X0, const cnmf_solver_config&
   t.compress_seconds = c->elapsed(2, 3);
   }
 
-  std::mt19937_64 rng;
-  bool rng_ready = false;
-  auto get_rng = [&]() -> std::mt19937_64& {
-    if (!rng_ready) {
-      uint64_t consumed = 0;
-      CK(cudaMemcpy(&consumed, consumed_dev, sizeof(uint64_t), cudaMemcpyDeviceToHost));
-      rng.seed(cfg.seed);
-      rng.discard(consumed);
-      rng_ready = true;
-    }
-    return rng;
-  };
-
   auto timed_error = [&]() {
     CK(cudaEventRecord(c->ev[2], c->stream));
     const double e = recon_error(c, X, st.a, st.b, k);
@@ -807,7 +899,7 @@ void run_device_impl(cnmf_context* c, const XView& X0, const cnmf_solver_config&
     t.status = CNMF_ABORTED;
     std::snprintf(t.message, sizeof t.message, "non-finite objective at iteration 0");
   } else {
-    push(0, previous, 0.0);
+    push(0, previous, 0.0, 0);
   }
   const uint64_t max_it = cfg.max_iterations, every = cfg.error_interval;
   uint64_t it = 1;
@@ -815,14 +907,14 @@ void run_device_impl(cnmf_context* c, const XView& X0, const cnmf_solver_config&
     uint64_t e = ((it + every - 1) / every) * every;
     if (e > max_it) e = max_it;
     if (dense_hals)
-      run_dense_hals(c, hr, X, db, normalize_a, (int64_t)it - 1, (int64_t)e, get_rng,
+      run_dense_hals(c, hr, X, db, normalize_a, (int64_t)it - 1, (int64_t)e, rs,
                      &t.update_seconds, &t.redraws, recheck);
     else if (algo == CNMF_MU)
       run_mu(c, st, X, db, (int64_t)(e - it + 1), &t.update_seconds);
     else if (algo == CNMF_MU_RP)
       run_mu_rp(c, st, db, (int64_t)(e - it + 1), &t.update_seconds);
     else
-      run_hals(c, hr, normalize_a, cfg.alpha, cfg.beta, (int64_t)it - 1, (int64_t)e, get_rng,
+      run_hals(c, hr, normalize_a, cfg.alpha, cfg.beta, (int64_t)it - 1, (int64_t)e, rs,
                &t.update_seconds, &t.redraws, recheck);
     t.iterations_run = e;
     const double err = timed_error();
@@ -832,7 +924,7 @@ void run_device_impl(cnmf_context* c, const XView& X0, const cnmf_solver_config&
                     (unsigned long long)e);
       break;
     }
-    push(e, err, t.update_seconds);
+    push(e, err, t.update_seconds, rs.draws());
     const bool converged = previous == 0.0 ? err == 0.0
                                            : std::fabs(previous - err) / previous <
                                                  cfg.rel_tolerance;
@@ -932,7 +1024,8 @@ cnmf_status cnmf_context_create(int device, cnmf_context** out) {
       cudaEventCreateWithFlags(&c->fork, cudaEventDisableTiming) != cudaSuccess ||
       cudaEventCreateWithFlags(&c->join, cudaEventDisableTiming) != cudaSuccess ||
       cudaDeviceGetAttribute(&c->nsm, cudaDevAttrMultiProcessorCount, device) != cudaSuccess ||
-      cudaMallocHost(&c->halt_host, sizeof(HaltInfo)) != cudaSuccess) {
+      cudaMallocHost(&c->halt_host, sizeof(HaltInfo)) != cudaSuccess ||
+      cudaMallocHost(&c->pos_host, 2 * sizeof(uint64_t)) != cudaSuccess) {
     delete c;
     return CNMF_ERR_CUDA;
   }
@@ -954,6 +1047,7 @@ void cnmf_context_destroy(cnmf_context* c) {
   for (auto& e : c->ev)
     if (e) cudaEventDestroy(e);
   if (c->halt_host) cudaFreeHost(c->halt_host);
+  if (c->pos_host) cudaFreeHost(c->pos_host);
   if (c->side) {
     cudaStreamSynchronize(c->side);
     cudaStreamDestroy(c->side);
@@ -1150,6 +1244,19 @@ cnmf_status cnmf_context_create_sharded(int device, int rank, int world,
   return CNMF_OK;
 }
 
+cnmf_status cnmf_context_create_hosted(int device, int rank, int world,
+                                       const cnmf_host_collectives* coll, cnmf_context** out) {
+  if (!out || !coll || !coll->allreduce || !coll->allgather || world < 1 || rank < 0 ||
+      rank >= world)
+    return CNMF_ERR_CONFIG;
+  const cnmf_status s = cnmf_context_create(device, out);
+  if (s != CNMF_OK) return s;
+  (*out)->hosted = *coll;
+  (*out)->rank = rank;
+  (*out)->world = world;
+  return CNMF_OK;
+}
+
 cnmf_status cnmf_run_sharded_device(cnmf_context* c, const float* x_shard, uint64_t d, uint64_t n,
                                     uint64_t col_begin, uint64_t n_local, uint64_t ldx,
                                     const cnmf_solver_config* cfg, float* a_dev, float* b_local_dev,
@@ -1177,7 +1284,7 @@ cnmf_status cnmf_initialize(cnmf_context* c, uint64_t d, uint64_t n, uint64_t k,
       throw Fail(CNMF_ERR_CONFIG, "initialize requires positive dimensions");
     double* acm = c->ws<double>("init_acm", d * k);
     double* bcm = c->ws<double>("init_bcm", n * k);
-    gen_init(c, seed, (int64_t)d, (int64_t)n, (int)k, acm, bcm);
+    gen_init(c, seed, (int64_t)d, (int64_t)n, (int)k, acm, bcm, 0);
     launch_cm_to_rm(acm, (int64_t)d, (int)k, a, c->stream);
     launch_cm_to_rm(bcm, (int64_t)n, (int)k, b, c->stream);
     CK(cudaGetLastError());
@@ -1308,11 +1415,10 @@ cnmf_status cnmf_fasthals_rp_steps(cnmf_context* c, const float* xhat, const flo
     CK(cudaMemcpyAsync(st.bchk, b_check, sizeof(double) * q * k, cudaMemcpyDeviceToDevice,
                        c->stream));
     CK(cudaGetLastError());
-    std::mt19937_64 rng(rng_seed);
+    RunStream rs = fresh_stream(c, rng_seed, redraw_reserve((int64_t)d, (int64_t)n));
     double secs = 0.0;
     uint64_t nr = 0;
-    run_hals(c, hr, normalize_a, alpha, beta, 0, (int64_t)steps,
-             [&]() -> std::mt19937_64& { return rng; }, &secs, &nr);
+    run_hals(c, hr, normalize_a, alpha, beta, 0, (int64_t)steps, rs, &secs, &nr);
     launch_cm_to_rm(st.a, (int64_t)d, (int)k, a, c->stream);
     launch_cm_to_rm(st.b, (int64_t)n, (int)k, b, c->stream);
     CK(cudaMemcpyAsync(a_hat, st.ahat, sizeof(double) * q * k, cudaMemcpyDeviceToDevice, c->stream));

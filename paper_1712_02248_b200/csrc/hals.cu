@@ -410,6 +410,7 @@ __global__ void __launch_bounds__(kThreads, 1) hals_kernel(const HalsArgs p) {
   }
   if (S.dense && __ldcg(&S.halt->halted)) return;  // queued behind a halt: no-op
   unsigned long long ep = p.epoch0;
+  unsigned long long nr = S.nr0;  // norm all-reduces so far (slot tags)
   bool have_g = false, have_w = false;
   double* bcur = S.b;  // B as of the start of the B half
   double* bnxt = S.bold;
@@ -520,7 +521,7 @@ __global__ void __launch_bounds__(kThreads, 1) hals_kernel(const HalsArgs p) {
             an[i] = ok ? __ldcg(S.a + (int64_t)(j + 1) * d + a_lo + r) : 0.0;
           }
           HALS_PROF(2);
-          const double total = allreduce_fused(S, G, cta, ep, nrm, red8, s_red);
+          const double total = allreduce_fused(S, G, cta, ep, nr, nrm, red8, s_red);
           HALS_PROF(3);
           if (total == 0.0) {  // column emptied: host redraws a_j (solvers.cpp:435)
 #pragma unroll
@@ -528,8 +529,10 @@ __global__ void __launch_bounds__(kThreads, 1) hals_kernel(const HalsArgs p) {
               const int r = tid + kThreads * i;
               if (i < rpt && r < na) S.a[(int64_t)j * d + a_lo + r] = 0.0;
             }
-            if (cta == 0 && tid == 0)
+            if (cta == 0 && tid == 0) {
               *S.halt = HaltInfo{1, it + 1, 0, j, kEvZeroA, bcur == S.bold, ep};
+              S.halt->last_nr = nr;
+            }
             return;
           }
           const double inv_nrm = s_red[1];
@@ -553,13 +556,16 @@ __global__ void __launch_bounds__(kThreads, 1) hals_kernel(const HalsArgs p) {
       }
       __syncthreads();
       if (jd < k) {  // dead B column: host redraws b_jd (solvers.cpp:424-428)
-        if (cta == 0 && tid == 0)
+        if (cta == 0 && tid == 0) {
           *S.halt = HaltInfo{1, it + 1, 0, jd, kEvDeadB, bcur == S.bold, ep};
+          S.halt->last_nr = nr;
+        }
         return;
       }
       if (S.dense) {  // one half per launch
         if (cta == 0 && tid == 0) {
           *S.halt = HaltInfo{0, it + 1, 0, 0, 0, bcur == S.bold, ep};
+          S.halt->last_nr = nr;
           if (prof)
             for (int i = 0; i < 21; ++i) S.prof[i] += s_prof[i];
         }
@@ -740,7 +746,7 @@ __global__ void __launch_bounds__(kThreads, 1) hals_kernel(const HalsArgs p) {
       slice_reduce(S.part, G, nel, S.bchk);
       exchange_fast(S, G, ep);
       if (cta == 0 && tid < 4) S.zpart[4 * G + tid] = zmask[tid];
-      if (cta == 0 && tid == 0) *S.halt = HaltInfo{1, it + 1, 1, jd, kEvShard, bnxt == S.bold, ep};
+      if (cta == 0 && tid == 0) { *S.halt = HaltInfo{1, it + 1, 1, jd, kEvShard, bnxt == S.bold, ep}; S.halt->last_nr = nr; }
       return;
     }
     int j0 = k;
@@ -760,6 +766,7 @@ __global__ void __launch_bounds__(kThreads, 1) hals_kernel(const HalsArgs p) {
         // pad = 1 tells the host the current B is the second buffer
         *S.halt = j0 < jd ? HaltInfo{1, it + 1, 1, j0, kEvZeroB, bnxt == S.bold, ep}
                           : HaltInfo{1, it + 1, 1, jd, kEvDeadA, bnxt == S.bold, ep};
+          S.halt->last_nr = nr;
       }
       return;
     }
@@ -781,6 +788,7 @@ __global__ void __launch_bounds__(kThreads, 1) hals_kernel(const HalsArgs p) {
   }
   if (cta == 0 && tid == 0) {
     *S.halt = HaltInfo{0, p.it_end, 0, 0, 0, bcur == S.bold, ep};
+    S.halt->last_nr = nr;
     if (prof)
       for (int i = 0; i < 21; ++i) S.prof[i] += s_prof[i];
   }

@@ -110,9 +110,15 @@ __device__ __forceinline__ void arrive_release(unsigned* bar) {
 // stored with its sign bit set on every other use of its buffer, so one
 // 64-bit store carries both the value and its freshness and the arrival
 // needs no release fence (the counter only says "everyone has written";
-// a reader that still sees last use's sign re-reads that slot).  The first
-// use of a buffer is the negative one: the zeroed slots never match it.
-__device__ __forceinline__ bool tag_neg(unsigned long long ep) { return ((ep >> 1) & 1ULL) == 0; }
+// a reader that still sees last use's sign re-reads that slot).  Buffer and
+// tag follow nr, the count of these all-reduces in the run (carried across
+// launches in HaltInfo::last_nr / HalsState::nr0), NOT the barrier epoch:
+// other grid barriers between two uses must not make a buffer's next use
+// carry its previous tag.  Use nr goes to buffer nr & 1 with the tag flipped
+// every second use, so consecutive uses of one buffer always differ; the
+// first use of each buffer is the negative one, which the zeroed slots
+// never match.
+__device__ __forceinline__ bool tag_neg(unsigned long long nr) { return ((nr >> 1) & 1ULL) == 0; }
 
 __device__ __forceinline__ void st_tagged(double* slot, double v, bool neg) {
   const double t = neg ? -v : v;
@@ -166,10 +172,12 @@ __device__ __forceinline__ void arrive_relaxed(unsigned* bar) {
 // CTA partials (lanes over CTAs in a fixed order, then a butterfly), so every
 // CTA computes the bitwise-identical total.  Lane 0 also stores 1/sqrt(total)
 // (0 when total == 0) into s_out[1] so callers normalise with one multiply.
-// Partials are double-buffered by epoch parity: a CTA can only write slot
-// (ep + 2) after every CTA arrived at ep + 1, i.e. finished reading ep.
+// Partials are double-buffered by use parity: a CTA can only write use
+// nr + 2's slot after every CTA arrived at use nr + 1, i.e. finished reading
+// use nr.
 __device__ __forceinline__ double allreduce_fused(const HalsState& S, int G, int cta,
-                                                  unsigned long long& ep, double v,
+                                                  unsigned long long& ep, unsigned long long& nr,
+                                                  double v,
                                                   double* red8, double* s_out,
                                                   long long* prof = nullptr) {
   const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
@@ -181,8 +189,8 @@ __device__ __forceinline__ double allreduce_fused(const HalsState& S, int G, int
   ++ep;
   if (wid == 0) {
     if (prof && lane == 0) t1 = clock64();
-    double* slot = S.npart + (ep & 1ULL) * G;
-    const bool neg = tag_neg(ep);
+    double* slot = S.npart + (nr & 1ULL) * G;
+    const bool neg = tag_neg(nr);
     if (lane == 0) {
       double t = 0.0;  // CTA partial: the warp partials in a fixed order
 #pragma unroll
@@ -208,6 +216,7 @@ __device__ __forceinline__ double allreduce_fused(const HalsState& S, int G, int
       }
     }
   }
+  ++nr;
   __syncthreads();
   return s_out[0];
 }

@@ -242,6 +242,7 @@ __global__ void __launch_bounds__(kThreads, 1) hals_resident_kernel(const ResArg
   };
 
   unsigned long long ep = p.epoch0;
+  unsigned long long nr = S.nr0;  // norm all-reduces so far (slot tags)
   bool have_g = false, have_w = false;
   int half = p.start_half, col0 = p.start_col, skip = p.skip_dead;
   const bool constrained = !(p.alpha == 0.0 && p.beta == 0.0);
@@ -298,12 +299,12 @@ __global__ void __launch_bounds__(kThreads, 1) hals_resident_kernel(const ResArg
             v = v > 0.0 ? v : 0.0;
           }
           RES_PROF(2);
-          const double total = allreduce_fused(S, G, cta, ep, v * v, red8, s_red, prof ? s_prof + 17 : nullptr);
+          const double total = allreduce_fused(S, G, cta, ep, nr, v * v, red8, s_red, prof ? s_prof + 17 : nullptr);
           RES_PROF(3);
           if (total == 0.0) {  // column emptied: host redraws a_j (solvers.cpp:435)
             if (live) AS[r * kp1 + j] = 0.0;
             write_back(bsc);
-            if (cta == 0 && tid == 0) *S.halt = HaltInfo{1, it + 1, 0, j, kEvZeroA, 0, ep};
+            if (cta == 0 && tid == 0) { *S.halt = HaltInfo{1, it + 1, 0, j, kEvZeroA, 0, ep}; S.halt->last_nr = nr; }
             return;
           }
           if (live) {  // solvers.cpp:436
@@ -316,7 +317,7 @@ __global__ void __launch_bounds__(kThreads, 1) hals_resident_kernel(const ResArg
       __syncthreads();
       if (jd < k) {  // dead B column: host redraws b_jd (solvers.cpp:424-428)
         write_back(bsc);
-        if (cta == 0 && tid == 0) *S.halt = HaltInfo{1, it + 1, 0, jd, kEvDeadB, 0, ep};
+        if (cta == 0 && tid == 0) { *S.halt = HaltInfo{1, it + 1, 0, jd, kEvDeadB, 0, ep}; S.halt->last_nr = nr; }
         return;
       }
       partial_rows(LM, AS, na, l, lp, k, RED, S.part + (int64_t)cta * nel);  // A-hat (438)
@@ -430,7 +431,7 @@ __global__ void __launch_bounds__(kThreads, 1) hals_resident_kernel(const ResArg
         S.bold[(int64_t)c * n + b_lo + r] = bsc[r * kp1 + c];
       }
       write_back(bsn);
-      if (cta == 0 && tid == 0) *S.halt = HaltInfo{1, it + 1, 1, jd, kEvShard, 0, ep};
+      if (cta == 0 && tid == 0) { *S.halt = HaltInfo{1, it + 1, 1, jd, kEvShard, 0, ep}; S.halt->last_nr = nr; }
       return;
     }
     int j0 = k;
@@ -442,9 +443,11 @@ __global__ void __launch_bounds__(kThreads, 1) hals_resident_kernel(const ResArg
       if (j0 < jd && tid < nbr)
         for (int c = j0 + 1; c < jd; ++c) bsn[tid * kp1 + c] = bsc[tid * kp1 + c];
       write_back(bsn);
-      if (cta == 0 && tid == 0)
+      if (cta == 0 && tid == 0) {
         *S.halt = j0 < jd ? HaltInfo{1, it + 1, 1, j0, kEvZeroB, 0, ep}
                           : HaltInfo{1, it + 1, 1, jd, kEvDeadA, 0, ep};
+        S.halt->last_nr = nr;
+      }
       return;
     }
     RES_PROF(13);
@@ -464,6 +467,7 @@ __global__ void __launch_bounds__(kThreads, 1) hals_resident_kernel(const ResArg
   write_back(bsc);
   if (cta == 0 && tid == 0) {
     *S.halt = HaltInfo{0, p.it_end, 0, 0, 0, 0, ep};
+    S.halt->last_nr = nr;
     if (prof)
       for (int i = 0; i < 21; ++i) S.prof[i] += s_prof[i];
   }

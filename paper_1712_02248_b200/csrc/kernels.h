@@ -52,6 +52,13 @@ void launch_uniform_init(const uint64_t* words, uint64_t d, uint64_t n, int k, d
 void launch_uniform_init_exact(const uint64_t* words, uint64_t nwords, uint64_t d, uint64_t n,
                                int k, double* a_cm, double* b_cm, int* flag, uint64_t* consumed,
                                cudaStream_t s);
+// reinit_column (solvers.cpp:28-31) served on the device: rows_total draws
+// uniform_positive() * 1e-3 from words[*pos ...] (the run stream), entries
+// [off, off + count) into col; advances *pos past the draws (rejections of
+// exact zeros included).  flag: scratch, 0 on entry; 2 after = out of words.
+void launch_redraw_fill(const uint64_t* words, uint64_t nwords, uint64_t* pos, uint64_t rows_total,
+                        uint64_t off, uint64_t count, double* col, int* flag, int nsm,
+                        cudaStream_t s);
 
 // ---- xstream.cu: the X-streaming contractions ----------------------------
 // Y (m x lp, ld lp) = X (m x n, ld ldx) * S (n x lp, ld lp)          ["NN"]
@@ -134,6 +141,7 @@ struct HaltInfo {
                // 5 sharded: B half done on this rank (column = first dead-A column or k)
   int pad;
   unsigned long long last_epoch;  // exchange epoch reached (next launch starts above it)
+  unsigned long long last_nr;     // norm all-reduces done so far (next launch's HalsState::nr0)
 };
 enum { kEvDeadB = 1, kEvZeroA = 2, kEvDeadA = 3, kEvZeroB = 4, kEvShard = 5 };
 
@@ -170,6 +178,8 @@ struct HalsState {
   const double* pd;
   const double* gd;
   const double* wd;
+  unsigned long long nr0;  // norm all-reduces (allreduce_fused) of earlier launches of this run:
+                           // picks the slot buffer and its freshness tag (HaltInfo::last_nr)
   int sharded;       // 1: X column-sharded across ranks: after each B half the kernel halts
                      // (kEvShard) with this rank's B-check partial in bchk, its non-zero
                      // column mask in zpart[4 grid ..], the new B in b (resident kernel:

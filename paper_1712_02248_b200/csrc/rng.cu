@@ -283,6 +283,44 @@ __global__ void uniform_init_exact_kernel(const uint64_t* __restrict__ words, ui
   *flag = 3;
 }
 
+// reinit_column (solvers.cpp:28-31) from the run stream: rows_total values
+// uniform_positive() * 1e-3 taken from words[*pos ...]; entries [off, off +
+// count) land in col.  The map kernel assumes no rejected (exact zero)
+// draw in the window and flags one; the exact kernel then redoes the window
+// sequentially with the reference's rejection, and always advances *pos.
+__global__ void redraw_map_kernel(const uint64_t* __restrict__ words, const uint64_t* __restrict__ pos,
+                                  uint64_t rows_total, uint64_t off, uint64_t count,
+                                  double* __restrict__ col, int* __restrict__ flag) {
+  const uint64_t p0 = *pos;
+  for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < rows_total;
+       i += (uint64_t)gridDim.x * blockDim.x) {
+    const double u = u53(words[p0 + i]);
+    if (u == 0.0) *flag = 1;
+    if (i >= off && i < off + count) col[i - off] = u * 1e-3;
+  }
+}
+
+__global__ void redraw_exact_kernel(const uint64_t* __restrict__ words, uint64_t nwords,
+                                    uint64_t* __restrict__ pos, uint64_t rows_total, uint64_t off,
+                                    uint64_t count, double* __restrict__ col, int* __restrict__ flag) {
+  if (threadIdx.x != 0 || blockIdx.x != 0) return;
+  uint64_t p = *pos;
+  if (*flag == 0) {
+    *pos = p + rows_total;
+    return;
+  }
+  for (uint64_t i = 0; i < rows_total; ++i) {
+    double u = 0.0;
+    while (u == 0.0) {
+      if (p >= nwords) { *flag = 2; return; }
+      u = u53(words[p++]);
+    }
+    if (i >= off && i < off + count) col[i - off] = u * 1e-3;
+  }
+  *pos = p;
+  *flag = 0;
+}
+
 }  // namespace
 
 void launch_mt_streams(const MtJobs& jobs, int njobs, cudaStream_t s) {
@@ -345,6 +383,16 @@ void launch_uniform_init_exact(const uint64_t* words, uint64_t nwords, uint64_t 
                                cudaStream_t s) {
   note_launches(1);
   uniform_init_exact_kernel<<<1, 32, 0, s>>>(words, nwords, d, n, k, a_cm, b_cm, flag, consumed);
+}
+
+void launch_redraw_fill(const uint64_t* words, uint64_t nwords, uint64_t* pos, uint64_t rows_total,
+                        uint64_t off, uint64_t count, double* col, int* flag, int nsm,
+                        cudaStream_t s) {
+  const int blocks = (int)std::min<uint64_t>((rows_total + 255) / 256, (uint64_t)nsm * 4);
+  note_launches(2);
+  redraw_map_kernel<<<blocks > 0 ? blocks : 1, 256, 0, s>>>(words, pos, rows_total, off, count,
+                                                             col, flag);
+  redraw_exact_kernel<<<1, 32, 0, s>>>(words, nwords, pos, rows_total, off, count, col, flag);
 }
 
 }  // namespace cnmf

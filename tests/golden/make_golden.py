@@ -6,7 +6,7 @@ sources (oracle/Makefile `ref` target), on inputs this repo can regenerate
 anywhere (mt19937_64 streams and the oracle's counter-based synthetic
 generator).  Run here, where /root/reference is mounted:
 
-    make -C oracle ref && python tests/golden/make_golden.py [--c2]
+    make -C oracle ref && python tests/golden/make_golden.py
 
 The GPU box has no /root/reference; tests read only these committed files.
 """
@@ -29,8 +29,7 @@ def x_summary(x):
 
 def main():
     ap = argparse.ArgumentParser()
-    ap.add_argument("--c2", action="store_true", help="also the C2 trajectory (~2 min)")
-    args = ap.parse_args()
+    ap.parse_args()
     o, r = Oracle(), Reference()
 
     # 1. variate streams (rng.hpp:17-44) and gaussian_sketch / initialize
@@ -82,16 +81,7 @@ def main():
                         a=A.astype(np.float32), b=B.astype(np.float32),
                         gini=np.array([t.gini_b]), update_seconds=np.array([t.update_seconds]))
 
-    # 4. C2 (BASELINE configs[1]) trajectory + factor summaries
-    if args.c2:
-        x2 = o.synth_x(10000, 5000, 16, 1, 1, 0.05, 1)
-        A, B, t = r.run(x2.astype(np.float64), 16, q=36, w=2, max_iterations=200,
-                        error_interval=1, rel_tolerance=1e-300, sketch_seed=1, seed=1)
-        np.savez_compressed(os.path.join(HERE, "c2.npz"), x_summary=x_summary(x2),
-                            iters=np.array(t.iterations), errors=np.array(t.errors),
-                            a_colnorm=np.linalg.norm(A, axis=0), b_colnorm=np.linalg.norm(B, axis=0),
-                            a_head=A[:64].astype(np.float32), b_head=B[:64].astype(np.float32),
-                            gini=np.array([t.gini_b]), update_seconds=np.array([t.update_seconds]))
+    # C2, C3 and C4 at full size: tests/golden/make_golden_big.py
     print("golden fixtures written to", HERE)
 
 

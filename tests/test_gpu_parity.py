@@ -402,32 +402,6 @@ def test_run_c1_trajectory_parity(ctx, oracle):
     assert res.trace.x_passes == 4 * 2 + 4
 
 
-def test_run_c2_trajectory_against_golden(ctx, oracle):
-    """BASELINE configs[1] (C2) at full size against the committed reference
-    trajectory (tests/golden/c2.npz, produced by the reference itself)."""
-    import os
-    import paper_1712_02248_b200 as cb
-    g = np.load(os.path.join(os.path.dirname(__file__), "golden", "c2.npz"))
-    x = oracle.synth_x(10000, 5000, 16, 1, 1, 0.05, 1)
-    x64 = x.astype(np.float64)
-    assert np.array_equal(np.array([x64.sum(), (x64 * x64).sum(), x64[0, 0], x64[-1, -1],
-                                    x64.max()]), g["x_summary"])
-    cfg = cb.SolverConfig(algorithm=cb.FASTHALS_RP, k=16, sketch=cb.SketchConfig(36, 2, 1),
-                          max_iterations=200, error_interval=1, rel_tolerance=1e-300, seed=1)
-    res = ctx.run(x, cfg)
-    xn = float(np.sum(x64 ** 2))
-    assert [r.iteration for r in res.trace.records] == list(g["iters"])
-    got = rel_err([r.error for r in res.trace.records], xn)
-    want = rel_err(g["errors"], xn)
-    assert np.max(np.abs(got - want) / want) < TRAJ_RTOL
-    assert np.allclose(np.linalg.norm(res.a.astype(np.float64), axis=0), g["a_colnorm"],
-                       rtol=FACTOR_RTOL)
-    assert np.allclose(np.linalg.norm(res.b.astype(np.float64), axis=0), g["b_colnorm"],
-                       rtol=FACTOR_RTOL)
-    assert rel_fro(res.a[:64], g["a_head"]) < FACTOR_RTOL
-    assert rel_fro(res.b[:64], g["b_head"]) < FACTOR_RTOL
-
-
 def test_run_penalized_cadence_parity(ctx, oracle):
     x = oracle.synth_x(400, 300, 6, 1, 1, 0.05, 3)
     res, ra, rb, rt = _run_both(ctx, oracle, x, k=6, q=12, w=1, iters=23, every=5, alpha=0.01,

@@ -6,7 +6,7 @@ sys.path.insert(0, ROOT)
 import paper_1712_02248_b200 as cb
 from oracle import Oracle
 o = Oracle()
-g = np.load(os.path.join(ROOT, "tests", "golden", "c2.npz"))
+g = np.load(os.path.join(ROOT, "tests", "golden", "c2_full.npz"))
 x = o.synth_x(10000, 5000, 16, 1, 1, 0.05, 1)
 xn = float(np.sum(x.astype(np.float64) ** 2))
 cfg = cb.SolverConfig(algorithm=cb.FASTHALS_RP, k=16, sketch=cb.SketchConfig(36, 2, 1),

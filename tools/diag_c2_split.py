@@ -8,7 +8,7 @@ sys.path.insert(0, ROOT)
 import paper_1712_02248_b200 as cb
 from oracle import Oracle
 o = Oracle(); ctx = cb.Context(0)
-g = np.load(os.path.join(ROOT, "tests", "golden", "c2.npz"))
+g = np.load(os.path.join(ROOT, "tests", "golden", "c2_full.npz"))
 d, n, k, q, w, IT = 10000, 5000, 16, 36, 2, 20
 x = o.synth_x(d, n, 16, 1, 1, 0.05, 1); x64 = x.astype(np.float64)
 xn = float(np.sum(x64 ** 2))
