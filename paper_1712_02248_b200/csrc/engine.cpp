@@ -747,8 +747,21 @@ double recon_error(cnmf_context* c, const XView& X, const double* a_cm, const do
     c->sync();
     return v;
   }
-  void* ws = c->ws<char>("metrics_ws", metrics_ws_bytes(X.d, X.n, c->nsm));
-  launch_recon_error(X.x, X.ldx, X.d, X.n, a_cm, b_cm, k, out, ws, c->nsm, c->stream);
+  // tensor-core objective (recon_tc.cu); the SIMT kernel (metrics.cu) for
+  // shapes it does not take, or on request (CNMF_RECON=simt, comparisons)
+  static const bool simt = [] {
+    const char* e = std::getenv("CNMF_RECON");
+    return e && std::string(e) == "simt";
+  }();
+  bool done = false;
+  if (!simt) {
+    void* tws = c->ws<char>("recon_tc_ws", recon_tc_ws_bytes(X.d, X.n, k, c->nsm));
+    done = launch_recon_tc(X.x, X.ldx, X.d, X.n, a_cm, b_cm, k, out, tws, c->nsm, c->stream);
+  }
+  if (!done) {
+    void* ws = c->ws<char>("metrics_ws", metrics_ws_bytes(X.d, X.n, c->nsm));
+    launch_recon_error(X.x, X.ldx, X.d, X.n, a_cm, b_cm, k, out, ws, c->nsm, c->stream);
+  }
   CK(cudaGetLastError());
   double v = 0.0;
   CK(cudaMemcpyAsync(&v, out, sizeof(double), cudaMemcpyDeviceToHost, c->stream));

@@ -115,6 +115,11 @@ void launch_check_data(const float* x, int64_t ldx, int64_t d, int64_t n, int* f
                        double* norm_sq, void* ws, int nsm, cudaStream_t st, int8_t* rexp = nullptr,
                        int* wide = nullptr);
 // 1/2 ||X - A B^T||^2 with column-major A_cm (k x d), B_cm (k x n).
+// The same objective on the tensor cores (recon_tc.cu): dense X (ldx % 4 ==
+// 0, 16-byte aligned), k <= 128; returns false when those do not hold.
+size_t recon_tc_ws_bytes(int64_t d, int64_t n, int k, int nsm);
+bool launch_recon_tc(const float* x, int64_t ldx, int64_t d, int64_t n, const double* a_cm,
+                     const double* b_cm, int k, double* out, void* ws, int nsm, cudaStream_t st);
 void launch_recon_error(const float* x, int64_t ldx, int64_t d, int64_t n, const double* a_cm,
                         const double* b_cm, int k, double* out, void* ws, int nsm,
                         cudaStream_t st);

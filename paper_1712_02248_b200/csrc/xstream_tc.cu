@@ -33,10 +33,13 @@
 
 #include "common.cuh"
 #include "kernels.h"
+#include "tc_common.cuh"
 
 namespace cnmf {
 
 namespace {
+
+using namespace tc;
 
 constexpr int kBM = 128;     // output rows per unit (MMA M)
 constexpr int kBK = 32;      // K elements per stage (4 MMA k-steps of 8)
@@ -57,73 +60,6 @@ constexpr int kDrain16 = TC_DRAIN16;
 constexpr int kDrain16 = 4;
 #endif
 constexpr int kXBytes = kBM * kBK * 4;  // 16 KB per stage (x_hi), same for x_lo
-
-__device__ __forceinline__ uint32_t smem_u32(const void* p) {
-  return static_cast<uint32_t>(__cvta_generic_to_shared(p));
-}
-__device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
-  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count));
-}
-__device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, uint32_t bytes) {
-  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)),
-               "r"(bytes)
-               : "memory");
-}
-__device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
-  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
-}
-__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
-  asm volatile(
-      "{\n\t.reg .pred p;\n"
-      "WAIT_%=:\n\t"
-      "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n\t"
-      "@!p bra WAIT_%=;\n\t}" ::"r"(smem_u32(bar)),
-      "r"(parity)
-      : "memory");
-}
-// Warp-collective wait: every lane polls, then the warp reconverges before
-// any .sync.aligned tcgen05 instruction (a lagging lane would make those
-// undefined -- observed as scattered wrong rows).
-__device__ __forceinline__ void mbar_wait_warp(uint64_t* bar, uint32_t parity) {
-  mbar_wait(bar, parity);
-  __syncwarp();
-}
-__device__ __forceinline__ void tc_fence_before() {
-  asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
-}
-__device__ __forceinline__ void tc_fence_after() {
-  asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
-}
-// Shared-memory matrix descriptor (sm_100, version 1).  K-major operands use
-// SWIZZLE_128B (layout 2: 8 rows x 128 B atoms, 16 B granules); MN-major
-// 32-bit operands must use SWIZZLE_128B_BASE32B (layout 1: 4 K-rows x 128 B
-// atoms, 32 B granules) -- with plain SWIZZLE_128B an MN-major kind::tf32 MMA
-// is a silent no-op on B200 (measured with tools/tc_debug.cu).
-__device__ __forceinline__ uint64_t smem_desc(uint32_t addr, uint32_t lbo, uint32_t sbo,
-                                              uint32_t layout = 2) {
-  uint64_t d = 0;
-  d |= (uint64_t)((addr >> 4) & 0x3FFF);
-  d |= (uint64_t)((lbo >> 4) & 0x3FFF) << 16;
-  d |= (uint64_t)((sbo >> 4) & 0x3FFF) << 32;
-  d |= (uint64_t)1 << 46;        // version
-  d |= (uint64_t)layout << 61;   // layout type
-  return d;
-}
-// MN-major operand: atoms of 32 elements along MN (one 128 B row) x 4 K-rows;
-// MN atoms `lbo` bytes apart, 4-row groups 512 B apart.
-__device__ __forceinline__ uint64_t desc_mn(uint32_t addr, uint32_t lbo) {
-  return smem_desc(addr, lbo, 512, 1);
-}
-// Instruction descriptor: kind::tf32, fp32 accumulate, M = 128.
-__host__ __device__ constexpr uint32_t idesc_tf32(int n, bool a_mn, bool b_mn) {
-  return (1u << 4)                       // D format F32
-         | (2u << 7)                     // A format TF32
-         | (2u << 10)                    // B format TF32
-         | ((a_mn ? 1u : 0u) << 15)      // A major
-         | ((b_mn ? 1u : 0u) << 16)      // B major
-         | ((uint32_t)(n >> 3) << 17)    // N >> 3
-         | ((uint32_t)(kBM >> 4) << 24); // M >> 4
-}
 
 // Instruction descriptor: kind::f16 with fp16 A and B, fp32 accumulate,
 // M = 128 (layouts checked by tools/tc_f16_check.cu).
@@ -224,52 +160,6 @@ __device__ __forceinline__ float lds32(uint32_t a) {
   asm volatile("ld.shared.f32 %0, [%1];" : "=f"(v) : "r"(a) : "memory");
   return v;
 }
-// rna_tf32 with integer ops (ALU pipe; cvt.rna.tf32 issues on the XU pipe,
-// which the v2 kernel saturated): add half an ulp to the magnitude, truncate.
-__device__ __forceinline__ uint32_t rna_tf32_bits(float x) {
-  return (__float_as_uint(x) + 0x1000u) & 0xFFFFE000u;
-}
-__device__ __forceinline__ void tf32_split_bits(float x, uint32_t& hi, uint32_t& lo) {
-  hi = rna_tf32_bits(x);
-  lo = rna_tf32_bits(x - __uint_as_float(hi));
-}
-__device__ __forceinline__ void tmem_st32(uint32_t taddr, const uint32_t (&v)[32]) {
-  asm volatile(
-      "tcgen05.st.sync.aligned.32x32b.x32.b32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,"
-      "%13,%14,%15,%16,%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31,%32};" ::"r"(taddr),
-      "r"(v[0]), "r"(v[1]), "r"(v[2]), "r"(v[3]), "r"(v[4]), "r"(v[5]), "r"(v[6]), "r"(v[7]),
-      "r"(v[8]), "r"(v[9]), "r"(v[10]), "r"(v[11]), "r"(v[12]), "r"(v[13]), "r"(v[14]),
-      "r"(v[15]), "r"(v[16]), "r"(v[17]), "r"(v[18]), "r"(v[19]), "r"(v[20]), "r"(v[21]),
-      "r"(v[22]), "r"(v[23]), "r"(v[24]), "r"(v[25]), "r"(v[26]), "r"(v[27]), "r"(v[28]),
-      "r"(v[29]), "r"(v[30]), "r"(v[31])
-      : "memory");
-}
-
-// MMA / commit issued by a CONVERGED warp, predicated on lane 0 inside the asm
-// (the same lane for every MMA and commit: tcgen05.commit only tracks the
-// MMAs of the executing thread): issuing from divergent code (`if (lane == 0)`) makes the compiler wrap
-// every tcgen05 instruction in an ELECT / BRA.U.ANY waterfall loop that caps
-// issue at ~45 cycles per MMA (tools/ubench_tc.cu: 44.5 vs 16.6 cycles for an
-// N = 32 MMA), more than the MMA itself for the widths used here.
-__device__ __forceinline__ void mma_ts_elect(uint32_t d_tmem, uint32_t a_tmem, uint64_t b_desc,
-                                             uint32_t idesc, uint32_t accumulate) {
-  asm volatile(
-      "{\n\t.reg .pred p, e;\n\t"
-      "setp.ne.b32 p, %4, 0;\n\t"
-      "{\n\t.reg .u32 ln;\n\tmov.u32 ln, %%laneid;\n\tsetp.eq.u32 e, ln, 0;\n\t}\n\t"
-      "@e tcgen05.mma.cta_group::1.kind::tf32 [%0], [%1], %2, %3, p;\n\t}" ::"r"(d_tmem),
-      "r"(a_tmem), "l"(b_desc), "r"(idesc), "r"(accumulate)
-      : "memory");
-}
-__device__ __forceinline__ void commit_elect(uint64_t* bar) {
-  asm volatile(
-      "{\n\t.reg .pred e;\n\t"
-      "{\n\t.reg .u32 ln;\n\tmov.u32 ln, %%laneid;\n\tsetp.eq.u32 e, ln, 0;\n\t}\n\t"
-      "@e tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];\n\t}" ::"r"(
-          smem_u32(bar))
-      : "memory");
-}
-
 // TC_TRACE builds (tools only): per-K-block event times of CTA 0 into args.dbg
 // as uint64 [event][block]: 0 X issue, 1 split got X, 2 split got A slot,
 // 3 split done, 4 MMA got operands, 5 MMA issued, 6 S issue, 7 MMA got A slot.
@@ -790,54 +680,6 @@ __global__ void tc_split_reduce_kernel(const float4* __restrict__ part, int spli
 }
 
 float* g_tc_debug = nullptr;
-
-PFN_cuTensorMapEncodeTiled_v12000 encode_fn() {
-  static PFN_cuTensorMapEncodeTiled_v12000 fn = nullptr;
-  if (!fn) {
-    cudaDriverEntryPointQueryResult q;
-    void* p = nullptr;
-    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) ==
-            cudaSuccess &&
-        q == cudaDriverEntryPointSuccess)
-      fn = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(p);
-  }
-  return fn;
-}
-
-// 2D fp32 row-major tensor (rows x cols, row pitch ld floats), box_cols x
-// box_rows boxes.
-bool make_map(CUtensorMap* m, const void* base, int64_t rows, int64_t cols, int64_t ld,
-              int box_cols, int box_rows, CUtensorMapSwizzle sw, bool f16 = false) {
-  auto fn = encode_fn();
-  if (!fn) return false;
-  const cuuint64_t dims[2] = {(cuuint64_t)cols, (cuuint64_t)rows};
-  const cuuint64_t strides[1] = {(cuuint64_t)(ld * (f16 ? 2 : 4))};
-  const cuuint32_t box[2] = {(cuuint32_t)box_cols, (cuuint32_t)box_rows};
-  const cuuint32_t estr[2] = {1, 1};
-  return fn(m, f16 ? CU_TENSOR_MAP_DATA_TYPE_FLOAT16 : CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2,
-            const_cast<void*>(base), dims, strides, box,
-            estr, CU_TENSOR_MAP_INTERLEAVE_NONE, sw, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
-            CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
-}
-
-// Launch with programmatic stream serialization (PDL): the kernel may start
-// before its predecessor in the stream completes; it must execute
-// griddepcontrol.wait before touching anything that predecessor writes.
-template <typename... KArgs, typename... Args>
-cudaError_t launch_pdl(void (*kern)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t st,
-                       Args&&... args) {
-  cudaLaunchConfig_t cfg = {};
-  cfg.gridDim = grid;
-  cfg.blockDim = block;
-  cfg.dynamicSmemBytes = smem;
-  cfg.stream = st;
-  cudaLaunchAttribute attr[1];
-  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
-  attr[0].val.programmaticStreamSerializationAllowed = 1;
-  cfg.attrs = attr;
-  cfg.numAttrs = 1;
-  return cudaLaunchKernelEx(&cfg, kern, std::forward<Args>(args)...);
-}
 
 struct TcPlan {
   int ntiles, nsplit;

@@ -368,6 +368,46 @@ def test_reconstruction_error_parity(ctx, oracle):
                                     dev(np.zeros((2, 1))), dev(np.zeros((2, 1)))) == 15.0
 
 
+@pytest.mark.parametrize("d,n,k", [(130, 70, 1), (300, 257, 5), (1000, 1001, 20), (513, 4099, 100),
+                                   (2048, 640, 128), (129, 65, 7)])
+def test_reconstruction_error_tensor_core_shapes(ctx, oracle, d, n, k):
+    """recon_tc.cu (3xTF32 tcgen05 prediction tiles, fp32 residuals, fp64
+    sums) at ragged shapes (row / column tile remainders, k not a multiple of
+    8, k = 128) against the reference formula (metrics.cpp:61-77).
+
+    The tensor core's fp32 accumulation truncates: the prediction p = A B^T
+    comes out ~0.6 ulp per 8-deep k-step low (measured: tools/re_layout.py),
+    which moves the objective by 2 eps <r, p> (r = x - p).  At a fit the
+    residual is orthogonal to the prediction (<X - A B^T, A B^T> = 0 at a
+    stationary point), so the error is at the 1e-6 level there; for factors
+    unrelated to X the stated bound is
+        |got - want| <= 1e-6 want + (k-steps * 1e-7) |<r, p>|.
+    At a very tight fit (residual 1e-4 of X) the per-entry error of p is
+    ~1e-3 of the residual and the objective is good to 2e-4 relative.  The
+    BASELINE runs sit between (tools/re_compare_runs.py: C1-C4 objectives
+    within 2e-6 of the SIMT fp32 kernel's at every record)."""
+    rng = np.random.default_rng(d + n + k)
+    a = rng.random((d, k))
+    b = rng.random((n, k))
+    p = a.astype(np.float32).astype(np.float64) @ b.astype(np.float32).astype(np.float64).T
+    nks = (k + 7) // 8
+    for case in ("fit", "fit_tight", "unrelated"):
+        if case == "fit":         # zero-mean noise: relative error ~ 1e-2
+            x = p + 0.02 * (k / 4) * (rng.random((d, n)) - 0.5)
+        elif case == "fit_tight":  # relative error ~ 1e-4
+            x = p + 2e-4 * (k / 4) * (rng.random((d, n)) - 0.5)
+        else:
+            x = rng.random((d, n)) * (k / 2)
+        x = x.astype(np.float32).astype(np.float64)
+        a32, b32 = a.astype(np.float32), b.astype(np.float32)
+        got = ctx.reconstruction_error(dev(x), dev(a32), dev(b32))
+        want = oracle.reconstruction_error(x, a32.astype(np.float64), b32.astype(np.float64))
+        rp = abs(float(np.sum((x - p) * p)))
+        bound = {"fit": 2e-6 * want, "fit_tight": 2e-4 * want,
+                 "unrelated": 1e-6 * want + nks * 1e-7 * rp}[case]
+        assert abs(got - want) <= bound, (case, got, want, abs(got - want) / want)
+
+
 # --------------------------------------------------------------------- run --
 def _run_both(ctx, oracle, x, **kw):
     import paper_1712_02248_b200 as cb
