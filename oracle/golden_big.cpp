@@ -184,10 +184,32 @@ int main(int argc, char** argv) {
   f.b = DenseMatrix(n, k);
   for (double& v : f.b.values) v = rng.uniform_positive();
   t = clk::now();
-  const ProjectorPair p = build_projectors(x, cfg.sketch);
+  ProjectorPair p = build_projectors(x, cfg.sketch);
   meta("build_projectors_seconds", secs(t));
-  const DenseMatrix xhat = compress_left(x, p);
-  const DenseMatrix xcheck = compress_right(x, p);
+  DenseMatrix xhat = compress_left(x, p);
+  DenseMatrix xcheck = compress_right(x, p);
+  // Sensitivity experiments only (tools/c3_sensitivity.sh; never set for the
+  // committed goldens): GOLDEN_VIEWS_F32=1 rounds the projectors and the
+  // compressed views to fp32 (the device path's storage precision);
+  // GOLDEN_VIEWS_PERTURB=eps multiplies every entry by (1 + eps u), u uniform
+  // in [-1, 1) from a fixed LCG (a stand-in for contraction rounding).
+  if (std::getenv("GOLDEN_VIEWS_F32") || std::getenv("GOLDEN_VIEWS_PERTURB")) {
+    ProjectorPair& pm = p;
+    const double eps = std::getenv("GOLDEN_VIEWS_PERTURB")
+                           ? std::strtod(std::getenv("GOLDEN_VIEWS_PERTURB"), nullptr)
+                           : 0.0;
+    std::uint64_t st = 0x9E3779B97F4A7C15ull;
+    for (DenseMatrix* m : {&pm.left, &pm.right, &xhat, &xcheck})
+      for (double& v : m->values) {
+        if (eps != 0.0) {
+          st = st * 6364136223846793005ull + 1442695040888963407ull;
+          const double u = static_cast<double>(st >> 11) * 0x1.0p-53 * 2.0 - 1.0;
+          v *= 1.0 + eps * u;
+        }
+        if (std::getenv("GOLDEN_VIEWS_F32")) v = static_cast<double>(static_cast<float>(v));
+      }
+    meta("views_perturbed", eps);
+  }
   DenseMatrix a_hat = compress_factor_a(f.a, p);
   DenseMatrix b_check = compress_factor_b(f.b, p);
   meta("compress_seconds", secs(t));

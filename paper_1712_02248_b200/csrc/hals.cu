@@ -365,6 +365,150 @@ __device__ __forceinline__ void load8(const double* p, double (&v)[8]) {
   }
 }
 
+// ---- B sweep on the FP64 tensor cores ------------------------------------
+// The B half's column updates are row-local (solvers.cpp:444-451, the B update
+// forms 480-509): every row of B runs its own k-step Gauss-Seidel chain
+// against w.  Each warp takes 16-row strips of the CTA's rows in turn, stages
+// the strip's k columns in shared memory (column-major, stride kBsStr), and
+// sweeps it in 16-column blocks:
+//   * block product acc = B_strip w[:, block] as m8n8k4 DMMAs (two 8-row x
+//     two 8-column tiles, chain over all k columns with the current values:
+//     columns before the block already updated, the block's own still old);
+//   * in-block chain: lane (g, t4) of the accumulator layout holds row g's
+//     columns {2t4, 2t4+1, 8+2t4, 9+2t4}, so column t of the block is owned
+//     by lane t4 = (t % 8) / 2 of each 4-lane row group; the owner's new value
+//     and delta are broadcast in the group (shuffle), and every lane folds the
+//     delta into its later columns' accumulators (acc_u += delta w_ju).
+// w sits in shared memory (row stride kgs = 16-padded k + 4: conflict-free
+// fragments), the strip rows are read once from L2/HBM and written once.
+// The SIMT sweep it replaces re-read every B row from L2 once per 16-column
+// block and ran ~18% of the DFMA peak (profiles/r01_hals_c3_summary.md).
+constexpr int kBsRows = 16;  // rows per warp strip
+constexpr int kBsStr = 20;   // strip column stride (doubles, == 4 mod 16)
+__host__ __device__ constexpr int bs_kgs(int k) { return ((k + 15) & ~15) + 4; }
+__host__ __device__ constexpr int64_t bs_smem_doubles(int k) {
+  return (int64_t)((k + 3) & ~3) * bs_kgs(k) + (int64_t)(kThreads / 32) * ((k + 3) & ~3) * kBsStr;
+}
+// Static shared memory of hals_kernel is ~2.4 KB; the DMMA sweep is used
+// when its dynamic share fits next to it (k <= 100).
+__host__ __device__ constexpr bool bs_dmma_fits(int k) {
+  return bs_smem_doubles(k) * 8 + 4096 <= 227 * 1024;
+}
+
+template <bool kConstrained>
+__device__ __noinline__ void b_sweep_dmma(const HalsState& S, const double* __restrict__ ws,
+                                          const double* __restrict__ s_diag,
+                                          const double* __restrict__ s_winv, double* strips,
+                                          const double* __restrict__ bcur, double* __restrict__ bnxt,
+                                          int64_t b_lo, int nbr, int col0, int jd, double alpha,
+                                          unsigned* zmask) {
+  const int k = S.k, k4 = (k + 3) & ~3, kgs = bs_kgs(k);
+  const int64_t n = S.n;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int g = lane >> 2, t4 = lane & 3, grp = lane & ~3;
+  double* bs = strips + (int64_t)warp * k4 * kBsStr;
+  const int nstrip = (nbr + kBsRows - 1) / kBsRows;
+  for (int si = warp; si < nstrip; si += kThreads / 32) {
+    const int r0 = si * kBsRows, nr = min(kBsRows, nbr - r0);
+    const int64_t rbase = b_lo + r0;
+    __syncwarp();  // the previous strip's write-back reads are done
+    // Columns < col0 were updated by an earlier launch and carried into bcur
+    // by the caller's resume convention; the rest are the old B.
+    for (int e = lane; e < k4 * kBsRows; e += 32) {
+      const int c = e >> 4, rr = e & 15;
+      double* dst = bs + c * kBsStr + rr;
+      if (c < k && rr < nr) cp_async8(dst, bcur + (int64_t)c * n + rbase + rr);
+      else *dst = 0.0;
+    }
+    cp_async_commit();
+    cp_async_wait_all();
+    __syncwarp();
+    unsigned zm0 = 0u, zm1 = 0u, zm2 = 0u, zm3 = 0u;  // lane 0: non-zero columns
+    for (int jb = col0 & ~15; jb < jd; jb += 16) {
+      const int t0 = max(col0 - jb, 0), nbj = min(16, jd - jb);
+      if (t0 >= nbj) continue;
+      // p of this lane's accumulator entries (issued before the chain)
+      double pv[2][2][2];
+#pragma unroll
+      for (int i = 0; i < 2; ++i)
+#pragma unroll
+        for (int h = 0; h < 2; ++h)
+#pragma unroll
+          for (int e = 0; e < 2; ++e) {
+            const int c = jb + 8 * h + 2 * t4 + e, r = 8 * i + g;
+            pv[i][h][e] = (c < k && r < nr) ? __ldcg(S.p + (int64_t)c * n + rbase + r) : 0.0;
+          }
+      double acc[2][2][2];
+#pragma unroll
+      for (int i = 0; i < 2; ++i)
+#pragma unroll
+        for (int h = 0; h < 2; ++h) acc[i][h][0] = acc[i][h][1] = 0.0;
+      const double* ap = bs + t4 * kBsStr + g;  // A[g][t] = B[8i + g][c + t]
+      const double* wp = ws + t4 * kgs + jb + g;  // B[t][g] = w[c + t][jb + 8h + g]
+#pragma unroll 5
+      for (int c = 0; c < k4; c += 4) {
+        const double a0 = ap[c * kBsStr], a1 = ap[c * kBsStr + 8];
+        const double w0 = wp[c * kgs], w1 = wp[c * kgs + 8];
+        dmma(acc[0][0][0], acc[0][0][1], a0, w0);
+        dmma(acc[0][1][0], acc[0][1][1], a0, w1);
+        dmma(acc[1][0][0], acc[1][0][1], a1, w0);
+        dmma(acc[1][1][0], acc[1][1][1], a1, w1);
+      }
+#pragma unroll
+      for (int t = 0; t < 16; ++t) {
+        if (t < t0) continue;
+        if (t >= nbj) break;
+        const int j = jb + t, hh = t >> 3, ee = t & 1, ow = grp | ((t & 7) >> 1);
+        const bool owner = t4 == ((t & 7) >> 1);
+        const double wjj = s_diag[j], winv = s_winv[j];
+        const double2 wr0 = *reinterpret_cast<const double2*>(ws + j * kgs + jb + 2 * t4);
+        const double2 wr1 = *reinterpret_cast<const double2*>(ws + j * kgs + jb + 8 + 2 * t4);
+        const double wv[2][2] = {{(2 * t4 > t) ? wr0.x : 0.0, (2 * t4 + 1 > t) ? wr0.y : 0.0},
+                                 {(8 + 2 * t4 > t) ? wr1.x : 0.0, (9 + 2 * t4 > t) ? wr1.y : 0.0}};
+        bool nz = false;
+#pragma unroll
+        for (int i = 0; i < 2; ++i) {
+          const int r = 8 * i + g;
+          const double bo = bs[j * kBsStr + r];
+          const double sv = acc[i][hh][ee], pp = pv[i][hh][ee];
+          // solvers.cpp:480-490 (unconstrained) / 502-508 (constrained); the
+          // division is a multiplication by the precomputed reciprocal
+          const double v = kConstrained ? (bo * wjj + pp - sv - alpha) * winv : bo + (pp - sv) * winv;
+          const double vf = v > 0.0 ? v : 0.0;
+          const double dl = __shfl_sync(0xffffffffu, vf - bo, ow);
+          if (owner && r < nr) {
+            bs[j * kBsStr + r] = vf;
+            nz |= vf != 0.0;
+          }
+#pragma unroll
+          for (int h = 0; h < 2; ++h)
+#pragma unroll
+            for (int e = 0; e < 2; ++e) acc[i][h][e] = fma(dl, wv[h][e], acc[i][h][e]);
+        }
+        if (__any_sync(0xffffffffu, nz)) {
+          const unsigned bit = 1u << (j & 31);
+          const int wq = j >> 5;
+          zm0 |= wq == 0 ? bit : 0u;
+          zm1 |= wq == 1 ? bit : 0u;
+          zm2 |= wq == 2 ? bit : 0u;
+          zm3 |= wq == 3 ? bit : 0u;
+        }
+      }
+    }
+    if (lane == 0) {
+      if (zm0) atomicOr(&zmask[0], zm0);
+      if (zm1) atomicOr(&zmask[1], zm1);
+      if (zm2) atomicOr(&zmask[2], zm2);
+      if (zm3) atomicOr(&zmask[3], zm3);
+    }
+    __syncwarp();
+    for (int e = lane; e < k * kBsRows; e += 32) {
+      const int c = e >> 4, rr = e & 15;
+      if (rr < nr) bnxt[(int64_t)c * n + rbase + rr] = bs[c * kBsStr + rr];
+    }
+  }
+}
+
 // RPT: A rows per thread; NB: columns per sweep block (16 halves the sweeps'
 // re-reads of A and B -- one pass over all k columns per block -- where the
 // registers allow it; the 6-row instance keeps 8).
@@ -612,6 +756,25 @@ __global__ void __launch_bounds__(kThreads, 1) hals_kernel(const HalsArgs p) {
       for (int r = tid; r < nbr; r += kThreads)
         bnxt[(int64_t)c * n + b_lo + r] = bcur[(int64_t)c * n + b_lo + r];
     const bool constrained = !(p.alpha == 0.0 && p.beta == 0.0);
+    if (!S.dense && bs_dmma_fits(k)) {
+      // w in the DMMA sweep's layout (row stride kgs, rows/columns zero-padded)
+      const int k4 = (k + 3) & ~3, kgs = bs_kgs(k);
+      double* ws = smem;
+      __syncthreads();  // everyone is done with the product stage / gw copy
+      for (int e = tid; e < k4 * kgs; e += kThreads) {
+        const int r = e / kgs, c = e - r * kgs;
+        ws[e] = (r < k && c < k) ? wsc[r * k + c] : 0.0;
+      }
+      for (int e = tid; e < k; e += kThreads)
+        s_ginv[e] = constrained ? 1.0 / (wsc[e * k + e] + p.beta) : 1.0 / wsc[e * k + e];
+      __syncthreads();
+      if (constrained)
+        b_sweep_dmma<true>(S, ws, s_diag, s_ginv, smem + (int64_t)k4 * kgs, bcur, bnxt, b_lo, nbr,
+                           col0, jd, p.alpha, zmask);
+      else
+        b_sweep_dmma<false>(S, ws, s_diag, s_ginv, smem + (int64_t)k4 * kgs, bcur, bnxt, b_lo, nbr,
+                            col0, jd, 0.0, zmask);
+    } else {
     // Rows are independent: kRB rows per thread per pass (rows rb0 + tid +
     // 256 i), 8-aligned column blocks as in the A half, deltas folded into
     // the block's later accumulators, zero-column flags by warp ballot.
@@ -717,6 +880,7 @@ __global__ void __launch_bounds__(kThreads, 1) hals_kernel(const HalsArgs p) {
     };
     if (nbr <= kThreads) b_sweep(std::integral_constant<int, 1>{});
     else b_sweep(std::integral_constant<int, kRB>{});
+    }
     __syncthreads();
     HALS_PROF(10);
     if (tid < 4) S.zpart[cta * 4 + tid] = zmask[tid];
@@ -803,7 +967,9 @@ size_t hals_smem_bytes(const HalsState& st, int /*rows_a*/) {
   const int64_t sweep = k * ((k + 15) & ~15);
   const int64_t part = (kRing * partial_stage_bytes((int)lp, (int)k) + 7) / 8;  // cp.async ring
   const int64_t gram = ((l + 3) & ~3) * ((k + 7) & ~7);
-  return (size_t)std::max(std::max(prod, sweep), std::max(part, gram)) * sizeof(double);
+  const int64_t bsw = (!st.dense && bs_dmma_fits((int)k)) ? bs_smem_doubles((int)k) : 0;
+  return (size_t)std::max(std::max(std::max(prod, sweep), std::max(part, gram)), bsw) *
+         sizeof(double);
 }
 
 // Column-wise compress_factor_a / compress_factor_b (compression.cpp:90-96):
