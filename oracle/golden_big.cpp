@@ -36,6 +36,7 @@
 
 #include "cnmf/compression.hpp"
 #include "cnmf/metrics.hpp"
+#include "cnmf/qr.hpp"
 #include "cnmf/rng.hpp"
 #include "cnmf/solvers.hpp"
 
@@ -83,6 +84,70 @@ double par_error(const DenseMatrix& x, const FactorPair& f) {
   double s = 0.0;
   for (double p : part) s += p;
   return s;
+}
+
+
+// ---- sensitivity experiments (tools/c3_sensitivity.sh; never used for the
+// committed goldens).  GOLDEN_RF_PERTURB=eps rebuilds the projectors with
+// the reference's own gaussian_sketch and thin_qr but multithreaded fp64
+// contractions, and multiplies every range-finder product (the sketch and each
+// power-iteration product, before its thin_qr) by (1 + eps u), u uniform in
+// [-1, 1): a stand-in for the device contraction's rounding.  The compressed
+// views are then formed exactly (fp64).
+std::uint64_t g_lcg = 0x9E3779B97F4A7C15ull;
+void perturb(DenseMatrix& m, double eps) {
+  if (eps == 0.0) return;
+  for (double& v : m.values) {
+    g_lcg = g_lcg * 6364136223846793005ull + 1442695040888963407ull;
+    v *= 1.0 + eps * (static_cast<double>(g_lcg >> 11) * 0x1.0p-53 * 2.0 - 1.0);
+  }
+}
+// x (d x n) * s (n x l), rows in parallel
+DenseMatrix par_xs(const DenseMatrix& x, const DenseMatrix& s) {
+  DenseMatrix y(x.rows, s.cols);
+  parallel_blocks(x.rows, 64, [&](std::size_t, std::size_t r0, std::size_t r1) {
+    for (std::size_t i = r0; i < r1; ++i)
+      for (std::size_t j = 0; j < x.cols; ++j) {
+        const double xv = x(i, j);
+        const double* sr = s.row(j);
+        double* yr = y.row(i);
+        for (std::size_t c = 0; c < s.cols; ++c) yr[c] += xv * sr[c];
+      }
+  });
+  return y;
+}
+// x^T (n x d) * t (d x l), output rows (columns of x) in parallel
+DenseMatrix par_xts(const DenseMatrix& x, const DenseMatrix& t) {
+  DenseMatrix z(x.cols, t.cols);
+  parallel_blocks(x.cols, 256, [&](std::size_t, std::size_t c0, std::size_t c1) {
+    for (std::size_t i = 0; i < x.rows; ++i) {
+      const double* xr = x.row(i);
+      const double* tr = t.row(i);
+      for (std::size_t j = c0; j < c1; ++j) {
+        double* zr = z.row(j);
+        const double xv = xr[j];
+        for (std::size_t c = 0; c < t.cols; ++c) zr[c] += xv * tr[c];
+      }
+    }
+  });
+  return z;
+}
+DenseMatrix rf_perturbed(const DenseMatrix& x, bool tr, std::size_t q, std::size_t w,
+                         std::uint64_t seed, double eps) {
+  const std::size_t op_cols = tr ? x.rows : x.cols;
+  DenseMatrix omega = gaussian_sketch(op_cols, q, seed);
+  DenseMatrix y = tr ? par_xts(x, omega) : par_xs(x, omega);
+  perturb(y, eps);
+  DenseMatrix basis = thin_qr(y).q;
+  for (std::size_t it = 0; it < w; ++it) {
+    DenseMatrix z0 = tr ? par_xs(x, basis) : par_xts(x, basis);
+    perturb(z0, eps);
+    DenseMatrix z = thin_qr(z0).q;
+    DenseMatrix b0 = tr ? par_xts(x, z) : par_xs(x, z);
+    perturb(b0, eps);
+    basis = thin_qr(b0).q;
+  }
+  return basis;
 }
 
 void put(const std::string& dir, const std::string& name, const void* p, std::size_t bytes) {
@@ -184,10 +249,19 @@ int main(int argc, char** argv) {
   f.b = DenseMatrix(n, k);
   for (double& v : f.b.values) v = rng.uniform_positive();
   t = clk::now();
-  ProjectorPair p = build_projectors(x, cfg.sketch);
+  const char* rfp = std::getenv("GOLDEN_RF_PERTURB");
+  ProjectorPair p;
+  if (rfp) {
+    const double eps = std::strtod(rfp, nullptr);
+    p.left = rf_perturbed(x, false, q, w, seed * 2, eps);
+    p.right = transpose(rf_perturbed(x, true, q, w, seed * 2 + 1, eps));
+    meta("rf_perturbed", eps);
+  } else {
+    p = build_projectors(x, cfg.sketch);
+  }
   meta("build_projectors_seconds", secs(t));
-  DenseMatrix xhat = compress_left(x, p);
-  DenseMatrix xcheck = compress_right(x, p);
+  DenseMatrix xhat = rfp ? transpose(par_xts(x, p.left)) : compress_left(x, p);
+  DenseMatrix xcheck = rfp ? par_xs(x, transpose(p.right)) : compress_right(x, p);
   // Sensitivity experiments only (tools/c3_sensitivity.sh; never set for the
   // committed goldens): GOLDEN_VIEWS_F32=1 rounds the projectors and the
   // compressed views to fp32 (the device path's storage precision);

@@ -6,7 +6,22 @@
 
 #include <cuda/atomic>
 
+#include <atomic>
+
 namespace cnmf {
+
+// cudaFuncSetAttribute(MaxDynamicSharedMemorySize) is a per-device setting:
+// each call site keeps one bit per device in `done` (a second context on
+// another device of the same process sets it there too).
+inline void smem_attr_once(std::atomic<unsigned>& done, const void* fn, int bytes) {
+  int dev = 0;
+  cudaGetDevice(&dev);
+  const unsigned bit = 1u << (dev & 31);
+  if (!(done.load(std::memory_order_acquire) & bit)) {
+    cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes);
+    done.fetch_or(bit, std::memory_order_acq_rel);
+  }
+}
 
 constexpr int kWarp = 32;
 

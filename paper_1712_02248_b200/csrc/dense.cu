@@ -360,12 +360,8 @@ void xs64_launch(const float* x, int64_t ldx, int64_t m, int64_t n, const double
   int64_t splits = xs64_splits(tiles, K, nsm);
   const int64_t kchunk = ((K + splits - 1) / splits + kBK - 1) / kBK * kBK;
   splits = (K + kchunk - 1) / kchunk;
-  static bool attr = false;
-  if (!attr) {
-    cudaFuncSetAttribute(xs64_kernel<kTN, LP>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                         (int)Sh::smem);
-    attr = true;
-  }
+  static std::atomic<unsigned> attr{0u};
+  smem_attr_once(attr, (const void*)(xs64_kernel<kTN, LP>), (int)Sh::smem);
   double* dst = splits > 1 ? ws : out;
   note_launches(1);
   xs64_kernel<kTN, LP><<<dim3((unsigned)tiles, (unsigned)splits), kXT, Sh::smem, st>>>(
@@ -455,12 +451,8 @@ void launch_cm_to_rm_pad64(const double* f_cm, int64_t rows, int k, int lp, doub
 
 void launch_mu_update(const double* t_in, int64_t rows, int k, const double* num, int ldn,
                       const double* g, int semi, double* t_out, int nsm, cudaStream_t st) {
-  static bool attr = false;
-  if (!attr) {
-    cudaFuncSetAttribute(mu_update_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                         (int)(sizeof(double) * 128 * 128));
-    attr = true;
-  }
+  static std::atomic<unsigned> attr{0u};
+  smem_attr_once(attr, (const void*)(mu_update_kernel), (int)(sizeof(double) * 128 * 128));
   note_launches(1);
   mu_update_kernel<<<(unsigned)std::min<int64_t>((rows + 127) / 128, 8 * nsm), 128,
                      sizeof(double) * k * k, st>>>(t_in, rows, k, num, ldn, g, semi, t_out);
@@ -469,12 +461,8 @@ void launch_mu_update(const double* t_in, int64_t rows, int k, const double* num
 void launch_rows_small64(const float* in, int64_t rows, int l, int lp, const double* m, int k,
                          double* out, int ldo, int nsm, cudaStream_t st) {
   const int64_t total = rows * k;
-  static bool attr = false;
-  if (!attr) {
-    cudaFuncSetAttribute(rows_small64_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                         (int)(sizeof(double) * 128 * 128));
-    attr = true;
-  }
+  static std::atomic<unsigned> attr{0u};
+  smem_attr_once(attr, (const void*)(rows_small64_kernel), (int)(sizeof(double) * 128 * 128));
   note_launches(1);
   rows_small64_kernel<<<(unsigned)std::min<int64_t>((total + 255) / 256, 8 * nsm), 256,
                         sizeof(double) * l * k, st>>>(in, rows, l, lp, m, k, out, ldo);

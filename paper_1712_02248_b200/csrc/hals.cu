@@ -236,8 +236,17 @@ __device__ __noinline__ void small_partial_t(const float* __restrict__ in, int n
   };
   for (int p0 = 0; p0 < ntile; p0 += kTPW * (kThreads / 32)) {
     double acc[kTPW][2];
+    // per-tile fragment offsets, computed once per pass (an integer division
+    // per tile per stage showed up as 3% of the C4 kernel's stall samples)
+    int xoff[kTPW], foff[kTPW];
 #pragma unroll
-    for (int u = 0; u < kTPW; ++u) acc[u][0] = acc[u][1] = 0.0;
+    for (int u = 0; u < kTPW; ++u) {
+      acc[u][0] = acc[u][1] = 0.0;
+      const int tI = p0 + warp + (kThreads / 32) * u;
+      const int l0 = (tI / nct) * 8, c0 = (tI % nct) * 8;
+      xoff[u] = t4 * lps + l0 + g;
+      foff[u] = c0 + g < k ? (c0 + g) * kFS + t4 : -1;
+    }
     __syncthreads();  // previous users of the ring are done
 #pragma unroll
     for (int i = 0; i < kRing - 1; ++i) issue(i);
@@ -252,10 +261,9 @@ __device__ __noinline__ void small_partial_t(const float* __restrict__ in, int n
       for (int u = 0; u < kTPW; ++u) {
         const int tI = p0 + warp + (kThreads / 32) * u;
         if (tI >= ntile) break;  // warp-uniform
-        const int l0 = (tI / nct) * 8, c0 = (tI % nct) * 8;
-        const bool bok = c0 + g < k;
-        const float* xa = xs + t4 * lps + l0 + g;
-        const double* fb = fs + (bok ? (c0 + g) * kFS : 0) + t4;
+        const bool bok = foff[u] >= 0;
+        const float* xa = xs + xoff[u];
+        const double* fb = fs + (bok ? foff[u] : t4);
 #pragma unroll
         for (int rs = 0; rs < kSRP; rs += 4) {
           const double av = (double)xa[rs * lps];      // A[g][t] = In[rs + t][l0 + g]
@@ -280,17 +288,155 @@ __device__ __noinline__ void small_partial_t(const float* __restrict__ in, int n
   __syncthreads();
 }
 
-// One pass over the rows whenever the l x k tile grid fits 128 tiles, two up
-// to 256 (8 tiles per warp streamed the rows 4x at C4: 195 tiles; 32 tiles
-// per warp spilled).
+// Register-blocked variant: the 8 warps form a wl x wc grid over the l x k
+// tile grid, each warp owning a BL x BC block of 8 x 8 output tiles for the
+// whole row stream.  Per k-step a warp loads BL A fragments (fp32 -> fp64)
+// and BC B fragments for BL * BC DMMAs (C4: 4 x 7 tiles, 11 shared loads per
+// 28 DMMAs; the one-tile-per-item form above needed two loads per DMMA and
+// was shared-memory bound: short-scoreboard stalls on its fragment loads were
+// the C4 kernel's second hottest lines).  One pass over the rows for any
+// l, k <= 128.
+template <int BL, int BC>
+__device__ __noinline__ void small_partial_blk(const float* __restrict__ in, int nrows, int l,
+                                               int lp, int k, const double* __restrict__ F,
+                                               int64_t ldf, double* ringd, double* __restrict__ part,
+                                               int wc) {
+  const int lps = lps_partial(lp);
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int g = lane >> 2, t4 = lane & 3;
+  const int nlt = (l + 7) >> 3, nct = (k + 7) >> 3;
+  const int wi = warp / wc, wj = warp - wi * wc;
+  const int lt0 = wi * BL, ct0 = wj * BC;
+  const int nst = (nrows + kSRP - 1) / kSRP;
+  const int q4 = lp >> 2, nchunk = kSRP * q4;
+  const int64_t sbytes = partial_stage_bytes(lp, k);
+  char* ring = reinterpret_cast<char*>(ringd);
+  auto xst = [&](int st) { return reinterpret_cast<float*>(ring + (st % kRing) * sbytes); };
+  auto fst = [&](int st) {
+    return reinterpret_cast<double*>(ring + (st % kRing) * sbytes + (int64_t)kSRP * lps * 4);
+  };
+  auto issue = [&](int st) {  // always commits a group (empty past the end)
+    if (st < nst) {
+      const int r0 = st * kSRP;
+      float* xd = xst(st);
+      for (int e = threadIdx.x; e < nchunk; e += kThreads) {
+        const int rr = e / q4, c4 = e - rr * q4;
+        const bool ok = r0 + rr < nrows;
+        cp_async16(xd + rr * lps + 4 * c4, in + (int64_t)(ok ? r0 + rr : 0) * lp + 4 * c4, ok ? 16 : 0);
+      }
+      double* fd = fst(st);
+      for (int e = threadIdx.x; e < kSRP * k; e += kThreads) {  // coalesced along each column
+        const int c = e / kSRP, rr = e - c * kSRP;
+        if (r0 + rr < nrows) cp_async8(fd + c * kFS + rr, F + (int64_t)c * ldf + r0 + rr);
+        else fd[c * kFS + rr] = 0.0;
+      }
+    }
+    cp_async_commit();
+  };
+  // fragment offsets: A[g][t] = In[rs + t][l0 + g], B[t][g] = F[c0 + g][rs + t];
+  // tiles past the grid read row/column 0 and are never stored
+  int xo[BL], fo[BC];
+#pragma unroll
+  for (int i = 0; i < BL; ++i) {
+    const int lt = lt0 + i;
+    xo[i] = t4 * lps + (lt < nlt ? lt * 8 + g : 0);
+  }
+#pragma unroll
+  for (int j = 0; j < BC; ++j) {
+    const int c = (ct0 + j) * 8 + g;
+    fo[j] = (c < k ? c : 0) * kFS + t4;
+  }
+  double acc[BL][BC][2];
+#pragma unroll
+  for (int i = 0; i < BL; ++i)
+#pragma unroll
+    for (int j = 0; j < BC; ++j) acc[i][j][0] = acc[i][j][1] = 0.0;
+  const bool active = lt0 < nlt && ct0 < nct;  // warp-uniform
+  __syncthreads();  // previous users of the ring are done
+#pragma unroll
+  for (int i = 0; i < kRing - 1; ++i) issue(i);
+  for (int st = 0; st < nst; ++st) {
+    cp_async_wait<kRing - 2>();
+    __syncthreads();  // stage st visible to all; the slot refilled below is free
+    issue(st + kRing - 1);
+    if (!active) continue;
+    const float* xs = xst(st);
+    const double* fs = fst(st);
+#pragma unroll 2
+    for (int rs = 0; rs < kSRP; rs += 4) {
+      double av[BL], bv[BC];
+#pragma unroll
+      for (int i = 0; i < BL; ++i) av[i] = (double)xs[xo[i] + rs * lps];
+#pragma unroll
+      for (int j = 0; j < BC; ++j) bv[j] = fs[fo[j] + rs];
+#pragma unroll
+      for (int i = 0; i < BL; ++i)
+#pragma unroll
+        for (int j = 0; j < BC; ++j) dmma(acc[i][j][0], acc[i][j][1], av[i], bv[j]);
+    }
+  }
+  cp_async_wait<0>();
+  if (active) {
+#pragma unroll
+    for (int i = 0; i < BL; ++i)
+#pragma unroll
+      for (int j = 0; j < BC; ++j) {
+        const int li = (lt0 + i) * 8 + g, c = (ct0 + j) * 8 + 2 * t4;
+        if (lt0 + i < nlt && ct0 + j < nct && li < l) {
+          if (c < k) part[li * k + c] = acc[i][j][0];
+          if (c + 1 < k) part[li * k + c + 1] = acc[i][j][1];
+        }
+      }
+  }
+  for (int e = l * k + threadIdx.x; e < lp * k; e += kThreads) part[e] = 0.0;
+  __syncthreads();
+}
+
+// Per-warp block shapes (BL x BC tiles) and the 8-warp grid (wl x wc) they
+// imply, cheapest first by fragment loads per DMMA.
 __device__ void small_partial(const float* __restrict__ in, int nrows, int l, int lp, int k,
                               const double* __restrict__ F, int64_t ldf, double* ring,
                               double* __restrict__ part) {
-  const int ntile = ((l + 7) >> 3) * ((k + 7) >> 3);
-  if (ntile <= 8 * (kThreads / 32))
-    small_partial_t<8>(in, nrows, l, lp, k, F, ldf, ring, part);
-  else
-    small_partial_t<16>(in, nrows, l, lp, k, F, ldf, ring, part);
+  const int nlt = (l + 7) >> 3, nct = (k + 7) >> 3;
+  auto fits = [&](int wl, int bl, int bc) {  // wl x (8 / wl) warps of bl x bc tiles
+    return (nlt + wl - 1) / wl <= bl && (nct + 8 / wl - 1) / (8 / wl) <= bc;
+  };
+  if (fits(4, 2, 2)) small_partial_blk<2, 2>(in, nrows, l, lp, k, F, ldf, ring, part, 2);
+  else if (fits(2, 4, 2)) small_partial_blk<4, 2>(in, nrows, l, lp, k, F, ldf, ring, part, 4);
+  else if (fits(4, 3, 4)) small_partial_blk<3, 4>(in, nrows, l, lp, k, F, ldf, ring, part, 2);
+  else if (fits(2, 5, 2)) small_partial_blk<5, 2>(in, nrows, l, lp, k, F, ldf, ring, part, 4);
+  else if (fits(4, 4, 4)) small_partial_blk<4, 4>(in, nrows, l, lp, k, F, ldf, ring, part, 2);
+  else if (fits(2, 6, 4)) small_partial_blk<6, 4>(in, nrows, l, lp, k, F, ldf, ring, part, 4);
+  else if (fits(4, 4, 7)) small_partial_blk<4, 7>(in, nrows, l, lp, k, F, ldf, ring, part, 2);
+  else if (fits(4, 4, 8)) small_partial_blk<4, 8>(in, nrows, l, lp, k, F, ldf, ring, part, 2);
+  else {
+    const int ntile = nlt * nct;
+    if (ntile <= 8 * (kThreads / 32))
+      small_partial_t<8>(in, nrows, l, lp, k, F, ldf, ring, part);
+    else
+      small_partial_t<16>(in, nrows, l, lp, k, F, ldf, ring, part);
+  }
+}
+
+// Block-wide staging copy dst[e] = f(e) for e < total with eight loads in
+// flight per thread before any store (a plain strided loop waits one L2
+// round trip per element: ~30k cycles for a 100 x 112 Gram, measured by ncu
+// as the top long-scoreboard stall of the C4 kernel).
+template <typename F>
+__device__ __forceinline__ void stage8(double* __restrict__ dst, int total, F f) {
+  for (int e0 = threadIdx.x; e0 < total; e0 += 8 * kThreads) {
+    double v[8];
+#pragma unroll
+    for (int u = 0; u < 8; ++u) {
+      const int e = e0 + u * kThreads;
+      v[u] = e < total ? f(e) : 0.0;
+    }
+#pragma unroll
+    for (int u = 0; u < 8; ++u) {
+      const int e = e0 + u * kThreads;
+      if (e < total) dst[e] = v[u];
+    }
+  }
 }
 
 // Gram of a final lp x k fp64 matrix M (rows >= l are zero), fp64:
@@ -303,10 +449,10 @@ __device__ __noinline__ void gram_to_scratch(const double* __restrict__ M, int l
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const int g = lane >> 2, t4 = lane & 3;
   __syncthreads();
-  for (int e = threadIdx.x; e < l4 * k8; e += kThreads) {
+  stage8(st, l4 * k8, [&](int e) {
     const int r = e / k8, c = e - r * k8;
-    st[e] = (r < l && c < k) ? __ldcg(M + r * k + c) : 0.0;
-  }
+    return (r < l && c < k) ? __ldcg(M + r * k + c) : 0.0;
+  });
   __syncthreads();
   const int nkt = k8 >> 3, ntri = nkt * (nkt + 1) / 2, nqs = l4 >> 2;
   for (int tI = warp; tI < ntri; tI += kThreads / 32) {
@@ -340,10 +486,10 @@ __device__ __noinline__ void gram_to_scratch(const double* __restrict__ M, int l
 // halves (four 16-byte vector loads, broadcast across the warp).
 __device__ __forceinline__ void load_gram(double* gw, const double* __restrict__ src, int k, int kg,
                                           bool cg) {
-  for (int e = threadIdx.x; e < k * kg; e += kThreads) {
+  stage8(gw, k * kg, [&](int e) {
     const int r = e / kg, c = e - r * kg;
-    gw[e] = c < k ? (cg ? __ldcg(src + r * k + c) : src[r * k + c]) : 0.0;
-  }
+    return c < k ? (cg ? __ldcg(src + r * k + c) : src[r * k + c]) : 0.0;
+  });
 }
 template <int N>
 __device__ __forceinline__ void loadn(const double* p, double (&v)[N]) {
@@ -569,7 +715,7 @@ __global__ void __launch_bounds__(kThreads, 1) hals_kernel(const HalsArgs p) {
       } else {
         if (!have_g) gram_to_scratch(S.bchk, l, k, smem, gsc);
         // h = X-check B-check for this CTA's rows (solvers.cpp:421)
-        for (int e = tid; e < lp * k; e += kThreads) Ms[e] = __ldcg(S.bchk + e);
+        stage8(Ms, lp * k, [&](int e) { return __ldcg(S.bchk + e); });
         HALS_PROF(0);
         rows_times_small(S.xc + a_lo * lp, na, lp, l, k, Ms, ring64,
                          [&](int r, int c, double v) { S.h[(int64_t)c * d + a_lo + r] = v; });
@@ -737,14 +883,17 @@ __global__ void __launch_bounds__(kThreads, 1) hals_kernel(const HalsArgs p) {
     } else {
       if (!have_w) gram_to_scratch(S.ahat, l, k, smem, wsc);
       // p = X-hat^T A-hat for this CTA's rows (solvers.cpp:442)
-      for (int e = tid; e < lp * k; e += kThreads) Ms[e] = __ldcg(S.ahat + e);
+      stage8(Ms, lp * k, [&](int e) { return __ldcg(S.ahat + e); });
       rows_times_small(S.xht + b_lo * lp, nbr, lp, l, k, Ms, ring64,
                        [&](int r, int c, double v) { S.p[(int64_t)c * n + b_lo + r] = v; });
-      load_gram(gw, wsc, k, kg, false);
+      if (!bs_dmma_fits(k)) load_gram(gw, wsc, k, kg, false);  // (the DMMA sweep stages its own)
     }
     if (tid < 4) zmask[tid] = 0u;
     __syncthreads();
-    for (int e = tid; e < k; e += kThreads) s_diag[e] = gw[e * kg + e];
+    if (!S.dense && bs_dmma_fits(k))
+      for (int e = tid; e < k; e += kThreads) s_diag[e] = wsc[e * k + e];
+    else
+      for (int e = tid; e < k; e += kThreads) s_diag[e] = gw[e * kg + e];
     __syncthreads();
     int jd = k;
     for (int j = col0; j < k; ++j)
@@ -761,10 +910,10 @@ __global__ void __launch_bounds__(kThreads, 1) hals_kernel(const HalsArgs p) {
       const int k4 = (k + 3) & ~3, kgs = bs_kgs(k);
       double* ws = smem;
       __syncthreads();  // everyone is done with the product stage / gw copy
-      for (int e = tid; e < k4 * kgs; e += kThreads) {
+      stage8(ws, k4 * kgs, [&](int e) {
         const int r = e / kgs, c = e - r * kgs;
-        ws[e] = (r < k && c < k) ? wsc[r * k + c] : 0.0;
-      }
+        return (r < k && c < k) ? wsc[r * k + c] : 0.0;
+      });
       for (int e = tid; e < k; e += kThreads)
         s_ginv[e] = constrained ? 1.0 / (wsc[e * k + e] + p.beta) : 1.0 / wsc[e * k + e];
       __syncthreads();

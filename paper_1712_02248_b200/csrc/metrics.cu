@@ -258,12 +258,8 @@ void launch_recon_error(const float* x, int64_t ldx, int64_t d, int64_t n, const
   const int64_t tiles = ((d + kTile - 1) / kTile) * ((n + kTile - 1) / kTile);
   const int grid = (int)std::max<int64_t>(1, std::min<int64_t>(tiles, (int64_t)nsm * 4));
   const size_t smem = sizeof(float) * 2 * k * kTile;
-  static bool attr = false;
-  if (!attr) {
-    cudaFuncSetAttribute(recon_error_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                         (int)(sizeof(float) * 2 * 128 * kTile));
-    attr = true;
-  }
+  static std::atomic<unsigned> attr{0u};
+  smem_attr_once(attr, (const void*)(recon_error_kernel), (int)(sizeof(float) * 2 * 128 * kTile));
   double* part = static_cast<double*>(ws);
   note_launches(1);
   recon_error_kernel<<<grid, 256, smem, st>>>(x, ldx, d, n, a_cm, b_cm, k, part);

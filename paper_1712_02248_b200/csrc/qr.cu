@@ -355,12 +355,8 @@ void gram(const float* y, int64_t rows, int l, int lp, const QrWs& w, int nsm,
 
 void chol_inv(int l, int lp, const QrWs& w, cudaStream_t st) {
   const size_t smem = sizeof(double) * (l * (l | 1) + 3 * l);
-  static bool attr = false;
-  if (!attr) {
-    cudaFuncSetAttribute(chol_inv_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                         (int)(sizeof(double) * (128 * 129 + 3 * 128)));
-    attr = true;
-  }
+  static std::atomic<unsigned> attr{0u};
+  smem_attr_once(attr, (const void*)(chol_inv_kernel), (int)(sizeof(double) * (128 * 129 + 3 * 128)));
   note_launches(1);
   chol_inv_kernel<<<1, 128, smem, st>>>(w.g, l, lp, w.rinv64, w.rinv, w.flag);
 }
@@ -423,12 +419,8 @@ void launch_thin_qr(const float* y, int64_t rows, int l, int lp, float* q, void*
 void launch_householder_signs(float* q, int64_t rows, int l, int lp, float* sgn, int nsm,
                               cudaStream_t st) {
   const size_t smem = sizeof(double) * (l * l + l);
-  static bool attr = false;
-  if (!attr) {
-    cudaFuncSetAttribute(householder_signs_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                         (int)(sizeof(double) * (128 * 128 + 128)));
-    attr = true;
-  }
+  static std::atomic<unsigned> attr{0u};
+  smem_attr_once(attr, (const void*)(householder_signs_kernel), (int)(sizeof(double) * (128 * 128 + 128)));
   note_launches(2);
   householder_signs_kernel<<<1, 256, smem, st>>>(q, l, lp, sgn);
   const int64_t total = rows * lp;

@@ -340,12 +340,9 @@ void launch_mt_jump(uint64_t seed, uint64_t nwords, uint64_t J, int K, const uin
   note_launches(1);
   mt_stream_kernel<<<1, 160, 0, s>>>(jobs, 1);
   if (K > 1) {
-    static bool attr = false;
     const int smem = (int)jump_state_smem();
-    if (!attr) {
-      cudaFuncSetAttribute(mt_jump_state_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
-      attr = true;
-    }
+    static std::atomic<unsigned> attr{0u};
+    smem_attr_once(attr, (const void*)(mt_jump_state_kernel), smem);
     note_launches(1);
     const int parts = std::max(1, 148 / (K - 1));  // about one wave of CTAs
     cudaMemsetAsync(states, 0, sizeof(uint64_t) * kN * (K - 1), s);

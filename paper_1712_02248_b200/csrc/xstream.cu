@@ -209,12 +209,8 @@ void dispatch(const float* x, int64_t ldx, int64_t m, int64_t n, const float* s,
 #define CNMF_XS_CASE(LPV)                                                              \
   case LPV: {                                                                           \
     const int smem = (int)sizeof(float) * 2 * kBK * (kBM + kAPad + LPV);                \
-    static bool attr = false;                                                           \
-    if (!attr) {                                                                        \
-      cudaFuncSetAttribute(xs_kernel<kTN, LPV>,                                         \
-                           cudaFuncAttributeMaxDynamicSharedMemorySize, smem);          \
-      attr = true;                                                                      \
-    }                                                                                   \
+    static std::atomic<unsigned> attr{0u};                                              \
+    smem_attr_once(attr, (const void*)(xs_kernel<kTN, LPV>), smem);                     \
     note_launches(1);                                                                   \
     xs_kernel<kTN, LPV><<<grid, 256, smem, st>>>(x, ldx, m, n, s, dst, p.kchunk);       \
     break;                                                                              \

@@ -721,11 +721,8 @@ template <bool kTN, int L, bool kF16>
 cudaError_t run_tc(const CUtensorMap& mx, const CUtensorMap& mh, const CUtensorMap& ml,
                    const TcArgs& a, int grid, cudaStream_t st) {
   constexpr int smem = TcRings<L, kF16>::kBytes + 1024;
-  static bool attr = false;
-  if (!attr) {
-    cudaFuncSetAttribute(xs_tc_kernel<kTN, L, kF16>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
-    attr = true;
-  }
+  static std::atomic<unsigned> attr{0u};
+  smem_attr_once(attr, (const void*)(xs_tc_kernel<kTN, L, kF16>), smem);
   note_launches(1);
   return launch_pdl(xs_tc_kernel<kTN, L, kF16>, dim3(grid), dim3(kThreadsTC), (size_t)smem, st, mx,
                     mh, ml, a);

@@ -32,6 +32,16 @@ print("variant", os.environ.get("CNMF_XS", "default"), name)
 for i, r in enumerate(tr.records):
     print(f"it {r.iteration:4d} err {got[i]:.9f} ref {want[i]:.9f} dev {abs(got[i]-want[i])/want[i]:.2e} "
           f"draws {r.rng_draws} ref {int(draws[g['iters'][i]])}")
+# the final objective recomputed in fp64 (torch, row chunks) from the run's
+# own final factors: separates factor accuracy from objective-evaluation accuracy
+a64, b64 = a.double(), b.double()
+tot = 0.0
+for r0 in range(0, d, 4096):
+    rr = x[r0:r0 + 4096].double() - a64[r0:r0 + 4096] @ b64.T
+    tot += float((rr * rr).sum())
+e64 = np.sqrt(tot / xn)
+print(f"final objective: device {got[-1]:.9f}  fp64(torch) {e64:.9f}  reference {want[-1]:.9f}  "
+      f"device-vs-fp64 {abs(got[-1] - e64) / e64:.2e}  fp64-vs-ref {abs(e64 - want[-1]) / want[-1]:.2e}")
 af = a.double().cpu().numpy(); bf = b.double().cpu().numpy()
 for nm, gf, rf in (("A", af, g["a"]), ("B", bf, g["b"])):
     rf = rf.astype(np.float64)
