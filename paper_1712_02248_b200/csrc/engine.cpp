@@ -879,8 +879,37 @@ void run_device_impl(cnmf_context* c, const XView& X0, const cnmf_solver_config&
   CK(cudaMemsetAsync(omega_r, 0, sizeof(float) * d * lp, c->stream));
   CK(cudaEventRecord(c->ev[2], c->stream));
   int passes = build_projectors_dev(c, X, q, lp, w, cfg.sketch_seed, omega_l, omega_r, lm, rt);
+  // Diagnostics only (tools/proj_swap.py): replace the projectors (and
+  // optionally the compressed views) by externally computed ones, to split
+  // a trajectory difference between the range finder, the views and HALS.
+  FILE* diag = nullptr;
+  int64_t diag_hdr[4] = {0, 0, 0, 0};
+  std::vector<float> diag_buf;
+  auto diag_load = [&](float* dst, int64_t rows) {
+    if (std::fread(diag_buf.data(), 4, (size_t)rows * lp, diag) != (size_t)rows * lp)
+      throw Fail(CNMF_ERR_INPUT, "CNMF_DIAG_PROJ: short file");
+    CK(cudaMemcpyAsync(dst, diag_buf.data(), sizeof(float) * rows * lp, cudaMemcpyHostToDevice,
+                       c->stream));
+    c->sync();
+  };
+  if (const char* path = std::getenv("CNMF_DIAG_PROJ")) {
+    diag = std::fopen(path, "rb");
+    if (!diag || std::fread(diag_hdr, 8, 4, diag) != 4 || diag_hdr[0] != d || diag_hdr[1] != n ||
+        diag_hdr[2] != lp)
+      throw Fail(CNMF_ERR_INPUT, "CNMF_DIAG_PROJ: bad file");
+    diag_buf.resize((size_t)std::max(d, n) * lp);
+    diag_load(lm, d);
+    diag_load(rt, n);
+  }
   x_times(c, X, true, lm, lp, xht, xs, c->stream);   // X-hat^T = X^T L
   x_times(c, X, false, rt, lp, xc, xs, c->stream);   // X-check = X R^T
+  if (diag) {
+    if (diag_hdr[3]) {
+      diag_load(xc, d);
+      diag_load(xht, n);
+    }
+    std::fclose(diag);
+  }
   passes += 2;
   CK(cudaEventRecord(c->ev[3], c->stream));
   CK(cudaGetLastError());

@@ -57,6 +57,7 @@ struct HalsArgs {
   int it_begin, it_end, start_half, start_col;
   int skip_dead;       // column whose dead check is skipped once (just redrawn), or -1
   int rows_a, rows_b;  // rows per CTA
+  int a_dmma;          // A-sweep block products on the DMMA path (shared memory permitting)
   unsigned long long epoch0;
 };
 
@@ -484,12 +485,70 @@ __device__ __noinline__ void gram_to_scratch(const double* __restrict__ M, int l
 // g / w in shared memory: k x kg, row stride kg = k rounded up to 8 with zero
 // padding, so a block's 8 coefficients of one row are two aligned 32-byte
 // halves (four 16-byte vector loads, broadcast across the warp).
+// Row stride of g / w in shared memory: k rounded up to 16, plus 4 (== 4 mod
+// 16 doubles: the DMMA B fragments of the A-sweep block product are
+// conflict-free); rows k .. k4 - 1 are zero.
+__host__ __device__ constexpr int gram_stride(int k) { return ((k + 15) & ~15) + 4; }
 __device__ __forceinline__ void load_gram(double* gw, const double* __restrict__ src, int k, int kg,
                                           bool cg) {
-  stage8(gw, k * kg, [&](int e) {
+  const int k4 = (k + 3) & ~3;
+  stage8(gw, k4 * kg, [&](int e) {
     const int r = e / kg, c = e - r * kg;
-    return c < k ? (cg ? __ldcg(src + r * k + c) : src[r * k + c]) : 0.0;
+    return (r < k && c < k) ? (cg ? __ldcg(src + r * k + c) : src[r * k + c]) : 0.0;
   });
+}
+
+// ---- A-sweep block product on the FP64 tensor cores ---------------------
+// acc(r, t) = sum_c A[r][c] g[c][jb + t] for the CTA's rows, t < 8 NT: the
+// product every column block of the A sweep starts from (solvers.cpp:429,
+// the running A g_j).  A is read from L2 (column-major state) as DMMA A
+// fragments, g from shared memory; the results go to shared memory (row
+// stride 8 NT + 1), from where each thread takes its rows.  Replaces a SIMT
+// loop that re-read every A row per block with 4 loads in flight per thread
+// (latency-bound: the hottest line of the C4 kernel's ncu profile).
+template <int NT>
+__device__ __noinline__ void a_block_dmma(const double* __restrict__ a, int64_t d, int64_t a_lo,
+                                          int na, int k, const double* __restrict__ gw, int kg,
+                                          int jb, double* __restrict__ accs) {
+  constexpr int NBS = 8 * NT + 1;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, g = lane >> 2, t4 = lane & 3;
+  const int k4 = (k + 3) & ~3;
+  const int npair = (na + 15) >> 4;
+  for (int pI = warp; pI < npair; pI += kThreads / 32) {
+    const int r0 = pI * 16, ra = r0 + g, rb = r0 + 8 + g;
+    const double* pa = a + a_lo + (ra < na ? ra : 0) + (int64_t)t4 * d;
+    const double* pb = a + a_lo + (rb < na ? rb : 0) + (int64_t)t4 * d;
+    const double* wp = gw + t4 * kg + jb + g;
+    double acc[2][NT][2];
+#pragma unroll
+    for (int i = 0; i < 2; ++i)
+#pragma unroll
+      for (int h = 0; h < NT; ++h) acc[i][h][0] = acc[i][h][1] = 0.0;
+#pragma unroll 5
+    for (int c = 0; c < k4; c += 4) {
+      const bool okc = c + t4 < k;
+      const double a0 = (okc && ra < na) ? __ldcg(pa + (int64_t)c * d) : 0.0;
+      const double a1 = (okc && rb < na) ? __ldcg(pb + (int64_t)c * d) : 0.0;
+#pragma unroll
+      for (int h = 0; h < NT; ++h) {
+        const double wv = wp[c * kg + 8 * h];
+        dmma(acc[0][h][0], acc[0][h][1], a0, wv);
+        dmma(acc[1][h][0], acc[1][h][1], a1, wv);
+      }
+    }
+#pragma unroll
+    for (int i = 0; i < 2; ++i)
+#pragma unroll
+      for (int h = 0; h < NT; ++h) {
+        double* dst = accs + (r0 + 8 * i + g) * NBS + 8 * h + 2 * t4;
+        dst[0] = acc[i][h][0];
+        dst[1] = acc[i][h][1];
+      }
+  }
+}
+// Shared memory of the DMMA A-sweep product (doubles), next to g.
+__host__ __device__ constexpr int64_t a_dmma_doubles(int rows_a, int nb) {
+  return (int64_t)((rows_a + 15) & ~15) * (nb + 1);
 }
 template <int N>
 __device__ __forceinline__ void loadn(const double* p, double (&v)[N]) {
@@ -600,46 +659,61 @@ __device__ __noinline__ void b_sweep_dmma(const HalsState& S, const double* __re
         dmma(acc[1][0][0], acc[1][0][1], a1, w0);
         dmma(acc[1][1][0], acc[1][1][1], a1, w1);
       }
+      // in-block chain; bit t of nzb: this lane owns a non-zero entry of column jb + t
+      unsigned nzb = 0u;
+      auto chain = [&](auto full_c) {
+        constexpr bool kFull = decltype(full_c)::value;  // all 16 columns, from the first
+        const double* wrow = ws + jb * kgs + jb + 2 * t4;
+        double2 wr0 = *reinterpret_cast<const double2*>(wrow + (kFull ? 0 : t0) * kgs);
+        double2 wr1 = *reinterpret_cast<const double2*>(wrow + (kFull ? 0 : t0) * kgs + 8);
 #pragma unroll
-      for (int t = 0; t < 16; ++t) {
-        if (t < t0) continue;
-        if (t >= nbj) break;
-        const int j = jb + t, hh = t >> 3, ee = t & 1, ow = grp | ((t & 7) >> 1);
-        const bool owner = t4 == ((t & 7) >> 1);
-        const double wjj = s_diag[j], winv = s_winv[j];
-        const double2 wr0 = *reinterpret_cast<const double2*>(ws + j * kgs + jb + 2 * t4);
-        const double2 wr1 = *reinterpret_cast<const double2*>(ws + j * kgs + jb + 8 + 2 * t4);
-        const double wv[2][2] = {{(2 * t4 > t) ? wr0.x : 0.0, (2 * t4 + 1 > t) ? wr0.y : 0.0},
-                                 {(8 + 2 * t4 > t) ? wr1.x : 0.0, (9 + 2 * t4 > t) ? wr1.y : 0.0}};
-        bool nz = false;
-#pragma unroll
-        for (int i = 0; i < 2; ++i) {
-          const int r = 8 * i + g;
-          const double bo = bs[j * kBsStr + r];
-          const double sv = acc[i][hh][ee], pp = pv[i][hh][ee];
-          // solvers.cpp:480-490 (unconstrained) / 502-508 (constrained); the
-          // division is a multiplication by the precomputed reciprocal
-          const double v = kConstrained ? (bo * wjj + pp - sv - alpha) * winv : bo + (pp - sv) * winv;
-          const double vf = v > 0.0 ? v : 0.0;
-          const double dl = __shfl_sync(0xffffffffu, vf - bo, ow);
-          if (owner && r < nr) {
-            bs[j * kBsStr + r] = vf;
-            nz |= vf != 0.0;
+        for (int t = 0; t < 16; ++t) {
+          if constexpr (!kFull) {
+            if (t < t0) continue;
+            if (t >= nbj) break;
           }
+          const int j = jb + t, hh = t >> 3, ee = t & 1, ow = grp | ((t & 7) >> 1);
+          const bool owner = t4 == ((t & 7) >> 1);
+          const double wjj = s_diag[j], winv = s_winv[j];
+          // row j of w for this lane's columns; the next row is loaded while
+          // this step's chain runs
+          const double wv[2][2] = {{(2 * t4 > t) ? wr0.x : 0.0, (2 * t4 + 1 > t) ? wr0.y : 0.0},
+                                   {(8 + 2 * t4 > t) ? wr1.x : 0.0, (9 + 2 * t4 > t) ? wr1.y : 0.0}};
+          if (t + 1 < 16) {
+            wr0 = *reinterpret_cast<const double2*>(wrow + (t + 1) * kgs);
+            wr1 = *reinterpret_cast<const double2*>(wrow + (t + 1) * kgs + 8);
+          }
+          bool nz = false;
 #pragma unroll
-          for (int h = 0; h < 2; ++h)
+          for (int i = 0; i < 2; ++i) {
+            const int r = 8 * i + g;
+            const double bo = bs[j * kBsStr + r];
+            const double sv = acc[i][hh][ee], pp = pv[i][hh][ee];
+            // solvers.cpp:480-490 (unconstrained) / 502-508 (constrained); the
+            // division is a multiplication by the precomputed reciprocal
+            const double v = kConstrained ? (bo * wjj + pp - sv - alpha) * winv : bo + (pp - sv) * winv;
+            const double vf = v > 0.0 ? v : 0.0;
+            const double dl = __shfl_sync(0xffffffffu, vf - bo, ow);
+            if (owner && r < nr) {
+              bs[j * kBsStr + r] = vf;
+              nz |= vf != 0.0;
+            }
 #pragma unroll
-            for (int e = 0; e < 2; ++e) acc[i][h][e] = fma(dl, wv[h][e], acc[i][h][e]);
+            for (int h = 0; h < 2; ++h)
+#pragma unroll
+              for (int e = 0; e < 2; ++e) acc[i][h][e] = fma(dl, wv[h][e], acc[i][h][e]);
+          }
+          nzb |= nz ? (1u << t) : 0u;
         }
-        if (__any_sync(0xffffffffu, nz)) {
-          const unsigned bit = 1u << (j & 31);
-          const int wq = j >> 5;
-          zm0 |= wq == 0 ? bit : 0u;
-          zm1 |= wq == 1 ? bit : 0u;
-          zm2 |= wq == 2 ? bit : 0u;
-          zm3 |= wq == 3 ? bit : 0u;
-        }
-      }
+      };
+      if (t0 == 0 && nbj == 16) chain(std::true_type{});
+      else chain(std::false_type{});
+      const unsigned nzw = __reduce_or_sync(0xffffffffu, nzb) << (jb & 16);
+      const int wq = jb >> 5;
+      zm0 |= wq == 0 ? nzw : 0u;
+      zm1 |= wq == 1 ? nzw : 0u;
+      zm2 |= wq == 2 ? nzw : 0u;
+      zm3 |= wq == 3 ? nzw : 0u;
     }
     if (lane == 0) {
       if (zm0) atomicOr(&zmask[0], zm0);
@@ -671,7 +745,7 @@ __global__ void __launch_bounds__(kThreads, 1) hals_kernel(const HalsArgs p) {
 
   const HalsState& S = p.st;
   const int G = gridDim.x, cta = blockIdx.x, tid = threadIdx.x;
-  const int k = S.k, lp = S.lp, l = S.l, kp1 = k + 1, lpp = lp + 1, kg = (k + 15) & ~15;
+  const int k = S.k, lp = S.lp, l = S.l, kp1 = k + 1, lpp = lp + 1, kg = gram_stride(k);
   const int64_t d = S.d, n = S.n;
   const int64_t a_lo = min(d, (int64_t)cta * p.rows_a), a_hi = min(d, a_lo + p.rows_a);
   const int64_t b_lo = min(n, (int64_t)cta * p.rows_b), b_hi = min(n, b_lo + p.rows_b);
@@ -745,6 +819,19 @@ __global__ void __launch_bounds__(kThreads, 1) hals_kernel(const HalsArgs p) {
         const int t0 = max(col0 - jb, 0), nbj = min(NB, jd - jb);
         if (t0 >= nbj) continue;  // resumed at col0 == jd: nothing left in this block
         double acc[RPT][NB];
+        if (p.a_dmma) {
+          double* accs = smem + (int64_t)((k + 3) & ~3) * kg;
+          __syncthreads();  // the previous block's A updates are written
+          a_block_dmma<NB / 8>(S.a, d, a_lo, na, k, gw, kg, jb, accs);
+          __syncthreads();
+#pragma unroll
+          for (int i = 0; i < RPT; ++i) {
+            const int r = tid + kThreads * i;
+            const bool ok = i < rpt && r < na;
+#pragma unroll
+            for (int t = 0; t < NB; ++t) acc[i][t] = ok ? accs[r * (NB + 1) + t] : 0.0;
+          }
+        } else {
 #pragma unroll
         for (int i = 0; i < RPT; ++i)
 #pragma unroll
@@ -769,6 +856,7 @@ __global__ void __launch_bounds__(kThreads, 1) hals_kernel(const HalsArgs p) {
 #pragma unroll
               for (int t = 0; t < NB; ++t) acc[i][t] = fma(av4[i][cc], gv[t], acc[i][t]);
           }
+        }
         }
         double hv[RPT], av[RPT];
 #pragma unroll
@@ -1109,11 +1197,16 @@ __global__ void __launch_bounds__(kThreads, 1) hals_kernel(const HalsArgs p) {
 }
 
 // Shared memory (bytes): the max over phases.
+// g plus the DMMA A-sweep product buffer (bytes), for block width nb
+static size_t a_dmma_smem(const HalsState& st, int rows_a, int nb) {
+  const int64_t k4 = (st.k + 3) & ~3;
+  return (size_t)(k4 * gram_stride(st.k) + a_dmma_doubles(rows_a, nb)) * sizeof(double);
+}
 size_t hals_smem_bytes(const HalsState& st, int /*rows_a*/) {
   const int64_t k = st.k, lp = st.lp, l = st.l, kp1 = k + 1, lpp = lp + 1;
   const int64_t k4 = (k + 3) & ~3;
   const int64_t prod = lp * k + (kRing * (int64_t)rts_stage_floats((int)lp) + 1) / 2;
-  const int64_t sweep = k * ((k + 15) & ~15);
+  const int64_t sweep = ((k + 3) & ~3) * gram_stride((int)k);
   const int64_t part = (kRing * partial_stage_bytes((int)lp, (int)k) + 7) / 8;  // cp.async ring
   const int64_t gram = ((l + 3) & ~3) * ((k + 7) & ~7);
   const int64_t bsw = (!st.dense && bs_dmma_fits((int)k)) ? bs_smem_doubles((int)k) : 0;
@@ -1179,12 +1272,20 @@ cudaError_t launch_hals(const HalsState& st, int normalize_a, double alpha, doub
   a.epoch0 = epoch0;
   a.rows_a = rows_per_cta(st.d, grid);
   a.rows_b = rows_per_cta(st.n, grid);
-  const size_t smem = hals_smem_bytes(st, a.rows_a);
+  size_t smem = hals_smem_bytes(st, a.rows_a);
   if (smem > 227 * 1024) return cudaErrorInvalidConfiguration;
   // rows per thread of the A sweep (register-resident across the column chain)
   const int rpt = (a.rows_a + kThreads - 1) / kThreads;
   if (rpt > kMaxRPTLarge) return cudaErrorInvalidConfiguration;
   const bool large = rpt > 3 || std::getenv("CNMF_HALS_RPT6") != nullptr;  // env: tests only
+  // DMMA block products in the A sweep where g and the product buffer fit
+  // next to the kernel's static shared memory (CNMF_HALS_ASIMT: comparisons)
+  const size_t adm = a_dmma_smem(st, a.rows_a, large ? 8 : 16);
+  // Measured: C4 (k = 100) A sweep 344k -> 267k cycles per iteration; at
+  // C3 (k = 50, 676 rows per SM) the SIMT loop is faster (163k vs 197k), so
+  // the tensor-core product is taken from k > 64.
+  a.a_dmma = adm + 4096 <= 227 * 1024 && st.k > 64 && std::getenv("CNMF_HALS_ASIMT") == nullptr;
+  if (a.a_dmma) smem = std::max(smem, adm);
   const void* fn = large ? (const void*)hals_kernel<kMaxRPTLarge, 8> : (const void*)hals_kernel<3, 16>;
   cudaError_t e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   if (e != cudaSuccess) return e;

@@ -353,6 +353,73 @@ void gram(const float* y, int64_t rows, int l, int lp, const QrWs& w, int nsm,
   gram_reduce_kernel<<<(lp * lp + 7) / 8, 256, 0, st>>>(w.part, grid, l, lp, w.g);
 }
 
+
+// Q = Y R^-1 in fp64 on the FP64 tensor cores (m8n8k4 DMMA): Y fp32 (rows x
+// lp, widened exactly), R^-1 fp64 (lp x lp, upper triangular, zero padded)
+// staged in shared memory, Q rounded to fp32 once.  CholeskyQR's R^-1 spans
+// the sketch's condition number (~1e4-1e5 at C3), so the products' rounding
+// is amplified by it in the small singular directions of Y: through the
+// 3xTF32 X-stream kernel (fp32 R^-1, ~1e-6 relative error) the range finder's
+// basis missed the reference's span by up to 1e-3 at C3 and the FastHALS-RP
+// trajectory by 5e-4 (tools/proj_swap.py: fp64 projectors with the device's
+// own compressed views track the reference within 8e-6).
+// One warp per 8-row tile, all column tiles in registers (lp <= 128).
+__global__ void __launch_bounds__(256) apply_rinv64_kernel(const float* __restrict__ y,
+                                                           int64_t rows, int l, int lp,
+                                                           const double* __restrict__ rinv,
+                                                           float* __restrict__ q) {
+  extern __shared__ double rs[];  // lp x (lp + 4)
+  const int rsd = lp + 4;
+  for (int e = threadIdx.x; e < lp * lp; e += blockDim.x) rs[(e / lp) * rsd + e % lp] = rinv[e];
+  __syncthreads();
+  const int lane = threadIdx.x & 31, g = lane >> 2, t4 = lane & 3;
+  const int nct = (l + 7) >> 3;
+  const int64_t ntiles = (rows + 7) / 8;
+  for (int64_t tI = (int64_t)blockIdx.x * 8 + (threadIdx.x >> 5); tI < ntiles;
+       tI += (int64_t)gridDim.x * 8) {
+    const int64_t r = tI * 8 + g;
+    const float* yr = y + (r < rows ? r : 0) * lp + t4;
+    double acc[16][2];
+#pragma unroll
+    for (int j = 0; j < 16; ++j) acc[j][0] = acc[j][1] = 0.0;
+#pragma unroll 4
+    for (int kk = 0; kk < l; kk += 4) {
+      const double a = (kk + t4 < lp && r < rows) ? (double)__ldg(yr + kk) : 0.0;
+      const double* bp = rs + (kk + t4) * rsd + g;
+#pragma unroll
+      for (int j = 0; j < 16; ++j)
+        if (j < nct && j * 8 + 8 > kk) {  // R^-1 is upper triangular: tiles left of kk are zero
+          const double b = bp[j * 8];
+          asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0, %1}, {%2}, {%3}, {%0, %1};"
+                       : "+d"(acc[j][0]), "+d"(acc[j][1])
+                       : "d"(a), "d"(b));
+        }
+    }
+    if (r < rows) {
+      float* qr_ = q + r * lp;
+#pragma unroll
+      for (int j = 0; j < 16; ++j) {
+        const int c = j * 8 + 2 * t4;
+        if (c < lp) {
+          qr_[c] = c < l ? (float)acc[j][0] : 0.f;
+          if (c + 1 < lp) qr_[c + 1] = c + 1 < l ? (float)acc[j][1] : 0.f;
+        }
+      }
+    }
+  }
+}
+
+void apply_rinv64(const float* y, int64_t rows, int l, int lp, const double* rinv64, float* q,
+                  int nsm, cudaStream_t st) {
+  const int smem = (int)(sizeof(double) * lp * (lp + 4));
+  static std::atomic<unsigned> attr{0u};
+  smem_attr_once(attr, (const void*)(apply_rinv64_kernel), (int)(sizeof(double) * 128 * 132));
+  const int64_t ntiles = (rows + 7) / 8;
+  const int grid = (int)std::max<int64_t>(1, std::min<int64_t>((ntiles + 7) / 8, nsm));
+  note_launches(1);
+  apply_rinv64_kernel<<<grid, 256, smem, st>>>(y, rows, l, lp, rinv64, q);
+}
+
 void chol_inv(int l, int lp, const QrWs& w, cudaStream_t st) {
   const size_t smem = sizeof(double) * (l * (l | 1) + 3 * l);
   static std::atomic<unsigned> attr{0u};
@@ -387,13 +454,13 @@ void launch_thin_qr_dist(const float* y, int64_t rows, int l, int lp, float* q, 
   allreduce_g(w.g, (size_t)lp * lp);
   chol_inv(l, lp, w, st);
   if (passes >= 2) {
-    launch_xs_nn(y, lp, rows, lp, w.rinv, lp, w.q1, w.xs_ws, nsm, st);
+    apply_rinv64(y, rows, l, lp, w.rinv64, w.q1, nsm, st);
     gram(w.q1, rows, l, lp, w, nsm, st);
     allreduce_g(w.g, (size_t)lp * lp);
     chol_inv(l, lp, w, st);
-    launch_xs_nn(w.q1, lp, rows, lp, w.rinv, lp, q, w.xs_ws, nsm, st);
+    apply_rinv64(w.q1, rows, l, lp, w.rinv64, q, nsm, st);
   } else {
-    launch_xs_nn(y, lp, rows, lp, w.rinv, lp, q, w.xs_ws, nsm, st);
+    apply_rinv64(y, rows, l, lp, w.rinv64, q, nsm, st);
   }
   *flag_out = w.flag;
 }
@@ -405,12 +472,12 @@ void launch_thin_qr(const float* y, int64_t rows, int l, int lp, float* q, void*
   gram(y, rows, l, lp, w, nsm, st);
   chol_inv(l, lp, w, st);
   if (passes >= 2) {
-    launch_xs_nn(y, lp, rows, lp, w.rinv, lp, w.q1, w.xs_ws, nsm, st);
+    apply_rinv64(y, rows, l, lp, w.rinv64, w.q1, nsm, st);
     gram(w.q1, rows, l, lp, w, nsm, st);
     chol_inv(l, lp, w, st);
-    launch_xs_nn(w.q1, lp, rows, lp, w.rinv, lp, q, w.xs_ws, nsm, st);
+    apply_rinv64(w.q1, rows, l, lp, w.rinv64, q, nsm, st);
   } else {
-    launch_xs_nn(y, lp, rows, lp, w.rinv, lp, q, w.xs_ws, nsm, st);
+    apply_rinv64(y, rows, l, lp, w.rinv64, q, nsm, st);
   }
   note_launches(1);
   householder_kernel<<<1, 1024, 0, st>>>(y, rows, l, lp, w.hw, w.hv, q, w.flag);
