@@ -20,6 +20,12 @@
  * Threading: a context owns one CUDA stream and serializes its calls; use
  * one context per concurrent caller (the reference's run() is reentrant,
  * solvers.hpp:100-105, cli.cpp:231-247).
+ *
+ * Streams: the context's stream does not synchronise with other streams.
+ * Entry points taking device pointers read their inputs when called: the
+ * caller completes the work producing them first (the Python binding
+ * synchronises torch's current stream before every call).  Every entry point
+ * returns with its own work complete.
  */
 #ifndef CNMF_B200_H_
 #define CNMF_B200_H_
@@ -31,7 +37,7 @@
 extern "C" {
 #endif
 
-#define CNMF_B200_ABI_VERSION 2
+#define CNMF_B200_ABI_VERSION 3
 
 typedef enum cnmf_status {
   CNMF_OK = 0,
@@ -113,6 +119,9 @@ typedef struct cnmf_run_trace {
                                  run Rng's stream) */
   uint64_t x_passes;          /* X-streaming contractions performed */
   char message[256];
+  double sketch_kappa;        /* condition estimate of X Omega that chose the range finder's
+                                 arithmetic (0: not estimated) */
+  int32_t range_finder_fp64;  /* 1: the range finder ran in fp64 (engine.cpp rf_mode) */
 } cnmf_run_trace;
 
 typedef struct cnmf_context cnmf_context;

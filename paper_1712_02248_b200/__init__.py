@@ -104,7 +104,8 @@ class _Trace(C.Structure):
                 ("power_iterations", C.c_uint64), ("alpha", C.c_double), ("beta", C.c_double),
                 ("seed", C.c_uint64), ("estimate_flops_per_iteration", C.c_double),
                 ("estimate_memory_floats", C.c_double), ("x_norm_sq", C.c_double),
-                ("redraws", C.c_uint64), ("x_passes", C.c_uint64), ("message", C.c_char * 256)]
+                ("redraws", C.c_uint64), ("x_passes", C.c_uint64), ("message", C.c_char * 256),
+                ("sketch_kappa", C.c_double), ("range_finder_fp64", C.c_int32)]
 
 
 # Every exported symbol of include/cnmf_b200.h (checked by tests/test_abi.py).
@@ -191,7 +192,7 @@ def load_library(path: str = LIB_PATH):
                                           C.c_char_p, C.c_size_t]
     L.cnmf_pairwise_distortion.argtypes = [vp, u64, u64, vp, u64, u64, u64, dp, dp, C.c_char_p,
                                            C.c_size_t]
-    if L.cnmf_abi_version() != 2:
+    if L.cnmf_abi_version() != 3:
         raise CudaError("libcnmf_b200.so ABI version mismatch")
     _lib = L
     return L
@@ -264,6 +265,8 @@ class RunTrace:
     redraws: int
     x_passes: int
     message: str
+    sketch_kappa: float = 0.0       # condition estimate that chose the range finder's arithmetic
+    range_finder_fp64: int = 0      # 1: the range finder ran in fp64
 
     @property
     def status_name(self) -> str:
@@ -303,6 +306,15 @@ def _check_device_operands(x, a, b, d, n, k):
     if x.stride(0) < n:
         raise DimensionError("x row stride is shorter than its width")
     torch.cuda.current_stream(x.device).synchronize()
+
+
+def _torch_ready():
+    """The library computes on its own (non-blocking) stream: inputs produced by
+    torch on its current stream must be complete before a device-pointer call
+    reads them (include/cnmf_b200.h, "Streams")."""
+    import torch
+    if torch.cuda.is_available():
+        torch.cuda.current_stream().synchronize()
 
 
 class Context:
@@ -351,7 +363,8 @@ class Context:
                         tr.error_seconds, tr.gini_b, tr.status, tr.iterations_run,
                         tr.power_iterations, tr.alpha, tr.beta, tr.seed,
                         tr.estimate_flops_per_iteration, tr.estimate_memory_floats,
-                        tr.x_norm_sq, tr.redraws, tr.x_passes, tr.message.decode())
+                        tr.x_norm_sq, tr.redraws, tr.x_passes, tr.message.decode(),
+                        tr.sketch_kappa, tr.range_finder_fp64)
 
     def run(self, x, config: SolverConfig) -> RunResult:
         """cnmf::run with X in host memory (numpy, float32, row-major)."""
@@ -406,26 +419,31 @@ class Context:
 
     # ---- step level (torch CUDA tensors) -------------------------------------
     def gaussian_sketch(self, rows, cols, seed, out):
+        _torch_ready()
         self._check(self.L.cnmf_gaussian_sketch(self.h, rows, cols, seed, _ptr(out)))
         return out
 
     def initialize(self, d, n, k, seed, a, b):
+        _torch_ready()
         self._check(self.L.cnmf_initialize(self.h, d, n, k, seed, _ptr(a), _ptr(b)))
         return a, b
 
     def powered_range_finder(self, x, q, w, seed, transpose, out):
+        _torch_ready()
         d, n = x.shape
         self._check(self.L.cnmf_powered_range_finder(self.h, _ptr(x), d, n, x.stride(0), q, w,
                                                      seed, int(transpose), _ptr(out)))
         return out
 
     def build_projectors(self, x, q, w, seed, left, right):
+        _torch_ready()
         d, n = x.shape
         self._check(self.L.cnmf_build_projectors(self.h, _ptr(x), d, n, x.stride(0), q, w, seed,
                                                  _ptr(left), _ptr(right)))
         return left, right
 
     def compress(self, x, left, right, xhat, xcheck):
+        _torch_ready()
         d, n = x.shape
         q = left.shape[1]
         self._check(self.L.cnmf_compress(self.h, _ptr(x), d, n, x.stride(0), _ptr(left),
@@ -433,6 +451,7 @@ class Context:
         return xhat, xcheck
 
     def compress_factors(self, a, b, left, right, a_hat, b_check):
+        _torch_ready()
         d, k = a.shape
         n = b.shape[0]
         q = left.shape[1]
@@ -443,6 +462,7 @@ class Context:
 
     def fasthals_rp_steps(self, xhat, xcheck, left, right, a, b, a_hat, b_check,
                           normalize_a=True, alpha=0.0, beta=0.0, rng_seed=1, steps=1) -> int:
+        _torch_ready()
         d, k = a.shape
         n = b.shape[0]
         q = left.shape[1]
@@ -454,6 +474,7 @@ class Context:
         return red.value
 
     def reconstruction_error(self, x, a, b) -> float:
+        _torch_ready()
         d, n = x.shape
         out = C.c_double()
         self._check(self.L.cnmf_reconstruction_error(self.h, _ptr(x), d, n, x.stride(0), _ptr(a),
@@ -461,22 +482,26 @@ class Context:
         return out.value
 
     def thin_qr(self, y, out):
+        _torch_ready()
         self._check(self.L.cnmf_thin_qr(self.h, _ptr(y), y.shape[0], y.shape[1], _ptr(out)))
         return out
 
     def xs_nn(self, x, s, out):
+        _torch_ready()
         d, n = x.shape
         self._check(self.L.cnmf_xs_nn(self.h, _ptr(x), d, n, x.stride(0), _ptr(s), s.shape[1],
                                       _ptr(out)))
         return out
 
     def xs_tn(self, x, t, out):
+        _torch_ready()
         d, n = x.shape
         self._check(self.L.cnmf_xs_tn(self.h, _ptr(x), d, n, x.stride(0), _ptr(t), t.shape[1],
                                       _ptr(out)))
         return out
 
     def time_xstream(self, x, l, transpose, iters=10) -> float:
+        _torch_ready()
         d, n = x.shape
         out = C.c_double()
         self._check(self.L.cnmf_time_xstream(self.h, _ptr(x), d, n, x.stride(0), l,
@@ -485,6 +510,7 @@ class Context:
 
     def synth_x(self, d, n, rank, factor_kind, noise_kind, sigma, seed, out, col_lo=0,
                 col_hi=None):
+        _torch_ready()
         col_hi = n if col_hi is None else col_hi
         self._check(self.L.cnmf_synth_x(self.h, d, n, rank, factor_kind, noise_kind, sigma, seed,
                                         col_lo, col_hi, out.stride(0), _ptr(out)))

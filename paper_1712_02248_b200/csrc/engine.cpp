@@ -62,6 +62,8 @@ struct cnmf_context {
   HaltInfo* halt_host = nullptr;  // pinned
   uint64_t* pos_host = nullptr;   // pinned (the run stream's position)
   void* nccl = nullptr;           // ncclComm_t of a sharded context
+  double last_kappa = 0.0;        // condition estimate of the last run's sketch (0: not taken)
+  int last_rf64 = 0;              // the last build_projectors ran the fp64 range finder
   cnmf_host_collectives hosted{}; // host-staged collectives of a sharded context (tests)
   std::vector<char> host_stage;
   std::map<std::string, bool> filled;  // device copies uploaded once (jump polynomials)
@@ -336,7 +338,7 @@ const int8_t* x_row_exponents(cnmf_context* c, const float* x, int64_t ldx, int6
 // (launch_householder_signs), for the entry points that hand bases out.
 int range_finder(cnmf_context* c, const XView& X, int q, int lp, uint64_t w, bool transpose,
                  const float* omega, float* basis, const std::string& tag,
-                 cudaStream_t st = nullptr, bool canonical = false) {
+                 cudaStream_t st = nullptr, bool canonical = false, bool first_done = false) {
   if (!st) st = c->stream;
   const int64_t rows = transpose ? X.n : X.d, cols = transpose ? X.d : X.n;
   float* y = c->ws<float>("rf_y_" + tag, rows * lp);
@@ -347,14 +349,75 @@ int range_finder(cnmf_context* c, const XView& X, int q, int lp, uint64_t w, boo
   auto apply = [&](const float* s, float* out, bool tn) { x_times(c, X, tn, s, lp, out, xs, st); };
   // intermediate re-orthonormalisations take one Cholesky pass (they only
   // carry a span into the next X pass); the basis handed on takes two
-  apply(omega, y, transpose);
-  launch_thin_qr(y, rows, q, lp, basis, qws, c->nsm, st, w == 0 ? 2 : 1);
+  if (!first_done) {  // (build_projectors_dev may have taken the first step already)
+    apply(omega, y, transpose);
+    launch_thin_qr(y, rows, q, lp, basis, qws, c->nsm, st, w == 0 ? 2 : 1);
+  }
   for (uint64_t it = 0; it < w; ++it) {
     apply(basis, z, !transpose);
     launch_thin_qr(z, cols, q, lp, zq, qws, c->nsm, st, 1);
     apply(zq, y, transpose);
     launch_thin_qr(y, rows, q, lp, basis, qws, c->nsm, st, it + 1 == w ? 2 : 1);
   }
+  if (canonical)
+    launch_householder_signs(basis, rows, q, lp, c->ws<float>("hh_sgn_" + tag, 128), c->nsm, st);
+  CK(cudaGetLastError());
+  return 1 + 2 * (int)w;
+}
+
+// The range finder's arithmetic.  fp64 (default): every X contraction on the
+// FP64 tensor cores (dense.cu xs64, X widened exactly, fp64 accumulation),
+// fp64 sketch products and CholeskyQR; the basis is rounded to fp32 once at
+// the end.  tc (CNMF_RF=tc): the tcgen05 X-stream kernel with fp32 storage.
+// Why: the basis must reproduce the reference's spans including the
+// directions the sketch resolves at the noise level (sigma_1 / sigma_l ~ 1e5
+// at C3).  The tensor cores' fp32-accumulated contractions (3xTF32 1e-6,
+// BF16x9 with exact products 1.9e-7 relative) move the C3 FastHALS-RP
+// trajectory 1e-4 per contraction -- even ONE of the ten (tools/rf_stages.py:
+// all others exact fp64, the last on the tensor cores: 1.1e-4) -- while
+// rounding the exact products to fp32 between steps moves it 1.2e-6; with
+// fp64 projectors the device's own compressed views (3xTF32) track the
+// reference within 8e-6 (tools/proj_swap.py).  The views keep the fast path.
+// CNMF_RF=fp64 | tc forces a path; the default (auto) takes fp64 when the
+// sketch's condition estimate says the tensor-core contractions' ~1e-6
+// relative error would reach the reference's weakest resolved directions:
+// kappa(X Omega) from the first CholeskyQR's R (one extra tensor-core pass).
+enum class RfMode { kAuto, kFp64, kTc };
+static RfMode rf_mode() {  // read per call (tests switch it)
+  const char* e = std::getenv("CNMF_RF");
+  if (e && std::string(e) == "tc") return RfMode::kTc;
+  if (e && std::string(e) == "fp64") return RfMode::kFp64;
+  return RfMode::kAuto;
+}
+constexpr double kRfKappaMax = 1e3;  // see DESIGN.md section 4 (measured per config)
+
+// range_finder_impl (compression.cpp:23-42) in fp64 arithmetic; `omega` is
+// the fp32 sketch (op_cols x lp), `basis` the fp32 result (rows x lp).
+int range_finder64(cnmf_context* c, const XView& X, int q, int lp, uint64_t w, bool transpose,
+                   const float* omega, float* basis, const std::string& tag, cudaStream_t st,
+                   bool canonical, bool /*first_done*/ = false) {
+  const int64_t rows = transpose ? X.n : X.d, cols = transpose ? X.d : X.n;
+  double* om = c->ws<double>("rf64_om_" + tag, cols * lp);
+  double* y = c->ws<double>("rf64_y_" + tag, rows * lp);
+  double* b = c->ws<double>("rf64_b_" + tag, rows * lp);
+  double* z = c->ws<double>("rf64_z_" + tag, cols * lp);
+  double* zq = c->ws<double>("rf64_zq_" + tag, cols * lp);
+  double* xs = c->ws<double>("rf64_xs_" + tag, xs64_ws_doubles(X.d, X.n, lp, c->nsm));
+  void* qws = c->ws<char>("qr64_ws_" + tag, qr64_ws_bytes(std::max(X.d, X.n), lp, c->nsm));
+  auto apply = [&](const double* s, double* out, bool tn) {
+    if (tn) launch_xs64_tn(X.x, X.ldx, X.d, X.n, s, lp, out, xs, c->nsm, st);
+    else launch_xs64_nn(X.x, X.ldx, X.d, X.n, s, lp, out, xs, c->nsm, st);
+  };
+  launch_f32_to_f64(omega, cols * lp, om, c->nsm, st);
+  apply(om, y, transpose);
+  launch_thin_qr64(y, rows, q, lp, b, qws, c->nsm, st, w == 0 ? 2 : 1);
+  for (uint64_t it = 0; it < w; ++it) {
+    apply(b, z, !transpose);
+    launch_thin_qr64(z, cols, q, lp, zq, qws, c->nsm, st, 1);
+    apply(zq, y, transpose);
+    launch_thin_qr64(y, rows, q, lp, b, qws, c->nsm, st, it + 1 == w ? 2 : 1);
+  }
+  launch_f64_to_f32(b, rows * lp, basis, c->nsm, st);
   if (canonical)
     launch_householder_signs(basis, rows, q, lp, c->ws<float>("hh_sgn_" + tag, 128), c->nsm, st);
   CK(cudaGetLastError());
@@ -370,8 +433,31 @@ int build_projectors_dev(cnmf_context* c, const XView& X, int q, int lp, uint64_
   CK(cudaStreamWaitEvent(c->side, c->fork, 0));
   gen_normals(c, seed * 2, X.n, q, omega_l, lp, "L", c->stream);
   gen_normals(c, seed * 2 + 1, X.d, q, omega_r, lp, "R", c->side);
-  int passes = range_finder(c, X, q, lp, w, false, omega_l, lm, "L", c->stream, canonical);
-  passes += range_finder(c, X, q, lp, w, true, omega_r, rt, "R", c->side, canonical);
+  // CSR X keeps the fp32 SpMM range finder (no fp64 sparse contraction)
+  const RfMode mode = rf_mode();
+  bool use64 = !X.sp && mode != RfMode::kTc, first_done = false;
+  c->last_kappa = 0.0;
+  int passes = 0;
+  if (use64 && mode == RfMode::kAuto) {
+    // the tensor-core range finder's first step for L (kept if it is chosen)
+    const int64_t d = X.d;
+    float* y = c->ws<float>("rf_y_L", d * lp);
+    float* xs = c->ws<float>("xs_ws_L", xstream_ws_floats(X.d, X.n, lp, c->nsm));
+    void* qws = c->ws<char>("qr_ws_L", qr_ws_bytes(std::max(X.d, X.n), lp, c->nsm));
+    x_times(c, X, false, omega_l, lp, y, xs, c->stream);
+    launch_thin_qr(y, d, q, lp, lm, qws, c->nsm, c->stream, w == 0 ? 2 : 1);
+    const double kappa = qr_kappa_estimate(qws, d, q, lp, c->nsm, c->stream);
+    use64 = kappa > kRfKappaMax;
+    first_done = !use64;
+    passes = use64 ? 1 : 0;  // the estimate's pass is wasted when fp64 is chosen
+    c->last_kappa = kappa;
+    if (std::getenv("CNMF_RF_DEBUG"))
+      std::fprintf(stderr, "range finder: kappa(X Omega) ~ %.3g -> %s\n", kappa, use64 ? "fp64" : "tc");
+  }
+  c->last_rf64 = use64 ? 1 : 0;
+  auto rf = use64 ? range_finder64 : range_finder;
+  passes += rf(c, X, q, lp, w, false, omega_l, lm, "L", c->stream, canonical, first_done);
+  passes += rf(c, X, q, lp, w, true, omega_r, rt, "R", c->side, canonical, false);
   CK(cudaEventRecord(c->join, c->side));
   CK(cudaStreamWaitEvent(c->stream, c->join, 0));
   return passes;
@@ -918,6 +1004,8 @@ void run_device_impl(cnmf_context* c, const XView& X0, const cnmf_solver_config&
   st.lm = lm;
   st.rt = rt;
   t.x_passes = (uint64_t)passes;
+  t.sketch_kappa = c->last_kappa;
+  t.range_finder_fp64 = c->last_rf64;
 
   // a_hat = L^T A, b_check = R B (solvers.cpp:219-220)
   launch_compress_factors(st, 0, -1, c->stream);
@@ -1023,6 +1111,9 @@ cnmf_status guarded(cnmf_context* c, F&& f) {
   try {
     CK(cudaSetDevice(c->device));
     f();
+    // every entry point returns with its work complete (the caller may read
+    // device outputs from any stream)
+    CK(cudaStreamSynchronize(c->stream));
     c->err.clear();
     return CNMF_OK;
   } catch (const Fail& e) {

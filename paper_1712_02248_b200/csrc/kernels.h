@@ -101,6 +101,13 @@ void launch_thin_qr_dist(const float* y, int64_t rows, int l, int lp, float* q, 
 // the same; the final QR restores full orthogonality).
 void launch_thin_qr(const float* y, int64_t rows, int l, int lp, float* q, void* ws, int nsm,
                     cudaStream_t st, int passes = 2);
+// fp64 in and out (the range finder's fp64 path); ws: qr64_ws_bytes.
+size_t qr64_ws_bytes(int64_t rows, int lp, int nsm);
+void launch_thin_qr64(const double* y, int64_t rows, int l, int lp, double* q, void* ws, int nsm,
+                      cudaStream_t st, int passes = 2);
+void launch_f64_to_f32(const double* a, int64_t total, float* b, int nsm, cudaStream_t st);
+double qr_kappa_estimate(const void* ws, int64_t rows, int l, int lp, int nsm, cudaStream_t st);
+void launch_f32_to_f64(const float* a, int64_t total, double* b, int nsm, cudaStream_t st);
 // Flip the columns of an orthonormal q (rows x lp, l used) to the reference's
 // Householder signs (qr.cpp:35); sgn: l floats of device scratch.  Only the
 // step-level entry points that return bases need it: FastHALS-RP uses L, R

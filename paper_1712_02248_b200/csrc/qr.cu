@@ -14,6 +14,7 @@
 #include "kernels.h"
 
 #include <functional>
+#include <vector>
 
 namespace cnmf {
 
@@ -364,10 +365,11 @@ void gram(const float* y, int64_t rows, int l, int lp, const QrWs& w, int nsm,
 // trajectory by 5e-4 (tools/proj_swap.py: fp64 projectors with the device's
 // own compressed views track the reference within 8e-6).
 // One warp per 8-row tile, all column tiles in registers (lp <= 128).
-__global__ void __launch_bounds__(256) apply_rinv64_kernel(const float* __restrict__ y,
+template <typename In, typename Out>
+__global__ void __launch_bounds__(256) apply_rinv64_kernel(const In* __restrict__ y,
                                                            int64_t rows, int l, int lp,
                                                            const double* __restrict__ rinv,
-                                                           float* __restrict__ q) {
+                                                           Out* __restrict__ q) {
   extern __shared__ double rs[];  // lp x (lp + 4)
   const int rsd = lp + 4;
   for (int e = threadIdx.x; e < lp * lp; e += blockDim.x) rs[(e / lp) * rsd + e % lp] = rinv[e];
@@ -378,7 +380,7 @@ __global__ void __launch_bounds__(256) apply_rinv64_kernel(const float* __restri
   for (int64_t tI = (int64_t)blockIdx.x * 8 + (threadIdx.x >> 5); tI < ntiles;
        tI += (int64_t)gridDim.x * 8) {
     const int64_t r = tI * 8 + g;
-    const float* yr = y + (r < rows ? r : 0) * lp + t4;
+    const In* yr = y + (r < rows ? r : 0) * lp + t4;
     double acc[16][2];
 #pragma unroll
     for (int j = 0; j < 16; ++j) acc[j][0] = acc[j][1] = 0.0;
@@ -396,28 +398,47 @@ __global__ void __launch_bounds__(256) apply_rinv64_kernel(const float* __restri
         }
     }
     if (r < rows) {
-      float* qr_ = q + r * lp;
+      Out* qr_ = q + r * lp;
 #pragma unroll
       for (int j = 0; j < 16; ++j) {
         const int c = j * 8 + 2 * t4;
         if (c < lp) {
-          qr_[c] = c < l ? (float)acc[j][0] : 0.f;
-          if (c + 1 < lp) qr_[c + 1] = c + 1 < l ? (float)acc[j][1] : 0.f;
+          qr_[c] = c < l ? (Out)acc[j][0] : (Out)0;
+          if (c + 1 < lp) qr_[c + 1] = c + 1 < l ? (Out)acc[j][1] : (Out)0;
         }
       }
     }
   }
 }
 
-void apply_rinv64(const float* y, int64_t rows, int l, int lp, const double* rinv64, float* q,
+template <typename In, typename Out>
+void apply_rinv64(const In* y, int64_t rows, int l, int lp, const double* rinv64, Out* q,
                   int nsm, cudaStream_t st) {
   const int smem = (int)(sizeof(double) * lp * (lp + 4));
   static std::atomic<unsigned> attr{0u};
-  smem_attr_once(attr, (const void*)(apply_rinv64_kernel), (int)(sizeof(double) * 128 * 132));
+  smem_attr_once(attr, (const void*)(apply_rinv64_kernel<In, Out>), (int)(sizeof(double) * 128 * 132));
   const int64_t ntiles = (rows + 7) / 8;
   const int grid = (int)std::max<int64_t>(1, std::min<int64_t>((ntiles + 7) / 8, nsm));
   note_launches(1);
-  apply_rinv64_kernel<<<grid, 256, smem, st>>>(y, rows, l, lp, rinv64, q);
+  apply_rinv64_kernel<In, Out><<<grid, 256, smem, st>>>(y, rows, l, lp, rinv64, q);
+}
+
+__global__ void f64_to_f32_kernel(const double* __restrict__ a, int64_t total, float* __restrict__ b,
+                                  const int* __restrict__ only_if) {
+  if (only_if && *only_if == 0) return;
+  for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < total;
+       e += (int64_t)gridDim.x * blockDim.x)
+    b[e] = (float)a[e];
+}
+__global__ void f32_to_f64_kernel(const float* __restrict__ a, int64_t total, double* __restrict__ b,
+                                  const int* __restrict__ only_if) {
+  if (only_if && *only_if == 0) return;
+  for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < total;
+       e += (int64_t)gridDim.x * blockDim.x)
+    b[e] = (double)a[e];
+}
+int conv_grid(int64_t total, int nsm) {
+  return (int)std::max<int64_t>(1, std::min<int64_t>((total + 255) / 256, (int64_t)nsm * 8));
 }
 
 void chol_inv(int l, int lp, const QrWs& w, cudaStream_t st) {
@@ -481,6 +502,64 @@ void launch_thin_qr(const float* y, int64_t rows, int l, int lp, float* q, void*
   }
   note_launches(1);
   householder_kernel<<<1, 1024, 0, st>>>(y, rows, l, lp, w.hw, w.hv, q, w.flag);
+}
+
+// CholeskyQR(2) of an fp64 rows x lp matrix into an fp64 basis (the range
+// finder's fp64 path, engine.cpp): fp64 Gram (dense.cu launch_gram_cm), the
+// same Cholesky / inverse and fp64 DMMA application; on a breakdown the
+// Householder kernel runs on the fp32 rounding of y (device-side flag).
+size_t qr64_ws_bytes(int64_t rows, int lp, int nsm) {
+  return qr_ws_bytes(rows, lp, nsm) + sizeof(double) * (gram_cm_ws_doubles(rows, lp, nsm) + 64);
+}
+void launch_thin_qr64(const double* y, int64_t rows, int l, int lp, double* q, void* ws, int nsm,
+                      cudaStream_t st, int passes) {
+  const QrWs w = carve(ws, rows, lp, nsm);
+  double* gws = reinterpret_cast<double*>(static_cast<char*>(ws) + qr_ws_bytes(rows, lp, nsm));
+  double* q1 = w.hw;  // rows x lp doubles (the Householder working copy when it runs)
+  cudaMemsetAsync(w.flag, 0, sizeof(int), st);
+  launch_gram_cm(y, rows, lp, w.g, gws, nsm, st, true);
+  chol_inv(l, lp, w, st);
+  if (passes >= 2) {
+    apply_rinv64(y, rows, l, lp, w.rinv64, q1, nsm, st);
+    launch_gram_cm(q1, rows, lp, w.g, gws, nsm, st, true);
+    chol_inv(l, lp, w, st);
+    apply_rinv64(q1, rows, l, lp, w.rinv64, q, nsm, st);
+  } else {
+    apply_rinv64(y, rows, l, lp, w.rinv64, q, nsm, st);
+  }
+  // breakdown (rank deficiency): Householder on fp32 y, result widened
+  const int64_t total = rows * lp;
+  note_launches(3);
+  f64_to_f32_kernel<<<conv_grid(total, nsm), 256, 0, st>>>(y, total, w.q1, w.flag);
+  householder_kernel<<<1, 1024, 0, st>>>(w.q1, rows, l, lp, w.hw, w.hv, w.xs_ws, w.flag);
+  f32_to_f64_kernel<<<conv_grid(total, nsm), 256, 0, st>>>(w.xs_ws, total, q, w.flag);
+}
+
+// Condition estimate of the last CholeskyQR's input: max_j r_jj / min_j r_jj
+// of its R (from R^-1's diagonal in the workspace).  Synchronises `st`.
+double qr_kappa_estimate(const void* ws, int64_t rows, int l, int lp, int nsm, cudaStream_t st) {
+  const QrWs w = carve(const_cast<void*>(ws), rows, lp, nsm);
+  std::vector<double> dg(l);
+  if (cudaMemcpy2DAsync(dg.data(), sizeof(double), w.rinv64, sizeof(double) * (lp + 1),
+                        sizeof(double), l, cudaMemcpyDeviceToHost, st) != cudaSuccess ||
+      cudaStreamSynchronize(st) != cudaSuccess)
+    return 0.0;
+  double mx = 0.0, mn = 1e308;
+  for (double v : dg) {
+    if (!(v > 0.0)) return 1e308;  // breakdown
+    mx = std::max(mx, 1.0 / v);
+    mn = std::min(mn, 1.0 / v);
+  }
+  return mx / mn;
+}
+
+void launch_f64_to_f32(const double* a, int64_t total, float* b, int nsm, cudaStream_t st) {
+  note_launches(1);
+  f64_to_f32_kernel<<<conv_grid(total, nsm), 256, 0, st>>>(a, total, b, nullptr);
+}
+void launch_f32_to_f64(const float* a, int64_t total, double* b, int nsm, cudaStream_t st) {
+  note_launches(1);
+  f32_to_f64_kernel<<<conv_grid(total, nsm), 256, 0, st>>>(a, total, b, nullptr);
 }
 
 void launch_householder_signs(float* q, int64_t rows, int l, int lp, float* sgn, int nsm,

@@ -28,7 +28,7 @@ def test_exports_every_header_symbol(lib):
     assert sorted(cb.EXPORTS) == syms
     for s in syms:
         assert hasattr(lib, s), s
-    assert lib.cnmf_abi_version() == 2
+    assert lib.cnmf_abi_version() == 3
 
 
 def test_config_defaults_match_reference(lib):

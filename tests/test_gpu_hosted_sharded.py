@@ -27,6 +27,14 @@ import pytest
 torch = pytest.importorskip("torch")
 pytestmark = pytest.mark.gpu
 
+
+@pytest.fixture(autouse=True)
+def _tc_range_finder(monkeypatch):
+    """Sharded runs build their projectors with the tensor-core range finder
+    (csrc/sharded.inc); the single-GPU runs they are compared with take the
+    same arithmetic (CNMF_RF=tc, engine.cpp rf_mode)."""
+    monkeypatch.setenv("CNMF_RF", "tc")
+
 CASES = {
     # name: (d, n, rank, factor_kind, noise_kind, sigma, k, q, w, iters, every, stream)
     "c1like": (1000, 1001, 20, 0, 1, 0.01, 20, 30, 2, 25, 5, False),

@@ -14,6 +14,14 @@ torch = pytest.importorskip("torch")
 pytestmark = pytest.mark.gpu
 
 
+@pytest.fixture(autouse=True)
+def _tc_range_finder(monkeypatch):
+    """Sharded runs build their projectors with the tensor-core range finder
+    (csrc/sharded.inc); the single-GPU runs they are compared with take the
+    same arithmetic (CNMF_RF=tc, engine.cpp rf_mode)."""
+    monkeypatch.setenv("CNMF_RF", "tc")
+
+
 def _cfg(cb, k, q, w, iters, every=1):
     return cb.SolverConfig(algorithm=cb.FASTHALS_RP, k=k, sketch=cb.SketchConfig(q, w, 1),
                            max_iterations=iters, error_interval=every, rel_tolerance=1e-300, seed=1)
