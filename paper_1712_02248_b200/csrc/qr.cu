@@ -207,27 +207,33 @@ __global__ void __launch_bounds__(128) chol_inv_kernel(const double* __restrict_
     rinv64[e] = 0.0;
   }
   __syncthreads();
-  // thread c owns column c of R^-1, kept transposed in row c of gs's lower
-  // triangle (gs[c][i] = Rinv[i][c], i < c) -- untouched by the factorisation
-  for (int c = tid; c < l; c += nt) {
-    double* xc = gs + c * ls;
-    for (int i = c - 1; i >= 0; --i) {
-      const double* ri = gs + i * ls;
-      double s0 = ri[c] * rdi[c], s1 = 0.0;  // q = c term
-      int q = i + 1;
-      for (; q + 1 < c; q += 2) {
-        s0 = fma(ri[q], xc[q], s0);
-        s1 = fma(ri[q + 1], xc[q + 1], s1);
+  // R^-1 = X by right-looking back substitution of R X = I, one barrier per
+  // row: B starts as I; at step i (descending) row i of X is final,
+  // X[i][c] = B[i][c] / r_i (X[i][i] = 1 / r_i), and every B[a][c] with
+  // a < i <= c takes -R[a][i] X[i][c] (element-parallel on the 8 x 16 thread
+  // grid).  B[a][c] (a < c) lives transposed in gs's strict lower triangle,
+  // gs[c][a].  The column-per-thread back substitution this replaces was a
+  // serial O(l^2) chain per thread (36.6 us per call at l = 36).
+  for (int c = 1 + (tid >> 4); c < l; c += 8)
+    for (int a = tid & 15; a < c; a += 16) gs[c * ls + a] = 0.0;
+  __syncthreads();
+  {
+    const int ty = tid >> 4, tx = tid & 15;
+    for (int i = l - 1; i > 0; --i) {
+      const double di = rdi[i];
+      for (int c = i + tx; c < l; c += 16) {
+        const double xic = c == i ? di : gs[c * ls + i] * di;
+        for (int a = ty; a < i; a += 8) gs[c * ls + a] = fma(-gs[a * ls + i], xic, gs[c * ls + a]);
       }
-      if (q < c) s0 = fma(ri[q], xc[q], s0);
-      xc[i] = -(s0 + s1) * rdi[i];
+      __syncthreads();
     }
-    rinv[c * lp + c] = (float)rdi[c];
-    rinv64[c * lp + c] = rdi[c];
-    for (int i = 0; i < c; ++i) {
-      rinv[i * lp + c] = (float)xc[i];
-      rinv64[i * lp + c] = xc[i];
-    }
+  }
+  for (int e = tid; e < l * l; e += nt) {
+    const int i = e / l, c = e - i * l;
+    if (c < i) continue;
+    const double v = c == i ? rdi[i] : gs[c * ls + i] * rdi[i];
+    rinv[i * lp + c] = (float)v;
+    rinv64[i * lp + c] = v;
   }
 }
 
