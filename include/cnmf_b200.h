@@ -46,7 +46,8 @@ typedef enum cnmf_status {
   CNMF_ERR_INPUT = 3,       /* cnmf::InputError      */
   CNMF_ERR_CUDA = 4,        /* device / driver failure, or no device */
   CNMF_ERR_NCCL = 5,        /* collective failure (sharded runs)     */
-  CNMF_ERR_UNSUPPORTED = 6  /* valid for the reference, not built here */
+  CNMF_ERR_UNSUPPORTED = 6  /* valid for the reference, not built here: k or q above 128
+                               (rows of A past 1536 per SM in the streaming HALS kernel) */
 } cnmf_status;
 
 /* cnmf::Algorithm, algorithm.hpp:8-15 (same order). */

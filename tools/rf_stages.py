@@ -85,6 +85,10 @@ def rf(om, transpose, opts):
                 return x64.T @ s if a_is_t else x64 @ s
             if "firstexact" in opts and cnt[0] < nlast:
                 return x64.T @ s if a_is_t else x64 @ s
+            ndev = int(next((o[5:] for o in opts if o.startswith("first")
+                             and o[5:].isdigit()), "0"))
+            if ndev and cnt[0] > ndev:  # the first ndev contractions on the device, the rest exact
+                return x64.T @ s if a_is_t else x64 @ s
             out = dev_xs(s, a_is_t)
             if "chk" not in first:
                 ex = x64.T @ r32(s) if a_is_t else x64 @ r32(s)
@@ -133,7 +137,10 @@ for tag in sys.argv[2:]:
                 "devboth": {"store32", "om32", "devqr", "devxs"},
                 "lastexact": {"store32", "om32", "devqr", "devxs", "lastexact"},
                 "firstexact": {"store32", "om32", "devqr", "devxs", "firstexact"},
-                "lastexact_c": {"chol", "store32", "om32", "devxs", "lastexact"}}[tag]
+                "lastexact_c": {"chol", "store32", "om32", "devxs", "lastexact"},
+                "first1": {"store32", "om32", "devqr", "devxs", "first1"},
+                "first2": {"store32", "om32", "devqr", "devxs", "first2"},
+                "first3": {"store32", "om32", "devqr", "devxs", "first3"}}[tag]
         L = rf(om_l, False, opts)
         Rt = rf(om_r, True, opts)
     torch.cuda.synchronize()
