@@ -24,7 +24,15 @@ namespace {
 
 constexpr int kBK = 32;    // reduction depth per stage (8 MMA k-steps of 4)
 constexpr int kXT = 256;   // threads per X-stream CTA (8 warps: 4 row groups x 2 column halves)
-constexpr int kNS = 3;     // cp.async pipeline stages
+// Up to LP = 96: two cp.async stages and two CTAs per SM (<= 128 registers):
+// the range finder's fp64 passes at C3 take 107.5 ms vs 119-121 ms with one
+// CTA of three or four stages (tools/rf_kappa.py; the second CTA hides the
+// other's barriers).  Wider tiles keep one CTA of three stages (their 64+
+// accumulator doubles do not fit 128 registers).
+template <int LP> struct Xs64Occ {
+  static constexpr int kStages = LP <= 96 ? 2 : 3;
+  static constexpr int kMinBlocks = LP <= 96 ? 2 : 1;
+};
 constexpr int kNNS = kBK + 4;   // NN X-tile row stride (floats): conflict-free fragment reads
 constexpr int kXBM = 128;  // output rows per CTA
 constexpr int kTNS = kXBM + 8;  // TN X-tile row stride (floats)
@@ -36,7 +44,8 @@ struct Xs64Shape {
   static constexpr int SLD = LP + 2;        // S-tile row stride (doubles)
   static constexpr int XF = (kXBM * kNNS > kBK * kTNS) ? kXBM * kNNS : kBK * kTNS;  // floats
   static constexpr size_t stage_bytes = sizeof(float) * XF + sizeof(double) * kBK * SLD;
-  static constexpr size_t smem = kNS * stage_bytes;
+  static constexpr int NS = Xs64Occ<LP>::kStages;
+  static constexpr size_t smem = NS * stage_bytes;
 };
 
 __device__ __forceinline__ void cp_async16(void* dst, const void* src, int src_bytes) {
@@ -74,7 +83,7 @@ __device__ __forceinline__ void dmma(double& d0, double& d1, double a, double b)
 // SIMT fp64 tile moved 2.5 bytes of shared memory per FMA.  X (fp32) and S
 // (fp64) stream through a 3-stage cp.async ring.
 template <bool kTN, int LP>
-__global__ void __launch_bounds__(kXT, 1) xs64_kernel(const float* __restrict__ x, int64_t ldx,
+__global__ void __launch_bounds__(kXT, Xs64Occ<LP>::kMinBlocks) xs64_kernel(const float* __restrict__ x, int64_t ldx,
                                                       int64_t m, int64_t n,
                                                       const double* __restrict__ s,
                                                       double* __restrict__ out, int64_t kchunk,
@@ -136,6 +145,7 @@ __global__ void __launch_bounds__(kXT, 1) xs64_kernel(const float* __restrict__ 
 
   const int64_t nst = (kend - kbeg + kBK - 1) / kBK;
 #pragma unroll
+  constexpr int kNS = Sh::NS;
   for (int p = 0; p < kNS - 1; ++p) {
     if (p < nst) issue(kbeg + p * kBK, p);
     asm volatile("cp.async.commit_group;" ::: "memory");
