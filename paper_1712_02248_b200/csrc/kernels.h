@@ -107,6 +107,10 @@ void launch_thin_qr64(const double* y, int64_t rows, int l, int lp, double* q, v
                       cudaStream_t st, int passes = 2);
 void launch_f64_to_f32(const double* a, int64_t total, float* b, int nsm, cudaStream_t st);
 double qr_kappa_estimate(const void* ws, int64_t rows, int l, int lp, int nsm, cudaStream_t st);
+void launch_thin_qr64_dist(const double* y, int64_t rows, int l, int lp, double* q, void* ws,
+                           int nsm, cudaStream_t st,
+                           const std::function<void(double*, size_t)>& allreduce_g,
+                           int** flag_out, int passes = 2);
 void launch_f32_to_f64(const float* a, int64_t total, double* b, int nsm, cudaStream_t st);
 // Flip the columns of an orthonormal q (rows x lp, l used) to the reference's
 // Householder signs (qr.cpp:35); sgn: l floats of device scratch.  Only the

@@ -559,6 +559,31 @@ double qr_kappa_estimate(const void* ws, int64_t rows, int l, int lp, int nsm, c
   return mx / mn;
 }
 
+// Row-sharded fp64 CholeskyQR(2): local fp64 Grams summed by allreduce_g;
+// *flag_out is set on a breakdown (the caller falls back, sharded.inc).
+void launch_thin_qr64_dist(const double* y, int64_t rows, int l, int lp, double* q, void* ws,
+                           int nsm, cudaStream_t st,
+                           const std::function<void(double*, size_t)>& allreduce_g,
+                           int** flag_out, int passes) {
+  const QrWs w = carve(ws, rows, lp, nsm);
+  double* gws = reinterpret_cast<double*>(static_cast<char*>(ws) + qr_ws_bytes(rows, lp, nsm));
+  double* q1 = w.hw;
+  cudaMemsetAsync(w.flag, 0, sizeof(int), st);
+  launch_gram_cm(y, rows, lp, w.g, gws, nsm, st, true);
+  allreduce_g(w.g, (size_t)lp * lp);
+  chol_inv(l, lp, w, st);
+  if (passes >= 2) {
+    apply_rinv64(y, rows, l, lp, w.rinv64, q1, nsm, st);
+    launch_gram_cm(q1, rows, lp, w.g, gws, nsm, st, true);
+    allreduce_g(w.g, (size_t)lp * lp);
+    chol_inv(l, lp, w, st);
+    apply_rinv64(q1, rows, l, lp, w.rinv64, q, nsm, st);
+  } else {
+    apply_rinv64(y, rows, l, lp, w.rinv64, q, nsm, st);
+  }
+  *flag_out = w.flag;
+}
+
 void launch_f64_to_f32(const double* a, int64_t total, float* b, int nsm, cudaStream_t st) {
   note_launches(1);
   f64_to_f32_kernel<<<conv_grid(total, nsm), 256, 0, st>>>(a, total, b, nullptr);

@@ -80,6 +80,19 @@ def _worker(rank, world, port, case, out_dir):
 
 @pytest.mark.parametrize("case", sorted(CASES))
 def test_hosted_sharded_world2_matches_single_gpu(ctx, case):
+    _run_case(ctx, case)
+
+
+@pytest.mark.parametrize("case", ["c1like", "streaming"])
+def test_hosted_sharded_world2_fp64_range_finder(ctx, case, monkeypatch):
+    """The fp64 range finder through the sharded path:
+    fp64 sketch all-reduces, row-sharded fp64 CholeskyQR with all-reduced
+    fp64 Grams, against the single-GPU fp64 range finder."""
+    monkeypatch.setenv("CNMF_RF", "fp64")
+    _run_case(ctx, case)
+
+
+def _run_case(ctx, case):
     import socket
 
     import torch.multiprocessing as mp
