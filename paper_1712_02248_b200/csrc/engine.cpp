@@ -540,7 +540,7 @@ void run_hals(cnmf_context* c, HalsRun& hr, int normalize_a, double alpha, doubl
               int64_t ib, int64_t ie, RunStream& rs, double* update_seconds, uint64_t* redraws,
               bool recheck_dead = false) {
   HalsState& st = hr.st;
-  int half = 0, col = 0, skip = -1;
+  int half = 0, col = 0, skip = -1, valid = 0;
   int64_t begin = ib;
   rs.settle();
   CK(cudaEventRecord(c->ev[0], c->stream));
@@ -551,7 +551,7 @@ void run_hals(cnmf_context* c, HalsRun& hr, int normalize_a, double alpha, doubl
                               hr.epoch, hr.grid, c->stream));
     else
       CK(launch_hals(st, normalize_a, alpha, beta, (int)begin, (int)ie, half, col, skip,
-                     hr.epoch, hr.grid, c->stream));
+                     hr.epoch, hr.grid, c->stream, valid));
     CK(cudaMemcpyAsync(c->halt_host, st.halt, sizeof(HaltInfo), cudaMemcpyDeviceToHost,
                        c->stream));
     rs.queue_pos();
@@ -563,6 +563,8 @@ void run_hals(cnmf_context* c, HalsRun& hr, int normalize_a, double alpha, doubl
     if (h.pad) std::swap(st.b, st.bold);  // the kernel double-buffers B
     if (!h.halted) break;
     const int j = h.column;
+    // ZeroA / ZeroB change only A / B: the resumed half's products stay valid
+    valid = (h.kind == kEvZeroA || h.kind == kEvZeroB) ? 1 : 0;
     switch (h.kind) {
       case kEvDeadB:  // solvers.cpp:424-428
         rs.redraw(st.b + (int64_t)j * st.n, st.n);

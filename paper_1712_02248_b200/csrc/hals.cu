@@ -56,6 +56,7 @@ struct HalsArgs {
   double alpha, beta;
   int it_begin, it_end, start_half, start_col;
   int skip_dead;       // column whose dead check is skipped once (just redrawn), or -1
+  int products_valid;  // the first half's products (h, g or p, w) are current (ZeroA / ZeroB resume)
   int rows_a, rows_b;  // rows per CTA
   int a_dmma;          // A-sweep block products on the DMMA path (shared memory permitting)
   unsigned long long epoch0;
@@ -776,6 +777,10 @@ __global__ void __launch_bounds__(kThreads, 1) hals_kernel(const HalsArgs p) {
   unsigned long long ep = p.epoch0;
   unsigned long long nr = S.nr0;  // norm all-reduces so far (slot tags)
   bool have_g = false, have_w = false;
+  // resumed after an emptied column (ZeroA / ZeroB: the redraw changed A or B
+  // only, not B-check or A-hat): the halted launch's h, g (A half) or p, w
+  // (B half) are still current in global memory -- skip recomputing them
+  bool reuse = p.products_valid != 0;
   double* bcur = S.b;  // B as of the start of the B half
   double* bnxt = S.bold;
   int half = p.start_half, col0 = p.start_col, skip = p.skip_dead;
@@ -787,12 +792,15 @@ __global__ void __launch_bounds__(kThreads, 1) hals_kernel(const HalsArgs p) {
       if (S.dense) {  // p = X B, g = B^T B prepared by the host (solvers.cpp:154-155)
         load_gram(gw, S.gd, k, kg, true);
       } else {
-        if (!have_g) gram_to_scratch(S.bchk, l, k, smem, gsc);
-        // h = X-check B-check for this CTA's rows (solvers.cpp:421)
-        stage8(Ms, lp * k, [&](int e) { return __ldcg(S.bchk + e); });
-        HALS_PROF(0);
-        rows_times_small(S.xc + a_lo * lp, na, lp, l, k, Ms, ring64,
-                         [&](int r, int c, double v) { S.h[(int64_t)c * d + a_lo + r] = v; });
+        if (!reuse) {
+          if (!have_g) gram_to_scratch(S.bchk, l, k, smem, gsc);
+          // h = X-check B-check for this CTA's rows (solvers.cpp:421)
+          stage8(Ms, lp * k, [&](int e) { return __ldcg(S.bchk + e); });
+          HALS_PROF(0);
+          rows_times_small(S.xc + a_lo * lp, na, lp, l, k, Ms, ring64,
+                           [&](int r, int c, double v) { S.h[(int64_t)c * d + a_lo + r] = v; });
+        }
+        reuse = false;
         load_gram(gw, gsc, k, kg, false);
       }
       __syncthreads();
@@ -969,11 +977,14 @@ __global__ void __launch_bounds__(kThreads, 1) hals_kernel(const HalsArgs p) {
     if (S.dense) {  // p = X^T A, w = A^T A prepared by the host (solvers.cpp:175-176)
       load_gram(gw, S.wd, k, kg, true);
     } else {
-      if (!have_w) gram_to_scratch(S.ahat, l, k, smem, wsc);
-      // p = X-hat^T A-hat for this CTA's rows (solvers.cpp:442)
-      stage8(Ms, lp * k, [&](int e) { return __ldcg(S.ahat + e); });
-      rows_times_small(S.xht + b_lo * lp, nbr, lp, l, k, Ms, ring64,
-                       [&](int r, int c, double v) { S.p[(int64_t)c * n + b_lo + r] = v; });
+      if (!reuse) {
+        if (!have_w) gram_to_scratch(S.ahat, l, k, smem, wsc);
+        // p = X-hat^T A-hat for this CTA's rows (solvers.cpp:442)
+        stage8(Ms, lp * k, [&](int e) { return __ldcg(S.ahat + e); });
+        rows_times_small(S.xht + b_lo * lp, nbr, lp, l, k, Ms, ring64,
+                         [&](int r, int c, double v) { S.p[(int64_t)c * n + b_lo + r] = v; });
+      }
+      reuse = false;
       if (!bs_dmma_fits(k)) load_gram(gw, wsc, k, kg, false);  // (the DMMA sweep stages its own)
     }
     if (tid < 4) zmask[tid] = 0u;
@@ -1258,8 +1269,9 @@ int hals_grid(const HalsState& st, int nsm) {
 
 cudaError_t launch_hals(const HalsState& st, int normalize_a, double alpha, double beta,
                         int it_begin, int it_end, int start_half, int start_col, int skip_dead,
-                        unsigned long long epoch0, int grid, cudaStream_t s) {
+                        unsigned long long epoch0, int grid, cudaStream_t s, int products_valid) {
   HalsArgs a;
+  a.products_valid = products_valid;
   a.st = st;
   a.normalize_a = normalize_a;
   a.alpha = alpha;

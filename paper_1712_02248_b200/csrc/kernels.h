@@ -207,9 +207,12 @@ int hals_grid(const HalsState& st, int nsm);
 // Returns the cooperative-launch error, if any.
 // it_begin/it_end are 0-based; HaltInfo::iter reports the 1-based iteration.
 // epoch0 must exceed every epoch of earlier launches (HaltInfo::last_epoch).
+// products_valid: resuming after an emptied column (ZeroA / ZeroB), the halted
+// launch's products for the resumed half are reused (dense and sharded runs: 0).
 cudaError_t launch_hals(const HalsState& st, int normalize_a, double alpha, double beta,
                         int it_begin, int it_end, int start_half, int start_col, int skip_dead,
-                        unsigned long long epoch0, int grid, cudaStream_t s);
+                        unsigned long long epoch0, int grid, cudaStream_t s,
+                        int products_valid = 0);
 // Shared-memory-resident variant (hals_resident.cu): same contract; grid 0
 // means the configuration does not fit and the streaming kernel is used.
 int hals_resident_grid(const HalsState& st, int nsm);
