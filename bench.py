@@ -271,6 +271,18 @@ def cpu_reference_sample(name, c, timed_steps=1):
     return vals, kind, sample
 
 
+def shared_config(name, c, world):
+    """The config dict BOTH arms print, identical for the same workload and N
+    (the driver's same_config); what each arm ran on is in its own keys
+    (impl, cpu_baseline)."""
+    x_bytes = 4.0 * c["d"] * ((c["n"] + world - 1) // world)  # per GPU
+    big = x_bytes > L2_BYTES
+    return config_dict(name, c, f"X column-sharded over {world} GPUs (NCCL)" if world > 1
+                       else "1 GPU",
+                       {"l2": ("inputs larger than L2 (X %.0f MB > 126 MB)" % (x_bytes / 1e6))
+                        if big else "L2 flushed (256 MB write) between timed steps"})
+
+
 def config_dict(name, c, parallelism, extra=None):
     """The workload description both arms print (same keys: same_config)."""
     out = {"workload": workload_desc(name, c), "d": c["d"], "n": c["n"], "k": c["k"],
@@ -294,10 +306,12 @@ def run_reference_arm(args, name, c, rank):
             "warmup": args.warmup, "ms_per_step": v * 1e3, "higher_is_better": False,
             "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
             "impl": "reference",
-            "config": config_dict(name, c, "single host thread (the reference is single-threaded)"),
+            "config": shared_config(name, c, args.gpus),
             "cpu_baseline": {"value": v, "unit": "s", "cores": 1, "kind": kind,
                              "sample": sample, "host_cpu": model, "host_cores": ncpu,
-                             "pinning": "sched_setaffinity core 0 (taskset -c 0)"},
+                             "pinning": "sched_setaffinity core 0 (taskset -c 0)",
+                             "note": "the reference solver is single-threaded (cli.cpp:231-247 "
+                                     "only runs independent jobs in parallel)"},
             "e2e": {"value": v, "unit": "s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
     print(json.dumps(line), flush=True)
 
@@ -406,11 +420,7 @@ def run_ours(args, name, c, rank, world, local_rank):
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms_per_step,
             "higher_is_better": False, "scaling": "strong", "vs_baseline": None,
             "dtype": "f32", "data": "synthetic",
-            "config": config_dict(name, c, f"X column-sharded over {world} GPUs (NCCL)"
-                                  if world > 1 else "1 GPU",
-                                  {"l2": ("inputs larger than L2 (X %.0f MB > 126 MB)"
-                                          % (x_bytes / 1e6)) if big else
-                                   "L2 flushed (256 MB write) between timed steps"}),
+            "config": shared_config(name, c, world),
             "compress_seconds": mean_comp, "hals_seconds": upd_mean,
             "hals_ms_per_iteration": t_iter * 1e3,
             "redraws_per_run": redraws,
