@@ -574,7 +574,11 @@ __global__ void __launch_bounds__(kThreadsTC, 1)
       int64_t k0, k1;
       unit_k(u, k0, k1);
       const int tile = u % args.ntiles, split = u / args.ntiles;
+#ifdef TC_EPI64  // experiment: fp64 running sums in the epilogue (spills; precision tests only)
+      double run[L];
+#else
       float run[L];
+#endif
 #pragma unroll
       for (int c = 0; c < L; ++c) run[c] = 0.f;
       for (int64_t g0 = k0; g0 < k1; g0 += (int64_t)kDr * kBK) {
@@ -621,7 +625,9 @@ __global__ void __launch_bounds__(kThreadsTC, 1)
         } else {
 #pragma unroll
           for (int c = 0; c < L; c += 4)
-            if (c < args.lp) *reinterpret_cast<float4*>(dst + c) = make_float4(run[c], run[c + 1], run[c + 2], run[c + 3]);
+            if (c < args.lp)
+              *reinterpret_cast<float4*>(dst + c) =
+                  make_float4((float)run[c], (float)run[c + 1], (float)run[c + 2], (float)run[c + 3]);
         }
       }
     }
