@@ -287,6 +287,7 @@ struct XView {
   int64_t ldx, d, n;
   const CsrView* sp = nullptr;
   const int8_t* rexp = nullptr;  // per-row exponents: the contractions' fp16 path
+  bool tf32_exact = false;       // every element exactly a tf32 value (count data): kX1 path
 };
 
 // The X contractions' fp16 hi/lo path (xstream_tc.cu) is opt-in:
@@ -313,9 +314,22 @@ void x_times(cnmf_context* c, const XView& X, bool transpose, const float* s, in
   if (X.sp)
     launch_csr_spmm_f32(*X.sp, transpose, s, lp, lp, out, lp, c->nsm, st);
   else if (transpose)
-    launch_xs_tn(X.x, X.ldx, X.d, X.n, s, lp, out, xs_ws, c->nsm, st);
+    launch_xs_tn(X.x, X.ldx, X.d, X.n, s, lp, out, xs_ws, c->nsm, st, nullptr, X.tf32_exact);
   else
-    launch_xs_nn(X.x, X.ldx, X.d, X.n, s, lp, out, xs_ws, c->nsm, st, X.rexp);
+    launch_xs_nn(X.x, X.ldx, X.d, X.n, s, lp, out, xs_ws, c->nsm, st, X.rexp, X.tf32_exact);
+}
+
+// Whether every element of a dense X is exactly a tf32 value (one X read,
+// synchronises): the step entry points' counterpart of check_data's flag.
+bool x_tf32_exact(cnmf_context* c, const XView& X) {
+  if (X.sp) return false;
+  int* flag = c->ws<int>("x_exact_flag", 4);
+  CK(cudaMemsetAsync(flag, 0, sizeof(int), c->stream));
+  launch_x_tf32_exact(X.x, X.ldx, X.d, X.n, flag, c->nsm, c->stream);
+  int h = 1;
+  CK(cudaMemcpyAsync(&h, flag, sizeof(int), cudaMemcpyDeviceToHost, c->stream));
+  c->sync();
+  return h == 0;
 }
 
 const int8_t* x_row_exponents(cnmf_context* c, const float* x, int64_t ldx, int64_t d, int64_t n,
@@ -544,8 +558,12 @@ void run_hals(cnmf_context* c, HalsRun& hr, int normalize_a, double alpha, doubl
   int64_t begin = ib;
   rs.settle();
   CK(cudaEventRecord(c->ev[0], c->stream));
+  // CNMF_HALS_TRACE: per-launch device time and halt events on stderr
+  // (diagnostics; ev[2] / ev[3] bracket each launch)
+  static const bool trace = std::getenv("CNMF_HALS_TRACE") != nullptr;
   for (;;) {
     st.nr0 = hr.nr;
+    if (trace) CK(cudaEventRecord(c->ev[2], c->stream));
     if (hr.resident)
       CK(launch_hals_resident(st, normalize_a, alpha, beta, (int)begin, (int)ie, half, col, skip,
                               hr.epoch, hr.grid, c->stream));
@@ -554,10 +572,15 @@ void run_hals(cnmf_context* c, HalsRun& hr, int normalize_a, double alpha, doubl
                      hr.epoch, hr.grid, c->stream, valid));
     CK(cudaMemcpyAsync(c->halt_host, st.halt, sizeof(HaltInfo), cudaMemcpyDeviceToHost,
                        c->stream));
+    if (trace) CK(cudaEventRecord(c->ev[3], c->stream));
     rs.queue_pos();
     c->sync();
     rs.take_pos();
     const HaltInfo h = *c->halt_host;
+    if (trace)
+      std::fprintf(stderr, "hals launch: from iter %lld half %d col %d valid %d: %.1f us, %s kind %d col %d iter %lld\n",
+                   (long long)begin, half, col, valid, 1e6 * c->elapsed(2, 3), h.halted ? "halt" : "done",
+                   h.kind, h.column, (long long)h.iter);
     hr.epoch = h.last_epoch;
     hr.nr = h.last_nr;
     if (h.pad) std::swap(st.b, st.bold);  // the kernel double-buffers B
@@ -924,9 +947,10 @@ void run_device_impl(cnmf_context* c, const XView& X0, const cnmf_solver_config&
     int* flag = c->ws<int>("cflag", 4);
     double* nrm = c->ws<double>("xnorm", 1);
     void* ws = c->ws<char>("metrics_ws", metrics_ws_bytes(d, n, c->nsm));
-    CK(cudaMemsetAsync(flag, 0, 2 * sizeof(int), c->stream));
+    CK(cudaMemsetAsync(flag, 0, 3 * sizeof(int), c->stream));
     // the same read of X yields the row exponents of the contractions' fp16
-    // path (flag[1]: some row spans more than 2^30, keep 3xTF32)
+    // path (flag[1]: some row spans more than 2^30, keep 3xTF32) and whether
+    // X is exact in tf32 (flag[2] == 0: the contractions' two-product mode)
     int8_t* rexp = (!X.sp && compressed && xs_f16_for(d, n))
                        ? c->ws<int8_t>("x_rexp_run", xs_rexp_bytes(d)) : nullptr;
     if (rexp) CK(cudaMemsetAsync(rexp, 0, xs_rexp_bytes(d), c->stream));
@@ -934,14 +958,15 @@ void run_device_impl(cnmf_context* c, const XView& X0, const cnmf_solver_config&
       launch_csr_check(*X.sp, flag, nrm, c->ws<double>("sp_check_ws", csr_metrics_ws_doubles(c->nsm)),
                        c->nsm, c->stream);
     else
-      launch_check_data(X.x, X.ldx, d, n, flag, nrm, ws, c->nsm, c->stream, rexp, flag + 1);
+      launch_check_data(X.x, X.ldx, d, n, flag, nrm, ws, c->nsm, c->stream, rexp, flag + 1, flag + 2);
     CK(cudaGetLastError());
-    int hflag[2] = {0, 0};
-    CK(cudaMemcpyAsync(hflag, flag, 2 * sizeof(int), cudaMemcpyDeviceToHost, c->stream));
+    int hflag[3] = {0, 0, 1};
+    CK(cudaMemcpyAsync(hflag, flag, 3 * sizeof(int), cudaMemcpyDeviceToHost, c->stream));
     CK(cudaMemcpyAsync(&t.x_norm_sq, nrm, sizeof(double), cudaMemcpyDeviceToHost, c->stream));
     c->sync();
     if (hflag[0]) throw Fail(CNMF_ERR_INPUT, "solver input must be entrywise non-negative and finite");
     if (rexp && !hflag[1]) X.rexp = rexp;
+    X.tf32_exact = !X.sp && hflag[2] == 0;
   }
 
   const bool dense_hals = algo == CNMF_FASTHALS || algo == CNMF_HALS;
@@ -1487,8 +1512,9 @@ cnmf_status cnmf_compress(cnmf_context* c, const float* x, uint64_t d, uint64_t 
     float* xht = c->ws<float>("cmp_XhT", n * lp);
     float* xcp = c->ws<float>("cmp_Xc", d * lp);
     float* xs = c->ws<float>("xs_ws", xstream_ws_floats((int64_t)d, (int64_t)n, lp, c->nsm));
-    launch_xs_tn(X.x, X.ldx, X.d, X.n, lm, lp, xht, xs, c->nsm, c->stream);
-    launch_xs_nn(X.x, X.ldx, X.d, X.n, rt, lp, xcp, xs, c->nsm, c->stream);
+    const bool ex = x_tf32_exact(c, X);
+    launch_xs_tn(X.x, X.ldx, X.d, X.n, lm, lp, xht, xs, c->nsm, c->stream, nullptr, ex);
+    launch_xs_nn(X.x, X.ldx, X.d, X.n, rt, lp, xcp, xs, c->nsm, c->stream, nullptr, ex);
     launch_transpose(xht, (int64_t)n, (int64_t)q, lp, xhat, (int64_t)n, c->stream);
     launch_unpad_cols(xcp, (int64_t)d, lp, xcheck, (int)q, c->stream);
     CK(cudaGetLastError());
@@ -1608,7 +1634,7 @@ cnmf_status cnmf_xs_nn(cnmf_context* c, const float* x, uint64_t d, uint64_t n, 
     float* yp = c->ws<float>("xs_y", d * lp);
     float* ws = c->ws<float>("xs_ws", xstream_ws_floats((int64_t)d, (int64_t)n, lp, c->nsm));
     const int8_t* rexp = x_row_exponents(c, X.x, X.ldx, X.d, X.n, "abi");  // fp16 path (large X)
-    launch_xs_nn(X.x, X.ldx, X.d, X.n, sp, lp, yp, ws, c->nsm, c->stream, rexp);
+    launch_xs_nn(X.x, X.ldx, X.d, X.n, sp, lp, yp, ws, c->nsm, c->stream, rexp, x_tf32_exact(c, X));
     launch_unpad_cols(yp, (int64_t)d, lp, y, (int)l, c->stream);
     CK(cudaGetLastError());
     c->sync();
@@ -1624,7 +1650,7 @@ cnmf_status cnmf_xs_tn(cnmf_context* c, const float* x, uint64_t d, uint64_t n, 
     float* tp = padded(c, "xs_t", t, (int64_t)d, (int)l, lp);
     float* zp = c->ws<float>("xs_z", n * lp);
     float* ws = c->ws<float>("xs_ws", xstream_ws_floats((int64_t)d, (int64_t)n, lp, c->nsm));
-    launch_xs_tn(X.x, X.ldx, X.d, X.n, tp, lp, zp, ws, c->nsm, c->stream);
+    launch_xs_tn(X.x, X.ldx, X.d, X.n, tp, lp, zp, ws, c->nsm, c->stream, nullptr, x_tf32_exact(c, X));
     launch_unpad_cols(zp, (int64_t)n, lp, z, (int)l, c->stream);
     CK(cudaGetLastError());
     c->sync();
@@ -1650,11 +1676,12 @@ cnmf_status cnmf_time_xstream(cnmf_context* c, const float* x, uint64_t d, uint6
     // per-X preprocessing of the fp16 path, once per X (a run does it once
     // for its 4w + 4 contractions): outside the per-launch timing
     const int8_t* rexp = x_row_exponents(c, X.x, X.ldx, X.d, X.n, "tx");
+    const bool ex = x_tf32_exact(c, X);  // as check_data decides it for a run
     auto once = [&] {
       if (transpose)
-        launch_xs_tn(X.x, X.ldx, X.d, X.n, s, lp, y, ws, c->nsm, c->stream);
+        launch_xs_tn(X.x, X.ldx, X.d, X.n, s, lp, y, ws, c->nsm, c->stream, nullptr, ex);
       else
-        launch_xs_nn(X.x, X.ldx, X.d, X.n, s, lp, y, ws, c->nsm, c->stream, rexp);
+        launch_xs_nn(X.x, X.ldx, X.d, X.n, s, lp, y, ws, c->nsm, c->stream, rexp, ex);
     };
     once();  // warm-up
     CK(cudaEventRecord(c->ev[0], c->stream));

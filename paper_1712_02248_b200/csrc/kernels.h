@@ -68,10 +68,15 @@ void launch_redraw_fill(const uint64_t* words, uint64_t nwords, uint64_t* pos, u
 size_t xstream_ws_floats(int64_t m, int64_t n, int lp, int nsm);
 // rexp (optional, from launch_x_rowexp over this X): per-row exponents that
 // select the tensor-core kernel's fp16 hi/lo path.
+// x_exact: every element of X is exactly a tf32 value (launch_x_tf32_exact /
+// check_data): the tensor-core kernel's two-product mode (kX1), bitwise the
+// same result.
 void launch_xs_nn(const float* x, int64_t ldx, int64_t m, int64_t n, const float* s, int lp,
-                  float* y, float* ws, int nsm, cudaStream_t st, const int8_t* rexp = nullptr);
+                  float* y, float* ws, int nsm, cudaStream_t st, const int8_t* rexp = nullptr,
+                  bool x_exact = false);
 void launch_xs_tn(const float* x, int64_t ldx, int64_t m, int64_t n, const float* t, int lp,
-                  float* z, float* ws, int nsm, cudaStream_t st, const int8_t* rexp = nullptr);
+                  float* z, float* ws, int nsm, cudaStream_t st, const int8_t* rexp = nullptr,
+                  bool x_exact = false);
 
 // xstream_tc.cu: the same contractions on tcgen05 tensor cores (3xTF32,
 // TMA-staged operands, TMEM accumulators).  Returns false (nothing launched)
@@ -80,7 +85,11 @@ size_t xstream_tc_ws_floats(int64_t m, int64_t n, int lp, int nsm);
 void xstream_tc_set_debug(float* dbg);  // tools/tc_debug.cu only
 bool launch_xs_tc(bool tn, const float* x, int64_t ldx, int64_t m, int64_t n, const float* s,
                   int lp, float* out, float* ws, int nsm, cudaStream_t st,
-                  const int8_t* rexp = nullptr);
+                  const int8_t* rexp = nullptr, bool x_exact = false);
+// flag |= 1 unless every element of X (d x n, ld ldx, 16 B aligned rows) is
+// exactly representable in tf32 (low 13 mantissa bits zero).
+void launch_x_tf32_exact(const float* x, int64_t ldx, int64_t d, int64_t n, int* flag, int nsm,
+                         cudaStream_t st);
 // Per-row exponents of X (d rows, xs_rexp_bytes(d) bytes, zero padded) and a
 // flag set when some row's dynamic range exceeds 2^30 (keep 3xTF32 then).
 size_t xs_rexp_bytes(int64_t rows);
@@ -124,7 +133,7 @@ void launch_householder_signs(float* q, int64_t rows, int l, int lp, float* sgn,
 size_t metrics_ws_bytes(int64_t d, int64_t n, int nsm);
 void launch_check_data(const float* x, int64_t ldx, int64_t d, int64_t n, int* flag,
                        double* norm_sq, void* ws, int nsm, cudaStream_t st, int8_t* rexp = nullptr,
-                       int* wide = nullptr);
+                       int* wide = nullptr, int* inexact = nullptr);
 // 1/2 ||X - A B^T||^2 with column-major A_cm (k x d), B_cm (k x n).
 // The same objective on the tensor cores (recon_tc.cu): dense X (ldx % 4 ==
 // 0, 16-byte aligned), k <= 128; returns false when those do not hold.

@@ -19,16 +19,19 @@ constexpr int kTile = 64;
 // -- the row's exponent for the X-stream kernel's fp16 path (row max scaled
 // into [2^14, 2^15)) plus `wide` when a row's smallest nonzero magnitude is
 // below 2^-30 of its max.  One read of X serves the validation and the
-// scaling.
+// scaling.  inexact |= 1 when some element is not exactly a tf32 value (the
+// X-stream kernel's two-product mode needs every element exact).
 __global__ void __launch_bounds__(256) check_data_kernel(const float* __restrict__ x, int64_t ldx,
                                                          int64_t d, int64_t n,
                                                          int* __restrict__ flag,
                                                          double* __restrict__ part,
                                                          int8_t* __restrict__ rexp,
-                                                         int* __restrict__ wide) {
+                                                         int* __restrict__ wide,
+                                                         int* __restrict__ inexact) {
   __shared__ double red[8];
   double s = 0.0;
   int bad = 0;
+  unsigned low = 0u;
   const int lane = threadIdx.x & 31;
   const int64_t n4 = (n + 3) / 4;
   const bool vec = (ldx % 4) == 0 && (reinterpret_cast<uintptr_t>(x) & 15) == 0;
@@ -48,6 +51,7 @@ __global__ void __launch_bounds__(256) check_data_kernel(const float* __restrict
 #pragma unroll
       for (int q = 0; q < 4; ++q) {
         if (!(v[q] >= 0.f) || !isfinite(v[q])) bad = 1;
+        low |= __float_as_uint(v[q]);
         s += (double)v[q] * (double)v[q];
         mx = fmaxf(mx, v[q]);
         if (v[q] > 0.f) mn = fminf(mn, v[q]);
@@ -71,6 +75,7 @@ __global__ void __launch_bounds__(256) check_data_kernel(const float* __restrict
     }
   }
   if (__syncthreads_or(bad) && threadIdx.x == 0) *flag = 1;
+  if (__syncthreads_or((low & 0x1FFFu) != 0u) && threadIdx.x == 0 && inexact) *inexact = 1;
   s = block_sum(s, red);
   if (threadIdx.x == 0) part[blockIdx.x] = s;
 }
@@ -243,11 +248,11 @@ size_t metrics_ws_bytes(int64_t, int64_t, int nsm) { return sizeof(double) * (ns
 
 void launch_check_data(const float* x, int64_t ldx, int64_t d, int64_t n, int* flag,
                        double* norm_sq, void* ws, int nsm, cudaStream_t st, int8_t* rexp,
-                       int* wide) {
+                       int* wide, int* inexact) {
   const int grid = nsm * 4;
   double* part = static_cast<double*>(ws);
   note_launches(1);
-  check_data_kernel<<<grid, 256, 0, st>>>(x, ldx, d, n, flag, part, rexp, wide);
+  check_data_kernel<<<grid, 256, 0, st>>>(x, ldx, d, n, flag, part, rexp, wide, inexact);
   note_launches(1);
   sum_partials_kernel<<<1, 32, 0, st>>>(part, grid, norm_sq, 1.0);
 }

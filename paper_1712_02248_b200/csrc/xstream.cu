@@ -256,14 +256,14 @@ static bool use_tc() {
 }
 
 void launch_xs_nn(const float* x, int64_t ldx, int64_t m, int64_t n, const float* s, int lp,
-                  float* y, float* ws, int nsm, cudaStream_t st, const int8_t* rexp) {
-  if (use_tc() && launch_xs_tc(false, x, ldx, m, n, s, lp, y, ws, nsm, st, rexp)) return;
+                  float* y, float* ws, int nsm, cudaStream_t st, const int8_t* rexp, bool x_exact) {
+  if (use_tc() && launch_xs_tc(false, x, ldx, m, n, s, lp, y, ws, nsm, st, rexp, x_exact)) return;
   dispatch<false>(x, ldx, m, n, s, lp, y, ws, nsm, st);
 }
 
 void launch_xs_tn(const float* x, int64_t ldx, int64_t m, int64_t n, const float* t, int lp,
-                  float* z, float* ws, int nsm, cudaStream_t st, const int8_t* rexp) {
-  if (use_tc() && launch_xs_tc(true, x, ldx, m, n, t, lp, z, ws, nsm, st, rexp)) return;
+                  float* z, float* ws, int nsm, cudaStream_t st, const int8_t* rexp, bool x_exact) {
+  if (use_tc() && launch_xs_tc(true, x, ldx, m, n, t, lp, z, ws, nsm, st, rexp, x_exact)) return;
   dispatch<true>(x, ldx, m, n, t, lp, z, ws, nsm, st);
 }
 

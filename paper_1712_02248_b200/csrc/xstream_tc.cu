@@ -80,7 +80,14 @@ constexpr int kXBytes = kBM * kBK * 4;  // 16 KB per stage (x_hi), same for x_lo
 //          (harmless), so x's exactness is what matters.
 //          The x0 s0 products accumulate in their own chain (L <= 96), so the
 //          small terms are not rounded against the large ones.
-constexpr int kTF32 = 0, kF16 = 1, kBF9 = 2;
+//   kX1    X exact in tf32 (every element's low 13 mantissa bits zero, e.g.
+//          count data: check_data / launch_x_tf32_exact decide per X): x_lo
+//          = 0, so 3xTF32 reduces to x s_hi + x s_lo -- the same products
+//          into the same accumulator in the same order, bitwise the kTF32
+//          result -- and the MMA reads X straight from the TMA stage (both
+//          operands from shared memory, no split warps, no tensor-memory
+//          operand stores: the limiter of the kTF32 kernel, DESIGN 3.1).
+constexpr int kTF32 = 0, kF16 = 1, kBF9 = 2, kX1 = 3;
 
 // Instruction descriptor: kind::f16 with fp16 A and B, fp32 accumulate,
 // M = 128 (layouts checked by tools/tc_f16_check.cu); bf16 sets the A / B
@@ -125,7 +132,7 @@ struct TcArgs {
 // stage is released as soon as the split warps have read it.
 template <int L, int kMode = kTF32> struct TcRings {
   // fp16 / bf16 S stages are LH halves wide: 64-element SWIZZLE_128B atoms
-  static constexpr bool kHalf = kMode != kTF32;
+  static constexpr bool kHalf = kMode == kF16 || kMode == kBF9;
   static constexpr int LH = (L + 63) & ~63;
   static constexpr int kBBytes = kHalf ? kBK * LH * 2 : kBK * L * 4;  // one S piece per K-block
   static constexpr int kPieces = kMode == kBF9 ? 3 : 2;               // S pieces per stage
@@ -136,7 +143,8 @@ template <int L, int kMode = kTF32> struct TcRings {
 #ifdef TC_XSTAGES
   static constexpr int kXStages = TC_XSTAGES;
 #else
-  static constexpr int kXStages = L <= 32 ? 8 : (L <= 64 ? 6 : (L <= 96 ? 5 : 4));
+  static constexpr int kXStages = kMode == kX1 ? (L <= 64 ? 8 : (L <= 96 ? 6 : 5))
+                                               : (L <= 32 ? 8 : (L <= 64 ? 6 : (L <= 96 ? 5 : 4)));
 #endif
   static constexpr int kBFit = (kBudget - kXStages * kXBytes) / (kPieces * kBBytes);
 #ifdef TC_BSTAGES
@@ -167,7 +175,7 @@ template <int L, int kMode = kTF32> struct TcRings {
 #else
   static constexpr int kOpStages = kOpFit > 4 ? 4 : kOpFit;
 #endif
-  static constexpr uint32_t kTmemNeed = kAOff + kOpStages * kASlot;
+  static constexpr uint32_t kTmemNeed = kAOff + (kMode == kX1 ? 0 : kOpStages * kASlot);
   static constexpr uint32_t kTmemCols =
       kTmemNeed <= 32 ? 32 : (kTmemNeed <= 64 ? 64 : (kTmemNeed <= 128 ? 128 : (kTmemNeed <= 256 ? 256 : 512)));
 };
@@ -207,7 +215,7 @@ __global__ void __launch_bounds__(kThreadsTC, 1)
                  const __grid_constant__ CUtensorMap map_bl, const __grid_constant__ CUtensorMap map_b2,
                  const TcArgs args) {
   using R = TcRings<L, kMode>;
-  constexpr bool kIsF16 = kMode == kF16, kIsBF9 = kMode == kBF9;
+  constexpr bool kIsF16 = kMode == kF16, kIsBF9 = kMode == kBF9, kIsX1 = kMode == kX1;
   constexpr int kDr = kIsF16 ? kDrain16 : kDrain;  // K-blocks per accumulator drain
   constexpr int kSX = R::kXStages, kSO = R::kOpStages, kSB = R::kBStages;
   constexpr uint32_t kTmemCols = R::kTmemCols;
@@ -222,7 +230,7 @@ __global__ void __launch_bounds__(kThreadsTC, 1)
   if (threadIdx.x == 0) {
     for (int s = 0; s < kSX; ++s) {
       mbar_init(&xfull[s], 1);
-      mbar_init(&xempty[s], 4);
+      mbar_init(&xempty[s], kIsX1 ? 1 : 4);  // kX1: released by the MMA commit
     }
     for (int s = 0; s < kSO; ++s) {
       mbar_init(&opready[s], 4);
@@ -268,8 +276,11 @@ __global__ void __launch_bounds__(kThreadsTC, 1)
 
   if (warp == kWarpTMA) {
     // ---------------- X producer ----------------
-    // NN: one 32 (k) x 128 (rows) box, SWIZZLE_128B (conflict-free row reads);
-    // TN: one 128 (rows of Z = columns of X) x 32 (k) box, no swizzle.
+    // NN: one 32 (k) x 128 (rows) box, SWIZZLE_128B (conflict-free row reads;
+    // for kX1 the K-major SW128 A operand as it stands);
+    // TN: one 128 (rows of Z = columns of X) x 32 (k) box, no swizzle; kX1:
+    // four 32 x 32 boxes in the MN-major SW128/32 B-atom operand layout (the
+    // same as S's).
     if (lane == 0) {
       int nblk = 0;
       int s = 0;
@@ -282,8 +293,15 @@ __global__ void __launch_bounds__(kThreadsTC, 1)
           mbar_wait(&xempty[s], ph ^ 1);
           TC_EV(0, nblk++);
           mbar_expect_tx(&xfull[s], kXBytes);
-          if (!kTN) tma(x_addr(s), &map_x, &xfull[s], (int)kk, row0);
-          else tma(x_addr(s), &map_x, &xfull[s], row0, (int)kk);
+          if (!kTN) {
+            tma(x_addr(s), &map_x, &xfull[s], (int)kk, row0);
+          } else if constexpr (kIsX1) {
+#pragma unroll
+            for (int a = 0; a < kBM / 32; ++a)
+              tma(x_addr(s) + a * (kBK * 128), &map_x, &xfull[s], row0 + 32 * a, (int)kk);
+          } else {
+            tma(x_addr(s), &map_x, &xfull[s], row0, (int)kk);
+          }
           if (++s == kSX) {
             s = 0;
             ph ^= 1;
@@ -341,8 +359,8 @@ __global__ void __launch_bounds__(kThreadsTC, 1)
       int nblk = 0;
       const uint32_t idesc = idesc_tf32(args.nmma, false, true);
       constexpr uint32_t kLoOff = (L / 32) * (kBK * 128);
-      int o = 0, b = 0, ab = 0;
-      uint32_t oph = 0, bph = 0, aph = 0;
+      int o = 0, b = 0, ab = 0, xs = 0;
+      uint32_t oph = 0, bph = 0, aph = 0, xph = 0;
       for (int u = blockIdx.x; u < units; u += gridDim.x) {
         int64_t k0, k1;
         unit_k(u, k0, k1);
@@ -353,6 +371,41 @@ __global__ void __launch_bounds__(kThreadsTC, 1)
           const uint32_t d = tmem + ab * R::kAccCols;
           uint32_t acc = 0;
           for (int64_t kk = g0; kk < g1; kk += kBK) {
+            if constexpr (kIsX1) {
+              // X straight from its TMA stage: x s_hi then x s_lo per k-step
+              // (kTF32's order with its zero x_lo s_hi product dropped).
+              // K-major SW128 (NN): 8-row groups 1 KB apart, a k-step is 32 B
+              // into the swizzle atom; MN-major (TN): as S.
+              mbar_wait_warp(&xfull[xs], xph);
+              mbar_wait_warp(&bfull[b], bph);
+              if (lane == 0) TC_EV(4, nblk);
+              tc_fence_after();
+              const uint32_t idx = idesc_tf32(args.nmma, kTN, true);
+              const uint64_t ax = kTN ? desc_mn(x_addr(xs), kBK * 128) : smem_desc(x_addr(xs), 16, 1024, 2);
+              const uint64_t bh = desc_mn(b_addr(b), kBK * 128);
+              const uint64_t bl = desc_mn(b_addr(b) + kLoOff, kBK * 128);
+#pragma unroll
+              for (int ks = 0; ks < kBK / 8; ++ks) {
+                const uint64_t koff = (uint64_t)(ks * 1024 >> 4);
+                const uint64_t aoff = kTN ? koff : (uint64_t)(ks * 32 >> 4);
+                mma_ss_elect(d, ax + aoff, bh + koff, idx, acc);
+                mma_ss_elect(d, ax + aoff, bl + koff, idx, 1u);
+                acc = 1u;
+              }
+              commit_elect(&xempty[xs]);  // X stage and S stage free once these MMAs complete
+              commit_elect(&bempty[b]);
+              if (lane == 0) TC_EV(5, nblk);
+              ++nblk;
+              if (++xs == kSX) {
+                xs = 0;
+                xph ^= 1;
+              }
+              if (++b == kSB) {
+                b = 0;
+                bph ^= 1;
+              }
+              continue;
+            }
             mbar_wait(&opready[o], oph);
             if (lane == 0) TC_EV(7, nblk);
             mbar_wait_warp(&bfull[b], bph);
@@ -434,7 +487,7 @@ __global__ void __launch_bounds__(kThreadsTC, 1)
         }
       }
     }
-  } else if (warp >= kWarpSplit0 && warp < kWarpSplit0 + 4) {
+  } else if (!kIsX1 && warp >= kWarpSplit0 && warp < kWarpSplit0 + 4) {
     // ---------------- split warps: X stage -> (x_hi, x_lo) in tensor memory ----
     // Warp w may only access TMEM lanes 32 (w % 4) .. +31: it owns those tile
     // rows; each thread splits its row's 32 K values.
@@ -859,6 +912,42 @@ static int xs_tc_mode(const int8_t* rexp) {
   return m;
 }
 
+// CNMF_XS_EXACT=0 keeps the three-product kernel for tf32-exact X
+// (comparisons only: the results are bitwise the same).
+static bool xs_exact_enabled() {
+  const char* e = std::getenv("CNMF_XS_EXACT");
+  return !(e && std::string(e) == "0");
+}
+
+// flag |= 1 when some element of X has a nonzero low 13 mantissa bits, i.e.
+// is not exactly a tf32 value (kX1 needs every element exact).
+__global__ void x_tf32_exact_kernel(const float* __restrict__ x, int64_t ldx, int64_t d, int64_t n,
+                                    int* __restrict__ flag) {
+  unsigned any = 0u;
+  const int64_t n4 = n / 4;
+  for (int64_t i = blockIdx.y; i < d; i += gridDim.y) {
+    const float* row = x + i * ldx;
+    for (int64_t c = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; c < n4; c += (int64_t)gridDim.x * blockDim.x) {
+      const uint4 v = __ldg(reinterpret_cast<const uint4*>(row) + c);
+      any |= v.x | v.y | v.z | v.w;
+    }
+    if (blockIdx.x == 0 && threadIdx.x < (n & 3)) any |= __float_as_uint(__ldg(row + 4 * n4 + threadIdx.x));
+  }
+  if (__syncthreads_or((any & 0x1FFFu) != 0u) && threadIdx.x == 0) atomicOr(flag, 1);
+}
+
+void launch_x_tf32_exact(const float* x, int64_t ldx, int64_t d, int64_t n, int* flag, int nsm,
+                         cudaStream_t st) {
+  if ((ldx % 4) != 0 || (reinterpret_cast<uintptr_t>(x) & 15)) {  // outside the kernel's envelope
+    cudaMemsetAsync(flag, 0xFF, sizeof(int), st);
+    return;
+  }
+  note_launches(1);
+  const int gx = (int)std::max<int64_t>(1, std::min<int64_t>((n / 4 + 255) / 256, 8));
+  const int gy = (int)std::max<int64_t>(1, std::min<int64_t>(d, (int64_t)nsm * 8 / gx));
+  x_tf32_exact_kernel<<<dim3(gx, gy), 256, 0, st>>>(x, ldx, d, n, flag);
+}
+
 size_t xs_rexp_bytes(int64_t rows) { return (size_t)((rows + 3) / 4 * 4 + 64); }
 
 void launch_x_rowexp(const float* x, int64_t ldx, int64_t d, int64_t n, int8_t* rexp, int* wide,
@@ -873,12 +962,14 @@ void launch_x_rowexp(const float* x, int64_t ldx, int64_t d, int64_t n, int8_t* 
 // of X, per-column scaling of S): half the tensor-memory operand bytes and
 // half the MMA time of 3xTF32 at the same 22-bit operand precision.
 bool launch_xs_tc(bool tn, const float* x, int64_t ldx, int64_t m, int64_t n, const float* s,
-                  int lp, float* out, float* ws, int nsm, cudaStream_t st, const int8_t* rexp) {
+                  int lp, float* out, float* ws, int nsm, cudaStream_t st, const int8_t* rexp,
+                  bool x_exact) {
   const int L = (lp + 31) & ~31;
   if (L > 128 || (ldx % 4) != 0 || (reinterpret_cast<uintptr_t>(x) & 15)) return false;
   int mode = xs_tc_mode(rexp);
   if (mode == kF16 && L > 96) mode = kTF32;  // two accumulators fit TMEM up to L = 96
-  const bool f16 = mode == kF16, bf9 = mode == kBF9;
+  if (mode == kTF32 && x_exact && xs_exact_enabled()) mode = kX1;
+  const bool f16 = mode == kF16, bf9 = mode == kBF9, x1 = mode == kX1;
   const int LH = (L + 63) & ~63;
   const int64_t rows_out = tn ? n : m, kdim = tn ? m : n;
   const TcPlan p = tc_plan(rows_out, kdim, nsm);
@@ -913,7 +1004,9 @@ bool launch_xs_tc(bool tn, const float* x, int64_t ldx, int64_t m, int64_t n, co
   // X: NN boxes 32 (k) x 128 (rows), 128 B swizzle; TN boxes 128 x 32 (k), unswizzled.
   // S hi / lo: MN-major operand atoms: tf32 32 x 32 boxes, 128 B swizzle with
   // 32 B atoms; fp16 64 x 32 boxes, 128 B swizzle.
-  bool ok = tn ? make_map(&mx, x, m, n, ldx, kBM, kBK, CU_TENSOR_MAP_SWIZZLE_NONE)
+  // kX1 TN: 32 x 32 boxes in the MN-major operand layout (as S).
+  bool ok = tn ? (x1 ? make_map(&mx, x, m, n, ldx, 32, kBK, CU_TENSOR_MAP_SWIZZLE_128B_ATOM_32B)
+                     : make_map(&mx, x, m, n, ldx, kBM, kBK, CU_TENSOR_MAP_SWIZZLE_NONE))
                : make_map(&mx, x, m, n, ldx, kBK, kBM, CU_TENSOR_MAP_SWIZZLE_128B);
   if (bf9)
     ok = ok && make_map(&mh, b16[0], kdim, LH, LH, 64, kBK, CU_TENSOR_MAP_SWIZZLE_128B, true) &&
@@ -946,6 +1039,7 @@ bool launch_xs_tc(bool tn, const float* x, int64_t ldx, int64_t m, int64_t n, co
   case (TN ? 1000 : 0) + LL:                                                                  \
     e = bf9 ? run_tc<TN, LL, kBF9>(mx, mh, ml, m2, a, grid, st)                               \
             : (f16 && LL <= 96) ? run_tc<TN, (LL <= 96 ? LL : 96), kF16>(mx, mh, ml, m2, a, grid, st) \
+            : x1                ? run_tc<TN, LL, kX1>(mx, mh, ml, m2, a, grid, st)           \
                                 : run_tc<TN, LL, kTF32>(mx, mh, ml, m2, a, grid, st);        \
     break;
   switch ((tn ? 1000 : 0) + L) {

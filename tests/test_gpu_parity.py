@@ -135,6 +135,48 @@ def test_xstream_deterministic(ctx):
     assert torch.equal(y1, y2)
 
 
+@pytest.mark.parametrize("d,n,l", [(1000, 1000, 120), (333, 517, 17), (64, 4096, 128),
+                                   (5000, 37, 8), (2049, 1500, 64), (700, 900, 96)])
+def test_xstream_exact_operands(ctx, d, n, l, monkeypatch):
+    """Count data (every element exactly a tf32 value, values up to 2047 and
+    exact zeros) takes the two-product mode (X straight from its TMA stage):
+    bitwise the three-product kernel's result (CNMF_XS_EXACT=0), and within
+    the contraction tolerance of the fp64 product."""
+    rng = np.random.default_rng(d + 3 * n + l)
+    x = rng.poisson(rng.gamma(0.3, 4.0, size=(d, n))).astype(np.float32)
+    x[rng.random((d, n)) < 1e-3] = 2047.0
+    s = rng.standard_normal((n, l)).astype(np.float32)
+    t = rng.standard_normal((d, l)).astype(np.float32)
+    xd, sd, td = dev(x), dev(s), dev(t)
+    out = {}
+    for flag in ("1", "0"):
+        monkeypatch.setenv("CNMF_XS_EXACT", flag)
+        y = torch.empty((d, l), device="cuda")
+        z = torch.empty((n, l), device="cuda")
+        ctx.xs_nn(xd, sd, y)
+        ctx.xs_tn(xd, td, z)
+        out[flag] = (host(y), host(z))
+    x64 = x.astype(np.float64)
+    assert rel_fro(out["1"][0], x64 @ s.astype(np.float64)) < 1e-5
+    assert rel_fro(out["1"][1], x64.T @ t.astype(np.float64)) < 1e-5
+    assert np.array_equal(out["1"][0], out["0"][0])
+    assert np.array_equal(out["1"][1], out["0"][1])
+
+
+def test_xstream_nearly_exact_operands_stay_three_product(ctx):
+    """One element off the tf32 grid sends the whole X down the 3xTF32 path:
+    the result keeps that element's low bits."""
+    rng = np.random.default_rng(77)
+    d, n, l = 512, 640, 32
+    x = rng.integers(0, 50, size=(d, n)).astype(np.float32)
+    x[17, 33] = np.float32(1.0) + np.float32(2.0 ** -20)  # not a tf32 value
+    s = np.zeros((n, l), dtype=np.float32)
+    s[33, :] = 1.0
+    y = torch.empty((d, l), device="cuda")
+    ctx.xs_nn(dev(x), dev(s), y)
+    assert np.all(host(y)[17] == x[17, 33])
+
+
 # --------------------------------------------------------------------- QR --
 @pytest.mark.parametrize("rows,l", [(20, 6), (1000, 30), (10000, 36), (5000, 128)])
 def test_thin_qr_orthonormal_same_span(ctx, rows, l):
