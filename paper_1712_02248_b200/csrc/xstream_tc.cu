@@ -82,11 +82,12 @@ constexpr int kXBytes = kBM * kBK * 4;  // 16 KB per stage (x_hi), same for x_lo
 //          small terms are not rounded against the large ones.
 //   kX1    X exact in tf32 (every element's low 13 mantissa bits zero, e.g.
 //          count data: check_data / launch_x_tf32_exact decide per X): x_lo
-//          = 0, so 3xTF32 reduces to x s_hi + x s_lo -- the same products
-//          into the same accumulator in the same order, bitwise the kTF32
-//          result -- and the MMA reads X straight from the TMA stage (both
-//          operands from shared memory, no split warps, no tensor-memory
-//          operand stores: the limiter of the kTF32 kernel, DESIGN 3.1).
+//          = 0, so 3xTF32 reduces to x s_hi + x s_lo -- the same products,
+//          here summed in two accumulator chains (x s_hi and x s_lo apart,
+//          added in the epilogue) -- and the MMA reads X straight from the
+//          TMA stage (both operands from shared memory, no split warps, no
+//          tensor-memory operand stores: the limiter of the kTF32 kernel,
+//          DESIGN 3.1).
 constexpr int kTF32 = 0, kF16 = 1, kBF9 = 2, kX1 = 3;
 
 // Instruction descriptor: kind::f16 with fp16 A and B, fp32 accumulate,
@@ -162,7 +163,19 @@ template <int L, int kMode = kTF32> struct TcRings {
   // in a second accumulator, so the big one's rounding cannot swamp them;
   // the epilogue folds the two (L <= 96: 2 x 2L accumulator columns + 4
   // operand slots of 32 fill the 512 TMEM columns)
-  static constexpr int kChains = kMode == kF16 ? 2 : (kMode == kBF9 && L <= 96 ? 2 : 1);
+  // kX1 issues x [s_hi | s_lo] as ONE N = L + nmma MMA per k-step: with both
+  // operands in shared memory the MMAs are bound by shared-memory reads (4 KB
+  // of A + 4 KB of B per N = 128 k-step, i.e. the SM's 128 B/clk for its 64
+  // cycles), and the merged MMA reads x once for both products (C4: NN 70.8 ->
+  // 77.6%, TN 71.0 -> 77.4% of HBM).  The two products land in separate
+  // accumulator columns (all 512 TMEM columns at L = 128) and the epilogue
+  // adds them.  -DTC_X1_NOMERGE keeps the two-MMA form (comparisons).
+#ifdef TC_X1_NOMERGE
+  static constexpr bool kMerge = false;
+#else
+  static constexpr bool kMerge = kMode == kX1;
+#endif
+  static constexpr int kChains = kMode == kF16 ? 2 : ((kMode == kBF9 && L <= 96) || kMerge ? 2 : 1);
   static constexpr int kAccCols = kChains * L;
   static constexpr int kAOff = 2 * kAccCols;
   // A operand slot per K-block: tf32 x_hi | x_lo 32 + 32 columns; fp16 two
@@ -173,7 +186,7 @@ template <int L, int kMode = kTF32> struct TcRings {
 #ifdef TC_OPSTAGES
   static constexpr int kOpStages = TC_OPSTAGES;
 #else
-  static constexpr int kOpStages = kOpFit > 4 ? 4 : kOpFit;
+  static constexpr int kOpStages = kOpFit > 4 ? 4 : (kOpFit < 1 ? 1 : kOpFit);  // kX1 uses none
 #endif
   static constexpr uint32_t kTmemNeed = kAOff + (kMode == kX1 ? 0 : kOpStages * kASlot);
   static constexpr uint32_t kTmemCols =
@@ -388,8 +401,14 @@ __global__ void __launch_bounds__(kThreadsTC, 1)
               for (int ks = 0; ks < kBK / 8; ++ks) {
                 const uint64_t koff = (uint64_t)(ks * 1024 >> 4);
                 const uint64_t aoff = kTN ? koff : (uint64_t)(ks * 32 >> 4);
-                mma_ss_elect(d, ax + aoff, bh + koff, idx, acc);
-                mma_ss_elect(d, ax + aoff, bl + koff, idx, 1u);
+                if constexpr (R::kMerge) {
+                  // s_hi's L columns and s_lo's atoms are contiguous in the stage:
+                  // one N = L + nmma MMA, the two products in separate columns
+                  mma_ss_elect(d, ax + aoff, bh + koff, idesc_tf32(L + args.nmma, kTN, true), acc);
+                } else {
+                  mma_ss_elect(d, ax + aoff, bh + koff, idx, acc);
+                  mma_ss_elect(d, ax + aoff, bl + koff, idx, 1u);
+                }
                 acc = 1u;
               }
               commit_elect(&xempty[xs]);  // X stage and S stage free once these MMAs complete
