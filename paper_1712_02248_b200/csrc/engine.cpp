@@ -187,18 +187,22 @@ struct RunStream {
   uint64_t seed = 0;
   uint64_t nwords = 0;
   uint64_t* words = nullptr;
-  uint64_t* pos = nullptr;     // device: next unused raw word
+  uint64_t* pos = nullptr;     // device: [0] next unused raw word, [1] redraws the HALS kernel served itself
   int* flag = nullptr;         // device scratch of the fill kernels
   uint64_t init_end = 0;       // raw words initialize() used (host, after settle)
   uint64_t pos_host = 0;       // host copy of *pos (refreshed by sync_pos / take_pos)
+  uint64_t inline_host = 0;    // host copy of pos[1]
   uint64_t* pos_pinned = nullptr;
   bool pending = true;         // init_end not read back yet
 
   // queues the D2H copy of *pos (read it after the stream syncs)
   void queue_pos() {
-    CK(cudaMemcpyAsync(pos_pinned, pos, sizeof(uint64_t), cudaMemcpyDeviceToHost, c->stream));
+    CK(cudaMemcpyAsync(pos_pinned, pos, 2 * sizeof(uint64_t), cudaMemcpyDeviceToHost, c->stream));
   }
-  void take_pos() { pos_host = *pos_pinned; }
+  void take_pos() {
+    pos_host = pos_pinned[0];
+    inline_host = pos_pinned[1];
+  }
   void sync_pos() {
     queue_pos();
     c->sync();
@@ -244,9 +248,10 @@ RunStream gen_init(cnmf_context* c, uint64_t seed, int64_t d, int64_t n, int k, 
   rs.words = c->ws<uint64_t>("words_run", rs.nwords);
   int* flag = c->ws<int>("iflag", 4);
   rs.flag = flag + 1;
-  rs.pos = c->ws<uint64_t>("iconsumed", 1);
+  rs.pos = c->ws<uint64_t>("iconsumed", 2);
   rs.pos_pinned = c->pos_host;
   CK(cudaMemsetAsync(flag, 0, 2 * sizeof(int), c->stream));
+  CK(cudaMemsetAsync(rs.pos, 0, 2 * sizeof(uint64_t), c->stream));
   CK(cudaMemcpyAsync(rs.pos, &total, sizeof(uint64_t), cudaMemcpyHostToDevice, c->stream));
   gen_words(c, seed, rs.nwords, rs.words, "run", c->stream);
   launch_uniform_init(rs.words, d, n, k, a_cm, b_cm, flag, c->nsm, c->stream);
@@ -265,10 +270,10 @@ RunStream fresh_stream(cnmf_context* c, uint64_t seed, uint64_t reserve) {
   rs.words = c->ws<uint64_t>("words_run", rs.nwords);
   int* flag = c->ws<int>("iflag", 4);
   rs.flag = flag + 1;
-  rs.pos = c->ws<uint64_t>("iconsumed", 1);
+  rs.pos = c->ws<uint64_t>("iconsumed", 2);
   rs.pos_pinned = c->pos_host;
   CK(cudaMemsetAsync(flag, 0, 2 * sizeof(int), c->stream));
-  CK(cudaMemsetAsync(rs.pos, 0, sizeof(uint64_t), c->stream));
+  CK(cudaMemsetAsync(rs.pos, 0, 2 * sizeof(uint64_t), c->stream));
   gen_words(c, seed, rs.nwords, rs.words, "run", c->stream);
   rs.pending = false;
   return rs;
@@ -521,6 +526,10 @@ HalsRun make_hals(cnmf_context* c, int64_t d, int64_t n, int l, int lp, int k,
   s.gsc = c->ws<double>("hals_gsc", (size_t)r.grid * k * k);
   s.wsc = c->ws<double>("hals_wsc", (size_t)r.grid * k * k);
   s.part = c->ws<double>("hals_part", hals_part_doubles(r.grid, lp, k));
+  s.part_ctas = r.grid;
+  s.words = nullptr;  // run_hals hands the run stream to the streaming kernel
+  s.nwords = 0;
+  s.pos = nullptr;
   s.npart = c->ws<double>("hals_npart", (size_t)2 * r.grid);
   s.zpart = c->ws<unsigned>("hals_zpart", (size_t)4 * r.grid + 4);
   s.sharded = 0;
@@ -561,8 +570,14 @@ void run_hals(cnmf_context* c, HalsRun& hr, int normalize_a, double alpha, doubl
   // CNMF_HALS_TRACE: per-launch device time and halt events on stderr
   // (diagnostics; ev[2] / ev[3] bracket each launch)
   static const bool trace = std::getenv("CNMF_HALS_TRACE") != nullptr;
+  uint64_t inline_seen = rs.inline_host;
   for (;;) {
     st.nr0 = hr.nr;
+    // the streaming kernel serves emptied A columns from the run stream itself
+    // (words may have been regenerated longer by a host-side redraw's grow)
+    st.words = reinterpret_cast<const unsigned long long*>(rs.words);
+    st.nwords = rs.nwords;
+    st.pos = reinterpret_cast<unsigned long long*>(rs.pos);
     if (trace) CK(cudaEventRecord(c->ev[2], c->stream));
     if (hr.resident)
       CK(launch_hals_resident(st, normalize_a, alpha, beta, (int)begin, (int)ie, half, col, skip,
@@ -576,6 +591,8 @@ void run_hals(cnmf_context* c, HalsRun& hr, int normalize_a, double alpha, doubl
     rs.queue_pos();
     c->sync();
     rs.take_pos();
+    *redraws += rs.inline_host - inline_seen;
+    inline_seen = rs.inline_host;
     const HaltInfo h = *c->halt_host;
     if (trace)
       std::fprintf(stderr, "hals launch: from iter %lld half %d col %d valid %d: %.1f us, %s kind %d col %d iter %lld\n",

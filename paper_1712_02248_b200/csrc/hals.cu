@@ -730,6 +730,42 @@ __device__ __noinline__ void b_sweep_dmma(const HalsState& S, const double* __re
   }
 }
 
+// An emptied A column served inside the kernel (reinit_column + the norm of
+// normalize_column, solvers.cpp:28-31,40-45,435-436): row i of the column
+// takes the run stream's word pos + i as uniform_positive() * kReinitScale,
+// written unnormalised to S.a; one norm all-reduce follows, which also carries
+// "some word was a rejected draw" (uniform_positive redraws an exact zero,
+// probability 2^-53 per word) as +inf.  Returns 0 when the stream's next d
+// words are not on the device (nothing done), 1 when served (s_red holds the
+// squared norm and its inverse root; *s_pos and S.pos advanced, S.pos[1]
+// counted), 2 when a rejected draw leaves the event to the host (the
+// all-reduce was run: the caller advances ep and nr for 1 and 2).
+__device__ __noinline__ int serve_zero_a(const HalsState& S, int G, int cta, unsigned long long ep,
+                                         unsigned long long nr, int j, int64_t a_lo, int na,
+                                         unsigned long long* s_pos, double* red8, double* s_red) {
+  const unsigned long long p0 = *s_pos;
+  if (p0 + (unsigned long long)S.d + 64ULL > S.nwords) return 0;
+  double n2 = 0.0;
+  bool bad = false;
+  for (int r = threadIdx.x; r < na; r += kThreads) {
+    const double u = (double)(__ldcg(S.words + p0 + (unsigned long long)(a_lo + r)) >> 11) * 0x1.0p-53;
+    bad |= u == 0.0;
+    const double v = u * 1e-3;  // kReinitScale
+    S.a[(int64_t)j * S.d + a_lo + r] = v;
+    n2 = fma(v, v, n2);
+  }
+  const double tot = allreduce_fused(S, G, cta, ep, nr, bad ? INFINITY : n2, red8, s_red);
+  if (!(tot < INFINITY)) return 2;
+  if (threadIdx.x == 0) {
+    *s_pos = p0 + (unsigned long long)S.d;
+    if (cta == 0) {
+      S.pos[0] = p0 + (unsigned long long)S.d;
+      S.pos[1] += 1ULL;
+    }
+  }
+  return 1;
+}
+
 // RPT: A rows per thread; NB: columns per sweep block (16 halves the sweeps'
 // re-reads of A and B -- one pass over all k columns per block -- where the
 // registers allow it; the 6-row instance keeps 8).
@@ -743,6 +779,7 @@ __global__ void __launch_bounds__(kThreads, 1) hals_kernel(const HalsArgs p) {
   __shared__ double s_ginv[128];  // 1 / g_jj (A half)
   __shared__ double s_red[2];     // norm all-reduce: total, 1/sqrt(total)
   __shared__ long long s_prof[21];
+  __shared__ unsigned long long s_rng_pos;
 
   const HalsState& S = p.st;
   const int G = gridDim.x, cta = blockIdx.x, tid = threadIdx.x;
@@ -776,6 +813,10 @@ __global__ void __launch_bounds__(kThreads, 1) hals_kernel(const HalsArgs p) {
   if (S.dense && __ldcg(&S.halt->halted)) return;  // queued behind a halt: no-op
   unsigned long long ep = p.epoch0;
   unsigned long long nr = S.nr0;  // norm all-reduces so far (slot tags)
+  // The run stream's position: read once per launch (before this CTA's first
+  // grid exchange, hence before CTA 0 can have advanced it) and advanced by
+  // every CTA alike at each redraw served in-kernel (serve_zero_a).
+  if (tid == 0) s_rng_pos = (S.words != nullptr && !S.dense) ? __ldcg(S.pos) : 0ULL;
   bool have_g = false, have_w = false;
   // resumed after an emptied column (ZeroA / ZeroB: the redraw changed A or B
   // only, not B-check or A-hat): the halted launch's h, g (A half) or p, w
@@ -909,17 +950,42 @@ __global__ void __launch_bounds__(kThreads, 1) hals_kernel(const HalsArgs p) {
           HALS_PROF(2);
           const double total = allreduce_fused(S, G, cta, ep, nr, nrm, red8, s_red);
           HALS_PROF(3);
-          if (total == 0.0) {  // column emptied: host redraws a_j (solvers.cpp:435)
+          if (total == 0.0) {  // column emptied: a_j is redrawn (solvers.cpp:435)
+            // served in-kernel from the run stream when possible (serve_zero_a)
+            // Opt-in (-DHALS_INKERNEL_REDRAW): correct (the redraw tests pass with
+            // it, 13 instead of 37 launches at C4), but the call's register
+            // constraints slow the steady-state sweep by 4.7% (C4: 108.0 vs
+            // 103.2 ms for iterations 2-100), which cancels the ~130 us per
+            // event the host round trip costs -- so every event halts.
+#ifdef HALS_INKERNEL_REDRAW
+            const int sv = (S.words != nullptr && !S.dense)
+                               ? serve_zero_a(S, G, cta, ep, nr, j, a_lo, na, &s_rng_pos, red8, s_red)
+                               : 0;
+#else
+            const int sv = 0;
+#endif
+            if (sv != 0) {  // it ran one norm all-reduce
+              ++ep;
+              ++nr;
+            }
+            if (sv == 1) {
 #pragma unroll
-            for (int i = 0; i < RPT; ++i) {
-              const int r = tid + kThreads * i;
-              if (i < rpt && r < na) S.a[(int64_t)j * d + a_lo + r] = 0.0;
+              for (int i = 0; i < RPT; ++i) {
+                const int r = tid + kThreads * i;
+                vv[i] = (i < rpt && r < na) ? __ldcg(S.a + (int64_t)j * d + a_lo + r) : 0.0;
+              }
+            } else {  // the host redraws a_j and relaunches at column j + 1
+#pragma unroll
+              for (int i = 0; i < RPT; ++i) {
+                const int r = tid + kThreads * i;
+                if (i < rpt && r < na) S.a[(int64_t)j * d + a_lo + r] = 0.0;
+              }
+              if (cta == 0 && tid == 0) {
+                *S.halt = HaltInfo{1, it + 1, 0, j, kEvZeroA, bcur == S.bold, ep};
+                S.halt->last_nr = nr;
+              }
+              return;
             }
-            if (cta == 0 && tid == 0) {
-              *S.halt = HaltInfo{1, it + 1, 0, j, kEvZeroA, bcur == S.bold, ep};
-              S.halt->last_nr = nr;
-            }
-            return;
           }
           const double inv_nrm = s_red[1];
           double gr[NB];  // row j of g: the later columns' coefficients of a_j
@@ -1241,6 +1307,72 @@ __global__ void compress_factor_kernel(const float* __restrict__ basis, int64_t 
   if (threadIdx.x == 0) out[li * k + c] = li < l ? s : 0.0;
 }
 
+// All columns at once (run start): CTA c takes a contiguous block of rows,
+// streams it in 32-row stages through shared memory (the basis rows and the
+// factor's column segments, both read coalesced exactly once) and keeps a
+// register tile of the lp x k output per thread -- l' = lane + 32 a, column =
+// warp + 8 b: the basis values are conflict-free loads, the factor values
+// warp-wide broadcasts, 4 x 16 fp64 FMAs per 20 shared loads.  Per-CTA
+// partials in `part`, summed over the CTAs in a fixed order by
+// compress_factor_reduce_kernel.  The one-CTA-per-output kernel above read
+// the basis with stride lp once per column: 3.3 ms per factor at C4.
+constexpr int kCfRows = 32, kCfA = 4, kCfB = 16;  // lp <= 128, k <= 128
+__global__ void __launch_bounds__(256) compress_factor_tile_kernel(
+    const float* __restrict__ basis, int64_t rows, int lp, const double* __restrict__ f_cm, int k,
+    int64_t rows_per_cta, double* __restrict__ part) {
+  __shared__ float bs[kCfRows][128];   // row reads / writes walk consecutive words
+  __shared__ double fs[128][kCfRows];  // read as warp-wide broadcasts (48 KB static in all)
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int64_t r0 = (int64_t)blockIdx.x * rows_per_cta, r1 = min(rows, r0 + rows_per_cta);
+  double acc[kCfA][kCfB];
+#pragma unroll
+  for (int a = 0; a < kCfA; ++a)
+#pragma unroll
+    for (int b = 0; b < kCfB; ++b) acc[a][b] = 0.0;
+  for (int64_t s0 = r0; s0 < r1; s0 += kCfRows) {
+    const int nr = (int)min((int64_t)kCfRows, r1 - s0);
+    __syncthreads();
+    for (int e = threadIdx.x; e < kCfRows * 128; e += 256) {
+      const int r = e >> 7, c = e & 127;
+      bs[r][c] = (r < nr && c < lp) ? basis[(s0 + r) * lp + c] : 0.f;
+    }
+    for (int e = threadIdx.x; e < 128 * kCfRows; e += 256) {
+      const int c = e >> 5, r = e & 31;
+      fs[c][r] = (r < nr && c < k) ? f_cm[(int64_t)c * rows + s0 + r] : 0.0;
+    }
+    __syncthreads();
+#pragma unroll 4
+    for (int r = 0; r < kCfRows; ++r) {
+      double bv[kCfA];
+#pragma unroll
+      for (int a = 0; a < kCfA; ++a) bv[a] = (double)bs[r][lane + 32 * a];
+#pragma unroll
+      for (int b = 0; b < kCfB; ++b) {
+        const double fv = fs[warp + 8 * b][r];
+#pragma unroll
+        for (int a = 0; a < kCfA; ++a) acc[a][b] = fma(bv[a], fv, acc[a][b]);
+      }
+    }
+  }
+  double* out = part + (int64_t)blockIdx.x * lp * k;
+#pragma unroll
+  for (int a = 0; a < kCfA; ++a)
+#pragma unroll
+    for (int b = 0; b < kCfB; ++b) {
+      const int li = lane + 32 * a, c = warp + 8 * b;
+      if (li < lp && c < k) out[li * k + c] = acc[a][b];
+    }
+}
+
+__global__ void compress_factor_reduce_kernel(const double* __restrict__ part, int ctas, int lp, int k,
+                                              int l, double* __restrict__ out) {
+  const int e = blockIdx.x * blockDim.x + threadIdx.x;
+  if (e >= lp * k) return;
+  double s = 0.0;
+  for (int c = 0; c < ctas; ++c) s += part[(int64_t)c * lp * k + e];
+  out[e] = e / k < l ? s : 0.0;
+}
+
 __global__ void normalize_column_kernel(double* __restrict__ a_cm, int64_t d, int j) {
   __shared__ double red[32];
   double* col = a_cm + (int64_t)j * d;
@@ -1307,6 +1439,18 @@ cudaError_t launch_hals(const HalsState& st, int normalize_a, double alpha, doub
 }
 
 void launch_compress_factors(const HalsState& st, int which, int column, cudaStream_t s) {
+  if (column < 0 && st.part_ctas > 0 && st.lp <= 128 && st.k <= 128) {
+    const float* basis = which == 0 ? st.lm : st.rt;
+    const int64_t rows = which == 0 ? st.d : st.n;
+    const int64_t per = ((rows + st.part_ctas - 1) / st.part_ctas + kCfRows - 1) / kCfRows * kCfRows;
+    const int ctas = (int)std::max<int64_t>(1, (rows + per - 1) / per);
+    note_launches(2);
+    compress_factor_tile_kernel<<<ctas, 256, 0, s>>>(basis, rows, st.lp, which == 0 ? st.a : st.b, st.k,
+                                                     per, st.part);
+    compress_factor_reduce_kernel<<<(st.lp * st.k + 255) / 256, 256, 0, s>>>(
+        st.part, ctas, st.lp, st.k, st.l, which == 0 ? st.ahat : st.bchk);
+    return;
+  }
   const dim3 grid(st.lp, column >= 0 ? 1 : st.k);
   note_launches(1);
   if (which == 0)

@@ -187,6 +187,15 @@ struct HalsState {
   double* gsc;       // [grid][k*k] per-CTA copy of g = B-check^T B-check (fp64)
   double* wsc;       // [grid][k*k] per-CTA copy of w = A-hat^T A-hat (fp64)
   double* part;      // [grid][lp*k] partial sums
+  int part_ctas;     // CTAs' worth of partial slots in `part` (the run's HALS grid)
+  // The run Rng's raw mt19937_64 words (RunStream, engine.cpp), so that the
+  // streaming kernel serves an emptied A column itself (reinit_column,
+  // solvers.cpp:28-31,435) instead of halting to the host: pos[0] is the next
+  // unused word, pos[1] counts the redraws served in-kernel.  words == null:
+  // every event halts (resident kernel, dense and sharded runs).
+  const unsigned long long* words;
+  unsigned long long nwords;
+  unsigned long long* pos;
   double* npart;     // [2][grid] column-norm partials (by exchange parity)
   unsigned* zpart;   // [grid][4] non-zero-column bitmasks, then [4] the CTA-OR (sharded halt)
   unsigned* bar;     // monotonic grid-barrier arrival counter (reset per run)

@@ -142,96 +142,88 @@ __global__ void gram_reduce_kernel(const double* __restrict__ part, int grid, in
   }
 }
 
-// Upper Cholesky G = R^T R and R^-1 in one CTA (fp64, shared memory).  R is
-// kept in the upper triangle, R^-1 (column-major) in the strict lower
-// triangle: Rinv[i][c] lives at gs[c][i].  flag |= 1 when a pivot is
-// non-positive or below 1e-13 of its original diagonal (Y numerically rank
-// deficient at fp32 resolution).
-// Cholesky G = R^T R (R upper) and R^-1, fp64, one CTA of 128 threads.
-// Right-looking factorisation, one barrier per column: every thread reads
-// the pivot p_j and row j (left unscaled), and the trailing upper triangle
-// takes g_ab -= g_ja g_jb / p_j -- warps over rows a, lanes over columns b
-// (no index division).  Row j is final after step j; R_jb = g_jb / sqrt(p_j)
-// is applied afterwards in one parallel pass.  R^-1 is built column-parallel
-// by back substitution -- column c by thread c, two accumulator chains:
-// Rinv[c][c] = 1/r_c, Rinv[i][c] = -(sum_{q=i+1..c} R[i][q] Rinv[q][c]) / r_i.
-// Fails (flag) if a pivot drops below 1e-13 * its original diagonal (rank
-// deficiency -> Householder fallback).
-__global__ void __launch_bounds__(128) chol_inv_kernel(const double* __restrict__ g, int l,
-                                                       int lp, double* __restrict__ rinv64,
-                                                       float* __restrict__ rinv,
-                                                       int* __restrict__ flag) {
-  // gs: l rows of stride ls (R upper; R^-1 transposed into the lower part),
-  // then diag0, rd, rdi.  The odd row stride keeps the column-parallel back
-  // substitution (thread c walks row c) free of bank conflicts.
+// Cholesky G = R^T R (R upper) and R^-1 in one CTA of 1024 threads (fp64,
+// shared memory), ONE elimination sweep with one barrier per column.
+// Symmetric Gaussian elimination G = L D L^T (L unit lower, D the pivots)
+// gives R = D^1/2 L^T, hence R^-1 = L^-T D^-1/2, and L^-1 is what the same row
+// operations make of the identity.  Row a of the workspace holds both: its
+// strict lower part (columns < a) the row of M -> L^-1 (unit diagonal
+// implicit), its upper part (columns >= a) the row of the trailing G.  At
+// step j every row a > j takes f_a = G[j][a] / p_j times row j off both parts:
+// columns < j of M, M[a][j] = -f_a, columns >= a of G.  A warp owns a row, its
+// lanes the columns (l <= 128: four per lane).
+// Afterwards R^-1[i][c] = M[c][i] / sqrt(p_c).  The previous version ran the
+// factorisation and a right-looking back substitution as two sweeps of l
+// barriers each on 128 threads: 389 us per call at l = 120, 40 us at l = 36
+// (profiles/r02_c4_launch_summary.txt).
+// flag |= 1 when a pivot is non-positive or below 1e-13 of its original
+// diagonal (Y numerically rank deficient at fp32 resolution -> Householder).
+constexpr int kCholThreads = 1024;
+__global__ void __launch_bounds__(kCholThreads) chol_inv_kernel(const double* __restrict__ g, int l,
+                                                                int lp, double* __restrict__ rinv64,
+                                                                float* __restrict__ rinv,
+                                                                int* __restrict__ flag) {
   extern __shared__ double gs[];
   const int ls = l | 1;
   double* diag0 = gs + l * ls;
-  double* rd = diag0 + l;
-  double* rdi = rd + l;
+  double* rdi = diag0 + l;
   const int tid = threadIdx.x, nt = blockDim.x, lane = tid & 31, warp = tid >> 5, nw = nt >> 5;
-  for (int e = tid; e < l * l; e += nt) gs[(e / l) * ls + e % l] = g[(e / l) * lp + e % l];
+  for (int e = tid; e < l * l; e += nt) {
+    const int a = e / l, b = e - a * l;
+    gs[a * ls + b] = b >= a ? g[a * lp + b] : 0.0;
+  }
   for (int e = tid; e < l; e += nt) diag0[e] = g[e * lp + e];
-  __syncthreads();
-  for (int j = 0; j < l; ++j) {
-    const double piv = gs[j * ls + j];
-    if (!(piv > 1e-13 * diag0[j]) || !(piv > 0.0)) {  // uniform across the CTA
-      if (tid == 0) *flag = 1;
-      return;
-    }
-    const double ip = 1.0 / piv;
-    const double* rowj = gs + j * ls;
-    // trailing update, element-parallel: thread (ty, tx) of an 8 x 16 grid
-    // (nt = 128) strides over the rows / columns after j, upper triangle
-    // kept -- the same fma per element as a row walk, without a dependent
-    // chain per row or an index division per element
-    const int ty = tid >> 4, tx = tid & 15;
-    for (int a = j + 1 + ty; a < l; a += 8) {
-      const double f = rowj[a] * ip;
-      double* rowa = gs + a * ls;
-      for (int b = a + ((tx - a) & 15); b < l; b += 16) rowa[b] = fma(-f, rowj[b], rowa[b]);
-    }
-    __syncthreads();
-  }
-  for (int j = tid; j < l; j += nt) {
-    const double pj = gs[j * ls + j];
-    const double ir = 1.0 / sqrt(pj);
-    rdi[j] = ir;
-    rd[j] = pj * ir;
-  }
-  __syncthreads();
-  for (int i = warp; i < l; i += nw)
-    for (int b = i + 1 + lane; b < l; b += 32) gs[i * ls + b] *= rdi[i];
   for (int e = tid; e < lp * lp; e += nt) {  // padding and the lower triangle stay zero
     rinv[e] = 0.f;
     rinv64[e] = 0.0;
   }
   __syncthreads();
-  // R^-1 = X by right-looking back substitution of R X = I, one barrier per
-  // row: B starts as I; at step i (descending) row i of X is final,
-  // X[i][c] = B[i][c] / r_i (X[i][i] = 1 / r_i), and every B[a][c] with
-  // a < i <= c takes -R[a][i] X[i][c] (element-parallel on the 8 x 16 thread
-  // grid).  B[a][c] (a < c) lives transposed in gs's strict lower triangle,
-  // gs[c][a].  The column-per-thread back substitution this replaces was a
-  // serial O(l^2) chain per thread (36.6 us per call at l = 36).
-  for (int c = 1 + (tid >> 4); c < l; c += 8)
-    for (int a = tid & 15; a < c; a += 16) gs[c * ls + a] = 0.0;
-  __syncthreads();
-  {
-    const int ty = tid >> 4, tx = tid & 15;
-    for (int i = l - 1; i > 0; --i) {
-      const double di = rdi[i];
-      for (int c = i + tx; c < l; c += 16) {
-        const double xic = c == i ? di : gs[c * ls + i] * di;
-        for (int a = ty; a < i; a += 8) gs[c * ls + a] = fma(-gs[a * ls + i], xic, gs[c * ls + a]);
-      }
-      __syncthreads();
+  for (int j = 0; j < l; ++j) {
+    const double* rowj = gs + j * ls;
+    const double piv = rowj[j];
+    if (!(piv > 1e-13 * diag0[j]) || !(piv > 0.0)) {  // uniform across the CTA
+      if (tid == 0) *flag = 1;
+      return;
     }
+    const double ip = __drcp_rn(piv);
+    // lane t owns columns t + 32 u of every row: row j's values are loaded
+    // once per step (M[j][j] = 1 is implicit -- its slot holds the pivot),
+    // and a row a > j updates columns <= j (M) and >= a (G).  Two rows per
+    // pass, loads before stores, so the shared-memory latencies overlap.
+    double vj[4];
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+      const int b = lane + 32 * u;
+      vj[u] = b == j ? 1.0 : (b < l ? rowj[b] : 0.0);
+    }
+    for (int a0 = j + 1 + warp; a0 < l; a0 += 2 * nw) {
+      const int a1 = a0 + nw;
+      const bool two = a1 < l;
+      double* row0 = gs + a0 * ls;
+      double* row1 = gs + (two ? a1 : a0) * ls;
+      const double f0 = rowj[a0] * ip, f1 = two ? rowj[a1] * ip : 0.0;
+      double v0[4], v1[4];
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+        const int b = lane + 32 * u;
+        v0[u] = (b <= j || (b >= a0 && b < l)) ? row0[b] : 0.0;
+        v1[u] = (two && (b <= j || (b >= a1 && b < l))) ? row1[b] : 0.0;
+      }
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+        const int b = lane + 32 * u;
+        if (b <= j || (b >= a0 && b < l)) row0[b] = fma(-f0, vj[u], v0[u]);
+        if (two && (b <= j || (b >= a1 && b < l))) row1[b] = fma(-f1, vj[u], v1[u]);
+      }
+    }
+    __syncthreads();
   }
+  for (int j = tid; j < l; j += nt) rdi[j] = 1.0 / sqrt(gs[j * ls + j]);
+  __syncthreads();
   for (int e = tid; e < l * l; e += nt) {
-    const int i = e / l, c = e - i * l;
-    if (c < i) continue;
-    const double v = c == i ? rdi[i] : gs[c * ls + i] * rdi[i];
+    const int c = e / l, i = e - c * l;  // consecutive threads walk row c of M
+    if (i > c) continue;
+    const double v = i == c ? rdi[c] : gs[c * ls + i] * rdi[c];
     rinv[i * lp + c] = (float)v;
     rinv64[i * lp + c] = v;
   }
@@ -452,7 +444,7 @@ void chol_inv(int l, int lp, const QrWs& w, cudaStream_t st) {
   static std::atomic<unsigned> attr{0u};
   smem_attr_once(attr, (const void*)(chol_inv_kernel), (int)(sizeof(double) * (128 * 129 + 3 * 128)));
   note_launches(1);
-  chol_inv_kernel<<<1, 128, smem, st>>>(w.g, l, lp, w.rinv64, w.rinv, w.flag);
+  chol_inv_kernel<<<1, kCholThreads, smem, st>>>(w.g, l, lp, w.rinv64, w.rinv, w.flag);
 }
 
 }  // namespace
