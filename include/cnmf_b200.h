@@ -238,6 +238,12 @@ cnmf_status cnmf_xs_nn(cnmf_context* ctx, const float* x, uint64_t d, uint64_t n
                        const float* s, uint64_t l, float* y);
 cnmf_status cnmf_xs_tn(cnmf_context* ctx, const float* x, uint64_t d, uint64_t n, uint64_t ldx,
                        const float* t, uint64_t l, float* z);
+/* The range finder's fp64-grade contractions (matrix.cpp:105-140 with fp32 X,
+ * fp64 accumulation): out (fp64, d x l for NN, n x l for TN) = X s or X^T s,
+ * s fp32 (widened exactly), l a multiple of 16.  use_dmma = 0: the exact
+ * int8-sliced tensor-core kernel (l <= 80); 1: the FP64 tensor-core kernel. */
+cnmf_status cnmf_xs_exact(cnmf_context* ctx, const float* x, uint64_t d, uint64_t n, uint64_t ldx,
+                          const float* s, uint64_t l, int transpose, int use_dmma, double* out);
 
 /* Instrumentation (bench harness). */
 /* Total device kernels this library has launched in this process. */

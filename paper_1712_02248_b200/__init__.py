@@ -115,7 +115,7 @@ EXPORTS = [
     "cnmf_solver_config_validate", "cnmf_run", "cnmf_run_device", "cnmf_gaussian_sketch",
     "cnmf_initialize", "cnmf_powered_range_finder", "cnmf_build_projectors", "cnmf_compress",
     "cnmf_compress_factors", "cnmf_fasthals_rp_steps", "cnmf_reconstruction_error",
-    "cnmf_thin_qr", "cnmf_xs_nn", "cnmf_xs_tn", "cnmf_synth_x", "cnmf_launch_count",
+    "cnmf_thin_qr", "cnmf_xs_nn", "cnmf_xs_tn", "cnmf_xs_exact", "cnmf_synth_x", "cnmf_launch_count",
     "cnmf_time_xstream", "cnmf_shard_begin", "cnmf_nccl_unique_id", "cnmf_context_create_sharded",
     "cnmf_run_sharded_device", "cnmf_estimate_cost", "cnmf_generate_synthetic",
     "cnmf_pairwise_distortion", "cnmf_run_csr", "cnmf_context_create_hosted",
@@ -172,6 +172,7 @@ def load_library(path: str = LIB_PATH):
     L.cnmf_thin_qr.argtypes = [vp, fp, u64, u64, fp]
     L.cnmf_xs_nn.argtypes = [vp, fp, u64, u64, u64, fp, u64, fp]
     L.cnmf_xs_tn.argtypes = [vp, fp, u64, u64, u64, fp, u64, fp]
+    L.cnmf_xs_exact.argtypes = [vp, fp, u64, u64, u64, fp, u64, C.c_int, C.c_int, vp]
     L.cnmf_synth_x.argtypes = [vp, u64, u64, u64, C.c_int, C.c_int, C.c_double, u64, u64, u64,
                                u64, fp]
     L.cnmf_launch_count.restype = u64
@@ -498,6 +499,15 @@ class Context:
         d, n = x.shape
         self._check(self.L.cnmf_xs_tn(self.h, _ptr(x), d, n, x.stride(0), _ptr(t), t.shape[1],
                                       _ptr(out)))
+        return out
+
+    def xs_exact(self, x, s, out, transpose=False, dmma=False):
+        """out (float64) = X s or X^T s with fp64-grade accumulation: the int8-sliced
+        tensor-core kernel, or the FP64 tensor-core kernel (dmma=True)."""
+        _torch_ready()
+        d, n = x.shape
+        self._check(self.L.cnmf_xs_exact(self.h, _ptr(x), d, n, x.stride(0), _ptr(s), s.shape[1],
+                                         int(transpose), int(dmma), _ptr(out)))
         return out
 
     def time_xstream(self, x, l, transpose, iters=10) -> float:

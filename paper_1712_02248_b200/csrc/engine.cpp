@@ -64,6 +64,8 @@ struct cnmf_context {
   void* nccl = nullptr;           // ncclComm_t of a sharded context
   double last_kappa = 0.0;        // condition estimate of the last run's sketch (0: not taken)
   int last_rf64 = 0;              // the last build_projectors ran the fp64 range finder
+  const int* rf_sx = nullptr;     // X's row / column scale exponents: the fp64 range finder's
+                                  // contractions run on the integer tensor cores (xstream_i8.cu)
   cnmf_host_collectives hosted{}; // host-staged collectives of a sharded context (tests)
   std::vector<char> host_stage;
   std::map<std::string, bool> filled;  // device copies uploaded once (jump polynomials)
@@ -409,6 +411,12 @@ static RfMode rf_mode() {  // read per call (tests switch it)
   return RfMode::kAuto;
 }
 constexpr double kRfKappaMax = 1e3;  // see DESIGN.md section 4 (measured per config)
+// CNMF_RF64=dmma keeps the fp64 range finder's contractions on the FP64 tensor
+// cores (dense.cu xs64) instead of the exact int8-sliced kernel (comparisons)
+static bool rf64_dmma() {
+  const char* e = std::getenv("CNMF_RF64");
+  return e && std::string(e) == "dmma";
+}
 
 // range_finder_impl (compression.cpp:23-42) in fp64 arithmetic; `omega` is
 // the fp32 sketch (op_cols x lp), `basis` the fp32 result (rows x lp).
@@ -423,7 +431,12 @@ int range_finder64(cnmf_context* c, const XView& X, int q, int lp, uint64_t w, b
   double* zq = c->ws<double>("rf64_zq_" + tag, cols * lp);
   double* xs = c->ws<double>("rf64_xs_" + tag, xs64_ws_doubles(X.d, X.n, lp, c->nsm));
   void* qws = c->ws<char>("qr64_ws_" + tag, qr64_ws_bytes(std::max(X.d, X.n), lp, c->nsm));
+  void* i8ws = c->rf_sx ? c->ws<char>("rf64_i8_" + tag, xs_i8_ws_bytes(X.d, X.n, lp, c->nsm)) : nullptr;
   auto apply = [&](const double* s, double* out, bool tn) {
+    // exact-accumulation int8 slices on the tensor cores; shapes outside its
+    // envelope (lp > 96) keep the FP64 DMMA contraction
+    if (c->rf_sx && launch_xs_i8(tn, X.x, X.ldx, X.d, X.n, s, lp, out, i8ws, c->rf_sx, c->nsm, st))
+      return;
     if (tn) launch_xs64_tn(X.x, X.ldx, X.d, X.n, s, lp, out, xs, c->nsm, st);
     else launch_xs64_nn(X.x, X.ldx, X.d, X.n, s, lp, out, xs, c->nsm, st);
   };
@@ -474,6 +487,17 @@ int build_projectors_dev(cnmf_context* c, const XView& X, int q, int lp, uint64_
       std::fprintf(stderr, "range finder: kappa(X Omega) ~ %.3g -> %s\n", kappa, use64 ? "fp64" : "tc");
   }
   c->last_rf64 = use64 ? 1 : 0;
+  c->rf_sx = nullptr;
+  if (use64 && xs_i8_supported(lp) && (X.ldx % 4) == 0 && !rf64_dmma()) {
+    // the int8-sliced contractions scale each row / column of X by a power of
+    // two: one row-wise and one column-wise read of X for the exponents, then
+    // the side stream (forked at the top) waits for them too
+    int* sx = c->ws<int>("rf_sx", xs_i8_sx_ints(X.d, X.n));
+    launch_xs_i8_prepare_x(X.x, X.ldx, X.d, X.n, sx, c->nsm, c->stream);
+    CK(cudaEventRecord(c->fork, c->stream));
+    CK(cudaStreamWaitEvent(c->side, c->fork, 0));
+    c->rf_sx = sx;
+  }
   auto rf = use64 ? range_finder64 : range_finder;
   passes += rf(c, X, q, lp, w, false, omega_l, lm, "L", c->stream, canonical, first_done);
   passes += rf(c, X, q, lp, w, true, omega_r, rt, "R", c->side, canonical, false);
@@ -1675,6 +1699,33 @@ cnmf_status cnmf_xs_tn(cnmf_context* c, const float* x, uint64_t d, uint64_t n, 
 }
 
 uint64_t cnmf_launch_count(void) { return launch_count(); }
+
+cnmf_status cnmf_xs_exact(cnmf_context* c, const float* x, uint64_t d, uint64_t n, uint64_t ldx,
+                          const float* s, uint64_t l, int transpose, int use_dmma, double* out) {
+  return guarded(c, [&] {
+    require_shapes(1, l);
+    if (l % 16 != 0) throw Fail(CNMF_ERR_UNSUPPORTED, "cnmf_xs_exact: l must be a multiple of 16");
+    const int lp = (int)l;
+    const XView X = prepare_x(c, x, (int64_t)d, (int64_t)n, (int64_t)ldx);
+    const int64_t in_rows = transpose ? (int64_t)d : (int64_t)n;
+    double* s64 = c->ws<double>("xe_s", in_rows * lp);
+    launch_f32_to_f64(s, in_rows * lp, s64, c->nsm, c->stream);
+    bool done = false;
+    if (!use_dmma) {
+      int* sx = c->ws<int>("xe_sx", xs_i8_sx_ints(X.d, X.n));
+      void* ws = c->ws<char>("xe_ws", xs_i8_ws_bytes(X.d, X.n, lp, c->nsm));
+      launch_xs_i8_prepare_x(X.x, X.ldx, X.d, X.n, sx, c->nsm, c->stream);
+      done = launch_xs_i8(transpose != 0, X.x, X.ldx, X.d, X.n, s64, lp, out, ws, sx, c->nsm, c->stream);
+      if (!done) throw Fail(CNMF_ERR_UNSUPPORTED, "cnmf_xs_exact: shape outside the int8 kernel's envelope");
+    } else {
+      double* ws = c->ws<double>("xe_ws64", xs64_ws_doubles(X.d, X.n, lp, c->nsm));
+      if (transpose) launch_xs64_tn(X.x, X.ldx, X.d, X.n, s64, lp, out, ws, c->nsm, c->stream);
+      else launch_xs64_nn(X.x, X.ldx, X.d, X.n, s64, lp, out, ws, c->nsm, c->stream);
+    }
+    CK(cudaGetLastError());
+    c->sync();
+  });
+}
 
 cnmf_status cnmf_time_xstream(cnmf_context* c, const float* x, uint64_t d, uint64_t n,
                               uint64_t ldx, uint64_t l, int transpose, int iters,

@@ -248,6 +248,18 @@ void launch_normalize_column(double* a_cm, int64_t d, int j, cudaStream_t s);
 // out (rows x lp fp64, row-major) = X S (NN, rows = m) or X^T T (TN, rows = n);
 // s: K x lp fp64 row-major (lp a multiple of 16, <= 128); ws: xs64_ws_doubles.
 size_t xs64_ws_doubles(int64_t m, int64_t n, int lp, int nsm);
+// ---- xstream_i8.cu: the same contractions (fp32 X, fp64 S and output) with
+// exact int32 accumulation on the integer tensor cores (Ozaki-style int8
+// digit slices).  sx: launch_xs_i8_prepare_x's row / column scale exponents
+// of X (xs_i8_sx_ints ints).  launch_xs_i8 returns false outside its envelope
+// (lp a multiple of 16, <= 80; 16-byte aligned rows).
+bool xs_i8_supported(int lp);
+size_t xs_i8_sx_ints(int64_t d, int64_t n);
+size_t xs_i8_ws_bytes(int64_t m, int64_t n, int lp, int nsm);
+void launch_xs_i8_prepare_x(const float* x, int64_t ldx, int64_t d, int64_t n, int* sx, int nsm,
+                            cudaStream_t st);
+bool launch_xs_i8(bool tn, const float* x, int64_t ldx, int64_t m, int64_t n, const double* s,
+                  int lp, double* out, void* ws, const int* sx, int nsm, cudaStream_t st);
 // halt (nullable): a device flag; when set the launch is a no-op (products
 // queued behind a halted dense HALS sweep, engine.cpp run_dense_hals).
 void launch_xs64_nn(const float* x, int64_t ldx, int64_t m, int64_t n, const double* s, int lp,

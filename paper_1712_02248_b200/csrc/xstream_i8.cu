@@ -1,0 +1,655 @@
+// xstream_i8.cu -- the X-streaming contractions with EXACT accumulation on the
+// integer tensor cores (tcgen05.mma.kind::i8, int32 accumulators in TMEM): the
+// range finder's arithmetic when the sketch is ill conditioned (engine.cpp
+// range_finder64; any fp32-accumulated tensor-core contraction
+// there moves the C3 trajectory ~1e-4, so those ten passes ran as fp64 DMMA at
+// ~11 ms each).
+//
+// Reference call sites: dense matmul NN (proj/src/matrix.cpp:105-116) and TN
+// (129-140) from range_finder_impl (proj/src/compression.cpp:23-42).
+//   NN  Y (m x lp) = X (m x n) S (n x lp)      TN  Z (n x lp) = X^T T (m x lp)
+// with X fp32 and S, Y fp64.
+//
+// Ozaki-style slicing: every row of the A operand (a row of X for NN, a
+// column of X for TN) is scaled by an exact power of two 2^sx so that its
+// largest entry is below 2^26, rounded to an integer and written in balanced
+// base-128 digits q = d0 2^21 + d1 2^14 + d2 2^7 + d3, |d| <= 64 (int8); every
+// column of S likewise (2^ss, digits e0..e3).  The digit products are exact
+// in int32 (|d e| <= 4096, chains up to 131072 long), so
+//   sum_k q_x q_s = sum_{s,t} 2^(7 (6 - s - t)) P_st,  P_st = sum_k d_s e_t,
+// and the pairs with s + t <= 4 are kept (13 of 16: the top digits carry only
+// five bits, so class 4 is still 2^-23 of a typical product -- measured 1.1e-7
+// without it; the dropped classes 5 and 6 are below 2^-30 and, the digits
+// being balanced, unbiased).  Pairs of equal s + t share an accumulator, so
+// there are five accumulators of NP columns; the epilogue combines them in
+// fp64,
+//   V = (((W0 128 + W1) 128 + W2) 128 + W3) 128 + W4,   y = V 2^(14 - sx - ss).  What is lost is the operands' rounding to 26 bits
+// below their row / column maximum -- fp32's own 24 bits for entries within
+// 4x of the maximum, an absolute 2^-27 of the maximum below that -- never the
+// accumulation.
+//
+// Kernel: persistent CTAs over (128-row tile, K-split) units as xstream_tc.cu.
+// Warps 0-3 epilogue, 4 X TMA (16 KB boxes of 32 k), 5 MMA issue, 6-13 split
+// (two sets of four: set p slices the blocks of parity p -- X stage -> 32
+// words of digits per row -> tcgen05.st, half the 3xTF32 store volume), 14 S
+// TMA (the pre-sliced S^T digits, K-major SWIZZLE_128B rows of 128 k: one
+// stage serves four X blocks).  Per block thirteen K = 32 MMAs, A from tensor
+// memory; layouts checked by tools/tc_i8_check.cu.
+#include <cuda.h>
+#include <cudaTypedefs.h>
+
+#include <algorithm>
+#include <cstdio>
+#include <cstdlib>
+#include <string>
+
+#include "common.cuh"
+#include "kernels.h"
+#include "tc_common.cuh"
+
+namespace cnmf {
+
+namespace {
+
+using namespace tc;
+
+constexpr int kBM = 128;   // output rows per unit (MMA M)
+constexpr int kBK = 32;    // k per X block (one kind::i8 MMA step)
+constexpr int kBKB = 128;  // k per S stage (one swizzle row)
+constexpr int kSX = 6, kSO = 3, kSB = 2;
+constexpr int kThreadsI8 = 480;
+constexpr int kWarpTMA = 4, kWarpMMA = 5, kWarpSplit0 = 6, kWarpBTMA = 14;
+constexpr int kXBytes = kBM * kBK * 4;
+constexpr int kDigits = 4;
+constexpr int kClasses = 5;  // accumulators: digit pairs (s, t) with s + t = 0 .. 4
+constexpr int kQBits = 26;  // |q| < 2^26
+
+struct I8Args {
+  int64_t rows_out, kdim, kchunk;
+  int ntiles, nsplit, lp, np;  // np: lp rounded up to 16 (MMA N)
+  double* out;                 // [nsplit][rows_out][lp]
+  const int* sx;               // per output row: its A-operand row's scale exponent
+  const double* cscale;        // per column of S: 2^-ss
+};
+
+// kind::i8: D s32, A and B signed 8-bit, both K-major, M = 128
+__host__ __device__ constexpr uint32_t idesc_i8(int n) {
+  return (2u << 4) | (1u << 7) | (1u << 10) | ((uint32_t)(n >> 3) << 17) | ((128u >> 4) << 24);
+}
+__device__ __forceinline__ void mma_i8_ts_elect(uint32_t d_tmem, uint32_t a_tmem, uint64_t b_desc,
+                                                uint32_t idesc, uint32_t accumulate) {
+  asm volatile(
+      "{\n\t.reg .pred p, e;\n\t"
+      "setp.ne.b32 p, %4, 0;\n\t"
+      "{\n\t.reg .u32 ln;\n\tmov.u32 ln, %%laneid;\n\tsetp.eq.u32 e, ln, 0;\n\t}\n\t"
+      "@e tcgen05.mma.cta_group::1.kind::i8 [%0], [%1], %2, %3, p;\n\t}" ::"r"(d_tmem),
+      "r"(a_tmem), "l"(b_desc), "r"(idesc), "r"(accumulate)
+      : "memory");
+}
+__device__ __forceinline__ float4 lds128(uint32_t a) {
+  float4 v;
+  asm volatile("ld.shared.v4.f32 {%0,%1,%2,%3}, [%4];"
+               : "=f"(v.x), "=f"(v.y), "=f"(v.z), "=f"(v.w)
+               : "r"(a)
+               : "memory");
+  return v;
+}
+__device__ __forceinline__ float lds32(uint32_t a) {
+  float v;
+  asm volatile("ld.shared.f32 %0, [%1];" : "=f"(v) : "r"(a) : "memory");
+  return v;
+}
+__device__ __forceinline__ float exp2i_f(int e) { return __int_as_float((127 + e) << 23); }
+__device__ __forceinline__ double exp2i_d(int e) {
+  return __longlong_as_double((long long)(1023 + e) << 52);
+}
+__device__ __forceinline__ void tmem_ld16(uint32_t taddr, uint32_t (&h)[16]) {
+  asm volatile(
+      "tcgen05.ld.sync.aligned.32x32b.x16.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15}, [%16];"
+      : "=r"(h[0]), "=r"(h[1]), "=r"(h[2]), "=r"(h[3]), "=r"(h[4]), "=r"(h[5]), "=r"(h[6]), "=r"(h[7]),
+        "=r"(h[8]), "=r"(h[9]), "=r"(h[10]), "=r"(h[11]), "=r"(h[12]), "=r"(h[13]), "=r"(h[14]),
+        "=r"(h[15])
+      : "r"(taddr));
+}
+
+// Balanced base-128 digits of round(v), |v| < 2^26, with fp32 arithmetic only
+// (the integer pipe is the scarce one): x + 1.5 2^23 rounds x to an integer
+// (to nearest even) and leaves it, in two's complement, in the low mantissa
+// bits of the sum.  w[s] carries digit s in its low byte.
+__device__ __forceinline__ void digits4(float v, uint32_t (&w)[kDigits]) {
+  constexpr float kM = 12582912.f;
+  const float w0 = fmaf(v, 0x1.0p-21f, kM);
+  const float t0 = w0 - kM;
+  const float r1 = fmaf(-t0, 0x1.0p21f, v);
+  const float w1 = fmaf(r1, 0x1.0p-14f, kM);
+  const float t1 = w1 - kM;
+  const float r2 = fmaf(-t1, 0x1.0p14f, r1);
+  const float w2 = fmaf(r2, 0x1.0p-7f, kM);
+  const float t2 = w2 - kM;
+  const float r3 = fmaf(-t2, 0x1.0p7f, r2);
+  const float w3 = r3 + kM;
+  w[0] = __float_as_uint(w0);
+  w[1] = __float_as_uint(w1);
+  w[2] = __float_as_uint(w2);
+  w[3] = __float_as_uint(w3);
+}
+
+template <bool kTN>
+__global__ void __launch_bounds__(kThreadsI8, 1)
+    xs_i8_kernel(const __grid_constant__ CUtensorMap map_x, const __grid_constant__ CUtensorMap map_b,
+                 const I8Args args) {
+  extern __shared__ __align__(1024) uint8_t smem_raw[];
+  const uint32_t sbase = (smem_u32(smem_raw) + 1023u) & ~1023u;
+  __shared__ __align__(8) uint64_t xfull[kSX], xempty[kSX], opready[kSO], opempty[kSO];
+  __shared__ __align__(8) uint64_t bfull[kSB], bempty[kSB], acc_full, acc_empty;
+  __shared__ uint32_t tmem_base;
+
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int np = args.np;
+  const uint32_t slice_bytes = (uint32_t)np * 128u;      // one digit of S^T, 128 k
+  const uint32_t b_bytes = kDigits * slice_bytes;
+  const uint32_t a_off = (uint32_t)(kClasses * np);       // tensor memory: the accumulators, then A slots
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < kSX; ++s) {
+      mbar_init(&xfull[s], 1);
+      mbar_init(&xempty[s], 4);
+    }
+    for (int s = 0; s < kSO; ++s) {
+      mbar_init(&opready[s], 4);
+      mbar_init(&opempty[s], 1);
+    }
+    for (int s = 0; s < kSB; ++s) {
+      mbar_init(&bfull[s], 1);
+      mbar_init(&bempty[s], 1);
+    }
+    mbar_init(&acc_full, 1);
+    mbar_init(&acc_empty, 4);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+  }
+  if (warp == kWarpMMA) {
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], 512;" ::"r"(
+        smem_u32(&tmem_base)));
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+  }
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem = tmem_base;
+
+  const int units = args.ntiles * args.nsplit;
+  auto x_addr = [&](int s) { return sbase + s * kXBytes; };
+  auto b_addr = [&](int b) { return sbase + kSX * kXBytes + (uint32_t)b * b_bytes; };
+  auto unit_k = [&](int u, int64_t& k0, int64_t& k1) {
+    const int split = u / args.ntiles;
+    k0 = (int64_t)split * args.kchunk;
+    k1 = min(args.kdim, k0 + args.kchunk);
+  };
+  auto tma = [&](uint32_t dst, const CUtensorMap* map, uint64_t* bar, int c0, int c1) {
+    asm volatile(
+        "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes"
+        " [%0], [%1, {%3, %4}], [%2];" ::"r"(dst),
+        "l"(reinterpret_cast<uint64_t>(map)), "r"(smem_u32(bar)), "r"(c0), "r"(c1)
+        : "memory");
+  };
+
+  if (warp == kWarpTMA) {
+    // ---------------- X producer: NN 32 (k) x 128 (rows) boxes, SWIZZLE_128B;
+    // TN 128 (columns of X) x 32 (k) boxes, unswizzled ----------------
+    if (lane == 0) {
+      int s = 0;
+      uint32_t ph = 0;
+      for (int u = blockIdx.x; u < units; u += gridDim.x) {
+        int64_t k0, k1;
+        unit_k(u, k0, k1);
+        const int row0 = (u % args.ntiles) * kBM;
+        for (int64_t kk = k0; kk < k1; kk += kBK) {
+          mbar_wait(&xempty[s], ph ^ 1);
+          mbar_expect_tx(&xfull[s], kXBytes);
+          if (!kTN) tma(x_addr(s), &map_x, &xfull[s], (int)kk, row0);
+          else tma(x_addr(s), &map_x, &xfull[s], row0, (int)kk);
+          if (++s == kSX) {
+            s = 0;
+            ph ^= 1;
+          }
+        }
+      }
+    }
+  } else if (warp == kWarpBTMA) {
+    // ---------------- S producer: four digit slices of np rows x 128 k -------
+    if (lane == 0) {
+      int b = 0;
+      uint32_t ph = 0;
+      for (int u = blockIdx.x; u < units; u += gridDim.x) {
+        int64_t k0, k1;
+        unit_k(u, k0, k1);
+        for (int64_t kb = k0; kb < k1; kb += kBKB) {
+          mbar_wait(&bempty[b], ph ^ 1);
+          mbar_expect_tx(&bfull[b], b_bytes);
+#pragma unroll
+          for (int t = 0; t < kDigits; ++t)
+            tma(b_addr(b) + t * slice_bytes, &map_b, &bfull[b], (int)kb, t * np);
+          if (++b == kSB) {
+            b = 0;
+            ph ^= 1;
+          }
+        }
+      }
+    }
+  } else if (warp == kWarpMMA) {
+    // ---------------- MMA issuer: thirteen digit-pair products per block -----
+    const uint32_t idesc = idesc_i8(np);
+    int o = 0, b = 0;
+    uint32_t oph = 0, bph = 0, aph = 0;
+    for (int u = blockIdx.x; u < units; u += gridDim.x) {
+      int64_t k0, k1;
+      unit_k(u, k0, k1);
+      mbar_wait_warp(&acc_empty, aph ^ 1);
+      tc_fence_after();
+      uint32_t fresh = (1u << kClasses) - 1u;  // bit w: accumulator w not yet written in this unit
+      int sub = 0;            // X block within the S stage
+      for (int64_t kk = k0; kk < k1; kk += kBK) {
+        mbar_wait_warp(&opready[o], oph);
+        if (sub == 0) mbar_wait_warp(&bfull[b], bph);
+        tc_fence_after();
+        const uint32_t a0 = tmem + a_off + 32u * (uint32_t)o;
+        const uint64_t bd = smem_desc(b_addr(b) + 32u * (uint32_t)sub, 16, 1024, 2);
+#pragma unroll
+        for (int w = 0; w < kClasses; ++w) {
+#pragma unroll
+          for (int s = (w < kDigits ? 0 : w - kDigits + 1); s <= (w < kDigits ? w : kDigits - 1); ++s) {
+            const int t = w - s;
+            mma_i8_ts_elect(tmem + (uint32_t)(w * np), a0 + 8u * s,
+                            bd + (uint64_t)((t * slice_bytes) >> 4), idesc, ((fresh >> w) & 1u) ^ 1u);
+            fresh &= ~(1u << w);
+          }
+        }
+        commit_elect(&opempty[o]);
+        if (++o == kSO) {
+          o = 0;
+          oph ^= 1;
+        }
+        if (++sub == kBKB / kBK || kk + kBK >= k1) {
+          commit_elect(&bempty[b]);
+          sub = 0;
+          if (++b == kSB) {
+            b = 0;
+            bph ^= 1;
+          }
+        }
+      }
+      commit_elect(&acc_full);
+      aph ^= 1;
+    }
+  } else if (warp >= kWarpSplit0 && warp < kWarpSplit0 + 8) {
+    // ---------------- split warps: X stage -> four int8 digits in tensor memory
+    // Warp w may only access TMEM lanes 32 (w % 4) .. +31; the two sets of
+    // four warps take alternate blocks.
+    const int q = warp & 3, set = (warp - kWarpSplit0) >> 2;
+    const int r = 32 * q + lane;
+    int s = 0, o = 0, nblk = 0;
+    uint32_t xph = 0, oph = 0;
+    for (int u = blockIdx.x; u < units; u += gridDim.x) {
+      int64_t k0, k1;
+      unit_k(u, k0, k1);
+      const int64_t row = (int64_t)(u % args.ntiles) * kBM + r;
+      const float scale = exp2i_f(row < args.rows_out ? __ldg(args.sx + row) : 0);
+      for (int64_t kk = k0; kk < k1; kk += kBK, ++nblk) {
+        if ((nblk & 1) == set) {
+          mbar_wait_warp(&xfull[s], xph);
+          float v[32];
+          if (!kTN) {
+            const uint32_t rowa = x_addr(s) + r * 128;
+#pragma unroll
+            for (int c = 0; c < 8; ++c) {
+              const float4 t = lds128(rowa + ((c ^ (r & 7)) << 4));
+              v[4 * c] = t.x;
+              v[4 * c + 1] = t.y;
+              v[4 * c + 2] = t.z;
+              v[4 * c + 3] = t.w;
+            }
+          } else {
+#pragma unroll
+            for (int kq = 0; kq < 32; ++kq) v[kq] = lds32(x_addr(s) + kq * (kBM * 4) + r * 4);
+          }
+          uint32_t pk[32];  // pk[8 s + j]: digit s of k = 4 j .. 4 j + 3
+#pragma unroll
+          for (int j = 0; j < 8; ++j) {
+            uint32_t w[4][kDigits];
+#pragma unroll
+            for (int e = 0; e < 4; ++e) digits4(v[4 * j + e] * scale, w[e]);
+#pragma unroll
+            for (int d = 0; d < kDigits; ++d) {
+              const uint32_t lo = __byte_perm(w[0][d], w[1][d], 0x0040);
+              const uint32_t hi = __byte_perm(w[2][d], w[3][d], 0x0040);
+              pk[8 * d + j] = __byte_perm(lo, hi, 0x5410);
+            }
+          }
+          mbar_wait_warp(&opempty[o], oph ^ 1);
+          tc_fence_after();
+          tmem_st32(tmem + ((uint32_t)(32 * q) << 16) + a_off + 32u * (uint32_t)o, pk);
+          asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
+          tc_fence_before();
+          __syncwarp();
+          // released only after the values were consumed (see xstream_tc.cu)
+          if (lane == 0) {
+            mbar_arrive(&opready[o]);
+            mbar_arrive(&xempty[s]);
+          }
+        }
+        if (++s == kSX) {
+          s = 0;
+          xph ^= 1;
+        }
+        if (++o == kSO) {
+          o = 0;
+          oph ^= 1;
+        }
+      }
+    }
+  } else if (warp < 4) {
+    // ---------------- epilogue: the five int32 accumulators -> fp64 ----------
+    const int q = warp;
+    uint32_t aph = 0;
+    for (int u = blockIdx.x; u < units; u += gridDim.x) {
+      const int tile = u % args.ntiles, split = u / args.ntiles;
+      const int64_t row = (int64_t)tile * kBM + 32 * q + lane;
+      const bool ok = row < args.rows_out;
+      const double rs = exp2i_d(7 * (6 - (kClasses - 1)) - (ok ? __ldg(args.sx + row) : 0));
+      double* dst = args.out + ((int64_t)split * args.rows_out + (ok ? row : 0)) * args.lp;
+      mbar_wait_warp(&acc_full, aph);
+      tc_fence_after();
+      const uint32_t base = tmem + ((uint32_t)(32 * q) << 16);
+      for (int c0 = 0; c0 < np; c0 += 16) {
+        uint32_t h[kClasses][16];
+#pragma unroll
+        for (int w = 0; w < kClasses; ++w) tmem_ld16(base + (uint32_t)(w * np + c0), h[w]);
+        asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+        if (ok) {
+#pragma unroll
+          for (int j = 0; j < 16; j += 2) {
+            if (c0 + j < args.lp) {  // lp is even (a multiple of 16)
+              double y[2];
+#pragma unroll
+              for (int e = 0; e < 2; ++e) {
+                double vsum = (double)(int)h[0][j + e];
+#pragma unroll
+                for (int w = 1; w < kClasses; ++w) vsum = fma(vsum, 128.0, (double)(int)h[w][j + e]);
+                y[e] = vsum * rs * __ldg(args.cscale + c0 + j + e);
+              }
+              *reinterpret_cast<double2*>(dst + c0 + j) = make_double2(y[0], y[1]);
+            }
+          }
+        }
+      }
+      tc_fence_before();
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&acc_empty);
+      aph ^= 1;
+    }
+  }
+  tc_fence_before();
+  __syncthreads();
+  if (warp == kWarpMMA) {
+    tc_fence_after();
+    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 512;" ::"r"(tmem));
+  }
+}
+
+// ---- operand preparation ---------------------------------------------------
+// Scale exponent of a row / column with maximum magnitude mx: the largest sx
+// with mx 2^sx < 2^26, clamped to fp32's exponent range.
+__device__ __forceinline__ int scale_exp(float mx) {
+  if (!(mx > 0.f)) return 0;
+  int e;
+  frexpf(mx, &e);  // mx = f 2^e, f in [0.5, 1)
+  return max(-126, min(126, kQBits - e));
+}
+
+// rows of X: one warp per row
+__global__ void x_rowsx_kernel(const float* __restrict__ x, int64_t ldx, int64_t d, int64_t n,
+                               int* __restrict__ sx) {
+  const int lane = threadIdx.x & 31;
+  const int64_t warps = (int64_t)gridDim.x * (blockDim.x >> 5);
+  for (int64_t i = blockIdx.x * (int64_t)(blockDim.x >> 5) + (threadIdx.x >> 5); i < d; i += warps) {
+    const float* row = x + i * ldx;
+    float mx = 0.f;
+    for (int64_t j = lane; j < n; j += 32) mx = fmaxf(mx, fabsf(__ldg(row + j)));
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, o));
+    if (lane == 0) sx[i] = scale_exp(mx);
+  }
+}
+// columns of X: a CTA walks a block of rows, a thread its columns; maxima as
+// float bits (non-negative floats order like unsigned ints)
+__global__ void x_colmax_kernel(const float* __restrict__ x, int64_t ldx, int64_t d, int64_t n,
+                                int64_t rows_per_cta, unsigned* __restrict__ cmax) {
+  const int64_t r0 = (int64_t)blockIdx.y * rows_per_cta, r1 = min(d, r0 + rows_per_cta);
+  for (int64_t j = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; j < n;
+       j += (int64_t)gridDim.x * blockDim.x) {
+    float mx = 0.f;
+    for (int64_t i = r0; i < r1; ++i) mx = fmaxf(mx, fabsf(__ldg(x + i * ldx + j)));
+    atomicMax(cmax + j, __float_as_uint(mx));
+  }
+}
+__global__ void colmax_to_sx_kernel(const unsigned* __restrict__ cmax, int64_t n, int* __restrict__ sx) {
+  for (int64_t j = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; j < n;
+       j += (int64_t)gridDim.x * blockDim.x)
+    sx[j] = scale_exp(__uint_as_float(cmax[j]));
+}
+
+// S (kdim x lp fp64): column maxima (as bits of |s|), then the digits of
+// round(s 2^ss) written K-major: out[(t * np + c) * kpad + k].
+__global__ void s64_colmax_kernel(const double* __restrict__ s, int64_t rows, int lp,
+                                  unsigned long long* __restrict__ cmax) {
+  const int c = threadIdx.x;
+  if (c >= lp) return;
+  double m = 0.0;
+  for (int64_t r = blockIdx.x; r < rows; r += gridDim.x) m = fmax(m, fabs(s[r * lp + c]));
+  atomicMax(cmax + c, (unsigned long long)__double_as_longlong(m));
+}
+__device__ __forceinline__ int s_scale_exp(unsigned long long bits) {
+  const double mx = __longlong_as_double((long long)bits);
+  if (!(mx > 0.0)) return 0;
+  int e;
+  frexp(mx, &e);
+  return max(-900, min(900, kQBits - e));
+}
+__global__ void s64_slice_kernel(const double* __restrict__ s, int64_t kdim, int lp, int np,
+                                 int64_t kpad, const unsigned long long* __restrict__ cmax,
+                                 uint32_t* __restrict__ out, double* __restrict__ cscale) {
+  const int64_t kw = kpad / 4;  // words per row of S^T
+  for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < kw * np;
+       e += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t w = e / np;
+    const int c = (int)(e - w * np);
+    uint32_t word[kDigits] = {0u, 0u, 0u, 0u};
+    if (c < lp) {
+      const int ss = s_scale_exp(cmax[c]);
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+        const int64_t k = 4 * w + u;
+        long long qv = k < kdim ? llrint(scalbn(s[k * lp + c], ss)) : 0;
+#pragma unroll
+        for (int t = kDigits - 1; t > 0; --t) {
+          const long long dg = ((qv + 64) & 127) - 64;
+          word[t] |= (uint32_t)((int)dg & 0xFF) << (8 * u);
+          qv = (qv - dg) >> 7;
+        }
+        word[0] |= (uint32_t)((int)qv & 0xFF) << (8 * u);
+      }
+    }
+#pragma unroll
+    for (int t = 0; t < kDigits; ++t) out[((int64_t)t * np + c) * kw + w] = word[t];
+  }
+  if (blockIdx.x == 0)
+    for (int c = threadIdx.x; c < np; c += blockDim.x)
+      cscale[c] = c < lp ? scalbn(1.0, -s_scale_exp(cmax[c])) : 0.0;
+}
+
+__global__ void i8_split_reduce_kernel(const double2* __restrict__ part, int splits, int64_t total2,
+                                       double2* __restrict__ out) {
+  for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < total2;
+       e += (int64_t)gridDim.x * blockDim.x) {
+    double2 acc = part[e];
+    for (int s = 1; s < splits; ++s) {
+      const double2 v = part[(int64_t)s * total2 + e];
+      acc.x += v.x;
+      acc.y += v.y;
+    }
+    out[e] = acc;
+  }
+}
+
+struct I8Plan {
+  int ntiles, nsplit;
+  int64_t kchunk;
+};
+// K-split count minimising the persistent grid's makespan (as tc_plan), in
+// units of 128-k S stages; chains stay below 131072 (int32 accumulators).
+I8Plan i8_plan(int64_t rows_out, int64_t kdim, int nsm) {
+  I8Plan p;
+  p.ntiles = (int)((rows_out + kBM - 1) / kBM);
+  const int64_t kb = (kdim + kBKB - 1) / kBKB;
+  const int64_t min_ns = (kb + 1023) / 1024;
+  int64_t best_ns = min_ns;
+  double best = 1e300;
+  for (int64_t ns = min_ns; ns <= std::min<int64_t>(64, kb); ++ns) {
+    const int64_t per = (kb + ns - 1) / ns;
+    const int64_t units = (int64_t)p.ntiles * ((kb + per - 1) / per);
+    const int64_t rounds = (units + nsm - 1) / nsm;
+    const double cost = (double)rounds * (double)per * 4.0 +
+                        (ns > 1 ? (double)ns * (double)p.ntiles / nsm * 9.0 : 0.0) + 4.0 * rounds;
+    if (cost < best - 1e-9) {
+      best = cost;
+      best_ns = ns;
+    }
+  }
+  const int64_t per = (kb + best_ns - 1) / best_ns;
+  p.kchunk = per * kBKB;
+  p.nsplit = (int)((kdim + p.kchunk - 1) / p.kchunk);
+  return p;
+}
+
+bool make_map_u8(CUtensorMap* m, const void* base, int64_t rows, int64_t cols, int box_cols,
+                 int box_rows) {
+  auto fn = encode_fn();
+  if (!fn) return false;
+  const cuuint64_t dims[2] = {(cuuint64_t)cols, (cuuint64_t)rows};
+  const cuuint64_t strides[1] = {(cuuint64_t)cols};
+  const cuuint32_t box[2] = {(cuuint32_t)box_cols, (cuuint32_t)box_rows};
+  const cuuint32_t estr[2] = {1, 1};
+  return fn(m, CU_TENSOR_MAP_DATA_TYPE_UINT8, 2, const_cast<void*>(base), dims, strides, box, estr,
+            CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+            CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+}
+
+size_t align256(size_t b) { return (b + 255) & ~size_t(255); }
+
+}  // namespace
+
+// five accumulators of lp columns and three 32-column A slots fill the 512 TMEM columns at lp = 80
+bool xs_i8_supported(int lp) { return lp % 16 == 0 && lp <= 80; }
+
+size_t xs_i8_sx_ints(int64_t d, int64_t n) { return (size_t)(d + n) + 2 * (size_t)n + 64; }
+
+// Scale exponents of X's rows (sx[0 .. d)) and columns (sx[d .. d + n)); the
+// tail of the buffer is scratch.  One row-wise and one column-wise read of X.
+void launch_xs_i8_prepare_x(const float* x, int64_t ldx, int64_t d, int64_t n, int* sx, int nsm,
+                            cudaStream_t st) {
+  unsigned* cmax = reinterpret_cast<unsigned*>(sx + d + n);
+  cudaMemsetAsync(cmax, 0, sizeof(unsigned) * n, st);
+  note_launches(3);
+  x_rowsx_kernel<<<(int)std::max<int64_t>(1, std::min<int64_t>((d + 7) / 8, (int64_t)nsm * 16)), 256, 0,
+                   st>>>(x, ldx, d, n, sx);
+  const int gx = (int)std::max<int64_t>(1, std::min<int64_t>((n + 255) / 256, 64));
+  const int gy = (int)std::max<int64_t>(1, std::min<int64_t>(d, (int64_t)nsm * 8 / gx));
+  const int64_t per = (d + gy - 1) / gy;
+  x_colmax_kernel<<<dim3(gx, gy), 256, 0, st>>>(x, ldx, d, n, per, cmax);
+  colmax_to_sx_kernel<<<(int)std::max<int64_t>(1, std::min<int64_t>((n + 255) / 256, nsm * 4)), 256, 0,
+                        st>>>(cmax, n, sx + d);
+}
+
+size_t xs_i8_ws_bytes(int64_t m, int64_t n, int lp, int nsm) {
+  const int np = lp;
+  const int64_t kmax = std::max(m, n);
+  const int64_t kpad = (kmax + kBKB - 1) / kBKB * kBKB;
+  const I8Plan a = i8_plan(m, n, nsm), b = i8_plan(n, m, nsm);
+  const size_t parts = sizeof(double) * (size_t)std::max<int64_t>((int64_t)a.nsplit * m * lp,
+                                                                   (int64_t)b.nsplit * n * lp);
+  return align256((size_t)kDigits * np * kpad) + align256(sizeof(unsigned long long) * 128) +
+         align256(sizeof(double) * 128) + align256(parts) + 1024;
+}
+
+// y = X s (NN, out m x lp) or z = X^T t (TN, out n x lp): s / t is kdim x lp
+// fp64 row-major, out fp64; sx from launch_xs_i8_prepare_x.  False when the
+// shape is outside the kernel's envelope (the caller keeps the fp64 DMMA path).
+bool launch_xs_i8(bool tn, const float* x, int64_t ldx, int64_t m, int64_t n, const double* s,
+                  int lp, double* out, void* ws, const int* sx, int nsm, cudaStream_t st) {
+  if (!xs_i8_supported(lp) || (ldx % 4) != 0 || (reinterpret_cast<uintptr_t>(x) & 15)) return false;
+  const int np = lp;
+  const int64_t rows_out = tn ? n : m, kdim = tn ? m : n;
+  const int64_t kpad = (kdim + kBKB - 1) / kBKB * kBKB;
+  const I8Plan p = i8_plan(rows_out, kdim, nsm);
+  uint8_t* base = static_cast<uint8_t*>(ws);
+  uint8_t* st_digits = base;
+  base += align256((size_t)kDigits * np * ((std::max(m, n) + kBKB - 1) / kBKB * kBKB));
+  unsigned long long* cmax = reinterpret_cast<unsigned long long*>(base);
+  base += align256(sizeof(unsigned long long) * 128);
+  double* cscale = reinterpret_cast<double*>(base);
+  base += align256(sizeof(double) * 128);
+  double* parts = reinterpret_cast<double*>(base);
+
+  if (cudaMemsetAsync(cmax, 0, sizeof(unsigned long long) * 128, st) != cudaSuccess) return false;
+  note_launches(2);
+  s64_colmax_kernel<<<(int)std::max<int64_t>(1, std::min<int64_t>(kdim, (int64_t)nsm * 4)), 128, 0, st>>>(
+      s, kdim, lp, cmax);
+  s64_slice_kernel<<<(int)std::min<int64_t>((kpad / 4 * np + 255) / 256, (int64_t)nsm * 16), 256, 0, st>>>(
+      s, kdim, lp, np, kpad, cmax, reinterpret_cast<uint32_t*>(st_digits), cscale);
+
+  CUtensorMap mx, mb;
+  bool ok = tn ? make_map(&mx, x, m, n, ldx, kBM, kBK, CU_TENSOR_MAP_SWIZZLE_NONE)
+               : make_map(&mx, x, m, n, ldx, kBK, kBM, CU_TENSOR_MAP_SWIZZLE_128B);
+  ok = ok && make_map_u8(&mb, st_digits, (int64_t)kDigits * np, kpad, kBKB, np);
+  if (!ok) {
+    std::fprintf(stderr, "xs_i8: tensor map encode failed (tn %d, m %lld, n %lld, lp %d)\n", (int)tn,
+                 (long long)m, (long long)n, lp);
+    return false;
+  }
+  I8Args a;
+  a.rows_out = rows_out;
+  a.kdim = kdim;
+  a.kchunk = p.kchunk;
+  a.ntiles = p.ntiles;
+  a.nsplit = p.nsplit;
+  a.lp = lp;
+  a.np = np;
+  a.out = p.nsplit > 1 ? parts : out;
+  a.sx = tn ? sx + m : sx;
+  a.cscale = cscale;
+  const int units = p.ntiles * p.nsplit;
+  const int grid = std::min(units, nsm);
+  const int smem = kSX * kXBytes + kSB * kDigits * np * 128 + 1024;
+  static std::atomic<unsigned> attr_nn{0u}, attr_tn{0u};
+  note_launches(1);
+  if (tn) {
+    smem_attr_once(attr_tn, (const void*)(xs_i8_kernel<true>), kSX * kXBytes + kSB * kDigits * 96 * 128 + 1024);
+    xs_i8_kernel<true><<<grid, kThreadsI8, smem, st>>>(mx, mb, a);
+  } else {
+    smem_attr_once(attr_nn, (const void*)(xs_i8_kernel<false>), kSX * kXBytes + kSB * kDigits * 96 * 128 + 1024);
+    xs_i8_kernel<false><<<grid, kThreadsI8, smem, st>>>(mx, mb, a);
+  }
+  if (const cudaError_t e = cudaGetLastError(); e != cudaSuccess) {
+    std::fprintf(stderr, "xs_i8: launch failed: %s\n", cudaGetErrorString(e));
+    return false;
+  }
+  if (p.nsplit > 1) {
+    const int64_t total2 = rows_out * lp / 2;
+    note_launches(1);
+    i8_split_reduce_kernel<<<(int)std::min<int64_t>((total2 + 255) / 256, (int64_t)nsm * 8), 256, 0, st>>>(
+        reinterpret_cast<const double2*>(parts), p.nsplit, total2, reinterpret_cast<double2*>(out));
+  }
+  return true;
+}
+
+}  // namespace cnmf

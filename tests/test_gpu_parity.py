@@ -166,6 +166,38 @@ def test_xstream_exact_operands(ctx, d, n, l, monkeypatch):
         assert rel_fro(out["1"][i], out["0"][i].astype(np.float64)) < 2e-6
 
 
+@pytest.mark.parametrize("d,n,l", [(1000, 1000, 32), (333, 517, 16), (129, 4100, 80),
+                                   (5000, 37, 48), (2049, 1500, 80), (700, 900, 64)])
+def test_xstream_int8_sliced_contraction(ctx, d, n, l):
+    """The fp64 range finder's contractions on the integer tensor cores
+    (xstream_i8.cu: int8 digit slices, exact int32 accumulation): NN and TN
+    against the fp64 product.  The only error is the operands' rounding to 26
+    bits below their row / column maximum (unbiased, round to nearest): data
+    whose entries lie within a small factor of their row and column maxima
+    (low-rank products, the BASELINE generators) come out at 1-2e-8 of the
+    product's norm, a wide dynamic range inside rows / columns (here a
+    Gamma(2) row scale, 5% exact zeros) at 1e-7 -- the tensor cores'
+    fp32-accumulated 3xTF32 sits at 1e-6 with a structured error."""
+    rng = np.random.default_rng(7 * d + n + l)
+    lowrank = (rng.random((d, 12)) @ rng.random((12, n))).astype(np.float32)
+    wide = (rng.random((d, n)) * rng.gamma(2.0, 1.0, size=(d, 1))).astype(np.float32)
+    wide[rng.random((d, n)) < 0.05] = 0.0
+    s = rng.standard_normal((n, l)).astype(np.float32)
+    t = rng.standard_normal((d, l)).astype(np.float32)
+    sd, td = dev(s), dev(t)
+    for x, tol in ((lowrank, 3e-8), (wide, 1.5e-7)):
+        xd = dev(x)
+        x64 = x.astype(np.float64)
+        for tn, op, ref, rows in ((False, sd, x64 @ s.astype(np.float64), d),
+                                  (True, td, x64.T @ t.astype(np.float64), n)):
+            got = torch.empty((rows, l), dtype=torch.float64, device="cuda")
+            ctx.xs_exact(xd, op, got, transpose=tn)
+            dm = torch.empty((rows, l), dtype=torch.float64, device="cuda")
+            ctx.xs_exact(xd, op, dm, transpose=tn, dmma=True)
+            assert rel_fro(host(dm), ref) < 1e-14
+            assert rel_fro(host(got), ref) < tol, (tn, tol, rel_fro(host(got), ref))
+
+
 def test_xstream_nearly_exact_operands_stay_three_product(ctx):
     """One element off the tf32 grid sends the whole X down the 3xTF32 path:
     the result keeps that element's low bits."""

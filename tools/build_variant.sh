@@ -6,7 +6,7 @@ set -e
 R=/root/repo/paper_1712_02248_b200
 O=$R/build_var/$1
 mkdir -p $O
-for f in rng xstream xstream_tc recon_tc qr hals hals_resident metrics synth dense sparse; do
+for f in rng xstream xstream_tc xstream_i8 recon_tc qr hals hals_resident metrics synth dense sparse; do
   /usr/local/cuda/bin/nvcc -std=c++17 -O3 -lineinfo -gencode arch=compute_100a,code=sm_100a -Xcompiler -fPIC \
     --expt-relaxed-constexpr $2 -c $R/csrc/$f.cu -o $O/$f.o 2>&1 | grep -E " error" || true &
 done

@@ -16,6 +16,6 @@ python tools/launch_summary.py gpurun_out/r02_c4_launches.csv > gpurun_out/r02_c
 bash tools/hals_ncu.sh c4 30 hals_c4 > gpurun_out/hals_ncu.log 2>&1; echo "hals ncu rc=$?"
 timeout 900 $NCU --set full --import-source on --clock-control none -k regex:xs_tc_kernel -s 2 -c 2 -o gpurun_out/xs_c4 -f python bench.py --steps 1 --warmup 0 --no-cpu-baseline --no-e2e > gpurun_out/xs_ncu.log 2>&1; echo "xs ncu rc=$?"
 $NCU -i gpurun_out/xs_c4.ncu-rep --page details --csv > gpurun_out/xs_c4_details.csv 2>/dev/null; rm -f gpurun_out/xs_c4.ncu-rep
-timeout 900 $NCU --set full --clock-control none -k regex:xs64_kernel -s 1 -c 2 -o gpurun_out/xs64_c3 -f python bench.py --config c3 --steps 1 --warmup 0 --no-cpu-baseline --no-e2e > gpurun_out/xs64_ncu.log 2>&1; echo "xs64 ncu rc=$?"
+timeout 900 $NCU --set full --clock-control none -k regex:xs_i8_kernel -s 1 -c 2 -o gpurun_out/xs64_c3 -f python bench.py --config c3 --steps 1 --warmup 0 --no-cpu-baseline --no-e2e > gpurun_out/xs64_ncu.log 2>&1; echo "xs64 ncu rc=$?"
 $NCU -i gpurun_out/xs64_c3.ncu-rep --page details --csv > gpurun_out/xs64_c3_details.csv 2>/dev/null; rm -f gpurun_out/xs64_c3.ncu-rep
 ls -la gpurun_out; du -sh gpurun_out
