@@ -15,7 +15,7 @@
 // largest entry is below 2^26, rounded to an integer and written in balanced
 // base-128 digits q = d0 2^21 + d1 2^14 + d2 2^7 + d3, |d| <= 64 (int8); every
 // column of S likewise (2^ss, digits e0..e3).  The digit products are exact
-// in int32 (|d e| <= 4096, chains up to 131072 long), so
+// in int32 (|d e| <= 4096, K-split chains of at most 65536), so
 //   sum_k q_x q_s = sum_{s,t} 2^(7 (6 - s - t)) P_st,  P_st = sum_k d_s e_t,
 // and the pairs with s + t <= 4 are kept (13 of 16: the top digits carry only
 // five bits, so class 4 is still 2^-23 of a typical product -- measured 1.1e-7
@@ -61,7 +61,11 @@ constexpr int kThreadsI8 = 480;
 constexpr int kWarpTMA = 4, kWarpMMA = 5, kWarpSplit0 = 6, kWarpBTMA = 14;
 constexpr int kXBytes = kBM * kBK * 4;
 constexpr int kDigits = 4;
+#ifdef I8_CLASSES  // experiments
+constexpr int kClasses = I8_CLASSES;
+#else
 constexpr int kClasses = 5;  // accumulators: digit pairs (s, t) with s + t = 0 .. 4
+#endif
 constexpr int kQBits = 26;  // |q| < 2^26
 
 struct I8Args {
@@ -317,7 +321,12 @@ __global__ void __launch_bounds__(kThreadsI8, 1)
           for (int j = 0; j < 8; ++j) {
             uint32_t w[4][kDigits];
 #pragma unroll
+#ifdef I8_FAKE_SPLIT  // timing experiment: no digit arithmetic (wrong results)
+            for (int e = 0; e < 4; ++e)
+              for (int d = 0; d < kDigits; ++d) w[e][d] = __float_as_uint(v[4 * j + e] * scale) >> (8 * d);
+#else
             for (int e = 0; e < 4; ++e) digits4(v[4 * j + e] * scale, w[e]);
+#endif
 #pragma unroll
             for (int d = 0; d < kDigits; ++d) {
               const uint32_t lo = __byte_perm(w[0][d], w[1][d], 0x0040);
@@ -506,12 +515,13 @@ struct I8Plan {
   int64_t kchunk;
 };
 // K-split count minimising the persistent grid's makespan (as tc_plan), in
-// units of 128-k S stages; chains stay below 131072 (int32 accumulators).
+// units of 128-k S stages; chains stay at or below 65536 k: an accumulator
+// takes up to four digit pairs of |d e| <= 4096 per k, 2^30 at most.
 I8Plan i8_plan(int64_t rows_out, int64_t kdim, int nsm) {
   I8Plan p;
   p.ntiles = (int)((rows_out + kBM - 1) / kBM);
   const int64_t kb = (kdim + kBKB - 1) / kBKB;
-  const int64_t min_ns = (kb + 1023) / 1024;
+  const int64_t min_ns = (kb + 511) / 512;
   int64_t best_ns = min_ns;
   double best = 1e300;
   for (int64_t ns = min_ns; ns <= std::min<int64_t>(64, kb); ++ns) {
