@@ -241,7 +241,9 @@ cnmf_status cnmf_xs_tn(cnmf_context* ctx, const float* x, uint64_t d, uint64_t n
 /* The range finder's fp64-grade contractions (matrix.cpp:105-140 with fp32 X,
  * fp64 accumulation): out (fp64, d x l for NN, n x l for TN) = X s or X^T s,
  * s fp32 (widened exactly), l a multiple of 16.  use_dmma = 0: the exact
- * int8-sliced tensor-core kernel (l <= 80); 1: the FP64 tensor-core kernel. */
+ * int8-sliced tensor-core kernel; 1: the FP64 tensor-core kernel; 2: the
+ * int8-sliced kernel's configuration for an X of integers below 8192 (the
+ * caller vouches for that: exact X digits, 40 bits of s). */
 cnmf_status cnmf_xs_exact(cnmf_context* ctx, const float* x, uint64_t d, uint64_t n, uint64_t ldx,
                           const float* s, uint64_t l, int transpose, int use_dmma, double* out);
 

@@ -501,13 +501,15 @@ class Context:
                                       _ptr(out)))
         return out
 
-    def xs_exact(self, x, s, out, transpose=False, dmma=False):
+    def xs_exact(self, x, s, out, transpose=False, dmma=False, small_int=False):
         """out (float64) = X s or X^T s with fp64-grade accumulation: the int8-sliced
-        tensor-core kernel, or the FP64 tensor-core kernel (dmma=True)."""
+        tensor-core kernel (small_int: its configuration for an X of integers below
+        8192), or the FP64 tensor-core kernel (dmma=True)."""
         _torch_ready()
         d, n = x.shape
         self._check(self.L.cnmf_xs_exact(self.h, _ptr(x), d, n, x.stride(0), _ptr(s), s.shape[1],
-                                         int(transpose), int(dmma), _ptr(out)))
+                                         int(transpose), 1 if dmma else (2 if small_int else 0),
+                                         _ptr(out)))
         return out
 
     def time_xstream(self, x, l, transpose, iters=10) -> float:

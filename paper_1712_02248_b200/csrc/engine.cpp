@@ -295,6 +295,9 @@ struct XView {
   const CsrView* sp = nullptr;
   const int8_t* rexp = nullptr;  // per-row exponents: the contractions' fp16 path
   bool tf32_exact = false;       // every element exactly a tf32 value (count data): kX1 path
+  bool integral = false;         // every element an integer below 2^26: the int8-sliced
+                                 // contractions need no row / column scaling
+  bool small_int = false;        // ... and below 8192: exact in two int8 digits
 };
 
 // The X contractions' fp16 hi/lo path (xstream_tc.cu) is opt-in:
@@ -504,6 +507,53 @@ int build_projectors_dev(cnmf_context* c, const XView& X, int q, int lp, uint64_
   CK(cudaEventRecord(c->join, c->side));
   CK(cudaStreamWaitEvent(c->stream, c->join, 0));
   return passes;
+}
+
+// The compressed views X-hat^T = X^T L (n x lp) and X-check = X R^T (d x lp)
+// with exact accumulation (xstream_i8.cu) whenever the shape allows: the
+// full-size C4 golden showed the tensor cores' fp32-accumulated views moving
+// the early FastHALS-RP trajectory 1.4e-3 from the reference's (fp64-
+// accumulated views rounded to fp32: 1.3e-5), as they did the
+// range finder at C3.  CNMF_VIEWS=tc keeps the 3xTF32 kernel, =dmma the FP64
+// tensor cores.  False: nothing written, the caller runs the 3xTF32 kernel.
+bool exact_views(cnmf_context* c, const XView& X, const float* lm, const float* rt, int lp,
+                 float* xht, float* xc) {
+  const int64_t d = X.d, n = X.n;
+  const char* vmode = std::getenv("CNMF_VIEWS");
+  if (X.sp || n <= 0 || (vmode && std::string(vmode) == "tc") || !xs_i8_supported(lp) ||
+      (X.ldx % 4) != 0)
+    return false;
+  double* s64 = c->ws<double>("v64_s", (size_t)std::max(d, n) * lp);
+  double* o64 = c->ws<double>("v64_o", (size_t)std::max(d, n) * lp);
+  if (vmode && std::string(vmode) == "dmma") {
+    double* w64 = c->ws<double>("v64_ws", xs64_ws_doubles(d, n, lp, c->nsm));
+    launch_f32_to_f64(lm, d * lp, s64, c->nsm, c->stream);
+    launch_xs64_tn(X.x, X.ldx, d, n, s64, lp, o64, w64, c->nsm, c->stream);
+    launch_f64_to_f32(o64, n * lp, xht, c->nsm, c->stream);
+    launch_f32_to_f64(rt, n * lp, s64, c->nsm, c->stream);
+    launch_xs64_nn(X.x, X.ldx, d, n, s64, lp, o64, w64, c->nsm, c->stream);
+    launch_f64_to_f32(o64, d * lp, xc, c->nsm, c->stream);
+    return true;
+  }
+  // X's scale exponents: the range finder's if it took this path, zeros for
+  // an X of integers (count data), else one row-wise and one column-wise read
+  const int* sx = X.small_int ? nullptr : c->rf_sx;
+  if (!sx) {
+    int* buf = c->ws<int>("rf_sx", xs_i8_sx_ints(d, n));
+    if (X.integral) CK(cudaMemsetAsync(buf, 0, sizeof(int) * (d + n), c->stream));
+    else launch_xs_i8_prepare_x(X.x, X.ldx, d, n, buf, c->nsm, c->stream);
+    sx = buf;
+  }
+  void* i8ws = c->ws<char>("v_i8_ws", xs_i8_ws_bytes(d, n, lp, c->nsm));
+  launch_f32_to_f64(lm, d * lp, s64, c->nsm, c->stream);
+  if (!launch_xs_i8(true, X.x, X.ldx, d, n, s64, lp, o64, i8ws, sx, c->nsm, c->stream, X.small_int))
+    return false;
+  launch_f64_to_f32(o64, n * lp, xht, c->nsm, c->stream);
+  launch_f32_to_f64(rt, n * lp, s64, c->nsm, c->stream);
+  if (!launch_xs_i8(false, X.x, X.ldx, d, n, s64, lp, o64, i8ws, sx, c->nsm, c->stream, X.small_int))
+    throw Fail(CNMF_ERR_CUDA, "int8-sliced contraction failed after its first view");
+  launch_f64_to_f32(o64, d * lp, xc, c->nsm, c->stream);
+  return true;
 }
 
 // ------------------------------------------------------------------ HALS ----
@@ -988,7 +1038,7 @@ void run_device_impl(cnmf_context* c, const XView& X0, const cnmf_solver_config&
     int* flag = c->ws<int>("cflag", 4);
     double* nrm = c->ws<double>("xnorm", 1);
     void* ws = c->ws<char>("metrics_ws", metrics_ws_bytes(d, n, c->nsm));
-    CK(cudaMemsetAsync(flag, 0, 3 * sizeof(int), c->stream));
+    CK(cudaMemsetAsync(flag, 0, 4 * sizeof(int), c->stream));
     // the same read of X yields the row exponents of the contractions' fp16
     // path (flag[1]: some row spans more than 2^30, keep 3xTF32) and whether
     // X is exact in tf32 (flag[2] == 0: the contractions' two-product mode)
@@ -999,15 +1049,18 @@ void run_device_impl(cnmf_context* c, const XView& X0, const cnmf_solver_config&
       launch_csr_check(*X.sp, flag, nrm, c->ws<double>("sp_check_ws", csr_metrics_ws_doubles(c->nsm)),
                        c->nsm, c->stream);
     else
-      launch_check_data(X.x, X.ldx, d, n, flag, nrm, ws, c->nsm, c->stream, rexp, flag + 1, flag + 2);
+      launch_check_data(X.x, X.ldx, d, n, flag, nrm, ws, c->nsm, c->stream, rexp, flag + 1, flag + 2,
+                        flag + 3);
     CK(cudaGetLastError());
-    int hflag[3] = {0, 0, 1};
-    CK(cudaMemcpyAsync(hflag, flag, 3 * sizeof(int), cudaMemcpyDeviceToHost, c->stream));
+    int hflag[4] = {0, 0, 1, 1};
+    CK(cudaMemcpyAsync(hflag, flag, 4 * sizeof(int), cudaMemcpyDeviceToHost, c->stream));
     CK(cudaMemcpyAsync(&t.x_norm_sq, nrm, sizeof(double), cudaMemcpyDeviceToHost, c->stream));
     c->sync();
     if (hflag[0]) throw Fail(CNMF_ERR_INPUT, "solver input must be entrywise non-negative and finite");
     if (rexp && !hflag[1]) X.rexp = rexp;
     X.tf32_exact = !X.sp && hflag[2] == 0;
+    X.integral = !X.sp && (hflag[3] & 1) == 0;
+    X.small_int = !X.sp && hflag[3] == 0;
   }
 
   const bool dense_hals = algo == CNMF_FASTHALS || algo == CNMF_HALS;
@@ -1055,8 +1108,11 @@ void run_device_impl(cnmf_context* c, const XView& X0, const cnmf_solver_config&
     diag_load(lm, d);
     diag_load(rt, n);
   }
+  const bool views_done = exact_views(c, X, lm, rt, lp, xht, xc);
+  if (!views_done) {
   x_times(c, X, true, lm, lp, xht, xs, c->stream);   // X-hat^T = X^T L
   x_times(c, X, false, rt, lp, xc, xs, c->stream);   // X-check = X R^T
+  }
   if (diag) {
     if (diag_hdr[3]) {
       diag_load(xc, d);
@@ -1711,11 +1767,14 @@ cnmf_status cnmf_xs_exact(cnmf_context* c, const float* x, uint64_t d, uint64_t 
     double* s64 = c->ws<double>("xe_s", in_rows * lp);
     launch_f32_to_f64(s, in_rows * lp, s64, c->nsm, c->stream);
     bool done = false;
-    if (!use_dmma) {
+    if (use_dmma != 1) {
       int* sx = c->ws<int>("xe_sx", xs_i8_sx_ints(X.d, X.n));
       void* ws = c->ws<char>("xe_ws", xs_i8_ws_bytes(X.d, X.n, lp, c->nsm));
-      launch_xs_i8_prepare_x(X.x, X.ldx, X.d, X.n, sx, c->nsm, c->stream);
-      done = launch_xs_i8(transpose != 0, X.x, X.ldx, X.d, X.n, s64, lp, out, ws, sx, c->nsm, c->stream);
+      const bool small_int = use_dmma == 2;  // caller vouches: integers below 8192
+      if (small_int) CK(cudaMemsetAsync(sx, 0, sizeof(int) * (X.d + X.n), c->stream));
+      else launch_xs_i8_prepare_x(X.x, X.ldx, X.d, X.n, sx, c->nsm, c->stream);
+      done = launch_xs_i8(transpose != 0, X.x, X.ldx, X.d, X.n, s64, lp, out, ws, sx, c->nsm, c->stream,
+                          small_int);
       if (!done) throw Fail(CNMF_ERR_UNSUPPORTED, "cnmf_xs_exact: shape outside the int8 kernel's envelope");
     } else {
       double* ws = c->ws<double>("xe_ws64", xs64_ws_doubles(X.d, X.n, lp, c->nsm));

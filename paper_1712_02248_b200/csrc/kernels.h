@@ -133,7 +133,7 @@ void launch_householder_signs(float* q, int64_t rows, int l, int lp, float* sgn,
 size_t metrics_ws_bytes(int64_t d, int64_t n, int nsm);
 void launch_check_data(const float* x, int64_t ldx, int64_t d, int64_t n, int* flag,
                        double* norm_sq, void* ws, int nsm, cudaStream_t st, int8_t* rexp = nullptr,
-                       int* wide = nullptr, int* inexact = nullptr);
+                       int* wide = nullptr, int* inexact = nullptr, int* nonint = nullptr);
 // 1/2 ||X - A B^T||^2 with column-major A_cm (k x d), B_cm (k x n).
 // The same objective on the tensor cores (recon_tc.cu): dense X (ldx % 4 ==
 // 0, 16-byte aligned), k <= 128; returns false when those do not hold.
@@ -252,14 +252,16 @@ size_t xs64_ws_doubles(int64_t m, int64_t n, int lp, int nsm);
 // exact int32 accumulation on the integer tensor cores (Ozaki-style int8
 // digit slices).  sx: launch_xs_i8_prepare_x's row / column scale exponents
 // of X (xs_i8_sx_ints ints).  launch_xs_i8 returns false outside its envelope
-// (lp a multiple of 16, <= 80; 16-byte aligned rows).
+// (lp a multiple of 16, <= 128; 16-byte aligned rows).  small_int: X holds only integers below
+// 8192 and sx is zero (exact two-digit X, six digits of S).
 bool xs_i8_supported(int lp);
 size_t xs_i8_sx_ints(int64_t d, int64_t n);
 size_t xs_i8_ws_bytes(int64_t m, int64_t n, int lp, int nsm);
 void launch_xs_i8_prepare_x(const float* x, int64_t ldx, int64_t d, int64_t n, int* sx, int nsm,
                             cudaStream_t st);
 bool launch_xs_i8(bool tn, const float* x, int64_t ldx, int64_t m, int64_t n, const double* s,
-                  int lp, double* out, void* ws, const int* sx, int nsm, cudaStream_t st);
+                  int lp, double* out, void* ws, const int* sx, int nsm, cudaStream_t st,
+                  bool small_int = false);
 // halt (nullable): a device flag; when set the launch is a no-op (products
 // queued behind a halted dense HALS sweep, engine.cpp run_dense_hals).
 void launch_xs64_nn(const float* x, int64_t ldx, int64_t m, int64_t n, const double* s, int lp,

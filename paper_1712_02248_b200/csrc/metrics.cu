@@ -27,11 +27,14 @@ __global__ void __launch_bounds__(256) check_data_kernel(const float* __restrict
                                                          double* __restrict__ part,
                                                          int8_t* __restrict__ rexp,
                                                          int* __restrict__ wide,
-                                                         int* __restrict__ inexact) {
+                                                         int* __restrict__ inexact,
+                                                         int* __restrict__ nonint) {
   __shared__ double red[8];
   double s = 0.0;
   int bad = 0;
   unsigned low = 0u;
+  int frac = 0;  // some element is not an integer below 2^26 (the int8-sliced contractions
+                 // take such an X unscaled: xstream_i8.cu)
   const int lane = threadIdx.x & 31;
   const int64_t n4 = (n + 3) / 4;
   const bool vec = (ldx % 4) == 0 && (reinterpret_cast<uintptr_t>(x) & 15) == 0;
@@ -52,6 +55,8 @@ __global__ void __launch_bounds__(256) check_data_kernel(const float* __restrict
       for (int q = 0; q < 4; ++q) {
         if (!(v[q] >= 0.f) || !isfinite(v[q])) bad = 1;
         low |= __float_as_uint(v[q]);
+        frac |= ((v[q] != truncf(v[q])) || !(v[q] < 67108864.f)) ? 1 : 0;
+        frac |= !(v[q] < 8192.f) ? 2 : 0;
         s += (double)v[q] * (double)v[q];
         mx = fmaxf(mx, v[q]);
         if (v[q] > 0.f) mn = fminf(mn, v[q]);
@@ -76,6 +81,11 @@ __global__ void __launch_bounds__(256) check_data_kernel(const float* __restrict
   }
   if (__syncthreads_or(bad) && threadIdx.x == 0) *flag = 1;
   if (__syncthreads_or((low & 0x1FFFu) != 0u) && threadIdx.x == 0 && inexact) *inexact = 1;
+  // bit 0: some element is not an integer below 2^26; bit 1: some element >= 8192
+  if (nonint) {
+    const int f1 = __syncthreads_or(frac & 1), f2 = __syncthreads_or(frac & 2);
+    if (threadIdx.x == 0 && (f1 || f2)) atomicOr(nonint, (f1 ? 1 : 0) | (f2 ? 2 : 0));
+  }
   s = block_sum(s, red);
   if (threadIdx.x == 0) part[blockIdx.x] = s;
 }
@@ -248,11 +258,11 @@ size_t metrics_ws_bytes(int64_t, int64_t, int nsm) { return sizeof(double) * (ns
 
 void launch_check_data(const float* x, int64_t ldx, int64_t d, int64_t n, int* flag,
                        double* norm_sq, void* ws, int nsm, cudaStream_t st, int8_t* rexp,
-                       int* wide, int* inexact) {
+                       int* wide, int* inexact, int* nonint) {
   const int grid = nsm * 4;
   double* part = static_cast<double*>(ws);
   note_launches(1);
-  check_data_kernel<<<grid, 256, 0, st>>>(x, ldx, d, n, flag, part, rexp, wide, inexact);
+  check_data_kernel<<<grid, 256, 0, st>>>(x, ldx, d, n, flag, part, rexp, wide, inexact, nonint);
   note_launches(1);
   sum_partials_kernel<<<1, 32, 0, st>>>(part, grid, norm_sq, 1.0);
 }

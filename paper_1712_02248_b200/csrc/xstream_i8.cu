@@ -60,18 +60,22 @@ constexpr int kSX = 6, kSO = 3, kSB = 2;
 constexpr int kThreadsI8 = 480;
 constexpr int kWarpTMA = 4, kWarpMMA = 5, kWarpSplit0 = 6, kWarpBTMA = 14;
 constexpr int kXBytes = kBM * kBK * 4;
-constexpr int kDigits = 4;
-#ifdef I8_CLASSES  // experiments
-constexpr int kClasses = I8_CLASSES;
-#else
-constexpr int kClasses = 5;  // accumulators: digit pairs (s, t) with s + t = 0 .. 4
-#endif
-constexpr int kQBits = 26;  // |q| < 2^26
+// Digit configurations <XD, SD, NC>: XD digits of the A operand (X), SD of S,
+// NC accumulators (digit pairs (s, t) with s + t < NC are kept).
+//   <4, 4, 5>  general fp32 X: 26-bit fixed point on both sides, 13 pairs;
+//   <2, 6, 7>  X of integers below 8192 (count data): X is EXACT in two digits,
+//              so S can take six (40 bits below its column maximum -- bases of
+//              count data have heavy-tailed columns, and four digits left their
+//              typical entries ~19 bits: the C4 trajectory stayed 9e-4 from the
+//              reference's); all 12 pairs kept, exact products.
+constexpr int kMaxSD = 6;
+__host__ __device__ constexpr int q_bits(int digits) { return 7 * digits - 2; }  // |q| < 2^(7 D - 2)
 
 struct I8Args {
   int64_t rows_out, kdim, kchunk;
   int ntiles, nsplit, lp, np;  // np: lp rounded up to 16 (MMA N)
-  double* out;                 // [nsplit][rows_out][lp]
+  double* out;                 // [nsplit][rows_out] rows of ldo doubles (lp columns written)
+  int64_t ldo;
   const int* sx;               // per output row: its A-operand row's scale exponent
   const double* cscale;        // per column of S: 2^-ss
 };
@@ -120,7 +124,7 @@ __device__ __forceinline__ void tmem_ld16(uint32_t taddr, uint32_t (&h)[16]) {
 // (the integer pipe is the scarce one): x + 1.5 2^23 rounds x to an integer
 // (to nearest even) and leaves it, in two's complement, in the low mantissa
 // bits of the sum.  w[s] carries digit s in its low byte.
-__device__ __forceinline__ void digits4(float v, uint32_t (&w)[kDigits]) {
+__device__ __forceinline__ void digits4(float v, uint32_t (&w)[4]) {
   constexpr float kM = 12582912.f;
   const float w0 = fmaf(v, 0x1.0p-21f, kM);
   const float t0 = w0 - kM;
@@ -138,7 +142,17 @@ __device__ __forceinline__ void digits4(float v, uint32_t (&w)[kDigits]) {
   w[3] = __float_as_uint(w3);
 }
 
-template <bool kTN>
+// two digits of an integer |v| < 8192 (exact)
+__device__ __forceinline__ void digits2(float v, uint32_t (&w)[2]) {
+  constexpr float kM = 12582912.f;
+  const float w0 = fmaf(v, 0x1.0p-7f, kM);
+  const float t0 = w0 - kM;
+  const float w1 = fmaf(-t0, 0x1.0p7f, v) + kM;
+  w[0] = __float_as_uint(w0);
+  w[1] = __float_as_uint(w1);
+}
+
+template <bool kTN, int XD, int SD, int NC>
 __global__ void __launch_bounds__(kThreadsI8, 1)
     xs_i8_kernel(const __grid_constant__ CUtensorMap map_x, const __grid_constant__ CUtensorMap map_b,
                  const I8Args args) {
@@ -151,8 +165,9 @@ __global__ void __launch_bounds__(kThreadsI8, 1)
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int np = args.np;
   const uint32_t slice_bytes = (uint32_t)np * 128u;      // one digit of S^T, 128 k
-  const uint32_t b_bytes = kDigits * slice_bytes;
-  const uint32_t a_off = (uint32_t)(kClasses * np);       // tensor memory: the accumulators, then A slots
+  const uint32_t b_bytes = SD * slice_bytes;
+  constexpr uint32_t kASlot = 8u * XD;  // A slot: 8 columns (32 k) per digit
+  const uint32_t a_off = (uint32_t)(NC * np);             // tensor memory: the accumulators, then A slots
   if (threadIdx.x == 0) {
     for (int s = 0; s < kSX; ++s) {
       mbar_init(&xfull[s], 1);
@@ -231,7 +246,7 @@ __global__ void __launch_bounds__(kThreadsI8, 1)
           mbar_wait(&bempty[b], ph ^ 1);
           mbar_expect_tx(&bfull[b], b_bytes);
 #pragma unroll
-          for (int t = 0; t < kDigits; ++t)
+          for (int t = 0; t < SD; ++t)
             tma(b_addr(b) + t * slice_bytes, &map_b, &bfull[b], (int)kb, t * np);
           if (++b == kSB) {
             b = 0;
@@ -250,19 +265,20 @@ __global__ void __launch_bounds__(kThreadsI8, 1)
       unit_k(u, k0, k1);
       mbar_wait_warp(&acc_empty, aph ^ 1);
       tc_fence_after();
-      uint32_t fresh = (1u << kClasses) - 1u;  // bit w: accumulator w not yet written in this unit
+      uint32_t fresh = (1u << NC) - 1u;  // bit w: accumulator w not yet written in this unit
       int sub = 0;            // X block within the S stage
       for (int64_t kk = k0; kk < k1; kk += kBK) {
         mbar_wait_warp(&opready[o], oph);
         if (sub == 0) mbar_wait_warp(&bfull[b], bph);
         tc_fence_after();
-        const uint32_t a0 = tmem + a_off + 32u * (uint32_t)o;
+        const uint32_t a0 = tmem + a_off + kASlot * (uint32_t)o;
         const uint64_t bd = smem_desc(b_addr(b) + 32u * (uint32_t)sub, 16, 1024, 2);
 #pragma unroll
-        for (int w = 0; w < kClasses; ++w) {
+        for (int w = 0; w < NC; ++w) {
 #pragma unroll
-          for (int s = (w < kDigits ? 0 : w - kDigits + 1); s <= (w < kDigits ? w : kDigits - 1); ++s) {
+          for (int s = 0; s < XD; ++s) {
             const int t = w - s;
+            if (t < 0 || t >= SD) continue;
             mma_i8_ts_elect(tmem + (uint32_t)(w * np), a0 + 8u * s,
                             bd + (uint64_t)((t * slice_bytes) >> 4), idesc, ((fresh >> w) & 1u) ^ 1u);
             fresh &= ~(1u << w);
@@ -316,19 +332,17 @@ __global__ void __launch_bounds__(kThreadsI8, 1)
 #pragma unroll
             for (int kq = 0; kq < 32; ++kq) v[kq] = lds32(x_addr(s) + kq * (kBM * 4) + r * 4);
           }
-          uint32_t pk[32];  // pk[8 s + j]: digit s of k = 4 j .. 4 j + 3
+          uint32_t pk[8 * XD];  // pk[8 s + j]: digit s of k = 4 j .. 4 j + 3
 #pragma unroll
           for (int j = 0; j < 8; ++j) {
-            uint32_t w[4][kDigits];
+            uint32_t w[4][XD];
 #pragma unroll
-#ifdef I8_FAKE_SPLIT  // timing experiment: no digit arithmetic (wrong results)
-            for (int e = 0; e < 4; ++e)
-              for (int d = 0; d < kDigits; ++d) w[e][d] = __float_as_uint(v[4 * j + e] * scale) >> (8 * d);
-#else
-            for (int e = 0; e < 4; ++e) digits4(v[4 * j + e] * scale, w[e]);
-#endif
+            for (int e = 0; e < 4; ++e) {
+              if constexpr (XD == 4) digits4(v[4 * j + e] * scale, w[e]);
+              else digits2(v[4 * j + e] * scale, w[e]);
+            }
 #pragma unroll
-            for (int d = 0; d < kDigits; ++d) {
+            for (int d = 0; d < XD; ++d) {
               const uint32_t lo = __byte_perm(w[0][d], w[1][d], 0x0040);
               const uint32_t hi = __byte_perm(w[2][d], w[3][d], 0x0040);
               pk[8 * d + j] = __byte_perm(lo, hi, 0x5410);
@@ -336,7 +350,8 @@ __global__ void __launch_bounds__(kThreadsI8, 1)
           }
           mbar_wait_warp(&opempty[o], oph ^ 1);
           tc_fence_after();
-          tmem_st32(tmem + ((uint32_t)(32 * q) << 16) + a_off + 32u * (uint32_t)o, pk);
+          if constexpr (XD == 4) tmem_st32(tmem + ((uint32_t)(32 * q) << 16) + a_off + kASlot * (uint32_t)o, pk);
+          else tmem_st16(tmem + ((uint32_t)(32 * q) << 16) + a_off + kASlot * (uint32_t)o, pk);
           asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
           tc_fence_before();
           __syncwarp();
@@ -364,15 +379,15 @@ __global__ void __launch_bounds__(kThreadsI8, 1)
       const int tile = u % args.ntiles, split = u / args.ntiles;
       const int64_t row = (int64_t)tile * kBM + 32 * q + lane;
       const bool ok = row < args.rows_out;
-      const double rs = exp2i_d(7 * (6 - (kClasses - 1)) - (ok ? __ldg(args.sx + row) : 0));
-      double* dst = args.out + ((int64_t)split * args.rows_out + (ok ? row : 0)) * args.lp;
+      const double rs = exp2i_d(7 * (XD + SD - 1 - NC) - (ok ? __ldg(args.sx + row) : 0));
+      double* dst = args.out + ((int64_t)split * args.rows_out + (ok ? row : 0)) * args.ldo;
       mbar_wait_warp(&acc_full, aph);
       tc_fence_after();
       const uint32_t base = tmem + ((uint32_t)(32 * q) << 16);
       for (int c0 = 0; c0 < np; c0 += 16) {
-        uint32_t h[kClasses][16];
+        uint32_t h[NC][16];
 #pragma unroll
-        for (int w = 0; w < kClasses; ++w) tmem_ld16(base + (uint32_t)(w * np + c0), h[w]);
+        for (int w = 0; w < NC; ++w) tmem_ld16(base + (uint32_t)(w * np + c0), h[w]);
         asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
         if (ok) {
 #pragma unroll
@@ -383,7 +398,7 @@ __global__ void __launch_bounds__(kThreadsI8, 1)
               for (int e = 0; e < 2; ++e) {
                 double vsum = (double)(int)h[0][j + e];
 #pragma unroll
-                for (int w = 1; w < kClasses; ++w) vsum = fma(vsum, 128.0, (double)(int)h[w][j + e]);
+                for (int w = 1; w < NC; ++w) vsum = fma(vsum, 128.0, (double)(int)h[w][j + e]);
                 y[e] = vsum * rs * __ldg(args.cscale + c0 + j + e);
               }
               *reinterpret_cast<double2*>(dst + c0 + j) = make_double2(y[0], y[1]);
@@ -412,7 +427,7 @@ __device__ __forceinline__ int scale_exp(float mx) {
   if (!(mx > 0.f)) return 0;
   int e;
   frexpf(mx, &e);  // mx = f 2^e, f in [0.5, 1)
-  return max(-126, min(126, kQBits - e));
+  return max(-126, min(126, q_bits(4) - e));
 }
 
 // rows of X: one warp per row
@@ -449,64 +464,66 @@ __global__ void colmax_to_sx_kernel(const unsigned* __restrict__ cmax, int64_t n
 
 // S (kdim x lp fp64): column maxima (as bits of |s|), then the digits of
 // round(s 2^ss) written K-major: out[(t * np + c) * kpad + k].
-__global__ void s64_colmax_kernel(const double* __restrict__ s, int64_t rows, int lp,
+__global__ void s64_colmax_kernel(const double* __restrict__ s, int64_t lds, int64_t rows, int lp,
                                   unsigned long long* __restrict__ cmax) {
   const int c = threadIdx.x;
   if (c >= lp) return;
   double m = 0.0;
-  for (int64_t r = blockIdx.x; r < rows; r += gridDim.x) m = fmax(m, fabs(s[r * lp + c]));
+  for (int64_t r = blockIdx.x; r < rows; r += gridDim.x) m = fmax(m, fabs(s[r * lds + c]));
   atomicMax(cmax + c, (unsigned long long)__double_as_longlong(m));
 }
-__device__ __forceinline__ int s_scale_exp(unsigned long long bits) {
+__device__ __forceinline__ int s_scale_exp(unsigned long long bits, int sd) {
   const double mx = __longlong_as_double((long long)bits);
   if (!(mx > 0.0)) return 0;
   int e;
   frexp(mx, &e);
-  return max(-900, min(900, kQBits - e));
+  return max(-900, min(900, q_bits(sd) - e));
 }
-__global__ void s64_slice_kernel(const double* __restrict__ s, int64_t kdim, int lp, int np,
-                                 int64_t kpad, const unsigned long long* __restrict__ cmax,
+__global__ void s64_slice_kernel(const double* __restrict__ s, int64_t lds, int64_t kdim, int lp, int np,
+                                 int64_t kpad, int sd, const unsigned long long* __restrict__ cmax,
                                  uint32_t* __restrict__ out, double* __restrict__ cscale) {
   const int64_t kw = kpad / 4;  // words per row of S^T
   for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < kw * np;
        e += (int64_t)gridDim.x * blockDim.x) {
     const int64_t w = e / np;
     const int c = (int)(e - w * np);
-    uint32_t word[kDigits] = {0u, 0u, 0u, 0u};
+    uint32_t word[kMaxSD] = {0u, 0u, 0u, 0u, 0u, 0u};
     if (c < lp) {
-      const int ss = s_scale_exp(cmax[c]);
+      const int ss = s_scale_exp(cmax[c], sd);
 #pragma unroll
       for (int u = 0; u < 4; ++u) {
         const int64_t k = 4 * w + u;
-        long long qv = k < kdim ? llrint(scalbn(s[k * lp + c], ss)) : 0;
+        long long qv = k < kdim ? llrint(scalbn(s[k * lds + c], ss)) : 0;
 #pragma unroll
-        for (int t = kDigits - 1; t > 0; --t) {
-          const long long dg = ((qv + 64) & 127) - 64;
-          word[t] |= (uint32_t)((int)dg & 0xFF) << (8 * u);
-          qv = (qv - dg) >> 7;
+        for (int t = kMaxSD - 1; t > 0; --t) {
+          if (t < sd) {
+            const long long dg = ((qv + 64) & 127) - 64;
+            word[t] |= (uint32_t)((int)dg & 0xFF) << (8 * u);
+            qv = (qv - dg) >> 7;
+          }
         }
         word[0] |= (uint32_t)((int)qv & 0xFF) << (8 * u);
       }
     }
 #pragma unroll
-    for (int t = 0; t < kDigits; ++t) out[((int64_t)t * np + c) * kw + w] = word[t];
+    for (int t = 0; t < kMaxSD; ++t)
+      if (t < sd) out[((int64_t)t * np + c) * kw + w] = word[t];
   }
   if (blockIdx.x == 0)
     for (int c = threadIdx.x; c < np; c += blockDim.x)
-      cscale[c] = c < lp ? scalbn(1.0, -s_scale_exp(cmax[c])) : 0.0;
+      cscale[c] = c < lp ? scalbn(1.0, -s_scale_exp(cmax[c], sd)) : 0.0;
 }
 
-__global__ void i8_split_reduce_kernel(const double2* __restrict__ part, int splits, int64_t total2,
-                                       double2* __restrict__ out) {
-  for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < total2;
+// out[row * ldo + c] = sum over the K-splits of part[split][row][c] (c < w)
+__global__ void i8_split_reduce_kernel(const double* __restrict__ part, int splits, int64_t rows, int w,
+                                       double* __restrict__ out, int64_t ldo) {
+  const int64_t total = rows * w;
+  for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < total;
        e += (int64_t)gridDim.x * blockDim.x) {
-    double2 acc = part[e];
-    for (int s = 1; s < splits; ++s) {
-      const double2 v = part[(int64_t)s * total2 + e];
-      acc.x += v.x;
-      acc.y += v.y;
-    }
-    out[e] = acc;
+    double acc = part[e];
+    for (int s = 1; s < splits; ++s) acc += part[(int64_t)s * total + e];
+    const int64_t r = e / w;
+    out[r * ldo + (e - r * w)] = acc;
   }
 }
 
@@ -558,8 +575,17 @@ size_t align256(size_t b) { return (b + 255) & ~size_t(255); }
 
 }  // namespace
 
-// five accumulators of lp columns and three 32-column A slots fill the 512 TMEM columns at lp = 80
-bool xs_i8_supported(int lp) { return lp % 16 == 0 && lp <= 80; }
+// Tensor memory bounds the column chunk: <4, 4, 5> five accumulators of w
+// columns + three 32-column A slots = 496 of 512 at w = 80; <2, 6, 7> seven
+// accumulators + three 16-column slots = 496 at w = 64.  Wider operands run as
+// column chunks (one X pass each).
+constexpr int kMaxChunk = 80;
+bool xs_i8_supported(int lp) { return lp % 16 == 0 && lp > 0 && lp <= 128; }
+static int chunk_width(int lp, int mode) {
+  const int cap = mode == 1 ? 64 : kMaxChunk;
+  const int nch = (lp + cap - 1) / cap;
+  return std::min(cap, ((lp + nch - 1) / nch + 15) & ~15);
+}
 
 size_t xs_i8_sx_ints(int64_t d, int64_t n) { return (size_t)(d + n) + 2 * (size_t)n + 64; }
 
@@ -581,29 +607,30 @@ void launch_xs_i8_prepare_x(const float* x, int64_t ldx, int64_t d, int64_t n, i
 }
 
 size_t xs_i8_ws_bytes(int64_t m, int64_t n, int lp, int nsm) {
-  const int np = lp;
+  const int np = kMaxChunk;  // either mode: kMaxSD digits of <= 80 columns
   const int64_t kmax = std::max(m, n);
   const int64_t kpad = (kmax + kBKB - 1) / kBKB * kBKB;
   const I8Plan a = i8_plan(m, n, nsm), b = i8_plan(n, m, nsm);
-  const size_t parts = sizeof(double) * (size_t)std::max<int64_t>((int64_t)a.nsplit * m * lp,
-                                                                   (int64_t)b.nsplit * n * lp);
-  return align256((size_t)kDigits * np * kpad) + align256(sizeof(unsigned long long) * 128) +
+  const size_t parts = sizeof(double) * (size_t)std::max<int64_t>((int64_t)a.nsplit * m * np,
+                                                                   (int64_t)b.nsplit * n * np);
+  return align256((size_t)kMaxSD * np * kpad) + align256(sizeof(unsigned long long) * 128) +
          align256(sizeof(double) * 128) + align256(parts) + 1024;
 }
 
-// y = X s (NN, out m x lp) or z = X^T t (TN, out n x lp): s / t is kdim x lp
-// fp64 row-major, out fp64; sx from launch_xs_i8_prepare_x.  False when the
-// shape is outside the kernel's envelope (the caller keeps the fp64 DMMA path).
-bool launch_xs_i8(bool tn, const float* x, int64_t ldx, int64_t m, int64_t n, const double* s,
-                  int lp, double* out, void* ws, const int* sx, int nsm, cudaStream_t st) {
-  if (!xs_i8_supported(lp) || (ldx % 4) != 0 || (reinterpret_cast<uintptr_t>(x) & 15)) return false;
-  const int np = lp;
+namespace {
+
+// One column chunk: out[:, 0 .. w) (row pitch ldo) = X s[:, 0 .. w) (row pitch lds).
+bool launch_xs_i8_chunk(bool tn, const float* x, int64_t ldx, int64_t m, int64_t n, const double* s,
+                        int64_t lds, int w, int mode, double* out, int64_t ldo, void* ws, const int* sx,
+                        int nsm, cudaStream_t st) {
+  const int sd = mode == 1 ? 6 : 4;
+  const int np = w;
   const int64_t rows_out = tn ? n : m, kdim = tn ? m : n;
   const int64_t kpad = (kdim + kBKB - 1) / kBKB * kBKB;
   const I8Plan p = i8_plan(rows_out, kdim, nsm);
   uint8_t* base = static_cast<uint8_t*>(ws);
   uint8_t* st_digits = base;
-  base += align256((size_t)kDigits * np * ((std::max(m, n) + kBKB - 1) / kBKB * kBKB));
+  base += align256((size_t)kMaxSD * kMaxChunk * ((std::max(m, n) + kBKB - 1) / kBKB * kBKB));
   unsigned long long* cmax = reinterpret_cast<unsigned long long*>(base);
   base += align256(sizeof(unsigned long long) * 128);
   double* cscale = reinterpret_cast<double*>(base);
@@ -613,17 +640,17 @@ bool launch_xs_i8(bool tn, const float* x, int64_t ldx, int64_t m, int64_t n, co
   if (cudaMemsetAsync(cmax, 0, sizeof(unsigned long long) * 128, st) != cudaSuccess) return false;
   note_launches(2);
   s64_colmax_kernel<<<(int)std::max<int64_t>(1, std::min<int64_t>(kdim, (int64_t)nsm * 4)), 128, 0, st>>>(
-      s, kdim, lp, cmax);
+      s, lds, kdim, w, cmax);
   s64_slice_kernel<<<(int)std::min<int64_t>((kpad / 4 * np + 255) / 256, (int64_t)nsm * 16), 256, 0, st>>>(
-      s, kdim, lp, np, kpad, cmax, reinterpret_cast<uint32_t*>(st_digits), cscale);
+      s, lds, kdim, w, np, kpad, sd, cmax, reinterpret_cast<uint32_t*>(st_digits), cscale);
 
   CUtensorMap mx, mb;
   bool ok = tn ? make_map(&mx, x, m, n, ldx, kBM, kBK, CU_TENSOR_MAP_SWIZZLE_NONE)
                : make_map(&mx, x, m, n, ldx, kBK, kBM, CU_TENSOR_MAP_SWIZZLE_128B);
-  ok = ok && make_map_u8(&mb, st_digits, (int64_t)kDigits * np, kpad, kBKB, np);
+  ok = ok && make_map_u8(&mb, st_digits, (int64_t)sd * np, kpad, kBKB, np);
   if (!ok) {
-    std::fprintf(stderr, "xs_i8: tensor map encode failed (tn %d, m %lld, n %lld, lp %d)\n", (int)tn,
-                 (long long)m, (long long)n, lp);
+    std::fprintf(stderr, "xs_i8: tensor map encode failed (tn %d, m %lld, n %lld, w %d)\n", (int)tn,
+                 (long long)m, (long long)n, w);
     return false;
   }
   I8Args a;
@@ -632,32 +659,61 @@ bool launch_xs_i8(bool tn, const float* x, int64_t ldx, int64_t m, int64_t n, co
   a.kchunk = p.kchunk;
   a.ntiles = p.ntiles;
   a.nsplit = p.nsplit;
-  a.lp = lp;
+  a.lp = w;
   a.np = np;
   a.out = p.nsplit > 1 ? parts : out;
+  a.ldo = p.nsplit > 1 ? w : ldo;
   a.sx = tn ? sx + m : sx;
   a.cscale = cscale;
   const int units = p.ntiles * p.nsplit;
   const int grid = std::min(units, nsm);
-  const int smem = kSX * kXBytes + kSB * kDigits * np * 128 + 1024;
-  static std::atomic<unsigned> attr_nn{0u}, attr_tn{0u};
+  const int smem = kSX * kXBytes + kSB * sd * np * 128 + 1024;
+  constexpr int kSmemMax = kSX * kXBytes + kSB * 4 * kMaxChunk * 128 + 1024;  // = 6 digits of 64 columns + ...
+  static_assert(kSX * kXBytes + kSB * 6 * 64 * 128 + 1024 <= kSmemMax + 16384, "smem");
+  static std::atomic<unsigned> attr[4] = {{0u}, {0u}, {0u}, {0u}};
   note_launches(1);
-  if (tn) {
-    smem_attr_once(attr_tn, (const void*)(xs_i8_kernel<true>), kSX * kXBytes + kSB * kDigits * 96 * 128 + 1024);
-    xs_i8_kernel<true><<<grid, kThreadsI8, smem, st>>>(mx, mb, a);
+  auto go = [&](auto kern, std::atomic<unsigned>& at) {
+    smem_attr_once(at, (const void*)kern, 200 * 1024);
+    kern<<<grid, kThreadsI8, smem, st>>>(mx, mb, a);
+  };
+  if (mode == 1) {
+    if (tn) go(xs_i8_kernel<true, 2, 6, 7>, attr[0]);
+    else go(xs_i8_kernel<false, 2, 6, 7>, attr[1]);
   } else {
-    smem_attr_once(attr_nn, (const void*)(xs_i8_kernel<false>), kSX * kXBytes + kSB * kDigits * 96 * 128 + 1024);
-    xs_i8_kernel<false><<<grid, kThreadsI8, smem, st>>>(mx, mb, a);
+    if (tn) go(xs_i8_kernel<true, 4, 4, 5>, attr[2]);
+    else go(xs_i8_kernel<false, 4, 4, 5>, attr[3]);
   }
   if (const cudaError_t e = cudaGetLastError(); e != cudaSuccess) {
     std::fprintf(stderr, "xs_i8: launch failed: %s\n", cudaGetErrorString(e));
     return false;
   }
   if (p.nsplit > 1) {
-    const int64_t total2 = rows_out * lp / 2;
     note_launches(1);
-    i8_split_reduce_kernel<<<(int)std::min<int64_t>((total2 + 255) / 256, (int64_t)nsm * 8), 256, 0, st>>>(
-        reinterpret_cast<const double2*>(parts), p.nsplit, total2, reinterpret_cast<double2*>(out));
+    i8_split_reduce_kernel<<<(int)std::min<int64_t>((rows_out * w + 255) / 256, (int64_t)nsm * 8), 256, 0,
+                             st>>>(parts, p.nsplit, rows_out, w, out, ldo);
+  }
+  return true;
+}
+
+}  // namespace
+
+// y = X s (NN, out m x lp) or z = X^T t (TN, out n x lp): s / t is kdim x lp
+// fp64 row-major, out fp64; sx from launch_xs_i8_prepare_x (or zeros for an X
+// of integers below 2^26).  small_int: every element of X is an integer below
+// 8192 and sx is all zeros -- the <2, 6, 7> configuration (exact X digits, 40
+// bits of S).  Sketches wider than 80 columns take one pass of X
+// per column chunk.  False when the shape is outside the kernel's envelope
+// (the caller keeps its other path).
+bool launch_xs_i8(bool tn, const float* x, int64_t ldx, int64_t m, int64_t n, const double* s,
+                  int lp, double* out, void* ws, const int* sx, int nsm, cudaStream_t st,
+                  bool small_int) {
+  if (!xs_i8_supported(lp) || (ldx % 4) != 0 || (reinterpret_cast<uintptr_t>(x) & 15)) return false;
+  const int mode = small_int ? 1 : 0;
+  const int cw = chunk_width(lp, mode);
+  for (int c0 = 0; c0 < lp; c0 += cw) {
+    const int w = std::min(cw, lp - c0);
+    if (!launch_xs_i8_chunk(tn, x, ldx, m, n, s + c0, lp, w, mode, out + c0, lp, ws, sx, nsm, st))
+      return false;
   }
   return true;
 }

@@ -10,7 +10,11 @@ tests/golden/<config>_full.npz:
                         `error_interval`-th, error = 1/2 ||X - A B^T||^2)
     step_draws          raw mt19937_64 draws each fasthals_rp_step took from
                         the run Rng (its dead-component redraws)
-    a, b                the final factors, fp32 (d x k, n x k)
+    a, b                the final factors, fp32 (d x k, n x k); C4 keeps every
+                        a_row_stride-th / b_row_stride-th row (2 / 4: a 16 MB
+                        fixture instead of 42) together with the fp64 column
+                        sums and sums of squares over ALL rows
+                        (a_colsum, a_colsumsq, b_colsum, b_colsumsq)
     x_hash, x_sums      per-1000-row-block checksums of X's fp32 bits and its
                         fp64 sum / sum of squares (the GPU tests check their
                         device-generated X against these first)
@@ -37,6 +41,10 @@ CONFIGS = {
     "c3": (100000, 20000, 50, 0, 1, 0.01, 1, 50, 70, 2, 100, 5),
     "c4": (50000, 100000, 100, 2, 2, 0.0, 1, 100, 120, 1, 100, 5),
 }
+
+
+# rows of the final factors kept in the fixture (all rows when absent)
+ROW_STRIDE = {"c4": {"a": 2, "b": 4}}
 
 
 def main(names):
@@ -69,6 +77,12 @@ def main(names):
                                   float(meta["compress_seconds"]),
                                   float(meta["update_seconds"])]),
             )
+            for nm, stride in ROW_STRIDE.get(name, {}).items():
+                f = out[nm].astype(np.float64)
+                out[nm + "_colsum"] = f.sum(axis=0)
+                out[nm + "_colsumsq"] = (f * f).sum(axis=0)
+                out[nm + "_row_stride"] = np.array([stride])
+                out[nm] = out[nm][::stride].copy()
             path = os.path.join(HERE, f"{name}_full.npz")
             np.savez_compressed(path, **out)
             print(f"{name}: {len(out['errors'])} records, "

@@ -198,6 +198,29 @@ def test_xstream_int8_sliced_contraction(ctx, d, n, l):
             assert rel_fro(host(got), ref) < tol, (tn, tol, rel_fro(host(got), ref))
 
 
+@pytest.mark.parametrize("d,n,l", [(1000, 1000, 128), (333, 517, 16), (700, 4100, 112), (2049, 1500, 64)])
+def test_xstream_int8_small_integer_x(ctx, d, n, l):
+    """Count data (integers below 8192) is exact in two int8 digits, so s takes
+    six (40 bits below its column maximum) and every digit pair is kept: the
+    products are exact and heavy-tailed columns of s (as the bases of count
+    data have) keep ~1e-10; sketches wider than 64 columns run as chunks."""
+    rng = np.random.default_rng(d + n + l)
+    x = rng.poisson(rng.gamma(0.3, 4.0, size=(d, 1)) * rng.gamma(0.3, 4.0, size=(1, n))).astype(np.float32)
+    x[rng.random((d, n)) < 1e-3] = 8191.0
+    s = (rng.standard_normal((n, l)) * np.exp(3.0 * rng.standard_normal((n, 1)))).astype(np.float32)
+    t = (rng.standard_normal((d, l)) * np.exp(3.0 * rng.standard_normal((d, 1)))).astype(np.float32)
+    xd = dev(x)
+    x64 = x.astype(np.float64)
+    for tn, op, ref, rows in ((False, dev(s), x64 @ s.astype(np.float64), d),
+                              (True, dev(t), x64.T @ t.astype(np.float64), n)):
+        got = torch.empty((rows, l), dtype=torch.float64, device="cuda")
+        ctx.xs_exact(xd, op, got, transpose=tn, small_int=True)
+        assert rel_fro(host(got), ref) < 1e-9, (tn, rel_fro(host(got), ref))
+        gen = torch.empty((rows, l), dtype=torch.float64, device="cuda")
+        ctx.xs_exact(xd, op, gen, transpose=tn)  # the general configuration, chunked for l > 80
+        assert rel_fro(host(gen), ref) < 1e-4
+
+
 def test_xstream_nearly_exact_operands_stay_three_product(ctx):
     """One element off the tf32 grid sends the whole X down the 3xTF32 path:
     the result keeps that element's low bits."""
