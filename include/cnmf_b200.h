@@ -246,6 +246,12 @@ cnmf_status cnmf_xs_tn(cnmf_context* ctx, const float* x, uint64_t d, uint64_t n
  * caller vouches for that: exact X digits, 40 bits of s). */
 cnmf_status cnmf_xs_exact(cnmf_context* ctx, const float* x, uint64_t d, uint64_t n, uint64_t ldx,
                           const float* s, uint64_t l, int transpose, int use_dmma, double* out);
+/* Seconds per exact-accumulation contraction (cnmf_xs_exact's int8-sliced
+ * kernel on a seeded Gaussian operand, S slicing and every column chunk
+ * included; the per-X preprocessing once, outside), and the reads of X it makes. */
+cnmf_status cnmf_time_xs_exact(cnmf_context* ctx, const float* x, uint64_t d, uint64_t n,
+                               uint64_t ldx, uint64_t l, int transpose, int iters,
+                               double* seconds_per_launch, int* x_passes);
 
 /* Instrumentation (bench harness). */
 /* Total device kernels this library has launched in this process. */

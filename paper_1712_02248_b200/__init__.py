@@ -116,7 +116,7 @@ EXPORTS = [
     "cnmf_initialize", "cnmf_powered_range_finder", "cnmf_build_projectors", "cnmf_compress",
     "cnmf_compress_factors", "cnmf_fasthals_rp_steps", "cnmf_reconstruction_error",
     "cnmf_thin_qr", "cnmf_xs_nn", "cnmf_xs_tn", "cnmf_xs_exact", "cnmf_synth_x", "cnmf_launch_count",
-    "cnmf_time_xstream", "cnmf_shard_begin", "cnmf_nccl_unique_id", "cnmf_context_create_sharded",
+    "cnmf_time_xstream", "cnmf_time_xs_exact", "cnmf_shard_begin", "cnmf_nccl_unique_id", "cnmf_context_create_sharded",
     "cnmf_run_sharded_device", "cnmf_estimate_cost", "cnmf_generate_synthetic",
     "cnmf_pairwise_distortion", "cnmf_run_csr", "cnmf_context_create_hosted",
 ]
@@ -177,6 +177,7 @@ def load_library(path: str = LIB_PATH):
                                u64, fp]
     L.cnmf_launch_count.restype = u64
     L.cnmf_time_xstream.argtypes = [vp, fp, u64, u64, u64, u64, C.c_int, C.c_int, dp]
+    L.cnmf_time_xs_exact.argtypes = [vp, fp, u64, u64, u64, u64, C.c_int, C.c_int, dp, C.POINTER(C.c_int)]
     L.cnmf_shard_begin.argtypes = [u64, C.c_int, C.c_int]
     L.cnmf_shard_begin.restype = u64
     L.cnmf_nccl_unique_id.argtypes = [C.c_char_p]
@@ -519,6 +520,15 @@ class Context:
         self._check(self.L.cnmf_time_xstream(self.h, _ptr(x), d, n, x.stride(0), l,
                                              int(transpose), iters, C.byref(out)))
         return out.value
+
+    def time_xs_exact(self, x, l, transpose, iters=5):
+        """(seconds per exact-accumulation contraction, reads of X it makes)."""
+        _torch_ready()
+        d, n = x.shape
+        out, passes = C.c_double(), C.c_int()
+        self._check(self.L.cnmf_time_xs_exact(self.h, _ptr(x), d, n, x.stride(0), l, int(transpose),
+                                              iters, C.byref(out), C.byref(passes)))
+        return out.value, passes.value
 
     def synth_x(self, d, n, rank, factor_kind, noise_kind, sigma, seed, out, col_lo=0,
                 col_hi=None):

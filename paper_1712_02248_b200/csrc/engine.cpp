@@ -1820,6 +1820,53 @@ cnmf_status cnmf_time_xstream(cnmf_context* c, const float* x, uint64_t d, uint6
   });
 }
 
+cnmf_status cnmf_time_xs_exact(cnmf_context* c, const float* x, uint64_t d, uint64_t n,
+                               uint64_t ldx, uint64_t l, int transpose, int iters,
+                               double* seconds_per_launch, int* x_passes) {
+  return guarded(c, [&] {
+    require_shapes(1, l);
+    if (iters < 1) throw Fail(CNMF_ERR_CONFIG, "iters must be positive");
+    const int lp = pad16((int)l);
+    XView X = prepare_x(c, x, (int64_t)d, (int64_t)n, (int64_t)ldx);
+    const int64_t in_rows = transpose ? (int64_t)d : (int64_t)n;
+    const int64_t out_rows = transpose ? (int64_t)n : (int64_t)d;
+    float* s = c->ws<float>("tx_s", in_rows * lp);
+    double* s64 = c->ws<double>("txe_s64", in_rows * lp);
+    double* y = c->ws<double>("txe_y", out_rows * lp);
+    gen_normals(c, 12345, in_rows, (int64_t)l, s, lp, "tx");
+    launch_f32_to_f64(s, in_rows * lp, s64, c->nsm, c->stream);
+    // per-X preprocessing, once per X as in a run: the data-validation read
+    // decides the digit configuration, the exponent reads serve every call
+    int* flag = c->ws<int>("cflag", 4);
+    double* nrm = c->ws<double>("xnorm", 1);
+    void* mws = c->ws<char>("metrics_ws", metrics_ws_bytes(X.d, X.n, c->nsm));
+    CK(cudaMemsetAsync(flag, 0, 4 * sizeof(int), c->stream));
+    launch_check_data(X.x, X.ldx, X.d, X.n, flag, nrm, mws, c->nsm, c->stream, nullptr, flag + 1, flag + 2,
+                      flag + 3);
+    int hflag[4] = {0, 0, 1, 3};
+    CK(cudaMemcpyAsync(hflag, flag, sizeof hflag, cudaMemcpyDeviceToHost, c->stream));
+    c->sync();
+    const bool small_int = hflag[3] == 0;
+    int* sx = c->ws<int>("txe_sx", xs_i8_sx_ints(X.d, X.n));
+    if (small_int) CK(cudaMemsetAsync(sx, 0, sizeof(int) * (X.d + X.n), c->stream));
+    else launch_xs_i8_prepare_x(X.x, X.ldx, X.d, X.n, sx, c->nsm, c->stream);
+    void* ws = c->ws<char>("txe_ws", xs_i8_ws_bytes(X.d, X.n, lp, c->nsm));
+    auto once = [&] {
+      if (!launch_xs_i8(transpose != 0, X.x, X.ldx, X.d, X.n, s64, lp, y, ws, sx, c->nsm, c->stream,
+                        small_int))
+        throw Fail(CNMF_ERR_UNSUPPORTED, "shape outside the int8-sliced kernel's envelope");
+    };
+    once();  // warm-up
+    CK(cudaEventRecord(c->ev[0], c->stream));
+    for (int i = 0; i < iters; ++i) once();
+    CK(cudaEventRecord(c->ev[1], c->stream));
+    CK(cudaGetLastError());
+    c->sync();
+    *seconds_per_launch = c->elapsed(0, 1) / iters;
+    if (x_passes) *x_passes = xs_i8_x_passes(lp, small_int);
+  });
+}
+
 cnmf_status cnmf_synth_x(cnmf_context* c, uint64_t d, uint64_t n, uint64_t rank, int factor_kind,
                          int noise_kind, double sigma, uint64_t seed, uint64_t col_lo,
                          uint64_t col_hi, uint64_t ldx, float* x) {

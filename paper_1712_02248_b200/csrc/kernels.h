@@ -256,6 +256,7 @@ size_t xs64_ws_doubles(int64_t m, int64_t n, int lp, int nsm);
 // 8192 and sx is zero (exact two-digit X, six digits of S).
 bool xs_i8_supported(int lp);
 size_t xs_i8_sx_ints(int64_t d, int64_t n);
+int xs_i8_x_passes(int lp, bool small_int);
 size_t xs_i8_ws_bytes(int64_t m, int64_t n, int lp, int nsm);
 void launch_xs_i8_prepare_x(const float* x, int64_t ldx, int64_t d, int64_t n, int* sx, int nsm,
                             cudaStream_t st);

@@ -587,6 +587,12 @@ static int chunk_width(int lp, int mode) {
   return std::min(cap, ((lp + nch - 1) / nch + 15) & ~15);
 }
 
+// reads of X one contraction makes (column chunks)
+int xs_i8_x_passes(int lp, bool small_int) {
+  const int cw = chunk_width(lp, small_int ? 1 : 0);
+  return (lp + cw - 1) / cw;
+}
+
 size_t xs_i8_sx_ints(int64_t d, int64_t n) { return (size_t)(d + n) + 2 * (size_t)n + 64; }
 
 // Scale exponents of X's rows (sx[0 .. d)) and columns (sx[d .. d + n)); the
