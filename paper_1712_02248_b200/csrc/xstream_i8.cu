@@ -56,7 +56,15 @@ using namespace tc;
 constexpr int kBM = 128;   // output rows per unit (MMA M)
 constexpr int kBK = 32;    // k per X block (one kind::i8 MMA step)
 constexpr int kBKB = 128;  // k per S stage (one swizzle row)
-constexpr int kSX = 6, kSO = 3, kSB = 2;
+#ifdef I8_SX
+constexpr int kSX = I8_SX;
+#else
+constexpr int kSX = 6;
+#endif
+constexpr int kSB = 2;
+// A operand slots in tensor memory: what the 512 columns leave beside the
+// accumulators (<4,4,5> at 80 columns: 400 + 3 x 32; <2,6,7> at 64: 448 + 4 x 16)
+__host__ __device__ constexpr int a_slots(int xd) { return xd == 2 ? 4 : 3; }
 constexpr int kThreadsI8 = 480;
 constexpr int kWarpTMA = 4, kWarpMMA = 5, kWarpSplit0 = 6, kWarpBTMA = 14;
 constexpr int kXBytes = kBM * kBK * 4;
@@ -76,6 +84,7 @@ struct I8Args {
   int ntiles, nsplit, lp, np;  // np: lp rounded up to 16 (MMA N)
   double* out;                 // [nsplit][rows_out] rows of ldo doubles (lp columns written)
   int64_t ldo;
+  int64_t pair_out;            // kPair: CTA 1's offset into out (its chunk's columns or partials)
   const int* sx;               // per output row: its A-operand row's scale exponent
   const double* cscale;        // per column of S: 2^-ss
 };
@@ -152,18 +161,30 @@ __device__ __forceinline__ void digits2(float v, uint32_t (&w)[2]) {
   w[1] = __float_as_uint(w1);
 }
 
-template <bool kTN, int XD, int SD, int NC>
+// kPair: launched as clusters of two CTAs that take the two column chunks of
+// one (tile, K-split) unit: CTA 0 streams each X stage ONCE into both CTAs'
+// shared memory (TMA multicast), so a two-chunk contraction reads X once
+// instead of twice; each CTA slices the stage and runs its own chunk's MMAs
+// against its own S digits.  A stage is refilled when both CTAs' split warps
+// have released it (the peer's arrive remotely on CTA 0's xpeer barriers).
+template <bool kTN, int XD, int SD, int NC, bool kPair>
 __global__ void __launch_bounds__(kThreadsI8, 1)
     xs_i8_kernel(const __grid_constant__ CUtensorMap map_x, const __grid_constant__ CUtensorMap map_b,
                  const I8Args args) {
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   const uint32_t sbase = (smem_u32(smem_raw) + 1023u) & ~1023u;
+  constexpr int kSO = a_slots(XD);
   __shared__ __align__(8) uint64_t xfull[kSX], xempty[kSX], opready[kSO], opempty[kSO];
   __shared__ __align__(8) uint64_t bfull[kSB], bempty[kSB], acc_full, acc_empty;
+  __shared__ __align__(8) uint64_t xpeer[kSX];  // kPair, CTA 0: the peer's releases of X stages
   __shared__ uint32_t tmem_base;
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int np = args.np;
+  uint32_t rank = 0;  // CTA within the pair = column chunk
+  if constexpr (kPair) asm volatile("mov.u32 %0, %%cluster_ctarank;" : "=r"(rank));
+  const int wid = kPair ? (int)(blockIdx.x >> 1) : (int)blockIdx.x;
+  const int wstride = kPair ? (int)(gridDim.x >> 1) : (int)gridDim.x;
   const uint32_t slice_bytes = (uint32_t)np * 128u;      // one digit of S^T, 128 k
   const uint32_t b_bytes = SD * slice_bytes;
   constexpr uint32_t kASlot = 8u * XD;  // A slot: 8 columns (32 k) per digit
@@ -172,6 +193,7 @@ __global__ void __launch_bounds__(kThreadsI8, 1)
     for (int s = 0; s < kSX; ++s) {
       mbar_init(&xfull[s], 1);
       mbar_init(&xempty[s], 4);
+      mbar_init(&xpeer[s], 4);
     }
     for (int s = 0; s < kSO; ++s) {
       mbar_init(&opready[s], 4);
@@ -194,6 +216,10 @@ __global__ void __launch_bounds__(kThreadsI8, 1)
   tc_fence_before();
   __syncthreads();
   tc_fence_after();
+  if constexpr (kPair) {  // both CTAs' barriers exist before any remote arrive or multicast
+    asm volatile("barrier.cluster.arrive.release.aligned;" ::: "memory");
+    asm volatile("barrier.cluster.wait.acquire.aligned;" ::: "memory");
+  }
   const uint32_t tmem = tmem_base;
 
   const int units = args.ntiles * args.nsplit;
@@ -218,15 +244,30 @@ __global__ void __launch_bounds__(kThreadsI8, 1)
     if (lane == 0) {
       int s = 0;
       uint32_t ph = 0;
-      for (int u = blockIdx.x; u < units; u += gridDim.x) {
+      for (int u = wid; u < units; u += wstride) {
         int64_t k0, k1;
         unit_k(u, k0, k1);
         const int row0 = (u % args.ntiles) * kBM;
         for (int64_t kk = k0; kk < k1; kk += kBK) {
           mbar_wait(&xempty[s], ph ^ 1);
+          if constexpr (kPair) {
+            if (rank == 0) mbar_wait(&xpeer[s], ph ^ 1);
+          }
           mbar_expect_tx(&xfull[s], kXBytes);
-          if (!kTN) tma(x_addr(s), &map_x, &xfull[s], (int)kk, row0);
-          else tma(x_addr(s), &map_x, &xfull[s], row0, (int)kk);
+          if constexpr (kPair) {
+            if (rank == 0) {  // one load for both CTAs: same offsets, each CTA's own xfull
+              const int c0 = kTN ? row0 : (int)kk, c1 = kTN ? (int)kk : row0;
+              asm volatile(
+                  "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes"
+                  ".multicast::cluster [%0], [%1, {%3, %4}], [%2], %5;" ::"r"(x_addr(s)),
+                  "l"(reinterpret_cast<uint64_t>(&map_x)), "r"(smem_u32(&xfull[s])), "r"(c0), "r"(c1),
+                  "h"((uint16_t)3)
+                  : "memory");
+            }
+          } else {
+            if (!kTN) tma(x_addr(s), &map_x, &xfull[s], (int)kk, row0);
+            else tma(x_addr(s), &map_x, &xfull[s], row0, (int)kk);
+          }
           if (++s == kSX) {
             s = 0;
             ph ^= 1;
@@ -239,7 +280,7 @@ __global__ void __launch_bounds__(kThreadsI8, 1)
     if (lane == 0) {
       int b = 0;
       uint32_t ph = 0;
-      for (int u = blockIdx.x; u < units; u += gridDim.x) {
+      for (int u = wid; u < units; u += wstride) {
         int64_t k0, k1;
         unit_k(u, k0, k1);
         for (int64_t kb = k0; kb < k1; kb += kBKB) {
@@ -247,7 +288,7 @@ __global__ void __launch_bounds__(kThreadsI8, 1)
           mbar_expect_tx(&bfull[b], b_bytes);
 #pragma unroll
           for (int t = 0; t < SD; ++t)
-            tma(b_addr(b) + t * slice_bytes, &map_b, &bfull[b], (int)kb, t * np);
+            tma(b_addr(b) + t * slice_bytes, &map_b, &bfull[b], (int)kb, ((int)rank * SD + t) * np);
           if (++b == kSB) {
             b = 0;
             ph ^= 1;
@@ -260,7 +301,7 @@ __global__ void __launch_bounds__(kThreadsI8, 1)
     const uint32_t idesc = idesc_i8(np);
     int o = 0, b = 0;
     uint32_t oph = 0, bph = 0, aph = 0;
-    for (int u = blockIdx.x; u < units; u += gridDim.x) {
+    for (int u = wid; u < units; u += wstride) {
       int64_t k0, k1;
       unit_k(u, k0, k1);
       mbar_wait_warp(&acc_empty, aph ^ 1);
@@ -309,7 +350,7 @@ __global__ void __launch_bounds__(kThreadsI8, 1)
     const int r = 32 * q + lane;
     int s = 0, o = 0, nblk = 0;
     uint32_t xph = 0, oph = 0;
-    for (int u = blockIdx.x; u < units; u += gridDim.x) {
+    for (int u = wid; u < units; u += wstride) {
       int64_t k0, k1;
       unit_k(u, k0, k1);
       const int64_t row = (int64_t)(u % args.ntiles) * kBM + r;
@@ -359,6 +400,13 @@ __global__ void __launch_bounds__(kThreadsI8, 1)
           if (lane == 0) {
             mbar_arrive(&opready[o]);
             mbar_arrive(&xempty[s]);
+            if constexpr (kPair) {
+              if (rank == 1) {  // tell CTA 0 (which refills both copies) that this copy is free
+                uint32_t remote;
+                asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(remote) : "r"(smem_u32(&xpeer[s])), "r"(0));
+                asm volatile("mbarrier.arrive.release.cluster.shared::cluster.b64 _, [%0];" ::"r"(remote) : "memory");
+              }
+            }
           }
         }
         if (++s == kSX) {
@@ -375,12 +423,12 @@ __global__ void __launch_bounds__(kThreadsI8, 1)
     // ---------------- epilogue: the five int32 accumulators -> fp64 ----------
     const int q = warp;
     uint32_t aph = 0;
-    for (int u = blockIdx.x; u < units; u += gridDim.x) {
+    for (int u = wid; u < units; u += wstride) {
       const int tile = u % args.ntiles, split = u / args.ntiles;
       const int64_t row = (int64_t)tile * kBM + 32 * q + lane;
       const bool ok = row < args.rows_out;
       const double rs = exp2i_d(7 * (XD + SD - 1 - NC) - (ok ? __ldg(args.sx + row) : 0));
-      double* dst = args.out + ((int64_t)split * args.rows_out + (ok ? row : 0)) * args.ldo;
+      double* dst = args.out + (int64_t)rank * args.pair_out + ((int64_t)split * args.rows_out + (ok ? row : 0)) * args.ldo;
       mbar_wait_warp(&acc_full, aph);
       tc_fence_after();
       const uint32_t base = tmem + ((uint32_t)(32 * q) << 16);
@@ -399,7 +447,7 @@ __global__ void __launch_bounds__(kThreadsI8, 1)
                 double vsum = (double)(int)h[0][j + e];
 #pragma unroll
                 for (int w = 1; w < NC; ++w) vsum = fma(vsum, 128.0, (double)(int)h[w][j + e]);
-                y[e] = vsum * rs * __ldg(args.cscale + c0 + j + e);
+                y[e] = vsum * rs * __ldg(args.cscale + 128 * rank + c0 + j + e);
               }
               *reinterpret_cast<double2*>(dst + c0 + j) = make_double2(y[0], y[1]);
             }
@@ -417,6 +465,10 @@ __global__ void __launch_bounds__(kThreadsI8, 1)
   if (warp == kWarpMMA) {
     tc_fence_after();
     asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 512;" ::"r"(tmem));
+  }
+  if constexpr (kPair) {  // no CTA leaves while its peer may still signal or multicast to it
+    asm volatile("barrier.cluster.arrive.release.aligned;" ::: "memory");
+    asm volatile("barrier.cluster.wait.acquire.aligned;" ::: "memory");
   }
 }
 
@@ -580,6 +632,7 @@ size_t align256(size_t b) { return (b + 255) & ~size_t(255); }
 // accumulators + three 16-column slots = 496 at w = 64.  Wider operands run as
 // column chunks (one X pass each).
 constexpr int kMaxChunk = 80;
+constexpr int kDigitRows = 2 * 6 * 64;  // rows of the S^T digit buffer: a pair of <2,6,7> chunks (>= 6 x 80)
 bool xs_i8_supported(int lp) { return lp % 16 == 0 && lp > 0 && lp <= 128; }
 static int chunk_width(int lp, int mode) {
   const int cap = mode == 1 ? 64 : kMaxChunk;
@@ -590,6 +643,7 @@ static int chunk_width(int lp, int mode) {
 // reads of X one contraction makes (column chunks)
 int xs_i8_x_passes(int lp, bool small_int) {
   const int cw = chunk_width(lp, small_int ? 1 : 0);
+  if (small_int && lp == 2 * cw) return 1;  // the CTA-pair kernel (unless CNMF_I8_PAIR=0)
   return (lp + cw - 1) / cw;
 }
 
@@ -613,14 +667,17 @@ void launch_xs_i8_prepare_x(const float* x, int64_t ldx, int64_t d, int64_t n, i
 }
 
 size_t xs_i8_ws_bytes(int64_t m, int64_t n, int lp, int nsm) {
-  const int np = kMaxChunk;  // either mode: kMaxSD digits of <= 80 columns
+  (void)lp;
+  const int np = kMaxChunk;  // either mode: up to 80 columns per chunk
   const int64_t kmax = std::max(m, n);
   const int64_t kpad = (kmax + kBKB - 1) / kBKB * kBKB;
-  const I8Plan a = i8_plan(m, n, nsm), b = i8_plan(n, m, nsm);
-  const size_t parts = sizeof(double) * (size_t)std::max<int64_t>((int64_t)a.nsplit * m * np,
-                                                                   (int64_t)b.nsplit * n * np);
-  return align256((size_t)kMaxSD * np * kpad) + align256(sizeof(unsigned long long) * 128) +
-         align256(sizeof(double) * 128) + align256(parts) + 1024;
+  int64_t parts = 0;  // K-split partials: single chunks on nsm CTAs, chunk pairs on nsm / 2 clusters
+  for (int workers : {nsm, std::max(1, nsm / 2)}) {
+    const I8Plan a = i8_plan(m, n, workers), b = i8_plan(n, m, workers);
+    parts = std::max(parts, std::max<int64_t>((int64_t)a.nsplit * m, (int64_t)b.nsplit * n) * np * 2);
+  }
+  return align256((size_t)kDigitRows * kpad) + align256(sizeof(unsigned long long) * 256) +
+         align256(sizeof(double) * 256) + align256(sizeof(double) * (size_t)parts) + 1024;
 }
 
 namespace {
@@ -636,11 +693,11 @@ bool launch_xs_i8_chunk(bool tn, const float* x, int64_t ldx, int64_t m, int64_t
   const I8Plan p = i8_plan(rows_out, kdim, nsm);
   uint8_t* base = static_cast<uint8_t*>(ws);
   uint8_t* st_digits = base;
-  base += align256((size_t)kMaxSD * kMaxChunk * ((std::max(m, n) + kBKB - 1) / kBKB * kBKB));
+  base += align256((size_t)kDigitRows * ((std::max(m, n) + kBKB - 1) / kBKB * kBKB));
   unsigned long long* cmax = reinterpret_cast<unsigned long long*>(base);
-  base += align256(sizeof(unsigned long long) * 128);
+  base += align256(sizeof(unsigned long long) * 256);
   double* cscale = reinterpret_cast<double*>(base);
-  base += align256(sizeof(double) * 128);
+  base += align256(sizeof(double) * 256);
   double* parts = reinterpret_cast<double*>(base);
 
   if (cudaMemsetAsync(cmax, 0, sizeof(unsigned long long) * 128, st) != cudaSuccess) return false;
@@ -669,25 +726,24 @@ bool launch_xs_i8_chunk(bool tn, const float* x, int64_t ldx, int64_t m, int64_t
   a.np = np;
   a.out = p.nsplit > 1 ? parts : out;
   a.ldo = p.nsplit > 1 ? w : ldo;
+  a.pair_out = 0;
   a.sx = tn ? sx + m : sx;
   a.cscale = cscale;
   const int units = p.ntiles * p.nsplit;
   const int grid = std::min(units, nsm);
   const int smem = kSX * kXBytes + kSB * sd * np * 128 + 1024;
-  constexpr int kSmemMax = kSX * kXBytes + kSB * 4 * kMaxChunk * 128 + 1024;  // = 6 digits of 64 columns + ...
-  static_assert(kSX * kXBytes + kSB * 6 * 64 * 128 + 1024 <= kSmemMax + 16384, "smem");
   static std::atomic<unsigned> attr[4] = {{0u}, {0u}, {0u}, {0u}};
   note_launches(1);
   auto go = [&](auto kern, std::atomic<unsigned>& at) {
-    smem_attr_once(at, (const void*)kern, 200 * 1024);
+    smem_attr_once(at, (const void*)kern, kSX * kXBytes + kSB * 6 * 64 * 128 + 1024);
     kern<<<grid, kThreadsI8, smem, st>>>(mx, mb, a);
   };
   if (mode == 1) {
-    if (tn) go(xs_i8_kernel<true, 2, 6, 7>, attr[0]);
-    else go(xs_i8_kernel<false, 2, 6, 7>, attr[1]);
+    if (tn) go(xs_i8_kernel<true, 2, 6, 7, false>, attr[0]);
+    else go(xs_i8_kernel<false, 2, 6, 7, false>, attr[1]);
   } else {
-    if (tn) go(xs_i8_kernel<true, 4, 4, 5>, attr[2]);
-    else go(xs_i8_kernel<false, 4, 4, 5>, attr[3]);
+    if (tn) go(xs_i8_kernel<true, 4, 4, 5, false>, attr[2]);
+    else go(xs_i8_kernel<false, 4, 4, 5, false>, attr[3]);
   }
   if (const cudaError_t e = cudaGetLastError(); e != cudaSuccess) {
     std::fprintf(stderr, "xs_i8: launch failed: %s\n", cudaGetErrorString(e));
@@ -698,6 +754,91 @@ bool launch_xs_i8_chunk(bool tn, const float* x, int64_t ldx, int64_t m, int64_t
     i8_split_reduce_kernel<<<(int)std::min<int64_t>((rows_out * w + 255) / 256, (int64_t)nsm * 8), 256, 0,
                              st>>>(parts, p.nsplit, rows_out, w, out, ldo);
   }
+  return true;
+}
+
+// Two equal column chunks in ONE pass over X: clusters of two CTAs, the X
+// stages multicast to both (xs_i8_kernel kPair).  <2, 6, 7> only (C4's 128-wide
+// views of count data: 2 x 64 columns).
+bool launch_xs_i8_pair(bool tn, const float* x, int64_t ldx, int64_t m, int64_t n, const double* s,
+                       int lp, double* out, void* ws, const int* sx, int nsm, cudaStream_t st) {
+  constexpr int sd = 6;
+  const int w = lp / 2, np = w;
+  const int64_t rows_out = tn ? n : m, kdim = tn ? m : n;
+  const int64_t kpad = (kdim + kBKB - 1) / kBKB * kBKB;
+  const int pairs_max = nsm / 2;
+  const I8Plan p = i8_plan(rows_out, kdim, pairs_max);
+  uint8_t* base = static_cast<uint8_t*>(ws);
+  uint8_t* st_digits = base;
+  base += align256((size_t)kDigitRows * ((std::max(m, n) + kBKB - 1) / kBKB * kBKB));
+  unsigned long long* cmax = reinterpret_cast<unsigned long long*>(base);
+  base += align256(sizeof(unsigned long long) * 256);
+  double* cscale = reinterpret_cast<double*>(base);
+  base += align256(sizeof(double) * 256);
+  double* parts = reinterpret_cast<double*>(base);
+
+  if (cudaMemsetAsync(cmax, 0, sizeof(unsigned long long) * 256, st) != cudaSuccess) return false;
+  for (int ch = 0; ch < 2; ++ch) {
+    note_launches(2);
+    s64_colmax_kernel<<<(int)std::max<int64_t>(1, std::min<int64_t>(kdim, (int64_t)nsm * 4)), 128, 0, st>>>(
+        s + ch * w, lp, kdim, w, cmax + 128 * ch);
+    s64_slice_kernel<<<(int)std::min<int64_t>((kpad / 4 * np + 255) / 256, (int64_t)nsm * 16), 256, 0, st>>>(
+        s + ch * w, lp, kdim, w, np, kpad, sd, cmax + 128 * ch,
+        reinterpret_cast<uint32_t*>(st_digits + (size_t)ch * sd * np * kpad), cscale + 128 * ch);
+  }
+  CUtensorMap mx, mb;
+  bool ok = tn ? make_map(&mx, x, m, n, ldx, kBM, kBK, CU_TENSOR_MAP_SWIZZLE_NONE)
+               : make_map(&mx, x, m, n, ldx, kBK, kBM, CU_TENSOR_MAP_SWIZZLE_128B);
+  ok = ok && make_map_u8(&mb, st_digits, (int64_t)2 * sd * np, kpad, kBKB, np);
+  if (!ok) return false;
+  I8Args a;
+  a.rows_out = rows_out;
+  a.kdim = kdim;
+  a.kchunk = p.kchunk;
+  a.ntiles = p.ntiles;
+  a.nsplit = p.nsplit;
+  a.lp = w;
+  a.np = np;
+  a.out = p.nsplit > 1 ? parts : out;
+  a.ldo = p.nsplit > 1 ? w : lp;
+  a.pair_out = p.nsplit > 1 ? (int64_t)p.nsplit * rows_out * w : w;
+  a.sx = tn ? sx + m : sx;
+  a.cscale = cscale;
+  const int units = p.ntiles * p.nsplit;
+  const int pairs = std::min(units, pairs_max);
+  const int smem = kSX * kXBytes + kSB * sd * np * 128 + 1024;
+  static std::atomic<unsigned> attr_tn{0u}, attr_nn{0u};
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(2 * pairs);
+  cfg.blockDim = dim3(kThreadsI8);
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = st;
+  cudaLaunchAttribute at[1];
+  at[0].id = cudaLaunchAttributeClusterDimension;
+  at[0].val.clusterDim.x = 2;
+  at[0].val.clusterDim.y = 1;
+  at[0].val.clusterDim.z = 1;
+  cfg.attrs = at;
+  cfg.numAttrs = 1;
+  note_launches(1);
+  cudaError_t e;
+  if (tn) {
+    smem_attr_once(attr_tn, (const void*)(xs_i8_kernel<true, 2, 6, 7, true>), kSX * kXBytes + kSB * 6 * 64 * 128 + 1024);
+    e = cudaLaunchKernelEx(&cfg, xs_i8_kernel<true, 2, 6, 7, true>, mx, mb, a);
+  } else {
+    smem_attr_once(attr_nn, (const void*)(xs_i8_kernel<false, 2, 6, 7, true>), kSX * kXBytes + kSB * 6 * 64 * 128 + 1024);
+    e = cudaLaunchKernelEx(&cfg, xs_i8_kernel<false, 2, 6, 7, true>, mx, mb, a);
+  }
+  if (e != cudaSuccess || (e = cudaGetLastError()) != cudaSuccess) {
+    std::fprintf(stderr, "xs_i8: paired launch failed: %s\n", cudaGetErrorString(e));
+    return false;
+  }
+  if (p.nsplit > 1)
+    for (int ch = 0; ch < 2; ++ch) {
+      note_launches(1);
+      i8_split_reduce_kernel<<<(int)std::min<int64_t>((rows_out * w + 255) / 256, (int64_t)nsm * 8), 256, 0,
+                               st>>>(parts + (int64_t)ch * a.pair_out, p.nsplit, rows_out, w, out + ch * w, lp);
+    }
   return true;
 }
 
@@ -716,6 +857,9 @@ bool launch_xs_i8(bool tn, const float* x, int64_t ldx, int64_t m, int64_t n, co
   if (!xs_i8_supported(lp) || (ldx % 4) != 0 || (reinterpret_cast<uintptr_t>(x) & 15)) return false;
   const int mode = small_int ? 1 : 0;
   const int cw = chunk_width(lp, mode);
+  static const bool no_pair = [] { const char* e = std::getenv("CNMF_I8_PAIR"); return e && std::string(e) == "0"; }();
+  if (mode == 1 && lp == 2 * cw && nsm >= 2 && !no_pair)  // one pass over X for both chunks
+    return launch_xs_i8_pair(tn, x, ldx, m, n, s, lp, out, ws, sx, nsm, st);
   for (int c0 = 0; c0 < lp; c0 += cw) {
     const int w = std::min(cw, lp - c0);
     if (!launch_xs_i8_chunk(tn, x, ldx, m, n, s + c0, lp, w, mode, out + c0, lp, ws, sx, nsm, st))
