@@ -641,9 +641,13 @@ static int chunk_width(int lp, int mode) {
 }
 
 // reads of X one contraction makes (column chunks)
+static bool i8_pair_enabled() {  // read per call (tests switch it)
+  const char* e = std::getenv("CNMF_I8_PAIR");
+  return e && std::string(e) == "1";
+}
 int xs_i8_x_passes(int lp, bool small_int) {
   const int cw = chunk_width(lp, small_int ? 1 : 0);
-  if (small_int && lp == 2 * cw) return 1;  // the CTA-pair kernel (unless CNMF_I8_PAIR=0)
+  if (small_int && lp == 2 * cw && i8_pair_enabled()) return 1;
   return (lp + cw - 1) / cw;
 }
 
@@ -857,8 +861,11 @@ bool launch_xs_i8(bool tn, const float* x, int64_t ldx, int64_t m, int64_t n, co
   if (!xs_i8_supported(lp) || (ldx % 4) != 0 || (reinterpret_cast<uintptr_t>(x) & 15)) return false;
   const int mode = small_int ? 1 : 0;
   const int cw = chunk_width(lp, mode);
-  static const bool no_pair = [] { const char* e = std::getenv("CNMF_I8_PAIR"); return e && std::string(e) == "0"; }();
-  if (mode == 1 && lp == 2 * cw && nsm >= 2 && !no_pair)  // one pass over X for both chunks
+  // CNMF_I8_PAIR=1: both chunks in one pass over X (CTA pairs, TMA multicast).
+  // Opt-in: half the DRAM traffic but no faster -- the kernel is bound by its
+  // per-block operand hand-off, not by HBM (C4: 9.0 ms per 128-wide contraction
+  // against 2 x 4.1 ms for the two chunk passes).
+  if (mode == 1 && lp == 2 * cw && nsm >= 2 && i8_pair_enabled())
     return launch_xs_i8_pair(tn, x, ldx, m, n, s, lp, out, ws, sx, nsm, st);
   for (int c0 = 0; c0 < lp; c0 += cw) {
     const int w = std::min(cw, lp - c0);

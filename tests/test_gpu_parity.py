@@ -198,12 +198,18 @@ def test_xstream_int8_sliced_contraction(ctx, d, n, l):
             assert rel_fro(host(got), ref) < tol, (tn, tol, rel_fro(host(got), ref))
 
 
-@pytest.mark.parametrize("d,n,l", [(1000, 1000, 128), (333, 517, 16), (700, 4100, 112), (2049, 1500, 64)])
-def test_xstream_int8_small_integer_x(ctx, d, n, l):
+@pytest.mark.parametrize("d,n,l,pair", [(1000, 1000, 128, False), (333, 517, 16, False),
+                                        (700, 4100, 112, False), (2049, 1500, 64, False),
+                                        (1000, 1000, 128, True), (5000, 3000, 128, True)])
+def test_xstream_int8_small_integer_x(ctx, d, n, l, pair, monkeypatch):
     """Count data (integers below 8192) is exact in two int8 digits, so s takes
     six (40 bits below its column maximum) and every digit pair is kept: the
     products are exact and heavy-tailed columns of s (as the bases of count
-    data have) keep ~1e-10; sketches wider than 64 columns run as chunks."""
+    data have) keep ~1e-10; sketches wider than 64 columns run as chunks, or
+    (pair: CNMF_I8_PAIR=1) as clusters of two CTAs sharing each X stage by TMA
+    multicast, one chunk per CTA."""
+    if pair:
+        monkeypatch.setenv("CNMF_I8_PAIR", "1")
     rng = np.random.default_rng(d + n + l)
     x = rng.poisson(rng.gamma(0.3, 4.0, size=(d, 1)) * rng.gamma(0.3, 4.0, size=(1, n))).astype(np.float32)
     x[rng.random((d, n)) < 1e-3] = 8191.0
