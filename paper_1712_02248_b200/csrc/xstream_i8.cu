@@ -314,6 +314,26 @@ __global__ void __launch_bounds__(kThreadsI8, 1)
         tc_fence_after();
         const uint32_t a0 = tmem + a_off + kASlot * (uint32_t)o;
         const uint64_t bd = smem_desc(b_addr(b) + 32u * (uint32_t)sub, 16, 1024, 2);
+#ifdef I8_MERGE  // measured and rejected: C3 2.9 -> 3.7 ms per contraction, C4 no better
+        if (fresh == 0u) {
+          // Later blocks of a unit: the S digits t = 0 .. of one X digit s are
+          // contiguous in the stage and their accumulators (classes s + t) in
+          // tensor memory, so x_s [e_t | e_t+1 | ...] is ONE MMA of up to 256
+          // columns -- 4 instead of 12 (<2,6,7>) or 6 instead of 13 (<4,4,5>)
+          // instructions and reads of the A digit per block.
+          const int gmax = 256 / np;
+#pragma unroll
+          for (int s = 0; s < XD; ++s) {
+            const int tcount = (NC - s) < SD ? (NC - s) : SD;
+            for (int t = 0; t < tcount; t += gmax) {
+              const int g = (tcount - t) < gmax ? (tcount - t) : gmax;
+              mma_i8_ts_elect(tmem + (uint32_t)((s + t) * np), a0 + 8u * s,
+                              bd + (uint64_t)((t * slice_bytes) >> 4), idesc_i8(g * np), 1u);
+            }
+          }
+        } else
+#endif
+        {
 #pragma unroll
         for (int w = 0; w < NC; ++w) {
 #pragma unroll
@@ -324,6 +344,7 @@ __global__ void __launch_bounds__(kThreadsI8, 1)
                             bd + (uint64_t)((t * slice_bytes) >> 4), idesc, ((fresh >> w) & 1u) ^ 1u);
             fresh &= ~(1u << w);
           }
+        }
         }
         commit_elect(&opempty[o]);
         if (++o == kSO) {
