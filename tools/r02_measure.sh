@@ -18,4 +18,8 @@ timeout 900 $NCU --set full --import-source on --clock-control none -k regex:xs_
 $NCU -i gpurun_out/xs_c4.ncu-rep --page details --csv > gpurun_out/xs_c4_details.csv 2>/dev/null; rm -f gpurun_out/xs_c4.ncu-rep
 timeout 900 $NCU --set full --clock-control none -k regex:xs_i8_kernel -s 1 -c 2 -o gpurun_out/xs64_c3 -f python bench.py --config c3 --steps 1 --warmup 0 --no-cpu-baseline --no-e2e > gpurun_out/xs64_ncu.log 2>&1; echo "xs64 ncu rc=$?"
 $NCU -i gpurun_out/xs64_c3.ncu-rep --page details --csv > gpurun_out/xs64_c3_details.csv 2>/dev/null; rm -f gpurun_out/xs64_c3.ncu-rep
+timeout 900 $NCU --set full --clock-control none -k regex:xs_i8_kernel -s 1 -c 2 -o gpurun_out/xsi8_c4 -f python bench.py --steps 1 --warmup 0 --no-cpu-baseline --no-e2e > gpurun_out/xsi8_c4_ncu.log 2>&1; echo "xs_i8 c4 ncu rc=$?"
+$NCU -i gpurun_out/xsi8_c4.ncu-rep --page details --csv > gpurun_out/xsi8_c4_details.csv 2>/dev/null; rm -f gpurun_out/xsi8_c4.ncu-rep
+timeout 900 $NCU --metrics gpu__time_duration.sum --clock-control none --csv --log-file gpurun_out/r02_c3_launches.csv python bench.py --config c3 --steps 1 --warmup 0 --no-cpu-baseline --no-e2e > /dev/null 2>&1; echo "c3 launches rc=$?"
+python tools/launch_summary.py gpurun_out/r02_c3_launches.csv > gpurun_out/r02_c3_launch_summary.txt 2>&1
 ls -la gpurun_out; du -sh gpurun_out
