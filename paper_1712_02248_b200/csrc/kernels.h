@@ -255,6 +255,7 @@ size_t xs64_ws_doubles(int64_t m, int64_t n, int lp, int nsm);
 // (lp a multiple of 16, <= 128; 16-byte aligned rows).  small_int: X holds only integers below
 // 8192 and sx is zero (exact two-digit X, six digits of S).
 bool xs_i8_supported(int lp);
+void xs_i8_set_debug(unsigned long long* dbg);  // tools/i8_trace.cu only (I8_TRACE builds)
 size_t xs_i8_sx_ints(int64_t d, int64_t n);
 int xs_i8_x_passes(int lp, bool small_int);
 size_t xs_i8_ws_bytes(int64_t m, int64_t n, int lp, int nsm);

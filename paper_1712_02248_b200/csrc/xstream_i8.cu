@@ -79,7 +79,23 @@ constexpr int kXBytes = kBM * kBK * 4;
 constexpr int kMaxSD = 6;
 __host__ __device__ constexpr int q_bits(int digits) { return 7 * digits - 2; }  // |q| < 2^(7 D - 2)
 
+// I8_TRACE builds (tools/i8_trace.cu only): per-K-block event times of CTA 0,
+// uint64 [event][block]: 0 X issue, 1 split got X, 2 digits done, 3 split got
+// its A slot, 4 tensor-memory store done, 5 MMA got operands, 6 MMA issued.
+#ifdef I8_TRACE
+#define I8_EV(ev, blk)                                                                  \
+  do {                                                                                  \
+    const int blk_ = (blk);                                                             \
+    if (blockIdx.x == 0 && args.dbg && blk_ < 4096) args.dbg[(ev) * 4096 + blk_] = clock64(); \
+  } while (0)
+#else
+#define I8_EV(ev, blk) \
+  do {                 \
+  } while (0)
+#endif
+
 struct I8Args {
+  unsigned long long* dbg;     // trace buffer (I8_TRACE builds), else null
   int64_t rows_out, kdim, kchunk;
   int ntiles, nsplit, lp, np;  // np: lp rounded up to 16 (MMA N)
   double* out;                 // [nsplit][rows_out] rows of ldo doubles (lp columns written)
@@ -243,6 +259,7 @@ __global__ void __launch_bounds__(kThreadsI8, 1)
     // TN 128 (columns of X) x 32 (k) boxes, unswizzled ----------------
     if (lane == 0) {
       int s = 0;
+      [[maybe_unused]] int tblk = 0;
       uint32_t ph = 0;
       for (int u = wid; u < units; u += wstride) {
         int64_t k0, k1;
@@ -253,6 +270,7 @@ __global__ void __launch_bounds__(kThreadsI8, 1)
           if constexpr (kPair) {
             if (rank == 0) mbar_wait(&xpeer[s], ph ^ 1);
           }
+          I8_EV(0, tblk++);
           mbar_expect_tx(&xfull[s], kXBytes);
           if constexpr (kPair) {
             if (rank == 0) {  // one load for both CTAs: same offsets, each CTA's own xfull
@@ -299,6 +317,7 @@ __global__ void __launch_bounds__(kThreadsI8, 1)
   } else if (warp == kWarpMMA) {
     // ---------------- MMA issuer: thirteen digit-pair products per block -----
     const uint32_t idesc = idesc_i8(np);
+    [[maybe_unused]] int mblk = 0;
     int o = 0, b = 0;
     uint32_t oph = 0, bph = 0, aph = 0;
     for (int u = wid; u < units; u += wstride) {
@@ -311,6 +330,7 @@ __global__ void __launch_bounds__(kThreadsI8, 1)
       for (int64_t kk = k0; kk < k1; kk += kBK) {
         mbar_wait_warp(&opready[o], oph);
         if (sub == 0) mbar_wait_warp(&bfull[b], bph);
+        if (lane == 0) I8_EV(5, mblk);
         tc_fence_after();
         const uint32_t a0 = tmem + a_off + kASlot * (uint32_t)o;
         const uint64_t bd = smem_desc(b_addr(b) + 32u * (uint32_t)sub, 16, 1024, 2);
@@ -347,6 +367,8 @@ __global__ void __launch_bounds__(kThreadsI8, 1)
         }
         }
         commit_elect(&opempty[o]);
+        if (lane == 0) I8_EV(6, mblk);
+        ++mblk;
         if (++o == kSO) {
           o = 0;
           oph ^= 1;
@@ -379,6 +401,7 @@ __global__ void __launch_bounds__(kThreadsI8, 1)
       for (int64_t kk = k0; kk < k1; kk += kBK, ++nblk) {
         if ((nblk & 1) == set) {
           mbar_wait_warp(&xfull[s], xph);
+          if (q == 0 && lane == 0) I8_EV(1, nblk);
           float v[32];
           if (!kTN) {
             const uint32_t rowa = x_addr(s) + r * 128;
@@ -410,11 +433,14 @@ __global__ void __launch_bounds__(kThreadsI8, 1)
               pk[8 * d + j] = __byte_perm(lo, hi, 0x5410);
             }
           }
+          if (q == 0 && lane == 0) I8_EV(2, nblk);
           mbar_wait_warp(&opempty[o], oph ^ 1);
+          if (q == 0 && lane == 0) I8_EV(3, nblk);
           tc_fence_after();
           if constexpr (XD == 4) tmem_st32(tmem + ((uint32_t)(32 * q) << 16) + a_off + kASlot * (uint32_t)o, pk);
           else tmem_st16(tmem + ((uint32_t)(32 * q) << 16) + a_off + kASlot * (uint32_t)o, pk);
           asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
+          if (q == 0 && lane == 0) I8_EV(4, nblk);
           tc_fence_before();
           __syncwarp();
           // released only after the values were consumed (see xstream_tc.cu)
@@ -646,6 +672,8 @@ bool make_map_u8(CUtensorMap* m, const void* base, int64_t rows, int64_t cols, i
 
 size_t align256(size_t b) { return (b + 255) & ~size_t(255); }
 
+unsigned long long* g_i8_debug = nullptr;
+
 }  // namespace
 
 // Tensor memory bounds the column chunk: <4, 4, 5> five accumulators of w
@@ -654,6 +682,8 @@ size_t align256(size_t b) { return (b + 255) & ~size_t(255); }
 // column chunks (one X pass each).
 constexpr int kMaxChunk = 80;
 constexpr int kDigitRows = 2 * 6 * 64;  // rows of the S^T digit buffer: a pair of <2,6,7> chunks (>= 6 x 80)
+void xs_i8_set_debug(unsigned long long* dbg) { g_i8_debug = dbg; }  // tools/i8_trace.cu only
+
 bool xs_i8_supported(int lp) { return lp % 16 == 0 && lp > 0 && lp <= 128; }
 static int chunk_width(int lp, int mode) {
   const int cap = mode == 1 ? 64 : kMaxChunk;
@@ -742,6 +772,7 @@ bool launch_xs_i8_chunk(bool tn, const float* x, int64_t ldx, int64_t m, int64_t
     return false;
   }
   I8Args a;
+  a.dbg = g_i8_debug;
   a.rows_out = rows_out;
   a.kdim = kdim;
   a.kchunk = p.kchunk;
@@ -817,6 +848,7 @@ bool launch_xs_i8_pair(bool tn, const float* x, int64_t ldx, int64_t m, int64_t 
   ok = ok && make_map_u8(&mb, st_digits, (int64_t)2 * sd * np, kpad, kBKB, np);
   if (!ok) return false;
   I8Args a;
+  a.dbg = g_i8_debug;
   a.rows_out = rows_out;
   a.kdim = kdim;
   a.kchunk = p.kchunk;
