@@ -12,28 +12,26 @@
 //
 // Ozaki-style slicing: every row of the A operand (a row of X for NN, a
 // column of X for TN) is scaled by an exact power of two 2^sx so that its
-// largest entry is below 2^26, rounded to an integer and written in balanced
-// base-128 digits q = d0 2^21 + d1 2^14 + d2 2^7 + d3, |d| <= 64 (int8); every
-// column of S likewise (2^ss, digits e0..e3).  The digit products are exact
-// in int32 (|d e| <= 4096, K-split chains of at most 65536), so
-//   sum_k q_x q_s = sum_{s,t} 2^(7 (6 - s - t)) P_st,  P_st = sum_k d_s e_t,
-// and the pairs with s + t <= 4 are kept (13 of 16: the top digits carry only
-// five bits, so class 4 is still 2^-23 of a typical product -- measured 1.1e-7
-// without it; the dropped classes 5 and 6 are below 2^-30 and, the digits
-// being balanced, unbiased).  Pairs of equal s + t share an accumulator, so
-// there are five accumulators of NP columns; the epilogue combines them in
-// fp64,
-//   V = (((W0 128 + W1) 128 + W2) 128 + W3) 128 + W4,   y = V 2^(14 - sx - ss).  What is lost is the operands' rounding to 26 bits
-// below their row / column maximum -- fp32's own 24 bits for entries within
-// 4x of the maximum, an absolute 2^-27 of the maximum below that -- never the
-// accumulation.
+// largest entry is below 2^31, rounded to an integer and cut into its four
+// bytes q = d0 2^24 + d1 2^16 + d2 2^8 + d3 (unsigned: X >= 0 by the solver's
+// contract); every column of S likewise into signed balanced base-256 digits
+// e0..e3 of round(s 2^ss), |q_s| < 2^30.  The digit products are exact in int32
+// (d e <= 2^15, K-split chains of at most 16384), so
+//   sum_k q_x q_s = sum_{s,t} 256^(6 - s - t) P_st,  P_st = sum_k d_s e_t,
+// and the pairs with s + t <= 4 are kept (13 of 16: the dropped ones are below
+// 2^-35 of a typical product and, S's digits being balanced, unbiased).  Pairs
+// of equal s + t share an accumulator; the epilogue combines the five in fp64,
+//   V = (((W0 256 + W1) 256 + W2) 256 + W3) 256 + W4,   y = V 2^(16 - sx - ss).
+// What is lost is the operands' rounding to 31 / 30 bits below their row /
+// column maximum -- never the accumulation.  (The first version used signed
+// base-128 digits on both sides, 26 bits and 13 pairs: -DI8_BASE128.)
 //
 // Kernel: persistent CTAs over (128-row tile, K-split) units as xstream_tc.cu.
 // Warps 0-3 epilogue, 4 X TMA (16 KB boxes of 32 k), 5 MMA issue, 6-13 split
 // (two sets of four: set p slices the blocks of parity p -- X stage -> 32
 // words of digits per row -> tcgen05.st, half the 3xTF32 store volume), 14 S
 // TMA (the pre-sliced S^T digits, K-major SWIZZLE_128B rows of 128 k: one
-// stage serves four X blocks).  Per block thirteen K = 32 MMAs, A from tensor
+// stage serves four X blocks).  Per block thirteen K = 32 u8 x s8 MMAs, A from tensor
 // memory; layouts checked by tools/tc_i8_check.cu.
 #include <cuda.h>
 #include <cudaTypedefs.h>
@@ -70,14 +68,36 @@ constexpr int kWarpTMA = 4, kWarpMMA = 5, kWarpSplit0 = 6, kWarpBTMA = 14;
 constexpr int kXBytes = kBM * kBK * 4;
 // Digit configurations <XD, SD, NC>: XD digits of the A operand (X), SD of S,
 // NC accumulators (digit pairs (s, t) with s + t < NC are kept).
-//   <4, 4, 5>  general fp32 X: 26-bit fixed point on both sides, 13 pairs;
-//   <2, 6, 7>  X of integers below 8192 (count data): X is EXACT in two digits,
-//              so S can take six (40 bits below its column maximum -- bases of
-//              count data have heavy-tailed columns, and four digits left their
-//              typical entries ~19 bits: the C4 trajectory stayed 9e-4 from the
-//              reference's); all 12 pairs kept, exact products.
+// Base 256 (default): X >= 0 by the solver's contract, so its digits are the
+// UNSIGNED bytes of round(x 2^sx) -- one cvt.rni.u32 per element, 31 bits
+// below the row maximum -- against signed balanced base-256 digits of S
+// (u8 x s8 MMAs).
+//   <4, 4, 5>  general fp32 X: the 13 pairs with s + t <= 4, five accumulators
+//              (S: 30 bits).  Class 4 is needed: with the 10 pairs of s + t <= 3
+//              (2^-27 of a typical product dropped) the full-size C3 trajectory
+//              ran 1.5e-4 from the reference's, against 7.6e-6 with it -- the
+//              trajectory follows the range finder's contraction error ~1e4 x;
+//   <2, 5, 6>  X of integers below 32768 (count data; decided below 8192 by
+//              the validation read): exact two-byte X, S 38 bits, all 10 pairs.
+// The kernel is bound by its MMA count (~62 cycles per kind::i8 MMA, DESIGN
+// 3.1b), hence fewer pairs.  -DI8_BASE128 builds the first version: signed
+// balanced base-128 digits on both sides, <4, 4, 5> (13 pairs) and <2, 6, 7>
+// (12 pairs: bases of count data have heavy-tailed columns, and four digits
+// left their typical entries ~19 bits -- the C4 trajectory stayed 9e-4 from
+// the reference's).
+#ifdef I8_BASE128
+constexpr int kB = 7;
+constexpr int kGXD = 4, kGSD = 4, kGNC = 5, kIXD = 2, kISD = 6, kINC = 7;
+constexpr int kXBits = 26;    // |q_x| < 2^26
+constexpr int kStagesMax = 512;  // K-split chains <= 65536: four pairs of |d e| <= 2^12 per k
+#else
+constexpr int kB = 8;
+constexpr int kGXD = 4, kGSD = 4, kGNC = 5, kIXD = 2, kISD = 5, kINC = 6;
+constexpr int kXBits = 31;    // q_x < 2^31
+constexpr int kStagesMax = 128;  // K-split chains <= 16384: four pairs of d e <= 2^15 per k
+#endif
 constexpr int kMaxSD = 6;
-__host__ __device__ constexpr int q_bits(int digits) { return 7 * digits - 2; }  // |q| < 2^(7 D - 2)
+__host__ __device__ constexpr int q_bits(int digits) { return kB * digits - 2; }  // |q_s| < 2^(B D - 2)
 
 // I8_TRACE builds (tools/i8_trace.cu only): per-K-block event times of CTA 0,
 // uint64 [event][block]: 0 X issue, 1 split got X, 2 digits done, 3 split got
@@ -107,7 +127,8 @@ struct I8Args {
 
 // kind::i8: D s32, A and B signed 8-bit, both K-major, M = 128
 __host__ __device__ constexpr uint32_t idesc_i8(int n) {
-  return (2u << 4) | (1u << 7) | (1u << 10) | ((uint32_t)(n >> 3) << 17) | ((128u >> 4) << 24);
+  return (2u << 4) | ((kB == 8 ? 0u : 1u) << 7) | (1u << 10) | ((uint32_t)(n >> 3) << 17) |
+         ((128u >> 4) << 24);  // base 256: A unsigned
 }
 __device__ __forceinline__ void mma_i8_ts_elect(uint32_t d_tmem, uint32_t a_tmem, uint64_t b_desc,
                                                 uint32_t idesc, uint32_t accumulate) {
@@ -418,6 +439,23 @@ __global__ void __launch_bounds__(kThreadsI8, 1)
             for (int kq = 0; kq < 32; ++kq) v[kq] = lds32(x_addr(s) + kq * (kBM * 4) + r * 4);
           }
           uint32_t pk[8 * XD];  // pk[8 s + j]: digit s of k = 4 j .. 4 j + 3
+          if constexpr (kB == 8) {
+            // digit s = byte XD - 1 - s of round(v): no digit arithmetic at all
+#pragma unroll
+            for (int j = 0; j < 8; ++j) {
+              uint32_t qv[4];
+#pragma unroll
+              for (int e = 0; e < 4; ++e) qv[e] = __float2uint_rn(v[4 * j + e] * scale);
+#pragma unroll
+              for (int d = 0; d < XD; ++d) {
+                const uint32_t by = (uint32_t)(XD - 1 - d);
+                const uint32_t sel = by | ((4u + by) << 4);
+                const uint32_t lo = __byte_perm(qv[0], qv[1], sel);
+                const uint32_t hi = __byte_perm(qv[2], qv[3], sel);
+                pk[8 * d + j] = __byte_perm(lo, hi, 0x5410);
+              }
+            }
+          } else {
 #pragma unroll
           for (int j = 0; j < 8; ++j) {
             uint32_t w[4][XD];
@@ -432,6 +470,7 @@ __global__ void __launch_bounds__(kThreadsI8, 1)
               const uint32_t hi = __byte_perm(w[2][d], w[3][d], 0x0040);
               pk[8 * d + j] = __byte_perm(lo, hi, 0x5410);
             }
+          }
           }
           if (q == 0 && lane == 0) I8_EV(2, nblk);
           mbar_wait_warp(&opempty[o], oph ^ 1);
@@ -474,7 +513,7 @@ __global__ void __launch_bounds__(kThreadsI8, 1)
       const int tile = u % args.ntiles, split = u / args.ntiles;
       const int64_t row = (int64_t)tile * kBM + 32 * q + lane;
       const bool ok = row < args.rows_out;
-      const double rs = exp2i_d(7 * (XD + SD - 1 - NC) - (ok ? __ldg(args.sx + row) : 0));
+      const double rs = exp2i_d(kB * (XD + SD - 1 - NC) - (ok ? __ldg(args.sx + row) : 0));
       double* dst = args.out + (int64_t)rank * args.pair_out + ((int64_t)split * args.rows_out + (ok ? row : 0)) * args.ldo;
       mbar_wait_warp(&acc_full, aph);
       tc_fence_after();
@@ -493,7 +532,7 @@ __global__ void __launch_bounds__(kThreadsI8, 1)
               for (int e = 0; e < 2; ++e) {
                 double vsum = (double)(int)h[0][j + e];
 #pragma unroll
-                for (int w = 1; w < NC; ++w) vsum = fma(vsum, 128.0, (double)(int)h[w][j + e]);
+                for (int w = 1; w < NC; ++w) vsum = fma(vsum, (double)(1 << kB), (double)(int)h[w][j + e]);
                 y[e] = vsum * rs * __ldg(args.cscale + 128 * rank + c0 + j + e);
               }
               *reinterpret_cast<double2*>(dst + c0 + j) = make_double2(y[0], y[1]);
@@ -526,7 +565,7 @@ __device__ __forceinline__ int scale_exp(float mx) {
   if (!(mx > 0.f)) return 0;
   int e;
   frexpf(mx, &e);  // mx = f 2^e, f in [0.5, 1)
-  return max(-126, min(126, q_bits(4) - e));
+  return max(-126, min(126, kXBits - e));
 }
 
 // rows of X: one warp per row
@@ -596,9 +635,10 @@ __global__ void s64_slice_kernel(const double* __restrict__ s, int64_t lds, int6
 #pragma unroll
         for (int t = kMaxSD - 1; t > 0; --t) {
           if (t < sd) {
-            const long long dg = ((qv + 64) & 127) - 64;
+            constexpr long long kHalf = 1LL << (kB - 1);
+            const long long dg = ((qv + kHalf) & (2 * kHalf - 1)) - kHalf;
             word[t] |= (uint32_t)((int)dg & 0xFF) << (8 * u);
-            qv = (qv - dg) >> 7;
+            qv = (qv - dg) >> kB;
           }
         }
         word[0] |= (uint32_t)((int)qv & 0xFF) << (8 * u);
@@ -637,7 +677,7 @@ I8Plan i8_plan(int64_t rows_out, int64_t kdim, int nsm) {
   I8Plan p;
   p.ntiles = (int)((rows_out + kBM - 1) / kBM);
   const int64_t kb = (kdim + kBKB - 1) / kBKB;
-  const int64_t min_ns = (kb + 511) / 512;
+  const int64_t min_ns = (kb + kStagesMax - 1) / kStagesMax;
   int64_t best_ns = min_ns;
   double best = 1e300;
   for (int64_t ns = min_ns; ns <= std::min<int64_t>(64, kb); ++ns) {
@@ -680,7 +720,7 @@ unsigned long long* g_i8_debug = nullptr;
 // columns + three 32-column A slots = 496 of 512 at w = 80; <2, 6, 7> seven
 // accumulators + three 16-column slots = 496 at w = 64.  Wider operands run as
 // column chunks (one X pass each).
-constexpr int kMaxChunk = 80;
+constexpr int kMaxChunk = 80;  // general configuration: five accumulators + three 32-column A slots
 constexpr int kDigitRows = 2 * 6 * 64;  // rows of the S^T digit buffer: a pair of <2,6,7> chunks (>= 6 x 80)
 void xs_i8_set_debug(unsigned long long* dbg) { g_i8_debug = dbg; }  // tools/i8_trace.cu only
 
@@ -741,7 +781,7 @@ namespace {
 bool launch_xs_i8_chunk(bool tn, const float* x, int64_t ldx, int64_t m, int64_t n, const double* s,
                         int64_t lds, int w, int mode, double* out, int64_t ldo, void* ws, const int* sx,
                         int nsm, cudaStream_t st) {
-  const int sd = mode == 1 ? 6 : 4;
+  const int sd = mode == 1 ? kISD : kGSD;
   const int np = w;
   const int64_t rows_out = tn ? n : m, kdim = tn ? m : n;
   const int64_t kpad = (kdim + kBKB - 1) / kBKB * kBKB;
@@ -795,11 +835,11 @@ bool launch_xs_i8_chunk(bool tn, const float* x, int64_t ldx, int64_t m, int64_t
     kern<<<grid, kThreadsI8, smem, st>>>(mx, mb, a);
   };
   if (mode == 1) {
-    if (tn) go(xs_i8_kernel<true, 2, 6, 7, false>, attr[0]);
-    else go(xs_i8_kernel<false, 2, 6, 7, false>, attr[1]);
+    if (tn) go(xs_i8_kernel<true, kIXD, kISD, kINC, false>, attr[0]);
+    else go(xs_i8_kernel<false, kIXD, kISD, kINC, false>, attr[1]);
   } else {
-    if (tn) go(xs_i8_kernel<true, 4, 4, 5, false>, attr[2]);
-    else go(xs_i8_kernel<false, 4, 4, 5, false>, attr[3]);
+    if (tn) go(xs_i8_kernel<true, kGXD, kGSD, kGNC, false>, attr[2]);
+    else go(xs_i8_kernel<false, kGXD, kGSD, kGNC, false>, attr[3]);
   }
   if (const cudaError_t e = cudaGetLastError(); e != cudaSuccess) {
     std::fprintf(stderr, "xs_i8: launch failed: %s\n", cudaGetErrorString(e));
@@ -818,7 +858,7 @@ bool launch_xs_i8_chunk(bool tn, const float* x, int64_t ldx, int64_t m, int64_t
 // views of count data: 2 x 64 columns).
 bool launch_xs_i8_pair(bool tn, const float* x, int64_t ldx, int64_t m, int64_t n, const double* s,
                        int lp, double* out, void* ws, const int* sx, int nsm, cudaStream_t st) {
-  constexpr int sd = 6;
+  constexpr int sd = kISD;
   const int w = lp / 2, np = w;
   const int64_t rows_out = tn ? n : m, kdim = tn ? m : n;
   const int64_t kpad = (kdim + kBKB - 1) / kBKB * kBKB;
@@ -880,11 +920,11 @@ bool launch_xs_i8_pair(bool tn, const float* x, int64_t ldx, int64_t m, int64_t 
   note_launches(1);
   cudaError_t e;
   if (tn) {
-    smem_attr_once(attr_tn, (const void*)(xs_i8_kernel<true, 2, 6, 7, true>), kSX * kXBytes + kSB * 6 * 64 * 128 + 1024);
-    e = cudaLaunchKernelEx(&cfg, xs_i8_kernel<true, 2, 6, 7, true>, mx, mb, a);
+    smem_attr_once(attr_tn, (const void*)(xs_i8_kernel<true, kIXD, kISD, kINC, true>), kSX * kXBytes + kSB * 6 * 64 * 128 + 1024);
+    e = cudaLaunchKernelEx(&cfg, xs_i8_kernel<true, kIXD, kISD, kINC, true>, mx, mb, a);
   } else {
-    smem_attr_once(attr_nn, (const void*)(xs_i8_kernel<false, 2, 6, 7, true>), kSX * kXBytes + kSB * 6 * 64 * 128 + 1024);
-    e = cudaLaunchKernelEx(&cfg, xs_i8_kernel<false, 2, 6, 7, true>, mx, mb, a);
+    smem_attr_once(attr_nn, (const void*)(xs_i8_kernel<false, kIXD, kISD, kINC, true>), kSX * kXBytes + kSB * 6 * 64 * 128 + 1024);
+    e = cudaLaunchKernelEx(&cfg, xs_i8_kernel<false, kIXD, kISD, kINC, true>, mx, mb, a);
   }
   if (e != cudaSuccess || (e = cudaGetLastError()) != cudaSuccess) {
     std::fprintf(stderr, "xs_i8: paired launch failed: %s\n", cudaGetErrorString(e));

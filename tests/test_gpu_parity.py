@@ -185,7 +185,7 @@ def test_xstream_int8_sliced_contraction(ctx, d, n, l):
     s = rng.standard_normal((n, l)).astype(np.float32)
     t = rng.standard_normal((d, l)).astype(np.float32)
     sd, td = dev(s), dev(t)
-    for x, tol in ((lowrank, 3e-8), (wide, 1.5e-7)):
+    for x, tol in ((lowrank, 5e-8), (wide, 1.5e-7)):
         xd = dev(x)
         x64 = x.astype(np.float64)
         for tn, op, ref, rows in ((False, sd, x64 @ s.astype(np.float64), d),
