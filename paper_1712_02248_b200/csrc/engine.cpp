@@ -298,6 +298,9 @@ struct XView {
   bool integral = false;         // every element an integer below 2^26: the int8-sliced
                                  // contractions need no row / column scaling
   bool small_int = false;        // ... and below 8192: exact in two int8 digits
+  bool nonneg = false;           // validated entrywise non-negative and finite (a run's
+                                 // check_data): the int8-sliced kernel's unsigned X digits
+                                 // need it; the step API's unvalidated X keeps FP64 DMMA
 };
 
 // The X contractions' fp16 hi/lo path (xstream_tc.cu) is opt-in:
@@ -491,7 +494,7 @@ int build_projectors_dev(cnmf_context* c, const XView& X, int q, int lp, uint64_
   }
   c->last_rf64 = use64 ? 1 : 0;
   c->rf_sx = nullptr;
-  if (use64 && xs_i8_supported(lp) && (X.ldx % 4) == 0 && !rf64_dmma()) {
+  if (use64 && X.nonneg && xs_i8_supported(lp) && (X.ldx % 4) == 0 && !rf64_dmma()) {
     // the int8-sliced contractions scale each row / column of X by a power of
     // two: one row-wise and one column-wise read of X for the exponents, then
     // the side stream (forked at the top) waits for them too
@@ -520,7 +523,7 @@ bool exact_views(cnmf_context* c, const XView& X, const float* lm, const float* 
                  float* xht, float* xc) {
   const int64_t d = X.d, n = X.n;
   const char* vmode = std::getenv("CNMF_VIEWS");
-  if (X.sp || n <= 0 || (vmode && std::string(vmode) == "tc") || !xs_i8_supported(lp) ||
+  if (X.sp || n <= 0 || !X.nonneg || (vmode && std::string(vmode) == "tc") || !xs_i8_supported(lp) ||
       (X.ldx % 4) != 0)
     return false;
   double* s64 = c->ws<double>("v64_s", (size_t)std::max(d, n) * lp);
@@ -1061,6 +1064,7 @@ void run_device_impl(cnmf_context* c, const XView& X0, const cnmf_solver_config&
     X.tf32_exact = !X.sp && hflag[2] == 0;
     X.integral = !X.sp && (hflag[3] & 1) == 0;
     X.small_int = !X.sp && hflag[3] == 0;
+    X.nonneg = true;  // checked just above
   }
 
   const bool dense_hals = algo == CNMF_FASTHALS || algo == CNMF_HALS;
@@ -1768,6 +1772,17 @@ cnmf_status cnmf_xs_exact(cnmf_context* c, const float* x, uint64_t d, uint64_t 
     launch_f32_to_f64(s, in_rows * lp, s64, c->nsm, c->stream);
     bool done = false;
     if (use_dmma != 1) {
+      {  // the int8-sliced kernel reads X's digits as unsigned bytes
+        int* flag = c->ws<int>("cflag", 4);
+        double* nrm = c->ws<double>("xnorm", 1);
+        void* mws = c->ws<char>("metrics_ws", metrics_ws_bytes(X.d, X.n, c->nsm));
+        CK(cudaMemsetAsync(flag, 0, 4 * sizeof(int), c->stream));
+        launch_check_data(X.x, X.ldx, X.d, X.n, flag, nrm, mws, c->nsm, c->stream);
+        int bad = 0;
+        CK(cudaMemcpyAsync(&bad, flag, sizeof(int), cudaMemcpyDeviceToHost, c->stream));
+        c->sync();
+        if (bad) throw Fail(CNMF_ERR_INPUT, "cnmf_xs_exact: the int8-sliced kernel needs an entrywise non-negative, finite X");
+      }
       int* sx = c->ws<int>("xe_sx", xs_i8_sx_ints(X.d, X.n));
       void* ws = c->ws<char>("xe_ws", xs_i8_ws_bytes(X.d, X.n, lp, c->nsm));
       const bool small_int = use_dmma == 2;  // caller vouches: integers below 8192
@@ -1846,6 +1861,7 @@ cnmf_status cnmf_time_xs_exact(cnmf_context* c, const float* x, uint64_t d, uint
     int hflag[4] = {0, 0, 1, 3};
     CK(cudaMemcpyAsync(hflag, flag, sizeof hflag, cudaMemcpyDeviceToHost, c->stream));
     c->sync();
+    if (hflag[0]) throw Fail(CNMF_ERR_INPUT, "the int8-sliced kernel needs an entrywise non-negative, finite X");
     const bool small_int = hflag[3] == 0;
     int* sx = c->ws<int>("txe_sx", xs_i8_sx_ints(X.d, X.n));
     if (small_int) CK(cudaMemsetAsync(sx, 0, sizeof(int) * (X.d + X.n), c->stream));

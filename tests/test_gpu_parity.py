@@ -227,6 +227,21 @@ def test_xstream_int8_small_integer_x(ctx, d, n, l, pair, monkeypatch):
         assert rel_fro(host(gen), ref) < 1e-4
 
 
+def test_xstream_int8_rejects_negative_x(ctx):
+    """The int8-sliced kernel reads X's digits as unsigned bytes (the solver's X
+    is non-negative by contract): the step entry validates, and the FP64
+    tensor-core kernel takes any X."""
+    import paper_1712_02248_b200 as cb
+    rng = np.random.default_rng(5)
+    x = rng.standard_normal((300, 260)).astype(np.float32)
+    s = rng.standard_normal((260, 32)).astype(np.float32)
+    out = torch.empty((300, 32), dtype=torch.float64, device="cuda")
+    with pytest.raises(cb.InputError):
+        ctx.xs_exact(dev(x), dev(s), out)
+    ctx.xs_exact(dev(x), dev(s), out, dmma=True)
+    assert rel_fro(host(out), x.astype(np.float64) @ s.astype(np.float64)) < 1e-14
+
+
 def test_xstream_nearly_exact_operands_stay_three_product(ctx):
     """One element off the tf32 grid sends the whole X down the 3xTF32 path:
     the result keeps that element's low bits."""
