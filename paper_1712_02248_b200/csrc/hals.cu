@@ -769,7 +769,11 @@ __device__ __noinline__ int serve_zero_a(const HalsState& S, int G, int cta, uns
 // RPT: A rows per thread; NB: columns per sweep block (16 halves the sweeps'
 // re-reads of A and B -- one pass over all k columns per block -- where the
 // registers allow it; the 6-row instance keeps 8).
-template <int RPT, int NB>
+// kInl: an emptied A column is served inside the kernel (serve_zero_a).  The
+// call's register constraints slow the steady-state sweep by ~5%, so the host
+// uses this instance only for a run's first iterations, where the events
+// cluster (engine.cpp run_hals), and the plain one for the rest.
+template <int RPT, int NB, bool kInl>
 __global__ void __launch_bounds__(kThreads, 1) hals_kernel(const HalsArgs p) {
   extern __shared__ __align__(16) double smem[];
   __shared__ double red8[kThreads / 32];
@@ -952,18 +956,11 @@ __global__ void __launch_bounds__(kThreads, 1) hals_kernel(const HalsArgs p) {
           HALS_PROF(3);
           if (total == 0.0) {  // column emptied: a_j is redrawn (solvers.cpp:435)
             // served in-kernel from the run stream when possible (serve_zero_a)
-            // Opt-in (-DHALS_INKERNEL_REDRAW): correct (the redraw tests pass with
-            // it, 13 instead of 37 launches at C4), but the call's register
-            // constraints slow the steady-state sweep by 4.7% (C4: 108.0 vs
-            // 103.2 ms for iterations 2-100), which cancels the ~130 us per
-            // event the host round trip costs -- so every event halts.
-#ifdef HALS_INKERNEL_REDRAW
-            const int sv = (S.words != nullptr && !S.dense)
-                               ? serve_zero_a(S, G, cta, ep, nr, j, a_lo, na, &s_rng_pos, red8, s_red)
-                               : 0;
-#else
-            const int sv = 0;
-#endif
+            int sv = 0;
+            if constexpr (kInl) {
+              if (S.words != nullptr && !S.dense)
+                sv = serve_zero_a(S, G, cta, ep, nr, j, a_lo, na, &s_rng_pos, red8, s_red);
+            }
             if (sv != 0) {  // it ran one norm all-reduce
               ++ep;
               ++nr;
@@ -1430,7 +1427,10 @@ cudaError_t launch_hals(const HalsState& st, int normalize_a, double alpha, doub
   // the tensor-core product is taken from k > 64.
   a.a_dmma = adm + 4096 <= 227 * 1024 && st.k > 64 && std::getenv("CNMF_HALS_ASIMT") == nullptr;
   if (a.a_dmma) smem = std::max(smem, adm);
-  const void* fn = large ? (const void*)hals_kernel<kMaxRPTLarge, 8> : (const void*)hals_kernel<3, 16>;
+  const bool inl = st.words != nullptr && !st.dense;  // in-kernel service of emptied A columns
+  const void* fn = large ? (inl ? (const void*)hals_kernel<kMaxRPTLarge, 8, true>
+                                : (const void*)hals_kernel<kMaxRPTLarge, 8, false>)
+                         : (inl ? (const void*)hals_kernel<3, 16, true> : (const void*)hals_kernel<3, 16, false>);
   cudaError_t e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   if (e != cudaSuccess) return e;
   void* args[] = {&a};
