@@ -55,13 +55,14 @@ __global__ void __launch_bounds__(256) check_data_kernel(const float* __restrict
       for (int q = 0; q < 4; ++q) {
         if (!(v[q] >= 0.f) || !isfinite(v[q])) bad = 1;
         low |= __float_as_uint(v[q]);
-        frac |= ((v[q] != truncf(v[q])) || !(v[q] < 67108864.f)) ? 1 : 0;
-        frac |= !(v[q] < 8192.f) ? 2 : 0;
+        frac |= (v[q] != truncf(v[q])) ? 1 : 0;  // (the magnitude bounds: from mx, per row)
         s += (double)v[q] * (double)v[q];
         mx = fmaxf(mx, v[q]);
         if (v[q] > 0.f) mn = fminf(mn, v[q]);
       }
     }
+    frac |= !(mx < 67108864.f) ? 1 : 0;  // this lane's elements of the row
+    frac |= !(mx < 8192.f) ? 2 : 0;
     if (rexp) {
 #pragma unroll
       for (int o = 16; o > 0; o >>= 1) {
