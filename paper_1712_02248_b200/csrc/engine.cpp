@@ -426,9 +426,11 @@ static bool rf64_dmma() {
 
 // range_finder_impl (compression.cpp:23-42) in fp64 arithmetic; `omega` is
 // the fp32 sketch (op_cols x lp), `basis` the fp32 result (rows x lp).
+// first_done: the first step (sketch + its QR, left in this tag's workspace by
+// an earlier call with only_first) is skipped; only_first: stop after it.
 int range_finder64(cnmf_context* c, const XView& X, int q, int lp, uint64_t w, bool transpose,
                    const float* omega, float* basis, const std::string& tag, cudaStream_t st,
-                   bool canonical, bool /*first_done*/ = false) {
+                   bool canonical, bool first_done = false, bool only_first = false) {
   const int64_t rows = transpose ? X.n : X.d, cols = transpose ? X.d : X.n;
   double* om = c->ws<double>("rf64_om_" + tag, cols * lp);
   double* y = c->ws<double>("rf64_y_" + tag, rows * lp);
@@ -446,9 +448,16 @@ int range_finder64(cnmf_context* c, const XView& X, int q, int lp, uint64_t w, b
     if (tn) launch_xs64_tn(X.x, X.ldx, X.d, X.n, s, lp, out, xs, c->nsm, st);
     else launch_xs64_nn(X.x, X.ldx, X.d, X.n, s, lp, out, xs, c->nsm, st);
   };
-  launch_f32_to_f64(omega, cols * lp, om, c->nsm, st);
-  apply(om, y, transpose);
-  launch_thin_qr64(y, rows, q, lp, b, qws, c->nsm, st, w == 0 ? 2 : 1);
+  if (!first_done) {
+    launch_f32_to_f64(omega, cols * lp, om, c->nsm, st);
+    apply(om, y, transpose);
+    launch_thin_qr64(y, rows, q, lp, b, qws, c->nsm, st, w == 0 ? 2 : 1);
+  }
+  if (only_first) {  // the caller decides the arithmetic of the rest from this QR's R
+    launch_f64_to_f32(b, rows * lp, basis, c->nsm, st);
+    CK(cudaGetLastError());
+    return 1;
+  }
   for (uint64_t it = 0; it < w; ++it) {
     apply(b, z, !transpose);
     launch_thin_qr64(z, cols, q, lp, zq, qws, c->nsm, st, 1);
@@ -475,38 +484,58 @@ int build_projectors_dev(cnmf_context* c, const XView& X, int q, int lp, uint64_
   const RfMode mode = rf_mode();
   bool use64 = !X.sp && mode != RfMode::kTc, first_done = false;
   c->last_kappa = 0.0;
-  int passes = 0;
-  if (use64 && mode == RfMode::kAuto) {
-    // the tensor-core range finder's first step for L (kept if it is chosen)
-    const int64_t d = X.d;
-    float* y = c->ws<float>("rf_y_L", d * lp);
-    float* xs = c->ws<float>("xs_ws_L", xstream_ws_floats(X.d, X.n, lp, c->nsm));
-    void* qws = c->ws<char>("qr_ws_L", qr_ws_bytes(std::max(X.d, X.n), lp, c->nsm));
-    x_times(c, X, false, omega_l, lp, y, xs, c->stream);
-    launch_thin_qr(y, d, q, lp, lm, qws, c->nsm, c->stream, w == 0 ? 2 : 1);
-    const double kappa = qr_kappa_estimate(qws, d, q, lp, c->nsm, c->stream);
-    use64 = kappa > kRfKappaMax;
-    first_done = !use64;
-    passes = use64 ? 1 : 0;  // the estimate's pass is wasted when fp64 is chosen
-    c->last_kappa = kappa;
-    if (std::getenv("CNMF_RF_DEBUG"))
-      std::fprintf(stderr, "range finder: kappa(X Omega) ~ %.3g -> %s\n", kappa, use64 ? "fp64" : "tc");
-  }
-  c->last_rf64 = use64 ? 1 : 0;
   c->rf_sx = nullptr;
-  if (use64 && X.nonneg && xs_i8_supported(lp) && (X.ldx % 4) == 0 && !rf64_dmma()) {
-    // the int8-sliced contractions scale each row / column of X by a power of
-    // two: one row-wise and one column-wise read of X for the exponents, then
-    // the side stream (forked at the top) waits for them too
+  int passes = 0;
+  // The int8-sliced contractions scale each row / column of X by a power of
+  // two: one row-wise and one column-wise read of X for the exponents (the
+  // views need them too), then the side stream (forked at the top) waits.
+  const bool i8_ok = X.nonneg && xs_i8_supported(lp) && (X.ldx % 4) == 0 && !rf64_dmma();
+  auto prepare_sx = [&] {
+    if (c->rf_sx) return;
     int* sx = c->ws<int>("rf_sx", xs_i8_sx_ints(X.d, X.n));
     launch_xs_i8_prepare_x(X.x, X.ldx, X.d, X.n, sx, c->nsm, c->stream);
     CK(cudaEventRecord(c->fork, c->stream));
     CK(cudaStreamWaitEvent(c->side, c->fork, 0));
     c->rf_sx = sx;
+  };
+  if (use64 && mode == RfMode::kAuto) {
+    const int64_t d = X.d;
+    double kappa;
+    if (i8_ok && !X.small_int) {
+      // The first sketch with exact accumulation: it serves either arithmetic,
+      // so no pass is wasted when the estimate picks the exact range finder
+      // (general X computes the exponents for its views anyway).
+      prepare_sx();
+      range_finder64(c, X, q, lp, w, false, omega_l, lm, "L", c->stream, false, false, true);
+      void* qws = c->ws<char>("qr64_ws_L", qr64_ws_bytes(std::max(X.d, X.n), lp, c->nsm));
+      kappa = qr_kappa_estimate(qws, d, q, lp, c->nsm, c->stream);
+      use64 = kappa > kRfKappaMax;
+      first_done = true;  // lm (fp32) and the fp64 workspace both hold the first basis
+    } else {
+      // the tensor-core range finder's first step for L (kept if it is chosen)
+      float* y = c->ws<float>("rf_y_L", d * lp);
+      float* xs = c->ws<float>("xs_ws_L", xstream_ws_floats(X.d, X.n, lp, c->nsm));
+      void* qws = c->ws<char>("qr_ws_L", qr_ws_bytes(std::max(X.d, X.n), lp, c->nsm));
+      x_times(c, X, false, omega_l, lp, y, xs, c->stream);
+      launch_thin_qr(y, d, q, lp, lm, qws, c->nsm, c->stream, w == 0 ? 2 : 1);
+      kappa = qr_kappa_estimate(qws, d, q, lp, c->nsm, c->stream);
+      use64 = kappa > kRfKappaMax;
+      first_done = !use64;
+      passes = use64 ? 1 : 0;  // the estimate's pass is wasted when fp64 is chosen
+    }
+    c->last_kappa = kappa;
+    if (std::getenv("CNMF_RF_DEBUG"))
+      std::fprintf(stderr, "range finder: kappa(X Omega) ~ %.3g -> %s\n", kappa, use64 ? "fp64" : "tc");
   }
-  auto rf = use64 ? range_finder64 : range_finder;
-  passes += rf(c, X, q, lp, w, false, omega_l, lm, "L", c->stream, canonical, first_done);
-  passes += rf(c, X, q, lp, w, true, omega_r, rt, "R", c->side, canonical, false);
+  c->last_rf64 = use64 ? 1 : 0;
+  if (use64 && i8_ok) prepare_sx();
+  auto rf = [&](bool transpose, const float* omega, float* basis, const char* tag, cudaStream_t st,
+                bool done) {
+    return use64 ? range_finder64(c, X, q, lp, w, transpose, omega, basis, tag, st, canonical, done)
+                 : range_finder(c, X, q, lp, w, transpose, omega, basis, tag, st, canonical, done);
+  };
+  passes += rf(false, omega_l, lm, "L", c->stream, first_done);
+  passes += rf(true, omega_r, rt, "R", c->side, false);
   CK(cudaEventRecord(c->join, c->side));
   CK(cudaStreamWaitEvent(c->stream, c->join, 0));
   return passes;
