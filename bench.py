@@ -397,6 +397,13 @@ def run_ours(args, name, c, rank, world, local_rank):
     alg_bytes = 4.0 * d * nloc + 4.0 * (d + nloc) * q
     # the exact-accumulation contraction (int8 digit slices): the compressed
     # views always, the range finder of an ill-conditioned sketch
+    exact_traffic = None
+    prof = os.path.join(ROOT, "profiles", f"traffic_exact_{name}.json")
+    if os.path.exists(prof):
+        try:
+            exact_traffic = json.load(open(prof)).get("bytes_per_launch")
+        except Exception:
+            exact_traffic = None
     try:
         te_nn, pe_nn = ctx.time_xs_exact(xv, q, 0, iters=5)
         te_tn, pe_tn = ctx.time_xs_exact(xv, q, 1, iters=5)
@@ -405,7 +412,7 @@ def run_ours(args, name, c, rank, world, local_rank):
                  "frac": alg_bytes / te_nn / 1e9 / hbm, "launch_seconds": te_nn, "x_reads_per_contraction": pe_nn,
                  "per_x_read_frac": pe_nn * alg_bytes / te_nn / 1e9 / hbm,
                  "tn_achieved": alg_bytes / te_tn / 1e9, "tn_frac": alg_bytes / te_tn / 1e9 / hbm,
-                 "tn_launch_seconds": te_tn, "algorithmic_bytes": alg_bytes, "traffic": None,
+                 "tn_launch_seconds": te_tn, "algorithmic_bytes": alg_bytes, "traffic": exact_traffic,
                  "note": "a contraction wider than one column chunk (80 columns; 64 for integer X) reads X once per chunk"}
     except Exception as e:  # shape outside the kernel's envelope
         exact = {"unavailable": str(e)}
